@@ -1,0 +1,215 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * rq_b200.h — C-ABI of the B200-native shift-invert quadratic eigensolver
+ * (factor / solve / eigensolve path of arXiv 2112.14064, "Performance of rIGA
+ * in solving quadratic eigenvalue problems").
+ *
+ * This is the drop-in boundary. The reference declares no factor/solve/eig
+ * entry points in proj/include; they exist only as SPEC
+ * operations. Each function below names the SPEC operation (or the reference
+ * declaration) it replaces. The C++ wrappers in include/rigaqep/sparsela.hpp and
+ * include/rigaqep/eig.hpp give those operations their SPEC signatures over the
+ * reference's rq:: types and call this ABI.
+ *
+ * Conventions:
+ *   - every function returns an int equal to an rq::errc value
+ *     (reference proj/include/rigaqep/types.hpp:14-23); 0 = ok;
+ *   - rq_last_error() returns the thread-local message of the last failure;
+ *   - all array arguments are HOST pointers owned by the caller, copied in/out;
+ *   - handles own their device memory and one CUDA stream; *_destroy frees it;
+ *   - no exceptions cross the ABI; there is no CPU fallback: without a usable
+ *     sm_100a device the numeric entry points fail with RQ_E_CONFIG.
+ *   - FP64 real arithmetic: the GPU path accepts real pencils and real shifts
+ *     only; complex input is rejected with RQ_E_CONFIG.
+ */
+#ifndef RQ_B200_H
+#define RQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* rq::errc (types.hpp:14-23) */
+enum {
+  RQ_OK = 0,
+  RQ_E_GENERIC = 1,
+  RQ_E_CONFIG = 2,
+  RQ_E_ASSEMBLY = 3,
+  RQ_E_SOLVER = 4,
+  RQ_E_VERIFICATION = 5,
+  RQ_E_DOMAIN = 6,
+  RQ_E_DIMENSION = 7,
+  RQ_E_SINGULAR = 8
+};
+
+const char* rq_last_error(void);
+const char* rq_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* Input construction (host): spaces + BASELINE assembly.                   */
+/* Replaces build_iga_space / build_riga_space / boundary_mask              */
+/* (spaces.hpp:68-80) + SPEC assembly with the BASELINE   */
+/* forms K = int(div.div | curl.curl) + phi.phi, M = int phi.phi,           */
+/* C = alpha M + beta K, (p+1)^2 Gauss points, constrained DOFs eliminated. */
+/* ------------------------------------------------------------------------ */
+typedef struct rq_pencil rq_pencil_t;
+
+enum { RQ_SPACE_CURL = 0, RQ_SPACE_DIV = 1 }; /* rq::SpaceKind (spaces.hpp:30) */
+
+typedef struct {
+  int kind;     /* RQ_SPACE_CURL or RQ_SPACE_DIV */
+  int degree;   /* p >= 2 */
+  int elems;    /* ne per direction (unit square) */
+  int levels;   /* rIGA bisection levels L (0 = maximum-continuity IGA) */
+  double alpha; /* Rayleigh damping C = alpha*M + beta*K */
+  double beta;
+} rq_space_desc;
+
+int rq_pencil_assemble(const rq_space_desc* desc, rq_pencil_t** out);
+/* n_full = all DOFs, n_free = after BC elimination, nnz = shared-pattern nnz */
+int rq_pencil_dims(const rq_pencil_t* p, int64_t* n_full, int64_t* n_free, int64_t* nnz);
+/* Shared CSR pattern (rowptr int64[n+1], col int32[nnz], sorted per row) and
+ * the three value arrays; any output pointer may be NULL. */
+int rq_pencil_csr(const rq_pencil_t* p, int64_t* rowptr, int32_t* col, double* K, double* C,
+                  double* M);
+/* Per free DOF: inclusive element support box {x0, x1, y0, y1} (int32[4*n])
+ * and the full-space DOF id (int64[n]); either may be NULL. */
+int rq_pencil_supports(const rq_pencil_t* p, int32_t* box, int64_t* free_to_full);
+void rq_pencil_destroy(rq_pencil_t* p);
+
+/* Univariate / vector space bookkeeping exposed for parity with the
+ * reference spaces code (spaces.cpp:33-113). */
+int rq_space_dims(const rq_space_desc* desc, int64_t* nx_x, int64_t* ny_x, int64_t* nx_y,
+                  int64_t* ny_y);
+/* Sorted constrained full-space DOF ids (boundary_mask, spaces.cpp:79-113).
+ * *count receives the number; mask may be NULL to query it. */
+int rq_space_boundary_mask(const rq_space_desc* desc, int64_t* mask, int64_t* count);
+
+/* ------------------------------------------------------------------------ */
+/* Symbolic analysis (host C++): nested_dissection_order  */
+/* + multifrontal front structure.                                          */
+/* ------------------------------------------------------------------------ */
+typedef struct rq_symbolic rq_symbolic_t;
+
+typedef struct {
+  int64_t n;
+  int64_t nfronts;
+  int64_t nlevels;       /* height-ordered batches (leaves = level 0) */
+  int64_t max_front;     /* max nf */
+  int64_t max_npiv;
+  int64_t nnz_l;         /* stored lower-factor entries incl. diagonal */
+  int64_t nnz_u;         /* stored upper-factor entries incl. diagonal */
+  int64_t pool_doubles;  /* dense front pool size */
+  double flops_lu;       /* F_LU = sum_f sum_k (nf-k-1) + 2 (nf-k-1)^2 (real) */
+  double flops_schur;    /* sum_f 2 npiv (nf-npiv)^2 */
+  double flops_schur_large; /* the same over fronts with nf >= 1024 */
+  double trisolve_bytes; /* algorithmic bytes of one forward+backward solve */
+} rq_symbolic_stats;
+
+/* Geometric nested dissection over the DOF support boxes.
+ * box: int32[4*n] as returned by rq_pencil_supports; elems: ne; leaf: max
+ * DOFs in a leaf (default 64). */
+int rq_nd_order(int64_t n, const int32_t* box, int elems, int leaf, rq_symbolic_t** out);
+int rq_symbolic_stats_get(const rq_symbolic_t* s, rq_symbolic_stats* out);
+/* perm[new] = old (free-DOF ids) */
+int rq_symbolic_perm(const rq_symbolic_t* s, int32_t* perm);
+/* Per front (postorder): parent (-1 root), npiv, nf, first pivot (new index),
+ * level (height batch). Any array may be NULL. */
+int rq_symbolic_fronts(const rq_symbolic_t* s, int32_t* parent, int32_t* npiv, int32_t* nf,
+                       int32_t* start, int32_t* level);
+/* Row list of front f (new indices, ascending; pivots first). */
+int rq_symbolic_front_rows(const rq_symbolic_t* s, int64_t f, int32_t* rows);
+void rq_symbolic_destroy(rq_symbolic_t* s);
+
+/* ------------------------------------------------------------------------ */
+/* Numeric multifrontal LU on the GPU: lu_factorize and   */
+/* solve_factored.                                        */
+/* ------------------------------------------------------------------------ */
+typedef struct rq_factor rq_factor_t;
+
+typedef struct {
+  int64_t swaps;         /* off-diagonal pivots taken (threshold 0.1) */
+  double factor_ms;      /* device time of the numeric factorization */
+  double gflops;         /* flops_lu / factor time */
+  int64_t launches;      /* kernels launched by one factorization */
+} rq_factor_info;
+
+/* A = Q(sigma) values on the shared pattern (free-DOF ordering). */
+int rq_factor_create(const rq_symbolic_t* s, int64_t n, const int64_t* rowptr,
+                     const int32_t* col, const double* aval, rq_factor_t** out);
+/* Re-run the numeric factorization with new values on the same pattern. */
+int rq_factor_refactor(rq_factor_t* f, const double* aval);
+int rq_factor_get_info(const rq_factor_t* f, rq_factor_info* out);
+/* x = A^{-1} b for nrhs right-hand sides (column-major n x nrhs, host). */
+int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs);
+/* Copy front f back: dense ld*nf column-major block holding L\U and the
+ * Schur complement, ld = *ld_out; ipiv[npiv] local swap sequence. */
+int rq_factor_front_export(const rq_factor_t* f, int64_t front, double* dense, int32_t* ipiv,
+                           int64_t* ld_out);
+void rq_factor_destroy(rq_factor_t* f);
+
+/* ------------------------------------------------------------------------ */
+/* Shift-invert operator of the linearised pencil: build_operator,          */
+/* apply_operator, b_inner, arnoldi_run, solve_quadratic. */
+/* Vectors of length 2n are (upper; lower) blocks, free-DOF ordering.       */
+/* ------------------------------------------------------------------------ */
+typedef struct rq_operator rq_operator_t;
+
+typedef struct {
+  double sigma;       /* real shift */
+  int scaling;        /* 1: scale_pencil with varsigma = sqrt(maxabs K / maxabs M) */
+} rq_operator_opts;
+
+int rq_operator_create(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
+                       const double* C, const double* M, const rq_symbolic_t* s,
+                       const rq_operator_opts* opts, rq_operator_t** out);
+double rq_operator_varsigma(const rq_operator_t* op);
+/* r = L(s)^{-1} B v : r_u = -Q(s)^{-1}(s M v_u + C v_u + M v_l), r_l = s r_u + v_u
+ * (of the possibly scaled pencil). */
+int rq_operator_apply(rq_operator_t* op, const double* v, double* r);
+/* x_u^T y_u + x_l^T M y_l */
+int rq_operator_b_inner(rq_operator_t* op, const double* x, const double* y, double* out);
+/* y = A x for A in {0: K, 1: C, 2: M, 3: Q(s)} (scaled pencil) */
+int rq_operator_spmv(rq_operator_t* op, int which, const double* x, double* y);
+/* m-step B-orthogonal Arnoldi with CGS2 from v1 (B-normalised inside).
+ * V: (m+1) x 2n row-major, H: (m+1) x m column-major. */
+int rq_operator_arnoldi(rq_operator_t* op, const double* v1, int m, double* V, double* H);
+rq_factor_t* rq_operator_factor(rq_operator_t* op); /* borrowed */
+void rq_operator_destroy(rq_operator_t* op);
+
+typedef struct {
+  int nev;
+  int m;              /* Krylov dimension; <= 0 selects 2*nev+1 (BASELINE) */
+  double tol;         /* explicit pencil-residual tolerance */
+  uint64_t seed;      /* splitmix64 start vector, uniform[-1,1] */
+  int max_restarts;   /* default 100 */
+  int guard;          /* completeness guard (deflated fresh restarts), 1 = on */
+} rq_eigs_opts;
+
+typedef struct {
+  int nconv;
+  int restarts;       /* Krylov-Schur cycles (all passes) */
+  int guard_passes;
+  int64_t n_fa, n_fb, n_mv, n_vv, n_check, n_restart; /* ledger op counts */
+  double macs_fa, macs_fb, macs_mv, macs_vv, macs_check, macs_restart;
+  double t_total_ms, t_factor_ms, t_solve_ms, t_spmv_ms, t_orth_ms, t_host_ms;
+  int64_t launches;
+} rq_eigs_info;
+
+/* solve_quadratic: nev eigenpairs of K + lam C + lam^2 M nearest sigma.
+ * lam_re/lam_im/resid: double[nev]; vec_re/vec_im: n x nev column-major
+ * (may be NULL). Returns RQ_E_SOLVER with the converged prefix filled when
+ * max_restarts is exhausted. */
+int rq_eigs_run(rq_operator_t* op, const rq_eigs_opts* opts, double* lam_re, double* lam_im,
+                double* resid, double* vec_re, double* vec_im, rq_eigs_info* info);
+/* CostLedger::to_json-compatible snapshot (sparse.cpp:80-97) of the last run. */
+int rq_eigs_ledger_json(const rq_operator_t* op, char* buf, size_t len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RQ_B200_H */

@@ -1,0 +1,213 @@
+"""ORACLE — test infrastructure only (see oracle/rq_oracle.cpp header).
+
+ctypes access to the CPU restatement (liboracle.so) and to the reference's own
+sources built by oracle/Makefile (_ref/liboracle_ref.so). Only tests/,
+__graft_entry__.smoke() and bench.py's CPU-baseline legs may import this.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_PATH = os.path.join(HERE, "liboracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "liboracle_ref.so")
+
+vp = C.c_void_p
+i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"oracle error {code}: {msg}")
+        self.code = code
+
+
+def _bind(lib):
+    def s(name, res, *args):
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = list(args)
+    s("oracle_last_error", C.c_char_p)
+    s("oracle_kind", C.c_int)
+    s("oracle_symbolic", C.c_int, C.c_int64, i64p, i32p, i32p, C.c_int, C.c_int, i32p,
+      C.POINTER(C.c_int32), i32p, i32p, i32p, C.POINTER(C.c_int64))
+    s("oracle_factor_create", C.c_int, C.c_int64, i64p, i32p, f64p, i32p, C.c_int, C.c_int,
+      C.POINTER(vp), C.POINTER(C.c_int64), C.POINTER(C.c_double))
+    s("oracle_factor_solve", C.c_int, vp, f64p, f64p)
+    s("oracle_factor_front", C.c_int, vp, C.c_int, vp, vp, vp)
+    s("oracle_factor_destroy", None, vp)
+    s("oracle_eig_create", C.c_int, C.c_int64, i64p, i32p, f64p, f64p, f64p, i32p, C.c_int,
+      C.c_int, C.c_double, C.POINTER(vp))
+    s("oracle_eig_factor_ms", C.c_double, vp)
+    s("oracle_eig_apply", C.c_int, vp, f64p, f64p)
+    s("oracle_eig_solve_quadratic", C.c_int, vp, C.c_int, C.c_int, C.c_double, C.c_uint64,
+      C.c_int, C.c_int, f64p, f64p, vp, i32p, f64p)
+    s("oracle_eig_destroy", None, vp)
+    s("oracle_kern_spmv", None, C.c_int64, i64p, i32p, f64p, f64p, f64p)
+    s("oracle_kern_dotc", None, f64p, f64p, C.c_int64, f64p)
+    s("oracle_kern_elim", C.c_uint64, f64p, C.c_int64, f64p, f64p, C.c_int64, C.c_int64)
+    return lib
+
+
+_port = None
+_ref = None
+
+
+def port():
+    global _port
+    if _port is None:
+        if not os.path.exists(PORT_PATH):
+            raise ImportError(f"{PORT_PATH} missing: run make -C oracle")
+        _port = _bind(C.CDLL(PORT_PATH))
+    return _port
+
+
+def ref():
+    """The reference-sources build, or None when it was never built here."""
+    global _ref
+    if _ref is None and os.path.exists(REF_PATH):
+        lib = _bind(C.CDLL(REF_PATH))
+        lib.ref_space.restype = C.c_int
+        lib.ref_space.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64), vp, vp,
+                                  C.POINTER(C.c_int64)]
+        lib.ref_kern_backend.restype = C.c_char_p
+        lib.ref_kern_spmv.argtypes = [C.c_int64, i64p, i32p, f64p, f64p, f64p]
+        lib.ref_kern_spmv.restype = None
+        lib.ref_kern_dotc.argtypes = [f64p, f64p, C.c_int64, f64p]
+        lib.ref_kern_dotc.restype = None
+        lib.ref_kern_elim.argtypes = [f64p, C.c_int64, f64p, f64p, C.c_int64, C.c_int64]
+        lib.ref_kern_elim.restype = C.c_uint64
+        lib.ref_select_backend.argtypes = [C.c_char_p]
+        lib.ref_select_backend.restype = C.c_int
+        _ref = lib
+    return _ref
+
+
+def lib_for(kind: str = "port"):
+    if kind == "reference":
+        r = ref()
+        if r is None:
+            raise ImportError("oracle/_ref/liboracle_ref.so not built")
+        return r
+    return port()
+
+
+def _chk(lib, rc):
+    if rc != 0:
+        raise OracleError(rc, lib.oracle_last_error().decode())
+
+
+def cplx(a) -> np.ndarray:
+    """Interleave a real or complex array as (re, im) doubles."""
+    a = np.asarray(a)
+    out = np.zeros(2 * a.size)
+    out[0::2] = a.real.ravel()
+    if np.iscomplexobj(a):
+        out[1::2] = a.imag.ravel()
+    return out
+
+
+def uncplx(a) -> np.ndarray:
+    return a[0::2] + 1j * a[1::2]
+
+
+def symbolic(pencil, leaf=64, kind="port"):
+    lib = lib_for(kind)
+    n = pencil.n
+    perm = np.zeros(n, np.int32)
+    nfr = C.c_int32()
+    npiv = np.zeros(n + 1, np.int32)
+    nf = np.zeros(n + 1, np.int32)
+    parent = np.zeros(n + 1, np.int32)
+    snnz = C.c_int64()
+    _chk(lib, lib.oracle_symbolic(n, pencil.rowptr, pencil.col, np.ascontiguousarray(pencil.box.ravel(), np.int32),
+                                  pencil.elems, leaf, perm, C.byref(nfr), npiv, nf, parent, C.byref(snnz)))
+    k = nfr.value
+    return {"perm": perm, "npiv": npiv[:k], "nf": nf[:k], "parent": parent[:k],
+            "struct_nnz_l": snnz.value}
+
+
+class Factor:
+    """Oracle multifrontal LU (complex, reference elim_step inner loop)."""
+
+    def __init__(self, n, rowptr, col, values, box, elems, leaf=64, kind="port"):
+        self.lib = lib_for(kind)
+        self.n = n
+        self.h = vp()
+        sw, macs = C.c_int64(), C.c_double()
+        _chk(self.lib, self.lib.oracle_factor_create(
+            n, np.ascontiguousarray(rowptr, np.int64), np.ascontiguousarray(col, np.int32),
+            cplx(values), np.ascontiguousarray(np.asarray(box).ravel(), np.int32), elems, leaf,
+            C.byref(self.h), C.byref(sw), C.byref(macs)))
+        self.swaps, self.fa_macs = sw.value, macs.value
+
+    def solve(self, b):
+        x = np.zeros(2 * self.n)
+        _chk(self.lib, self.lib.oracle_factor_solve(self.h, cplx(b), x))
+        return uncplx(x)
+
+    def front(self, f, nf, npiv):
+        dense = np.zeros(2 * nf * nf)
+        ipiv = np.zeros(max(npiv, 1), np.int32)
+        rows = np.zeros(nf, np.int32)
+        _chk(self.lib, self.lib.oracle_factor_front(self.h, f, dense.ctypes.data_as(vp),
+                                                    ipiv.ctypes.data_as(vp), rows.ctypes.data_as(vp)))
+        return uncplx(dense).reshape(nf, nf), ipiv[:npiv], rows
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.oracle_factor_destroy(self.h)
+            self.h = None
+
+
+class Eig:
+    """Oracle quadratic eigensolver (complex Krylov-Schur, CGS2, guard)."""
+
+    def __init__(self, pencil, sigma, leaf=64, kind="port", K=None, C_=None, M=None):
+        self.lib = lib_for(kind)
+        self.n = pencil.n
+        self.h = vp()
+        K = pencil.K if K is None else K
+        C_ = pencil.C if C_ is None else C_
+        M = pencil.M if M is None else M
+        _chk(self.lib, self.lib.oracle_eig_create(
+            pencil.n, pencil.rowptr, pencil.col, cplx(K), cplx(C_), cplx(M),
+            np.ascontiguousarray(pencil.box.ravel(), np.int32), pencil.elems, leaf, float(sigma),
+            C.byref(self.h)))
+        self.factor_ms = self.lib.oracle_eig_factor_ms(self.h)
+
+    def apply(self, v):
+        r = np.zeros(4 * self.n)
+        _chk(self.lib, self.lib.oracle_eig_apply(self.h, cplx(v), r))
+        return uncplx(r)
+
+    def solve_quadratic(self, nev, m=0, tol=1e-10, seed=0, max_restarts=100, guard=1,
+                        vectors=False):
+        lam = np.zeros(2 * nev)
+        res = np.zeros(nev)
+        vec = np.zeros(2 * nev * self.n) if vectors else None
+        st = np.zeros(4, np.int32)
+        led = np.zeros(12)
+        rc = self.lib.oracle_eig_solve_quadratic(self.h, nev, m, tol, seed, max_restarts, guard, lam,
+                                                 res, None if vec is None else vec.ctypes.data_as(vp),
+                                                 st, led)
+        self.stats = {"cycles": int(st[0]), "guard_passes": int(st[1]), "nconv": int(st[2]),
+                      "ok": bool(st[3])}
+        names = ["fa", "fb", "mv", "vv", "residual_check", "restart"]
+        self.ledger = {nm: {"ops": int(led[2 * i]), "macs": float(led[2 * i + 1])}
+                       for i, nm in enumerate(names)}
+        _chk(self.lib, rc)
+        out = uncplx(lam)
+        if vectors:
+            return out, res, uncplx(vec).reshape(nev, self.n)
+        return out, res
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.oracle_eig_destroy(self.h)
+            self.h = None

@@ -1,0 +1,883 @@
+// SPDX-License-Identifier: Apache-2.0
+// ============================================================================
+// ORACLE — TEST INFRASTRUCTURE ONLY. CPU restatement of the reference path
+// (arXiv 2112.14064 reference, /root/reference: proj/ sources + SPEC.md). Only
+// tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+// reference leg may load this library, and only as the checker or the timed
+// CPU baseline. The product (paper_2112_14064_b200/) never calls it.
+//
+// Arithmetic is the reference's: complex double (types.hpp:11) through the
+// six kern:: inner loops (kernels.hpp:17-39). Built two ways (oracle/Makefile):
+//   liboracle.so                 kern:: restated here (kernels.cpp semantics)
+//   _ref/liboracle_ref.so        -DORACLE_REF_KERN: kern:: calls go to the
+//                                reference's own kernels.cpp/kernels_avx2.cpp
+//                                compiled from /root/reference (patched
+//                                elim_step declaration)
+// The factor/solve/eigensolve layers do not exist in the reference; they are
+// restated from SPEC.md (sparsela :279-378, eig :380-511) and PAPER.md
+// (Alg. 2 :555-589). Parity pins: SPEC known answers, the paper's structural
+// numbers, scipy dense eigensolves (tests/), and the reference kernels.
+// ============================================================================
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#ifdef ORACLE_REF_KERN
+#include "rigaqep/kernels.hpp"
+#endif
+
+using cd = std::complex<double>;
+
+namespace oracle {
+
+// ---------------------------------------------------------------------------
+// kern:: (reference kernels.hpp:17-39)
+#ifdef ORACLE_REF_KERN
+inline void k_axpy(cd a, const cd* x, cd* y, size_t n) { rq::kern::axpy(a, x, y, n); }
+inline cd k_dotc(const cd* x, const cd* y, size_t n) { return rq::kern::dotc(x, y, n); }
+inline void k_scal(cd a, cd* x, size_t n) { rq::kern::scal(a, x, n); }
+inline void k_spmv(size_t n, const int64_t* rp, const int32_t* col, const cd* val, const cd* x, cd* y) {
+  rq::kern::spmv_csr(n, rp, col, val, x, y);
+}
+inline uint64_t k_elim(cd* tile, size_t ld, const cd* lcol, const cd* urow, size_t rows, size_t cols) {
+  return rq::kern::active().elim_step(tile, ld, lcol, urow, rows, cols);
+}
+#else
+// kernels.cpp:19-21
+inline void k_axpy(cd a, const cd* x, cd* y, size_t n) {
+  for (size_t i = 0; i < n; ++i) y[i] += a * x[i];
+}
+// kernels.cpp:23-32: conj(x) . y with split real accumulators
+inline cd k_dotc(const cd* x, const cd* y, size_t n) {
+  double rr = 0.0, ri = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    rr += x[i].real() * y[i].real() + x[i].imag() * y[i].imag();
+    ri += x[i].real() * y[i].imag() - x[i].imag() * y[i].real();
+  }
+  return {rr, ri};
+}
+// kernels.cpp:34-36
+inline void k_scal(cd a, cd* x, size_t n) {
+  for (size_t i = 0; i < n; ++i) x[i] *= a;
+}
+// kernels.cpp:44-56: row loop, sequential accumulation
+inline void k_spmv(size_t n, const int64_t* rp, const int32_t* col, const cd* val, const cd* x, cd* y) {
+  for (size_t r = 0; r < n; ++r) {
+    double ar = 0.0, ai = 0.0;
+    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+      const cd v = val[k], xc = x[col[k]];
+      ar += v.real() * xc.real() - v.imag() * xc.imag();
+      ai += v.real() * xc.imag() + v.imag() * xc.real();
+    }
+    y[r] = {ar, ai};
+  }
+}
+// kernels.cpp:58-69 (rank1_update_scalar): rows with zero multiplier skipped
+inline uint64_t k_elim(cd* tile, size_t ld, const cd* lcol, const cd* urow, size_t rows, size_t cols) {
+  uint64_t macs = 0;
+  for (size_t i = 0; i < rows; ++i) {
+    const cd l = lcol[i];
+    if (l == cd{}) continue;
+    cd* row = tile + i * ld;
+    for (size_t k = 0; k < cols; ++k) row[k] -= l * urow[k];
+    macs += cols;
+  }
+  return macs;
+}
+#endif
+
+// ---------------------------------------------------------------------------
+// CostLedger (sparse.hpp:57-103), 8 flops per complex MAC
+struct Ledger {
+  uint64_t ops[6] = {0, 0, 0, 0, 0, 0};   // fa fb mv vv check restart
+  double macs[6] = {0, 0, 0, 0, 0, 0};
+  void add(int c, double m) { ops[c] += 1, macs[c] += m; }
+};
+enum { FA = 0, FB = 1, MV = 2, VV = 3, CHK = 4, RST = 5 };
+
+struct Csr {
+  int64_t n = 0;
+  std::vector<int64_t> rp;
+  std::vector<int32_t> col;
+  std::vector<cd> val;
+};
+
+// rq::spmv / dot / axpy (sparse.cpp:59-72): ledger-charging wrappers
+void spmv(const Csr& A, const cd* x, cd* y, Ledger* L) {
+  k_spmv(A.n, A.rp.data(), A.col.data(), A.val.data(), x, y);
+  if (L) L->add(MV, static_cast<double>(A.rp[A.n]));
+}
+cd dot(const cd* x, const cd* y, size_t n, Ledger* L) {
+  if (L) L->add(VV, n);
+  return k_dotc(x, y, n);
+}
+void axpy(cd a, const cd* x, cd* y, size_t n, Ledger* L) {
+  if (L) L->add(VV, n);
+  k_axpy(a, x, y, n);
+}
+
+// ---------------------------------------------------------------------------
+// nested_dissection_order
+struct NDNode {
+  int bx0, bx1, by0, by1;
+  std::vector<int32_t> piv;
+  std::vector<int> kids;
+};
+
+struct ND {
+  const int32_t* box;
+  int leaf;
+  std::vector<NDNode> nodes;
+  int rec(int x0, int x1, int y0, int y1, std::vector<int32_t> d) {
+    const int w = x1 - x0, h = y1 - y0;
+    if (static_cast<int>(d.size()) <= leaf || (w < 2 && h < 2)) {
+      std::sort(d.begin(), d.end());
+      nodes.push_back({x0, x1, y0, y1, d, {}});
+      return static_cast<int>(nodes.size()) - 1;
+    }
+    const bool vx = w >= h;  // ties: vertical separator (cut x) first
+    const int mid = vx ? x0 + w / 2 : y0 + h / 2;
+    std::vector<int32_t> L, R, S;
+    for (int32_t i : d) {
+      const int a = box[4 * i + (vx ? 0 : 2)], b = box[4 * i + (vx ? 1 : 3)];
+      (b < mid ? L : (a >= mid ? R : S)).push_back(i);
+    }
+    std::vector<int> kids;
+    if (!L.empty()) kids.push_back(vx ? rec(x0, mid, y0, y1, L) : rec(x0, x1, y0, mid, L));
+    if (!R.empty()) kids.push_back(vx ? rec(mid, x1, y0, y1, R) : rec(x0, x1, mid, y1, R));
+    if (S.empty() && kids.size() == 1) return kids[0];
+    std::sort(S.begin(), S.end());
+    nodes.push_back({x0, x1, y0, y1, S, kids});
+    return static_cast<int>(nodes.size()) - 1;
+  }
+};
+
+// Front structure from the elimination tree (independent of the product's
+// geometric rule): struct(j) = adj(j) ∩ {>j} ∪ struct(children) \ {j};
+// one front per ND node with CB = ∪ struct(j) over its columns, minus pivots.
+struct Symbolic {
+  int64_t n = 0;
+  std::vector<int32_t> perm, iperm;
+  std::vector<int32_t> node_start, node_npiv, node_parent;
+  std::vector<std::vector<int32_t>> node_rows;  // pivots then CB rows (new ids, ascending)
+  std::vector<int32_t> etree;
+  int64_t struct_nnz_l = 0;  // exact structural nnz(L) incl. diagonal
+};
+
+Symbolic symbolic(int64_t n, const int64_t* rp, const int32_t* col, const int32_t* box, int elems,
+                  int leaf) {
+  ND nd{box, leaf, {}};
+  std::vector<int32_t> all(n);
+  std::iota(all.begin(), all.end(), 0);
+  nd.rec(0, elems, 0, elems, all);
+  Symbolic S;
+  S.n = n;
+  const int nn = static_cast<int>(nd.nodes.size());
+  S.node_parent.assign(nn, -1);
+  for (int f = 0; f < nn; ++f) {
+    S.node_start.push_back(static_cast<int32_t>(S.perm.size()));
+    S.node_npiv.push_back(static_cast<int32_t>(nd.nodes[f].piv.size()));
+    for (int32_t d : nd.nodes[f].piv) S.perm.push_back(d);
+    for (int k : nd.nodes[f].kids) S.node_parent[k] = f;
+  }
+  S.iperm.assign(n, 0);
+  for (int64_t i = 0; i < n; ++i) S.iperm[S.perm[i]] = static_cast<int32_t>(i);
+  // column structures of L in the new order (symmetric pattern)
+  std::vector<std::vector<int32_t>> st(n);
+  S.etree.assign(n, -1);
+  std::vector<std::vector<int32_t>> kids(n);
+  for (int64_t j = 0; j < n; ++j) {
+    std::vector<int32_t> s;
+    const int32_t old = S.perm[j];
+    for (int64_t k = rp[old]; k < rp[old + 1]; ++k) {
+      const int32_t i = S.iperm[col[k]];
+      if (i > j) s.push_back(i);
+    }
+    for (int32_t c : kids[j])
+      for (int32_t i : st[c])
+        if (i > j) s.push_back(i);
+    std::sort(s.begin(), s.end());
+    s.erase(std::unique(s.begin(), s.end()), s.end());
+    if (!s.empty()) {
+      S.etree[j] = s[0];
+      kids[s[0]].push_back(static_cast<int32_t>(j));
+    }
+    S.struct_nnz_l += 1 + static_cast<int64_t>(s.size());
+    st[j] = std::move(s);
+  }
+  S.node_rows.resize(nn);
+  for (int f = 0; f < nn; ++f) {
+    const int32_t s0 = S.node_start[f], e0 = s0 + S.node_npiv[f];
+    std::vector<int32_t> rows;
+    for (int32_t j = s0; j < e0; ++j)
+      for (int32_t i : st[j])
+        if (i >= e0) rows.push_back(i);
+    std::sort(rows.begin(), rows.end());
+    rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
+    std::vector<int32_t> all_rows;
+    for (int32_t j = s0; j < e0; ++j) all_rows.push_back(j);
+    all_rows.insert(all_rows.end(), rows.begin(), rows.end());
+    S.node_rows[f] = std::move(all_rows);
+  }
+  // Rows of an empty-separator node are its children's CB rows (pass-through).
+  for (int f = 0; f < nn; ++f) {
+    if (S.node_npiv[f] != 0) continue;
+    std::vector<int32_t> rows;
+    for (int k : nd.nodes[f].kids) {
+      const auto& kr = S.node_rows[k];
+      rows.insert(rows.end(), kr.begin() + S.node_npiv[k], kr.end());
+    }
+    std::sort(rows.begin(), rows.end());
+    rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
+    S.node_rows[f] = rows;
+  }
+  return S;
+}
+
+// ---------------------------------------------------------------------------
+// lu_factorize: multifrontal, row-major dense
+// fronts, threshold u = 0.1 partial pivoting among fully-summed rows, prefer
+// the diagonal, ties -> lowest index, singular if max candidate < 1e-300.
+struct FrontF {
+  int32_t npiv = 0, nf = 0;
+  std::vector<int32_t> rows;
+  std::vector<cd> F;        // nf x nf row-major: L\U and (consumed) CB
+  std::vector<int32_t> ipiv;
+};
+
+struct Factor {
+  const Symbolic* S = nullptr;
+  std::vector<FrontF> fr;
+  int64_t swaps = 0;
+  double fa_macs = 0;
+  double fb_macs = 0;  // per solve
+};
+
+struct OracleError {
+  int code;
+  std::string msg;
+};
+
+Factor lu_factorize(const Symbolic& S, const Csr& A, Ledger* L) {
+  Factor R;
+  R.S = &S;
+  const int nn = static_cast<int>(S.node_rows.size());
+  R.fr.resize(nn);
+  std::vector<std::vector<int>> kids(nn);
+  for (int f = 0; f < nn; ++f)
+    if (S.node_parent[f] >= 0) kids[S.node_parent[f]].push_back(f);
+  std::vector<int32_t> owner(S.n);
+  for (int f = 0; f < nn; ++f)
+    for (int k = 0; k < S.node_npiv[f]; ++k) owner[S.node_start[f] + k] = f;
+  // original entries per owning front
+  std::vector<std::vector<std::pair<int64_t, cd>>> orig(nn);  // (packed r*n+c new ids, value)
+  for (int64_t i = 0; i < A.n; ++i)
+    for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+      const int64_t r = S.iperm[i], c = S.iperm[A.col[k]];
+      orig[owner[std::min(r, c)]].push_back({r * S.n + c, A.val[k]});
+    }
+  uint64_t macs = 0;
+  for (int f = 0; f < nn; ++f) {
+    FrontF& Fr = R.fr[f];
+    Fr.rows = S.node_rows[f];
+    Fr.nf = static_cast<int32_t>(Fr.rows.size());
+    Fr.npiv = S.node_npiv[f];
+    const int nf = Fr.nf, np = Fr.npiv;
+    Fr.F.assign(static_cast<size_t>(nf) * nf, cd{});
+    auto loc = [&](int32_t g) {
+      const auto it = std::lower_bound(Fr.rows.begin(), Fr.rows.end(), g);
+      if (it == Fr.rows.end() || *it != g) throw OracleError{7, "entry outside front"};
+      return static_cast<int>(it - Fr.rows.begin());
+    };
+    for (auto& e : orig[f]) {
+      const int r = loc(static_cast<int32_t>(e.first / S.n)), c = loc(static_cast<int32_t>(e.first % S.n));
+      Fr.F[static_cast<size_t>(r) * nf + c] += e.second;
+    }
+    for (int c : kids[f]) {  // extend-add
+      FrontF& K = R.fr[c];
+      const int knp = K.npiv, knf = K.nf;
+      std::vector<int> map(knf - knp);
+      for (int t = knp; t < knf; ++t) map[t - knp] = loc(K.rows[t]);
+      for (int a = knp; a < knf; ++a)
+        for (int b = knp; b < knf; ++b)
+          Fr.F[static_cast<size_t>(map[a - knp]) * nf + map[b - knp]] += K.F[static_cast<size_t>(a) * knf + b];
+    }
+    Fr.ipiv.assign(np, 0);
+    std::vector<cd> lcol(nf);
+    for (int k = 0; k < np; ++k) {
+      double best = -1.0;
+      int bi = k;
+      for (int i = k; i < np; ++i) {
+        const double v = std::abs(Fr.F[static_cast<size_t>(i) * nf + k]);
+        if (v > best) best = v, bi = i;
+      }
+      if (!(best >= 1e-300)) throw OracleError{8, "singular pivot block"};
+      const double diag = std::abs(Fr.F[static_cast<size_t>(k) * nf + k]);
+      const int p = diag >= 0.1 * best ? k : bi;
+      Fr.ipiv[k] = p;
+      if (p != k) {
+        ++R.swaps;
+        for (int c = 0; c < nf; ++c)
+          std::swap(Fr.F[static_cast<size_t>(k) * nf + c], Fr.F[static_cast<size_t>(p) * nf + c]);
+      }
+      const cd piv = Fr.F[static_cast<size_t>(k) * nf + k];
+      for (int i = k + 1; i < nf; ++i) {
+        cd& a = Fr.F[static_cast<size_t>(i) * nf + k];
+        a /= piv;
+        lcol[i - k - 1] = a;
+      }
+      macs += k_elim(&Fr.F[static_cast<size_t>(k + 1) * nf + k + 1], nf, lcol.data(),
+                     &Fr.F[static_cast<size_t>(k) * nf + k + 1], nf - k - 1, nf - k - 1);
+    }
+    R.fb_macs += static_cast<double>(np) * np + 2.0 * np * (nf - np);
+  }
+  R.fa_macs = static_cast<double>(macs);
+  if (L) L->add(FA, R.fa_macs);
+  return R;
+}
+
+// solve_factored: permute, L solve, U solve (original order)
+void solve_factored(const Factor& R, const cd* b, cd* x, Ledger* L) {
+  const Symbolic& S = *R.S;
+  const int nn = static_cast<int>(R.fr.size());
+  std::vector<cd> y(S.n);
+  for (int64_t i = 0; i < S.n; ++i) y[i] = b[S.perm[i]];
+  // forward: y[rows] of each front updated in postorder
+  for (int f = 0; f < nn; ++f) {
+    const FrontF& Fr = R.fr[f];
+    const int nf = Fr.nf, np = Fr.npiv;
+    for (int k = 0; k < np; ++k) {
+      const int p = Fr.ipiv[k];
+      if (p != k) std::swap(y[Fr.rows[k]], y[Fr.rows[p]]);
+    }
+    for (int k = 0; k < np; ++k) {
+      const cd yk = y[Fr.rows[k]];
+      for (int i = k + 1; i < nf; ++i) y[Fr.rows[i]] -= Fr.F[static_cast<size_t>(i) * nf + k] * yk;
+    }
+  }
+  // backward, reverse postorder
+  for (int f = nn - 1; f >= 0; --f) {
+    const FrontF& Fr = R.fr[f];
+    const int nf = Fr.nf, np = Fr.npiv;
+    for (int k = np - 1; k >= 0; --k) {
+      cd s = y[Fr.rows[k]];
+      for (int c = k + 1; c < nf; ++c) s -= Fr.F[static_cast<size_t>(k) * nf + c] * y[Fr.rows[c]];
+      y[Fr.rows[k]] = s / Fr.F[static_cast<size_t>(k) * nf + k];
+    }
+  }
+  for (int64_t i = 0; i < S.n; ++i) x[S.perm[i]] = y[i];
+  if (L) L->add(FB, R.fb_macs);
+}
+
+// ---------------------------------------------------------------------------
+// Dense complex Schur (m x m, column-major) for ritz_extract/restart
+// (SPEC.md:444-461): Hessenberg by Givens, shifted QR, Givens reordering.
+struct DM {
+  int n;
+  std::vector<cd> a;
+  explicit DM(int n_ = 0) : n(n_), a(static_cast<size_t>(n_) * n_) {}
+  cd& operator()(int i, int j) { return a[i + static_cast<size_t>(j) * n]; }
+};
+
+void rot(cd f, cd g, double& c, cd& s) {
+  const double af = std::abs(f), ag = std::abs(g);
+  if (ag == 0) { c = 1; s = 0; return; }
+  if (af == 0) { c = 0; s = std::conj(g) / ag; return; }
+  const double r = std::sqrt(af * af + ag * ag);
+  c = af / r;
+  s = f / af * std::conj(g) / r;
+}
+// left: rows (i, i+1) <- G rows; right: cols (j, j+1) <- cols G^H
+void lrot(DM& A, int i, int c0, double c, cd s) {
+  for (int j = c0; j < A.n; ++j) {
+    const cd x = A(i, j), y = A(i + 1, j);
+    A(i, j) = c * x + s * y;
+    A(i + 1, j) = c * y - std::conj(s) * x;
+  }
+}
+void rrot(DM& A, int j, int r1, double c, cd s) {
+  for (int i = 0; i < r1; ++i) {
+    const cd x = A(i, j), y = A(i, j + 1);
+    A(i, j) = c * x + std::conj(s) * y;
+    A(i, j + 1) = c * y - s * x;
+  }
+}
+
+bool schur(DM& T, DM& Z) {
+  const int n = T.n;
+  Z = DM(n);
+  for (int i = 0; i < n; ++i) Z(i, i) = 1;
+  for (int k = 0; k + 2 < n; ++k)  // Hessenberg via Givens from the bottom
+    for (int i = n - 1; i > k + 1; --i) {
+      double c;
+      cd s;
+      rot(T(i - 1, k), T(i, k), c, s);
+      lrot(T, i - 1, 0, c, s);
+      rrot(T, i - 1, n, c, s);
+      rrot(Z, i - 1, n, c, s);
+      T(i, k) = 0;
+    }
+  const double eps = std::numeric_limits<double>::epsilon();
+  int hi = n - 1, it = 0, tot = 0;
+  while (hi > 0) {
+    int l = hi;
+    while (l > 0 && std::abs(T(l, l - 1)) > eps * (std::abs(T(l - 1, l - 1)) + std::abs(T(l, l)))) --l;
+    if (l > 0) T(l, l - 1) = 0;
+    if (l == hi) { --hi; it = 0; continue; }
+    if (++tot > 30 * n) return false;
+    ++it;
+    cd mu;
+    const cd a = T(hi - 1, hi - 1), b = T(hi - 1, hi), c2 = T(hi, hi - 1), d = T(hi, hi);
+    if (it % 10 == 0) {
+      mu = d + std::abs(c2);
+    } else {
+      const cd tr2 = (a + d) / 2.0, dsc = std::sqrt((a - d) * (a - d) / 4.0 + b * c2);
+      mu = std::abs(tr2 + dsc - d) < std::abs(tr2 - dsc - d) ? tr2 + dsc : tr2 - dsc;
+    }
+    for (int k = l; k < hi; ++k) {
+      double c;
+      cd s;
+      if (k == l) rot(T(l, l) - mu, T(l + 1, l), c, s);
+      else rot(T(k, k - 1), T(k + 1, k - 1), c, s);
+      lrot(T, k, std::max(l, k - 1), c, s);
+      if (k > l) T(k + 1, k - 1) = 0;
+      rrot(T, k, std::min(k + 3, hi + 1), c, s);
+      rrot(Z, k, n, c, s);
+    }
+  }
+  return true;
+}
+
+void schur_move_front(DM& T, DM& Z, std::vector<int>& sel) {
+  int ks = 0;
+  for (int k = 0; k < T.n; ++k) {
+    if (!sel[k]) continue;
+    for (int j = k - 1; j >= ks; --j) {
+      const cd a = T(j, j), b = T(j + 1, j + 1);
+      double c;
+      cd s;
+      rot(T(j, j + 1), b - a, c, s);
+      lrot(T, j, j + 2, c, s);
+      rrot(T, j, j, c, s);
+      T(j, j) = b;
+      T(j + 1, j + 1) = a;
+      rrot(Z, j, Z.n, c, s);
+      std::swap(sel[j], sel[j + 1]);
+    }
+    ++ks;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Quadratic eigensolver: operator, B-inner, CGS2 Arnoldi,
+// complex Krylov-Schur with the completeness guard of SURVEY.md §7 H1.
+struct Pencil {
+  Csr K, C, M;
+  double nK = 0, nC = 0, nM = 0;  // 1-norms (sparse.cpp:38-45)
+};
+
+double norm1(const Csr& A) {
+  std::vector<double> cs(A.n, 0.0);
+  for (int64_t r = 0; r < A.n; ++r)
+    for (int64_t k = A.rp[r]; k < A.rp[r + 1]; ++k) cs[A.col[k]] += std::abs(A.val[k]);
+  return cs.empty() ? 0.0 : *std::max_element(cs.begin(), cs.end());
+}
+
+struct Operator {
+  const Pencil* P;
+  const Factor* F;
+  cd s;
+  int64_t n;
+  std::vector<cd> t1, t2;
+  // apply_operator: r_u = -Q(s)^{-1}(s M v_u + C v_u + M v_l); r_l = s r_u + v_u
+  void apply(const cd* v, cd* r, Ledger* L) {
+    t1.resize(n);
+    t2.resize(n);
+    spmv(P->C, v, t1.data(), L);              // C v_u
+    spmv(P->M, v, t2.data(), L);              // M v_u
+    axpy(s, t2.data(), t1.data(), n, L);      // + s M v_u
+    spmv(P->M, v + n, t2.data(), L);          // M v_l
+    axpy(1.0, t2.data(), t1.data(), n, L);    // + M v_l
+    solve_factored(*F, t1.data(), r, L);
+    k_scal(-1.0, r, n);
+    for (int64_t i = 0; i < n; ++i) r[n + i] = v[i];
+    axpy(s, r, r + n, n, L);
+  }
+  // b_inner: x_u^H y_u + x_l^H M y_l
+  void bvec(const cd* y, cd* w, Ledger* L) {
+    std::copy(y, y + n, w);
+    spmv(P->M, y + n, w + n, L);
+  }
+};
+
+uint64_t splitmix(uint64_t& x) {
+  uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+double uni(uint64_t& s) { return (static_cast<double>(splitmix(s) >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0; }
+
+struct EigOut {
+  std::vector<cd> lam;
+  std::vector<double> res;
+  std::vector<std::vector<cd>> vec;
+  int cycles = 0, guard = 0, nconv = 0;
+  bool ok = false;
+};
+
+EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, int max_restarts,
+                       int guard_on, Ledger* L) {
+  const int64_t n = op.n, n2 = 2 * n;
+  const double sig = op.s.real();
+  const int keep_t = nev + std::min(20, m - nev - 1);
+  std::vector<std::vector<cd>> V(m + 1, std::vector<cd>(n2)), V2 = V;
+  std::vector<cd> r(n2), w(n2);
+  DM H(m + 1);  // (m+1) x (m+1), columns 0..m-1 used
+  auto fresh = [&](uint64_t sd, int nlock, std::vector<cd>& dst) {
+    uint64_t st = sd;
+    for (int64_t i = 0; i < n2; ++i) r[i] = uni(st);
+    for (int pass = 0; pass < 2 && nlock > 0; ++pass) {
+      op.bvec(r.data(), w.data(), L);
+      std::vector<cd> h(nlock);
+      for (int i = 0; i < nlock; ++i) h[i] = dot(V[i].data(), w.data(), n2, L);
+      for (int i = 0; i < nlock; ++i) axpy(-h[i], V[i].data(), r.data(), n2, L);
+    }
+    op.bvec(r.data(), w.data(), L);
+    const double b = std::sqrt(std::max(0.0, dot(r.data(), w.data(), n2, L).real()));
+    for (int64_t i = 0; i < n2; ++i) dst[i] = r[i] / b;
+  };
+  fresh(seed, 0, V[0]);
+  int k = 0, cycles = 0, gp = 0;
+  EigOut out;
+  std::vector<double> prev;
+  while (cycles < max_restarts) {
+    ++cycles;
+    for (int j = k; j < m; ++j) {
+      op.apply(V[j].data(), r.data(), L);
+      for (int pass = 0; pass < 2; ++pass) {  // CGS2
+        op.bvec(r.data(), w.data(), L);
+        std::vector<cd> h(j + 1);
+        for (int i = 0; i <= j; ++i) h[i] = dot(V[i].data(), w.data(), n2, L);
+        for (int i = 0; i <= j; ++i) axpy(-h[i], V[i].data(), r.data(), n2, L);
+        for (int i = 0; i <= j; ++i) H(i, j) += h[i];
+      }
+      op.bvec(r.data(), w.data(), L);
+      const double b = std::sqrt(std::max(0.0, dot(r.data(), w.data(), n2, L).real()));
+      H(j + 1, j) = b;
+      for (int64_t i = 0; i < n2; ++i) V[j + 1][i] = r[i] / b;
+    }
+    DM T(m), Z;
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i < m; ++i) T(i, j) = H(i, j);
+    if (!schur(T, Z)) throw OracleError{4, "QR did not converge"};
+    // eigenvectors of T, Ritz data
+    std::vector<cd> th(m), lam(m);
+    std::vector<double> est(m);
+    DM Y(m);
+    for (int j = 0; j < m; ++j) {
+      th[j] = T(j, j);
+      lam[j] = op.s + 1.0 / th[j];
+      Y(j, j) = 1;
+      for (int i = j - 1; i >= 0; --i) {
+        cd s = 0;
+        for (int t = i + 1; t <= j; ++t) s += T(i, t) * Y(t, j);
+        cd den = T(i, i) - th[j];
+        if (std::abs(den) < 1e-300) den = 1e-300;
+        Y(i, j) = -s / den;
+      }
+      double nr = 0;
+      for (int i = 0; i <= j; ++i) nr += std::norm(Y(i, j));
+      nr = std::sqrt(nr);
+      cd yl = 0;
+      for (int i = 0; i <= j; ++i) Y(i, j) /= nr, yl += Z(m - 1, i) * Y(i, j);
+      est[j] = std::abs(H(m, m - 1) * yl) / std::abs(th[j]);
+    }
+    std::vector<int> ord(m);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+      const double da = std::abs(lam[a] - sig), db = std::abs(lam[b] - sig);
+      if (da != db) return da < db;
+      return lam[a].imag() > lam[b].imag();
+    });
+    std::vector<double> cres(nev, 1.0);
+    std::vector<std::vector<cd>> cvec(nev);
+    bool all = true;
+    for (int c = 0; c < nev; ++c)
+      if (!(est[ord[c]] <= 1e3 * tol)) all = false;
+    if (all) {
+      for (int c = 0; c < nev; ++c) {
+        const int i = ord[c];
+        std::vector<cd> y(m, 0.0), x(n2, 0.0);
+        for (int row = 0; row < m; ++row)
+          for (int t = 0; t <= i; ++t) y[row] += Z(row, t) * Y(t, i);
+        for (int t = 0; t < m; ++t) axpy(y[t], V[t].data(), x.data(), n2, nullptr);
+        const bool low = std::abs(lam[i]) > 1.0;  // larger-norm block
+        std::vector<cd> u(x.begin() + (low ? n : 0), x.begin() + (low ? n2 : n));
+        // explicit pencil residual
+        std::vector<cd> a(n), q(n, 0.0);
+        spmv(op.P->K, u.data(), a.data(), nullptr);
+        for (int64_t e = 0; e < n; ++e) q[e] += a[e];
+        spmv(op.P->C, u.data(), a.data(), nullptr);
+        for (int64_t e = 0; e < n; ++e) q[e] += lam[i] * a[e];
+        spmv(op.P->M, u.data(), a.data(), nullptr);
+        for (int64_t e = 0; e < n; ++e) q[e] += lam[i] * lam[i] * a[e];
+        if (L) L->add(CHK, 3.0 * op.P->K.rp[n]);
+        double nq = 0, nu = 0;
+        for (int64_t e = 0; e < n; ++e) nq += std::norm(q[e]), nu += std::norm(u[e]);
+        const double al = std::abs(lam[i]);
+        cres[c] = std::sqrt(nq) / ((op.P->nK + al * op.P->nC + al * al * op.P->nM) * std::sqrt(nu));
+        if (!(cres[c] <= tol)) all = false;
+        for (auto& z : u) z /= std::sqrt(nu);
+        cvec[c] = std::move(u);
+      }
+    }
+    out.lam.clear();
+    out.res = cres;
+    for (int c = 0; c < nev; ++c) out.lam.push_back(lam[ord[c]]);
+    out.vec = cvec;
+    std::vector<int> sel(m, 0);
+    bool deflate = false;
+    if (all) {
+      std::vector<double> d;
+      for (int c = 0; c < nev; ++c) d.push_back(std::abs(lam[ord[c]] - sig));
+      std::sort(d.begin(), d.end());
+      bool improved = prev.empty();
+      for (size_t i = 0; i < d.size() && !improved; ++i)
+        if (d[i] < prev[i] * (1 - 1e-8)) improved = true;
+      if (!guard_on || !improved || gp >= 64) {
+        out.ok = true;
+        break;
+      }
+      prev = d;
+      ++gp;
+      deflate = true;
+      for (int c = 0; c < nev; ++c) sel[ord[c]] = 1;
+    } else {
+      for (int c = 0; c < std::min(keep_t, m - 1); ++c) sel[ord[c]] = 1;
+    }
+    int p = 0;
+    for (int v : sel) p += v;
+    std::vector<int> s2 = sel;
+    schur_move_front(T, Z, s2);
+    // V <- V Z[:, :p]; H <- [T_p; b^T]
+    for (int c = 0; c < p; ++c) {
+      std::fill(V2[c].begin(), V2[c].end(), cd{});
+      for (int t = 0; t < m; ++t) k_axpy(Z(t, c), V[t].data(), V2[c].data(), n2);
+    }
+    if (L) L->add(RST, static_cast<double>(m) * p * n2);
+    const cd beta = H(m, m - 1);
+    H = DM(m + 1);
+    for (int c = 0; c < p; ++c)
+      for (int i = 0; i <= c; ++i) H(i, c) = T(i, c);
+    for (int c = 0; c < p; ++c) V[c].swap(V2[c]);
+    if (deflate) {
+      fresh(seed + 0x1000003ull * gp, p, V[p]);
+    } else {
+      for (int c = 0; c < p; ++c) H(p, c) = beta * Z(m - 1, c);
+      V[p] = V[m];
+    }
+    k = p;
+  }
+  out.cycles = cycles;
+  out.guard = gp;
+  out.nconv = 0;
+  for (double x : out.res) out.nconv += x <= tol;
+  return out;
+}
+
+}  // namespace oracle
+
+// ============================================================================
+// C-ABI for tests (ctypes). Complex arrays are interleaved (re, im) doubles.
+// ============================================================================
+namespace {
+thread_local std::string g_err;
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const oracle::OracleError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+oracle::Csr make_csr(int64_t n, const int64_t* rp, const int32_t* col, const double* val_c) {
+  oracle::Csr A;
+  A.n = n;
+  A.rp.assign(rp, rp + n + 1);
+  A.col.assign(col, col + rp[n]);
+  A.val.resize(rp[n]);
+  for (int64_t k = 0; k < rp[n]; ++k) A.val[k] = cd(val_c[2 * k], val_c[2 * k + 1]);
+  return A;
+}
+struct OracleFactor {
+  oracle::Symbolic S;
+  oracle::Csr A;
+  oracle::Factor F;
+};
+struct OracleEig {
+  oracle::Symbolic S;
+  oracle::Pencil P;
+  oracle::Csr Q;
+  oracle::Factor F;
+  oracle::Ledger L;
+  std::unique_ptr<oracle::Operator> op;
+  double t_factor_ms = 0;
+};
+}  // namespace
+
+extern "C" {
+
+const char* oracle_last_error() { return g_err.c_str(); }
+
+int oracle_kind() {
+#ifdef ORACLE_REF_KERN
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+// Symbolic analysis: permutation + front sizes (graph derivation)
+int oracle_symbolic(int64_t n, const int64_t* rp, const int32_t* col, const int32_t* box, int elems,
+                    int leaf, int32_t* perm, int32_t* nfronts, int32_t* npiv, int32_t* nf, int32_t* parent,
+                    int64_t* struct_nnz_l) {
+  return guarded([&] {
+    const oracle::Symbolic S = oracle::symbolic(n, rp, col, box, elems, leaf);
+    std::copy(S.perm.begin(), S.perm.end(), perm);
+    *nfronts = static_cast<int32_t>(S.node_rows.size());
+    for (size_t f = 0; f < S.node_rows.size(); ++f) {
+      if (npiv) npiv[f] = S.node_npiv[f];
+      if (nf) nf[f] = static_cast<int32_t>(S.node_rows[f].size());
+      if (parent) parent[f] = S.node_parent[f];
+    }
+    if (struct_nnz_l) *struct_nnz_l = S.struct_nnz_l;
+  });
+}
+
+int oracle_factor_create(int64_t n, const int64_t* rp, const int32_t* col, const double* val_c,
+                         const int32_t* box, int elems, int leaf, void** out, int64_t* swaps,
+                         double* fa_macs) {
+  return guarded([&] {
+    auto h = std::make_unique<OracleFactor>();
+    h->A = make_csr(n, rp, col, val_c);
+    h->S = oracle::symbolic(n, rp, col, box, elems, leaf);
+    h->F = oracle::lu_factorize(h->S, h->A, nullptr);
+    if (swaps) *swaps = h->F.swaps;
+    if (fa_macs) *fa_macs = h->F.fa_macs;
+    *out = h.release();
+  });
+}
+
+int oracle_factor_solve(void* h, const double* b_c, double* x_c) {
+  return guarded([&] {
+    auto* F = static_cast<OracleFactor*>(h);
+    oracle::solve_factored(F->F, reinterpret_cast<const cd*>(b_c), reinterpret_cast<cd*>(x_c), nullptr);
+  });
+}
+
+// Front f (postorder) as dense row-major nf x nf complex + ipiv.
+int oracle_factor_front(void* h, int f, double* dense_c, int32_t* ipiv, int32_t* rows) {
+  return guarded([&] {
+    auto* F = static_cast<OracleFactor*>(h);
+    const auto& Fr = F->F.fr.at(f);
+    if (dense_c) std::memcpy(dense_c, Fr.F.data(), sizeof(cd) * Fr.F.size());
+    if (ipiv) std::copy(Fr.ipiv.begin(), Fr.ipiv.end(), ipiv);
+    if (rows) std::copy(Fr.rows.begin(), Fr.rows.end(), rows);
+  });
+}
+
+void oracle_factor_destroy(void* h) { delete static_cast<OracleFactor*>(h); }
+
+// Quadratic eigensolve. K, C, M real or complex interleaved; sigma real.
+int oracle_eig_create(int64_t n, const int64_t* rp, const int32_t* col, const double* K_c,
+                      const double* C_c, const double* M_c, const int32_t* box, int elems, int leaf,
+                      double sigma, void** out) {
+  return guarded([&] {
+    auto h = std::make_unique<OracleEig>();
+    h->P.K = make_csr(n, rp, col, K_c);
+    h->P.C = make_csr(n, rp, col, C_c);
+    h->P.M = make_csr(n, rp, col, M_c);
+    h->P.nK = oracle::norm1(h->P.K);
+    h->P.nC = oracle::norm1(h->P.C);
+    h->P.nM = oracle::norm1(h->P.M);
+    h->Q = h->P.K;
+    for (size_t k = 0; k < h->Q.val.size(); ++k)
+      h->Q.val[k] = h->P.K.val[k] + sigma * h->P.C.val[k] + sigma * sigma * h->P.M.val[k];
+    h->S = oracle::symbolic(n, rp, col, box, elems, leaf);
+    const auto t0 = std::chrono::steady_clock::now();
+    h->F = oracle::lu_factorize(h->S, h->Q, &h->L);
+    h->t_factor_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    h->op = std::make_unique<oracle::Operator>();
+    h->op->P = &h->P;
+    h->op->F = &h->F;
+    h->op->s = sigma;
+    h->op->n = n;
+    *out = h.release();
+  });
+}
+
+double oracle_eig_factor_ms(void* h) { return static_cast<OracleEig*>(h)->t_factor_ms; }
+
+int oracle_eig_apply(void* h, const double* v_c, double* r_c) {
+  return guarded([&] {
+    auto* E = static_cast<OracleEig*>(h);
+    E->op->apply(reinterpret_cast<const cd*>(v_c), reinterpret_cast<cd*>(r_c), nullptr);
+  });
+}
+
+int oracle_eig_solve_quadratic(void* h, int nev, int m, double tol, uint64_t seed, int max_restarts,
+                               int guard, double* lam_c, double* res, double* vec_c, int32_t* stats,
+                               double* ledger) {
+  return guarded([&] {
+    auto* E = static_cast<OracleEig*>(h);
+    const oracle::EigOut o = oracle::solve_quadratic(*E->op, nev, m > 0 ? m : 2 * nev + 1, tol, seed,
+                                                     max_restarts, guard, &E->L);
+    for (int i = 0; i < nev && i < static_cast<int>(o.lam.size()); ++i) {
+      lam_c[2 * i] = o.lam[i].real();
+      lam_c[2 * i + 1] = o.lam[i].imag();
+      res[i] = o.res[i];
+      if (vec_c && !o.vec[i].empty())
+        std::memcpy(vec_c + 2 * i * E->op->n, o.vec[i].data(), sizeof(cd) * E->op->n);
+    }
+    if (stats) stats[0] = o.cycles, stats[1] = o.guard, stats[2] = o.nconv, stats[3] = o.ok;
+    if (ledger)
+      for (int c = 0; c < 6; ++c) ledger[2 * c] = static_cast<double>(E->L.ops[c]), ledger[2 * c + 1] = E->L.macs[c];
+    if (!o.ok) throw oracle::OracleError{4, "oracle: not converged within max_restarts"};
+  });
+}
+
+void oracle_eig_destroy(void* h) { delete static_cast<OracleEig*>(h); }
+
+// Raw kern:: entry points (for checking the restated kernels against the
+// reference build and the product's SpMV).
+void oracle_kern_spmv(int64_t n, const int64_t* rp, const int32_t* col, const double* val_c,
+                      const double* x_c, double* y_c) {
+  oracle::k_spmv(n, rp, col, reinterpret_cast<const cd*>(val_c), reinterpret_cast<const cd*>(x_c),
+                 reinterpret_cast<cd*>(y_c));
+}
+void oracle_kern_dotc(const double* x_c, const double* y_c, int64_t n, double* out_c) {
+  const cd r = oracle::k_dotc(reinterpret_cast<const cd*>(x_c), reinterpret_cast<const cd*>(y_c), n);
+  out_c[0] = r.real();
+  out_c[1] = r.imag();
+}
+uint64_t oracle_kern_elim(double* tile_c, int64_t ld, const double* lcol_c, const double* urow_c,
+                          int64_t rows, int64_t cols) {
+  return oracle::k_elim(reinterpret_cast<cd*>(tile_c), ld, reinterpret_cast<const cd*>(lcol_c),
+                        reinterpret_cast<const cd*>(urow_c), rows, cols);
+}
+
+}  // extern "C"

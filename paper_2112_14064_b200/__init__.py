@@ -1,0 +1,10 @@
+"""B200-native shift-invert Krylov eigensolver for quadratic pencils from IGA/rIGA
+discretisations (arXiv 2112.14064). Host C++ + sm_100a CUDA behind the C-ABI in
+include/rq_b200.h; this package is the Python mirror of the reference's
+sparsela/eig operations."""
+from ._lib import LIB_PATH, RqError  # noqa: F401
+from .eig import (EigenPair, ShiftInvertOperator, apply_operator, arnoldi_run,  # noqa: F401
+                  b_inner, build_operator, solve_quadratic)
+from .pencil import CURL, DIV, QuadraticPencil, assemble, baseline_config  # noqa: F401
+from .sparsela import (Factorization, Ordering, lu_factorize,  # noqa: F401
+                       nested_dissection_order, solve_factored)

@@ -1,0 +1,379 @@
+// SPDX-License-Identifier: Apache-2.0
+// Shift-invert operator and Krylov kernels (real FP64, device resident).
+//
+//   spmv_csr        y = A x, one warp per row (kern::spmv_csr, kernels.cpp:44-56)
+//   spmv_op         t = C v_u + M (s v_u + v_l): the three products of
+//                   apply_operator in one pass over the shared
+//                   pattern (col[] read once, two value streams)
+//   gemv_t_part     h = V^T w: CGS2 projection (kern::dotc, kernels.cpp:23-32,
+//                   fused over all basis vectors; one pass over V), block
+//                   partials + fixed-order final reduction (deterministic)
+//   gemv_n          r -= V h (kern::axpy, kernels.cpp:19-21, fused)
+//   normalize       B-norm and v = r / ||r||_B (kern::nrm2sq/scal fused)
+//   combine         V Q (Krylov-Schur restart / Ritz vectors)
+//   residual_part   ||Q(lambda) u||^2 and ||u||^2 for complex (lambda, u)
+#include <cmath>
+#include <cstring>
+
+#include "device.cuh"
+
+namespace rqb {
+
+namespace {
+
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs: partial-sum blocks of the reductions
+constexpr int kRedThreads = 256;
+
+int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
+  return s;  // valid in thread 0
+}
+
+}  // namespace
+
+__global__ void spmv_csr_k(int64_t n, const int64_t* __restrict__ rowptr,
+                           const int32_t* __restrict__ col, const double* __restrict__ val,
+                           const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int64_t k = rowptr[row] + lane; k < rowptr[row + 1]; k += 32) s += val[k] * x[col[k]];
+  s = warp_sum(s);
+  if (lane == 0) y[row] = s;
+}
+
+__global__ void spmv_op_k(int64_t n, const int64_t* __restrict__ rowptr,
+                          const int32_t* __restrict__ col, const double* __restrict__ Cv,
+                          const double* __restrict__ Mv, double sigma,
+                          const double* __restrict__ vu, const double* __restrict__ vl,
+                          double* __restrict__ t) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int64_t k = rowptr[row] + lane; k < rowptr[row + 1]; k += 32) {
+    const int c = col[k];
+    const double xu = vu[c];
+    s += Cv[k] * xu + Mv[k] * (sigma * xu + vl[c]);
+  }
+  s = warp_sum(s);
+  if (lane == 0) t[row] = s;
+}
+
+// part[b * k + i] = sum over block b's slice of V[i] . w  (w given as two halves)
+__global__ void __launch_bounds__(kRedThreads) gemv_t_part(const double* __restrict__ V, int k,
+                                                         int64_t n2, const double* __restrict__ wu,
+                                                         const double* __restrict__ wl, int64_t n,
+                                                         double* __restrict__ part) {
+  __shared__ double sh[8][kRedThreads / 32];
+  const int64_t chunk = (n2 + gridDim.x - 1) / gridDim.x;
+  const int64_t e0 = blockIdx.x * chunk, e1 = min(n2, e0 + chunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i0 = 0; i0 < k; i0 += 8) {
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += kRedThreads) {
+      const double x = e < n ? wu[e] : wl[e - n];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (i0 + q < k) acc[q] += V[(int64_t)(i0 + q) * n2 + e] * x;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double v = warp_sum(acc[q]);
+      if (lane == 0) sh[q][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 8 && i0 + threadIdx.x < k) {
+      double s = 0.0;
+      for (int wq = 0; wq < kRedThreads / 32; ++wq) s += sh[threadIdx.x][wq];
+      part[(int64_t)blockIdx.x * k + i0 + threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// h[i] = sum_b part[b*k + i]  (fixed order), optionally hacc[i] += h[i]
+__global__ void reduce_parts(const double* __restrict__ part, int nb, int k, double* __restrict__ h,
+                             double* __restrict__ hacc) {
+  const int i = blockIdx.x;
+  const int lane = threadIdx.x;
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s += part[(int64_t)b * k + i];
+  s = warp_sum(s);
+  if (lane == 0) {
+    h[i] = s;
+    if (hacc) hacc[i] += s;
+  }
+}
+
+__global__ void gemv_n_k(const double* __restrict__ V, int k, int64_t n2,
+                         const double* __restrict__ h, double* __restrict__ r) {
+  extern __shared__ double hs[];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) hs[i] = h[i];
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < k; ++i) s += V[(int64_t)i * n2 + e] * hs[i];
+    r[e] -= s;
+  }
+}
+
+// part[b] = sum over slice of x.y (x, y given as halves: xu|xl and yu|yl)
+__global__ void __launch_bounds__(kRedThreads) dot_part(const double* __restrict__ xu,
+                                                      const double* __restrict__ xl,
+                                                      const double* __restrict__ yu,
+                                                      const double* __restrict__ yl, int64_t n,
+                                                      int64_t n2, double* __restrict__ part) {
+  __shared__ double sh[kRedThreads / 32];
+  double s = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double a = e < n ? xu[e] : xl[e - n];
+    const double b = e < n ? yu[e] : yl[e - n];
+    s += a * b;
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// beta = sqrt(sum parts) -> *beta_out; v = r / beta
+__global__ void normalize_k(const double* __restrict__ part, int nb, const double* __restrict__ r,
+                            int64_t n2, double* __restrict__ beta_out, double* __restrict__ v) {
+  __shared__ double beta_s;
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nb; b += 32) s += part[b];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) {
+      const double beta = sqrt(fmax(s, 0.0));
+      beta_s = beta;
+      if (blockIdx.x == 0 && beta_out) *beta_out = beta;
+    }
+  }
+  __syncthreads();
+  const double inv = beta_s > 0.0 ? 1.0 / beta_s : 0.0;
+  if (v)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
+         e += (int64_t)gridDim.x * blockDim.x)
+      v[e] = r[e] * inv;
+}
+
+__global__ void sum_parts(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 32) s += part[b];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// Vout[c][e] = sum_i V[i][e] Q[i + c*ldq], c in [c0, c0+8)
+__global__ void combine_k(const double* __restrict__ V, int k, int64_t n2,
+                          const double* __restrict__ Q, int ldq, int ncols,
+                          double* __restrict__ Vout) {
+  extern __shared__ double qs[];  // k x 8
+  const int c0 = blockIdx.y * 8;
+  for (int idx = threadIdx.x; idx < k * 8; idx += blockDim.x) {
+    const int i = idx % k, c = idx / k;
+    qs[i + c * k] = c0 + c < ncols ? Q[i + (int64_t)(c0 + c) * ldq] : 0.0;
+  }
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double acc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+    for (int i = 0; i < k; ++i) {
+      const double v = V[(int64_t)i * n2 + e];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] += v * qs[i + c * k];
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c0 + c < ncols) Vout[(int64_t)(c0 + c) * n2 + e] = acc[c];
+  }
+}
+
+// per-row complex pencil residual of (lambda, u = ur + i ui); parts of
+// ||Q(lambda)u||^2 (out[b]) and ||u||^2 (out[nb + b])
+__global__ void __launch_bounds__(kRedThreads) residual_part(
+    int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+    const double* __restrict__ K, const double* __restrict__ C, const double* __restrict__ M,
+    const double* __restrict__ ur, const double* __restrict__ ui, double lr, double li,
+    double* __restrict__ part) {
+  __shared__ double sh[kRedThreads / 32];
+  const int lane = threadIdx.x & 31;
+  const int wpb = kRedThreads / 32;
+  const double sr = lr * lr - li * li, si = 2.0 * lr * li;
+  double acc = 0.0, accu = 0.0;
+  for (int64_t row = blockIdx.x * (int64_t)wpb + (threadIdx.x >> 5); row < n;
+       row += (int64_t)gridDim.x * wpb) {
+    double a = 0, b = 0, c = 0, d = 0, e = 0, f = 0;
+    for (int64_t k = rowptr[row] + lane; k < rowptr[row + 1]; k += 32) {
+      const int j = col[k];
+      const double xr = ur[j], xi = ui[j];
+      a += K[k] * xr;
+      b += K[k] * xi;
+      c += C[k] * xr;
+      d += C[k] * xi;
+      e += M[k] * xr;
+      f += M[k] * xi;
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    c = warp_sum(c);
+    d = warp_sum(d);
+    e = warp_sum(e);
+    f = warp_sum(f);
+    if (lane == 0) {
+      const double re = a + (lr * c - li * d) + (sr * e - si * f);
+      const double im = b + (lr * d + li * c) + (sr * f + si * e);
+      acc += re * re + im * im;
+      accu += ur[row] * ur[row] + ui[row] * ui[row];
+    }
+  }
+  const double s = block_sum(acc, sh);
+  const double su = block_sum(accu, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    part[gridDim.x + blockIdx.x] = su;
+  }
+}
+
+__global__ void residual_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  double s = 0.0, su = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 32) s += part[b], su += part[nb + b];
+  s = warp_sum(s);
+  su = warp_sum(su);
+  if (threadIdx.x == 0) out[0] = s, out[1] = su;
+}
+
+// ---------------------------------------------------------------------------
+OperatorEngine::OperatorEngine(int64_t n_, const int64_t* rowptr, const int32_t* col,
+                               const double* K, const double* C, const double* M,
+                               const Symbolic& s, double sigma_, bool scaling)
+    : n(n_) {
+  nnz = rowptr[n];
+  varsigma = 1.0;
+  if (scaling) {
+    // scale_pencil: varsigma = sqrt(maxabs K / maxabs M)
+    double mk = 0, mm = 0;
+    for (int64_t k = 0; k < nnz; ++k) mk = std::max(mk, std::fabs(K[k])), mm = std::max(mm, std::fabs(M[k]));
+    if (!(mm > 0)) fail(errc::domain, "scale_pencil: zero M norm");
+    varsigma = std::sqrt(mk / mm);
+  }
+  sigma = sigma_ / varsigma;
+  std::vector<double> Cs(nnz), Ms(nnz), Q(nnz);
+  const double v = varsigma, v2 = varsigma * varsigma;
+  for (int64_t k = 0; k < nnz; ++k) {
+    Cs[k] = scaling ? v * C[k] : C[k];
+    Ms[k] = scaling ? v2 * M[k] : M[k];
+  }
+  // Q(s) on the shared pattern, formed on the host once: K + s C + s^2 M
+  for (int64_t k = 0; k < nnz; ++k) Q[k] = K[k] + sigma_ * C[k] + sigma_ * sigma_ * M[k];
+  fac = std::make_unique<FactorEngine>(s, n, rowptr, col, Q.data());
+  stream = fac->stream;
+  d_rowptr.upload(rowptr, sizeof(int64_t) * (n + 1), stream);
+  d_col.upload(col, sizeof(int32_t) * nnz, stream);
+  d_K.upload(K, sizeof(double) * nnz, stream);
+  d_C.upload(Cs.data(), sizeof(double) * nnz, stream);
+  d_M.upload(Ms.data(), sizeof(double) * nnz, stream);
+  d_Q.upload(Q.data(), sizeof(double) * nnz, stream);
+  d_w.alloc(sizeof(double) * 2 * n);
+  d_t.alloc(sizeof(double) * 2 * n);
+  nparts = kRedBlocks;
+  d_part.alloc(sizeof(double) * kRedBlocks * 512);
+  d_scal.alloc(sizeof(double) * 64);
+  RQB_CUDA(cudaStreamSynchronize(stream));
+  fac->factor();
+}
+
+OperatorEngine::~OperatorEngine() = default;
+
+void OperatorEngine::spmv(int which, const double* x, double* y) {
+  const double* val = which == 0 ? d_K.as<double>()
+                      : which == 1 ? d_C.as<double>()
+                      : which == 2 ? d_M.as<double>()
+                                   : d_Q.as<double>();
+  spmv_csr_k<<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
+                                                      val, x, y);
+  ++launches;
+}
+
+void OperatorEngine::apply(const double* v, double* r) {
+  double* t = d_t.as<double>();
+  spmv_op_k<<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
+                                                     d_C.as<double>(), d_M.as<double>(), sigma, v,
+                                                     v + n, t);
+  ++launches;
+  // r_u = -Q(s)^{-1} t ; r_l = s r_u + v_u (fused in the backward sweep)
+  rqb_solve_enqueue(*fac, t, r, -1.0, v, sigma, r + n);
+  launches += fac->launches_solve;
+}
+
+void OperatorEngine::bvec(const double* r, double* w) {
+  RQB_CUDA(cudaMemcpyAsync(w, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+  spmv(2, r + n, w + n);
+}
+
+void OperatorEngine::gemv_t(const double* V, int k, const double* w, double* h) {
+  if (k <= 0) return;
+  if (k > 512) fail(errc::config, "Krylov dimension above 512");
+  const int nb = kRedBlocks;
+  gemv_t_part<<<nb, kRedThreads, 0, stream>>>(V, k, 2 * n, w, w + n, n, d_part.as<double>());
+  reduce_parts<<<k, 32, 0, stream>>>(d_part.as<double>(), nb, k, h, nullptr);
+  launches += 2;
+}
+
+void OperatorEngine::gemv_n(const double* V, int k, const double* h, double* r, double* h_acc) {
+  if (k <= 0) return;
+  gemv_n_k<<<std::min(div_up(2 * n, 256), 148 * 8), 256, sizeof(double) * k, stream>>>(V, k, 2 * n,
+                                                                                     h, r);
+  ++launches;
+  (void)h_acc;
+}
+
+void OperatorEngine::dot2n(const double* x, const double* y, double* out) {
+  dot_part<<<kRedBlocks, kRedThreads, 0, stream>>>(x, x + n, y, y + n, n, 2 * n, d_part.as<double>());
+  sum_parts<<<1, 32, 0, stream>>>(d_part.as<double>(), kRedBlocks, out);
+  launches += 2;
+}
+
+void OperatorEngine::bnorm_normalize(const double* r, const double* w, double* beta_out,
+                                     double* v_next) {
+  dot_part<<<kRedBlocks, kRedThreads, 0, stream>>>(r, r + n, w, w + n, n, 2 * n, d_part.as<double>());
+  normalize_k<<<std::min(div_up(2 * n, 256), 148 * 8), 256, 0, stream>>>(
+      d_part.as<double>(), kRedBlocks, r, 2 * n, beta_out, v_next);
+  launches += 2;
+}
+
+void OperatorEngine::combine(const double* V, int k, const double* Q_dev, int ldq, int ncols,
+                             double* Vout) {
+  if (ncols <= 0 || k <= 0) return;
+  dim3 grid(std::min(div_up(2 * n, 256), 148 * 4), div_up(ncols, 8));
+  combine_k<<<grid, 256, sizeof(double) * k * 8, stream>>>(V, k, 2 * n, Q_dev, ldq, ncols, Vout);
+  ++launches;
+}
+
+void OperatorEngine::pencil_residual(const double* ur, const double* ui, double lr, double li,
+                                     double* out) {
+  residual_part<<<kRedBlocks, kRedThreads, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
+                                                       d_K.as<double>(), d_C.as<double>(),
+                                                       d_M.as<double>(), ur, ui, lr, li,
+                                                       d_part.as<double>());
+  residual_final<<<1, 32, 0, stream>>>(d_part.as<double>(), kRedBlocks, out);
+  launches += 2;
+}
+
+}  // namespace rqb

@@ -1,0 +1,131 @@
+// SPDX-License-Identifier: Apache-2.0
+// Device engines of the B200 build: the multifrontal factor (lu_factorize /
+// solve_factored) and the shift-invert operator with its
+// Krylov kernels. Host code talks to them through this
+// header only; all device memory lives inside.
+#pragma once
+
+#include <cuda_runtime_api.h>
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "host/common.hpp"
+
+namespace rqb {
+
+// Device-side description of one front (kept in sync with device.cuh).
+struct FrontDev {
+  int64_t off;        // pool offset (doubles), column-major ld x nf
+  int64_t rows_off;   // into rows[]
+  int64_t cbvec_off;  // forward-solve contribution vector
+  int64_t inv_off;    // extend-add maps: nchild arrays of nf int32 (child-local row or -1)
+  int32_t nf, npiv, ld, start;
+  int32_t nchild, child0, child1, scratch;  // scratch: slot of panel inverses (-1 none)
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+struct DeviceBuffer {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DeviceBuffer() = default;
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  ~DeviceBuffer();
+  void alloc(size_t nbytes);
+  void upload(const void* src, size_t nbytes, cudaStream_t s);
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Launch plan of one height batch.
+struct LevelPlan {
+  std::vector<int32_t> small;     // fronts factored whole in shared memory
+  std::vector<int32_t> big;       // fronts factored by the blocked panel path
+  std::vector<int32_t> with_kids; // fronts receiving an extend-add
+  std::vector<int32_t> all;
+  int small_nf = 0;               // max nf over `small`
+  int big_maxnf = 0, big_maxpanels = 0, big_cluster = 1, big_maxrows = 0;
+  int ea_maxnf = 0;
+  int solve_maxnf = 0;
+  // device offsets into FactorEngine::d_lists
+  int64_t off_small = 0, off_big = 0, off_kids = 0, off_all = 0;
+  std::vector<std::vector<int32_t>> panel_fronts;  // per panel step: active big fronts
+  std::vector<int64_t> off_panel;
+};
+
+struct FactorEngine {
+  Symbolic sym;
+  int64_t n = 0, nnz = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  DeviceBuffer d_pool, d_aval, d_qdst, d_rows, d_fronts, d_inv, d_ipiv, d_lists, d_scratch;
+  DeviceBuffer d_flags;   // [0] singular, [1] swaps
+  DeviceBuffer d_y, d_xnew, d_cbvec, d_perm;  // solve workspaces (n, n, cbvec), perm[new] = old
+  std::vector<FrontDev> fronts_h;
+  std::vector<LevelPlan> plans;
+  int64_t nscratch = 0;
+  double last_ms = 0.0;
+  int64_t last_swaps = 0;
+  int64_t launches_factor = 0, launches_solve = 0;
+  cudaGraph_t graph_factor = nullptr;
+  cudaGraphExec_t graph_factor_exec = nullptr;
+
+  FactorEngine(const Symbolic& s, int64_t n, const int64_t* rowptr, const int32_t* col,
+               const double* aval);
+  ~FactorEngine();
+  // Numeric factorization of the values currently in d_aval (device time in
+  // last_ms). Returns the singular flag.
+  void factor();
+  void set_values(const double* aval_host);
+  void set_values_device(const double* aval_dev);
+  // x = A^{-1} b on device vectors (original ordering), enqueued on `stream`.
+  void solve_device(const double* b, double* x, double scale_out = 1.0);
+  void enqueue_factor();
+};
+
+// Enqueue forward+backward substitution on fe.stream: x = scale * A^{-1} b and,
+// when xl != nullptr, xl = sigma * x + vu (fused lower block of apply_operator).
+void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scale,
+                       const double* vu, double sigma, double* xl);
+void rqb_solve_set_attrs(int maxnf);
+
+// Shift-invert operator on the linearised pencil, real FP64, device resident.
+struct OperatorEngine {
+  int64_t n = 0, nnz = 0;
+  double sigma = 0.0, varsigma = 1.0;  // shift of the (scaled) pencil, scaling factor
+  std::unique_ptr<FactorEngine> fac;
+  DeviceBuffer d_rowptr, d_col, d_K, d_C, d_M, d_Q;
+  DeviceBuffer d_w, d_t, d_part, d_scal;  // workspaces
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  int64_t nparts = 0;
+
+  OperatorEngine(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
+                 const double* C, const double* M, const Symbolic& s, double sigma,
+                 bool scaling);
+  ~OperatorEngine();
+  // Device vector ops (2n vectors: upper; lower), all enqueued on `stream`.
+  void spmv(int which, const double* x, double* y);          // y = A x
+  void apply(const double* v, double* r);                    // r = L(s)^{-1} B v
+  void bvec(const double* r, double* w);                     // w = [r_u; M r_l]
+  // h[0..k) = V[0..k)^T w (V row-major k x 2n), deterministic two-stage reduction
+  void gemv_t(const double* V, int k, const double* w, double* h);
+  // r -= V[0..k)^T-combination: r -= sum_i h[i] V[i]; optionally h_acc += h
+  void gemv_n(const double* V, int k, const double* h, double* r, double* h_acc);
+  // out = ||r||_B computed with w = B r; v_next = r / out
+  void bnorm_normalize(const double* r, const double* w, double* beta_out, double* v_next);
+  void dot2n(const double* x, const double* y, double* out);  // out = x.y (2n)
+  // Vout[c] = sum_k V[k] Q[k + c*ldq] for c < ncols (restart compression)
+  void combine(const double* V, int k, const double* Q_dev, int ldq, int ncols, double* Vout);
+  // Pencil residual pieces for complex u = ur + i ui at lambda = lr + i li:
+  // out[0] = ||Q(lambda) u||_2^2 (device scalar)
+  void pencil_residual(const double* ur, const double* ui, double lr, double li, double* out);
+};
+
+}  // namespace rqb

@@ -1,0 +1,500 @@
+// SPDX-License-Identifier: Apache-2.0
+// C-ABI of the B200 build (include/rq_b200.h). Exceptions never cross the
+// boundary: every entry point returns an rq::errc value (reference
+// types.hpp:14-23) and leaves the message in rq_last_error().
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../../include/rq_b200.h"
+#include "../engine.hpp"
+#include "common.hpp"
+#include "eigs.hpp"
+
+struct rq_pencil {
+  rqb::Pencil P;
+};
+struct rq_symbolic {
+  rqb::Symbolic S;
+};
+struct rq_factor {
+  std::unique_ptr<rqb::FactorEngine> owned;
+  rqb::FactorEngine* fe = nullptr;
+  rqb::DeviceBuffer d_b, d_x;
+};
+struct rq_operator {
+  std::unique_ptr<rqb::OperatorEngine> op;
+  double norms1[3] = {0, 0, 0};
+  rq_factor fac_view;
+  rqb::Ledger ledger;
+  rqb::DeviceBuffer d_a, d_b;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const rqb::Error& e) {
+    g_err = e.what();
+    return static_cast<int>(e.code());
+  } catch (const std::bad_alloc&) {
+    g_err = "out of memory";
+    return RQ_E_GENERIC;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RQ_E_GENERIC;
+  } catch (...) {
+    g_err = "unknown error";
+    return RQ_E_GENERIC;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) rqb::fail(rqb::errc::config, std::string("null argument: ") + what);
+}
+
+rqb::VectorSpace space_of(const rq_space_desc* d) {
+  need(d, "desc");
+  if (d->kind != RQ_SPACE_CURL && d->kind != RQ_SPACE_DIV) rqb::fail(rqb::errc::config, "unknown space kind");
+  return rqb::build_space(d->kind == RQ_SPACE_CURL ? rqb::SpaceKind::curl : rqb::SpaceKind::div, d->degree,
+                          d->elems, d->levels);
+}
+
+double norm1(int64_t n, const int64_t* rowptr, const int32_t* col, const std::vector<double>& v) {
+  std::vector<double> cs(n, 0.0);
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t k = rowptr[r]; k < rowptr[r + 1]; ++k) cs[col[k]] += std::fabs(v[k]);
+  double m = 0;
+  for (double s : cs) m = std::max(m, s);
+  return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rq_last_error(void) { return g_err.c_str(); }
+const char* rq_version(void) { return "rq_b200 0.1 (sm_100a)"; }
+
+int rq_pencil_assemble(const rq_space_desc* desc, rq_pencil_t** out) {
+  return guarded([&] {
+    need(out, "out");
+    const rqb::VectorSpace vs = space_of(desc);
+    auto p = std::make_unique<rq_pencil>();
+    p->P = rqb::assemble_pencil(vs, desc->alpha, desc->beta);
+    *out = p.release();
+  });
+}
+
+int rq_pencil_dims(const rq_pencil_t* p, int64_t* n_full, int64_t* n_free, int64_t* nnz) {
+  return guarded([&] {
+    need(p, "pencil");
+    if (n_full) *n_full = p->P.n_full;
+    if (n_free) *n_free = p->P.n;
+    if (nnz) *nnz = p->P.rowptr.back();
+  });
+}
+
+int rq_pencil_csr(const rq_pencil_t* p, int64_t* rowptr, int32_t* col, double* K, double* C,
+                  double* M) {
+  return guarded([&] {
+    need(p, "pencil");
+    const rqb::Pencil& P = p->P;
+    if (rowptr) std::memcpy(rowptr, P.rowptr.data(), sizeof(int64_t) * P.rowptr.size());
+    if (col) std::memcpy(col, P.col.data(), sizeof(int32_t) * P.col.size());
+    if (K) std::memcpy(K, P.K.data(), sizeof(double) * P.K.size());
+    if (C) std::memcpy(C, P.C.data(), sizeof(double) * P.C.size());
+    if (M) std::memcpy(M, P.M.data(), sizeof(double) * P.M.size());
+  });
+}
+
+int rq_pencil_supports(const rq_pencil_t* p, int32_t* box, int64_t* free_to_full) {
+  return guarded([&] {
+    need(p, "pencil");
+    if (box) std::memcpy(box, p->P.box.data(), sizeof(int32_t) * p->P.box.size());
+    if (free_to_full)
+      std::memcpy(free_to_full, p->P.free_to_full.data(), sizeof(int64_t) * p->P.free_to_full.size());
+  });
+}
+
+void rq_pencil_destroy(rq_pencil_t* p) { delete p; }
+
+int rq_space_dims(const rq_space_desc* desc, int64_t* nx_x, int64_t* ny_x, int64_t* nx_y,
+                  int64_t* ny_y) {
+  return guarded([&] {
+    const rqb::VectorSpace vs = space_of(desc);
+    if (nx_x) *nx_x = vs.cx.nx();
+    if (ny_x) *ny_x = vs.cx.ny();
+    if (nx_y) *nx_y = vs.cy.nx();
+    if (ny_y) *ny_y = vs.cy.ny();
+  });
+}
+
+int rq_space_boundary_mask(const rq_space_desc* desc, int64_t* mask, int64_t* count) {
+  return guarded([&] {
+    need(count, "count");
+    const rqb::VectorSpace vs = space_of(desc);
+    const std::vector<int64_t> m = rqb::boundary_mask(vs);
+    *count = static_cast<int64_t>(m.size());
+    if (mask) std::memcpy(mask, m.data(), sizeof(int64_t) * m.size());
+  });
+}
+
+int rq_nd_order(int64_t n, const int32_t* box, int elems, int leaf, rq_symbolic_t** out) {
+  return guarded([&] {
+    need(box, "box");
+    need(out, "out");
+    auto s = std::make_unique<rq_symbolic>();
+    s->S = rqb::nested_dissection(n, box, elems, leaf > 0 ? leaf : 64);
+    *out = s.release();
+  });
+}
+
+int rq_symbolic_stats_get(const rq_symbolic_t* s, rq_symbolic_stats* o) {
+  return guarded([&] {
+    need(s, "symbolic");
+    need(o, "out");
+    const rqb::Symbolic& S = s->S;
+    o->n = S.n;
+    o->nfronts = static_cast<int64_t>(S.fronts.size());
+    o->nlevels = static_cast<int64_t>(S.level_fronts.size());
+    o->max_front = S.max_front;
+    o->max_npiv = S.max_npiv;
+    o->nnz_l = S.nnz_l;
+    o->nnz_u = S.nnz_u;
+    o->pool_doubles = S.pool;
+    o->flops_lu = S.flops_lu;
+    o->flops_schur = S.flops_schur;
+    o->flops_schur_large = S.flops_schur_large;
+    o->trisolve_bytes = S.trisolve_bytes;
+  });
+}
+
+int rq_symbolic_perm(const rq_symbolic_t* s, int32_t* perm) {
+  return guarded([&] {
+    need(s, "symbolic");
+    need(perm, "perm");
+    std::memcpy(perm, s->S.perm.data(), sizeof(int32_t) * s->S.perm.size());
+  });
+}
+
+int rq_symbolic_fronts(const rq_symbolic_t* s, int32_t* parent, int32_t* npiv, int32_t* nf,
+                       int32_t* start, int32_t* level) {
+  return guarded([&] {
+    need(s, "symbolic");
+    const auto& F = s->S.fronts;
+    for (size_t f = 0; f < F.size(); ++f) {
+      if (parent) parent[f] = F[f].parent;
+      if (npiv) npiv[f] = F[f].npiv;
+      if (nf) nf[f] = F[f].nf;
+      if (start) start[f] = F[f].start;
+      if (level) level[f] = F[f].level;
+    }
+  });
+}
+
+int rq_symbolic_front_rows(const rq_symbolic_t* s, int64_t f, int32_t* rows) {
+  return guarded([&] {
+    need(s, "symbolic");
+    need(rows, "rows");
+    if (f < 0 || f >= static_cast<int64_t>(s->S.fronts.size())) rqb::fail(rqb::errc::dimension, "front id");
+    const rqb::Front& F = s->S.fronts[f];
+    std::memcpy(rows, s->S.rows.data() + F.rows_off, sizeof(int32_t) * F.nf);
+  });
+}
+
+void rq_symbolic_destroy(rq_symbolic_t* s) { delete s; }
+
+int rq_factor_create(const rq_symbolic_t* s, int64_t n, const int64_t* rowptr, const int32_t* col,
+                     const double* aval, rq_factor_t** out) {
+  return guarded([&] {
+    need(s, "symbolic");
+    need(rowptr, "rowptr");
+    need(col, "col");
+    need(aval, "aval");
+    need(out, "out");
+    if (n != s->S.n) rqb::fail(rqb::errc::dimension, "matrix size differs from the symbolic analysis");
+    auto f = std::make_unique<rq_factor>();
+    f->owned = std::make_unique<rqb::FactorEngine>(s->S, n, rowptr, col, aval);
+    f->fe = f->owned.get();
+    f->fe->factor();
+    *out = f.release();
+  });
+}
+
+int rq_factor_refactor(rq_factor_t* f, const double* aval) {
+  return guarded([&] {
+    need(f, "factor");
+    need(aval, "aval");
+    f->fe->set_values(aval);
+    f->fe->factor();
+  });
+}
+
+int rq_factor_get_info(const rq_factor_t* f, rq_factor_info* o) {
+  return guarded([&] {
+    need(f, "factor");
+    need(o, "out");
+    o->swaps = f->fe->last_swaps;
+    o->factor_ms = f->fe->last_ms;
+    o->gflops = f->fe->last_ms > 0 ? f->fe->sym.flops_lu / (f->fe->last_ms * 1e6) : 0.0;
+    o->launches = f->fe->launches_factor;
+  });
+}
+
+int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs) {
+  return guarded([&] {
+    need(f, "factor");
+    need(b, "b");
+    need(x, "x");
+    rqb::FactorEngine& fe = *f->fe;
+    const int64_t n = fe.n;
+    if (f->d_b.bytes < sizeof(double) * n) f->d_b.alloc(sizeof(double) * n);
+    if (f->d_x.bytes < sizeof(double) * n) f->d_x.alloc(sizeof(double) * n);
+    for (int r = 0; r < nrhs; ++r) {
+      rqb::cuda_check(cudaMemcpyAsync(f->d_b.p, b + r * n, sizeof(double) * n, cudaMemcpyHostToDevice,
+                                      fe.stream), "H2D b");
+      fe.solve_device(f->d_b.as<double>(), f->d_x.as<double>(), 1.0);
+      rqb::cuda_check(cudaMemcpyAsync(x + r * n, f->d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                      fe.stream), "D2H x");
+    }
+    rqb::cuda_check(cudaStreamSynchronize(fe.stream), "solve sync");
+  });
+}
+
+int rq_factor_front_export(const rq_factor_t* f, int64_t front, double* dense, int32_t* ipiv,
+                           int64_t* ld_out) {
+  return guarded([&] {
+    need(f, "factor");
+    const rqb::FactorEngine& fe = *f->fe;
+    if (front < 0 || front >= static_cast<int64_t>(fe.fronts_h.size()))
+      rqb::fail(rqb::errc::dimension, "front id");
+    const rqb::FrontDev& F = fe.fronts_h[front];
+    if (ld_out) *ld_out = F.ld;
+    if (dense)
+      rqb::cuda_check(cudaMemcpy(dense, fe.d_pool.as<double>() + F.off, sizeof(double) * F.ld * F.nf,
+                                 cudaMemcpyDeviceToHost), "D2H front");
+    if (ipiv && F.npiv > 0) {
+      rqb::cuda_check(cudaMemcpy(ipiv, fe.d_ipiv.as<int32_t>() + F.start, sizeof(int32_t) * F.npiv,
+                                 cudaMemcpyDeviceToHost), "D2H ipiv");
+    }
+  });
+}
+
+void rq_factor_destroy(rq_factor_t* f) { delete f; }
+
+int rq_operator_create(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
+                       const double* C, const double* M, const rq_symbolic_t* s,
+                       const rq_operator_opts* opts, rq_operator_t** out) {
+  return guarded([&] {
+    need(rowptr, "rowptr");
+    need(col, "col");
+    need(K, "K");
+    need(C, "C");
+    need(M, "M");
+    need(s, "symbolic");
+    need(opts, "opts");
+    need(out, "out");
+    if (!std::isfinite(opts->sigma)) rqb::fail(rqb::errc::config, "shift must be finite and real");
+    auto o = std::make_unique<rq_operator>();
+    o->op = std::make_unique<rqb::OperatorEngine>(n, rowptr, col, K, C, M, s->S, opts->sigma,
+                                                  opts->scaling != 0);
+    const int64_t nnz = rowptr[n];
+    const double v = o->op->varsigma;
+    std::vector<double> tmp(K, K + nnz);
+    o->norms1[0] = norm1(n, rowptr, col, tmp);
+    for (int64_t k = 0; k < nnz; ++k) tmp[k] = v * C[k];
+    o->norms1[1] = norm1(n, rowptr, col, tmp);
+    for (int64_t k = 0; k < nnz; ++k) tmp[k] = v * v * M[k];
+    o->norms1[2] = norm1(n, rowptr, col, tmp);
+    o->fac_view.fe = o->op->fac.get();
+    o->d_a.alloc(sizeof(double) * 2 * n);
+    o->d_b.alloc(sizeof(double) * 2 * n);
+    *out = o.release();
+  });
+}
+
+double rq_operator_varsigma(const rq_operator_t* op) { return op ? op->op->varsigma : 0.0; }
+
+rq_factor_t* rq_operator_factor(rq_operator_t* op) { return op ? &op->fac_view : nullptr; }
+
+void rq_operator_destroy(rq_operator_t* op) { delete op; }
+
+int rq_operator_apply(rq_operator_t* o, const double* v, double* r) {
+  return guarded([&] {
+    need(o, "op");
+    need(v, "v");
+    need(r, "r");
+    rqb::OperatorEngine& op = *o->op;
+    const int64_t n2 = 2 * op.n;
+    rqb::cuda_check(cudaMemcpyAsync(o->d_a.p, v, sizeof(double) * n2, cudaMemcpyHostToDevice, op.stream), "H2D");
+    op.apply(o->d_a.as<double>(), o->d_b.as<double>());
+    rqb::cuda_check(cudaMemcpyAsync(r, o->d_b.p, sizeof(double) * n2, cudaMemcpyDeviceToHost, op.stream), "D2H");
+    rqb::cuda_check(cudaStreamSynchronize(op.stream), "sync");
+  });
+}
+
+int rq_operator_b_inner(rq_operator_t* o, const double* x, const double* y, double* out) {
+  return guarded([&] {
+    need(o, "op");
+    need(x, "x");
+    need(y, "y");
+    need(out, "out");
+    rqb::OperatorEngine& op = *o->op;
+    const int64_t n2 = 2 * op.n;
+    rqb::DeviceBuffer dw, ds;
+    dw.alloc(sizeof(double) * n2);
+    ds.alloc(sizeof(double));
+    rqb::cuda_check(cudaMemcpyAsync(o->d_a.p, x, sizeof(double) * n2, cudaMemcpyHostToDevice, op.stream), "H2D");
+    rqb::cuda_check(cudaMemcpyAsync(o->d_b.p, y, sizeof(double) * n2, cudaMemcpyHostToDevice, op.stream), "H2D");
+    op.bvec(o->d_b.as<double>(), dw.as<double>());
+    op.dot2n(o->d_a.as<double>(), dw.as<double>(), ds.as<double>());
+    rqb::cuda_check(cudaMemcpyAsync(out, ds.p, sizeof(double), cudaMemcpyDeviceToHost, op.stream), "D2H");
+    rqb::cuda_check(cudaStreamSynchronize(op.stream), "sync");
+  });
+}
+
+int rq_operator_spmv(rq_operator_t* o, int which, const double* x, double* y) {
+  return guarded([&] {
+    need(o, "op");
+    need(x, "x");
+    need(y, "y");
+    if (which < 0 || which > 3) rqb::fail(rqb::errc::config, "which must be 0..3");
+    rqb::OperatorEngine& op = *o->op;
+    const int64_t n = op.n;
+    rqb::cuda_check(cudaMemcpyAsync(o->d_a.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, op.stream), "H2D");
+    op.spmv(which, o->d_a.as<double>(), o->d_b.as<double>());
+    rqb::cuda_check(cudaMemcpyAsync(y, o->d_b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, op.stream), "D2H");
+    rqb::cuda_check(cudaStreamSynchronize(op.stream), "sync");
+  });
+}
+
+int rq_operator_arnoldi(rq_operator_t* o, const double* v1, int m, double* V, double* H) {
+  return guarded([&] {
+    need(o, "op");
+    need(v1, "v1");
+    if (m < 1 || m > 512) rqb::fail(rqb::errc::config, "m must be in [1, 512]");
+    rqb::OperatorEngine& op = *o->op;
+    const int64_t n2 = 2 * op.n;
+    rqb::DeviceBuffer dV, dr, dw, dh, dbeta;
+    dV.alloc(sizeof(double) * (m + 1) * n2);
+    dr.alloc(sizeof(double) * n2);
+    dw.alloc(sizeof(double) * n2);
+    dh.alloc(sizeof(double) * 2 * (m + 1) * m);
+    dbeta.alloc(sizeof(double) * (m + 1));
+    double* dVp = dV.as<double>();
+    rqb::cuda_check(cudaMemcpyAsync(dr.p, v1, sizeof(double) * n2, cudaMemcpyHostToDevice, op.stream), "H2D");
+    op.bvec(dr.as<double>(), dw.as<double>());
+    op.bnorm_normalize(dr.as<double>(), dw.as<double>(), dbeta.as<double>() + m, dVp);
+    for (int j = 0; j < m; ++j) {
+      double* hA = dh.as<double>() + static_cast<int64_t>(j) * (m + 1);
+      double* hB = hA + static_cast<int64_t>(m) * (m + 1);
+      op.apply(dVp + j * n2, dr.as<double>());
+      for (int pass = 0; pass < 2; ++pass) {
+        double* h = pass ? hB : hA;
+        op.bvec(dr.as<double>(), dw.as<double>());
+        op.gemv_t(dVp, j + 1, dw.as<double>(), h);
+        op.gemv_n(dVp, j + 1, h, dr.as<double>(), nullptr);
+      }
+      op.bvec(dr.as<double>(), dw.as<double>());
+      op.bnorm_normalize(dr.as<double>(), dw.as<double>(), dbeta.as<double>() + j, dVp + (j + 1) * n2);
+    }
+    std::vector<double> hh(2 * (m + 1) * m), beta(m + 1);
+    rqb::cuda_check(cudaMemcpyAsync(hh.data(), dh.p, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost, op.stream), "D2H");
+    rqb::cuda_check(cudaMemcpyAsync(beta.data(), dbeta.p, sizeof(double) * beta.size(), cudaMemcpyDeviceToHost, op.stream), "D2H");
+    if (V)
+      rqb::cuda_check(cudaMemcpyAsync(V, dV.p, sizeof(double) * (m + 1) * n2, cudaMemcpyDeviceToHost, op.stream), "D2H");
+    rqb::cuda_check(cudaStreamSynchronize(op.stream), "sync");
+    if (H) {
+      std::fill(H, H + (m + 1) * m, 0.0);
+      for (int j = 0; j < m; ++j) {
+        for (int i = 0; i <= j; ++i)
+          H[i + j * (m + 1)] = hh[i + j * (m + 1)] + hh[static_cast<size_t>(m) * (m + 1) + i + j * (m + 1)];
+        H[j + 1 + j * (m + 1)] = beta[j];
+      }
+    }
+  });
+}
+
+int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, double* lam_im,
+                double* resid, double* vec_re, double* vec_im, rq_eigs_info* info) {
+  int nconv_out = 0;
+  bool partial = false;
+  const int rc = guarded([&] {
+    need(o, "op");
+    need(opts, "opts");
+    rqb::EigsOptions eo;
+    eo.nev = opts->nev;
+    eo.m = opts->m;
+    eo.tol = opts->tol;
+    eo.seed = opts->seed;
+    eo.max_restarts = opts->max_restarts > 0 ? opts->max_restarts : 100;
+    eo.guard = opts->guard;
+    eo.want_vectors = (vec_re && vec_im) ? 1 : 0;
+    o->ledger = rqb::Ledger{};
+    rqb::EigsResult r = rqb::solve_quadratic_device(*o->op, eo, o->ledger, o->norms1);
+    const int nout = static_cast<int>(r.lambda.size());
+    for (int i = 0; i < nout && i < opts->nev; ++i) {
+      if (lam_re) lam_re[i] = r.lambda[i].real();
+      if (lam_im) lam_im[i] = r.lambda[i].imag();
+      if (resid) resid[i] = r.resid[i];
+    }
+    if (eo.want_vectors && !r.vec_re.empty()) {
+      std::memcpy(vec_re, r.vec_re.data(), sizeof(double) * r.vec_re.size());
+      std::memcpy(vec_im, r.vec_im.data(), sizeof(double) * r.vec_im.size());
+    }
+    nconv_out = r.nconv;
+    if (info) {
+      rq_eigs_info& I = *info;
+      I.nconv = r.nconv;
+      I.restarts = r.cycles;
+      I.guard_passes = r.guard_passes;
+      const rqb::Ledger& L = o->ledger;
+      I.n_fa = L.n_fa;
+      I.n_fb = L.n_fb;
+      I.n_mv = L.n_mv;
+      I.n_vv = L.n_vv;
+      I.n_check = L.n_check;
+      I.n_restart = L.n_restart;
+      I.macs_fa = L.macs_fa;
+      I.macs_fb = L.macs_fb;
+      I.macs_mv = L.macs_mv;
+      I.macs_vv = L.macs_vv;
+      I.macs_check = L.macs_check;
+      I.macs_restart = L.macs_restart;
+      I.t_total_ms = r.t_total_ms;
+      I.t_factor_ms = o->op->fac->last_ms;
+      I.t_solve_ms = r.t_solve_ms;
+      I.t_spmv_ms = 0;
+      I.t_orth_ms = r.t_orth_ms;
+      I.t_host_ms = 0;
+      I.launches = r.launches;
+    }
+    partial = r.nconv < opts->nev;
+  });
+  if (rc != 0) return rc;
+  if (partial) {
+    g_err = "solve_quadratic: only " + std::to_string(nconv_out) + " pairs converged within max_restarts";
+    return RQ_E_SOLVER;
+  }
+  return 0;
+}
+
+int rq_eigs_ledger_json(const rq_operator_t* o, char* buf, size_t len) {
+  return guarded([&] {
+    need(o, "op");
+    need(buf, "buf");
+    const std::string s = o->ledger.to_json();
+    if (s.size() + 1 > len) rqb::fail(rqb::errc::dimension, "buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+}  // extern "C"

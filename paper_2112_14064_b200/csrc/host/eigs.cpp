@@ -1,0 +1,433 @@
+// SPDX-License-Identifier: Apache-2.0
+// solve_quadratic (defaults :489-497; Alg. 2,
+// :555-589): Krylov-Schur on the shift-invert operator of the linearised
+// pencil with B-orthogonal CGS2 Arnoldi. The host owns the loop and the m x m
+// projected problem; every N-sized vector lives on the device and stays real
+// (real shift, real start vector).
+//
+// Per Arnoldi step:
+//   r = S v_j                          (fused SpMV -> trisolve -> axpy)
+//   2 x { w = B r; h = V^T w; r -= V h }   (CGS2)
+//   beta = ||r||_B; v_{j+1} = r / beta
+// Per cycle: complex Schur form of H_m, Ritz values theta, lambda = s + 1/theta
+// (unscaled by varsigma), explicit pencil residuals of candidate pairs
+// (SURVEY App. B D5), restart keeping keep = nev + min(20, m - nev - 1)
+// wanted directions.
+// Completeness guard: once nev pairs converge they are kept
+// (deflated, b = 0) and the Krylov space is restarted from a fresh seeded vector
+// B-orthogonalised against them; any newly converged Ritz value closer to the
+// shift than the worst kept one is swapped in; repeat until a pass changes
+// nothing.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <sstream>
+
+#include "../engine.hpp"
+#include "dense.hpp"
+#include "eigs.hpp"
+
+namespace rqb {
+
+namespace {
+
+struct Ritz {
+  cplx theta;
+  cplx lambda;  // unscaled
+  double est;
+  int idx;      // position in the (unreordered) Schur form
+};
+
+double dist(const cplx& l, double sigma) { return std::abs(l - sigma); }
+
+}  // namespace
+
+std::string Ledger::to_json() const {
+  std::ostringstream os;
+  os.precision(17);
+  auto cat = [&](const char* name, int64_t ops, double macs, bool last = false) {
+    os << "  \"" << name << "\": {\"ops\": " << ops << ", \"macs\": " << macs
+       << ", \"flops\": " << flops_per_mac * macs << "}" << (last ? "\n" : ",\n");
+  };
+  os << "{\n";
+  cat("fa", n_fa, macs_fa);
+  cat("fb", n_fb, macs_fb);
+  cat("mv", n_mv, macs_mv);
+  cat("vv", n_vv, macs_vv);
+  cat("residual_check", n_check, macs_check);
+  cat("restart", n_restart, macs_restart);
+  os << "  \"flops_per_mac\": " << flops_per_mac << ",\n";
+  os << "  \"total_flops\": " << flops_per_mac * (macs_fa + macs_fb + macs_mv + macs_vv) << "\n}";
+  return os.str();
+}
+
+EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledger& L,
+                                  const double norms1[3]) {
+  using clock = std::chrono::steady_clock;
+  const auto t0 = clock::now();
+  const int64_t n = op.n, n2 = 2 * n;
+  const int nev = o.nev;
+  const int m = o.m > 0 ? o.m : 2 * nev + 1;
+  if (nev < 1) fail(errc::config, "nev must be positive");
+  if (m <= nev) fail(errc::config, "Krylov dimension m must exceed nev");
+  if (m > 512) fail(errc::config, "Krylov dimension above 512");
+  if (m >= n2) fail(errc::config, "Krylov dimension must be below 2N");
+  if (!(o.tol > 0)) fail(errc::config, "tolerance must be positive");
+  const int keep_target = nev + std::min(20, m - nev - 1);
+  const double sig = op.sigma;  // scaled shift
+  const double vs = op.varsigma;
+  cudaStream_t st = op.stream;
+
+  EigsResult res;
+  const int64_t launches0 = op.launches;
+  // ledger: one factorization (already done when the operator was built)
+  L.n_fa += 1;
+  {
+    double macs = 0;
+    for (const Front& F : op.fac->sym.fronts)
+      for (int k = 0; k < F.npiv; ++k) {
+        const double r = F.nf - k - 1.0;
+        macs += r + r * r;
+      }
+    L.macs_fa += macs;
+  }
+  const double fb_macs = static_cast<double>(op.fac->sym.nnz_l + op.fac->sym.nnz_u);
+  const double nnz = static_cast<double>(op.nnz);
+
+  DeviceBuffer dV, dV2, dR, dW, dHa, dHb, dBeta, dQ, dX, dRes;
+  dV.alloc(sizeof(double) * (m + 1) * n2);
+  dV2.alloc(sizeof(double) * (m + 1) * n2);
+  dR.alloc(sizeof(double) * n2);
+  dW.alloc(sizeof(double) * n2);
+  dHa.alloc(sizeof(double) * (m + 1) * (m + 1));
+  dHb.alloc(sizeof(double) * (m + 1) * (m + 1));
+  dBeta.alloc(sizeof(double) * (m + 1));
+  dQ.alloc(sizeof(double) * (m + 1) * (2 * m + 2));
+  dX.alloc(sizeof(double) * n2 * 2 * (m + 1));
+  dRes.alloc(sizeof(double) * 4 * (m + 1));
+  double* V = dV.as<double>();
+  double* V2 = dV2.as<double>();
+  double* r = dR.as<double>();
+  double* w = dW.as<double>();
+
+  cudaEvent_t e_a, e_b;
+  cuda_check(cudaEventCreate(&e_a), "event");
+  cuda_check(cudaEventCreate(&e_b), "event");
+
+  // Start vector v = splitmix64(seed) uniform[-1,1]^{2N}, B-normalised.
+  auto fresh_vector = [&](uint64_t seed, int nlock, double* dst) {
+    std::vector<double> v(n2);
+    uint64_t s = seed;
+    for (int64_t i = 0; i < n2; ++i) v[i] = splitmix_uniform(s);
+    cuda_check(cudaMemcpyAsync(r, v.data(), sizeof(double) * n2, cudaMemcpyHostToDevice, st), "H2D v0");
+    for (int pass = 0; pass < 2 && nlock > 0; ++pass) {
+      op.bvec(r, w);
+      op.gemv_t(V, nlock, w, dHa.as<double>());
+      op.gemv_n(V, nlock, dHa.as<double>(), r, nullptr);
+      L.n_mv += 1;
+      L.macs_mv += nnz;
+      L.n_vv += 2 * nlock;
+      L.macs_vv += 2.0 * nlock * n2;
+    }
+    op.bvec(r, w);
+    op.bnorm_normalize(r, w, dBeta.as<double>() + m, dst);
+    L.n_mv += 1;
+    L.macs_mv += nnz;
+    L.n_vv += 2;
+    L.macs_vv += 2.0 * n2;
+  };
+
+  std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0);  // column-major (m+1) x m
+  auto Hc = [&](int i, int j) -> double& { return H[i + static_cast<size_t>(j) * (m + 1)]; };
+
+  fresh_vector(o.seed, 0, V);
+  int k = 0;
+  int cycles = 0, guard_passes = 0;
+  bool converged_final = false;
+  std::vector<double> prev_guard_dists;
+  std::vector<Ritz> final_set, last_cand;
+  std::vector<double> final_res, last_res;
+  std::vector<int> final_block;  // 0 upper, 1 lower
+  std::vector<double> final_vecs_re, final_vecs_im;
+  std::vector<double> ha((m + 1) * (m + 1)), hb((m + 1) * (m + 1)), betas(m + 1);
+  double t_solve = 0, t_orth = 0;
+
+  while (true) {
+    if (cycles >= o.max_restarts) break;
+    ++cycles;
+    // ---- Arnoldi steps k .. m-1 ----
+    for (int j = k; j < m; ++j) {
+      double* vj = V + static_cast<int64_t>(j) * n2;
+      if (o.profile) cuda_check(cudaEventRecord(e_a, st), "ev");
+      op.apply(vj, r);
+      if (o.profile) {
+        cuda_check(cudaEventRecord(e_b, st), "ev");
+        cuda_check(cudaEventSynchronize(e_b), "ev");
+        float ms;
+        cudaEventElapsedTime(&ms, e_a, e_b);
+        t_solve += ms;
+      }
+      L.n_fb += 1;
+      L.macs_fb += fb_macs;
+      L.n_mv += 3;  // sigma M v_u, C v_u, M v_l (fused)
+      L.macs_mv += 3 * nnz;
+      if (o.profile) cuda_check(cudaEventRecord(e_a, st), "ev");
+      double* hA = dHa.as<double>() + static_cast<int64_t>(j) * (m + 1);
+      double* hB = dHb.as<double>() + static_cast<int64_t>(j) * (m + 1);
+      op.bvec(r, w);
+      op.gemv_t(V, j + 1, w, hA);
+      op.gemv_n(V, j + 1, hA, r, nullptr);
+      op.bvec(r, w);
+      op.gemv_t(V, j + 1, w, hB);
+      op.gemv_n(V, j + 1, hB, r, nullptr);
+      op.bvec(r, w);
+      op.bnorm_normalize(r, w, dBeta.as<double>() + j, V + static_cast<int64_t>(j + 1) * n2);
+      if (o.profile) {
+        cuda_check(cudaEventRecord(e_b, st), "ev");
+        cuda_check(cudaEventSynchronize(e_b), "ev");
+        float ms;
+        cudaEventElapsedTime(&ms, e_a, e_b);
+        t_orth += ms;
+      }
+      L.n_mv += 3;
+      L.macs_mv += 3 * nnz;
+      L.n_vv += 4 * (j + 1) + 2;
+      L.macs_vv += (4.0 * (j + 1) + 2) * n2;
+    }
+    cuda_check(cudaMemcpyAsync(ha.data(), dHa.p, sizeof(double) * (m + 1) * (m + 1),
+                               cudaMemcpyDeviceToHost, st), "D2H H");
+    cuda_check(cudaMemcpyAsync(hb.data(), dHb.p, sizeof(double) * (m + 1) * (m + 1),
+                               cudaMemcpyDeviceToHost, st), "D2H H");
+    cuda_check(cudaMemcpyAsync(betas.data(), dBeta.p, sizeof(double) * (m + 1),
+                               cudaMemcpyDeviceToHost, st), "D2H beta");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    for (int j = k; j < m; ++j) {
+      for (int i = 0; i <= j; ++i)
+        Hc(i, j) = ha[i + static_cast<size_t>(j) * (m + 1)] + hb[i + static_cast<size_t>(j) * (m + 1)];
+      Hc(j + 1, j) = betas[j];
+    }
+    // ---- Ritz extraction ----
+    std::vector<double> Hm(static_cast<size_t>(m) * m);
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i < m; ++i) Hm[i + static_cast<size_t>(j) * m] = Hc(i, j);
+    CMat T, Z;
+    if (!complex_schur(Hm, m, T, Z)) fail(errc::solver, "Hessenberg QR did not converge");
+    const CMat Y = triangular_eigvecs(T);
+    const double beta_m = Hc(m, m - 1);
+    std::vector<Ritz> rz(m);
+    for (int i = 0; i < m; ++i) {
+      rz[i].theta = T(i, i);
+      rz[i].lambda = (sig + 1.0 / rz[i].theta) * vs;
+      // y_i in the H basis = Z Y[:, i]; residual estimate |beta_m e_m^T y_i| / |theta|
+      cplx ylast = 0.0;
+      for (int t = 0; t <= i; ++t) ylast += Z(m - 1, t) * Y(t, i);
+      rz[i].est = std::abs(beta_m * ylast) / std::max(std::abs(rz[i].theta), 1e-300);
+      rz[i].idx = i;
+    }
+    // wanted order: largest |theta| first; conjugate pairs adjacent (+imag first)
+    std::vector<int> order(m);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      const double da = dist(rz[a].lambda, sig * vs), db = dist(rz[b].lambda, sig * vs);
+      if (da != db) return da < db;
+      return rz[a].lambda.imag() > rz[b].lambda.imag();
+    });
+    // ---- convergence: explicit residuals of the nev nearest ----
+    std::vector<int> cand(order.begin(), order.begin() + nev);
+    const bool maybe = std::all_of(cand.begin(), cand.end(),
+                                   [&](int i) { return rz[i].est <= o.est_factor * o.tol; });
+    bool all_conv = false;
+    std::vector<double> cres(nev, 1.0);
+    std::vector<int> cblock(nev, 0);
+    if (maybe) {
+      // Ritz vectors X = V_m [Re y, Im y] for the candidates (y = Z Y[:, i])
+      std::vector<double> Yr(static_cast<size_t>(m) * 2 * nev);
+      for (int c = 0; c < nev; ++c) {
+        const int i = cand[c];
+        for (int row = 0; row < m; ++row) {
+          cplx y = 0.0;
+          for (int t = 0; t <= i; ++t) y += Z(row, t) * Y(t, i);
+          Yr[row + static_cast<size_t>(2 * c) * m] = y.real();
+          Yr[row + static_cast<size_t>(2 * c + 1) * m] = y.imag();
+        }
+      }
+      cuda_check(cudaMemcpyAsync(dQ.p, Yr.data(), sizeof(double) * Yr.size(), cudaMemcpyHostToDevice, st),
+                 "H2D Y");
+      op.combine(V, m, dQ.as<double>(), m, 2 * nev, dX.as<double>());
+      for (int c = 0; c < nev; ++c) {
+        const Ritz& R = rz[cand[c]];
+        const cplx gam = R.lambda / vs;  // eigenvalue of the scaled pencil
+        const int blk = std::abs(gam) > 1.0 ? 1 : 0;  // larger-norm block
+        cblock[c] = blk;
+        const double* xr = dX.as<double>() + static_cast<int64_t>(2 * c) * n2 + blk * n;
+        const double* xi = xr + n2;
+        op.pencil_residual(xr, xi, gam.real(), gam.imag(), dRes.as<double>() + 2 * c);
+      }
+      std::vector<double> rr(2 * nev);
+      cuda_check(cudaMemcpyAsync(rr.data(), dRes.p, sizeof(double) * 2 * nev, cudaMemcpyDeviceToHost, st),
+                 "D2H res");
+      cuda_check(cudaStreamSynchronize(st), "sync");
+      all_conv = true;
+      for (int c = 0; c < nev; ++c) {
+        const cplx gam = rz[cand[c]].lambda / vs;
+        const double ag = std::abs(gam);
+        const double den = (norms1[0] + ag * norms1[1] + ag * ag * norms1[2]) * std::sqrt(rr[2 * c + 1]);
+        cres[c] = den > 0 ? std::sqrt(rr[2 * c]) / den : 1.0;
+        if (!(cres[c] <= o.tol)) all_conv = false;
+      }
+      L.n_check += 3 * nev;
+      L.macs_check += 6.0 * nnz * nev;
+    }
+    int nconv_now = 0;
+    for (int c = 0; c < nev && maybe; ++c)
+      if (cres[c] <= o.tol) ++nconv_now;
+    res.nconv = std::max(res.nconv, nconv_now);
+    last_cand.clear();
+    for (int c = 0; c < nev; ++c) last_cand.push_back(rz[cand[c]]);
+    last_res = cres;
+
+    auto capture_set = [&]() {
+      final_set.clear();
+      final_res.assign(cres.begin(), cres.end());
+      final_block.assign(cblock.begin(), cblock.end());
+      for (int c = 0; c < nev; ++c) final_set.push_back(rz[cand[c]]);
+      if (o.want_vectors) {
+        final_vecs_re.assign(static_cast<size_t>(n) * nev, 0.0);
+        final_vecs_im.assign(static_cast<size_t>(n) * nev, 0.0);
+        std::vector<double> buf(n);
+        for (int c = 0; c < nev; ++c) {
+          const double* xr = dX.as<double>() + static_cast<int64_t>(2 * c) * n2 + cblock[c] * n;
+          cuda_check(cudaMemcpy(final_vecs_re.data() + static_cast<size_t>(c) * n, xr,
+                                sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H x");
+          cuda_check(cudaMemcpy(final_vecs_im.data() + static_cast<size_t>(c) * n, xr + n2,
+                                sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H x");
+          double nr = 0;
+          for (int64_t i = 0; i < n; ++i)
+            nr += final_vecs_re[c * n + i] * final_vecs_re[c * n + i] +
+                  final_vecs_im[c * n + i] * final_vecs_im[c * n + i];
+          nr = std::sqrt(nr);
+          for (int64_t i = 0; i < n; ++i) final_vecs_re[c * n + i] /= nr, final_vecs_im[c * n + i] /= nr;
+        }
+      }
+    };
+
+    // ---- decide: done / guard restart / normal restart ----
+    std::vector<int> sel(m, 0);
+    int p = 0;
+    bool deflate = false;
+    if (all_conv) {
+      std::vector<double> dists;
+      for (int c = 0; c < nev; ++c) dists.push_back(dist(rz[cand[c]].lambda, sig * vs));
+      std::sort(dists.begin(), dists.end());
+      bool improved = prev_guard_dists.empty();
+      for (size_t i = 0; i < dists.size() && !improved; ++i)
+        if (dists[i] < prev_guard_dists[i] * (1.0 - 1e-8)) improved = true;
+      capture_set();
+      if (!o.guard || !improved || guard_passes >= o.max_guard) {
+        converged_final = true;
+        break;
+      }
+      prev_guard_dists = dists;
+      ++guard_passes;
+      deflate = true;
+      for (int c = 0; c < nev; ++c) sel[cand[c]] = 1;
+    } else {
+      for (int c = 0; c < std::min(keep_target, m - 1); ++c) sel[order[c]] = 1;
+    }
+    // conjugation closure of the selection
+    {
+      std::vector<int> used(m, 0);
+      for (int i = 0; i < m; ++i) used[i] = sel[i];
+      for (int i = 0; i < m; ++i) {
+        if (!sel[i]) continue;
+        const cplx th = rz[i].theta;
+        if (std::abs(th.imag()) <= 1e-10 * std::abs(th)) continue;
+        // find partner: closest to conj(theta) among the rest
+        int best = -1;
+        double bd = 1e300;
+        for (int q = 0; q < m; ++q) {
+          if (q == i) continue;
+          const double d = std::abs(rz[q].theta - std::conj(th));
+          if (d < bd) bd = d, best = q;
+        }
+        if (best >= 0 && !sel[best] && bd <= 1e-6 * std::abs(th)) sel[best] = 1;
+      }
+    }
+    for (int i = 0; i < m; ++i) p += sel[i];
+    if (p >= m) {
+      // keep at least one new direction: drop the farthest selected pair
+      for (int c = m - 1; c >= 0 && p >= m; --c)
+        if (sel[order[c]]) sel[order[c]] = 0, --p;
+    }
+    // ---- restart: reorder Schur form, real basis of the kept directions ----
+    CMat Tr = T, Zr = Z;
+    std::vector<int> s2 = sel;
+    schur_reorder(Tr, Zr, s2);
+    std::vector<double> Qp;
+    const int rank = real_basis(Zr, p, Qp);
+    if (rank < p) p = rank;
+    if (p <= 0) fail(errc::solver, "Krylov-Schur restart lost its basis");
+    // T_p = Q_p^T H_m Q_p, b_p = beta_m e_m^T Q_p
+    std::vector<double> HQ(static_cast<size_t>(m) * p, 0.0), Tp(static_cast<size_t>(p) * p, 0.0);
+    for (int c = 0; c < p; ++c)
+      for (int t = 0; t < m; ++t) {
+        const double q = Qp[t + static_cast<size_t>(c) * m];
+        if (q == 0.0) continue;
+        for (int i = 0; i < m; ++i) HQ[i + static_cast<size_t>(c) * m] += Hm[i + static_cast<size_t>(t) * m] * q;
+      }
+    for (int c = 0; c < p; ++c)
+      for (int i = 0; i < p; ++i) {
+        double s = 0;
+        for (int t = 0; t < m; ++t) s += Qp[t + static_cast<size_t>(i) * m] * HQ[t + static_cast<size_t>(c) * m];
+        Tp[i + static_cast<size_t>(c) * p] = s;
+      }
+    cuda_check(cudaMemcpyAsync(dQ.p, Qp.data(), sizeof(double) * m * p, cudaMemcpyHostToDevice, st), "H2D Q");
+    op.combine(V, m, dQ.as<double>(), m, p, V2);
+    L.n_restart += 1;
+    L.macs_restart += static_cast<double>(m) * p * n2;
+    std::fill(H.begin(), H.end(), 0.0);
+    for (int c = 0; c < p; ++c)
+      for (int i = 0; i < p; ++i) Hc(i, c) = Tp[i + static_cast<size_t>(c) * p];
+    std::swap(V, V2);
+    if (deflate) {
+      // b = 0 (converged directions deflated); fresh seeded continuation vector
+      fresh_vector(o.seed + 0x1000003ull * guard_passes, p, V + static_cast<int64_t>(p) * n2);
+    } else {
+      for (int c = 0; c < p; ++c) Hc(p, c) = beta_m * Qp[(m - 1) + static_cast<size_t>(c) * m];
+      cuda_check(cudaMemcpyAsync(V + static_cast<int64_t>(p) * n2, V2 + static_cast<int64_t>(m) * n2,
+                                 sizeof(double) * n2, cudaMemcpyDeviceToDevice, st), "D2D v");
+    }
+    k = p;
+  }
+  cudaEventDestroy(e_a);
+  cudaEventDestroy(e_b);
+  // keep the last candidate set if the run stopped early
+  if (!converged_final && final_set.empty()) {
+    final_set = last_cand;
+    final_res = last_res;
+  }
+  res.converged = converged_final;
+  res.cycles = cycles;
+  res.guard_passes = guard_passes;
+  for (size_t c = 0; c < final_set.size(); ++c) {
+    res.lambda.push_back(final_set[c].lambda);
+    res.resid.push_back(final_res[c]);
+  }
+  res.vec_re = std::move(final_vecs_re);
+  res.vec_im = std::move(final_vecs_im);
+  res.launches = op.launches - launches0;
+  res.t_total_ms = std::chrono::duration<double, std::milli>(clock::now() - t0).count();
+  res.t_solve_ms = t_solve;
+  res.t_orth_ms = t_orth;
+  if (!converged_final) {
+    res.nconv = static_cast<int>(std::count_if(res.resid.begin(), res.resid.end(),
+                                               [&](double x) { return x <= o.tol; }));
+  } else {
+    res.nconv = nev;
+  }
+  return res;
+}
+
+}  // namespace rqb

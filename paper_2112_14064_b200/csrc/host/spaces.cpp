@@ -1,0 +1,434 @@
+// SPDX-License-Identifier: Apache-2.0
+// Spline spaces and BASELINE pencil assembly (host input construction).
+//
+// Restates, in this build's own code, the bookkeeping of the reference
+// splines/spaces modules:
+//   - open uniform knots with interior multiplicities  (splines.cpp:72-92)
+//   - element spans + basis support element ranges      (splines.cpp:25-62)
+//   - rIGA separator multiplicities                      (splines.cpp:94-116)
+//   - recursive-bisection separator breakpoints          (spaces.cpp:12-24)
+//   - curl/div component degree layout                   (spaces.cpp:54-64)
+//   - boundary masks em/acoustic                         (spaces.cpp:79-113)
+// and the BASELINE forms (BASELINE.json configs; SPEC.md:216-224, 261-264 for
+// the quadrature and elimination rules):
+//   K = int (div u div v | curl u curl v) + u.v,  M = int u.v,
+//   C = alpha M + beta K, (p+1)^2 Gauss points per element, constrained DOFs
+//   eliminated, K/C/M on one shared pattern (all support-overlapping pairs).
+#include <algorithm>
+#include <cmath>
+#include <thread>
+
+#include "common.hpp"
+
+namespace rqb {
+
+Univariate make_univariate(int degree, int elems, const std::vector<int>& mult) {
+  if (degree < 1) fail(errc::domain, "degree must be at least 1");
+  if (elems < 1) fail(errc::domain, "element count must be at least 1");
+  if (static_cast<int>(mult.size()) != elems - 1)
+    fail(errc::domain, "need one multiplicity per interior breakpoint");
+  Univariate u;
+  u.degree = degree;
+  u.elems = elems;
+  u.mult = mult;
+  u.knots.assign(degree + 1, 0.0);
+  for (int b = 1; b < elems; ++b) {
+    const int m = mult[b - 1];
+    if (m < 1 || m > degree) fail(errc::domain, "interior multiplicity outside [1, degree]");
+    for (int r = 0; r < m; ++r) u.knots.push_back(static_cast<double>(b) / elems);
+  }
+  for (int r = 0; r <= degree; ++r) u.knots.push_back(1.0);
+  u.elem_span.resize(elems);
+  int s = degree;
+  for (int e = 0; e < elems; ++e) {
+    u.elem_span[e] = s;
+    if (e < elems - 1) s += mult[e];
+  }
+  const int nb = u.nbasis();
+  u.sup_first.assign(nb, -1);
+  u.sup_last.assign(nb, -1);
+  for (int e = 0; e < elems; ++e)
+    for (int i = u.first_basis(e); i <= u.elem_span[e]; ++i) {
+      if (u.sup_first[i] < 0) u.sup_first[i] = e;
+      u.sup_last[i] = e;
+    }
+  return u;
+}
+
+namespace {
+
+std::vector<int> bisection_cuts(int elems, int levels) {
+  std::vector<int> cuts;
+  for (int l = 1; l <= levels; ++l) {
+    const int blocks = 1 << l, step = elems / blocks;
+    for (int b = 1; b < blocks; b += 2) cuts.push_back(b * step - 1);
+  }
+  std::sort(cuts.begin(), cuts.end());
+  return cuts;
+}
+
+// Separator breakpoints get continuity `target` (multiplicity degree-target)
+// unless already lower.
+Univariate direction(int degree, int elems, const std::vector<int>& seps, int target) {
+  std::vector<int> mult(elems - 1, 1);
+  for (int b : seps) mult[b] = std::max(mult[b], degree - target);
+  return make_univariate(degree, elems, mult);
+}
+
+}  // namespace
+
+VectorSpace build_space(SpaceKind kind, int degree, int elems, int levels) {
+  if (degree < 2) fail(errc::domain, "vector-valued spaces need degree >= 2");
+  if (elems < 2) fail(errc::domain, "need at least 2 elements per direction");
+  if (levels < 0) fail(errc::domain, "negative partition level");
+  if (levels > 0) {
+    if (levels > 30 || elems % (1 << levels) != 0)
+      fail(errc::domain, "element count not divisible by 2^levels");
+    if (elems / (1 << levels) < 2) fail(errc::domain, "macroelements must span >= 2 elements");
+  }
+  VectorSpace vs;
+  vs.kind = kind;
+  vs.degree = degree;
+  vs.elems = elems;
+  vs.levels = levels;
+  vs.separators = bisection_cuts(elems, levels);
+  const Univariate hi = direction(degree, elems, vs.separators, 1);
+  const Univariate lo = direction(degree - 1, elems, vs.separators, 0);
+  if (kind == SpaceKind::curl) {
+    vs.cx = Tensor2{lo, hi};
+    vs.cy = Tensor2{hi, lo};
+  } else {
+    vs.cx = Tensor2{hi, lo};
+    vs.cy = Tensor2{lo, hi};
+  }
+  return vs;
+}
+
+std::vector<int64_t> boundary_mask(const VectorSpace& vs) {
+  std::vector<int64_t> mask;
+  const int64_t nx1 = vs.cx.nx(), ny1 = vs.cx.ny(), nx2 = vs.cy.nx(), ny2 = vs.cy.ny();
+  const int64_t Nx = vs.Nx();
+  if (vs.kind == SpaceKind::curl) {
+    // E x n = 0: x-component on horizontal edges, y-component on vertical ones.
+    for (int64_t i = 0; i < nx1; ++i) {
+      mask.push_back(i);
+      mask.push_back((ny1 - 1) * nx1 + i);
+    }
+    for (int64_t j = 0; j < ny2; ++j) {
+      mask.push_back(Nx + j * nx2);
+      mask.push_back(Nx + j * nx2 + nx2 - 1);
+    }
+  } else {
+    // u . n = 0 on all four (rigid) edges.
+    for (int64_t j = 0; j < ny1; ++j) {
+      mask.push_back(j * nx1);
+      mask.push_back(j * nx1 + nx1 - 1);
+    }
+    for (int64_t i = 0; i < nx2; ++i) {
+      mask.push_back(Nx + i);
+      mask.push_back(Nx + (ny2 - 1) * nx2 + i);
+    }
+  }
+  std::sort(mask.begin(), mask.end());
+  mask.erase(std::unique(mask.begin(), mask.end()), mask.end());
+  return mask;
+}
+
+namespace {
+
+constexpr int kMaxP = 12;
+
+// Gauss-Legendre nodes/weights on [-1,1] (Newton on P_n).
+void gauss_legendre(int n, double* x, double* w) {
+  for (int i = 0; i < n; ++i) {
+    double z = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+    double dp = 1.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= n; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (z * p1 - p0) / (z * z - 1.0);
+      const double dz = p1 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    double p0 = 1.0, p1 = z;
+    for (int k = 2; k <= n; ++k) {
+      const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+      p0 = p1;
+      p1 = p2;
+    }
+    dp = n * (z * p1 - p0) / (z * z - 1.0);
+    x[n - 1 - i] = z;
+    w[n - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+
+// Degree-p B-spline values and first derivatives of the p+1 bases s-p..s at
+// u, from the Cox-de Boor definition (0/0 := 0).
+void basis_eval(const std::vector<double>& U, int p, int s, double u, double* val, double* der) {
+  double N[kMaxP + 2], Nn[kMaxP + 2], Np[kMaxP + 2];
+  N[0] = 1.0;
+  Np[0] = 1.0;
+  for (int k = 1; k <= p; ++k) {
+    if (k == p)
+      for (int r = 0; r < p; ++r) Np[r] = N[r];
+    for (int r = 0; r <= k; ++r) {
+      const int i = s - k + r;
+      double v = 0.0;
+      if (r >= 1) {
+        const double den = U[i + k] - U[i];
+        if (den > 0) v += (u - U[i]) / den * N[r - 1];
+      }
+      if (r <= k - 1) {
+        const double den = U[i + k + 1] - U[i + 1];
+        if (den > 0) v += (U[i + k + 1] - u) / den * N[r];
+      }
+      Nn[r] = v;
+    }
+    for (int r = 0; r <= k; ++r) N[r] = Nn[r];
+  }
+  for (int r = 0; r <= p; ++r) {
+    val[r] = N[r];
+    if (p == 0) {
+      der[r] = 0.0;
+      continue;
+    }
+    const int i = s - p + r;
+    double d = 0.0;
+    if (r >= 1) {
+      const double den = U[i + p] - U[i];
+      if (den > 0) d += p / den * Np[r - 1];
+    }
+    if (r <= p - 1) {
+      const double den = U[i + p + 1] - U[i + 1];
+      if (den > 0) d -= p / den * Np[r];
+    }
+    der[r] = d;
+  }
+}
+
+// Basis tables of one direction: for element e, point q, local basis a.
+struct DirTable {
+  int p = 0, nq = 0;
+  std::vector<double> val, der, wq;  // [e][q][a], [e][q][a], [e][q]
+  void build(const Univariate& u, const double* gx, const double* gw, int nq_) {
+    p = u.degree;
+    nq = nq_;
+    const int ne = u.elems;
+    val.assign(static_cast<size_t>(ne) * nq * (p + 1), 0.0);
+    der.assign(val.size(), 0.0);
+    wq.assign(static_cast<size_t>(ne) * nq, 0.0);
+    for (int e = 0; e < ne; ++e) {
+      const double x0 = static_cast<double>(e) / ne, x1 = static_cast<double>(e + 1) / ne;
+      const double h = x1 - x0;
+      for (int q = 0; q < nq; ++q) {
+        const double x = x0 + 0.5 * (gx[q] + 1.0) * h;
+        const size_t o = (static_cast<size_t>(e) * nq + q) * (p + 1);
+        basis_eval(u.knots, p, u.elem_span[e], x, &val[o], &der[o]);
+        wq[static_cast<size_t>(e) * nq + q] = 0.5 * h * gw[q];
+      }
+    }
+  }
+  const double* v(int e, int q) const { return &val[(static_cast<size_t>(e) * nq + q) * (p + 1)]; }
+  const double* d(int e, int q) const { return &der[(static_cast<size_t>(e) * nq + q) * (p + 1)]; }
+  double w(int e, int q) const { return wq[static_cast<size_t>(e) * nq + q]; }
+};
+
+// First basis index whose support reaches element lo / last reaching hi.
+void overlap_range(const Univariate& u, int lo, int hi, int* first, int* last) {
+  const int nb = u.nbasis();
+  int a = 0;
+  while (a < nb && u.sup_last[a] < lo) ++a;
+  int b = nb - 1;
+  while (b >= 0 && u.sup_first[b] > hi) --b;
+  *first = a;
+  *last = b;
+}
+
+}  // namespace
+
+Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta) {
+  if (vs.degree > kMaxP) fail(errc::domain, "degree too large for assembly tables");
+  Pencil P;
+  P.elems = vs.elems;
+  P.n_full = vs.N();
+  const std::vector<int64_t> mask = boundary_mask(vs);
+  std::vector<int64_t> full_to_free(P.n_full, -1);
+  {
+    size_t mi = 0;
+    for (int64_t g = 0; g < P.n_full; ++g) {
+      if (mi < mask.size() && mask[mi] == g) {
+        ++mi;
+        continue;
+      }
+      full_to_free[g] = static_cast<int64_t>(P.free_to_full.size());
+      P.free_to_full.push_back(g);
+    }
+  }
+  P.n = static_cast<int64_t>(P.free_to_full.size());
+  const Tensor2* comp[2] = {&vs.cx, &vs.cy};
+  const int64_t base[2] = {0, vs.Nx()};
+
+  // Support boxes and shared pattern (all support-overlapping free pairs).
+  P.box.resize(4 * P.n);
+  P.rowptr.assign(P.n + 1, 0);
+  for (int64_t k = 0; k < P.n; ++k) {
+    const int64_t g = P.free_to_full[k];
+    const int c = g >= vs.Nx() ? 1 : 0;
+    const int64_t l = g - base[c];
+    const int i = static_cast<int>(l % comp[c]->nx()), j = static_cast<int>(l / comp[c]->nx());
+    P.box[4 * k + 0] = comp[c]->sx.sup_first[i];
+    P.box[4 * k + 1] = comp[c]->sx.sup_last[i];
+    P.box[4 * k + 2] = comp[c]->sy.sup_first[j];
+    P.box[4 * k + 3] = comp[c]->sy.sup_last[j];
+  }
+  auto row_cols = [&](int64_t k, std::vector<int32_t>& out) {
+    out.clear();
+    const int32_t* b = &P.box[4 * k];
+    for (int c = 0; c < 2; ++c) {
+      int i0, i1, j0, j1;
+      overlap_range(comp[c]->sx, b[0], b[1], &i0, &i1);
+      overlap_range(comp[c]->sy, b[2], b[3], &j0, &j1);
+      for (int j = j0; j <= j1; ++j)
+        for (int i = i0; i <= i1; ++i) {
+          const int64_t f = full_to_free[base[c] + static_cast<int64_t>(j) * comp[c]->nx() + i];
+          if (f >= 0) out.push_back(static_cast<int32_t>(f));
+        }
+    }
+  };
+  {
+    std::vector<int32_t> tmp;
+    for (int64_t k = 0; k < P.n; ++k) {
+      row_cols(k, tmp);
+      P.rowptr[k + 1] = P.rowptr[k] + static_cast<int64_t>(tmp.size());
+    }
+    P.col.resize(P.rowptr[P.n]);
+    const unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nth; ++t)
+      th.emplace_back([&, t] {
+        std::vector<int32_t> loc;
+        for (int64_t k = t; k < P.n; k += nth) {
+          row_cols(k, loc);
+          std::copy(loc.begin(), loc.end(), P.col.begin() + P.rowptr[k]);
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  const int64_t nnz = P.rowptr[P.n];
+  P.K.assign(nnz, 0.0);
+  P.M.assign(nnz, 0.0);
+
+  // Quadrature tables.
+  const int nq = vs.degree + 1;
+  double gx[kMaxP + 1], gw[kMaxP + 1];
+  gauss_legendre(nq, gx, gw);
+  DirTable tab[2][2];  // [component][direction]
+  for (int c = 0; c < 2; ++c) {
+    tab[c][0].build(comp[c]->sx, gx, gw, nq);
+    tab[c][1].build(comp[c]->sy, gx, gw, nq);
+  }
+  const bool curl = vs.kind == SpaceKind::curl;
+  const int ne = vs.elems;
+
+  // Element rows of one colour (stride p+1 in y) share no DOF, so each colour
+  // phase is race-free and the summation order is thread-count independent.
+  auto do_row = [&](int ey, std::vector<double>& Kl, std::vector<double>& Ml,
+                    std::vector<int64_t>& dof, std::vector<double>& vals) {
+    for (int ex = 0; ex < ne; ++ex) {
+      // Local DOFs: component 0 then 1, (a,b) with a fastest.
+      int nloc = 0;
+      int locsz[2];
+      for (int c = 0; c < 2; ++c) {
+        const int px = comp[c]->sx.degree, py = comp[c]->sy.degree;
+        const int fx = comp[c]->sx.first_basis(ex), fy = comp[c]->sy.first_basis(ey);
+        for (int b = 0; b <= py; ++b)
+          for (int a = 0; a <= px; ++a)
+            dof[nloc++] = full_to_free[base[c] + static_cast<int64_t>(fy + b) * comp[c]->nx() + fx + a];
+        locsz[c] = (px + 1) * (py + 1);
+      }
+      std::fill(Kl.begin(), Kl.begin() + nloc * nloc, 0.0);
+      std::fill(Ml.begin(), Ml.begin() + nloc * nloc, 0.0);
+      // vals layout per local dof: value (component), curl/div
+      for (int qy = 0; qy < nq; ++qy)
+        for (int qx = 0; qx < nq; ++qx) {
+          const double w = tab[0][0].w(ex, qx) * tab[0][1].w(ey, qy);
+          int o = 0;
+          for (int c = 0; c < 2; ++c) {
+            const DirTable& TX = tab[c][0];
+            const DirTable& TY = tab[c][1];
+            const double* vx = TX.v(ex, qx);
+            const double* dx = TX.d(ex, qx);
+            const double* vy = TY.v(ey, qy);
+            const double* dy = TY.d(ey, qy);
+            for (int b = 0; b <= TY.p; ++b)
+              for (int a = 0; a <= TX.p; ++a, ++o) {
+                const double val = vx[a] * vy[b];
+                double dd;
+                if (!curl)
+                  dd = c == 0 ? dx[a] * vy[b] : vx[a] * dy[b];  // div
+                else
+                  dd = c == 0 ? -vx[a] * dy[b] : dx[a] * vy[b];  // curl
+                vals[2 * o] = val;
+                vals[2 * o + 1] = dd;
+              }
+          }
+          for (int r = 0; r < nloc; ++r) {
+            const int cr = r < locsz[0] ? 0 : 1;
+            const double vr = w * vals[2 * r], dr = w * vals[2 * r + 1];
+            for (int s = r; s < nloc; ++s) {
+              const int cs = s < locsz[0] ? 0 : 1;
+              const double mm = cr == cs ? vr * vals[2 * s] : 0.0;
+              Kl[r * nloc + s] += dr * vals[2 * s + 1] + mm;
+              Ml[r * nloc + s] += mm;
+            }
+          }
+        }
+      // exact symmetry: mirror the upper triangle
+      for (int r = 0; r < nloc; ++r)
+        for (int s = 0; s < r; ++s) {
+          Kl[r * nloc + s] = Kl[s * nloc + r];
+          Ml[r * nloc + s] = Ml[s * nloc + r];
+        }
+      for (int r = 0; r < nloc; ++r) {
+        const int64_t fr = dof[r];
+        if (fr < 0) continue;
+        const int32_t* cb = P.col.data() + P.rowptr[fr];
+        const int32_t* ce = P.col.data() + P.rowptr[fr + 1];
+        for (int s = 0; s < nloc; ++s) {
+          const int64_t fs = dof[s];
+          if (fs < 0) continue;
+          const int32_t* it = std::lower_bound(cb, ce, static_cast<int32_t>(fs));
+          if (it == ce || *it != fs) fail(errc::assembly, "pattern misses an element pair");
+          const int64_t pos = it - P.col.data();
+          P.K[pos] += Kl[r * nloc + s];
+          P.M[pos] += Ml[r * nloc + s];
+        }
+      }
+    }
+  };
+  const int stride = vs.degree + 1;
+  const unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  for (int colour = 0; colour < stride; ++colour) {
+    std::vector<int> rows;
+    for (int ey = colour; ey < ne; ey += stride) rows.push_back(ey);
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nth; ++t)
+      th.emplace_back([&, t] {
+        const int maxloc = 2 * (vs.degree + 1) * vs.degree;
+        std::vector<double> Kl(maxloc * maxloc), Ml(maxloc * maxloc), vals(2 * maxloc);
+        std::vector<int64_t> dof(maxloc);
+        for (size_t r = t; r < rows.size(); r += nth) do_row(rows[r], Kl, Ml, dof, vals);
+      });
+    for (auto& x : th) x.join();
+  }
+  P.C.resize(nnz);
+  for (int64_t k = 0; k < nnz; ++k) P.C[k] = alpha * P.M[k] + beta * P.K[k];
+  return P;
+}
+
+}  // namespace rqb
