@@ -1,0 +1,112 @@
+// SPDX-License-Identifier: Apache-2.0
+// sparsela drop-in for the reference tree: the SPEC
+// signatures over the reference's own types (rq::SparseMatrix, rq::CostLedger,
+// rq::VectorSpace, rq::Error — proj/include/rigaqep/{sparse,spaces,types}.hpp),
+// implemented inline on top of the B200 C-ABI (include/rq_b200.h). A reference
+// build adds this directory to its include path and links librq_b200.so
+// (INTEGRATION.md). The GPU path is real FP64: complex matrices fail with
+// errc::config (no CPU fallback); complex right-hand sides are solved as two
+// real solves.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "rigaqep/sparse.hpp"
+#include "rigaqep/spaces.hpp"
+#include "rigaqep/types.hpp"
+#include "rq_b200.h"
+
+namespace rq {
+
+namespace b200 {
+inline void check(int rc) {
+  if (rc != 0) fail(static_cast<errc>(rc), std::string("rq_b200: ") + rq_last_error());
+}
+}  // namespace b200
+
+/// Ordering: permutation + front structure handle.
+struct Ordering {
+  std::vector<std::int32_t> perm;  // perm[new] = old (free DOFs)
+  std::string method = "geometric-nested-dissection";
+  std::shared_ptr<rq_symbolic_t> sym;
+};
+
+/// nested_dissection_order(space): geometric ND over the
+/// support boxes of the free DOFs (constrained = sorted eliminated DOF ids).
+inline Ordering nested_dissection_order(const VectorSpace& vs, const std::vector<long>& constrained,
+                                        int leaf = 64) {
+  std::vector<std::int32_t> box;
+  const TensorSpace2D* comp[2] = {&vs.comp_x, &vs.comp_y};
+  long g = 0;
+  std::size_t ci = 0;
+  for (int c = 0; c < 2; ++c)
+    for (int j = 0; j < comp[c]->ny(); ++j)
+      for (int i = 0; i < comp[c]->nx(); ++i, ++g) {
+        if (ci < constrained.size() && constrained[ci] == g) {
+          ++ci;
+          continue;
+        }
+        box.push_back(comp[c]->sx.support_first_elem(i));
+        box.push_back(comp[c]->sx.support_last_elem(i));
+        box.push_back(comp[c]->sy.support_first_elem(j));
+        box.push_back(comp[c]->sy.support_last_elem(j));
+      }
+  const std::int64_t n = static_cast<std::int64_t>(box.size() / 4);
+  rq_symbolic_t* s = nullptr;
+  b200::check(rq_nd_order(n, box.data(), vs.elems, leaf, &s));
+  Ordering o;
+  o.sym.reset(s, rq_symbolic_destroy);
+  o.perm.resize(n);
+  b200::check(rq_symbolic_perm(s, o.perm.data()));
+  return o;
+}
+
+/// Factorization: immutable, device resident, shareable.
+struct Factorization {
+  std::shared_ptr<rq_factor_t> f;
+  long n = 0;
+  std::int64_t nnz_l = 0, nnz_u = 0;
+  double flops = 0;
+};
+
+inline std::vector<double> real_values(const SparseMatrix& a) {
+  if (!a.is_real()) fail(errc::config, "the B200 path factors real matrices only");
+  std::vector<double> v(a.val.size());
+  for (std::size_t k = 0; k < v.size(); ++k) v[k] = a.val[k].real();
+  return v;
+}
+
+/// lu_factorize: one fa operation charged to the ledger.
+inline Factorization lu_factorize(const SparseMatrix& A, const Ordering& ord, CostLedger* ledger) {
+  const std::vector<double> v = real_values(A);
+  rq_factor_t* f = nullptr;
+  b200::check(rq_factor_create(ord.sym.get(), A.n, A.rowptr.data(), A.col.data(), v.data(), &f));
+  Factorization F;
+  F.f.reset(f, rq_factor_destroy);
+  F.n = A.n;
+  rq_symbolic_stats st{};
+  b200::check(rq_symbolic_stats_get(ord.sym.get(), &st));
+  F.nnz_l = st.nnz_l;
+  F.nnz_u = st.nnz_u;
+  F.flops = st.flops_lu;
+  if (ledger) ledger->add_fa(static_cast<std::uint64_t>(st.flops_lu / 2));
+  return F;
+}
+
+/// solve_factored: fb += nnz(L) + nnz(U) per real solve.
+inline std::vector<cdouble> solve_factored(const Factorization& F, const std::vector<cdouble>& rhs,
+                                           CostLedger* ledger) {
+  if (static_cast<long>(rhs.size()) != F.n) fail(errc::dimension, "solve_factored dimension mismatch");
+  std::vector<double> b(2 * F.n), x(2 * F.n);
+  for (long i = 0; i < F.n; ++i) b[i] = rhs[i].real(), b[F.n + i] = rhs[i].imag();
+  b200::check(rq_factor_solve(F.f.get(), b.data(), x.data(), 2));
+  std::vector<cdouble> out(F.n);
+  for (long i = 0; i < F.n; ++i) out[i] = {x[i], x[F.n + i]};
+  if (ledger) ledger->add_fb(static_cast<std::uint64_t>(F.nnz_l + F.nnz_u));
+  return out;
+}
+
+}  // namespace rq

@@ -197,6 +197,7 @@ typedef struct {
   double macs_fa, macs_fb, macs_mv, macs_vv, macs_check, macs_restart;
   double t_total_ms, t_factor_ms, t_solve_ms, t_spmv_ms, t_orth_ms, t_host_ms;
   int64_t launches;
+  double restart_defect; /* max ||H Q - Q T|| / ||H|| over restarts (exactness check) */
 } rq_eigs_info;
 
 /* solve_quadratic: nev eigenpairs of K + lam C + lam^2 M nearest sigma.

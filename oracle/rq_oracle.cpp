@@ -559,8 +559,10 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
   int k = 0, cycles = 0, gp = 0;
   EigOut out;
   std::vector<double> prev;
-  while (cycles < max_restarts) {
+  int pass_cycles = 0;  // max_restarts bounds each pass (main + every guard pass)
+  while (pass_cycles < max_restarts) {
     ++cycles;
+    ++pass_cycles;
     for (int j = k; j < m; ++j) {
       op.apply(V[j].data(), r.data(), L);
       for (int pass = 0; pass < 2; ++pass) {  // CGS2
@@ -659,6 +661,7 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
       }
       prev = d;
       ++gp;
+      pass_cycles = 0;
       deflate = true;
       for (int c = 0; c < nev; ++c) sel[ord[c]] = 1;
     } else {

@@ -76,7 +76,7 @@ class EigsInfo(C.Structure):
                 ("macs_restart", C.c_double), ("t_total_ms", C.c_double),
                 ("t_factor_ms", C.c_double), ("t_solve_ms", C.c_double),
                 ("t_spmv_ms", C.c_double), ("t_orth_ms", C.c_double), ("t_host_ms", C.c_double),
-                ("launches", C.c_int64)]
+                ("launches", C.c_int64), ("restart_defect", C.c_double)]
 
 
 def _sig(name, res, *args):

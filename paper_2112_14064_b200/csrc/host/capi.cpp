@@ -476,6 +476,7 @@ int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, doub
       I.t_orth_ms = r.t_orth_ms;
       I.t_host_ms = 0;
       I.launches = r.launches;
+      I.restart_defect = r.max_restart_defect;
     }
     partial = r.nconv < opts->nev;
   });

@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <numeric>
 #include <sstream>
 
@@ -41,6 +42,8 @@ struct Ritz {
 };
 
 double dist(const cplx& l, double sigma) { return std::abs(l - sigma); }
+
+constexpr double kClusterGap = 1e-4;  // relative Ritz-value gap below which values are one group
 
 }  // namespace
 
@@ -144,7 +147,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
 
   fresh_vector(o.seed, 0, V);
   int k = 0;
-  int cycles = 0, guard_passes = 0;
+  int cycles = 0, guard_passes = 0, pass_cycles = 0;
   bool converged_final = false;
   std::vector<double> prev_guard_dists;
   std::vector<Ritz> final_set, last_cand;
@@ -155,8 +158,11 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   double t_solve = 0, t_orth = 0;
 
   while (true) {
-    if (cycles >= o.max_restarts) break;
+    // max_restarts bounds each Krylov-Schur pass (the main run and every guard
+    // pass restart the count)
+    if (pass_cycles >= o.max_restarts) break;
     ++cycles;
+    ++pass_cycles;
     // ---- Arnoldi steps k .. m-1 ----
     for (int j = k; j < m; ++j) {
       double* vj = V + static_cast<int64_t>(j) * n2;
@@ -234,18 +240,56 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       if (da != db) return da < db;
       return rz[a].lambda.imag() > rz[b].lambda.imag();
     });
-    // ---- convergence: explicit residuals of the nev nearest ----
+    // ---- groups: conjugate pairs + clusters (single linkage, relative gap
+    // 1e-4). Kept sets are unions of whole groups, so they are closed under
+    // conjugation and never split a cluster: the real basis of the kept complex
+    // Schur vectors then spans an invariant subspace to ~eps / 1e-4.
+    std::vector<std::vector<int>> groups;
+    std::vector<int> group_of(m, -1);
+    {
+      std::vector<int> par(m);
+      std::iota(par.begin(), par.end(), 0);
+      std::function<int(int)> find = [&](int x) { return par[x] == x ? x : par[x] = find(par[x]); };
+      for (int i = 0; i < m; ++i)
+        for (int q = i + 1; q < m; ++q) {
+          const cplx a = rz[i].theta, b = rz[q].theta;
+          const double scale = std::max(std::abs(a), std::abs(b));
+          if (std::abs(a - b) <= kClusterGap * scale || std::abs(a - std::conj(b)) <= kClusterGap * scale)
+            par[find(i)] = find(q);
+        }
+      std::vector<int> root_group(m, -1);
+      for (int a = 0; a < m; ++a) {  // groups in wanted order of their best member
+        const int i = order[a];
+        const int r = find(i);
+        if (root_group[r] < 0) {
+          root_group[r] = static_cast<int>(groups.size());
+          groups.push_back({});
+        }
+        groups[root_group[r]].push_back(i);
+        group_of[i] = root_group[r];
+      }
+    }
+    // ---- convergence: explicit residuals of the nev nearest (+ their group mates) ----
     std::vector<int> cand(order.begin(), order.begin() + nev);
+    std::vector<int> chk = cand;
+    {
+      std::vector<int> in(m, 0);
+      for (int i : cand) in[i] = 1;
+      for (int i : cand)
+        for (int q : groups[group_of[i]])
+          if (!in[q]) in[q] = 1, chk.push_back(q);
+    }
+    const int nchk = static_cast<int>(chk.size());
     const bool maybe = std::all_of(cand.begin(), cand.end(),
                                    [&](int i) { return rz[i].est <= o.est_factor * o.tol; });
-    bool all_conv = false;
-    std::vector<double> cres(nev, 1.0);
-    std::vector<int> cblock(nev, 0);
+    bool all_conv = false, mates_conv = false;
+    std::vector<double> cres(nchk, 1.0);
+    std::vector<int> cblock(nchk, 0);
     if (maybe) {
-      // Ritz vectors X = V_m [Re y, Im y] for the candidates (y = Z Y[:, i])
-      std::vector<double> Yr(static_cast<size_t>(m) * 2 * nev);
-      for (int c = 0; c < nev; ++c) {
-        const int i = cand[c];
+      // Ritz vectors X = V_m [Re y, Im y] (y = Z Y[:, i])
+      std::vector<double> Yr(static_cast<size_t>(m) * 2 * nchk);
+      for (int c = 0; c < nchk; ++c) {
+        const int i = chk[c];
         for (int row = 0; row < m; ++row) {
           cplx y = 0.0;
           for (int t = 0; t <= i; ++t) y += Z(row, t) * Y(t, i);
@@ -255,30 +299,28 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       }
       cuda_check(cudaMemcpyAsync(dQ.p, Yr.data(), sizeof(double) * Yr.size(), cudaMemcpyHostToDevice, st),
                  "H2D Y");
-      op.combine(V, m, dQ.as<double>(), m, 2 * nev, dX.as<double>());
-      for (int c = 0; c < nev; ++c) {
-        const Ritz& R = rz[cand[c]];
-        const cplx gam = R.lambda / vs;  // eigenvalue of the scaled pencil
+      op.combine(V, m, dQ.as<double>(), m, 2 * nchk, dX.as<double>());
+      for (int c = 0; c < nchk; ++c) {
+        const cplx gam = rz[chk[c]].lambda / vs;  // eigenvalue of the scaled pencil
         const int blk = std::abs(gam) > 1.0 ? 1 : 0;  // larger-norm block
         cblock[c] = blk;
         const double* xr = dX.as<double>() + static_cast<int64_t>(2 * c) * n2 + blk * n;
-        const double* xi = xr + n2;
-        op.pencil_residual(xr, xi, gam.real(), gam.imag(), dRes.as<double>() + 2 * c);
+        op.pencil_residual(xr, xr + n2, gam.real(), gam.imag(), dRes.as<double>() + 2 * c);
       }
-      std::vector<double> rr(2 * nev);
-      cuda_check(cudaMemcpyAsync(rr.data(), dRes.p, sizeof(double) * 2 * nev, cudaMemcpyDeviceToHost, st),
+      std::vector<double> rr(2 * nchk);
+      cuda_check(cudaMemcpyAsync(rr.data(), dRes.p, sizeof(double) * 2 * nchk, cudaMemcpyDeviceToHost, st),
                  "D2H res");
       cuda_check(cudaStreamSynchronize(st), "sync");
-      all_conv = true;
-      for (int c = 0; c < nev; ++c) {
-        const cplx gam = rz[cand[c]].lambda / vs;
-        const double ag = std::abs(gam);
+      all_conv = mates_conv = true;
+      for (int c = 0; c < nchk; ++c) {
+        const double ag = std::abs(rz[chk[c]].lambda / vs);
         const double den = (norms1[0] + ag * norms1[1] + ag * ag * norms1[2]) * std::sqrt(rr[2 * c + 1]);
         cres[c] = den > 0 ? std::sqrt(rr[2 * c]) / den : 1.0;
-        if (!(cres[c] <= o.tol)) all_conv = false;
+        if (!(cres[c] <= o.tol)) (c < nev ? all_conv : mates_conv) = false;
       }
-      L.n_check += 3 * nev;
-      L.macs_check += 6.0 * nnz * nev;
+      mates_conv = mates_conv && all_conv;
+      L.n_check += 3 * nchk;
+      L.macs_check += 6.0 * nnz * nchk;
     }
     int nconv_now = 0;
     for (int c = 0; c < nev && maybe; ++c)
@@ -286,17 +328,16 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     res.nconv = std::max(res.nconv, nconv_now);
     last_cand.clear();
     for (int c = 0; c < nev; ++c) last_cand.push_back(rz[cand[c]]);
-    last_res = cres;
+    last_res.assign(cres.begin(), cres.begin() + nev);
 
     auto capture_set = [&]() {
       final_set.clear();
-      final_res.assign(cres.begin(), cres.end());
-      final_block.assign(cblock.begin(), cblock.end());
+      final_res.assign(cres.begin(), cres.begin() + nev);
+      final_block.assign(cblock.begin(), cblock.begin() + nev);
       for (int c = 0; c < nev; ++c) final_set.push_back(rz[cand[c]]);
       if (o.want_vectors) {
         final_vecs_re.assign(static_cast<size_t>(n) * nev, 0.0);
         final_vecs_im.assign(static_cast<size_t>(n) * nev, 0.0);
-        std::vector<double> buf(n);
         for (int c = 0; c < nev; ++c) {
           const double* xr = dX.as<double>() + static_cast<int64_t>(2 * c) * n2 + cblock[c] * n;
           cuda_check(cudaMemcpy(final_vecs_re.data() + static_cast<size_t>(c) * n, xr,
@@ -313,7 +354,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       }
     };
 
-    // ---- decide: done / guard restart / normal restart ----
+    // ---- decide: done / guard (deflated) restart / normal restart ----
     std::vector<int> sel(m, 0);
     int p = 0;
     bool deflate = false;
@@ -329,37 +370,40 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         converged_final = true;
         break;
       }
-      prev_guard_dists = dists;
-      ++guard_passes;
-      deflate = true;
-      for (int c = 0; c < nev; ++c) sel[cand[c]] = 1;
-    } else {
-      for (int c = 0; c < std::min(keep_target, m - 1); ++c) sel[order[c]] = 1;
-    }
-    // conjugation closure of the selection
-    {
-      std::vector<int> used(m, 0);
-      for (int i = 0; i < m; ++i) used[i] = sel[i];
-      for (int i = 0; i < m; ++i) {
-        if (!sel[i]) continue;
-        const cplx th = rz[i].theta;
-        if (std::abs(th.imag()) <= 1e-10 * std::abs(th)) continue;
-        // find partner: closest to conj(theta) among the rest
-        int best = -1;
-        double bd = 1e300;
-        for (int q = 0; q < m; ++q) {
-          if (q == i) continue;
-          const double d = std::abs(rz[q].theta - std::conj(th));
-          if (d < bd) bd = d, best = q;
-        }
-        if (best >= 0 && !sel[best] && bd <= 1e-6 * std::abs(th)) sel[best] = 1;
+      if (mates_conv && nchk <= m - 1) {
+        // every kept direction is converged: deflate them (b = 0) and restart
+        // the Krylov space from a fresh seeded vector (SPEC.md:457 fallback)
+        prev_guard_dists = dists;
+        ++guard_passes;
+        pass_cycles = 0;
+        deflate = true;
+        for (int i : chk) sel[i] = 1;
+        p = nchk;
       }
     }
-    for (int i = 0; i < m; ++i) p += sel[i];
-    if (p >= m) {
-      // keep at least one new direction: drop the farthest selected pair
-      for (int c = m - 1; c >= 0 && p >= m; --c)
-        if (sel[order[c]]) sel[order[c]] = 0, --p;
+    if (!deflate) {
+      for (const auto& g : groups) {
+        if (p >= keep_target || p + static_cast<int>(g.size()) > m - 1) break;
+        for (int i : g) sel[i] = 1;
+        p += static_cast<int>(g.size());
+      }
+      if (p == 0) {  // one cluster fills the whole space: fall back to conjugate pairs
+        for (int a = 0; a < m && p < keep_target; ++a) {
+          const int i = order[a];
+          if (sel[i]) continue;
+          int partner = -1;
+          double bd = 1e300;
+          if (std::abs(rz[i].theta.imag()) > 1e-12 * std::abs(rz[i].theta))
+            for (int q = 0; q < m; ++q)
+              if (q != i && !sel[q]) {
+                const double d = std::abs(rz[q].theta - std::conj(rz[i].theta));
+                if (d < bd) bd = d, partner = q;
+              }
+          if (p + 1 + (partner >= 0) > m - 1) break;
+          sel[i] = 1, ++p;
+          if (partner >= 0) sel[partner] = 1, ++p;
+        }
+      }
     }
     // ---- restart: reorder Schur form, real basis of the kept directions ----
     CMat Tr = T, Zr = Z;
@@ -383,6 +427,18 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         for (int t = 0; t < m; ++t) s += Qp[t + static_cast<size_t>(i) * m] * HQ[t + static_cast<size_t>(c) * m];
         Tp[i + static_cast<size_t>(c) * p] = s;
       }
+    {
+      // invariance defect ||H Q_p - Q_p T_p|| / ||H|| (exact restart needs ~eps)
+      double dmax = 0, hmax = 0;
+      for (double x : Hm) hmax = std::max(hmax, std::fabs(x));
+      for (int c = 0; c < p; ++c)
+        for (int i = 0; i < m; ++i) {
+          double s = HQ[i + static_cast<size_t>(c) * m];
+          for (int t = 0; t < p; ++t) s -= Qp[i + static_cast<size_t>(t) * m] * Tp[t + static_cast<size_t>(c) * p];
+          dmax = std::max(dmax, std::fabs(s));
+        }
+      res.max_restart_defect = std::max(res.max_restart_defect, dmax / std::max(hmax, 1e-300));
+    }
     cuda_check(cudaMemcpyAsync(dQ.p, Qp.data(), sizeof(double) * m * p, cudaMemcpyHostToDevice, st), "H2D Q");
     op.combine(V, m, dQ.as<double>(), m, p, V2);
     L.n_restart += 1;

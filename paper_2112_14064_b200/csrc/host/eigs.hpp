@@ -40,6 +40,7 @@ struct EigsResult {
   std::vector<double> vec_re, vec_im;  // n x nev column-major
   int64_t launches = 0;
   double t_total_ms = 0, t_solve_ms = 0, t_orth_ms = 0;
+  double max_restart_defect = 0;  // max ||H Q - Q T|| / ||H|| over restarts
 };
 
 // norms1 = {||K||_1, ||C||_1, ||M||_1} of the (scaled) pencil used by the

@@ -1,0 +1,258 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle on the
+same seeded inputs, plus size-independent properties at larger sizes.
+
+Tolerances (floating point, BASELINE north star): eigenvalues relative 1e-8,
+pencil residuals <= 1e-10; factor entries / solves relative 1e-10 against the
+oracle (both are backward-stable FP64 LU with the same pivot sequence; the
+difference is summation order, bounded by cond(A) * eps); integer work (pivot
+sequences, orderings) bit-exact.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2112_14064_b200 as rq
+
+pytestmark = pytest.mark.gpu
+
+SIGMA = -0.5
+
+
+def key(z):
+    return (round(abs(z - SIGMA), 7), -np.sign(z.imag), round(z.real, 7))
+
+
+def sorted_lams(lams):
+    return np.array(sorted(lams, key=key))
+
+
+class Tiny:
+    def __init__(self, A):
+        A = np.asarray(A, float)
+        n = A.shape[0]
+        self.n, self.elems = n, 1
+        self.rowptr = np.arange(0, n * n + 1, n, dtype=np.int64)
+        self.col = np.tile(np.arange(n, dtype=np.int32), n)
+        self.val = A.ravel()
+        self.box = np.zeros((n, 4), np.int32)
+
+
+def dense_factor(A):
+    t = Tiny(A)
+    o = rq.Ordering(t.n, t.box, 1)
+    return rq.lu_factorize((t.rowptr, t.col, t.val), o), o
+
+
+# --------------------------------------------------------------------------- factor
+def test_lu_known_answer_3x3():
+    A = [[4, 3, 0], [6, 3, 1], [0, 1, 2]]
+    f, o = dense_factor(A)
+    F, ipiv, ld = f.front(0)
+    assert list(ipiv) == [0, 1, 2] and f.info()["swaps"] == 0
+    np.testing.assert_allclose(np.tril(F[:3, :3], -1), [[0, 0, 0], [1.5, 0, 0], [0, -2 / 3, 0]], atol=1e-15)
+    np.testing.assert_allclose(np.triu(F[:3, :3]), [[4, 3, 0], [0, -1.5, 1], [0, 0, 8 / 3]], atol=1e-15)
+    np.testing.assert_allclose(np.asarray(A) @ f.solve(np.array([1.0, 2, 3])), [1, 2, 3], atol=1e-14)
+
+
+def test_identity_and_spd50():
+    f, _ = dense_factor(np.eye(5))
+    x = np.arange(5.0)
+    np.testing.assert_array_equal(f.solve(x), x)
+    rng = np.random.default_rng(0)
+    B = rng.standard_normal((50, 50))
+    A = B @ B.T + 50 * np.eye(50)
+    f, _ = dense_factor(A)
+    b = rng.standard_normal(50)
+    assert np.linalg.norm(A @ f.solve(b) - b) / np.linalg.norm(b) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [40, 170, 700, 1500])
+def test_dense_pivoting_matches_oracle(n):
+    """Single front through the SMEM (n<=160) and blocked/cluster (n>160) paths:
+    pivot sequence bit-exact, L\\U entries vs the oracle."""
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n))
+    A[np.arange(n), np.arange(n)] *= 0.05  # force threshold swaps
+    f, _ = dense_factor(A)
+    F, ipiv, ld = f.front(0)
+    t = Tiny(A)
+    of = oracle.Factor(n, t.rowptr, t.col, t.val, t.box, 1)
+    Fo, ipo, _ = of.front(0, n, n)
+    assert np.array_equal(ipiv, ipo)
+    assert f.info()["swaps"] == of.swaps > 0
+    err = np.max(np.abs(F[:n, :n] - Fo.real)) / np.max(np.abs(Fo))
+    assert err <= 1e-11
+    b = rng.standard_normal(n)
+    x = f.solve(b)
+    assert np.linalg.norm(A @ x - b) <= 1e-11 * np.linalg.norm(A, 1) * np.linalg.norm(x)
+
+
+def test_singular_is_reported():
+    A = np.ones((4, 4))
+    with pytest.raises(rq.RqError) as e:
+        dense_factor(A)
+    assert e.value.category == "singular"
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_riga", "cfg2_iga"])
+def test_multifrontal_vs_oracle(name):
+    P = rq.baseline_config(name)
+    o = rq.nested_dissection_order(P)
+    Q = P.q_values(SIGMA)
+    f = rq.lu_factorize((P.rowptr, P.col, Q), o)
+    of = oracle.Factor(P.n, P.rowptr, P.col, Q, P.box, P.elems)
+    # every front: pivots bit-exact, factor entries within 1e-10 relative
+    worst = 0.0
+    for fr in range(0, len(o.nf), max(1, len(o.nf) // 40)):
+        nf, npv = int(o.nf[fr]), int(o.npiv[fr])
+        F, ipiv, _ = f.front(fr)
+        Fo, ipo, rows = of.front(fr, nf, npv)
+        assert np.array_equal(rows, o.front_rows(fr))
+        assert np.array_equal(ipiv, ipo)
+        # compare the factor part (L and U panels)
+        mask = np.zeros((nf, nf), bool)
+        mask[:, :npv] = True
+        mask[:npv, :] = True
+        d = np.max(np.abs((F[:nf, :nf] - Fo.real)[mask])) / max(np.max(np.abs(Fo.real[mask])), 1e-300)
+        worst = max(worst, d)
+    assert worst <= 1e-10
+    rng = np.random.default_rng(7)
+    b = rng.standard_normal((P.n, 3))
+    x = f.solve(b)
+    xo = np.stack([of.solve(b[:, i]).real for i in range(3)], 1)
+    assert np.max(np.abs(x - xo)) <= 1e-9 * np.max(np.abs(xo))
+    A = P.to_scipy("K") + SIGMA * P.to_scipy("C") + SIGMA ** 2 * P.to_scipy("M")
+    assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) <= 1e-10
+
+
+def test_refactor_same_pattern(cfg1):
+    o = rq.nested_dissection_order(cfg1)
+    f = rq.lu_factorize((cfg1.rowptr, cfg1.col, cfg1.q_values(SIGMA)), o)
+    Q2 = cfg1.q_values(-1.5)
+    f.refactor(Q2)
+    A = cfg1.to_scipy("K") - 1.5 * cfg1.to_scipy("C") + 2.25 * cfg1.to_scipy("M")
+    b = np.ones(cfg1.n)
+    assert np.linalg.norm(A @ f.solve(b) - b) / np.linalg.norm(b) <= 1e-10
+
+
+# --------------------------------------------------------------------------- operator
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_riga"])
+def test_apply_spmv_binner_vs_oracle(name):
+    P = rq.baseline_config(name)
+    op = rq.build_operator(P, SIGMA)
+    E = oracle.Eig(P, SIGMA)
+    rng = np.random.default_rng(3)
+    v = rng.uniform(-1, 1, 2 * P.n)
+    r = op.apply(v)
+    ro = E.apply(v).real
+    assert np.max(np.abs(r - ro)) <= 1e-9 * np.max(np.abs(ro))
+    x = rng.standard_normal(P.n)
+    for w in "KCM":
+        y = op.spmv(w, x)
+        ys = P.to_scipy(w) @ x
+        assert np.max(np.abs(y - ys)) <= 1e-13 * np.max(np.abs(ys))
+    y = rng.standard_normal(2 * P.n)
+    bi = op.b_inner(v, y)
+    ref = v[:P.n] @ y[:P.n] + v[P.n:] @ (P.to_scipy("M") @ y[P.n:])
+    assert abs(bi - ref) <= 1e-12 * abs(ref) + 1e-14
+
+
+def test_arnoldi_invariants(cfg1):
+    """Arnoldi identity and B-orthonormality <= 1e-8."""
+    op = rq.build_operator(cfg1, SIGMA)
+    n = cfg1.n
+    v1 = np.random.default_rng(0).uniform(-1, 1, 2 * n)
+    m = 21
+    V, H = op.arnoldi(v1, m)
+    Mm = cfg1.to_scipy("M")
+    BV = np.concatenate([V[:, :n], (Mm @ V[:, n:].T).T], 1)
+    G = V @ BV.T
+    assert np.max(np.abs(G - np.eye(m + 1))) <= 1e-8
+    SV = np.stack([op.apply(V[j]) for j in range(m)])
+    R = SV.T - V.T @ H
+    assert np.max(np.abs(R)) <= 1e-8 * np.max(np.abs(H))
+    assert np.allclose(np.tril(H, -2), 0)
+
+
+# --------------------------------------------------------------------------- eigensolve
+def test_eigs_cfg1_vs_oracle(cfg1):
+    op = rq.build_operator(cfg1, SIGMA)
+    pairs = op.solve_quadratic(10, eps=1e-10, seed=0, vectors=True)
+    lam = np.array([p.lam for p in pairs])
+    res = np.array([p.residual for p in pairs])
+    E = oracle.Eig(cfg1, SIGMA)
+    lo, ro = E.solve_quadratic(10, tol=1e-10, seed=0)
+    a, b = sorted_lams(lam), sorted_lams(lo)
+    assert np.max(np.abs(a - b) / np.abs(b)) <= 1e-8
+    assert np.all(res <= 1e-10)
+    ref = -0.03 + 1j * np.sqrt(0.9991)  # closed form of the degenerate cluster
+    assert np.all(np.minimum(np.abs(lam - ref), np.abs(lam - np.conj(ref))) <= 1e-8 * abs(ref))
+    # eigenvector residual recomputed on the host
+    K, C, M = (cfg1.to_scipy(w) for w in "KCM")
+    for p in pairs[:4]:
+        u = p.u
+        r = K @ u + p.lam * (C @ u) + p.lam ** 2 * (M @ u)
+        nrm = lambda A: abs(A).sum(0).max()  # noqa: E731
+        den = (nrm(K) + abs(p.lam) * nrm(C) + abs(p.lam) ** 2 * nrm(M)) * np.linalg.norm(u)
+        assert np.linalg.norm(r) / den <= 1e-10
+    info = op.last_info
+    assert info["n_fa"] == 1 and info["restart_defect"] <= 1e-10
+    # counter laws: one solve per Arnoldi step, 4..6 mv per step
+    assert 4 <= info["n_mv"] / info["n_fb"] <= 7
+
+
+def test_eigs_nondegenerate_vs_oracle_and_scipy():
+    """Perturbed damping breaks the cluster: parity of a generic spectrum."""
+    from scipy.linalg import eigvals
+    P = rq.assemble(rq.DIV, 2, 8, 0)
+    diag = np.array([P.rowptr[i] + np.searchsorted(P.col[P.rowptr[i]:P.rowptr[i + 1]], i)
+                     for i in range(P.n)])
+    rng = np.random.default_rng(11)
+    P.C = P.C.copy()
+    P.C[diag] += 0.3 * rng.random(P.n)
+    op = rq.build_operator(P, SIGMA)
+    pairs = op.solve_quadratic(8, eps=1e-10)
+    lam = np.array([p.lam for p in pairs])
+    E = oracle.Eig(P, SIGMA, C_=P.C)
+    lo, _ = E.solve_quadratic(8, tol=1e-10)
+    assert np.max(np.abs(sorted_lams(lam) - sorted_lams(lo)) / np.abs(lo)) <= 1e-8
+    n = P.n
+    Kd, Cd, Md = (P.to_scipy(w).toarray() for w in "KCM")
+    Z, I = np.zeros((n, n)), np.eye(n)
+    w = eigvals(np.block([[Z, I], [-Kd, -Cd]]), np.block([[I, Z], [Z, Md]]))
+    w = w[np.argsort(np.abs(w - SIGMA))][:8]
+    for x in lam:
+        assert np.min(np.abs(w - x)) <= 1e-8 * abs(x)
+
+
+def test_eigs_cfg2_riga_vs_oracle(cfg2r):
+    op = rq.build_operator(cfg2r, SIGMA)
+    pairs = op.solve_quadratic(20, eps=1e-10, max_restarts=400)
+    lam = np.array([p.lam for p in pairs])
+    E = oracle.Eig(cfg2r, SIGMA)
+    lo, _ = E.solve_quadratic(20, tol=1e-10, max_restarts=400)
+    assert np.max(np.abs(sorted_lams(lam) - sorted_lams(lo)) / np.abs(lo)) <= 1e-8
+    assert max(p.residual for p in pairs) <= 1e-10
+
+
+def test_scaling_does_not_change_spectrum(cfg1):
+    a = rq.build_operator(cfg1, SIGMA, scaling=False).solve_quadratic(6)
+    b = rq.build_operator(cfg1, SIGMA, scaling=True).solve_quadratic(6)
+    la, lb = sorted_lams([p.lam for p in a]), sorted_lams([p.lam for p in b])
+    assert np.max(np.abs(la - lb) / np.abs(la)) <= 1e-6
+
+
+# --------------------------------------------------------------------------- larger sizes
+@pytest.mark.parametrize("name", ["cfg3_riga", "cfg3_iga"])
+def test_cfg3_solve_residual_and_cluster(name):
+    P = rq.baseline_config(name)
+    op = rq.build_operator(P, SIGMA)
+    fac = rq.lu_factorize((P.rowptr, P.col, P.q_values(SIGMA)), op.ordering)
+    A = P.to_scipy("K") + SIGMA * P.to_scipy("C") + SIGMA ** 2 * P.to_scipy("M")
+    b = np.random.default_rng(1).standard_normal(P.n)
+    assert np.linalg.norm(A @ fac.solve(b) - b) / np.linalg.norm(b) <= 1e-10
+    pairs = op.solve_quadratic(10, eps=1e-10, max_restarts=400)
+    ref = -0.03 + 1j * np.sqrt(0.9991)
+    lam = np.array([p.lam for p in pairs])
+    assert np.all(np.minimum(np.abs(lam - ref), np.abs(lam - np.conj(ref))) <= 1e-8 * abs(ref))
+    assert max(p.residual for p in pairs) <= 1e-10

@@ -1,0 +1,158 @@
+"""Spaces, boundary masks, assembled pattern: pinned against the reference's own
+spaces code (oracle/_ref, built from /root/reference) and the paper's numbers."""
+import numpy as np
+import pytest
+
+import paper_2112_14064_b200 as rq
+from paper_2112_14064_b200 import pencil as pen
+
+
+def ref_or_skip():
+    import oracle
+    r = oracle.ref()
+    if r is None:
+        pytest.skip("oracle/_ref not built (reference sources absent)")
+    return r
+
+
+def ref_space(kind, p, ne, L):
+    import ctypes as C
+    r = ref_or_skip()
+    n = C.c_int64()
+    nm = C.c_int64()
+    assert r.ref_space(kind, p, ne, L, C.byref(n), None, None, C.byref(nm)) == 0
+    box = np.zeros(4 * n.value, np.int32)
+    mask = np.zeros(nm.value, np.int64)
+    assert r.ref_space(kind, p, ne, L, C.byref(n), box.ctypes.data_as(C.c_void_p),
+                       mask.ctypes.data_as(C.c_void_p), C.byref(nm)) == 0
+    return n.value, box.reshape(-1, 4), mask
+
+
+def full_pattern_nnz(box):
+    # ordered pairs whose tensor supports share an element
+    x0, x1, y0, y1 = (box[:, i][:, None] for i in range(4))
+    ov = (x0 <= box[:, 1][None, :]) & (x1 >= box[:, 0][None, :]) & \
+         (y0 <= box[:, 3][None, :]) & (y1 >= box[:, 2][None, :])
+    return int(ov.sum())
+
+
+def test_paper_dimensions():
+    # PAPER.md:357,373 H(curl) p=4 ne=64: N = 9,112 (IGA), 10,804 (rIGA 16x16 macros)
+    for L, N in ((0, 9112), (2, 10804)):
+        (a, b), (c, d) = pen.space_dims(rq.CURL, 4, 64, L)
+        assert a * b + c * d == N
+
+
+@pytest.mark.parametrize("L,nnz", [(0, 1090240), (2, 1217968)])
+def test_paper_pattern_nnz(L, nnz):
+    # union pattern nnz of the full space
+    n, box, _ = ref_space(0, 4, 64, L)
+    assert full_pattern_nnz(box) == nnz
+
+
+@pytest.mark.parametrize("kind,p,ne,L", [(rq.DIV, 2, 32, 0), (rq.DIV, 3, 16, 2), (rq.CURL, 4, 16, 1),
+                                         (rq.CURL, 2, 8, 0), (rq.DIV, 3, 64, 3)])
+def test_supports_and_mask_match_reference(kind, p, ne, L):
+    n, box, mask = ref_space(kind, p, ne, L)
+    assert np.array_equal(pen.boundary_mask(kind, p, ne, L), mask)
+    P = rq.assemble(kind, p, ne, L)
+    assert P.n_full == n and P.n == n - mask.size
+    assert np.array_equal(P.box, box[P.free_to_full])
+    assert np.array_equal(np.setdiff1d(np.arange(n), mask), P.free_to_full)
+
+
+@pytest.mark.parametrize("name,nfull,nfree,nnz", [
+    ("cfg1", 2244, 2112, 61628),
+    ("cfg2_iga", 8844, 8580, 581976),
+    ("cfg2_riga", 10804, 10512, 669308),
+])
+def test_config_sizes(name, nfull, nfree, nnz):
+    P = rq.baseline_config(name)
+    assert (P.n_full, P.n, P.nnz) == (nfull, nfree, nnz)
+
+
+def test_p2_riga_equals_iga():
+    # at p=2 the separator rule is a no-op
+    a = rq.assemble(rq.CURL, 2, 16, 0)
+    b = rq.assemble(rq.CURL, 2, 16, 2)
+    assert a.n == b.n and np.array_equal(a.col, b.col) and np.array_equal(a.K, b.K)
+
+
+def test_assembly_properties(cfg1):
+    import scipy.sparse as sp
+    K, M, C = cfg1.to_scipy("K"), cfg1.to_scipy("M"), cfg1.to_scipy("C")
+    assert abs(K - K.T).max() == 0.0 and abs(M - M.T).max() == 0.0
+    assert abs(C - (0.05 * M + 0.01 * K)).max() < 1e-15 * abs(K).max()
+    # M SPD: smallest eigenvalue positive (dense, small mesh)
+    Ms = rq.assemble(rq.DIV, 2, 6).to_scipy("M").toarray()
+    assert np.linalg.eigvalsh(Ms).min() > 0
+    # sorted, unique column indices per row
+    for r in range(0, cfg1.n, 97):
+        c = cfg1.col[cfg1.rowptr[r]:cfg1.rowptr[r + 1]]
+        assert np.all(np.diff(c) > 0)
+    del sp
+
+
+def test_assembly_against_independent_quadrature():
+    """K, M of a small H(div) space vs an independent scipy-BSpline assembly."""
+    from scipy.interpolate import BSpline
+    p, ne = 2, 4
+    P = rq.assemble(rq.DIV, p, ne, 0)
+
+    def knots(deg):
+        return np.r_[np.zeros(deg), np.linspace(0, 1, ne + 1), np.ones(deg)]
+
+    def basis(deg):
+        t = knots(deg)
+        nb = len(t) - deg - 1
+        return [BSpline(t, np.eye(nb)[i], deg, extrapolate=False) for i in range(nb)]
+
+    hi, lo = basis(p), basis(p - 1)
+    # fine tensor Gauss rule per element (exact for the polynomial integrands)
+    g, w = np.polynomial.legendre.leggauss(8)
+    xs, ws = [], []
+    for e in range(ne):
+        a, b = e / ne, (e + 1) / ne
+        xs.append(a + (g + 1) * (b - a) / 2)
+        ws.append(w * (b - a) / 2)
+    xs, ws = np.concatenate(xs), np.concatenate(ws)
+
+    def ev(bs, x, d=0):
+        out = np.zeros((len(bs), len(x)))
+        for i, bb in enumerate(bs):
+            f = bb.derivative(d) if d else bb
+            v = f(x)
+            out[i] = np.nan_to_num(v)
+        return out
+
+    Hx, Hxd, Lx = ev(hi, xs), ev(hi, xs, 1), ev(lo, xs)
+    # x-comp: hi(x) lo(y); y-comp: lo(x) hi(y); index j*nx + i
+    nxh, nxl = len(hi), len(lo)
+    phis = []
+    for j in range(nxl):
+        for i in range(nxh):
+            phis.append(("x", i, j))
+    for j in range(nxh):
+        for i in range(nxl):
+            phis.append(("y", i, j))
+    W = np.outer(ws, ws)
+
+    def fields(ph):
+        c, i, j = ph
+        if c == "x":
+            v = np.outer(Hx[i], Lx[j])
+            d = np.outer(Hxd[i], Lx[j])
+            return v, np.zeros_like(v), d
+        v = np.outer(Lx[i], Hx[j])
+        d = np.outer(Lx[i], Hxd[j])
+        return np.zeros_like(v), v, d
+
+    F = [fields(phis[g]) for g in P.free_to_full]
+    Kd = P.to_scipy("K").toarray()
+    Md = P.to_scipy("M").toarray()
+    for a in range(0, P.n, 3):
+        for b in range(0, P.n, 5):
+            m = np.sum(W * (F[a][0] * F[b][0] + F[a][1] * F[b][1]))
+            k = np.sum(W * F[a][2] * F[b][2]) + m
+            assert abs(Md[a, b] - m) < 1e-13
+            assert abs(Kd[a, b] - k) < 1e-11
