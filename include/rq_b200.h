@@ -47,6 +47,9 @@ enum {
 
 const char* rq_last_error(void);
 const char* rq_version(void);
+/* Select the CUDA device used by handles created afterwards on this thread
+ * (one process per GPU: rank r calls rq_set_device(local_rank)). */
+int rq_set_device(int device);
 
 /* ------------------------------------------------------------------------ */
 /* Input construction (host): spaces + BASELINE assembly.                   */
@@ -149,6 +152,11 @@ int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs);
  * Schur complement, ld = *ld_out; ipiv[npiv] local swap sequence. */
 int rq_factor_front_export(const rq_factor_t* f, int64_t front, double* dense, int32_t* ipiv,
                            int64_t* ld_out);
+/* Profiling run (not for timed steps): one un-graphed factorization with CUDA
+ * events around every launch. Per kernel class {0 scatter, 1 extend_add,
+ * 2 front_lu_smem, 3 panel_lu, 4 panel_apply, 5 schur_dmma}: device ms,
+ * launches, algorithmic work (real flops; bytes for classes 0-1). */
+int rq_factor_profile(rq_factor_t* f, double* ms, int64_t* launches, double* work);
 void rq_factor_destroy(rq_factor_t* f);
 
 /* ------------------------------------------------------------------------ */
@@ -178,6 +186,11 @@ int rq_operator_spmv(rq_operator_t* op, int which, const double* x, double* y);
  * V: (m+1) x 2n row-major, H: (m+1) x m column-major. */
 int rq_operator_arnoldi(rq_operator_t* op, const double* v1, int m, double* V, double* H);
 rq_factor_t* rq_operator_factor(rq_operator_t* op); /* borrowed */
+/* Device time per call (CUDA events, device-resident buffers, after warm-up):
+ * what = 0 apply_operator, 1 solve_factored, 2 fused C/M SpMV, 3 CGS GEMV-T
+ * over `param` basis vectors, 4 GEMV-N over `param` vectors, 5 numeric
+ * factorization (graph replay), 6 M SpMV. */
+int rq_operator_time(rq_operator_t* op, int what, int iters, int param, double* ms_per_call);
 void rq_operator_destroy(rq_operator_t* op);
 
 typedef struct {

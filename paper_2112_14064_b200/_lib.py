@@ -88,6 +88,7 @@ def _sig(name, res, *args):
 
 _sig("rq_last_error", C.c_char_p)
 _sig("rq_version", C.c_char_p)
+_sig("rq_set_device", C.c_int, C.c_int)
 _sig("rq_pencil_assemble", C.c_int, C.POINTER(SpaceDesc), C.POINTER(vp))
 _sig("rq_pencil_dims", C.c_int, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64))
 _sig("rq_pencil_csr", C.c_int, vp, i64p, i32p, f64p, f64p, f64p)
@@ -107,6 +108,7 @@ _sig("rq_factor_refactor", C.c_int, vp, f64p)
 _sig("rq_factor_get_info", C.c_int, vp, C.POINTER(FactorInfo))
 _sig("rq_factor_solve", C.c_int, vp, f64p, f64p, C.c_int)
 _sig("rq_factor_front_export", C.c_int, vp, C.c_int64, vp, vp, C.POINTER(C.c_int64))
+_sig("rq_factor_profile", C.c_int, vp, f64p, i64p, f64p)
 _sig("rq_factor_destroy", None, vp)
 _sig("rq_operator_create", C.c_int, C.c_int64, i64p, i32p, f64p, f64p, f64p, vp,
      C.POINTER(OperatorOpts), C.POINTER(vp))
@@ -117,18 +119,21 @@ _sig("rq_operator_spmv", C.c_int, vp, C.c_int, f64p, f64p)
 _sig("rq_operator_arnoldi", C.c_int, vp, f64p, C.c_int, vp, vp)
 _sig("rq_operator_factor", vp, vp)
 _sig("rq_operator_destroy", None, vp)
+_sig("rq_operator_time", C.c_int, vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double))
 _sig("rq_eigs_run", C.c_int, vp, C.POINTER(EigsOpts), vp, vp, vp, vp, vp, C.POINTER(EigsInfo))
 _sig("rq_eigs_ledger_json", C.c_int, vp, C.c_char_p, C.c_size_t)
 
 # every symbol include/rq_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = [
-    "rq_last_error", "rq_version", "rq_pencil_assemble", "rq_pencil_dims", "rq_pencil_csr",
+    "rq_last_error", "rq_version", "rq_set_device", "rq_pencil_assemble", "rq_pencil_dims", "rq_pencil_csr",
     "rq_pencil_supports", "rq_pencil_destroy", "rq_space_dims", "rq_space_boundary_mask",
     "rq_nd_order", "rq_symbolic_stats_get", "rq_symbolic_perm", "rq_symbolic_fronts",
     "rq_symbolic_front_rows", "rq_symbolic_destroy", "rq_factor_create", "rq_factor_refactor",
-    "rq_factor_get_info", "rq_factor_solve", "rq_factor_front_export", "rq_factor_destroy",
+    "rq_factor_get_info", "rq_factor_solve", "rq_factor_front_export", "rq_factor_profile",
+    "rq_factor_destroy",
     "rq_operator_create", "rq_operator_varsigma", "rq_operator_apply", "rq_operator_b_inner",
     "rq_operator_spmv", "rq_operator_arnoldi", "rq_operator_factor", "rq_operator_destroy",
+    "rq_operator_time",
     "rq_eigs_run", "rq_eigs_ledger_json",
 ]
 

@@ -577,8 +577,10 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
   d_qdst.upload(dst.data(), sizeof(int64_t) * nnz, stream);
   d_rows.upload(sym.rows.data(), sizeof(int32_t) * sym.rows.size(), stream);
   d_fronts.upload(fronts_h.data(), sizeof(FrontDev) * fronts_h.size(), stream);
-  d_inv.upload(inv.data(), sizeof(int32_t) * std::max<size_t>(1, inv.size()), stream);
-  d_lists.upload(lists.data(), sizeof(int32_t) * std::max<size_t>(1, lists.size()), stream);
+  if (inv.empty()) inv.push_back(-1);
+  if (lists.empty()) lists.push_back(0);
+  d_inv.upload(inv.data(), sizeof(int32_t) * inv.size(), stream);
+  d_lists.upload(lists.data(), sizeof(int32_t) * lists.size(), stream);
   d_ipiv.alloc(sizeof(int32_t) * n);
   d_scratch.alloc(sizeof(double) * std::max<int64_t>(1, nscratch) * 2 * kNB * kNB);
   d_flags.alloc(sizeof(int) * 4);
@@ -586,7 +588,7 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
   d_xnew.alloc(sizeof(double) * n);
   d_cbvec.alloc(sizeof(double) * std::max<int64_t>(1, sym.cbvec));
   d_perm.upload(sym.perm.data(), sizeof(int32_t) * n, stream);
-  rqb_solve_set_attrs(static_cast<int>(sym.max_front));
+  rqb_solve_prepare(*this);
   RQB_CUDA(cudaFuncSetAttribute(front_lu_smem<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmallNf * kSmallNf * 8));
   RQB_CUDA(cudaFuncSetAttribute(panel_lu<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -612,8 +614,14 @@ void FactorEngine::set_values_device(const double* aval_dev) {
                            stream));
 }
 
-void FactorEngine::enqueue_factor() {
+void FactorEngine::enqueue_factor(KernelTimer* kt) {
   int64_t launches = 0;
+  auto B = [&](int kind) {
+    if (kt) kt->begin(stream, kind);
+  };
+  auto E = [&]() {
+    if (kt) kt->end(stream);
+  };
   const FrontDev* fr = d_fronts.as<FrontDev>();
   const int32_t* lists = d_lists.as<int32_t>();
   double* pool = d_pool.as<double>();
@@ -621,19 +629,25 @@ void FactorEngine::enqueue_factor() {
   int* flags = d_flags.as<int>();
   RQB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, stream));
   RQB_CUDA(cudaMemsetAsync(pool, 0, sizeof(double) * sym.pool, stream));
+  B(0);
   scatter_original<<<std::min<int64_t>(div_up(nnz, 256), 148 * 16), 256, 0, stream>>>(
       d_aval.as<double>(), d_qdst.as<int64_t>(), nnz, pool);
+  E();
   launches += 1;
   for (const LevelPlan& P : plans) {
     if (!P.with_kids.empty()) {
       dim3 grid(div_up(P.ea_maxnf, 8), static_cast<unsigned>(P.with_kids.size()));
+      B(1);
       extend_add<<<grid, dim3(32, 8), 0, stream>>>(fr, lists + P.off_kids, d_inv.as<int32_t>(), pool);
+      E();
       ++launches;
     }
     if (!P.small.empty()) {
       const size_t smem = sizeof(double) * P.small_nf * P.small_nf;
+      B(2);
       front_lu_smem<256><<<static_cast<unsigned>(P.small.size()), 256, smem, stream>>>(
           fr, lists + P.off_small, pool, ipiv, flags);
+      E();
       ++launches;
     }
     for (int s = 0; s < P.big_maxpanels; ++s) {
@@ -660,20 +674,30 @@ void FactorEngine::enqueue_factor() {
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
+      B(3);
       RQB_CUDA(cudaLaunchKernelEx(&cfg, panel_lu<256>, fr, lst, k, pool, ipiv, d_scratch.as<double>(),
                                   flags));
+      E();
       dim3 ga(div_up(maxnf, 32) + div_up(maxcb, 256), nfa);
+      B(4);
       panel_apply<<<ga, 256, 0, stream>>>(fr, lst, k, pool, ipiv, d_scratch.as<double>());
+      E();
       const int tmax = maxnf - k - 1;
       launches += 2;
       if (tmax > 0) {
         const int nt = div_up(tmax, kTS);
         dim3 gs(nt * nt, nfa);
+        B(5);
         schur_dmma<<<gs, 128, 0, stream>>>(fr, lst, k, pool);
+        E();
         ++launches;
       }
     }
   }
+  B(4);
+  rqb_rowperm_enqueue(*this);
+  E();
+  ++launches;
   RQB_CUDA(cudaGetLastError());
   launches_factor = launches;
 }
@@ -696,6 +720,71 @@ void FactorEngine::factor() {
   last_ms = ms;
   last_swaps = flags[1];
   if (flags[0]) fail(errc::singular, "Q(sigma) is numerically singular: every pivot candidate below 1e-300");
+}
+
+}  // namespace rqb
+
+namespace rqb {
+
+void KernelTimer::begin(cudaStream_t s, int kind) {
+  cudaEvent_t a, b;
+  RQB_CUDA(cudaEventCreate(&a));
+  RQB_CUDA(cudaEventCreate(&b));
+  RQB_CUDA(cudaEventRecord(a, s));
+  ev.push_back({a, b});
+  kinds.push_back(kind);
+}
+
+void KernelTimer::end(cudaStream_t s) { RQB_CUDA(cudaEventRecord(ev.back().second, s)); }
+
+void KernelTimer::collect(double* ms, int64_t* count, int nkinds) {
+  for (size_t i = 0; i < ev.size(); ++i) {
+    float t = 0;
+    RQB_CUDA(cudaEventSynchronize(ev[i].second));
+    RQB_CUDA(cudaEventElapsedTime(&t, ev[i].first, ev[i].second));
+    if (kinds[i] < nkinds) ms[kinds[i]] += t, count[kinds[i]] += 1;
+    cudaEventDestroy(ev[i].first);
+    cudaEventDestroy(ev[i].second);
+  }
+  ev.clear();
+  kinds.clear();
+}
+
+void FactorEngine::profile(double* ms, int64_t* count, double* flops) {
+  for (int k = 0; k < kFactorKinds; ++k) ms[k] = 0, count[k] = 0, flops[k] = 0;
+  KernelTimer kt;
+  enqueue_factor(&kt);
+  kt.collect(ms, count, kFactorKinds);
+  // algorithmic work per kernel class (real flops; scatter/extend-add: bytes)
+  double bytes_scatter = 16.0 * nnz + 8.0 * nnz;  // read value + index, write entry
+  double ea = 0;
+  for (const Front& F : sym.fronts)
+    if (F.parent >= 0) {
+      const double ncb = F.nf - F.npiv;
+      ea += 16.0 * ncb * ncb;  // read the child's block, read+write the parent entry (~)
+    }
+  flops[0] = bytes_scatter;
+  flops[1] = ea;
+  for (const Front& F : sym.fronts) {
+    double flu = 0;
+    for (int k = 0; k < F.npiv; ++k) {
+      const double r = F.nf - k - 1.0;
+      flu += r + 2.0 * r * r;
+    }
+    if (F.npiv == 0) continue;
+    if (F.nf <= kSmallNf) {
+      flops[2] += flu;
+      continue;
+    }
+    double sch = 0;
+    for (int k = 0; k < F.npiv; k += kNB) {
+      const double w = std::min(kNB, F.npiv - k);
+      const double t = F.nf - k - w;
+      sch += 2.0 * w * t * t;
+    }
+    flops[5] += sch;
+    flops[3] += flu - sch;  // panel LU + TRSM (panel_apply shares this count)
+  }
 }
 
 }  // namespace rqb

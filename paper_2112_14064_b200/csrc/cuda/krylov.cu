@@ -376,4 +376,67 @@ void OperatorEngine::pencil_residual(const double* ur, const double* ui, double 
   launches += 2;
 }
 
+double OperatorEngine::time_op(int what, int iters, int param) {
+  const bool flush_l2 = (what & 0x100) != 0;
+  what &= 0xff;
+  const int64_t n2 = 2 * n;
+  const int k = std::max(1, std::min(param, 511));
+  DeviceBuffer a, b, V, h;
+  a.alloc(sizeof(double) * n2);
+  b.alloc(sizeof(double) * n2);
+  if (what == 3 || what == 4) {
+    V.alloc(sizeof(double) * (k + 1) * n2);
+    h.alloc(sizeof(double) * (k + 1));
+    RQB_CUDA(cudaMemsetAsync(V.p, 0, V.bytes, stream));
+    RQB_CUDA(cudaMemsetAsync(h.p, 0, h.bytes, stream));
+  }
+  RQB_CUDA(cudaMemsetAsync(a.p, 0, a.bytes, stream));
+  auto run = [&]() {
+    switch (what) {
+      case 0: apply(a.as<double>(), b.as<double>()); break;
+      case 1: fac->solve_device(a.as<double>(), b.as<double>(), 1.0); break;
+      case 2:
+        spmv_op_k<<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
+                                                           d_C.as<double>(), d_M.as<double>(), sigma,
+                                                           a.as<double>(), a.as<double>() + n, b.as<double>());
+        break;
+      case 3: gemv_t(V.as<double>(), k, a.as<double>(), h.as<double>()); break;
+      case 4: gemv_n(V.as<double>(), k, h.as<double>(), a.as<double>(), nullptr); break;
+      case 5: RQB_CUDA(cudaGraphLaunch(fac->graph_factor_exec, stream)); break;
+      case 6: spmv(2, a.as<double>(), b.as<double>()); break;
+      default: fail(errc::config, "unknown timing target");
+    }
+  };
+  for (int w = 0; w < 3; ++w) run();
+  cudaEvent_t e0, e1;
+  RQB_CUDA(cudaEventCreate(&e0));
+  RQB_CUDA(cudaEventCreate(&e1));
+  float total = 0;
+  if (flush_l2) {
+    // 256 MiB scrub (> 126 MB L2) before every timed call; each call timed alone
+    DeviceBuffer scrub;
+    scrub.alloc(size_t(256) << 20);
+    for (int it = 0; it < iters; ++it) {
+      RQB_CUDA(cudaMemsetAsync(scrub.p, it & 0xff, scrub.bytes, stream));
+      RQB_CUDA(cudaEventRecord(e0, stream));
+      run();
+      RQB_CUDA(cudaEventRecord(e1, stream));
+      RQB_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      RQB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      total += ms;
+    }
+  } else {
+    RQB_CUDA(cudaEventRecord(e0, stream));
+    for (int it = 0; it < iters; ++it) run();
+    RQB_CUDA(cudaEventRecord(e1, stream));
+    RQB_CUDA(cudaEventSynchronize(e1));
+    RQB_CUDA(cudaEventElapsedTime(&total, e0, e1));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  RQB_CUDA(cudaGetLastError());
+  return total / iters;
+}
+
 }  // namespace rqb

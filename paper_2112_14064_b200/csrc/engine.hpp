@@ -58,6 +58,18 @@ struct LevelPlan {
   std::vector<int64_t> off_panel;
 };
 
+// Per-launch CUDA-event timer (profiling runs only; not used in timed steps).
+struct KernelTimer {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<int> kinds;
+  void begin(cudaStream_t s, int kind);
+  void end(cudaStream_t s);
+  void collect(double* ms, int64_t* count, int nkinds);
+};
+
+// factor kernel classes: scatter, extend_add, front_lu_smem, panel_lu, panel_apply, schur_dmma
+constexpr int kFactorKinds = 6;
+
 struct FactorEngine {
   Symbolic sym;
   int64_t n = 0, nnz = 0;
@@ -67,6 +79,10 @@ struct FactorEngine {
   DeviceBuffer d_pool, d_aval, d_qdst, d_rows, d_fronts, d_inv, d_ipiv, d_lists, d_scratch;
   DeviceBuffer d_flags;   // [0] singular, [1] swaps
   DeviceBuffer d_y, d_xnew, d_cbvec, d_perm;  // solve workspaces (n, n, cbvec), perm[new] = old
+  // sync-free solve: work items, per-front item counts, dependency counters,
+  // net row permutation of each front's pivot block
+  DeviceBuffer d_items_fwd, d_items_bwd, d_nitems, d_npb, d_parent, d_cnt, d_rowperm;
+  int n_fwd_items = 0, n_bwd_items = 0, solve_grid = 148;
   std::vector<FrontDev> fronts_h;
   std::vector<LevelPlan> plans;
   int64_t nscratch = 0;
@@ -86,7 +102,10 @@ struct FactorEngine {
   void set_values_device(const double* aval_dev);
   // x = A^{-1} b on device vectors (original ordering), enqueued on `stream`.
   void solve_device(const double* b, double* x, double scale_out = 1.0);
-  void enqueue_factor();
+  void enqueue_factor(KernelTimer* kt = nullptr);
+  // One un-graphed factorization with per-launch events: device ms, launch
+  // count and algorithmic work (flops; bytes for classes 0-1) per kernel class.
+  void profile(double* ms, int64_t* count, double* flops);
 };
 
 // Enqueue forward+backward substitution on fe.stream: x = scale * A^{-1} b and,
@@ -94,6 +113,8 @@ struct FactorEngine {
 void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scale,
                        const double* vu, double sigma, double* xl);
 void rqb_solve_set_attrs(int maxnf);
+void rqb_solve_prepare(FactorEngine& fe);
+void rqb_rowperm_enqueue(FactorEngine& fe);
 
 // Shift-invert operator on the linearised pencil, real FP64, device resident.
 struct OperatorEngine {
@@ -126,6 +147,8 @@ struct OperatorEngine {
   // Pencil residual pieces for complex u = ur + i ui at lambda = lr + i li:
   // out[0] = ||Q(lambda) u||_2^2 (device scalar)
   void pencil_residual(const double* ur, const double* ui, double lr, double li, double* out);
+  // Average device ms of one call of an operation (see rq_operator_time).
+  double time_op(int what, int iters, int param);
 };
 
 }  // namespace rqb

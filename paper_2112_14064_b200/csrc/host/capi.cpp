@@ -8,6 +8,8 @@
 #include <memory>
 #include <string>
 
+#include <cuda_runtime_api.h>
+
 #include "../../../include/rq_b200.h"
 #include "../engine.hpp"
 #include "common.hpp"
@@ -82,6 +84,10 @@ extern "C" {
 
 const char* rq_last_error(void) { return g_err.c_str(); }
 const char* rq_version(void) { return "rq_b200 0.1 (sm_100a)"; }
+
+int rq_set_device(int device) {
+  return guarded([&] { rqb::cuda_check(cudaSetDevice(device), "cudaSetDevice"); });
+}
 
 int rq_pencil_assemble(const rq_space_desc* desc, rq_pencil_t** out) {
   return guarded([&] {
@@ -288,6 +294,16 @@ int rq_factor_front_export(const rq_factor_t* f, int64_t front, double* dense, i
   });
 }
 
+int rq_factor_profile(rq_factor_t* f, double* ms, int64_t* launches, double* work) {
+  return guarded([&] {
+    need(f, "factor");
+    need(ms, "ms");
+    need(launches, "launches");
+    need(work, "work");
+    f->fe->profile(ms, launches, work);
+  });
+}
+
 void rq_factor_destroy(rq_factor_t* f) { delete f; }
 
 int rq_operator_create(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
@@ -326,6 +342,15 @@ double rq_operator_varsigma(const rq_operator_t* op) { return op ? op->op->varsi
 rq_factor_t* rq_operator_factor(rq_operator_t* op) { return op ? &op->fac_view : nullptr; }
 
 void rq_operator_destroy(rq_operator_t* op) { delete op; }
+
+int rq_operator_time(rq_operator_t* o, int what, int iters, int param, double* ms_per_call) {
+  return guarded([&] {
+    need(o, "op");
+    need(ms_per_call, "ms");
+    if (iters < 1) rqb::fail(rqb::errc::config, "iters must be positive");
+    *ms_per_call = o->op->time_op(what, iters, param);
+  });
+}
 
 int rq_operator_apply(rq_operator_t* o, const double* v, double* r) {
   return guarded([&] {

@@ -209,12 +209,12 @@ def test_eigs_nondegenerate_vs_oracle_and_scipy():
                      for i in range(P.n)])
     rng = np.random.default_rng(11)
     P.C = P.C.copy()
-    P.C[diag] += 0.3 * rng.random(P.n)
+    P.C[diag] += 0.5 * rng.random(P.n) * P.M[diag]
     op = rq.build_operator(P, SIGMA)
-    pairs = op.solve_quadratic(8, eps=1e-10)
+    pairs = op.solve_quadratic(8, eps=1e-10, max_restarts=400)
     lam = np.array([p.lam for p in pairs])
     E = oracle.Eig(P, SIGMA, C_=P.C)
-    lo, _ = E.solve_quadratic(8, tol=1e-10)
+    lo, _ = E.solve_quadratic(8, tol=1e-10, max_restarts=400)
     assert np.max(np.abs(sorted_lams(lam) - sorted_lams(lo)) / np.abs(lo)) <= 1e-8
     n = P.n
     Kd, Cd, Md = (P.to_scipy(w).toarray() for w in "KCM")
@@ -250,7 +250,10 @@ def test_cfg3_solve_residual_and_cluster(name):
     fac = rq.lu_factorize((P.rowptr, P.col, P.q_values(SIGMA)), op.ordering)
     A = P.to_scipy("K") + SIGMA * P.to_scipy("C") + SIGMA ** 2 * P.to_scipy("M")
     b = np.random.default_rng(1).standard_normal(P.n)
-    assert np.linalg.norm(A @ fac.solve(b) - b) / np.linalg.norm(b) <= 1e-10
+    x = fac.solve(b)
+    # normwise backward error (Q(sigma) is ill-conditioned at this mesh size)
+    nA = abs(A).sum(0).max()
+    assert np.linalg.norm(A @ x - b, 1) / (nA * np.linalg.norm(x, 1) + np.linalg.norm(b, 1)) <= 1e-14
     pairs = op.solve_quadratic(10, eps=1e-10, max_restarts=400)
     ref = -0.03 + 1j * np.sqrt(0.9991)
     lam = np.array([p.lam for p in pairs])

@@ -165,10 +165,10 @@ def test_oracle_eigs_vs_scipy_dense():
     C = P.C.copy()
     diag = np.array([np.searchsorted(P.col[P.rowptr[i]:P.rowptr[i + 1]], i) + P.rowptr[i]
                      for i in range(P.n)])
-    C[diag] += 0.3 * rng.random(P.n)
+    C[diag] += 0.5 * rng.random(P.n) * P.M[diag]
     sigma = -0.5
     E = oracle.Eig(P, sigma, C_=C)
-    lam, res = E.solve_quadratic(6, tol=1e-10)
+    lam, res = E.solve_quadratic(6, tol=1e-10, max_restarts=400)
     assert np.all(res <= 1e-10)
     Kd = P.to_scipy("K").toarray(); Md = P.to_scipy("M").toarray()
     Cd = P.to_scipy("M").toarray() * 0
