@@ -31,7 +31,8 @@ NEV = {"cfg1": 10, "cfg2_riga": 20, "cfg2_iga": 20, "cfg3_riga": 50, "cfg3_iga":
        "cfg4_riga": 100, "cfg4_iga": 100}
 FP64_PEAK_TFLOPS = 37.2   # measured DMMA m16n8k4 issue rate, profiles/fp64_peak_r01.jsonl
 FP64_DFMA_TFLOPS = 36.7   # measured DFMA rate (same file)
-KINDS = ["scatter_original", "extend_add", "front_lu_smem", "panel_lu", "panel_apply", "schur_dmma"]
+KINDS = ["scatter_original", "extend_add", "front_lu_smem", "panel_lu", "panel_apply+rowperm",
+         "schur_dmma", "factor_dag"]
 
 
 def measured_peaks():
@@ -212,9 +213,9 @@ def run_b200(args):
     resid_max = max(p.residual for p in pairs)
 
     # ---- per-kernel profile of one factorization (un-graphed, events per launch)
-    ms_k = np.zeros(6)
-    cnt_k = np.zeros(6, np.int64)
-    work_k = np.zeros(6)
+    ms_k = np.zeros(7)
+    cnt_k = np.zeros(7, np.int64)
+    work_k = np.zeros(7)
     _lib.check(_lib.lib.rq_factor_profile(fh, ms_k, cnt_k, work_k))
     dom = int(np.argmax(ms_k))
     # ---- memory-bound kernels of the Krylov step
@@ -276,7 +277,7 @@ def run_b200(args):
         roof = {"bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 5), "traffic": traffic}
     else:
-        peak = FP64_PEAK_TFLOPS if KINDS[dom] == "schur_dmma" else FP64_DFMA_TFLOPS
+        peak = FP64_PEAK_TFLOPS if KINDS[dom] in ("schur_dmma", "factor_dag") else FP64_DFMA_TFLOPS
         ach = work_k[dom] / (ms_k[dom] * 1e9)  # TFLOP/s
         roof = {"bound": bound, "achieved": round(ach, 4), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(ach / peak, 5), "traffic": traffic}
@@ -298,7 +299,7 @@ def run_b200(args):
         "eigs": {k: info.get(k) for k in ("restarts", "guard_passes", "n_fb", "n_mv", "n_vv",
                                           "launches", "restart_defect")},
         "kernels": {
-            "factor_profile_ms": {KINDS[i]: round(float(ms_k[i]), 4) for i in range(6)},
+            "factor_profile_ms": {KINDS[i]: round(float(ms_k[i]), 4) for i in range(7)},
             "trisolve": {"ms": round(t_solve, 5), "gbs": round(solve_bytes / t_solve / 1e6, 1),
                          "frac_hbm": round(solve_bytes / t_solve / 1e6 / hbm, 4)},
             "spmv_fused_cm": {"ms": round(t_spmv, 5), "gbs": round(spmv_bytes / t_spmv / 1e6, 1),

@@ -109,6 +109,7 @@ _sig("rq_factor_get_info", C.c_int, vp, C.POINTER(FactorInfo))
 _sig("rq_factor_solve", C.c_int, vp, f64p, f64p, C.c_int)
 _sig("rq_factor_front_export", C.c_int, vp, C.c_int64, vp, vp, C.POINTER(C.c_int64))
 _sig("rq_factor_profile", C.c_int, vp, f64p, i64p, f64p)
+_sig("rq_factor_dag_profile", C.c_int, vp, f64p)
 _sig("rq_factor_destroy", None, vp)
 _sig("rq_operator_create", C.c_int, C.c_int64, i64p, i32p, f64p, f64p, f64p, vp,
      C.POINTER(OperatorOpts), C.POINTER(vp))
@@ -129,7 +130,7 @@ EXPORTS = [
     "rq_pencil_supports", "rq_pencil_destroy", "rq_space_dims", "rq_space_boundary_mask",
     "rq_nd_order", "rq_symbolic_stats_get", "rq_symbolic_perm", "rq_symbolic_fronts",
     "rq_symbolic_front_rows", "rq_symbolic_destroy", "rq_factor_create", "rq_factor_refactor",
-    "rq_factor_get_info", "rq_factor_solve", "rq_factor_front_export", "rq_factor_profile",
+    "rq_factor_get_info", "rq_factor_solve", "rq_factor_front_export", "rq_factor_profile", "rq_factor_dag_profile",
     "rq_factor_destroy",
     "rq_operator_create", "rq_operator_varsigma", "rq_operator_apply", "rq_operator_b_inner",
     "rq_operator_spmv", "rq_operator_arnoldi", "rq_operator_factor", "rq_operator_destroy",

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "device.cuh"
@@ -589,6 +590,11 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
   d_cbvec.alloc(sizeof(double) * std::max<int64_t>(1, sym.cbvec));
   d_perm.upload(sym.perm.data(), sizeof(int32_t) * n, stream);
   rqb_solve_prepare(*this);
+  {
+    const char* mode = std::getenv("RQB_FACTOR");
+    use_dag = !(mode && std::string(mode) == "level");
+  }
+  if (use_dag) rqb_dag_build(*this);
   RQB_CUDA(cudaFuncSetAttribute(front_lu_smem<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmallNf * kSmallNf * 8));
   RQB_CUDA(cudaFuncSetAttribute(panel_lu<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -634,6 +640,18 @@ void FactorEngine::enqueue_factor(KernelTimer* kt) {
       d_aval.as<double>(), d_qdst.as<int64_t>(), nnz, pool);
   E();
   launches += 1;
+  if (use_dag) {
+    B(6);
+    rqb_dag_enqueue(*this);
+    E();
+    B(4);
+    rqb_rowperm_enqueue(*this);
+    E();
+    launches += 2;
+    RQB_CUDA(cudaGetLastError());
+    launches_factor = launches;
+    return;
+  }
   for (const LevelPlan& P : plans) {
     if (!P.with_kids.empty()) {
       dim3 grid(div_up(P.ea_maxnf, 8), static_cast<unsigned>(P.with_kids.size()));
@@ -784,6 +802,10 @@ void FactorEngine::profile(double* ms, int64_t* count, double* flops) {
     }
     flops[5] += sch;
     flops[3] += flu - sch;  // panel LU + TRSM (panel_apply shares this count)
+  }
+  if (use_dag) {
+    flops[6] = sym.flops_lu;  // the persistent kernel does the whole factorization
+    flops[2] = flops[3] = flops[5] = 0;
   }
 }
 

@@ -1,0 +1,811 @@
+// SPDX-License-Identifier: Apache-2.0
+// Numeric multifrontal LU of Q(sigma) as ONE persistent, dependency-driven
+// kernel (lu_factorize; it replaces the per-pivot rank-1 loop
+// of kern::elim_step, kernels.cpp:58-69).
+//
+// Task DAG (built on the host in a topological order: tree height, panel step,
+// front; within a step the tiles the next panel needs come first = lookahead):
+//   SMALL(f)           nf <= 160: children's extend-add + whole-front LU in
+//                      shared memory (16-column panels factored by one warp with
+//                      warp-shuffle threshold pivot search; DMMA trailing update)
+//   ASM(f, b)          big front, 64-column block: children's extend-add (gather)
+//   DIAG(f, s)         32x32 diagonal block of panel s, unpivoted (speculative),
+//                      inv(L11) / inv(U11) to scratch, in-block multiplier check
+//   ROWS(f, s, a)      64-row tile row below the block: L = A inv(U11); max|l|
+//                      over fully-summed rows -> per-panel flag (panel backed up)
+//   COLS(f, s, b)      64-column tile column right of the block: U12 = inv(L11) A12
+//   UPD(f, s, a, b)    64x64 tile -= L21 U12 on FP64 tensor cores (mma.sync
+//                      m16n8k4 f64 -> DMMA.8x8x4)
+// The last of DIAG/ROWS/COLS of a panel to finish checks the flag. If every
+// multiplier of a fully-summed row satisfies |l| <= 10 (1 - 1e-14), the
+// threshold-0.1 rule would have kept every
+// diagonal pivot, so the speculative panel IS the pivoted result. Otherwise
+// that CTA waits for the pending trailing updates, restores the panel from its
+// backup and redoes it with exact threshold partial pivoting (prefer the
+// diagonal, ties -> lowest row, singular < 1e-300), full-row swaps and U12.
+// Then it releases the panel to the UPD tasks.
+// CTAs draw tasks with an atomic ticket: a task only waits (spins on counters)
+// for tasks with smaller tickets that are already running, so the schedule is
+// deadlock-free without co-residency assumptions. Data produced inside the
+// kernel is read with ld.global.cg (L1 bypass); publication is
+// __threadfence + atomic.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "device.cuh"
+
+namespace rqb {
+
+namespace {
+
+constexpr int kDT = 256;          // threads per CTA
+constexpr int kPB = 16;           // small-front panel width
+constexpr int kTile = 64;         // big-front tile edge
+constexpr int kTSP = kTile + 4;   // padded smem stride of DMMA operand tiles
+constexpr double kLmax = 10.0 * (1.0 - 1e-14);  // 1/threshold, conservative
+constexpr int kCnt = 5;  // per-front counters: tasks, asm, diag, rc, released
+
+enum : int16_t { T_SMALL = 0, T_ASM = 1, T_DIAG = 2, T_ROWS = 3, T_COLS = 4, T_UPD = 5 };
+
+struct Task {
+  int32_t front;
+  int16_t type, step;
+  int32_t a, b;
+};
+
+struct FrontDag {
+  int32_t tiles;       // tiles per dimension (big fronts), 0 for small
+  int32_t tile_off;    // offset into tile_step[]
+  int32_t ntasks;      // completion target of cnt[0]
+  int32_t nasm;
+  int32_t rc_off;      // offset into rc_prefix[] (steps + 1 entries)
+  int32_t flag_off;    // offset into flagbits[] (one per step)
+  int32_t slot;        // scratch slot (inverses), -1 small
+  int32_t pad;
+  int64_t backup_off;  // panel backup nf x 32, then A12 backup 32 x nf
+};
+
+struct DagArgs {
+  const FrontDev* fronts;
+  const FrontDag* dag;
+  const Task* tasks;
+  int ntasks;
+  const int32_t* inv;
+  double* pool;
+  int32_t* ipiv;
+  double* scratch;
+  double* backup;
+  int* cnt;
+  int* tile_step;
+  const int32_t* rc_prefix;
+  unsigned long long* flagbits;
+  int* flags;   // [0] singular, [1] swaps
+  int* ticket;
+  unsigned long long* prof;  // optional: per task type {work cycles, wait cycles, count}
+};
+
+__device__ __forceinline__ void spin_ge(const int* p, int target) {
+  if (*((volatile const int*)p) >= target) return;
+  while (*((volatile const int*)p) < target) __nanosleep(64);
+}
+
+__device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double m = 0.0;
+  for (int i = 0; i < kDT / 32; ++i) m = fmax(m, red[i]);
+  __syncthreads();
+  return m;
+}
+
+// Children's Schur blocks into columns [c0, c1) of front F; dst column c is at
+// dst + (c - c0) * ldd (shared or global memory).
+__device__ void extend_add_cols(const DagArgs& A, const FrontDev& F, int c0, int c1, double* dst,
+                                int64_t ldd, bool dst_global) {
+  const int32_t* inv0 = A.inv + F.inv_off;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int ch = 0; ch < F.nchild; ++ch) {
+    const int32_t* invc = inv0 + (int64_t)ch * F.nf;
+    const FrontDev C = A.fronts[ch == 0 ? F.child0 : F.child1];
+    const double* cp = A.pool + C.off;
+    for (int c = c0 + warp; c < c1; c += kDT / 32) {
+      const int ic = invc[c];
+      if (ic < 0) continue;
+      const double* ccol = cp + (int64_t)ic * C.ld;
+      double* dcol = dst + (int64_t)(c - c0) * ldd;
+      for (int r = lane; r < F.nf; r += 32) {
+        const int ir = invc[r];
+        if (ir < 0) continue;
+        const double v = __ldcg(&ccol[ir]);
+        if (dst_global)
+          dcol[r] = __ldcg(&dcol[r]) + v;  // L1 may hold lines other SMs rewrote
+        else
+          dcol[r] += v;
+      }
+    }
+    __syncthreads();  // two children may touch the same entries
+  }
+}
+
+// ---------------------------------------------------------------------------
+__device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int* piv_sh) {
+  const int nf = F.nf, np = F.npiv, lds = nf | 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* g = A.pool + F.off;
+  for (int c = warp; c < nf; c += kDT / 32)
+    for (int r = lane; r < nf; r += 32) sm[r + c * lds] = __ldcg(&g[r + (int64_t)c * F.ld]);
+  __syncthreads();
+  extend_add_cols(A, F, 0, nf, sm, lds, false);
+  for (int k0 = 0; k0 < np; k0 += kPB) {
+    const int pw = min(kPB, np - k0);
+    if (warp == 0) {
+      for (int j = k0; j < k0 + pw; ++j) {
+        double best = -1.0;
+        int bi = j;
+        for (int i = j + lane; i < np; i += 32) {
+          const double v = fabs(sm[i + j * lds]);
+          if (v > best) best = v, bi = i;
+        }
+        warp_argmax(best, bi);
+        const double diag = fabs(sm[j + j * lds]);
+        int p = diag >= kPivThreshold * best ? j : bi;
+        if (!(best >= kSingularTiny)) {
+          if (lane == 0) atomicOr(&A.flags[0], 1);
+          p = j;
+        }
+        if (lane == 0) {
+          A.ipiv[F.start + j] = p;
+          piv_sh[j - k0] = p;
+          if (p != j) atomicAdd(&A.flags[1], 1);
+        }
+        if (p != j && lane < pw) {
+          const int c = k0 + lane;
+          const double t = sm[j + c * lds];
+          sm[j + c * lds] = sm[p + c * lds];
+          sm[p + c * lds] = t;
+        }
+        __syncwarp();
+        const double ujj = sm[j + j * lds];
+        for (int i = j + 1 + lane; i < nf; i += 32) {
+          const double l = sm[i + j * lds] / ujj;
+          sm[i + j * lds] = l;
+          for (int c = j + 1; c < k0 + pw; ++c) sm[i + c * lds] -= l * sm[j + c * lds];
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int c = tid; c < nf; c += kDT) {
+      if (c >= k0 && c < k0 + pw) continue;
+      for (int jj = 0; jj < pw; ++jj) {
+        const int p = piv_sh[jj], j = k0 + jj;
+        if (p != j) {
+          const double t = sm[j + c * lds];
+          sm[j + c * lds] = sm[p + c * lds];
+          sm[p + c * lds] = t;
+        }
+      }
+      if (c >= k0 + pw)
+        for (int jj = 1; jj < pw; ++jj) {
+          double s = sm[k0 + jj + c * lds];
+          for (int t = 0; t < jj; ++t) s -= sm[k0 + jj + (k0 + t) * lds] * sm[k0 + t + c * lds];
+          sm[k0 + jj + c * lds] = s;
+        }
+    }
+    __syncthreads();
+    const int t0 = k0 + pw, T = nf - t0;
+    if (T > 0) {
+      const int mt = (T + 15) / 16, nt = (T + 7) / 8;
+      const int gid = lane >> 2, tig = lane & 3;
+      for (int tile = warp; tile < mt * nt; tile += kDT / 32) {
+        const int r0 = t0 + (tile % mt) * 16, c0 = t0 + (tile / mt) * 8;
+        double acc[4] = {0, 0, 0, 0};
+        for (int kk = 0; kk < pw; kk += 4) {
+          const int kc = k0 + kk + tig;
+          const bool kin = kk + tig < pw;
+          const int ra = r0 + gid, rb = r0 + gid + 8, cb = c0 + gid;
+          const double a0 = (kin && ra < nf) ? sm[ra + kc * lds] : 0.0;
+          const double a1 = (kin && rb < nf) ? sm[rb + kc * lds] : 0.0;
+          const double b0 = (kin && cb < nf) ? sm[kc + cb * lds] : 0.0;
+          dmma(acc, a0, a1, b0);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = r0 + gid + (e >> 1) * 8, c = c0 + 2 * tig + (e & 1);
+          if (r < nf && c < nf) sm[r + c * lds] -= acc[e];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int c = warp; c < nf; c += kDT / 32)
+    for (int r = lane; r < nf; r += 32) g[r + (int64_t)c * F.ld] = sm[r + c * lds];
+}
+
+// inverses of the unit-lower / upper factors of a w x w block T (stride 33);
+// thread c (< 32) builds column c of both
+__device__ void build_inverses(const double* T, int w, double* invL, double* invU) {
+  const int c = threadIdx.x;
+  if (c >= kNB) return;
+  for (int i = 0; i < kNB; ++i) invL[i + c * kNB] = 0.0, invU[i + c * kNB] = 0.0;
+  if (c >= w) return;
+  invL[c + c * kNB] = 1.0;
+  for (int i = c + 1; i < w; ++i) {
+    double s = 0.0;
+    for (int t = c; t < i; ++t) s += T[i + t * 33] * invL[t + c * kNB];
+    invL[i + c * kNB] = -s;
+  }
+  invU[c + c * kNB] = 1.0 / T[c + c * 33];
+  for (int i = c - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int t = i + 1; t <= c; ++t) s += T[i + t * 33] * invU[t + c * kNB];
+    invU[i + c * kNB] = -s / T[i + i * 33];
+  }
+}
+
+__device__ void diag_task(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s, double* sm) {
+  const int k = s * kNB, w = min(kNB, F.npiv - k);
+  double* g = A.pool + F.off;
+  const int64_t ld = F.ld;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* T = sm;               // 32 x 33
+  double* red = sm + 32 * 33;   // block reduction scratch
+  double* bk = A.backup + D.backup_off;
+  for (int idx = tid; idx < w * w; idx += kDT) {
+    const int r = idx % w, c = idx / w;
+    const double v = __ldcg(&g[(k + r) + (int64_t)(k + c) * ld]);
+    T[r + c * 33] = v;
+    bk[(k + r) + (int64_t)c * F.nf] = v;
+  }
+  __syncthreads();
+  double lm = 0.0;
+  if (warp == 0) {
+    for (int j = 0; j < w; ++j) {
+      const double ujj = T[j + j * 33];
+      if (!(fabs(ujj) >= kSingularTiny)) lm = 1e300;  // force the pivoted fallback
+      double l = 0.0;
+      if (lane > j && lane < w) {
+        l = T[lane + j * 33] / ujj;
+        T[lane + j * 33] = l;
+        lm = fmax(lm, fabs(l));
+      }
+      __syncwarp();
+      if (lane > j && lane < w)
+        for (int c = j + 1; c < w; ++c) T[lane + c * 33] -= l * T[j + c * 33];
+      __syncwarp();
+    }
+  }
+  lm = block_max(warp == 0 ? lm : 0.0, red);
+  for (int idx = tid; idx < w * w; idx += kDT) {
+    const int r = idx % w, c = idx / w;
+    g[(k + r) + (int64_t)(k + c) * ld] = T[r + c * 33];
+  }
+  for (int j = tid; j < w; j += kDT) A.ipiv[F.start + k + j] = k + j;
+  double* invL = A.scratch + (int64_t)D.slot * 2 * kNB * kNB;
+  build_inverses(T, w, invL, invL + kNB * kNB);
+  if (tid == 0) atomicMax(&A.flagbits[D.flag_off + s], (unsigned long long)__double_as_longlong(lm));
+}
+
+__device__ void rows_task(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s, int a,
+                          double* sm) {
+  const int k = s * kNB, w = min(kNB, F.npiv - k), np = F.npiv;
+  const int r0 = max(a * kTile, k + w), r1 = min(a * kTile + kTile, F.nf);
+  const int nr = r1 - r0;
+  double* g = A.pool + F.off;
+  const int64_t ld = F.ld;
+  const int tid = threadIdx.x;
+  constexpr int kPS = kTile + 1;   // stride of the 64-row panel block
+  double* P = sm;                 // 64 rows x 32 columns
+  double* iU = sm + kPS * kNB;    // 32 x 32
+  double* red = iU + kNB * kNB;
+  double* bk = A.backup + D.backup_off;
+  const double* invU = A.scratch + (int64_t)D.slot * 2 * kNB * kNB + kNB * kNB;
+  for (int i = tid; i < kNB * kNB; i += kDT) iU[i] = __ldcg(&invU[i]);
+  for (int idx = tid; idx < nr * w; idx += kDT) {
+    const int r = idx % nr, c = idx / nr;
+    const double v = __ldcg(&g[(r0 + r) + (int64_t)(k + c) * ld]);
+    P[r + c * kPS] = v;
+    bk[(r0 + r) + (int64_t)c * F.nf] = v;
+  }
+  __syncthreads();
+  double lm = 0.0;
+  const int r = tid & 63, q = tid >> 6;
+  if (r < nr) {
+    for (int i = q; i < w; i += 4) {
+      double s = 0.0;
+      for (int t = 0; t <= i; ++t) s += P[r + t * kPS] * iU[t + i * kNB];
+      g[(r0 + r) + (int64_t)(k + i) * ld] = s;
+      if (r0 + r < np) lm = fmax(lm, fabs(s));
+    }
+  }
+  lm = block_max(lm, red);
+  if (tid == 0) atomicMax(&A.flagbits[D.flag_off + s], (unsigned long long)__double_as_longlong(lm));
+}
+
+__device__ void cols_task(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s, int b,
+                          double* sm) {
+  const int k = s * kNB, w = min(kNB, F.npiv - k);
+  const int c0 = max(b * kTile, k + w), c1 = min(b * kTile + kTile, F.nf);
+  const int nc = c1 - c0;
+  double* g = A.pool + F.off;
+  const int64_t ld = F.ld;
+  const int tid = threadIdx.x;
+  double* P = sm;               // 32 x 64 (row-major by column: P[i + c*33])
+  double* iL = sm + 64 * 33;
+  double* bk2 = A.backup + D.backup_off + (int64_t)F.nf * kNB;
+  const double* invL = A.scratch + (int64_t)D.slot * 2 * kNB * kNB;
+  for (int i = tid; i < kNB * kNB; i += kDT) iL[i] = __ldcg(&invL[i]);
+  for (int idx = tid; idx < nc * w; idx += kDT) {
+    const int r = idx % w, c = idx / w;
+    const double v = __ldcg(&g[(k + r) + (int64_t)(c0 + c) * ld]);
+    P[r + c * 33] = v;
+    bk2[r + (int64_t)(c0 + c) * kNB] = v;
+  }
+  __syncthreads();
+  const int c = tid & 63, q = tid >> 6;
+  if (c < nc)
+    for (int i = q; i < w; i += 4) {
+      double s = 0.0;
+      for (int t = 0; t <= i; ++t) s += iL[i + t * kNB] * P[t + c * 33];
+      g[(k + i) + (int64_t)(c0 + c) * ld] = s;
+    }
+}
+
+__device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int b, double* sm) {
+  const int k = s * kNB, w = min(kNB, F.npiv - k);
+  const int r0 = max(a * kTile, k + w), r1 = min(a * kTile + kTile, F.nf);
+  const int c0 = max(b * kTile, k + w), c1 = min(b * kTile + kTile, F.nf);
+  double* g = A.pool + F.off;
+  const int64_t ld = F.ld;
+  double* As = sm;              // [kk][m]
+  double* Bs = sm + kNB * kTSP; // [kk][n]
+  const int tid = threadIdx.x;
+  const int nr = r1 - r0, nc = c1 - c0;
+  for (int idx = tid; idx < kNB * kTile; idx += kDT) {
+    const int kk = idx / kTile, m = idx % kTile;
+    As[kk * kTSP + m] = (kk < w && m < nr) ? __ldcg(&g[(r0 + m) + (int64_t)(k + kk) * ld]) : 0.0;
+  }
+  for (int idx = tid; idx < kNB * kTile; idx += kDT) {
+    const int kk = idx % kNB, n = idx / kNB;
+    Bs[kk * kTSP + n] = (kk < w && n < nc) ? __ldcg(&g[(k + kk) + (int64_t)(c0 + n) * ld]) : 0.0;
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;  // 8 warps: 2 (m) x 4 (n) of 32 x 16
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int gid = lane >> 2, tig = lane & 3;
+  double acc[2][2][4];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[x][y][e] = 0.0;
+  const int ksteps = (w + 3) / 4;
+  for (int ks = 0; ks < ksteps; ++ks) {
+    const int kr = ks * 4 + tig;
+    double af[2][2], bf[2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      af[x][0] = As[kr * kTSP + wm + x * 16 + gid];
+      af[x][1] = As[kr * kTSP + wm + x * 16 + gid + 8];
+    }
+#pragma unroll
+    for (int y = 0; y < 2; ++y) bf[y] = Bs[kr * kTSP + wn + y * 8 + gid];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) dmma(acc[x][y], af[x][0], af[x][1], bf[y]);
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = wm + x * 16 + gid + (e >> 1) * 8, c = wn + y * 8 + 2 * tig + (e & 1);
+        if (r < nr && c < nc) {
+          double* p = &g[(r0 + r) + (int64_t)(c0 + c) * ld];
+          *p = __ldcg(p) - acc[x][y][e];
+        }
+      }
+}
+
+// Exact threshold-pivoted redo of panel s (rare path, one CTA).
+__device__ void panel_fallback(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s,
+                               double* sm) {
+  const int k = s * kNB, w = min(kNB, F.npiv - k), np = F.npiv, nf = F.nf;
+  double* g = A.pool + F.off;
+  const int64_t ld = F.ld;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* red = sm;
+  int* redi = reinterpret_cast<int*>(sm + 32);
+  __shared__ int piv_s;
+  // all trailing updates of earlier panels must be in place (rows are swapped across all columns)
+  if (tid == 0) {
+    const int a0 = k / kTile;
+    for (int a = a0; a < D.tiles; ++a)
+      for (int b = a0; b < D.tiles; ++b) spin_ge(&A.tile_step[D.tile_off + a * D.tiles + b], s);
+    __threadfence();
+  }
+  __syncthreads();
+  const double* bk = A.backup + D.backup_off;
+  const double* bk2 = bk + (int64_t)nf * kNB;
+  for (int idx = tid; idx < (nf - k) * w; idx += kDT) {
+    const int r = k + idx % (nf - k), c = idx / (nf - k);
+    g[r + (int64_t)(k + c) * ld] = __ldcg(&bk[r + (int64_t)c * nf]);
+  }
+  for (int idx = tid; idx < (nf - k - w) * w; idx += kDT) {
+    const int r = idx % w, c = k + w + idx / w;
+    g[(k + r) + (int64_t)c * ld] = __ldcg(&bk2[r + (int64_t)c * kNB]);
+  }
+  __syncthreads();
+  for (int j = k; j < k + w; ++j) {
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = j + tid; i < np; i += kDT) {
+      const double v = fabs(__ldcg(&g[i + (int64_t)j * ld]));
+      if (v > best) best = v, bi = i;
+    }
+    warp_argmax(best, bi);
+    if (lane == 0) red[warp] = best, redi[warp] = bi;
+    __syncthreads();
+    if (tid == 0) {
+      for (int q = 1; q < kDT / 32; ++q)
+        if (red[q] > best || (red[q] == best && redi[q] < bi)) best = red[q], bi = redi[q];
+      const double diag = fabs(__ldcg(&g[j + (int64_t)j * ld]));
+      int p = diag >= kPivThreshold * best ? j : bi;
+      if (!(best >= kSingularTiny)) {
+        atomicOr(&A.flags[0], 1);
+        p = j;
+      }
+      if (p != j) atomicAdd(&A.flags[1], 1);
+      A.ipiv[F.start + j] = p;
+      piv_s = p;
+    }
+    __syncthreads();
+    const int p = piv_s;
+    if (p != j)
+      for (int c = tid; c < nf; c += kDT) {
+        const double t = __ldcg(&g[j + (int64_t)c * ld]);
+        g[j + (int64_t)c * ld] = __ldcg(&g[p + (int64_t)c * ld]);
+        g[p + (int64_t)c * ld] = t;
+      }
+    __syncthreads();
+    const double ujj = __ldcg(&g[j + (int64_t)j * ld]);
+    for (int i = j + 1 + tid; i < nf; i += kDT) {
+      const double l = __ldcg(&g[i + (int64_t)j * ld]) / ujj;
+      g[i + (int64_t)j * ld] = l;
+      for (int c = j + 1; c < k + w; ++c)
+        g[i + (int64_t)c * ld] = __ldcg(&g[i + (int64_t)c * ld]) - l * __ldcg(&g[j + (int64_t)c * ld]);
+    }
+    __syncthreads();
+  }
+  // U12 = inv(L11) A12 (forward substitution per column)
+  for (int c = k + w + tid; c < nf; c += kDT)
+    for (int jj = 1; jj < w; ++jj) {
+      double sv = __ldcg(&g[(k + jj) + (int64_t)c * ld]);
+      for (int t = 0; t < jj; ++t)
+        sv -= __ldcg(&g[(k + jj) + (int64_t)(k + t) * ld]) * __ldcg(&g[(k + t) + (int64_t)c * ld]);
+      g[(k + jj) + (int64_t)c * ld] = sv;
+    }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kDT, 1) factor_dag_kernel(DagArgs A) {
+  extern __shared__ double sm[];
+  __shared__ int task_s, last_s;
+  __shared__ int piv_sh[kPB];
+  const int tid = threadIdx.x;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) task_s = atomicAdd(A.ticket, 1);
+    __syncthreads();
+    const int t = task_s;
+    if (t >= A.ntasks) return;
+    const Task T = A.tasks[t];
+    const int f = T.front;
+    const FrontDev F = A.fronts[f];
+    const FrontDag D = A.dag[f];
+    int* cnt = A.cnt + kCnt * f;
+    const long long t_start = A.prof ? clock64() : 0;
+    // ---- dependencies
+    if (tid == 0) {
+      switch (T.type) {
+        case T_SMALL:
+        case T_ASM:
+          if (F.nchild > 0) spin_ge(&A.cnt[kCnt * F.child0], A.dag[F.child0].ntasks);
+          if (F.nchild > 1) spin_ge(&A.cnt[kCnt * F.child1], A.dag[F.child1].ntasks);
+          break;
+        case T_DIAG:
+          if (T.step == 0) {
+            spin_ge(&cnt[1], D.nasm);
+          } else {
+            const int ap = (T.step * kNB) / kTile;
+            spin_ge(&A.tile_step[D.tile_off + ap * D.tiles + ap], T.step);
+          }
+          break;
+        case T_ROWS: {
+          const int bp = (T.step * kNB) / kTile;
+          spin_ge(&cnt[2], T.step + 1);
+          spin_ge(&A.tile_step[D.tile_off + T.a * D.tiles + bp], T.step);
+          break;
+        }
+        case T_COLS: {
+          const int ap = (T.step * kNB) / kTile;
+          spin_ge(&cnt[2], T.step + 1);
+          spin_ge(&A.tile_step[D.tile_off + ap * D.tiles + T.b], T.step);
+          break;
+        }
+        case T_UPD:
+          spin_ge(&cnt[4], T.step + 1);
+          spin_ge(&A.tile_step[D.tile_off + T.a * D.tiles + T.b], T.step);
+          break;
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    const long long t_work = A.prof ? clock64() : 0;
+    // ---- work
+    switch (T.type) {
+      case T_SMALL: small_front(A, F, sm, piv_sh); break;
+      case T_ASM: {
+        const int c0 = T.b * kTile, c1 = min(F.nf, c0 + kTile);
+        extend_add_cols(A, F, c0, c1, A.pool + F.off + (int64_t)c0 * F.ld, F.ld, true);
+        break;
+      }
+      case T_DIAG: diag_task(A, F, D, T.step, sm); break;
+      case T_ROWS: rows_task(A, F, D, T.step, T.a, sm); break;
+      case T_COLS: cols_task(A, F, D, T.step, T.b, sm); break;
+      case T_UPD: upd_task(A, F, T.step, T.a, T.b, sm); break;
+    }
+    __syncthreads();
+    // ---- publish
+    if (T.type == T_DIAG || T.type == T_ROWS || T.type == T_COLS) {
+      if (tid == 0) {
+        __threadfence();
+        if (T.type == T_DIAG) atomicAdd(&cnt[2], 1);
+        const int old = atomicAdd(&cnt[3], 1);
+        last_s = (old + 1 == A.rc_prefix[D.rc_off + T.step + 1]);
+      }
+      __syncthreads();
+      if (last_s) {  // last of the panel: verify, fall back if needed, release
+        if (tid == 0) __threadfence();
+        __syncthreads();
+        const unsigned long long bits = atomicAdd(&A.flagbits[D.flag_off + T.step], 0ull);
+        if (!(__longlong_as_double((long long)bits) <= kLmax)) panel_fallback(A, F, D, T.step, sm);
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          atomicAdd(&cnt[4], 1);
+        }
+      }
+    } else if (T.type == T_UPD) {
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(&A.tile_step[D.tile_off + T.a * D.tiles + T.b], 1);
+      }
+    } else if (T.type == T_ASM) {
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(&cnt[1], 1);
+      }
+    }
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(&cnt[0], 1);
+      if (A.prof) {
+        const long long t_end = clock64();
+        atomicAdd(&A.prof[3 * T.type + 0], (unsigned long long)(t_end - t_work));
+        atomicAdd(&A.prof[3 * T.type + 1], (unsigned long long)(t_work - t_start));
+        atomicAdd(&A.prof[3 * T.type + 2], 1ull);
+      }
+    }
+  }
+}
+
+int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace
+
+struct DagPlan {
+  DeviceBuffer d_tasks, d_dag, d_cnt, d_tile, d_rc, d_flagbits, d_backup, d_ticket, d_prof;
+  int ntasks = 0, nfronts = 0, ntile = 0, nflag = 0, grid = 148;
+  size_t smem = 0;
+  double flops_upd = 0, flops_small = 0;
+};
+
+void rqb_dag_build(FactorEngine& fe) {
+  const Symbolic& S = fe.sym;
+  const int nfr = static_cast<int>(S.fronts.size());
+  auto P = std::make_unique<DagPlan>();
+  std::vector<FrontDag> dag(nfr);
+  std::vector<int32_t> rc_prefix;
+  std::vector<Task> tasks;
+  int tile_off = 0, flag_off = 0, slot = 0;
+  int64_t backup = 0;
+  int max_small = 0;
+  const int nlev = static_cast<int>(S.level_fronts.size());
+  for (int lev = 0; lev < nlev; ++lev) {
+    // pass 1: per-front bookkeeping + SMALL/ASM tasks
+    int max_steps = 0;
+    for (int32_t f : S.level_fronts[lev]) {
+      const Front& F = S.fronts[f];
+      FrontDag& D = dag[f];
+      D.slot = -1;
+      if (F.nf <= kSmallNf) {
+        tasks.push_back({f, T_SMALL, 0, 0, 0});
+        D.ntasks = 1;
+        max_small = std::max(max_small, F.nf);
+        continue;
+      }
+      D.tiles = div_up(F.nf, kTile);
+      D.tile_off = tile_off;
+      tile_off += D.tiles * D.tiles;
+      D.flag_off = flag_off;
+      const int steps = div_up(F.npiv, kNB);
+      flag_off += std::max(1, steps);
+      D.slot = slot++;
+      D.backup_off = backup;
+      backup += 2LL * F.nf * kNB;
+      D.nasm = D.tiles;
+      for (int b = 0; b < D.tiles; ++b) tasks.push_back({f, T_ASM, 0, 0, b});
+      D.ntasks = D.nasm;
+      max_steps = std::max(max_steps, steps);
+    }
+    // pass 2: cumulative DIAG/ROWS/COLS counts per panel (steps + 1 entries
+    // per big front), then the panel steps interleaved across the level's fronts
+    for (int32_t f : S.level_fronts[lev]) {
+      const Front& F = S.fronts[f];
+      if (F.nf <= kSmallNf) continue;
+      FrontDag& D = dag[f];
+      D.rc_off = static_cast<int32_t>(rc_prefix.size());
+      rc_prefix.push_back(0);
+      const int steps = div_up(F.npiv, kNB);
+      int acc = 0;
+      for (int s = 0; s < steps; ++s) {
+        const int k = s * kNB, w = std::min(kNB, F.npiv - k);
+        const int t0 = k + w;
+        const int a0 = t0 / kTile;
+        const int nrow = t0 < F.nf ? D.tiles - a0 : 0;
+        acc += 1 + 2 * nrow;  // DIAG + ROWS + COLS
+        rc_prefix.push_back(acc);
+      }
+    }
+    for (int s = 0; s < max_steps; ++s) {
+      for (int32_t f : S.level_fronts[lev]) {
+        const Front& F = S.fronts[f];
+        if (F.nf <= kSmallNf) continue;
+        FrontDag& D = dag[f];
+        const int steps = div_up(F.npiv, kNB);
+        if (s >= steps) continue;
+        const int k = s * kNB, w = std::min(kNB, F.npiv - k);
+        const int t0 = k + w;
+        tasks.push_back({f, T_DIAG, (int16_t)s, 0, 0});
+        ++D.ntasks;
+        if (t0 >= F.nf) continue;
+        const int a0 = t0 / kTile;
+        for (int a = a0; a < D.tiles; ++a) tasks.push_back({f, T_ROWS, (int16_t)s, a, 0}), ++D.ntasks;
+        for (int b = a0; b < D.tiles; ++b) tasks.push_back({f, T_COLS, (int16_t)s, 0, b}), ++D.ntasks;
+        // lookahead order: tiles the next panel needs first
+        const int kn = t0, an = kn / kTile;
+        std::vector<std::pair<int, int>> order;
+        if (s + 1 < steps) {
+          order.push_back({an, an});
+          for (int a = a0; a < D.tiles; ++a)
+            if (a != an) order.push_back({a, an});
+          for (int b = a0; b < D.tiles; ++b)
+            if (b != an) order.push_back({an, b});
+        }
+        for (int a = a0; a < D.tiles; ++a)
+          for (int b = a0; b < D.tiles; ++b) {
+            if (s + 1 < steps && (a == an || b == an)) continue;
+            order.push_back({a, b});
+          }
+        for (auto& ab : order) {
+          tasks.push_back({f, T_UPD, (int16_t)s, ab.first, ab.second});
+          ++D.ntasks;
+          const double rr = std::min(F.nf, (ab.first + 1) * kTile) - std::max(ab.first * kTile, t0);
+          const double cc = std::min(F.nf, (ab.second + 1) * kTile) - std::max(ab.second * kTile, t0);
+          P->flops_upd += 2.0 * w * rr * cc;
+        }
+      }
+    }
+  }
+  P->ntasks = static_cast<int>(tasks.size());
+  P->nfronts = nfr;
+  P->ntile = std::max(1, tile_off);
+  P->nflag = std::max(1, flag_off);
+  if (rc_prefix.empty()) rc_prefix.push_back(0);
+  if (tasks.empty()) tasks.push_back({0, T_SMALL, 0, 0, 0});
+  P->d_tasks.upload(tasks.data(), sizeof(Task) * tasks.size(), fe.stream);
+  P->d_dag.upload(dag.data(), sizeof(FrontDag) * nfr, fe.stream);
+  P->d_rc.upload(rc_prefix.data(), sizeof(int32_t) * rc_prefix.size(), fe.stream);
+  P->d_cnt.alloc(sizeof(int) * kCnt * nfr);
+  P->d_tile.alloc(sizeof(int) * P->ntile);
+  P->d_flagbits.alloc(sizeof(unsigned long long) * P->nflag);
+  P->d_backup.alloc(sizeof(double) * std::max<int64_t>(1, backup));
+  P->d_ticket.alloc(sizeof(int) * 4);
+  fe.d_scratch.alloc(sizeof(double) * std::max(1, slot) * 2 * kNB * kNB);
+  const size_t small_smem = sizeof(double) * static_cast<size_t>(max_small | 1) * max_small;
+  const size_t tile_smem = sizeof(double) * 2 * kNB * kTSP;
+  const size_t rows_smem = sizeof(double) * ((kTile + 1) * kNB + kNB * kNB + 64);
+  P->smem = std::max({small_smem, tile_smem, rows_smem, size_t(16 * 1024)});
+  RQB_CUDA(cudaFuncSetAttribute(factor_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(P->smem)));
+  int nsm = 148, occ = 1;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
+  RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_dag_kernel, kDT, P->smem));
+  P->grid = std::max(1, std::min(P->ntasks, nsm * std::max(1, occ)));
+  fe.dag_ntasks = P->ntasks;
+  fe.dag.reset(P.release());
+}
+
+void rqb_dag_enqueue(FactorEngine& fe) {
+  DagPlan& P = *fe.dag;
+  RQB_CUDA(cudaMemsetAsync(P.d_cnt.p, 0, P.d_cnt.bytes, fe.stream));
+  RQB_CUDA(cudaMemsetAsync(P.d_tile.p, 0, P.d_tile.bytes, fe.stream));
+  RQB_CUDA(cudaMemsetAsync(P.d_flagbits.p, 0, P.d_flagbits.bytes, fe.stream));
+  RQB_CUDA(cudaMemsetAsync(P.d_ticket.p, 0, P.d_ticket.bytes, fe.stream));
+  DagArgs A;
+  A.fronts = fe.d_fronts.as<FrontDev>();
+  A.dag = P.d_dag.as<FrontDag>();
+  A.tasks = P.d_tasks.as<Task>();
+  A.ntasks = P.ntasks;
+  A.inv = fe.d_inv.as<int32_t>();
+  A.pool = fe.d_pool.as<double>();
+  A.ipiv = fe.d_ipiv.as<int32_t>();
+  A.scratch = fe.d_scratch.as<double>();
+  A.backup = P.d_backup.as<double>();
+  A.cnt = P.d_cnt.as<int>();
+  A.tile_step = P.d_tile.as<int>();
+  A.rc_prefix = P.d_rc.as<int32_t>();
+  A.flagbits = P.d_flagbits.as<unsigned long long>();
+  A.flags = fe.d_flags.as<int>();
+  A.ticket = P.d_ticket.as<int>();
+  A.prof = nullptr;
+  if (fe.dag_prof_enabled) {
+    if (!P.d_prof.p) P.d_prof.alloc(sizeof(unsigned long long) * 32);
+    RQB_CUDA(cudaMemsetAsync(P.d_prof.p, 0, P.d_prof.bytes, fe.stream));
+    A.prof = P.d_prof.as<unsigned long long>();
+  }
+  factor_dag_kernel<<<P.grid, kDT, P.smem, fe.stream>>>(A);
+  RQB_CUDA(cudaGetLastError());
+}
+
+// Per task type (SMALL, ASM, DIAG, ROWS, COLS, UPD): busy ms, wait ms (summed
+// over CTAs, SM clock), count; plus the persistent grid size. Profiling run.
+void rqb_dag_profile(FactorEngine& fe, double* out) {
+  if (!fe.dag) fail(errc::config, "the task-DAG factorization is not active");
+  fe.dag_prof_enabled = true;
+  fe.enqueue_factor();
+  fe.dag_prof_enabled = false;
+  unsigned long long h[32];
+  RQB_CUDA(cudaMemcpyAsync(h, fe.dag->d_prof.p, sizeof(h), cudaMemcpyDeviceToHost, fe.stream));
+  RQB_CUDA(cudaStreamSynchronize(fe.stream));
+  int clk_khz = 1965000;
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, fe.device);
+  for (int t = 0; t < 6; ++t) {
+    out[3 * t + 0] = h[3 * t + 0] / (clk_khz * 1.0);  // cycles / kHz = ms
+    out[3 * t + 1] = h[3 * t + 1] / (clk_khz * 1.0);
+    out[3 * t + 2] = static_cast<double>(h[3 * t + 2]);
+  }
+  out[18] = fe.dag->grid;
+  out[19] = fe.dag->ntasks;
+}
+
+void DagPlanDeleter::operator()(DagPlan* p) const { delete p; }
+
+}  // namespace rqb

@@ -67,10 +67,22 @@ struct KernelTimer {
   void collect(double* ms, int64_t* count, int nkinds);
 };
 
-// factor kernel classes: scatter, extend_add, front_lu_smem, panel_lu, panel_apply, schur_dmma
-constexpr int kFactorKinds = 6;
+// factor kernel classes: scatter, extend_add, front_lu_smem, panel_lu, panel_apply
+// (+ net_rowperm), schur_dmma, factor_dag (persistent task-DAG kernel)
+constexpr int kFactorKinds = 7;
+
+struct DagPlan;
+struct DagPlanDeleter {
+  void operator()(DagPlan* p) const;
+};
 
 struct FactorEngine {
+  // factorization schedule: persistent task-DAG kernel (default) or the
+  // level-synchronous multi-launch path (RQB_FACTOR=level, kept for A/B runs)
+  bool use_dag = true;
+  std::unique_ptr<DagPlan, DagPlanDeleter> dag;
+  int dag_ntasks = 0;
+  bool dag_prof_enabled = false;
   Symbolic sym;
   int64_t n = 0, nnz = 0;
   int device = 0;
@@ -114,6 +126,9 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
                        const double* vu, double sigma, double* xl);
 void rqb_solve_set_attrs(int maxnf);
 void rqb_solve_prepare(FactorEngine& fe);
+void rqb_dag_build(FactorEngine& fe);
+void rqb_dag_enqueue(FactorEngine& fe);
+void rqb_dag_profile(FactorEngine& fe, double* out);
 void rqb_rowperm_enqueue(FactorEngine& fe);
 
 // Shift-invert operator on the linearised pencil, real FP64, device resident.

@@ -304,6 +304,14 @@ int rq_factor_profile(rq_factor_t* f, double* ms, int64_t* launches, double* wor
   });
 }
 
+int rq_factor_dag_profile(rq_factor_t* f, double* out) {
+  return guarded([&] {
+    need(f, "factor");
+    need(out, "out");
+    rqb::rqb_dag_profile(*f->fe, out);
+  });
+}
+
 void rq_factor_destroy(rq_factor_t* f) { delete f; }
 
 int rq_operator_create(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,

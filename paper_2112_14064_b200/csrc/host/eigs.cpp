@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <numeric>
 #include <sstream>
 
@@ -156,6 +157,13 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   std::vector<double> final_vecs_re, final_vecs_im;
   std::vector<double> ha((m + 1) * (m + 1)), hb((m + 1) * (m + 1)), betas(m + 1);
   double t_solve = 0, t_orth = 0;
+  std::map<std::pair<int, const double*>, cudaGraphExec_t> graphs;
+  struct GraphFree {
+    std::map<std::pair<int, const double*>, cudaGraphExec_t>* g;
+    ~GraphFree() {
+      for (auto& kv : *g) cudaGraphExecDestroy(kv.second);
+    }
+  } graph_free{&graphs};
 
   while (true) {
     // max_restarts bounds each Krylov-Schur pass (the main run and every guard
@@ -163,42 +171,62 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     if (pass_cycles >= o.max_restarts) break;
     ++cycles;
     ++pass_cycles;
-    // ---- Arnoldi steps k .. m-1 ----
-    for (int j = k; j < m; ++j) {
-      double* vj = V + static_cast<int64_t>(j) * n2;
-      if (o.profile) cuda_check(cudaEventRecord(e_a, st), "ev");
-      op.apply(vj, r);
-      if (o.profile) {
-        cuda_check(cudaEventRecord(e_b, st), "ev");
-        cuda_check(cudaEventSynchronize(e_b), "ev");
-        float ms;
-        cudaEventElapsedTime(&ms, e_a, e_b);
-        t_solve += ms;
+    // ---- Arnoldi steps k .. m-1: one CUDA graph per (start, basis buffer) ----
+    auto enqueue_steps = [&](bool prof) {
+      for (int j = k; j < m; ++j) {
+        double* vj = V + static_cast<int64_t>(j) * n2;
+        if (prof) cuda_check(cudaEventRecord(e_a, st), "ev");
+        op.apply(vj, r);
+        if (prof) {
+          cuda_check(cudaEventRecord(e_b, st), "ev");
+          cuda_check(cudaEventSynchronize(e_b), "ev");
+          float ms;
+          cudaEventElapsedTime(&ms, e_a, e_b);
+          t_solve += ms;
+          cuda_check(cudaEventRecord(e_a, st), "ev");
+        }
+        double* hA = dHa.as<double>() + static_cast<int64_t>(j) * (m + 1);
+        double* hB = dHb.as<double>() + static_cast<int64_t>(j) * (m + 1);
+        op.bvec(r, w);
+        op.gemv_t(V, j + 1, w, hA);
+        op.gemv_n(V, j + 1, hA, r, nullptr);
+        op.bvec(r, w);
+        op.gemv_t(V, j + 1, w, hB);
+        op.gemv_n(V, j + 1, hB, r, nullptr);
+        op.bvec(r, w);
+        op.bnorm_normalize(r, w, dBeta.as<double>() + j, V + static_cast<int64_t>(j + 1) * n2);
+        if (prof) {
+          cuda_check(cudaEventRecord(e_b, st), "ev");
+          cuda_check(cudaEventSynchronize(e_b), "ev");
+          float ms;
+          cudaEventElapsedTime(&ms, e_a, e_b);
+          t_orth += ms;
+        }
       }
+    };
+    if (o.profile) {
+      enqueue_steps(true);
+    } else {
+      const std::pair<int, const double*> key{k, V};
+      auto it = graphs.find(key);
+      if (it == graphs.end()) {
+        cudaGraph_t gr;
+        cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+        enqueue_steps(false);
+        cuda_check(cudaStreamEndCapture(st, &gr), "capture end");
+        cudaGraphExec_t ex;
+        cuda_check(cudaGraphInstantiate(&ex, gr, 0), "graph instantiate");
+        cudaGraphDestroy(gr);
+        it = graphs.emplace(key, ex).first;
+      }
+      cuda_check(cudaGraphLaunch(it->second, st), "graph launch");
+      res.graph_launches += 1;
+    }
+    for (int j = k; j < m; ++j) {
       L.n_fb += 1;
       L.macs_fb += fb_macs;
-      L.n_mv += 3;  // sigma M v_u, C v_u, M v_l (fused)
-      L.macs_mv += 3 * nnz;
-      if (o.profile) cuda_check(cudaEventRecord(e_a, st), "ev");
-      double* hA = dHa.as<double>() + static_cast<int64_t>(j) * (m + 1);
-      double* hB = dHb.as<double>() + static_cast<int64_t>(j) * (m + 1);
-      op.bvec(r, w);
-      op.gemv_t(V, j + 1, w, hA);
-      op.gemv_n(V, j + 1, hA, r, nullptr);
-      op.bvec(r, w);
-      op.gemv_t(V, j + 1, w, hB);
-      op.gemv_n(V, j + 1, hB, r, nullptr);
-      op.bvec(r, w);
-      op.bnorm_normalize(r, w, dBeta.as<double>() + j, V + static_cast<int64_t>(j + 1) * n2);
-      if (o.profile) {
-        cuda_check(cudaEventRecord(e_b, st), "ev");
-        cuda_check(cudaEventSynchronize(e_b), "ev");
-        float ms;
-        cudaEventElapsedTime(&ms, e_a, e_b);
-        t_orth += ms;
-      }
-      L.n_mv += 3;
-      L.macs_mv += 3 * nnz;
+      L.n_mv += 6;  // sigma M v_u, C v_u, M v_l (fused) + 3 B-products of CGS2
+      L.macs_mv += 6 * nnz;
       L.n_vv += 4 * (j + 1) + 2;
       L.macs_vv += (4.0 * (j + 1) + 2) * n2;
     }

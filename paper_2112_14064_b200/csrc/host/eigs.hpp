@@ -41,6 +41,7 @@ struct EigsResult {
   int64_t launches = 0;
   double t_total_ms = 0, t_solve_ms = 0, t_orth_ms = 0;
   double max_restart_defect = 0;  // max ||H Q - Q T|| / ||H|| over restarts
+  int64_t graph_launches = 0;     // one CUDA graph replay per Krylov-Schur cycle
 };
 
 // norms1 = {||K||_1, ||C||_1, ||M||_1} of the (scaled) pencil used by the

@@ -81,7 +81,7 @@ def test_dense_pivoting_matches_oracle(n):
     assert np.array_equal(ipiv, ipo)
     assert f.info()["swaps"] == of.swaps > 0
     err = np.max(np.abs(F[:n, :n] - Fo.real)) / np.max(np.abs(Fo))
-    assert err <= 1e-11
+    assert err <= 1e-13 * n  # same pivots; summation order differs (growth ~ n eps)
     b = rng.standard_normal(n)
     x = f.solve(b)
     assert np.linalg.norm(A @ x - b) <= 1e-11 * np.linalg.norm(A, 1) * np.linalg.norm(x)
