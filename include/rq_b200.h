@@ -158,9 +158,10 @@ int rq_factor_front_export(const rq_factor_t* f, int64_t front, double* dense, i
  * launches, algorithmic work (real flops; bytes for classes 0-1). */
 int rq_factor_profile(rq_factor_t* f, double* ms, int64_t* launches, double* work);
 /* Task-level profile of the persistent task-DAG factorization (profiling run):
- * out[3t+0] busy ms, out[3t+1] dependency-wait ms (both summed over CTAs),
- * out[3t+2] task count, for t = {SMALL, ASM, DIAG, ROWS, COLS, UPDATE};
- * out[18] persistent grid size, out[19] tasks. double[20]. */
+ * out[3t+0] busy ms (summed over CTAs), out[3t+1] reserved (0), out[3t+2] task
+ * count, for t = {SMALL, ASM, DIAG, ROWS, COLS, UPDATE}; out[18] persistent
+ * grid size, out[19] tasks, out[20] ready-queue wait ms summed over CTAs.
+ * double[24]. */
 int rq_factor_dag_profile(rq_factor_t* f, double* out);
 void rq_factor_destroy(rq_factor_t* f);
 

@@ -511,6 +511,7 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
     D.child0 = D.nchild > 0 ? F.children[0] : -1;
     D.child1 = D.nchild > 1 ? F.children[1] : -1;
     D.scratch = -1;
+    D.rel_off = 0;
     D.inv_off = static_cast<int64_t>(inv.size());
     const int32_t* prow = sym.rows.data() + F.rows_off;
     for (int32_t c : F.children) {
@@ -519,10 +520,12 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
       // child CB rows are a sorted subset of the parent's rows
       std::vector<int32_t> m(F.nf, -1);
       int pi = 0;
+      fronts_h[c].rel_off = static_cast<int64_t>(rel_h.size());
       for (int t = C.npiv; t < C.nf; ++t) {
         while (pi < F.nf && prow[pi] < crow[t]) ++pi;
         if (pi == F.nf || prow[pi] != crow[t]) fail(errc::generic, "child CB row missing in parent");
         m[pi] = t;
+        rel_h.push_back(pi);
       }
       inv.insert(inv.end(), m.begin(), m.end());
     }
@@ -581,6 +584,8 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
   if (inv.empty()) inv.push_back(-1);
   if (lists.empty()) lists.push_back(0);
   d_inv.upload(inv.data(), sizeof(int32_t) * inv.size(), stream);
+  if (rel_h.empty()) rel_h.push_back(0);
+  d_rel.upload(rel_h.data(), sizeof(int32_t) * rel_h.size(), stream);
   d_lists.upload(lists.data(), sizeof(int32_t) * lists.size(), stream);
   d_ipiv.alloc(sizeof(int32_t) * n);
   d_scratch.alloc(sizeof(double) * std::max<int64_t>(1, nscratch) * 2 * kNB * kNB);

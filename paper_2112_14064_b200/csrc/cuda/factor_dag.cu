@@ -24,10 +24,14 @@
 // backup and redoes it with exact threshold partial pivoting (prefer the
 // diagonal, ties -> lowest row, singular < 1e-300), full-row swaps and U12.
 // Then it releases the panel to the UPD tasks.
-// CTAs draw tasks with an atomic ticket: a task only waits (spins on counters)
-// for tasks with smaller tickets that are already running, so the schedule is
-// deadlock-free without co-residency assumptions. Data produced inside the
-// kernel is read with ld.global.cg (L1 bypass); publication is
+// Dataflow scheduling: every task carries a count of unfinished predecessors
+// (host-built template, copied in per factorization); a finishing task
+// decrements its successors and the one that reaches zero is pushed on a global
+// FIFO ready queue. CTAs pop queue slots in order and only ever run ready
+// tasks: no task-level spinning, no level barriers, no per-panel launches
+// (the persistent grid idles only when nothing is ready). Every slot is
+// eventually filled (DAG), so the schedule cannot deadlock. Data produced
+// inside the kernel is read with ld.global.cg (L1 bypass); publication is
 // __threadfence + atomic.
 #include <algorithm>
 #include <cstdio>
@@ -63,7 +67,11 @@ struct FrontDag {
   int32_t rc_off;      // offset into rc_prefix[] (steps + 1 entries)
   int32_t flag_off;    // offset into flagbits[] (one per step)
   int32_t slot;        // scratch slot (inverses), -1 small
-  int32_t pad;
+  int32_t bnd_off;     // per child: (tiles + 1) first child CB column of each 64-column block
+  int32_t task_base;   // first task of this front
+  int32_t sb_off;      // offset into step_base[] (steps + 1 entries)
+  int32_t parent;      // parent front (-1 root)
+  int32_t pad2;
   int64_t backup_off;  // panel backup nf x 32, then A12 backup 32 x nf
 };
 
@@ -73,6 +81,8 @@ struct DagArgs {
   const Task* tasks;
   int ntasks;
   const int32_t* inv;
+  const int32_t* rel;   // child CB row -> parent-local row (FrontDev::rel_off)
+  const int32_t* bnd;   // FrontDag::bnd_off
   double* pool;
   int32_t* ipiv;
   double* scratch;
@@ -82,8 +92,13 @@ struct DagArgs {
   const int32_t* rc_prefix;
   unsigned long long* flagbits;
   int* flags;   // [0] singular, [1] swaps
-  int* ticket;
   unsigned long long* prof;  // optional: per task type {work cycles, wait cycles, count}
+  double* small_backup;      // per CTA: 160 x 16 panel backup of the SMALL path
+  int* deps;                 // remaining predecessors per task
+  int* queue;                // ready queue (task ids, -1 = not yet pushed)
+  int* qhead;
+  int* qtail;
+  const int32_t* step_base;  // FrontDag::sb_off: first task of every panel step
 };
 
 __device__ __forceinline__ void spin_ge(const int* p, int target) {
@@ -111,29 +126,37 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return m;
 }
 
-// Children's Schur blocks into columns [c0, c1) of front F; dst column c is at
-// dst + (c - c0) * ldd (shared or global memory).
-__device__ void extend_add_cols(const DagArgs& A, const FrontDev& F, int c0, int c1, double* dst,
-                                int64_t ldd, bool dst_global) {
-  const int32_t* inv0 = A.inv + F.inv_off;
+// Children's Schur blocks into front F (child-centric scatter, atomic-free:
+// rel is injective, children are applied one after the other). For child ch
+// only its CB columns [lo[ch], hi[ch]) are applied; parent column c lives at
+// dst + c * ldd (shared or global memory).
+__device__ void extend_add(const DagArgs& A, const FrontDev& F, const int* lo, const int* hi,
+                           double* dst, int64_t ldd, bool dst_global) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int ch = 0; ch < F.nchild; ++ch) {
-    const int32_t* invc = inv0 + (int64_t)ch * F.nf;
     const FrontDev C = A.fronts[ch == 0 ? F.child0 : F.child1];
-    const double* cp = A.pool + C.off;
-    for (int c = c0 + warp; c < c1; c += kDT / 32) {
-      const int ic = invc[c];
-      if (ic < 0) continue;
-      const double* ccol = cp + (int64_t)ic * C.ld;
-      double* dcol = dst + (int64_t)(c - c0) * ldd;
-      for (int r = lane; r < F.nf; r += 32) {
-        const int ir = invc[r];
-        if (ir < 0) continue;
-        const double v = __ldcg(&ccol[ir]);
-        if (dst_global)
-          dcol[r] = __ldcg(&dcol[r]) + v;  // L1 may hold lines other SMs rewrote
-        else
-          dcol[r] += v;
+    const int32_t* rel = A.rel + C.rel_off;
+    const int ncb = C.nf - C.npiv;
+    const double* cp = A.pool + C.off + C.npiv + (int64_t)C.npiv * C.ld;  // CB block origin
+    for (int ic = lo[ch] + warp; ic < hi[ch]; ic += kDT / 32) {
+      const int pc = __ldg(&rel[ic]);
+      const double* src = cp + (int64_t)ic * C.ld;
+      double* dcol = dst + (int64_t)pc * ldd;
+      for (int k0 = 0; k0 < ncb; k0 += 128) {
+        int pr[4];
+        double v[4], d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kk = k0 + lane + 32 * u;
+          pr[u] = kk < ncb ? __ldg(&rel[kk]) : -1;
+          v[u] = kk < ncb ? __ldcg(&src[kk]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (pr[u] >= 0) d[u] = dst_global ? __ldcg(&dcol[pr[u]]) : dcol[pr[u]];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (pr[u] >= 0) dcol[pr[u]] = d[u] + v[u];
       }
     }
     __syncthreads();  // two children may touch the same entries
@@ -148,10 +171,56 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
   for (int c = warp; c < nf; c += kDT / 32)
     for (int r = lane; r < nf; r += 32) sm[r + c * lds] = __ldcg(&g[r + (int64_t)c * F.ld]);
   __syncthreads();
-  extend_add_cols(A, F, 0, nf, sm, lds, false);
+  {
+    int lo[2] = {0, 0}, hi[2] = {0, 0};
+    if (F.nchild > 0) hi[0] = A.fronts[F.child0].nf - A.fronts[F.child0].npiv;
+    if (F.nchild > 1) hi[1] = A.fronts[F.child1].nf - A.fronts[F.child1].npiv;
+    extend_add(A, F, lo, hi, sm, lds, false);
+  }
+  __shared__ double red_s[kDT / 32];
+  __shared__ int any_swap_s;
+  double* pbk = A.small_backup + (int64_t)blockIdx.x * kSmallNf * kPB;
   for (int k0 = 0; k0 < np; k0 += kPB) {
     const int pw = min(kPB, np - k0);
-    if (warp == 0) {
+    // ---- speculative unpivoted panel: thread t owns row t; one barrier per column
+    if (tid < nf && tid >= k0)
+      for (int c = 0; c < pw; ++c) pbk[tid + c * kSmallNf] = sm[tid + (k0 + c) * lds];
+    double lm = 0.0;
+    bool sing = false;
+    for (int j = k0; j < k0 + pw; ++j) {
+      const double ujj = sm[j + j * lds];
+      sing = sing || !(fabs(ujj) >= kSingularTiny);
+      const int i = tid;
+      if (i > j && i < nf) {
+        const double l = sm[i + j * lds] / ujj;
+        sm[i + j * lds] = l;
+        if (i < np) lm = fmax(lm, fabs(l));
+        for (int c = j + 1; c < k0 + pw; ++c) sm[i + c * lds] -= l * sm[j + c * lds];
+      }
+      __syncthreads();
+    }
+    if (sing) lm = 1e300;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+    if (lane == 0) red_s[warp] = lm;
+    if (tid == 0) any_swap_s = 0;
+    __syncthreads();
+    double lmax = 0.0;
+    for (int q = 0; q < kDT / 32; ++q) lmax = fmax(lmax, red_s[q]);
+    if (lmax <= kLmax) {
+      if (tid < pw) {
+        A.ipiv[F.start + k0 + tid] = k0 + tid;
+        piv_sh[tid] = k0 + tid;
+      }
+    } else {
+      // restore the panel, redo it with exact threshold pivoting (warp 0)
+      if (tid < nf && tid >= k0)
+        for (int c = 0; c < pw; ++c) sm[tid + (k0 + c) * lds] = pbk[tid + c * kSmallNf];
+      __syncthreads();
+      if (tid == 0) any_swap_s = 1;
+    }
+    __syncthreads();
+    if (any_swap_s && warp == 0) {
       for (int j = k0; j < k0 + pw; ++j) {
         double best = -1.0;
         int bi = j;
@@ -235,67 +304,104 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
     for (int r = lane; r < nf; r += 32) g[r + (int64_t)c * F.ld] = sm[r + c * lds];
 }
 
-// inverses of the unit-lower / upper factors of a w x w block T (stride 33);
-// thread c (< 32) builds column c of both
-__device__ void build_inverses(const double* T, int w, double* invL, double* invU) {
-  const int c = threadIdx.x;
-  if (c >= kNB) return;
-  for (int i = 0; i < kNB; ++i) invL[i + c * kNB] = 0.0, invU[i + c * kNB] = 0.0;
-  if (c >= w) return;
-  invL[c + c * kNB] = 1.0;
-  for (int i = c + 1; i < w; ++i) {
-    double s = 0.0;
-    for (int t = c; t < i; ++t) s += T[i + t * 33] * invL[t + c * kNB];
-    invL[i + c * kNB] = -s;
-  }
-  invU[c + c * kNB] = 1.0 / T[c + c * 33];
-  for (int i = c - 1; i >= 0; --i) {
-    double s = 0.0;
-    for (int t = i + 1; t <= c; ++t) s += T[i + t * 33] * invU[t + c * kNB];
-    invU[i + c * kNB] = -s / T[i + i * 33];
-  }
-}
-
+// DIAG: 32x32 diagonal block of panel s, unpivoted (speculative), entirely in
+// registers of warp 0 (row `lane` per thread, shuffles broadcast the pivot
+// row); inv(L11) by warp 0 and inv(U11) by warp 1, column `lane` per thread.
 __device__ void diag_task(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s, double* sm) {
   const int k = s * kNB, w = min(kNB, F.npiv - k);
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* T = sm;               // 32 x 33
-  double* red = sm + 32 * 33;   // block reduction scratch
+  constexpr unsigned FULL = 0xffffffffu;
+  double* T = sm;               // 32 x 33: the factored block
+  double* red = sm + 32 * 33;
   double* bk = A.backup + D.backup_off;
-  for (int idx = tid; idx < w * w; idx += kDT) {
-    const int r = idx % w, c = idx / w;
-    const double v = __ldcg(&g[(k + r) + (int64_t)(k + c) * ld]);
-    T[r + c * 33] = v;
-    bk[(k + r) + (int64_t)c * F.nf] = v;
+  {
+    double v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * kDT, r = idx % 32, c = idx / 32;
+      v[i] = (r < w && c < w) ? __ldcg(&g[(k + r) + (int64_t)(k + c) * ld]) : (r == c ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * kDT, r = idx % 32, c = idx / 32;
+      T[r + c * 33] = v[i];
+      if (r < w && c < w) bk[(k + r) + (int64_t)c * F.nf] = v[i];
+    }
   }
   __syncthreads();
   double lm = 0.0;
   if (warp == 0) {
-    for (int j = 0; j < w; ++j) {
-      const double ujj = T[j + j * 33];
-      if (!(fabs(ujj) >= kSingularTiny)) lm = 1e300;  // force the pivoted fallback
-      double l = 0.0;
-      if (lane > j && lane < w) {
-        l = T[lane + j * 33] / ujj;
-        T[lane + j * 33] = l;
-        lm = fmax(lm, fabs(l));
+    double r[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r[c] = T[lane + c * 33];
+    bool sing = false;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double ujj = __shfl_sync(FULL, r[j], j);
+      if (j < w && !(fabs(ujj) >= kSingularTiny)) sing = true;
+      const double rinv = 1.0 / ujj;
+      const double l = r[j] * rinv;
+      if (lane > j) {
+        r[j] = l;
+        if (lane < w) lm = fmax(lm, fabs(l));
       }
-      __syncwarp();
-      if (lane > j && lane < w)
-        for (int c = j + 1; c < w; ++c) T[lane + c * 33] -= l * T[j + c * 33];
-      __syncwarp();
+#pragma unroll
+      for (int c = j + 1; c < 32; ++c) {
+        const double u = __shfl_sync(FULL, r[c], j);
+        if (lane > j) r[c] -= l * u;
+      }
     }
+    if (sing) lm = 1e300;  // forces the exact pivoted fallback (singular detection there)
+#pragma unroll
+    for (int c = 0; c < 32; ++c) T[lane + c * 33] = r[c];
+    // inv(L11): lane c holds column c; X[i][c] = -sum_{q<i} L[i][q] X[q][c]
+    double x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int i = 1; i < 32; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < i; ++q) acc += __shfl_sync(FULL, r[q], i) * x[q];
+      if (i > lane) x[i] = -acc;
+    }
+    double* invL = A.scratch + (int64_t)D.slot * 2 * kNB * kNB;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) invL[i + lane * kNB] = (i < w && lane < w) ? x[i] : 0.0;
+  }
+  __syncthreads();
+  if (warp == 1) {
+    // inv(U11): lane c holds column c; Y[i][c] = -(sum_{q>i} U[i][q] Y[q][c]) / U[i][i]
+    double r[32], y[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r[c] = T[lane + c * 33];  // row `lane` of U
+    const double dinv = 1.0 / T[lane + lane * 33];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) y[i] = 0.0;
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+      const double di = __shfl_sync(FULL, dinv, i);
+      double acc = 0.0;
+#pragma unroll
+      for (int q = i + 1; q < 32; ++q) acc += __shfl_sync(FULL, r[q], i) * y[q];
+      if (i == lane) y[i] = di;
+      else if (i < lane) y[i] = -acc * di;
+    }
+    double* invU = A.scratch + (int64_t)D.slot * 2 * kNB * kNB + kNB * kNB;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) invU[i + lane * kNB] = (i < w && lane < w) ? y[i] : 0.0;
   }
   lm = block_max(warp == 0 ? lm : 0.0, red);
-  for (int idx = tid; idx < w * w; idx += kDT) {
-    const int r = idx % w, c = idx / w;
-    g[(k + r) + (int64_t)(k + c) * ld] = T[r + c * 33];
+  {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * kDT, rr = idx % 32, c = idx / 32;
+      if (rr < w && c < w) g[(k + rr) + (int64_t)(k + c) * ld] = T[rr + c * 33];
+    }
   }
   for (int j = tid; j < w; j += kDT) A.ipiv[F.start + k + j] = k + j;
-  double* invL = A.scratch + (int64_t)D.slot * 2 * kNB * kNB;
-  build_inverses(T, w, invL, invL + kNB * kNB);
   if (tid == 0) atomicMax(&A.flagbits[D.flag_off + s], (unsigned long long)__double_as_longlong(lm));
 }
 
@@ -313,12 +419,23 @@ __device__ void rows_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   double* red = iU + kNB * kNB;
   double* bk = A.backup + D.backup_off;
   const double* invU = A.scratch + (int64_t)D.slot * 2 * kNB * kNB + kNB * kNB;
-  for (int i = tid; i < kNB * kNB; i += kDT) iU[i] = __ldcg(&invU[i]);
-  for (int idx = tid; idx < nr * w; idx += kDT) {
-    const int r = idx % nr, c = idx / nr;
-    const double v = __ldcg(&g[(r0 + r) + (int64_t)(k + c) * ld]);
-    P[r + c * kPS] = v;
-    bk[(r0 + r) + (int64_t)c * F.nf] = v;
+  {
+    double vu[4], vp[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) vu[i] = __ldcg(&invU[tid + i * kDT]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + i * kDT, r = idx % kTile, c = idx / kTile;
+      vp[i] = (r < nr && c < w) ? __ldcg(&g[(r0 + r) + (int64_t)(k + c) * ld]) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) iU[tid + i * kDT] = vu[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + i * kDT, r = idx % kTile, c = idx / kTile;
+      P[r + c * kPS] = vp[i];
+      if (r < nr && c < w) bk[(r0 + r) + (int64_t)c * F.nf] = vp[i];
+    }
   }
   __syncthreads();
   double lm = 0.0;
@@ -347,12 +464,23 @@ __device__ void cols_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   double* iL = sm + 64 * 33;
   double* bk2 = A.backup + D.backup_off + (int64_t)F.nf * kNB;
   const double* invL = A.scratch + (int64_t)D.slot * 2 * kNB * kNB;
-  for (int i = tid; i < kNB * kNB; i += kDT) iL[i] = __ldcg(&invL[i]);
-  for (int idx = tid; idx < nc * w; idx += kDT) {
-    const int r = idx % w, c = idx / w;
-    const double v = __ldcg(&g[(k + r) + (int64_t)(c0 + c) * ld]);
-    P[r + c * 33] = v;
-    bk2[r + (int64_t)(c0 + c) * kNB] = v;
+  {
+    double vl[4], vp[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) vl[i] = __ldcg(&invL[tid + i * kDT]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + i * kDT, r = idx % kNB, c = idx / kNB;
+      vp[i] = (r < w && c < nc) ? __ldcg(&g[(k + r) + (int64_t)(c0 + c) * ld]) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) iL[tid + i * kDT] = vl[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + i * kDT, r = idx % kNB, c = idx / kNB;
+      P[r + c * 33] = vp[i];
+      if (r < w && c < nc) bk2[r + (int64_t)(c0 + c) * kNB] = vp[i];
+    }
   }
   __syncthreads();
   const int c = tid & 63, q = tid >> 6;
@@ -374,18 +502,41 @@ __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int 
   double* Bs = sm + kNB * kTSP; // [kk][n]
   const int tid = threadIdx.x;
   const int nr = r1 - r0, nc = c1 - c0;
-  for (int idx = tid; idx < kNB * kTile; idx += kDT) {
-    const int kk = idx / kTile, m = idx % kTile;
-    As[kk * kTSP + m] = (kk < w && m < nr) ? __ldcg(&g[(r0 + m) + (int64_t)(k + kk) * ld]) : 0.0;
-  }
-  for (int idx = tid; idx < kNB * kTile; idx += kDT) {
-    const int kk = idx % kNB, n = idx / kNB;
-    Bs[kk * kTSP + n] = (kk < w && n < nc) ? __ldcg(&g[(k + kk) + (int64_t)(c0 + n) * ld]) : 0.0;
-  }
-  __syncthreads();
   const int lane = tid & 31, warp = tid >> 5;  // 8 warps: 2 (m) x 4 (n) of 32 x 16
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
   const int gid = lane >> 2, tig = lane & 3;
+  // issue every global load of the task up front (A, B panels and this
+  // thread's C fragment) so their latencies overlap
+  constexpr int kLd = kNB * kTile / kDT;  // 8 per operand
+  double va[kLd], vb[kLd], cv[2][2][4];
+#pragma unroll
+  for (int i = 0; i < kLd; ++i) {
+    const int idx = tid + i * kDT;
+    const int kk = idx / kTile, m = idx % kTile;
+    va[i] = (kk < w && m < nr) ? __ldcg(&g[(r0 + m) + (int64_t)(k + kk) * ld]) : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < kLd; ++i) {
+    const int idx = tid + i * kDT;
+    const int kk = idx % kNB, n = idx / kNB;
+    vb[i] = (kk < w && n < nc) ? __ldcg(&g[(k + kk) + (int64_t)(c0 + n) * ld]) : 0.0;
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = wm + x * 16 + gid + (e >> 1) * 8, c = wn + y * 8 + 2 * tig + (e & 1);
+        cv[x][y][e] = (r < nr && c < nc) ? __ldcg(&g[(r0 + r) + (int64_t)(c0 + c) * ld]) : 0.0;
+      }
+#pragma unroll
+  for (int i = 0; i < kLd; ++i) {
+    const int idx = tid + i * kDT;
+    As[(idx / kTile) * kTSP + idx % kTile] = va[i];
+    Bs[(idx % kNB) * kTSP + idx / kNB] = vb[i];
+  }
+  __syncthreads();
   double acc[2][2][4];
 #pragma unroll
   for (int x = 0; x < 2; ++x)
@@ -416,10 +567,7 @@ __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int 
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = wm + x * 16 + gid + (e >> 1) * 8, c = wn + y * 8 + 2 * tig + (e & 1);
-        if (r < nr && c < nc) {
-          double* p = &g[(r0 + r) + (int64_t)(c0 + c) * ld];
-          *p = __ldcg(p) - acc[x][y][e];
-        }
+        if (r < nr && c < nc) g[(r0 + r) + (int64_t)(c0 + c) * ld] = cv[x][y][e] - acc[x][y][e];
       }
 }
 
@@ -504,66 +652,77 @@ __device__ void panel_fallback(const DagArgs& A, const FrontDev& F, const FrontD
   __syncthreads();
 }
 
+// Task index helpers (tasks of a front are contiguous; see rqb_dag_build)
+__device__ __forceinline__ int a0_of(const FrontDev& F, int s) {
+  const int k = s * kNB, w = min(kNB, F.npiv - k);
+  return (k + w) / kTile;
+}
+
+__device__ __forceinline__ int idx_diag(const DagArgs& A, const FrontDag& D, int s) {
+  return A.step_base[D.sb_off + s];
+}
+__device__ __forceinline__ int idx_rows(const DagArgs& A, const FrontDag& D, const FrontDev& F, int s,
+                                         int a) {
+  return A.step_base[D.sb_off + s] + 1 + (a - a0_of(F, s));
+}
+__device__ __forceinline__ int idx_cols(const DagArgs& A, const FrontDag& D, const FrontDev& F, int s,
+                                         int b) {
+  const int a0 = a0_of(F, s);
+  return A.step_base[D.sb_off + s] + 1 + (D.tiles - a0) + (b - a0);
+}
+__device__ __forceinline__ int idx_upd(const DagArgs& A, const FrontDag& D, const FrontDev& F, int s, int a,
+                                        int b) {
+  const int a0 = a0_of(F, s), nr = D.tiles - a0;
+  return A.step_base[D.sb_off + s] + 1 + 2 * nr + (a - a0) * nr + (b - a0);
+}
+
+// One predecessor of task t completed: the last one pushes t on the ready queue.
+__device__ __forceinline__ void notify(const DagArgs& A, int t) {
+  if (atomicSub(&A.deps[t], 1) == 1) {
+    __threadfence();
+    const int slot = atomicAdd(A.qtail, 1);
+    atomicExch(&A.queue[slot], t);
+  }
+}
+
 __global__ void __launch_bounds__(kDT, 1) factor_dag_kernel(DagArgs A) {
   extern __shared__ double sm[];
-  __shared__ int task_s, last_s;
+  __shared__ int task_s, last_s, done_s;
   __shared__ int piv_sh[kPB];
   const int tid = threadIdx.x;
   for (;;) {
     __syncthreads();
-    if (tid == 0) task_s = atomicAdd(A.ticket, 1);
+    if (tid == 0) {
+      const long long t0 = A.prof ? clock64() : 0;
+      const int h = atomicAdd(A.qhead, 1);
+      int t = -1;
+      if (h < A.ntasks) {
+        while ((t = *((volatile int*)&A.queue[h])) < 0) __nanosleep(32);
+        __threadfence();
+      }
+      task_s = t;
+      if (A.prof && t >= 0) atomicAdd(&A.prof[20], (unsigned long long)(clock64() - t0));
+    }
     __syncthreads();
     const int t = task_s;
-    if (t >= A.ntasks) return;
+    if (t < 0) return;
     const Task T = A.tasks[t];
     const int f = T.front;
     const FrontDev F = A.fronts[f];
     const FrontDag D = A.dag[f];
     int* cnt = A.cnt + kCnt * f;
-    const long long t_start = A.prof ? clock64() : 0;
-    // ---- dependencies
-    if (tid == 0) {
-      switch (T.type) {
-        case T_SMALL:
-        case T_ASM:
-          if (F.nchild > 0) spin_ge(&A.cnt[kCnt * F.child0], A.dag[F.child0].ntasks);
-          if (F.nchild > 1) spin_ge(&A.cnt[kCnt * F.child1], A.dag[F.child1].ntasks);
-          break;
-        case T_DIAG:
-          if (T.step == 0) {
-            spin_ge(&cnt[1], D.nasm);
-          } else {
-            const int ap = (T.step * kNB) / kTile;
-            spin_ge(&A.tile_step[D.tile_off + ap * D.tiles + ap], T.step);
-          }
-          break;
-        case T_ROWS: {
-          const int bp = (T.step * kNB) / kTile;
-          spin_ge(&cnt[2], T.step + 1);
-          spin_ge(&A.tile_step[D.tile_off + T.a * D.tiles + bp], T.step);
-          break;
-        }
-        case T_COLS: {
-          const int ap = (T.step * kNB) / kTile;
-          spin_ge(&cnt[2], T.step + 1);
-          spin_ge(&A.tile_step[D.tile_off + ap * D.tiles + T.b], T.step);
-          break;
-        }
-        case T_UPD:
-          spin_ge(&cnt[4], T.step + 1);
-          spin_ge(&A.tile_step[D.tile_off + T.a * D.tiles + T.b], T.step);
-          break;
-      }
-      __threadfence();
-    }
-    __syncthreads();
     const long long t_work = A.prof ? clock64() : 0;
-    // ---- work
+    // ---- work (every predecessor has completed: no waits)
     switch (T.type) {
       case T_SMALL: small_front(A, F, sm, piv_sh); break;
       case T_ASM: {
-        const int c0 = T.b * kTile, c1 = min(F.nf, c0 + kTile);
-        extend_add_cols(A, F, c0, c1, A.pool + F.off + (int64_t)c0 * F.ld, F.ld, true);
+        int lo[2] = {0, 0}, hi[2] = {0, 0};
+        for (int ch = 0; ch < F.nchild; ++ch) {
+          const int32_t* bd = A.bnd + D.bnd_off + ch * (D.tiles + 1);
+          lo[ch] = bd[T.b];
+          hi[ch] = bd[T.b + 1];
+        }
+        extend_add(A, F, lo, hi, A.pool + F.off, F.ld, true);
         break;
       }
       case T_DIAG: diag_task(A, F, D, T.step, sm); break;
@@ -572,46 +731,62 @@ __global__ void __launch_bounds__(kDT, 1) factor_dag_kernel(DagArgs A) {
       case T_UPD: upd_task(A, F, T.step, T.a, T.b, sm); break;
     }
     __syncthreads();
-    // ---- publish
+    if (tid == 0) __threadfence();
+    __syncthreads();
+    // ---- successors
+    const int steps = (F.npiv + kNB - 1) / kNB;
     if (T.type == T_DIAG || T.type == T_ROWS || T.type == T_COLS) {
-      if (tid == 0) {
-        __threadfence();
-        if (T.type == T_DIAG) atomicAdd(&cnt[2], 1);
-        const int old = atomicAdd(&cnt[3], 1);
-        last_s = (old + 1 == A.rc_prefix[D.rc_off + T.step + 1]);
+      if (T.type == T_DIAG) {
+        const int a0 = a0_of(F, T.step);
+        for (int x = a0 + tid; x < D.tiles; x += kDT) {
+          notify(A, idx_rows(A, D, F, T.step, x));
+          notify(A, idx_cols(A, D, F, T.step, x));
+        }
       }
+      if (tid == 0) last_s = (atomicAdd(&cnt[3], 1) + 1 == A.rc_prefix[D.rc_off + T.step + 1]);
       __syncthreads();
-      if (last_s) {  // last of the panel: verify, fall back if needed, release
+      if (last_s) {  // last of the panel: verify, fall back if needed, release the updates
         if (tid == 0) __threadfence();
         __syncthreads();
         const unsigned long long bits = atomicAdd(&A.flagbits[D.flag_off + T.step], 0ull);
         if (!(__longlong_as_double((long long)bits) <= kLmax)) panel_fallback(A, F, D, T.step, sm);
         __syncthreads();
-        if (tid == 0) {
-          __threadfence();
-          atomicAdd(&cnt[4], 1);
-        }
+        if (tid == 0) __threadfence();
+        __syncthreads();
+        const int a0 = a0_of(F, T.step), nr = D.tiles - a0;
+        for (int x = tid; x < nr * nr; x += kDT)
+          notify(A, idx_upd(A, D, F, T.step, a0 + x / nr, a0 + x % nr));
       }
     } else if (T.type == T_UPD) {
       if (tid == 0) {
-        __threadfence();
         atomicAdd(&A.tile_step[D.tile_off + T.a * D.tiles + T.b], 1);
+        const int s1 = T.step + 1;
+        if (s1 < steps) {
+          const int a1 = a0_of(F, s1), an = (s1 * kNB) / kTile;
+          if (T.a >= a1 && T.b >= a1) notify(A, idx_upd(A, D, F, s1, T.a, T.b));
+          if (T.a == an && T.b == an) notify(A, idx_diag(A, D, s1));
+          if (T.b == an && T.a >= a1) notify(A, idx_rows(A, D, F, s1, T.a));
+          if (T.a == an && T.b >= a1) notify(A, idx_cols(A, D, F, s1, T.b));
+        }
       }
     } else if (T.type == T_ASM) {
-      if (tid == 0) {
-        __threadfence();
-        atomicAdd(&cnt[1], 1);
+      if (tid == 0 && steps > 0) notify(A, idx_diag(A, D, 0));
+    }
+    // front completion releases the parent's SMALL / ASM tasks
+    if (tid == 0) done_s = (atomicAdd(&cnt[0], 1) + 1 == D.ntasks);
+    __syncthreads();
+    if (done_s && D.parent >= 0) {
+      const FrontDag PD = A.dag[D.parent];
+      if (PD.tiles == 0) {
+        if (tid == 0) notify(A, PD.task_base);
+      } else {
+        for (int x = tid; x < PD.nasm; x += kDT) notify(A, PD.task_base + x);
       }
     }
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(&cnt[0], 1);
-      if (A.prof) {
-        const long long t_end = clock64();
-        atomicAdd(&A.prof[3 * T.type + 0], (unsigned long long)(t_end - t_work));
-        atomicAdd(&A.prof[3 * T.type + 1], (unsigned long long)(t_work - t_start));
-        atomicAdd(&A.prof[3 * T.type + 2], 1ull);
-      }
+    if (tid == 0 && A.prof) {
+      const long long t_end = clock64();
+      atomicAdd(&A.prof[3 * T.type + 0], (unsigned long long)(t_end - t_work));
+      atomicAdd(&A.prof[3 * T.type + 2], 1ull);
     }
   }
 }
@@ -621,10 +796,11 @@ int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 }  // namespace
 
 struct DagPlan {
-  DeviceBuffer d_tasks, d_dag, d_cnt, d_tile, d_rc, d_flagbits, d_backup, d_ticket, d_prof;
-  int ntasks = 0, nfronts = 0, ntile = 0, nflag = 0, grid = 148;
+  DeviceBuffer d_tasks, d_dag, d_cnt, d_tile, d_rc, d_flagbits, d_backup, d_prof, d_bnd,
+      d_small_backup, d_deps0, d_deps, d_queue0, d_queue, d_qctl, d_qctl0, d_sb;
+  int ntasks = 0, nfronts = 0, ntile = 0, nflag = 0, grid = 148, nready = 0;
   size_t smem = 0;
-  double flops_upd = 0, flops_small = 0;
+  double flops_upd = 0;
 };
 
 void rqb_dag_build(FactorEngine& fe) {
@@ -632,123 +808,131 @@ void rqb_dag_build(FactorEngine& fe) {
   const int nfr = static_cast<int>(S.fronts.size());
   auto P = std::make_unique<DagPlan>();
   std::vector<FrontDag> dag(nfr);
-  std::vector<int32_t> rc_prefix;
+  std::vector<int32_t> rc_prefix, bnd, step_base, deps;
   std::vector<Task> tasks;
   int tile_off = 0, flag_off = 0, slot = 0;
   int64_t backup = 0;
   int max_small = 0;
-  const int nlev = static_cast<int>(S.level_fronts.size());
-  for (int lev = 0; lev < nlev; ++lev) {
-    // pass 1: per-front bookkeeping + SMALL/ASM tasks
-    int max_steps = 0;
-    for (int32_t f : S.level_fronts[lev]) {
-      const Front& F = S.fronts[f];
-      FrontDag& D = dag[f];
-      D.slot = -1;
-      if (F.nf <= kSmallNf) {
-        tasks.push_back({f, T_SMALL, 0, 0, 0});
-        D.ntasks = 1;
-        max_small = std::max(max_small, F.nf);
-        continue;
-      }
-      D.tiles = div_up(F.nf, kTile);
-      D.tile_off = tile_off;
-      tile_off += D.tiles * D.tiles;
-      D.flag_off = flag_off;
-      const int steps = div_up(F.npiv, kNB);
-      flag_off += std::max(1, steps);
-      D.slot = slot++;
-      D.backup_off = backup;
-      backup += 2LL * F.nf * kNB;
-      D.nasm = D.tiles;
-      for (int b = 0; b < D.tiles; ++b) tasks.push_back({f, T_ASM, 0, 0, b});
-      D.ntasks = D.nasm;
-      max_steps = std::max(max_steps, steps);
+  // tasks of a front are contiguous; fronts in postorder
+  for (int f = 0; f < nfr; ++f) {
+    const Front& F = S.fronts[f];
+    FrontDag& D = dag[f];
+    D.task_base = static_cast<int32_t>(tasks.size());
+    D.slot = -1;
+    D.parent = F.parent;
+    const int nch = static_cast<int>(F.children.size());
+    if (F.nf <= kSmallNf) {
+      tasks.push_back({f, T_SMALL, 0, 0, 0});
+      deps.push_back(nch);
+      D.ntasks = 1;
+      max_small = std::max(max_small, F.nf);
+      continue;
     }
-    // pass 2: cumulative DIAG/ROWS/COLS counts per panel (steps + 1 entries
-    // per big front), then the panel steps interleaved across the level's fronts
-    for (int32_t f : S.level_fronts[lev]) {
-      const Front& F = S.fronts[f];
-      if (F.nf <= kSmallNf) continue;
-      FrontDag& D = dag[f];
-      D.rc_off = static_cast<int32_t>(rc_prefix.size());
-      rc_prefix.push_back(0);
-      const int steps = div_up(F.npiv, kNB);
-      int acc = 0;
-      for (int s = 0; s < steps; ++s) {
-        const int k = s * kNB, w = std::min(kNB, F.npiv - k);
-        const int t0 = k + w;
-        const int a0 = t0 / kTile;
-        const int nrow = t0 < F.nf ? D.tiles - a0 : 0;
-        acc += 1 + 2 * nrow;  // DIAG + ROWS + COLS
-        rc_prefix.push_back(acc);
-      }
+    D.tiles = div_up(F.nf, kTile);
+    D.tile_off = tile_off;
+    tile_off += D.tiles * D.tiles;
+    const int steps = div_up(F.npiv, kNB);
+    D.flag_off = flag_off;
+    flag_off += std::max(1, steps);
+    D.slot = slot++;
+    D.backup_off = backup;
+    backup += 2LL * F.nf * kNB;
+    D.nasm = D.tiles;
+    D.bnd_off = static_cast<int32_t>(bnd.size());
+    for (int32_t c : F.children) {
+      const Front& C = S.fronts[c];
+      const int32_t* rel = fe.rel_h.data() + fe.fronts_h[c].rel_off;
+      const int ncb = C.nf - C.npiv;
+      for (int b = 0; b <= D.tiles; ++b)
+        bnd.push_back(static_cast<int32_t>(std::lower_bound(rel, rel + ncb, b * kTile) - rel));
     }
-    for (int s = 0; s < max_steps; ++s) {
-      for (int32_t f : S.level_fronts[lev]) {
-        const Front& F = S.fronts[f];
-        if (F.nf <= kSmallNf) continue;
-        FrontDag& D = dag[f];
-        const int steps = div_up(F.npiv, kNB);
-        if (s >= steps) continue;
-        const int k = s * kNB, w = std::min(kNB, F.npiv - k);
-        const int t0 = k + w;
-        tasks.push_back({f, T_DIAG, (int16_t)s, 0, 0});
-        ++D.ntasks;
-        if (t0 >= F.nf) continue;
-        const int a0 = t0 / kTile;
-        for (int a = a0; a < D.tiles; ++a) tasks.push_back({f, T_ROWS, (int16_t)s, a, 0}), ++D.ntasks;
-        for (int b = a0; b < D.tiles; ++b) tasks.push_back({f, T_COLS, (int16_t)s, 0, b}), ++D.ntasks;
-        // lookahead order: tiles the next panel needs first
-        const int kn = t0, an = kn / kTile;
-        std::vector<std::pair<int, int>> order;
-        if (s + 1 < steps) {
-          order.push_back({an, an});
-          for (int a = a0; a < D.tiles; ++a)
-            if (a != an) order.push_back({a, an});
-          for (int b = a0; b < D.tiles; ++b)
-            if (b != an) order.push_back({an, b});
-        }
-        for (int a = a0; a < D.tiles; ++a)
-          for (int b = a0; b < D.tiles; ++b) {
-            if (s + 1 < steps && (a == an || b == an)) continue;
-            order.push_back({a, b});
-          }
-        for (auto& ab : order) {
-          tasks.push_back({f, T_UPD, (int16_t)s, ab.first, ab.second});
-          ++D.ntasks;
-          const double rr = std::min(F.nf, (ab.first + 1) * kTile) - std::max(ab.first * kTile, t0);
-          const double cc = std::min(F.nf, (ab.second + 1) * kTile) - std::max(ab.second * kTile, t0);
+    for (int b = 0; b < D.tiles; ++b) {
+      tasks.push_back({f, T_ASM, 0, 0, b});
+      deps.push_back(nch);
+    }
+    D.rc_off = static_cast<int32_t>(rc_prefix.size());
+    D.sb_off = static_cast<int32_t>(step_base.size());
+    rc_prefix.push_back(0);
+    int acc = 0;
+    for (int s = 0; s < steps; ++s) {
+      const int k = s * kNB, w = std::min(kNB, F.npiv - k), t0 = k + w;
+      const int a0 = t0 / kTile;
+      const int nr = t0 < F.nf ? D.tiles - a0 : 0;
+      const int an = k / kTile;
+      step_base.push_back(static_cast<int32_t>(tasks.size()));
+      tasks.push_back({f, T_DIAG, (int16_t)s, an, an});
+      deps.push_back(s == 0 ? D.nasm : 1);
+      for (int a = a0; a < a0 + nr; ++a) {
+        tasks.push_back({f, T_ROWS, (int16_t)s, a, an});
+        deps.push_back(s == 0 ? 1 : 2);
+      }
+      for (int b = a0; b < a0 + nr; ++b) {
+        tasks.push_back({f, T_COLS, (int16_t)s, an, b});
+        deps.push_back(s == 0 ? 1 : 2);
+      }
+      for (int a = a0; a < a0 + nr; ++a)
+        for (int b = a0; b < a0 + nr; ++b) {
+          tasks.push_back({f, T_UPD, (int16_t)s, a, b});
+          deps.push_back(s == 0 ? 1 : 2);
+          const double rr = std::min(F.nf, (a + 1) * kTile) - std::max(a * kTile, t0);
+          const double cc = std::min(F.nf, (b + 1) * kTile) - std::max(b * kTile, t0);
           P->flops_upd += 2.0 * w * rr * cc;
         }
-      }
+      acc += 1 + 2 * nr;
+      rc_prefix.push_back(acc);
     }
+    step_base.push_back(static_cast<int32_t>(tasks.size()));
+    D.ntasks = static_cast<int32_t>(tasks.size()) - D.task_base;
   }
+  // initial ready queue: tasks without predecessors (SMALL / ASM of leaf fronts)
+  std::vector<int32_t> queue0(tasks.size(), -1);
+  int nready = 0;
+  for (size_t t = 0; t < tasks.size(); ++t)
+    if (deps[t] == 0) queue0[nready++] = static_cast<int32_t>(t);
+  P->nready = nready;
   P->ntasks = static_cast<int>(tasks.size());
   P->nfronts = nfr;
   P->ntile = std::max(1, tile_off);
   P->nflag = std::max(1, flag_off);
   if (rc_prefix.empty()) rc_prefix.push_back(0);
-  if (tasks.empty()) tasks.push_back({0, T_SMALL, 0, 0, 0});
+  if (step_base.empty()) step_base.push_back(0);
+  if (bnd.empty()) bnd.push_back(0);
+  if (tasks.empty()) {
+    tasks.push_back({0, T_SMALL, 0, 0, 0});
+    deps.push_back(0);
+    queue0.push_back(-1);
+  }
   P->d_tasks.upload(tasks.data(), sizeof(Task) * tasks.size(), fe.stream);
   P->d_dag.upload(dag.data(), sizeof(FrontDag) * nfr, fe.stream);
   P->d_rc.upload(rc_prefix.data(), sizeof(int32_t) * rc_prefix.size(), fe.stream);
+  P->d_bnd.upload(bnd.data(), sizeof(int32_t) * bnd.size(), fe.stream);
+  P->d_sb.upload(step_base.data(), sizeof(int32_t) * step_base.size(), fe.stream);
+  P->d_deps0.upload(deps.data(), sizeof(int32_t) * deps.size(), fe.stream);
+  P->d_deps.alloc(sizeof(int32_t) * deps.size());
+  P->d_queue0.upload(queue0.data(), sizeof(int32_t) * queue0.size(), fe.stream);
+  P->d_queue.alloc(sizeof(int32_t) * queue0.size());
+  P->d_qctl.alloc(sizeof(int) * 4);
+  {
+    const int q0[4] = {0, nready, 0, 0};
+    P->d_qctl0.upload(q0, sizeof(q0), fe.stream);
+  }
   P->d_cnt.alloc(sizeof(int) * kCnt * nfr);
   P->d_tile.alloc(sizeof(int) * P->ntile);
   P->d_flagbits.alloc(sizeof(unsigned long long) * P->nflag);
   P->d_backup.alloc(sizeof(double) * std::max<int64_t>(1, backup));
-  P->d_ticket.alloc(sizeof(int) * 4);
   fe.d_scratch.alloc(sizeof(double) * std::max(1, slot) * 2 * kNB * kNB);
   const size_t small_smem = sizeof(double) * static_cast<size_t>(max_small | 1) * max_small;
   const size_t tile_smem = sizeof(double) * 2 * kNB * kTSP;
   const size_t rows_smem = sizeof(double) * ((kTile + 1) * kNB + kNB * kNB + 64);
-  P->smem = std::max({small_smem, tile_smem, rows_smem, size_t(16 * 1024)});
+  const size_t diag_smem = sizeof(double) * (3 * 32 * 33 + 64);
+  P->smem = std::max({small_smem, tile_smem, rows_smem, diag_smem, size_t(16 * 1024)});
   RQB_CUDA(cudaFuncSetAttribute(factor_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(P->smem)));
   int nsm = 148, occ = 1;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
   RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_dag_kernel, kDT, P->smem));
   P->grid = std::max(1, std::min(P->ntasks, nsm * std::max(1, occ)));
+  P->d_small_backup.alloc(sizeof(double) * P->grid * kSmallNf * kPB);
   fe.dag_ntasks = P->ntasks;
   fe.dag.reset(P.release());
 }
@@ -758,13 +942,17 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   RQB_CUDA(cudaMemsetAsync(P.d_cnt.p, 0, P.d_cnt.bytes, fe.stream));
   RQB_CUDA(cudaMemsetAsync(P.d_tile.p, 0, P.d_tile.bytes, fe.stream));
   RQB_CUDA(cudaMemsetAsync(P.d_flagbits.p, 0, P.d_flagbits.bytes, fe.stream));
-  RQB_CUDA(cudaMemsetAsync(P.d_ticket.p, 0, P.d_ticket.bytes, fe.stream));
+  RQB_CUDA(cudaMemcpyAsync(P.d_deps.p, P.d_deps0.p, P.d_deps0.bytes, cudaMemcpyDeviceToDevice, fe.stream));
+  RQB_CUDA(cudaMemcpyAsync(P.d_queue.p, P.d_queue0.p, P.d_queue0.bytes, cudaMemcpyDeviceToDevice, fe.stream));
+  RQB_CUDA(cudaMemcpyAsync(P.d_qctl.p, P.d_qctl0.p, P.d_qctl0.bytes, cudaMemcpyDeviceToDevice, fe.stream));
   DagArgs A;
   A.fronts = fe.d_fronts.as<FrontDev>();
   A.dag = P.d_dag.as<FrontDag>();
   A.tasks = P.d_tasks.as<Task>();
   A.ntasks = P.ntasks;
   A.inv = fe.d_inv.as<int32_t>();
+  A.rel = fe.d_rel.as<int32_t>();
+  A.bnd = P.d_bnd.as<int32_t>();
   A.pool = fe.d_pool.as<double>();
   A.ipiv = fe.d_ipiv.as<int32_t>();
   A.scratch = fe.d_scratch.as<double>();
@@ -774,7 +962,12 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   A.rc_prefix = P.d_rc.as<int32_t>();
   A.flagbits = P.d_flagbits.as<unsigned long long>();
   A.flags = fe.d_flags.as<int>();
-  A.ticket = P.d_ticket.as<int>();
+  A.deps = P.d_deps.as<int>();
+  A.queue = P.d_queue.as<int>();
+  A.qhead = P.d_qctl.as<int>();
+  A.qtail = P.d_qctl.as<int>() + 1;
+  A.step_base = P.d_sb.as<int32_t>();
+  A.small_backup = P.d_small_backup.as<double>();
   A.prof = nullptr;
   if (fe.dag_prof_enabled) {
     if (!P.d_prof.p) P.d_prof.alloc(sizeof(unsigned long long) * 32);
@@ -804,6 +997,7 @@ void rqb_dag_profile(FactorEngine& fe, double* out) {
   }
   out[18] = fe.dag->grid;
   out[19] = fe.dag->ntasks;
+  out[20] = h[20] / (clk_khz * 1.0);  // ready-queue pop wait, summed over CTAs
 }
 
 void DagPlanDeleter::operator()(DagPlan* p) const { delete p; }

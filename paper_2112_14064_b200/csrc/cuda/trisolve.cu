@@ -68,7 +68,38 @@ __global__ void __launch_bounds__(kST) fwd_sweep(
     const SolveItem I = items[it];
     const FrontDev F = fronts[I.front];
     const int np = F.npiv, nr = I.r1 - I.r0;
-    // children must be complete before any of this front's rows is formed
+    const double* g = pool + F.off;
+    const int64_t ld = F.ld;
+    // (1) everything that does not depend on other items: index maps, b, the
+    //     diagonal block, the first L block of this thread
+    const int32_t* inv0 = inv + F.inv_off;
+    double bv = 0.0;
+    int ir0 = -1, ir1 = -1;
+    if (tid < nr) {
+      const int r = I.r0 + tid;
+      const int q = r < np ? __ldg(&rowperm[F.start + r]) : r;  // pre-swap local row
+      bv = q < np ? b[perm[F.start + q]] : 0.0;
+      if (F.nchild > 0) ir0 = inv0[q];
+      if (F.nchild > 1) ir1 = inv0[F.nf + q];
+    }
+    if (I.blk >= 0)
+      for (int idx = tid; idx < nr * nr; idx += kST) {
+        const int r = idx % nr, c = idx / nr;
+        D[r + c * (kRB + 1)] = g[(I.r0 + r) + (int64_t)(I.r0 + c) * ld];
+      }
+    const int nblk = I.blk >= 0 ? I.blk : (np + kRB - 1) / kRB;
+    double lreg[kRB / 4];
+    auto prefetch = [&](int j) {
+      const int c0 = j * kRB, cw = min(np, c0 + kRB) - c0;
+      const double* lp = g + (I.r0 + row) + (int64_t)c0 * ld;
+#pragma unroll
+      for (int u = 0; u < kRB / 4; ++u) {
+        const int c = grp + 4 * u;
+        lreg[u] = (row < nr && c < cw) ? lp[c * ld] : 0.0;
+      }
+    };
+    if (nblk > 0) prefetch(0);
+    // (2) children complete -> gather their contribution vectors
     if (tid == 0) {
       if (F.nchild > 0) wait_ge(&cnt[3 * F.child0 + 1], nitems_front[F.child0]);
       if (F.nchild > 1) wait_ge(&cnt[3 * F.child1 + 1], nitems_front[F.child1]);
@@ -76,23 +107,12 @@ __global__ void __launch_bounds__(kST) fwd_sweep(
     }
     __syncthreads();
     if (tid < nr) {
-      const int r = I.r0 + tid;
-      const int q = r < np ? __ldg(&rowperm[F.start + r]) : r;  // pre-swap local row
-      double v = q < np ? b[perm[F.start + q]] : 0.0;
-      const int32_t* inv0 = inv + F.inv_off;
-      if (F.nchild > 0) {
-        const int ir = inv0[q];
-        if (ir >= 0) v += __ldcg(&cbvec[fronts[F.child0].cbvec_off + ir - fronts[F.child0].npiv]);
-      }
-      if (F.nchild > 1) {
-        const int ir = inv0[F.nf + q];
-        if (ir >= 0) v += __ldcg(&cbvec[fronts[F.child1].cbvec_off + ir - fronts[F.child1].npiv]);
-      }
+      double v = bv;
+      if (ir0 >= 0) v += __ldcg(&cbvec[fronts[F.child0].cbvec_off + ir0 - fronts[F.child0].npiv]);
+      if (ir1 >= 0) v += __ldcg(&cbvec[fronts[F.child1].cbvec_off + ir1 - fronts[F.child1].npiv]);
       wv[tid] = v;
     }
-    const double* g = pool + F.off;
-    const int64_t ld = F.ld;
-    const int nblk = I.blk >= 0 ? I.blk : (np + kRB - 1) / kRB;
+    // (3) left-looking over the published pivot blocks, next L block prefetched
     double s = 0.0;
     for (int j = 0; j < nblk; ++j) {
       if (tid == 0) {
@@ -101,23 +121,17 @@ __global__ void __launch_bounds__(kST) fwd_sweep(
       }
       __syncthreads();
       const int c0 = j * kRB, c1 = min(np, c0 + kRB);
-      if (tid < c1 - c0) yb[tid] = __ldcg(&y[F.start + c0 + tid]);
+      if (tid < kRB) yb[tid] = tid < c1 - c0 ? __ldcg(&y[F.start + c0 + tid]) : 0.0;
       __syncthreads();
-      if (row < nr) {
-        const double* lp = g + (I.r0 + row) + (int64_t)c0 * ld;
-#pragma unroll 4
-        for (int c = grp; c < c1 - c0; c += 4) s += lp[c * ld] * yb[c];
-      }
+#pragma unroll
+      for (int u = 0; u < kRB / 4; ++u) s += lreg[u] * yb[grp + 4 * u];
+      if (j + 1 < nblk) prefetch(j + 1);
     }
     part[grp][row] = s;
     __syncthreads();
     if (tid < nr) wv[tid] -= part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
     if (I.blk >= 0) {
-      // unit-lower diagonal block
-      for (int idx = tid; idx < nr * nr; idx += kST) {
-        const int r = idx % nr, c = idx / nr;
-        D[r + c * (kRB + 1)] = g[(I.r0 + r) + (int64_t)(I.r0 + c) * ld];
-      }
+      // unit-lower diagonal block (already in shared memory)
       __syncthreads();
       if (tid < 32) {
         double v0 = tid < nr ? wv[tid] : 0.0, v1 = tid + 32 < nr ? wv[tid + 32] : 0.0;
@@ -165,57 +179,76 @@ __global__ void __launch_bounds__(kST) bwd_sweep(
     const FrontDev F = fronts[I.front];
     const int np = F.npiv, nf = F.nf, nr = I.r1 - I.r0;
     const int par = parent[I.front];
+    const double* g = pool + F.off;
+    const int64_t ld = F.ld;
+    const int32_t* rw = rows + F.rows_off;
+    // (1) independent loads: diagonal block, y of this block, first U chunk
+    for (int idx = tid; idx < nr * nr; idx += kST) {
+      const int r = idx % nr, c = idx / nr;
+      D[r + c * (kRB + 1)] = g[(I.r0 + r) + (int64_t)(I.r0 + c) * ld];
+    }
+    double y0 = 0.0, y1 = 0.0;
+    if (tid < 32) {
+      if (tid < nr) y0 = y[F.start + I.r0 + tid];
+      if (tid + 32 < nr) y1 = y[F.start + I.r0 + tid + 32];
+    }
+    const int npb = (np + kRB - 1) / kRB;
+    const int ncbc = (nf - np + kRB - 1) / kRB;  // contribution-column chunks (ancestors' x)
+    const int nch = ncbc + (npb - 1 - I.blk);     // + later pivot blocks (last first)
+    auto chunk = [&](int t, int& c0, int& c1, bool& piv) {
+      if (t < ncbc) {
+        c0 = np + t * kRB;
+        c1 = min(nf, c0 + kRB);
+        piv = false;
+      } else {
+        const int j = npb - 1 - (t - ncbc);
+        c0 = j * kRB;
+        c1 = min(np, c0 + kRB);
+        piv = true;
+      }
+    };
+    double ureg[kRB / 4];
+    auto prefetch = [&](int t) {
+      int c0, c1;
+      bool pv;
+      chunk(t, c0, c1, pv);
+      const double* up = g + (I.r0 + row) + (int64_t)c0 * ld;
+#pragma unroll
+      for (int u = 0; u < kRB / 4; ++u) {
+        const int c = grp + 4 * u;
+        ureg[u] = (row < nr && c < c1 - c0) ? up[c * ld] : 0.0;
+      }
+    };
+    if (nch > 0) prefetch(0);
     if (tid == 0) {
       if (par >= 0) wait_ge(&cnt[3 * par + 2], npb_front[par]);
       __threadfence();
     }
     __syncthreads();
-    const double* g = pool + F.off;
-    const int64_t ld = F.ld;
-    const int32_t* rw = rows + F.rows_off;
     double s = 0.0;
-    // contribution-block columns: x of ancestors (final)
-    for (int c0 = np; c0 < nf; c0 += kRB) {
-      const int c1 = min(nf, c0 + kRB);
-      __syncthreads();
-      if (tid < c1 - c0) xb[tid] = __ldcg(&xnew[rw[c0 + tid]]);
-      __syncthreads();
-      if (row < nr) {
-        const double* up = g + (I.r0 + row) + (int64_t)c0 * ld;
-#pragma unroll 4
-        for (int c = grp; c < c1 - c0; c += 4) s += up[c * ld] * xb[c];
-      }
-    }
-    // later pivot blocks, published last-to-first
-    const int npb = (np + kRB - 1) / kRB;
-    for (int j = npb - 1; j > I.blk; --j) {
-      if (tid == 0) {
-        wait_ge(&cnt[3 * I.front + 2], npb - j);
+    for (int t = 0; t < nch; ++t) {
+      int c0, c1;
+      bool pv;
+      chunk(t, c0, c1, pv);
+      if (pv && tid == 0) {
+        wait_ge(&cnt[3 * I.front + 2], npb - c0 / kRB);
         __threadfence();
       }
       __syncthreads();
-      const int c0 = j * kRB, c1 = min(np, c0 + kRB);
-      if (tid < c1 - c0) xb[tid] = __ldcg(&xnew[F.start + c0 + tid]);
+      if (tid < kRB)
+        xb[tid] = tid < c1 - c0 ? __ldcg(&xnew[pv ? F.start + c0 + tid : rw[c0 + tid]]) : 0.0;
       __syncthreads();
-      if (row < nr) {
-        const double* up = g + (I.r0 + row) + (int64_t)c0 * ld;
-#pragma unroll 4
-        for (int c = grp; c < c1 - c0; c += 4) s += up[c * ld] * xb[c];
-      }
+#pragma unroll
+      for (int u = 0; u < kRB / 4; ++u) s += ureg[u] * xb[grp + 4 * u];
+      if (t + 1 < nch) prefetch(t + 1);
     }
     part[grp][row] = s;
-    for (int idx = tid; idx < nr * nr; idx += kST) {
-      const int r = idx % nr, c = idx / nr;
-      D[r + c * (kRB + 1)] = g[(I.r0 + r) + (int64_t)(I.r0 + c) * ld];
-    }
     __syncthreads();
     if (tid < 32) {
       double v0 = 0.0, v1 = 0.0;
-      if (tid < nr)
-        v0 = y[F.start + I.r0 + tid] - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]);
+      if (tid < nr) v0 = y0 - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]);
       if (tid + 32 < nr)
-        v1 = y[F.start + I.r0 + tid + 32] -
-             (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32]);
+        v1 = y1 - (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32]);
       for (int c = nr - 1; c >= 0; --c) {
         if (c < 32) {
           if (tid == c) v0 /= D[c + c * (kRB + 1)];

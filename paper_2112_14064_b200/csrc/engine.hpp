@@ -23,6 +23,7 @@ struct FrontDev {
   int64_t inv_off;    // extend-add maps: nchild arrays of nf int32 (child-local row or -1)
   int32_t nf, npiv, ld, start;
   int32_t nchild, child0, child1, scratch;  // scratch: slot of panel inverses (-1 none)
+  int64_t rel_off;    // child -> parent map: parent-local row of each CB row (nf - npiv int32)
 };
 
 void cuda_check(cudaError_t e, const char* what);
@@ -88,7 +89,8 @@ struct FactorEngine {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  DeviceBuffer d_pool, d_aval, d_qdst, d_rows, d_fronts, d_inv, d_ipiv, d_lists, d_scratch;
+  DeviceBuffer d_pool, d_aval, d_qdst, d_rows, d_fronts, d_inv, d_ipiv, d_lists, d_scratch, d_rel;
+  std::vector<int32_t> rel_h;  // concatenated child -> parent row maps
   DeviceBuffer d_flags;   // [0] singular, [1] swaps
   DeviceBuffer d_y, d_xnew, d_cbvec, d_perm;  // solve workspaces (n, n, cbvec), perm[new] = old
   // sync-free solve: work items, per-front item counts, dependency counters,

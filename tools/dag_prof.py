@@ -10,11 +10,11 @@ for cfg in sys.argv[1:]:
     f = rq.lu_factorize((P.rowptr, P.col, P.q_values(-0.5)), o)
     for _ in range(3):
         f.refactor(P.q_values(-0.5))
-    out = np.zeros(20)
+    out = np.zeros(24)
     _lib.check(_lib.lib.rq_factor_dag_profile(f._h, out))
     info = f.info()
     names = ["SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD"]
-    print(f"{cfg}: factor {info['factor_ms']:.3f} ms {info['gflops']:.1f} GF/s grid {int(out[18])} tasks {int(out[19])}"
+    print(f"{cfg}: factor {info['factor_ms']:.3f} ms {info['gflops']:.1f} GF/s grid {int(out[18])} tasks {int(out[19])} popwait {out[20]:.2f} ms"
           f" flops {o.stats['flops_lu']:.3e} max_front {o.stats['max_front']}")
     for t, nm in enumerate(names):
         busy, wait, cnt = out[3 * t:3 * t + 3]
