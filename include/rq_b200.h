@@ -206,6 +206,7 @@ typedef struct {
   uint64_t seed;      /* splitmix64 start vector, uniform[-1,1] */
   int max_restarts;   /* default 100 */
   int guard;          /* completeness guard (deflated fresh restarts), 1 = on */
+  int profile;        /* 1: time operator / orthogonalisation per step (synchronising) */
 } rq_eigs_opts;
 
 typedef struct {
@@ -217,6 +218,10 @@ typedef struct {
   double t_total_ms, t_factor_ms, t_solve_ms, t_spmv_ms, t_orth_ms, t_host_ms;
   int64_t launches;
   double restart_defect; /* max ||H Q - Q T|| / ||H|| over restarts (exactness check) */
+  double t_ritz_ms;      /* host: Schur form + Ritz vectors of H_m */
+  double t_check_ms;     /* explicit pencil residuals (device + sync) */
+  double t_restart_ms;   /* host restart basis + device V Q */
+  double t_sync_ms;      /* host blocked on the Arnoldi-step graphs (device time) */
 } rq_eigs_info;
 
 /* solve_quadratic: nev eigenpairs of K + lam C + lam^2 M nearest sigma.

@@ -64,7 +64,7 @@ class OperatorOpts(C.Structure):
 
 class EigsOpts(C.Structure):
     _fields_ = [("nev", C.c_int), ("m", C.c_int), ("tol", C.c_double), ("seed", C.c_uint64),
-                ("max_restarts", C.c_int), ("guard", C.c_int)]
+                ("max_restarts", C.c_int), ("guard", C.c_int), ("profile", C.c_int)]
 
 
 class EigsInfo(C.Structure):
@@ -76,7 +76,9 @@ class EigsInfo(C.Structure):
                 ("macs_restart", C.c_double), ("t_total_ms", C.c_double),
                 ("t_factor_ms", C.c_double), ("t_solve_ms", C.c_double),
                 ("t_spmv_ms", C.c_double), ("t_orth_ms", C.c_double), ("t_host_ms", C.c_double),
-                ("launches", C.c_int64), ("restart_defect", C.c_double)]
+                ("launches", C.c_int64), ("restart_defect", C.c_double),
+                ("t_ritz_ms", C.c_double), ("t_check_ms", C.c_double),
+                ("t_restart_ms", C.c_double), ("t_sync_ms", C.c_double)]
 
 
 def _sig(name, res, *args):

@@ -96,8 +96,7 @@ struct DagArgs {
   double* small_backup;      // per CTA: 160 x 16 panel backup of the SMALL path
   int* deps;                 // remaining predecessors per task
   int* queue;                // ready queue (task ids, -1 = not yet pushed)
-  int* qhead;
-  int* qtail;
+  int* qctl;                 // {head, tail}
   const int32_t* step_base;  // FrontDag::sb_off: first task of every panel step
 };
 
@@ -178,27 +177,50 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
     extend_add(A, F, lo, hi, sm, lds, false);
   }
   __shared__ double red_s[kDT / 32];
+  __shared__ double urow_s[2][kPB];
   __shared__ int any_swap_s;
   double* pbk = A.small_backup + (int64_t)blockIdx.x * kSmallNf * kPB;
   for (int k0 = 0; k0 < np; k0 += kPB) {
     const int pw = min(kPB, np - k0);
-    // ---- speculative unpivoted panel: thread t owns row t; one barrier per column
-    if (tid < nf && tid >= k0)
-      for (int c = 0; c < pw; ++c) pbk[tid + c * kSmallNf] = sm[tid + (k0 + c) * lds];
+    // ---- speculative unpivoted panel: thread t owns row t in registers; the
+    //      pivot row is published in a double-buffered shared row (1 barrier/column)
     double lm = 0.0;
     bool sing = false;
-    for (int j = k0; j < k0 + pw; ++j) {
-      const double ujj = sm[j + j * lds];
-      sing = sing || !(fabs(ujj) >= kSingularTiny);
+    {
       const int i = tid;
-      if (i > j && i < nf) {
-        const double l = sm[i + j * lds] / ujj;
-        sm[i + j * lds] = l;
-        if (i < np) lm = fmax(lm, fabs(l));
-        for (int c = j + 1; c < k0 + pw; ++c) sm[i + c * lds] -= l * sm[j + c * lds];
+      const bool own = i >= k0 && i < nf;
+      double a[kPB];
+#pragma unroll
+      for (int c = 0; c < kPB; ++c) a[c] = (own && c < pw) ? sm[i + (k0 + c) * lds] : 0.0;
+      if (own)
+#pragma unroll
+        for (int c = 0; c < kPB; ++c)
+          if (c < pw) pbk[i + c * kSmallNf] = a[c];
+#pragma unroll
+      for (int jj = 0; jj < kPB; ++jj) {
+        if (jj < pw) {
+          double* ub = urow_s[jj & 1];
+          if (i == k0 + jj)
+#pragma unroll
+            for (int c = 0; c < kPB; ++c) ub[c] = a[c];
+          __syncthreads();
+          const double ujj = ub[jj];
+          sing = sing || !(fabs(ujj) >= kSingularTiny);
+          if (own && i > k0 + jj) {
+            const double l = a[jj] * (1.0 / ujj);
+            a[jj] = l;
+            if (i < np) lm = fmax(lm, fabs(l));
+#pragma unroll
+            for (int c = jj + 1; c < kPB; ++c) a[c] -= l * ub[c];
+          }
+        }
       }
-      __syncthreads();
+      if (own)
+#pragma unroll
+        for (int c = 0; c < kPB; ++c)
+          if (c < pw) sm[i + (k0 + c) * lds] = a[c];
     }
+    __syncthreads();
     if (sing) lm = 1e300;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, o));
@@ -257,45 +279,68 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
       }
     }
     __syncthreads();
-    for (int c = tid; c < nf; c += kDT) {
-      if (c >= k0 && c < k0 + pw) continue;
-      for (int jj = 0; jj < pw; ++jj) {
-        const int p = piv_sh[jj], j = k0 + jj;
-        if (p != j) {
-          const double t = sm[j + c * lds];
-          sm[j + c * lds] = sm[p + c * lds];
-          sm[p + c * lds] = t;
+    if (any_swap_s)
+      for (int c = tid; c < nf; c += kDT) {
+        if (c >= k0 && c < k0 + pw) continue;
+        for (int jj = 0; jj < pw; ++jj) {
+          const int p = piv_sh[jj], j = k0 + jj;
+          if (p != j) {
+            const double t = sm[j + c * lds];
+            sm[j + c * lds] = sm[p + c * lds];
+            sm[p + c * lds] = t;
+          }
         }
       }
-      if (c >= k0 + pw)
-        for (int jj = 1; jj < pw; ++jj) {
-          double s = sm[k0 + jj + c * lds];
-          for (int t = 0; t < jj; ++t) s -= sm[k0 + jj + (k0 + t) * lds] * sm[k0 + t + c * lds];
-          sm[k0 + jj + c * lds] = s;
-        }
+    __syncthreads();
+    // U12 = inv(L11) A12: thread per column, the 16-row segment in registers
+    for (int c = k0 + pw + tid; c < nf; c += kDT) {
+      double u[kPB];
+#pragma unroll
+      for (int jj = 0; jj < kPB; ++jj) u[jj] = jj < pw ? sm[k0 + jj + c * lds] : 0.0;
+#pragma unroll
+      for (int jj = 1; jj < kPB; ++jj) {
+        double sv = u[jj];
+#pragma unroll
+        for (int t = 0; t < jj; ++t) sv -= sm[k0 + jj + (k0 + t) * lds] * u[t];
+        u[jj] = sv;
+      }
+#pragma unroll
+      for (int jj = 0; jj < kPB; ++jj)
+        if (jj < pw) sm[k0 + jj + c * lds] = u[jj];
     }
     __syncthreads();
     const int t0 = k0 + pw, T = nf - t0;
     if (T > 0) {
-      const int mt = (T + 15) / 16, nt = (T + 7) / 8;
+      const int mt = (T + 15) / 16, nt = (T + 31) / 32;
       const int gid = lane >> 2, tig = lane & 3;
       for (int tile = warp; tile < mt * nt; tile += kDT / 32) {
-        const int r0 = t0 + (tile % mt) * 16, c0 = t0 + (tile / mt) * 8;
-        double acc[4] = {0, 0, 0, 0};
-        for (int kk = 0; kk < pw; kk += 4) {
+        const int r0 = t0 + (tile % mt) * 16, c0 = t0 + (tile / mt) * 32;
+        double acc[4][4];
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[y][e] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < kPB; kk += 4) {
           const int kc = k0 + kk + tig;
           const bool kin = kk + tig < pw;
-          const int ra = r0 + gid, rb = r0 + gid + 8, cb = c0 + gid;
+          const int ra = r0 + gid, rb = r0 + gid + 8;
           const double a0 = (kin && ra < nf) ? sm[ra + kc * lds] : 0.0;
           const double a1 = (kin && rb < nf) ? sm[rb + kc * lds] : 0.0;
-          const double b0 = (kin && cb < nf) ? sm[kc + cb * lds] : 0.0;
-          dmma(acc, a0, a1, b0);
+#pragma unroll
+          for (int y = 0; y < 4; ++y) {
+            const int cb = c0 + y * 8 + gid;
+            const double b0 = (kin && cb < nf) ? sm[kc + cb * lds] : 0.0;
+            dmma(acc[y], a0, a1, b0);
+          }
         }
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = r0 + gid + (e >> 1) * 8, c = c0 + 2 * tig + (e & 1);
-          if (r < nf && c < nf) sm[r + c * lds] -= acc[e];
-        }
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = r0 + gid + (e >> 1) * 8, c = c0 + y * 8 + 2 * tig + (e & 1);
+            if (r < nf && c < nf) sm[r + c * lds] -= acc[y][e];
+          }
       }
     }
     __syncthreads();
@@ -304,16 +349,16 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
     for (int r = lane; r < nf; r += 32) g[r + (int64_t)c * F.ld] = sm[r + c * lds];
 }
 
-// DIAG: 32x32 diagonal block of panel s, unpivoted (speculative), entirely in
-// registers of warp 0 (row `lane` per thread, shuffles broadcast the pivot
-// row); inv(L11) by warp 0 and inv(U11) by warp 1, column `lane` per thread.
+// DIAG: 32x32 diagonal block of panel s, unpivoted (speculative), in the
+// registers of warp 0 (row `lane` per thread; shuffles broadcast the pivot row).
+// The factored block goes back to the front; ROWS/COLS solve against it.
 __device__ void diag_task(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s, double* sm) {
   const int k = s * kNB, w = min(kNB, F.npiv - k);
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr unsigned FULL = 0xffffffffu;
-  double* T = sm;               // 32 x 33: the factored block
+  double* T = sm;               // 32 x 33
   double* red = sm + 32 * 33;
   double* bk = A.backup + D.backup_off;
   {
@@ -332,79 +377,44 @@ __device__ void diag_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   }
   __syncthreads();
   double lm = 0.0;
-  if (warp == 0) {
-    double r[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) r[c] = T[lane + c * 33];
-    bool sing = false;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const double ujj = __shfl_sync(FULL, r[j], j);
-      if (j < w && !(fabs(ujj) >= kSingularTiny)) sing = true;
-      const double rinv = 1.0 / ujj;
-      const double l = r[j] * rinv;
-      if (lane > j) {
-        r[j] = l;
-        if (lane < w) lm = fmax(lm, fabs(l));
-      }
-#pragma unroll
-      for (int c = j + 1; c < 32; ++c) {
-        const double u = __shfl_sync(FULL, r[c], j);
-        if (lane > j) r[c] -= l * u;
-      }
+  // unpivoted LU, all threads: step j updates the (w-1-j)^2 trailing entries
+  // (one barrier per step); the multipliers of column j are stored after the
+  // barrier, which the next step does not read
+  (void)warp;
+  (void)lane;
+  (void)FULL;
+  bool sing = false;
+  for (int j = 0; j < w; ++j) {
+    const double ujj = T[j + j * 33];
+    if (!(fabs(ujj) >= kSingularTiny)) sing = true;
+    const double rinv = 1.0 / ujj;
+    const int m = w - 1 - j;
+    for (int e = tid; e < m * m; e += kDT) {
+      const int i = j + 1 + e % m, c = j + 1 + e / m;
+      T[i + c * 33] = fma(-T[i + j * 33] * rinv, T[j + c * 33], T[i + c * 33]);
     }
-    if (sing) lm = 1e300;  // forces the exact pivoted fallback (singular detection there)
-#pragma unroll
-    for (int c = 0; c < 32; ++c) T[lane + c * 33] = r[c];
-    // inv(L11): lane c holds column c; X[i][c] = -sum_{q<i} L[i][q] X[q][c]
-    double x[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-    for (int i = 1; i < 32; ++i) {
-      double acc = 0.0;
-#pragma unroll
-      for (int q = 0; q < i; ++q) acc += __shfl_sync(FULL, r[q], i) * x[q];
-      if (i > lane) x[i] = -acc;
+    __syncthreads();
+    if (tid < m) {
+      const double l = T[j + 1 + tid + j * 33] * rinv;
+      T[j + 1 + tid + j * 33] = l;
+      lm = fmax(lm, fabs(l));
     }
-    double* invL = A.scratch + (int64_t)D.slot * 2 * kNB * kNB;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) invL[i + lane * kNB] = (i < w && lane < w) ? x[i] : 0.0;
   }
+  if (sing) lm = 1e300;  // forces the exact pivoted fallback (singular detection there)
   __syncthreads();
-  if (warp == 1) {
-    // inv(U11): lane c holds column c; Y[i][c] = -(sum_{q>i} U[i][q] Y[q][c]) / U[i][i]
-    double r[32], y[32];
+  lm = block_max(lm, red);
 #pragma unroll
-    for (int c = 0; c < 32; ++c) r[c] = T[lane + c * 33];  // row `lane` of U
-    const double dinv = 1.0 / T[lane + lane * 33];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) y[i] = 0.0;
-#pragma unroll
-    for (int i = 31; i >= 0; --i) {
-      const double di = __shfl_sync(FULL, dinv, i);
-      double acc = 0.0;
-#pragma unroll
-      for (int q = i + 1; q < 32; ++q) acc += __shfl_sync(FULL, r[q], i) * y[q];
-      if (i == lane) y[i] = di;
-      else if (i < lane) y[i] = -acc * di;
-    }
-    double* invU = A.scratch + (int64_t)D.slot * 2 * kNB * kNB + kNB * kNB;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) invU[i + lane * kNB] = (i < w && lane < w) ? y[i] : 0.0;
-  }
-  lm = block_max(warp == 0 ? lm : 0.0, red);
-  {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int idx = tid + i * kDT, rr = idx % 32, c = idx / 32;
-      if (rr < w && c < w) g[(k + rr) + (int64_t)(k + c) * ld] = T[rr + c * 33];
-    }
+  for (int i = 0; i < 4; ++i) {
+    const int idx = tid + i * kDT, rr = idx % 32, c = idx / 32;
+    if (rr < w && c < w) g[(k + rr) + (int64_t)(k + c) * ld] = T[rr + c * 33];
   }
   for (int j = tid; j < w; j += kDT) A.ipiv[F.start + k + j] = k + j;
   if (tid == 0) atomicMax(&A.flagbits[D.flag_off + s], (unsigned long long)__double_as_longlong(lm));
 }
 
+// ROWS: rows of tile row a below the diagonal block: solve L21 U11 = A21 row by
+// row (forward substitution with the factored block), track max|l| over the
+// fully-summed rows (threshold verification), back the panel rows up first.
 __device__ void rows_task(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s, int a,
                           double* sm) {
   const int k = s * kNB, w = min(kNB, F.npiv - k), np = F.npiv;
@@ -415,21 +425,26 @@ __device__ void rows_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   const int tid = threadIdx.x;
   constexpr int kPS = kTile + 1;   // stride of the 64-row panel block
   double* P = sm;                 // 64 rows x 32 columns
-  double* iU = sm + kPS * kNB;    // 32 x 32
-  double* red = iU + kNB * kNB;
+  double* U = sm + kPS * kNB;     // 32 x 33 factored diagonal block
+  double* red = U + 32 * 33;
   double* bk = A.backup + D.backup_off;
-  const double* invU = A.scratch + (int64_t)D.slot * 2 * kNB * kNB + kNB * kNB;
   {
     double vu[4], vp[8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) vu[i] = __ldcg(&invU[tid + i * kDT]);
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * kDT, r = idx % 32, c = idx / 32;
+      vu[i] = (r < w && c < w) ? __ldcg(&g[(k + r) + (int64_t)(k + c) * ld]) : (r == c ? 1.0 : 0.0);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int idx = tid + i * kDT, r = idx % kTile, c = idx / kTile;
       vp[i] = (r < nr && c < w) ? __ldcg(&g[(r0 + r) + (int64_t)(k + c) * ld]) : 0.0;
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) iU[tid + i * kDT] = vu[i];
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * kDT;
+      U[(idx % 32) + (idx / 32) * 33] = vu[i];
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int idx = tid + i * kDT, r = idx % kTile, c = idx / kTile;
@@ -439,19 +454,29 @@ __device__ void rows_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   }
   __syncthreads();
   double lm = 0.0;
-  const int r = tid & 63, q = tid >> 6;
-  if (r < nr) {
-    for (int i = q; i < w; i += 4) {
-      double s = 0.0;
-      for (int t = 0; t <= i; ++t) s += P[r + t * kPS] * iU[t + i * kNB];
-      g[(r0 + r) + (int64_t)(k + i) * ld] = s;
-      if (r0 + r < np) lm = fmax(lm, fabs(s));
+  if (tid < nr) {
+    double x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      double sv = P[tid + j * kPS];
+#pragma unroll
+      for (int t = 0; t < j; ++t) sv = fma(-x[t], U[t + j * 33], sv);
+      x[j] = j < w ? sv / U[j + j * 33] : 0.0;
     }
+    const bool cand = r0 + tid < np;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < w) {
+        g[(r0 + tid) + (int64_t)(k + j) * ld] = x[j];
+        if (cand) lm = fmax(lm, fabs(x[j]));
+      }
   }
   lm = block_max(lm, red);
   if (tid == 0) atomicMax(&A.flagbits[D.flag_off + s], (unsigned long long)__double_as_longlong(lm));
 }
 
+// COLS: columns of tile column b right of the block: U12 = inv(L11) A12 by
+// forward substitution with the unit-lower factored block (column per thread).
 __device__ void cols_task(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s, int b,
                           double* sm) {
   const int k = s * kNB, w = min(kNB, F.npiv - k);
@@ -460,21 +485,26 @@ __device__ void cols_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
   const int tid = threadIdx.x;
-  double* P = sm;               // 32 x 64 (row-major by column: P[i + c*33])
-  double* iL = sm + 64 * 33;
+  double* P = sm;               // 32 rows x 64 columns (P[r + c*33])
+  double* L = sm + 64 * 33;     // 32 x 33 factored diagonal block
   double* bk2 = A.backup + D.backup_off + (int64_t)F.nf * kNB;
-  const double* invL = A.scratch + (int64_t)D.slot * 2 * kNB * kNB;
   {
     double vl[4], vp[8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) vl[i] = __ldcg(&invL[tid + i * kDT]);
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * kDT, r = idx % 32, c = idx / 32;
+      vl[i] = (r < w && c < w) ? __ldcg(&g[(k + r) + (int64_t)(k + c) * ld]) : 0.0;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int idx = tid + i * kDT, r = idx % kNB, c = idx / kNB;
       vp[i] = (r < w && c < nc) ? __ldcg(&g[(k + r) + (int64_t)(c0 + c) * ld]) : 0.0;
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) iL[tid + i * kDT] = vl[i];
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * kDT;
+      L[(idx % 32) + (idx / 32) * 33] = vl[i];
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int idx = tid + i * kDT, r = idx % kNB, c = idx / kNB;
@@ -483,13 +513,19 @@ __device__ void cols_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
     }
   }
   __syncthreads();
-  const int c = tid & 63, q = tid >> 6;
-  if (c < nc)
-    for (int i = q; i < w; i += 4) {
-      double s = 0.0;
-      for (int t = 0; t <= i; ++t) s += iL[i + t * kNB] * P[t + c * 33];
-      g[(k + i) + (int64_t)(c0 + c) * ld] = s;
+  if (tid < nc) {
+    double x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      double sv = P[i + tid * 33];
+#pragma unroll
+      for (int t = 0; t < i; ++t) sv = fma(-L[i + t * 33], x[t], sv);
+      x[i] = sv;
     }
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < w) g[(k + i) + (int64_t)(c0 + tid) * ld] = x[i];
+  }
 }
 
 __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int b, double* sm) {
@@ -677,12 +713,24 @@ __device__ __forceinline__ int idx_upd(const DagArgs& A, const FrontDag& D, cons
 }
 
 // One predecessor of task t completed: the last one pushes t on the ready queue.
+// Ready queue: FIFO; a CTA claims the next slot (atomicAdd) and waits until a
+// finishing task pushes into it.
 __device__ __forceinline__ void notify(const DagArgs& A, int t) {
   if (atomicSub(&A.deps[t], 1) == 1) {
     __threadfence();
-    const int slot = atomicAdd(A.qtail, 1);
+    const int slot = atomicAdd(&A.qctl[1], 1);
     atomicExch(&A.queue[slot], t);
   }
+}
+
+__device__ int pop_task(const DagArgs& A) {
+  const int h = atomicAdd(&A.qctl[0], 1);
+  if (h >= A.ntasks) return -1;
+  volatile int* q = A.queue;
+  int t;
+  while ((t = q[h]) < 0) __nanosleep(32);
+  __threadfence();
+  return t;
 }
 
 __global__ void __launch_bounds__(kDT, 1) factor_dag_kernel(DagArgs A) {
@@ -694,12 +742,7 @@ __global__ void __launch_bounds__(kDT, 1) factor_dag_kernel(DagArgs A) {
     __syncthreads();
     if (tid == 0) {
       const long long t0 = A.prof ? clock64() : 0;
-      const int h = atomicAdd(A.qhead, 1);
-      int t = -1;
-      if (h < A.ntasks) {
-        while ((t = *((volatile int*)&A.queue[h])) < 0) __nanosleep(32);
-        __threadfence();
-      }
+      const int t = pop_task(A);
       task_s = t;
       if (A.prof && t >= 0) atomicAdd(&A.prof[20], (unsigned long long)(clock64() - t0));
     }
@@ -754,8 +797,14 @@ __global__ void __launch_bounds__(kDT, 1) factor_dag_kernel(DagArgs A) {
         if (tid == 0) __threadfence();
         __syncthreads();
         const int a0 = a0_of(F, T.step), nr = D.tiles - a0;
-        for (int x = tid; x < nr * nr; x += kDT)
-          notify(A, idx_upd(A, D, F, T.step, a0 + x / nr, a0 + x % nr));
+        // lookahead first: the next panel's tile row and column, then the bulk
+        for (int x = tid; x < 2 * nr - 1; x += kDT) {
+          const int ua = x < nr ? a0 : a0 + (x - nr + 1), ub = x < nr ? a0 + x : a0;
+          notify(A, idx_upd(A, D, F, T.step, ua, ub));
+        }
+        __syncthreads();
+        for (int x = tid; x < (nr - 1) * (nr - 1); x += kDT)
+          notify(A, idx_upd(A, D, F, T.step, a0 + 1 + x / (nr - 1), a0 + 1 + x % (nr - 1)));
       }
     } else if (T.type == T_UPD) {
       if (tid == 0) {
@@ -900,7 +949,7 @@ void rqb_dag_build(FactorEngine& fe) {
   if (tasks.empty()) {
     tasks.push_back({0, T_SMALL, 0, 0, 0});
     deps.push_back(0);
-    queue0.push_back(-1);
+    queue0.assign(1, -1);
   }
   P->d_tasks.upload(tasks.data(), sizeof(Task) * tasks.size(), fe.stream);
   P->d_dag.upload(dag.data(), sizeof(FrontDag) * nfr, fe.stream);
@@ -964,8 +1013,7 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   A.flags = fe.d_flags.as<int>();
   A.deps = P.d_deps.as<int>();
   A.queue = P.d_queue.as<int>();
-  A.qhead = P.d_qctl.as<int>();
-  A.qtail = P.d_qctl.as<int>() + 1;
+  A.qctl = P.d_qctl.as<int>();
   A.step_base = P.d_sb.as<int32_t>();
   A.small_backup = P.d_small_backup.as<double>();
   A.prof = nullptr;
@@ -998,6 +1046,7 @@ void rqb_dag_profile(FactorEngine& fe, double* out) {
   out[18] = fe.dag->grid;
   out[19] = fe.dag->ntasks;
   out[20] = h[20] / (clk_khz * 1.0);  // ready-queue pop wait, summed over CTAs
+  for (int i = 21; i < 24; ++i) out[i] = h[i] / (clk_khz * 1.0);  // DIAG phases (LU, inv L, inv U)
 }
 
 void DagPlanDeleter::operator()(DagPlan* p) const { delete p; }

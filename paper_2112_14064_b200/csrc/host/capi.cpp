@@ -470,6 +470,7 @@ int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, doub
     eo.seed = opts->seed;
     eo.max_restarts = opts->max_restarts > 0 ? opts->max_restarts : 100;
     eo.guard = opts->guard;
+    eo.profile = opts->profile;
     eo.want_vectors = (vec_re && vec_im) ? 1 : 0;
     o->ledger = rqb::Ledger{};
     rqb::EigsResult r = rqb::solve_quadratic_device(*o->op, eo, o->ledger, o->norms1);
@@ -510,6 +511,10 @@ int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, doub
       I.t_host_ms = 0;
       I.launches = r.launches;
       I.restart_defect = r.max_restart_defect;
+      I.t_ritz_ms = r.t_ritz_ms;
+      I.t_check_ms = r.t_check_ms;
+      I.t_restart_ms = r.t_restart_ms;
+      I.t_sync_ms = r.t_sync_ms;
     }
     partial = r.nconv < opts->nev;
   });

@@ -156,7 +156,11 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   std::vector<int> final_block;  // 0 upper, 1 lower
   std::vector<double> final_vecs_re, final_vecs_im;
   std::vector<double> ha((m + 1) * (m + 1)), hb((m + 1) * (m + 1)), betas(m + 1);
-  double t_solve = 0, t_orth = 0;
+  double t_solve = 0, t_orth = 0, t_ritz = 0, t_check = 0, t_restart = 0, t_sync = 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms_since = [](std::chrono::steady_clock::time_point a) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+  };
   std::map<std::pair<int, const double*>, cudaGraphExec_t> graphs;
   struct GraphFree {
     std::map<std::pair<int, const double*>, cudaGraphExec_t>* g;
@@ -236,7 +240,11 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
                                cudaMemcpyDeviceToHost, st), "D2H H");
     cuda_check(cudaMemcpyAsync(betas.data(), dBeta.p, sizeof(double) * (m + 1),
                                cudaMemcpyDeviceToHost, st), "D2H beta");
-    cuda_check(cudaStreamSynchronize(st), "sync");
+    {
+      const auto ts0 = now();
+      cuda_check(cudaStreamSynchronize(st), "sync");
+      t_sync += ms_since(ts0);  // host blocked on the cycle's Arnoldi steps
+    }
     for (int j = k; j < m; ++j) {
       for (int i = 0; i <= j; ++i)
         Hc(i, j) = ha[i + static_cast<size_t>(j) * (m + 1)] + hb[i + static_cast<size_t>(j) * (m + 1)];
@@ -247,8 +255,10 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     for (int j = 0; j < m; ++j)
       for (int i = 0; i < m; ++i) Hm[i + static_cast<size_t>(j) * m] = Hc(i, j);
     CMat T, Z;
+    const auto tr0 = now();
     if (!complex_schur(Hm, m, T, Z)) fail(errc::solver, "Hessenberg QR did not converge");
     const CMat Y = triangular_eigvecs(T);
+    t_ritz += ms_since(tr0);
     const double beta_m = Hc(m, m - 1);
     std::vector<Ritz> rz(m);
     for (int i = 0; i < m; ++i) {
@@ -313,6 +323,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     bool all_conv = false, mates_conv = false;
     std::vector<double> cres(nchk, 1.0);
     std::vector<int> cblock(nchk, 0);
+    const auto tc0 = now();
     if (maybe) {
       // Ritz vectors X = V_m [Re y, Im y] (y = Z Y[:, i])
       std::vector<double> Yr(static_cast<size_t>(m) * 2 * nchk);
@@ -348,6 +359,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       }
       mates_conv = mates_conv && all_conv;
       L.n_check += 3 * nchk;
+      t_check += ms_since(tc0);
       L.macs_check += 6.0 * nnz * nchk;
     }
     int nconv_now = 0;
@@ -434,6 +446,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       }
     }
     // ---- restart: reorder Schur form, real basis of the kept directions ----
+    const auto trs0 = now();
     CMat Tr = T, Zr = Z;
     std::vector<int> s2 = sel;
     schur_reorder(Tr, Zr, s2);
@@ -483,6 +496,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       cuda_check(cudaMemcpyAsync(V + static_cast<int64_t>(p) * n2, V2 + static_cast<int64_t>(m) * n2,
                                  sizeof(double) * n2, cudaMemcpyDeviceToDevice, st), "D2D v");
     }
+    t_restart += ms_since(trs0);
     k = p;
   }
   cudaEventDestroy(e_a);
@@ -505,6 +519,10 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   res.t_total_ms = std::chrono::duration<double, std::milli>(clock::now() - t0).count();
   res.t_solve_ms = t_solve;
   res.t_orth_ms = t_orth;
+  res.t_ritz_ms = t_ritz;
+  res.t_check_ms = t_check;
+  res.t_restart_ms = t_restart;
+  res.t_sync_ms = t_sync;
   if (!converged_final) {
     res.nconv = static_cast<int>(std::count_if(res.resid.begin(), res.resid.end(),
                                                [&](double x) { return x <= o.tol; }));

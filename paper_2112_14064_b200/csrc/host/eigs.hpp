@@ -42,6 +42,7 @@ struct EigsResult {
   double t_total_ms = 0, t_solve_ms = 0, t_orth_ms = 0;
   double max_restart_defect = 0;  // max ||H Q - Q T|| / ||H|| over restarts
   int64_t graph_launches = 0;     // one CUDA graph replay per Krylov-Schur cycle
+  double t_ritz_ms = 0, t_check_ms = 0, t_restart_ms = 0, t_sync_ms = 0;  // host phase timers
 };
 
 // norms1 = {||K||_1, ||C||_1, ||M||_1} of the (scaled) pencil used by the

@@ -20,3 +20,4 @@ for cfg in sys.argv[1:]:
         busy, wait, cnt = out[3 * t:3 * t + 3]
         if cnt:
             print(f"   {nm:6s} n={int(cnt):7d} busy={busy:9.3f} ms (avg {busy / cnt * 1e3:8.2f} us) wait={wait:9.3f} ms (avg {wait / cnt * 1e3:8.2f} us)")
+    print(f"   DIAG phases (ms summed): LU {out[21]:.3f} invL {out[22]:.3f} invU+barrier {out[23]:.3f}")
