@@ -1,28 +1,30 @@
 // SPDX-License-Identifier: Apache-2.0
 // Multifrontal forward/backward substitution (solve_factored)
-// as two persistent, sync-free kernels (one per sweep) over the device-resident
-// fronts.
+// as two persistent dataflow kernels (one launch per sweep) over the
+// device-resident fronts.
 //
-// Work items are 64-row blocks of a front (pivot blocks, then contribution
-// rows), listed in a topological order of the dependency DAG (postorder of
-// the elimination tree forward, its reverse backward). CTAs draw items with an
-// atomic ticket, so an item only ever waits (spins) on items with smaller
-// tickets that are already running: no inter-launch waits, no level barriers,
-// and the whole sweep is one launch. Per item:
+// Work items are 64-row blocks of a front. Readiness is tracked per front:
+// when a front becomes ready (forward: its children completed; backward: the
+// nearest ancestor with pivots completed) one thread pushes ALL its items, in
+// order, on a FIFO ready queue; persistent CTAs claim queue slots in order.
+// Inside a front the items are left-looking and wait only for earlier items
+// of the same front (earlier queue slots, hence already claimed and running),
+// consuming each finished block as soon as it is published: the chain per
+// block is one 64x64 GEMV + one triangle, the L/U loads of the next block are
+// prefetched while waiting. No level barriers, one launch per sweep.
 //   forward   w = b(pivot rows, after the front's net row permutation) +
 //             children's contribution vectors (gather, atomic-free);
-//             s = sum over finished pivot blocks j of L[rows, j] y_j
-//             (left-looking, consumed as each block is published);
-//             pivot block: unit-lower 64x64 triangle from shared memory, write
-//             y, publish; contribution block: write w - s for the parent.
-//   backward  s = y - U[rows, cb] x_cb (ancestors' solution, already final)
-//             - U[rows, later pivot blocks] x (published in reverse order);
-//             upper 64x64 triangle; write x (ND order for descendants, caller
+//             s = L[rows, 0:j) y; pivot block: unit-lower 64x64 triangle in
+//             shared memory -> y; contribution rows: w - s -> the front's
+//             contribution vector for the parent.
+//   backward  s = y - U[rows, cb] x_cb (ancestors' solution) - U[rows, later] x;
+//             upper 64x64 triangle; writes x (ND order for descendants, caller
 //             order scaled, and the fused r_l = s r_u + v_u of apply_operator).
 // Loads of data produced inside the sweep use ld.global.cg (L1 bypass);
-// publication is __threadfence + atomicAdd, consumption volatile-spin +
-// __threadfence.
+// publication is __threadfence + atomic.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 
@@ -31,268 +33,512 @@ namespace rqb {
 constexpr int kRB = 64;   // rows per item
 constexpr int kST = 256;  // threads per CTA
 
+// One work item: up to 64 rows of a front, with the front fields it needs
+// (one 64-byte record; the item's first instruction loads need no further
+// indirection).
 struct SolveItem {
-  int32_t front, r0, r1, blk;  // local rows [r0, r1), pivot-block index (-1: contribution rows)
+  int64_t goff;                   // front's pool offset (doubles)
+  int32_t front, r0, nr, blk;     // local rows [r0, r0+nr); pivot-block index, -1 contribution rows
+  int32_t ld, np, nf, start;
+  int32_t npb, ncbb, parent, rows_off;
+  int32_t cbvec_off, ech_off, nech, pad;
 };
 
+struct SweepArgs {
+  const SolveItem* items;
+  int nitems;
+  int* deps;      // per front: unfinished predecessor fronts
+  int* queue;
+  int* qctl;      // {head, tail}
+  int* pub;       // per front: pivot blocks published (forward: first first; backward: last first)
+  int* fin;       // per front: forward items finished
+  int fwd;        // 1 forward, 0 backward (item layout of front_ready)
+  const int32_t* fbase;  // per front: first item of this sweep
+  const int32_t* fcnt;   // per front: items of this sweep
+  const int32_t* npb;    // per front: pivot blocks
+  const int32_t* ech;
+  const int4* gsrc;      // forward gather sources per front row {b, child0 cb, child1 cb, -}
+  const double* pool;
+  const int32_t* perm;
+  const int32_t* rows;
+  const double* b;
+  double* y;
+  double* cbvec;
+  double* xnew;
+  double* xout;
+  double scale;
+  const double* vu;
+  double sigma;
+  double* xl_out;
+  unsigned long long* trace;  // development trace (RQB_SOLVE_TRACE): per item 4 timestamps, SM, ns waited
+};
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define RQB_TRACE(k)                                                       \
+  if (A.trace && tid == 0) {                                               \
+    A.trace[8 * (size_t)it + (k)] = gtime();                               \
+  }
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Items enter the queue through a window of kWin pivot blocks: item v of a
+// front (forward: pivot block v, v == npb stands for all contribution items;
+// backward: the v-th block from the end) is pushed when the front becomes
+// ready (v < kWin) or when the front's item v - kWin publishes. An item then
+// waits for at most kWin - 1 blocks instead of holding a CTA through the
+// whole pivot chain. Pushes of one front happen in item order, so every wait
+// targets an earlier queue slot (deadlock freedom of the FIFO claim order).
+constexpr int kWin = 8;
+constexpr int kStage = 1024;  // staged solution entries per round (8 KB)
+// Fronts with at most kWholeNpb pivot blocks and kWholeCb contribution rows
+// are one item per sweep (a single CTA walks the whole front, its y / x kept
+// in shared memory): no inter-CTA publication latency on the many small
+// fronts near the leaves.
+constexpr int kWholeNpb = 2;
+constexpr int kWholeCb = kStage - kWholeNpb * kRB;
+constexpr int kWhole = -2;  // SolveItem::blk of a whole-front item
+
+__device__ __forceinline__ void push_items(const SweepArgs& A, int i0, int n) {
+  const int slot = atomicAdd(&A.qctl[1], n);
+  for (int i = 0; i < n; ++i) atomicExch(&A.queue[slot + i], i0 + i);
+}
+
+// push virtual items [v0, v1] of front f (clipped to what exists)
+__device__ __forceinline__ void push_window(const SweepArgs& A, int f, int v0, int v1) {
+  const int npb = A.npb[f], base = A.fbase[f];
+  if (A.fwd) {
+    v1 = min(v1, npb);
+    if (v0 > v1) return;
+    const int end = v1 == npb ? base + A.fcnt[f] : base + v1 + 1;
+    if (base + v0 < end) push_items(A, base + v0, end - base - v0);
+  } else {
+    v1 = min(v1, npb - 1);
+    if (v0 <= v1) push_items(A, base + v0, v1 - v0 + 1);
+  }
+}
+
+// one predecessor front of f finished; the last one opens f's window
+__device__ __forceinline__ void front_ready(const SweepArgs& A, int f) {
+  if (atomicSub(&A.deps[f], 1) == 1) {
+    __threadfence();
+    push_window(A, f, 0, kWin - 1);
+  }
+}
+
 __device__ __forceinline__ void wait_ge(const int* p, int target) {
-  if (*((volatile const int*)p) >= target) return;
-  while (*((volatile const int*)p) < target) __nanosleep(64);
+  while (ld_acquire(p) < target) __nanosleep(20);
 }
 
-__device__ __forceinline__ void publish(int* p) {
-  __threadfence();
-  atomicAdd(p, 1);
+__device__ __forceinline__ int pop_item(const SweepArgs& A) {
+  const int h = atomicAdd(&A.qctl[0], 1);
+  if (h >= A.nitems) return -1;
+  int t;
+  while ((t = ld_acquire(&A.queue[h])) < 0) __nanosleep(20);
+  return t;
 }
 
-// cnt layout per front: [3f+0] pivot blocks published, [3f+1] items published,
-// [3f+2] backward pivot blocks published. tickets: [0] fwd, [1] bwd.
-__global__ void __launch_bounds__(kST) fwd_sweep(
-    const FrontDev* __restrict__ fronts, const SolveItem* __restrict__ items, int nitems,
-    const int32_t* __restrict__ nitems_front, const int32_t* __restrict__ inv,
-    const double* __restrict__ pool, const int32_t* __restrict__ rowperm,
-    const int32_t* __restrict__ perm, const double* __restrict__ b, double* __restrict__ y,
-    double* __restrict__ cbvec, int* __restrict__ cnt, int* __restrict__ tickets) {
+// s += sum_{c in [cb, ce)} L[row, c] xs[c] for this thread's column class
+// (c = grp mod 4): eight independent column loads in flight per iteration,
+// each a 512-byte coalesced segment across the 64 rows of the item.
+__device__ __forceinline__ double stream_cols(const double* lp, int64_t ld, const double* xs, int cb, int ce,
+                                              int grp) {
+  double s0 = 0.0, s1 = 0.0;
+  int c = cb + grp;
+  for (; c + 28 < ce; c += 32) {
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = lp[(int64_t)(c + 4 * u) * ld];
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      s0 += a[u] * xs[c + 4 * u];
+      s1 += a[u + 1] * xs[c + 4 * u + 4];
+    }
+  }
+  for (; c < ce; c += 4) s0 += lp[(int64_t)c * ld] * xs[c];
+  return s0 + s1;
+}
+
+// registers of one 64-column block (issued before the wait for it)
+__device__ __forceinline__ void load_block(double (&r)[kRB / 4], const double* lp, int64_t ld, bool rowok, int c0,
+                                           int c1, int grp) {
+#pragma unroll
+  for (int u = 0; u < kRB / 4; ++u) {
+    const int c = c0 + grp + 4 * u;
+    r[u] = (rowok && c < c1) ? lp[(int64_t)c * ld] : 0.0;
+  }
+}
+
+// sum of r[u] xs[grp + 4u] over the cw valid columns of a block
+__device__ __forceinline__ double fma_block(const double (&r)[kRB / 4], const double* xs, int cw, int grp) {
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < kRB / 4; ++u)
+    if (grp + 4 * u < cw) s += r[u] * xs[grp + 4 * u];
+  return s;
+}
+
+// Diagonal block of an item into shared memory, padded to 64 x 64 with
+// zeros (rows/columns >= nr), so the triangles below run a fixed, fully
+// unrolled 64-step schedule. Backward: columns pre-scaled by the reciprocal
+// diagonal (E[r][c] = U[r][c] / U[c][c], rinv[r] = 1 / U[r][r]) so the serial
+// chain of the substitution is one shuffle + one FMA per step.
+template <bool kUpper>
+__device__ __forceinline__ void load_diag(double* D, double* rinv, const double* g, int64_t ld, int r0, int nr,
+                                          int tid) {
+  if (kUpper) {
+    if (tid < kRB) rinv[tid] = tid < nr ? 1.0 / g[(r0 + tid) + (int64_t)(r0 + tid) * ld] : 0.0;
+    __syncthreads();
+  }
+  for (int idx = tid; idx < kRB * kRB; idx += kST) {
+    const int r = idx & (kRB - 1), c = idx >> 6;
+    double v = (r < nr && c < nr) ? g[(r0 + r) + (int64_t)(r0 + c) * ld] : 0.0;
+    if (kUpper) v *= rinv[c];
+    D[r + c * (kRB + 1)] = v;
+  }
+}
+
+// forward: unit-lower 64x64 substitution in warp 0; lane holds rows lane, lane+32
+__device__ __forceinline__ void fwd_triangle(const double* D, int lane, double& v0, double& v1) {
+#pragma unroll
+  for (int c = 0; c < kRB; ++c) {
+    const double yc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
+    if (c < 32) {
+      if (lane > c) v0 -= D[lane + c * (kRB + 1)] * yc;
+      v1 -= D[lane + 32 + c * (kRB + 1)] * yc;
+    } else if (lane + 32 > c) {
+      v1 -= D[lane + 32 + c * (kRB + 1)] * yc;
+    }
+  }
+}
+
+// backward: upper substitution on the column-scaled block; on return v0/v1
+// are the right-hand sides after all updates (x = v * rinv[row])
+__device__ __forceinline__ void bwd_triangle(const double* E, int lane, double& v0, double& v1) {
+#pragma unroll
+  for (int c = kRB - 1; c >= 0; --c) {
+    const double vc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
+    if (c >= 32) {
+      v0 -= E[lane + c * (kRB + 1)] * vc;
+      if (lane + 32 < c) v1 -= E[lane + 32 + c * (kRB + 1)] * vc;
+    } else if (lane < c) {
+      v0 -= E[lane + c * (kRB + 1)] * vc;
+    }
+  }
+}
+
+__device__ __forceinline__ void red_release(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kST, 3) fwd_sweep(SweepArgs A) {
   __shared__ double D[kRB * (kRB + 1)];
-  __shared__ double yb[kRB];
+  __shared__ double stg[kStage];  // staged y (whole-front items: the front's own y)
   __shared__ double part[4][kRB];
   __shared__ double wv[kRB];
-  __shared__ int item_s;
+  __shared__ int item_s, avail_s;
   const int tid = threadIdx.x, row = tid & (kRB - 1), grp = tid >> 6;
   for (;;) {
     __syncthreads();
-    if (tid == 0) item_s = atomicAdd(&tickets[0], 1);
+    if (tid == 0) item_s = pop_item(A);
     __syncthreads();
     const int it = item_s;
-    if (it >= nitems) return;
-    const SolveItem I = items[it];
-    const FrontDev F = fronts[I.front];
-    const int np = F.npiv, nr = I.r1 - I.r0;
-    const double* g = pool + F.off;
-    const int64_t ld = F.ld;
-    // (1) everything that does not depend on other items: index maps, b, the
-    //     diagonal block, the first L block of this thread
-    const int32_t* inv0 = inv + F.inv_off;
-    double bv = 0.0;
-    int ir0 = -1, ir1 = -1;
-    if (tid < nr) {
-      const int r = I.r0 + tid;
-      const int q = r < np ? __ldg(&rowperm[F.start + r]) : r;  // pre-swap local row
-      bv = q < np ? b[perm[F.start + q]] : 0.0;
-      if (F.nchild > 0) ir0 = inv0[q];
-      if (F.nchild > 1) ir1 = inv0[F.nf + q];
+    if (it < 0) return;
+    RQB_TRACE(0);
+    const SolveItem I = A.items[it];
+    const int np = I.np;
+    const double* g = A.pool + I.goff;
+    const int64_t ld = I.ld;
+    const bool whole = I.blk == kWhole;
+    const int nck = whole ? I.npb + I.ncbb : 1;
+    unsigned long long waited = 0;
+    for (int ck = 0; ck < nck; ++ck) {
+      int r0 = I.r0, nr = I.nr, blk = I.blk;
+      if (whole) {
+        blk = ck < I.npb ? ck : -1;
+        r0 = ck < I.npb ? ck * kRB : np + (ck - I.npb) * kRB;
+        nr = (ck < I.npb ? min(np, r0 + kRB) : min(I.nf, r0 + kRB)) - r0;
+      }
+      // w = b + children's contributions (children complete: the front is ready)
+      if (tid < nr) {
+        const int4 src = __ldg(&A.gsrc[I.rows_off + r0 + tid]);
+        double v = src.x >= 0 ? A.b[src.x] : 0.0;
+        if (src.y >= 0) v += __ldcg(&A.cbvec[src.y]);
+        if (src.z >= 0) v += __ldcg(&A.cbvec[src.z]);
+        wv[tid] = v;
+      }
+      if (blk >= 0) load_diag<false>(D, nullptr, g, ld, r0, nr, tid);
+      __syncthreads();
+      if (ck == 0) RQB_TRACE(1);
+      // s = L[rows, 0:ncol) y
+      const int ncol = min(np, (blk >= 0 ? blk : I.npb) * kRB);
+      const double* lp = g + (r0 + row);
+      double s = 0.0;
+      if (whole) {  // y of the earlier blocks is this CTA's own (stg): no waits
+        if (row < nr) s = stream_cols(lp, ld, stg, 0, ncol, grp);
+      } else {
+        // rounds: take every block published so far, stage its y, stream it;
+        // the L of the first block not yet seen published is in flight during the wait
+        int done = 0;
+        while (done < ncol) {
+          const int b1 = min(ncol, done + kRB);
+          double lr[kRB / 4];
+          load_block(lr, lp, ld, row < nr, done, b1, grp);
+          if (tid == 0) {
+            const unsigned long long w0 = A.trace ? gtime() : 0;
+            int p;
+            while ((p = ld_acquire(&A.pub[I.front])) * kRB <= done) __nanosleep(20);
+            avail_s = min(ncol, p * kRB);
+            if (A.trace) {
+              const unsigned long long w1 = gtime();
+              waited += w1 - w0;
+              A.trace[8 * (size_t)it + 4] = w1;
+            }
+          }
+          __syncthreads();
+          const int avail = avail_s;
+          for (int base = done; base < avail; base += kStage) {
+            const int hi = min(avail, base + kStage);
+            for (int c = tid; c < hi - base; c += kST) stg[c] = __ldcg(&A.y[I.start + base + c]);
+            __syncthreads();
+            if (row < nr) {
+              if (base == done) {
+                s += fma_block(lr, stg, b1 - done, grp);
+                s += stream_cols(lp, ld, stg - base, b1, hi, grp);
+              } else {
+                s += stream_cols(lp, ld, stg - base, base, hi, grp);
+              }
+            }
+            __syncthreads();
+          }
+          done = avail;
+        }
+      }
+      part[grp][row] = s;
+      if (A.trace && tid == 0) A.trace[8 * (size_t)it + 6] = gtime();
+      __syncthreads();
+      if (blk >= 0) {
+        if (tid < 32) {
+          double v0 = tid < nr ? wv[tid] - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]) : 0.0;
+          double v1 = tid + 32 < nr
+                          ? wv[tid + 32] - (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32])
+                          : 0.0;
+          fwd_triangle(D, tid, v0, v1);
+          if (A.trace && tid == 0) A.trace[8 * (size_t)it + 7] = gtime();
+          if (tid < nr) A.y[I.start + r0 + tid] = v0;
+          if (tid + 32 < nr) A.y[I.start + r0 + tid + 32] = v1;
+          if (whole) {
+            if (tid < nr) stg[r0 + tid] = v0;
+            if (tid + 32 < nr) stg[r0 + tid + 32] = v1;
+          }
+        }
+      } else if (tid < nr) {
+        A.cbvec[I.cbvec_off + r0 + tid - np] = wv[tid] - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]);
+      }
+      __syncthreads();
     }
-    if (I.blk >= 0)
-      for (int idx = tid; idx < nr * nr; idx += kST) {
-        const int r = idx % nr, c = idx / nr;
-        D[r + c * (kRB + 1)] = g[(I.r0 + r) + (int64_t)(I.r0 + c) * ld];
-      }
-    const int nblk = I.blk >= 0 ? I.blk : (np + kRB - 1) / kRB;
-    double lreg[kRB / 4];
-    auto prefetch = [&](int j) {
-      const int c0 = j * kRB, cw = min(np, c0 + kRB) - c0;
-      const double* lp = g + (I.r0 + row) + (int64_t)c0 * ld;
-#pragma unroll
-      for (int u = 0; u < kRB / 4; ++u) {
-        const int c = grp + 4 * u;
-        lreg[u] = (row < nr && c < cw) ? lp[c * ld] : 0.0;
-      }
-    };
-    if (nblk > 0) prefetch(0);
-    // (2) children complete -> gather their contribution vectors
+    RQB_TRACE(2);
+    if (A.trace && tid == 0) A.trace[8 * (size_t)it + 5] = waited;
+    // ---- publish; the front's last item makes the parent one step readier
     if (tid == 0) {
-      if (F.nchild > 0) wait_ge(&cnt[3 * F.child0 + 1], nitems_front[F.child0]);
-      if (F.nchild > 1) wait_ge(&cnt[3 * F.child1 + 1], nitems_front[F.child1]);
+      if (I.blk >= 0) {
+        red_release(&A.pub[I.front], 1);
+        push_window(A, I.front, I.blk + kWin, I.blk + kWin);
+      }
       __threadfence();
+      RQB_TRACE(3);
+      const bool last = whole || atomicAdd(&A.fin[I.front], 1) + 1 == I.npb + I.ncbb;
+      if (last && I.parent >= 0) front_ready(A, I.parent);
     }
+  }
+}
+
+__global__ void __launch_bounds__(kST, 3) bwd_sweep(SweepArgs A) {
+  __shared__ double D[kRB * (kRB + 1)];
+  // staged x; whole-front items: [0, np) the front's own x, [kWholeNpb*64, ...) the ancestors' x_cb
+  __shared__ double stg[kStage];
+  __shared__ double part[4][kRB];
+  __shared__ double rinv[kRB];
+  __shared__ int item_s, avail_s;
+  const int tid = threadIdx.x, row = tid & (kRB - 1), grp = tid >> 6;
+  for (;;) {
     __syncthreads();
-    if (tid < nr) {
-      double v = bv;
-      if (ir0 >= 0) v += __ldcg(&cbvec[fronts[F.child0].cbvec_off + ir0 - fronts[F.child0].npiv]);
-      if (ir1 >= 0) v += __ldcg(&cbvec[fronts[F.child1].cbvec_off + ir1 - fronts[F.child1].npiv]);
-      wv[tid] = v;
-    }
-    // (3) left-looking over the published pivot blocks, next L block prefetched
-    double s = 0.0;
-    for (int j = 0; j < nblk; ++j) {
-      if (tid == 0) {
-        wait_ge(&cnt[3 * I.front + 0], j + 1);
-        __threadfence();
+    if (tid == 0) item_s = pop_item(A);
+    __syncthreads();
+    const int it = item_s;
+    if (it < 0) return;
+    RQB_TRACE(0);
+    const SolveItem I = A.items[it];
+    const int np = I.np, nf = I.nf;
+    const double* g = A.pool + I.goff;
+    const int64_t ld = I.ld;
+    const int32_t* rw = A.rows + I.rows_off;
+    const bool whole = I.blk == kWhole;
+    constexpr int kCbBase = kWholeNpb * kRB;
+    if (whole)
+      for (int c = tid; c < nf - np; c += kST) stg[kCbBase + c] = __ldcg(&A.xnew[rw[np + c]]);
+    const int nck = whole ? I.npb : 1;
+    unsigned long long waited = 0;
+    for (int ck = 0; ck < nck; ++ck) {
+      const int blk = whole ? I.npb - 1 - ck : I.blk;
+      const int r0 = blk * kRB, nr = min(np, r0 + kRB) - r0;
+      load_diag<true>(D, rinv, g, ld, r0, nr, tid);
+      double y0 = 0.0, y1 = 0.0;
+      if (tid < 32) {
+        if (tid < nr) y0 = A.y[I.start + r0 + tid];
+        if (tid + 32 < nr) y1 = A.y[I.start + r0 + tid + 32];
       }
       __syncthreads();
-      const int c0 = j * kRB, c1 = min(np, c0 + kRB);
-      if (tid < kRB) yb[tid] = tid < c1 - c0 ? __ldcg(&y[F.start + c0 + tid]) : 0.0;
-      __syncthreads();
-#pragma unroll
-      for (int u = 0; u < kRB / 4; ++u) s += lreg[u] * yb[grp + 4 * u];
-      if (j + 1 < nblk) prefetch(j + 1);
-    }
-    part[grp][row] = s;
-    __syncthreads();
-    if (tid < nr) wv[tid] -= part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
-    if (I.blk >= 0) {
-      // unit-lower diagonal block (already in shared memory)
+      if (ck == 0) RQB_TRACE(1);
+      // columns right of this block: contribution columns (ancestors' x, final
+      // since the front is ready), then this front's later pivot blocks
+      const double* up = g + (r0 + row);
+      const int lo = (blk + 1) * kRB;
+      double s = 0.0;
+      if (whole) {
+        if (row < nr) {
+          s = stream_cols(up, ld, stg + kCbBase - np, np, nf, grp);
+          s += stream_cols(up, ld, stg, lo, np, grp);
+        }
+      } else {
+        for (int base = np; base < nf; base += kStage) {
+          const int hi = min(nf, base + kStage);
+          for (int c = tid; c < hi - base; c += kST) stg[c] = __ldcg(&A.xnew[rw[base + c]]);
+          __syncthreads();
+          if (row < nr) s += stream_cols(up, ld, stg - base, base, hi, grp);
+          __syncthreads();
+        }
+        // later pivot blocks are published last first: rounds over [avail_lo, done_hi);
+        // the U of the next block to come is in flight during the wait
+        int done_hi = np;
+        while (done_hi > lo) {
+          const int b0 = max(lo, ((done_hi - 1) / kRB) * kRB);
+          double ur[kRB / 4];
+          load_block(ur, up, ld, row < nr, b0, done_hi, grp);
+          if (tid == 0) {
+            const unsigned long long w0 = A.trace ? gtime() : 0;
+            int p;
+            while (max(lo, (I.npb - (p = ld_acquire(&A.pub[I.front]))) * kRB) >= done_hi) __nanosleep(20);
+            avail_s = max(lo, (I.npb - p) * kRB);
+            if (A.trace) {
+              const unsigned long long w1 = gtime();
+              waited += w1 - w0;
+              A.trace[8 * (size_t)it + 4] = w1;
+            }
+          }
+          __syncthreads();
+          const int avail_lo = avail_s;
+          for (int top = done_hi; top > avail_lo; top -= kStage) {
+            const int bot = max(avail_lo, top - kStage);
+            for (int c = tid; c < top - bot; c += kST) stg[c] = __ldcg(&A.xnew[I.start + bot + c]);
+            __syncthreads();
+            if (row < nr) {
+              if (top == done_hi) {
+                s += fma_block(ur, stg + (b0 - bot), done_hi - b0, grp);
+                s += stream_cols(up, ld, stg - bot, bot, b0, grp);
+              } else {
+                s += stream_cols(up, ld, stg - bot, bot, top, grp);
+              }
+            }
+            __syncthreads();
+          }
+          done_hi = avail_lo;
+        }
+      }
+      part[grp][row] = s;
+      if (A.trace && tid == 0) A.trace[8 * (size_t)it + 6] = gtime();
       __syncthreads();
       if (tid < 32) {
-        double v0 = tid < nr ? wv[tid] : 0.0, v1 = tid + 32 < nr ? wv[tid + 32] : 0.0;
-        for (int c = 0; c < nr; ++c) {
-          const double yc = c < 32 ? __shfl_sync(0xffffffffu, v0, c) : __shfl_sync(0xffffffffu, v1, c - 32);
-          if (tid > c) v0 -= D[tid + c * (kRB + 1)] * yc;
-          if (tid + 32 > c && tid + 32 < nr) v1 -= D[tid + 32 + c * (kRB + 1)] * yc;
+        double v0 = 0.0, v1 = 0.0;
+        if (tid < nr) v0 = y0 - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]);
+        if (tid + 32 < nr)
+          v1 = y1 - (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32]);
+        bwd_triangle(D, tid, v0, v1);
+        v0 *= rinv[tid];
+        v1 *= rinv[tid + 32];
+        if (A.trace && tid == 0) A.trace[8 * (size_t)it + 7] = gtime();
+        for (int h = 0; h < 2; ++h) {
+          const int r = tid + 32 * h;
+          if (r < nr) {
+            const double v = h ? v1 : v0;
+            const int gi = I.start + r0 + r;
+            A.xnew[gi] = v;
+            if (whole) stg[r0 + r] = v;
+            const int o = A.perm[gi];
+            const double sv = A.scale * v;
+            A.xout[o] = sv;
+            if (A.xl_out) A.xl_out[o] = A.sigma * sv + A.vu[o];
+          }
         }
-        if (tid < nr) y[F.start + I.r0 + tid] = v0;
-        if (tid + 32 < nr) y[F.start + I.r0 + tid + 32] = v1;
       }
       __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        atomicAdd(&cnt[3 * I.front + 0], 1);
-        atomicAdd(&cnt[3 * I.front + 1], 1);
-      }
-    } else {
-      if (tid < nr) cbvec[F.cbvec_off + I.r0 + tid - np] = wv[tid];
-      __syncthreads();
-      if (tid == 0) publish(&cnt[3 * I.front + 1]);
     }
-  }
-}
-
-__global__ void __launch_bounds__(kST) bwd_sweep(
-    const FrontDev* __restrict__ fronts, const SolveItem* __restrict__ items, int nitems,
-    const int32_t* __restrict__ npb_front, const int32_t* __restrict__ parent,
-    const int32_t* __restrict__ rows, const double* __restrict__ pool,
-    const int32_t* __restrict__ perm, const double* __restrict__ y, double* __restrict__ xnew,
-    double* __restrict__ xout, double scale, const double* __restrict__ vu, double sigma,
-    double* __restrict__ xl_out, int* __restrict__ cnt, int* __restrict__ tickets) {
-  __shared__ double D[kRB * (kRB + 1)];
-  __shared__ double xb[kRB];
-  __shared__ double part[4][kRB];
-  __shared__ int item_s;
-  const int tid = threadIdx.x, row = tid & (kRB - 1), grp = tid >> 6;
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) item_s = atomicAdd(&tickets[1], 1);
-    __syncthreads();
-    const int it = item_s;
-    if (it >= nitems) return;
-    const SolveItem I = items[it];
-    const FrontDev F = fronts[I.front];
-    const int np = F.npiv, nf = F.nf, nr = I.r1 - I.r0;
-    const int par = parent[I.front];
-    const double* g = pool + F.off;
-    const int64_t ld = F.ld;
-    const int32_t* rw = rows + F.rows_off;
-    // (1) independent loads: diagonal block, y of this block, first U chunk
-    for (int idx = tid; idx < nr * nr; idx += kST) {
-      const int r = idx % nr, c = idx / nr;
-      D[r + c * (kRB + 1)] = g[(I.r0 + r) + (int64_t)(I.r0 + c) * ld];
-    }
-    double y0 = 0.0, y1 = 0.0;
-    if (tid < 32) {
-      if (tid < nr) y0 = y[F.start + I.r0 + tid];
-      if (tid + 32 < nr) y1 = y[F.start + I.r0 + tid + 32];
-    }
-    const int npb = (np + kRB - 1) / kRB;
-    const int ncbc = (nf - np + kRB - 1) / kRB;  // contribution-column chunks (ancestors' x)
-    const int nch = ncbc + (npb - 1 - I.blk);     // + later pivot blocks (last first)
-    auto chunk = [&](int t, int& c0, int& c1, bool& piv) {
-      if (t < ncbc) {
-        c0 = np + t * kRB;
-        c1 = min(nf, c0 + kRB);
-        piv = false;
-      } else {
-        const int j = npb - 1 - (t - ncbc);
-        c0 = j * kRB;
-        c1 = min(np, c0 + kRB);
-        piv = true;
-      }
-    };
-    double ureg[kRB / 4];
-    auto prefetch = [&](int t) {
-      int c0, c1;
-      bool pv;
-      chunk(t, c0, c1, pv);
-      const double* up = g + (I.r0 + row) + (int64_t)c0 * ld;
-#pragma unroll
-      for (int u = 0; u < kRB / 4; ++u) {
-        const int c = grp + 4 * u;
-        ureg[u] = (row < nr && c < c1 - c0) ? up[c * ld] : 0.0;
-      }
-    };
-    if (nch > 0) prefetch(0);
+    RQB_TRACE(2);
+    if (A.trace && tid == 0) A.trace[8 * (size_t)it + 5] = waited;
+    // ---- publish; block 0 completes the front: its effective children are ready
     if (tid == 0) {
-      if (par >= 0) wait_ge(&cnt[3 * par + 2], npb_front[par]);
-      __threadfence();
-    }
-    __syncthreads();
-    double s = 0.0;
-    for (int t = 0; t < nch; ++t) {
-      int c0, c1;
-      bool pv;
-      chunk(t, c0, c1, pv);
-      if (pv && tid == 0) {
-        wait_ge(&cnt[3 * I.front + 2], npb - c0 / kRB);
-        __threadfence();
+      if (!whole) {
+        red_release(&A.pub[I.front], 1);
+        const int v = I.npb - 1 - I.blk + kWin;
+        push_window(A, I.front, v, v);
       }
-      __syncthreads();
-      if (tid < kRB)
-        xb[tid] = tid < c1 - c0 ? __ldcg(&xnew[pv ? F.start + c0 + tid : rw[c0 + tid]]) : 0.0;
-      __syncthreads();
-#pragma unroll
-      for (int u = 0; u < kRB / 4; ++u) s += ureg[u] * xb[grp + 4 * u];
-      if (t + 1 < nch) prefetch(t + 1);
+      RQB_TRACE(3);
     }
-    part[grp][row] = s;
-    __syncthreads();
-    if (tid < 32) {
-      double v0 = 0.0, v1 = 0.0;
-      if (tid < nr) v0 = y0 - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]);
-      if (tid + 32 < nr)
-        v1 = y1 - (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32]);
-      for (int c = nr - 1; c >= 0; --c) {
-        if (c < 32) {
-          if (tid == c) v0 /= D[c + c * (kRB + 1)];
-        } else {
-          if (tid == c - 32) v1 /= D[c + c * (kRB + 1)];
-        }
-        const double xc = c < 32 ? __shfl_sync(0xffffffffu, v0, c) : __shfl_sync(0xffffffffu, v1, c - 32);
-        if (tid < c) v0 -= D[tid + c * (kRB + 1)] * xc;
-        if (tid + 32 < c) v1 -= D[tid + 32 + c * (kRB + 1)] * xc;
-      }
-      for (int h = 0; h < 2; ++h) {
-        const int r = tid + 32 * h;
-        if (r < nr) {
-          const double v = h ? v1 : v0;
-          const int gi = F.start + I.r0 + r;
-          xnew[gi] = v;
-          const int o = perm[gi];
-          const double sv = scale * v;
-          xout[o] = sv;
-          if (xl_out) xl_out[o] = sigma * sv + vu[o];
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) publish(&cnt[3 * I.front + 2]);
+    if (I.blk <= 0)
+      for (int x = tid; x < I.nech; x += kST) front_ready(A, A.ech[I.ech_off + x]);
   }
 }
 
-// Net row permutation of every front's pivot block after factorization:
-// rowperm[start + k] = pre-swap local row found at position k.
-__global__ void net_rowperm(const FrontDev* __restrict__ fronts, int nfronts,
-                            const int32_t* __restrict__ ipiv, int32_t* __restrict__ rowperm) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nfronts) return;
+// After factorization, one CTA per front: the net row permutation of its
+// pivot block (rowperm[start + k] = pre-swap local row at position k) and the
+// forward-sweep gather sources of every front row r (q = pre-swap row):
+// {caller index of b (pivot rows), child-0 / child-1 contribution-vector
+// entries, or -1}.
+__global__ void net_rowperm(const FrontDev* __restrict__ fronts, const int32_t* __restrict__ ipiv,
+                            const int32_t* __restrict__ perm, const int32_t* __restrict__ inv,
+                            int32_t* __restrict__ rowperm, int4* __restrict__ gsrc) {
+  const int f = blockIdx.x;
   const FrontDev F = fronts[f];
   int32_t* rp = rowperm + F.start;
-  for (int k = 0; k < F.npiv; ++k) rp[k] = k;
-  for (int k = 0; k < F.npiv; ++k) {
-    const int p = ipiv[F.start + k];
-    if (p != k) {
-      const int32_t t = rp[k];
-      rp[k] = rp[p];
-      rp[p] = t;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < F.npiv; ++k) rp[k] = k;
+    for (int k = 0; k < F.npiv; ++k) {
+      const int p = ipiv[F.start + k];
+      if (p != k) {
+        const int32_t t = rp[k];
+        rp[k] = rp[p];
+        rp[p] = t;
+      }
     }
+  }
+  __syncthreads();
+  int64_t c0off = 0, c1off = 0;
+  if (F.nchild > 0) c0off = fronts[F.child0].cbvec_off - fronts[F.child0].npiv;
+  if (F.nchild > 1) c1off = fronts[F.child1].cbvec_off - fronts[F.child1].npiv;
+  const int32_t* inv0 = inv + F.inv_off;
+  for (int r = threadIdx.x; r < F.nf; r += blockDim.x) {
+    const int q = r < F.npiv ? rp[r] : r;
+    int4 v;
+    v.x = q < F.npiv ? perm[F.start + q] : -1;
+    v.y = -1;
+    v.z = -1;
+    v.w = 0;
+    if (F.nchild > 0) {
+      const int ir = inv0[q];
+      if (ir >= 0) v.y = static_cast<int>(c0off + ir);
+    }
+    if (F.nchild > 1) {
+      const int ir = inv0[F.nf + q];
+      if (ir >= 0) v.z = static_cast<int>(c1off + ir);
+    }
+    gsrc[F.rows_off + r] = v;
   }
 }
 
@@ -304,64 +550,228 @@ void rqb_solve_prepare(FactorEngine& fe) {
   const Symbolic& S = fe.sym;
   const int nfr = static_cast<int>(S.fronts.size());
   std::vector<SolveItem> fwd, bwd;
-  std::vector<int32_t> nitems(nfr, 0), npb(nfr, 0), parent(nfr, -1);
+  std::vector<int32_t> ech, fbase_f(nfr), fcnt_f(nfr), fbase_b(nfr, 0), fcnt_b(nfr, 0);
+  std::vector<std::vector<int32_t>> echl(nfr);
+  std::vector<int32_t> npb(nfr), ncbb(nfr);
+  int64_t cbtot = 0;
   for (int f = 0; f < nfr; ++f) {
     const Front& F = S.fronts[f];
-    int a = F.parent;  // nearest ancestor that has pivots (empty separators pass through)
-    while (a >= 0 && S.fronts[a].npiv == 0) a = S.fronts[a].parent;
-    parent[f] = a;
-    const int nb = (F.npiv + kRB - 1) / kRB;
-    npb[f] = nb;
-    for (int b = 0; b < nb; ++b) fwd.push_back({f, b * kRB, std::min(F.npiv, (b + 1) * kRB), b});
-    for (int r = F.npiv; r < F.nf; r += kRB) fwd.push_back({f, r, std::min(F.nf, r + kRB), -1});
-    nitems[f] = nb + (F.nf - F.npiv + kRB - 1) / kRB;
+    npb[f] = (F.npiv + kRB - 1) / kRB;
+    ncbb[f] = (F.nf - F.npiv + kRB - 1) / kRB;
+    if (npb[f] + ncbb[f] == 0) throw Error(errc::solver, "solve: front without rows");
+    if (npb[f] > 0) {
+      int a = F.parent;  // nearest ancestor with pivots (empty separators pass through)
+      while (a >= 0 && S.fronts[a].npiv == 0) a = S.fronts[a].parent;
+      if (a >= 0) echl[a].push_back(f);
+    }
+    cbtot = std::max<int64_t>(cbtot, fe.fronts_h[f].cbvec_off + F.nf);
+  }
+  if (static_cast<int64_t>(S.rows.size()) > INT32_MAX || cbtot > INT32_MAX || fe.n > INT32_MAX)
+    throw Error(errc::solver, "solve: index range exceeds int32");
+  int32_t eoff = 0;
+  std::vector<int32_t> ech_off(nfr);
+  for (int f = 0; f < nfr; ++f) {
+    ech_off[f] = eoff;
+    ech.insert(ech.end(), echl[f].begin(), echl[f].end());
+    eoff += static_cast<int32_t>(echl[f].size());
+  }
+  auto item = [&](int f, int r0, int r1, int blk) {
+    const Front& F = S.fronts[f];
+    const FrontDev& D = fe.fronts_h[f];
+    SolveItem it{};
+    it.goff = D.off;
+    it.front = f;
+    it.r0 = r0;
+    it.nr = r1 - r0;
+    it.blk = blk;
+    it.ld = D.ld;
+    it.np = F.npiv;
+    it.nf = F.nf;
+    it.start = D.start;
+    it.npb = npb[f];
+    it.ncbb = ncbb[f];
+    it.parent = F.parent;
+    it.rows_off = static_cast<int32_t>(D.rows_off);
+    it.cbvec_off = static_cast<int32_t>(D.cbvec_off);
+    it.ech_off = ech_off[f];
+    it.nech = static_cast<int32_t>(echl[f].size());
+    return it;
+  };
+  {
+    int nsm = 148, occ = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_sweep, kST, 0);
+    fe.solve_grid = std::max(1, nsm * std::max(1, occ));
+  }
+  // whole-front items only on levels wide enough to keep every CTA busy
+  std::vector<int> lvl_count;
+  for (const Front& F : S.fronts) {
+    if (F.level >= static_cast<int>(lvl_count.size())) lvl_count.resize(F.level + 1, 0);
+    ++lvl_count[F.level];
+  }
+  const int whole_min = std::getenv("RQB_WHOLE_MIN") ? std::atoi(std::getenv("RQB_WHOLE_MIN")) : 2 * fe.solve_grid;
+  std::vector<char> whole(nfr);
+  std::vector<int32_t> vnpb_f(nfr);
+  for (int f = 0; f < nfr; ++f) {
+    const Front& F = S.fronts[f];
+    whole[f] = npb[f] <= kWholeNpb && F.nf - F.npiv <= kWholeCb && lvl_count[F.level] >= whole_min;
+    vnpb_f[f] = whole[f] ? 0 : npb[f];
+    fbase_f[f] = static_cast<int32_t>(fwd.size());
+    if (whole[f]) {
+      fwd.push_back(item(f, 0, F.nf, kWhole));
+    } else {
+      for (int b = 0; b < npb[f]; ++b) fwd.push_back(item(f, b * kRB, std::min(F.npiv, (b + 1) * kRB), b));
+      for (int r = F.npiv; r < F.nf; r += kRB) fwd.push_back(item(f, r, std::min(F.nf, r + kRB), -1));
+    }
+    fcnt_f[f] = static_cast<int32_t>(fwd.size()) - fbase_f[f];
   }
   for (int f = nfr - 1; f >= 0; --f) {
     const Front& F = S.fronts[f];
-    for (int b = npb[f] - 1; b >= 0; --b) bwd.push_back({f, b * kRB, std::min(F.npiv, (b + 1) * kRB), b});
+    fbase_b[f] = static_cast<int32_t>(bwd.size());
+    if (whole[f] && npb[f] > 0) {
+      bwd.push_back(item(f, 0, F.npiv, kWhole));
+    } else {
+      for (int b = npb[f] - 1; b >= 0; --b) bwd.push_back(item(f, b * kRB, std::min(F.npiv, (b + 1) * kRB), b));
+    }
+    fcnt_b[f] = static_cast<int32_t>(bwd.size()) - fbase_b[f];
+  }
+  // dataflow state template: front deps (forward: children; backward: the
+  // nearest ancestor with pivots), initial ready queues = the items of the
+  // fronts ready at launch, in front order, counters zero
+  std::vector<int32_t> dfwd(nfr), dbwd(nfr);
+  std::vector<int32_t> qf(std::max<size_t>(1, fwd.size()), -1), qb(std::max<size_t>(1, bwd.size()), -1);
+  int nf0 = 0, nb0 = 0;
+  for (int f = 0; f < nfr; ++f) {
+    const Front& F = S.fronts[f];
+    dfwd[f] = static_cast<int32_t>(F.children.size());
+    int a = F.parent;
+    while (a >= 0 && S.fronts[a].npiv == 0) a = S.fronts[a].parent;
+    dbwd[f] = a >= 0 ? 1 : 0;
+  }
+  for (int f = 0; f < nfr; ++f) {
+    if (dfwd[f] == 0) {  // window: pivot blocks [0, kWin) (+ contribution items if npb < kWin)
+      const int n = vnpb_f[f] < kWin ? fcnt_f[f] : kWin;
+      for (int i = 0; i < n; ++i) qf[nf0++] = fbase_f[f] + i;
+    }
+    if (dbwd[f] == 0)
+      for (int i = 0; i < std::min(fcnt_b[f], kWin); ++i) qb[nb0++] = fbase_b[f] + i;
   }
   fe.n_fwd_items = static_cast<int>(fwd.size());
   fe.n_bwd_items = static_cast<int>(bwd.size());
-  if (fwd.empty()) fwd.push_back({0, 0, 0, -1});
-  if (bwd.empty()) bwd.push_back({0, 0, 0, -1});
+  if (fwd.empty()) fwd.push_back(SolveItem{});
+  if (bwd.empty()) bwd.push_back(SolveItem{});
+  if (ech.empty()) ech.push_back(0);
   fe.d_items_fwd.upload(fwd.data(), sizeof(SolveItem) * fwd.size(), fe.stream);
   fe.d_items_bwd.upload(bwd.data(), sizeof(SolveItem) * bwd.size(), fe.stream);
-  fe.d_nitems.upload(nitems.data(), sizeof(int32_t) * nfr, fe.stream);
-  fe.d_npb.upload(npb.data(), sizeof(int32_t) * nfr, fe.stream);
-  fe.d_parent.upload(parent.data(), sizeof(int32_t) * nfr, fe.stream);
-  fe.d_cnt.alloc(sizeof(int) * (3 * nfr + 8));
+  std::vector<int32_t> fmeta;  // fbase_f, fcnt_f, fbase_b, fcnt_b, forward window npb (0: whole front)
+  fmeta.insert(fmeta.end(), fbase_f.begin(), fbase_f.end());
+  fmeta.insert(fmeta.end(), fcnt_f.begin(), fcnt_f.end());
+  fmeta.insert(fmeta.end(), fbase_b.begin(), fbase_b.end());
+  fmeta.insert(fmeta.end(), fcnt_b.begin(), fcnt_b.end());
+  fmeta.insert(fmeta.end(), vnpb_f.begin(), vnpb_f.end());
+  fe.d_sf.upload(fmeta.data(), sizeof(int32_t) * fmeta.size(), fe.stream);
+  fe.d_ech.upload(ech.data(), sizeof(int32_t) * ech.size(), fe.stream);
+  fe.d_gsrc.alloc(sizeof(int4) * std::max<size_t>(1, S.rows.size()));
+  std::vector<int32_t> st;
+  fe.st_dep_fwd = 0;
+  st.insert(st.end(), dfwd.begin(), dfwd.end());
+  fe.st_dep_bwd = static_cast<int64_t>(st.size());
+  st.insert(st.end(), dbwd.begin(), dbwd.end());
+  fe.st_q_fwd = static_cast<int64_t>(st.size());
+  st.insert(st.end(), qf.begin(), qf.end());
+  fe.st_q_bwd = static_cast<int64_t>(st.size());
+  st.insert(st.end(), qb.begin(), qb.end());
+  fe.st_qctl = static_cast<int64_t>(st.size());
+  st.insert(st.end(), {0, nf0, 0, nb0});
+  fe.st_cnt = static_cast<int64_t>(st.size());  // fwd published, fwd finished, bwd published
+  st.resize(st.size() + 3 * static_cast<size_t>(nfr), 0);
+  fe.d_state0.upload(st.data(), sizeof(int32_t) * st.size(), fe.stream);
+  fe.d_state.alloc(fe.d_state0.bytes);
   fe.d_rowperm.alloc(sizeof(int32_t) * std::max<int64_t>(1, fe.n));
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_sweep, kST, 0);
-  fe.solve_grid = std::max(1, nsm * std::max(1, occ));
 }
 
 void rqb_rowperm_enqueue(FactorEngine& fe) {
   const int nfr = static_cast<int>(fe.fronts_h.size());
-  net_rowperm<<<(nfr + 127) / 128, 128, 0, fe.stream>>>(fe.d_fronts.as<FrontDev>(), nfr,
-                                                        fe.d_ipiv.as<int32_t>(), fe.d_rowperm.as<int32_t>());
+  net_rowperm<<<nfr, 128, 0, fe.stream>>>(fe.d_fronts.as<FrontDev>(), fe.d_ipiv.as<int32_t>(),
+                                          fe.d_perm.as<int32_t>(), fe.d_inv.as<int32_t>(),
+                                          fe.d_rowperm.as<int32_t>(), fe.d_gsrc.as<int4>());
 }
 
 void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scale, const double* vu,
                        double sigma, double* xl) {
   const int nfr = static_cast<int>(fe.fronts_h.size());
-  RQB_CUDA(cudaMemsetAsync(fe.d_cnt.p, 0, sizeof(int) * (3 * nfr + 8), fe.stream));
-  int* cnt = fe.d_cnt.as<int>();
-  int* tickets = cnt + 3 * nfr;
-  const int gf = std::min(fe.solve_grid, std::max(1, fe.n_fwd_items));
-  fwd_sweep<<<gf, kST, 0, fe.stream>>>(
-      fe.d_fronts.as<FrontDev>(), fe.d_items_fwd.as<SolveItem>(), fe.n_fwd_items, fe.d_nitems.as<int32_t>(),
-      fe.d_inv.as<int32_t>(), fe.d_pool.as<double>(), fe.d_rowperm.as<int32_t>(), fe.d_perm.as<int32_t>(), b,
-      fe.d_y.as<double>(), fe.d_cbvec.as<double>(), cnt, tickets);
-  const int gb = std::min(fe.solve_grid, std::max(1, fe.n_bwd_items));
-  bwd_sweep<<<gb, kST, 0, fe.stream>>>(
-      fe.d_fronts.as<FrontDev>(), fe.d_items_bwd.as<SolveItem>(), fe.n_bwd_items, fe.d_npb.as<int32_t>(),
-      fe.d_parent.as<int32_t>(), fe.d_rows.as<int32_t>(), fe.d_pool.as<double>(), fe.d_perm.as<int32_t>(),
-      fe.d_y.as<double>(), fe.d_xnew.as<double>(), x, scale, vu, sigma, xl, cnt, tickets);
+  cudaStream_t st = fe.stream;
+  RQB_CUDA(cudaMemcpyAsync(fe.d_state.p, fe.d_state0.p, fe.d_state0.bytes, cudaMemcpyDeviceToDevice, st));
+  int* sb = fe.d_state.as<int>();
+  SweepArgs A{};
+  unsigned long long* trace = nullptr;
+  {
+    static int traced = 0;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (std::getenv("RQB_SOLVE_TRACE") && cs == cudaStreamCaptureStatusNone && traced < 3) {
+      ++traced;
+      RQB_CUDA(cudaMalloc(&trace, sizeof(unsigned long long) * 8 * (size_t)(fe.n_fwd_items + fe.n_bwd_items)));
+    }
+  }
+  A.trace = trace;
+  A.ech = fe.d_ech.as<int32_t>();
+  A.gsrc = fe.d_gsrc.as<int4>();
+  A.pool = fe.d_pool.as<double>();
+  A.perm = fe.d_perm.as<int32_t>();
+  A.rows = fe.d_rows.as<int32_t>();
+  A.b = b;
+  A.y = fe.d_y.as<double>();
+  A.cbvec = fe.d_cbvec.as<double>();
+  A.xnew = fe.d_xnew.as<double>();
+  A.xout = x;
+  A.scale = scale;
+  A.vu = vu;
+  A.sigma = sigma;
+  A.xl_out = xl;
+  SweepArgs F = A;
+  F.items = fe.d_items_fwd.as<SolveItem>();
+  F.nitems = fe.n_fwd_items;
+  F.deps = sb + fe.st_dep_fwd;
+  F.queue = sb + fe.st_q_fwd;
+  F.qctl = sb + fe.st_qctl;
+  F.pub = sb + fe.st_cnt;
+  F.fin = sb + fe.st_cnt + nfr;
+  F.fwd = 1;
+  F.fbase = fe.d_sf.as<int32_t>();
+  F.fcnt = F.fbase + nfr;
+  F.npb = fe.d_sf.as<int32_t>() + 4 * nfr;
+  if (fe.n_fwd_items > 0)
+    fwd_sweep<<<std::min(fe.solve_grid, fe.n_fwd_items), kST, 0, st>>>(F);
+  SweepArgs B = A;
+  B.items = fe.d_items_bwd.as<SolveItem>();
+  B.nitems = fe.n_bwd_items;
+  B.deps = sb + fe.st_dep_bwd;
+  B.queue = sb + fe.st_q_bwd;
+  B.qctl = sb + fe.st_qctl + 2;
+  B.pub = sb + fe.st_cnt + 2 * nfr;
+  B.fin = nullptr;
+  B.fwd = 0;
+  B.trace = trace ? trace + 8 * (size_t)fe.n_fwd_items : nullptr;
+  B.fbase = fe.d_sf.as<int32_t>() + 2 * nfr;
+  B.fcnt = B.fbase + nfr;
+  B.npb = B.fcnt;
+  if (fe.n_bwd_items > 0)
+    bwd_sweep<<<std::min(fe.solve_grid, fe.n_bwd_items), kST, 0, st>>>(B);
   RQB_CUDA(cudaGetLastError());
   fe.launches_solve = 2;
+  if (trace) {  // development trace: dump forward and backward item timings once per call
+    cudaStreamSynchronize(st);
+    std::vector<unsigned long long> h(8 * (size_t)(fe.n_fwd_items + fe.n_bwd_items));
+    cudaMemcpy(h.data(), trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+    if (FILE* fp = std::fopen(std::getenv("RQB_SOLVE_TRACE"), "ab")) {
+      const int32_t hdr[2] = {fe.n_fwd_items, fe.n_bwd_items};
+      std::fwrite(hdr, sizeof(hdr), 1, fp);
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
+      std::fclose(fp);
+    }
+    cudaFree(trace);
+  }
 }
 
 void rqb_solve_set_attrs(int) {}

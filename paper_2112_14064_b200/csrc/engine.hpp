@@ -95,7 +95,12 @@ struct FactorEngine {
   DeviceBuffer d_y, d_xnew, d_cbvec, d_perm;  // solve workspaces (n, n, cbvec), perm[new] = old
   // sync-free solve: work items, per-front item counts, dependency counters,
   // net row permutation of each front's pivot block
-  DeviceBuffer d_items_fwd, d_items_bwd, d_nitems, d_npb, d_parent, d_cnt, d_rowperm;
+  DeviceBuffer d_items_fwd, d_items_bwd, d_rowperm, d_sf, d_ech, d_gsrc;
+  // dataflow state of the two sweeps in one int32 buffer (template + live
+  // copy, reset by one D2D copy per solve): front deps fwd/bwd, ready queues
+  // fwd/bwd, {head, tail} x2, per-front published/finished counters
+  DeviceBuffer d_state0, d_state;
+  int64_t st_dep_fwd = 0, st_dep_bwd = 0, st_q_fwd = 0, st_q_bwd = 0, st_qctl = 0, st_cnt = 0;
   int n_fwd_items = 0, n_bwd_items = 0, solve_grid = 148;
   std::vector<FrontDev> fronts_h;
   std::vector<LevelPlan> plans;
