@@ -47,93 +47,255 @@ void rot_cols(CMat& T, int j, int r0, int r1, double c, cplx s) {
 
 }  // namespace
 
-bool complex_schur(const std::vector<double>& A, int n, CMat& T, CMat& Z) {
-  T = CMat(n);
-  Z = CMat(n);
-  for (int j = 0; j < n; ++j)
-    for (int i = 0; i < n; ++i) T(i, j) = A[i + static_cast<size_t>(j) * n];
-  for (int i = 0; i < n; ++i) Z(i, i) = 1.0;
-  // Householder reduction to upper Hessenberg form.
-  std::vector<cplx> v(n);
+namespace {
+
+// Householder reduction of the real n x n matrix H (column-major) to upper
+// Hessenberg form, H <- Q^T H Q, Zr <- Zr Q. Columns whose entries below the
+// subdiagonal are already zero (the Arnoldi part of a Krylov-Schur matrix)
+// are skipped; reflectors stop at the column's last nonzero row.
+void hessenberg_real(std::vector<double>& Hv, std::vector<double>& Zv, int n) {
+  auto H = [&](int i, int j) -> double& { return Hv[i + static_cast<size_t>(j) * n]; };
+  std::vector<double> v(n), w(n);
   for (int k = 0; k + 2 < n; ++k) {
+    int e = n - 1;
+    while (e > k + 1 && H(e, k) == 0.0) --e;
+    if (e == k + 1) continue;
     double alpha2 = 0.0;
-    for (int i = k + 1; i < n; ++i) alpha2 += std::norm(T(i, k));
-    const double alpha = std::sqrt(alpha2);
-    if (alpha == 0.0) continue;
-    const cplx x0 = T(k + 1, k);
-    const cplx ph = std::abs(x0) > 0 ? x0 / std::abs(x0) : cplx(1.0);
-    for (int i = k + 1; i < n; ++i) v[i] = T(i, k);
-    v[k + 1] += ph * alpha;
-    double vn = 0.0;
-    for (int i = k + 1; i < n; ++i) vn += std::norm(v[i]);
-    if (vn == 0.0) continue;
-    // T = (I - 2 v v^H / vn) T (I - 2 v v^H / vn)
-    for (int j = 0; j < n; ++j) {
-      cplx s = 0.0;
-      for (int i = k + 1; i < n; ++i) s += std::conj(v[i]) * T(i, j);
-      s *= 2.0 / vn;
-      for (int i = k + 1; i < n; ++i) T(i, j) -= v[i] * s;
+    for (int i = k + 1; i <= e; ++i) alpha2 += H(i, k) * H(i, k);
+    const double x0 = H(k + 1, k);
+    const double beta = -std::copysign(std::sqrt(alpha2), x0);
+    v[k + 1] = x0 - beta;
+    double vtv = v[k + 1] * v[k + 1];
+    for (int i = k + 2; i <= e; ++i) v[i] = H(i, k), vtv += v[i] * v[i];
+    const double tau = 2.0 / vtv;
+    // left: rows k+1..e of columns k+1..n-1; column k becomes beta e_1
+    H(k + 1, k) = beta;
+    for (int i = k + 2; i <= e; ++i) H(i, k) = 0.0;
+    for (int j = k + 1; j < n; ++j) {
+      double* col = &H(0, j);
+      double sdot = 0.0;
+      for (int i = k + 1; i <= e; ++i) sdot += v[i] * col[i];
+      sdot *= tau;
+      for (int i = k + 1; i <= e; ++i) col[i] -= sdot * v[i];
     }
-    for (int i = 0; i < n; ++i) {
-      cplx s = 0.0;
-      for (int j = k + 1; j < n; ++j) s += T(i, j) * v[j];
-      s *= 2.0 / vn;
-      for (int j = k + 1; j < n; ++j) T(i, j) -= s * std::conj(v[j]);
+    // right: columns k+1..e of H (all rows) and of Zr
+    for (double* M : {Hv.data(), Zv.data()}) {
+      std::fill(w.begin(), w.end(), 0.0);
+      for (int j = k + 1; j <= e; ++j) {
+        const double* col = M + static_cast<size_t>(j) * n;
+        const double vj = v[j];
+        for (int i = 0; i < n; ++i) w[i] += col[i] * vj;
+      }
+      for (int j = k + 1; j <= e; ++j) {
+        double* col = M + static_cast<size_t>(j) * n;
+        const double f = tau * v[j];
+        for (int i = 0; i < n; ++i) col[i] -= f * w[i];
+      }
     }
-    for (int i = 0; i < n; ++i) {
-      cplx s = 0.0;
-      for (int j = k + 1; j < n; ++j) s += Z(i, j) * v[j];
-      s *= 2.0 / vn;
-      for (int j = k + 1; j < n; ++j) Z(i, j) -= s * std::conj(v[j]);
-    }
-    for (int i = k + 2; i < n; ++i) T(i, k) = 0.0;
   }
-  // Single-shift complex QR.
+}
+
+// Francis double-shift QR of the real upper Hessenberg H to quasi-triangular
+// (real Schur) form, accumulating Zr; real eigenvalue pairs are split by a
+// rotation, complex pairs stay 2 x 2 blocks. Returns false if more than 30 n
+// iterations were needed.
+bool francis_real(std::vector<double>& Hv, std::vector<double>& Zv, int n) {
+  auto H = [&](int i, int j) -> double& { return Hv[i + static_cast<size_t>(j) * n]; };
   const double eps = std::numeric_limits<double>::epsilon();
-  int ihi = n - 1, iter = 0, total = 0;
-  while (ihi > 0) {
-    int l = ihi;
+  double anorm = 0.0;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i <= std::min(j + 1, n - 1); ++i) anorm += std::fabs(H(i, j));
+  if (anorm == 0.0) anorm = 1.0;
+  // rotation [c -s; s c] on rows/columns (k, k+1) that zeroes H(k+1, k) of a
+  // 2 x 2 block with real eigenvalues
+  auto split_real_pair = [&](int k) {
+    const double p = 0.5 * (H(k, k) - H(k + 1, k + 1));
+    const double q = p * p + H(k + 1, k) * H(k, k + 1);
+    if (q < 0.0) return;  // complex pair: stays a 2 x 2 block
+    const double zz = p + std::copysign(std::sqrt(q), p);
+    const double x = H(k + 1, k);
+    const double sc = std::fabs(x) + std::fabs(zz);
+    if (sc == 0.0) return;
+    double pp = x / sc, qq = zz / sc;
+    const double r = std::sqrt(pp * pp + qq * qq);
+    pp /= r;
+    qq /= r;
+    for (int j = k; j < n; ++j) {
+      const double t = H(k, j);
+      H(k, j) = qq * t + pp * H(k + 1, j);
+      H(k + 1, j) = qq * H(k + 1, j) - pp * t;
+    }
+    for (double* M : {Hv.data(), Zv.data()}) {
+      const int rows = M == Hv.data() ? k + 2 : n;
+      double* c0 = M + static_cast<size_t>(k) * n;
+      double* c1 = c0 + n;
+      for (int i = 0; i < rows; ++i) {
+        const double t = c0[i];
+        c0[i] = qq * t + pp * c1[i];
+        c1[i] = qq * c1[i] - pp * t;
+      }
+    }
+    H(k + 1, k) = 0.0;
+  };
+  int nn = n - 1, its = 0, total = 0;
+  while (nn >= 0) {
+    int l = nn;
     for (; l > 0; --l) {
-      const double s = std::abs(T(l - 1, l - 1)) + std::abs(T(l, l));
-      if (std::abs(T(l, l - 1)) <= eps * (s > 0 ? s : 1.0)) {
-        T(l, l - 1) = 0.0;
+      double s = std::fabs(H(l - 1, l - 1)) + std::fabs(H(l, l));
+      if (s == 0.0) s = anorm;
+      if (std::fabs(H(l, l - 1)) <= eps * s) {
+        H(l, l - 1) = 0.0;
         break;
       }
     }
-    if (l == ihi) {
-      --ihi;
-      iter = 0;
+    if (l == nn) {  // one eigenvalue
+      --nn;
+      its = 0;
+      continue;
+    }
+    if (l == nn - 1) {  // a 2 x 2 block
+      split_real_pair(nn - 1);
+      nn -= 2;
+      its = 0;
       continue;
     }
     if (++total > 30 * n) return false;
-    ++iter;
-    cplx mu;
-    if (iter % 11 == 10) {
-      mu = T(ihi, ihi) + 0.75 * std::abs(T(ihi, ihi - 1));  // exceptional shift
-    } else {
-      const cplx a = T(ihi - 1, ihi - 1), b = T(ihi - 1, ihi), c = T(ihi, ihi - 1), d = T(ihi, ihi);
-      const cplx half = 0.5 * (a - d);
-      const cplx disc = std::sqrt(half * half + b * c);
-      const cplx m1 = 0.5 * (a + d) + disc, m2 = 0.5 * (a + d) - disc;
-      mu = std::abs(m1 - d) < std::abs(m2 - d) ? m1 : m2;
+    ++its;
+    // shifts: eigenvalues of the trailing 2 x 2 (trace x + y, x y - w); an
+    // exceptional shift every 10 iterations without deflation
+    double x = H(nn, nn), y = H(nn - 1, nn - 1), w = H(nn, nn - 1) * H(nn - 1, nn);
+    if (its % 10 == 0) {
+      const double s = std::fabs(H(nn, nn - 1)) + std::fabs(H(nn - 1, nn - 2));
+      x = y = H(nn, nn) + 0.75 * s;
+      w = -0.4375 * s * s;
     }
-    cplx x = T(l, l) - mu, y = T(l + 1, l);
-    for (int k = l; k < ihi; ++k) {
-      if (k > l) {
-        x = T(k, k - 1);
-        y = T(k + 1, k - 1);
+    // first column of (H - s1)(H - s2), started at the lowest row m where two
+    // consecutive small subdiagonals allow it
+    int m = nn - 2;
+    double p = 0, q = 0, r = 0;
+    for (; m >= l; --m) {
+      const double z = H(m, m);
+      const double rr = x - z, ss = y - z;
+      p = (rr * ss - w) / H(m + 1, m) + H(m, m + 1);
+      q = H(m + 1, m + 1) - z - rr - ss;
+      r = H(m + 2, m + 1);
+      const double sc = std::fabs(p) + std::fabs(q) + std::fabs(r);
+      p /= sc;
+      q /= sc;
+      r /= sc;
+      if (m == l) break;
+      const double u = std::fabs(H(m, m - 1)) * (std::fabs(q) + std::fabs(r));
+      const double v = std::fabs(p) * (std::fabs(H(m - 1, m - 1)) + std::fabs(z) + std::fabs(H(m + 1, m + 1)));
+      if (u <= eps * v) break;
+    }
+    for (int i = m + 2; i <= nn; ++i) {
+      H(i, i - 2) = 0.0;
+      if (i != m + 2) H(i, i - 3) = 0.0;
+    }
+    // bulge chase with 3-element reflectors (2-element at the bottom)
+    for (int k = m; k <= nn - 1; ++k) {
+      const bool three = k != nn - 1;
+      double sc = 1.0;
+      if (k != m) {
+        p = H(k, k - 1);
+        q = H(k + 1, k - 1);
+        r = three ? H(k + 2, k - 1) : 0.0;
+        sc = std::fabs(p) + std::fabs(q) + std::fabs(r);
+        if (sc == 0.0) continue;
+        p /= sc;
+        q /= sc;
+        r /= sc;
       }
-      double c;
-      cplx s;
-      givens(x, y, c, s);
-      rot_rows(T, k, k > l ? k - 1 : k, n, c, s);
-      if (k > l) T(k + 1, k - 1) = 0.0;
-      rot_cols(T, k, 0, std::min(k + 3, ihi + 1), c, s);
-      rot_cols(Z, k, 0, n, c, s);
+      const double s = std::copysign(std::sqrt(p * p + q * q + r * r), p);
+      if (s == 0.0) continue;
+      if (k == m) {
+        if (l != m) H(k, k - 1) = -H(k, k - 1);
+      } else {
+        H(k, k - 1) = -s * sc;
+        H(k + 1, k - 1) = 0.0;
+        if (three) H(k + 2, k - 1) = 0.0;
+      }
+      p += s;
+      const double vx = p / s, vy = q / s, vz = r / s;
+      q /= p;
+      r /= p;
+      for (int j = k; j < n; ++j) {
+        double* col = &H(0, j);
+        double t = col[k] + q * col[k + 1];
+        if (three) {
+          t += r * col[k + 2];
+          col[k + 2] -= t * vz;
+        }
+        col[k + 1] -= t * vy;
+        col[k] -= t * vx;
+      }
+      for (double* M : {Hv.data(), Zv.data()}) {
+        const int rows = M == Hv.data() ? std::min(nn, k + 3) + 1 : n;
+        double* c0 = M + static_cast<size_t>(k) * n;
+        double* c1 = c0 + n;
+        double* c2 = c1 + n;
+        if (three) {
+          for (int i = 0; i < rows; ++i) {
+            const double t = vx * c0[i] + vy * c1[i] + vz * c2[i];
+            c2[i] -= t * r;
+            c1[i] -= t * q;
+            c0[i] -= t;
+          }
+        } else {
+          for (int i = 0; i < rows; ++i) {
+            const double t = vx * c0[i] + vy * c1[i];
+            c1[i] -= t * q;
+            c0[i] -= t;
+          }
+        }
+      }
     }
   }
   for (int j = 0; j < n; ++j)
-    for (int i = j + 1; i < n; ++i) T(i, j) = 0.0;
+    for (int i = j + 2; i < n; ++i) H(i, j) = 0.0;
+  return true;
+}
+
+}  // namespace
+
+// Real Hessenberg reduction + Francis double-shift QR (real arithmetic), then
+// each remaining 2 x 2 block (a complex-conjugate pair) is triangularised by
+// one complex rotation: A = Z T Z^H with T upper triangular.
+bool complex_schur(const std::vector<double>& A, int n, CMat& T, CMat& Z) {
+  std::vector<double> H(A.begin(), A.begin() + static_cast<size_t>(n) * n), Zr(static_cast<size_t>(n) * n, 0.0);
+  for (int i = 0; i < n; ++i) Zr[i + static_cast<size_t>(i) * n] = 1.0;
+  hessenberg_real(H, Zr, n);
+  if (!francis_real(H, Zr, n)) return false;
+  T = CMat(n);
+  Z = CMat(n);
+  for (size_t i = 0; i < H.size(); ++i) {
+    T.a[i] = H[i];
+    Z.a[i] = Zr[i];
+  }
+  for (int k = 0; k + 1 < n; ++k) {
+    if (T(k + 1, k) == 0.0) continue;
+    const cplx a = T(k, k), b = T(k, k + 1), c = T(k + 1, k), d = T(k + 1, k + 1);
+    const cplx p = 0.5 * (a - d);
+    const cplx mu_d = p + std::sqrt(p * p + b * c);  // mu - d for one eigenvalue mu of the block
+    const double r = std::hypot(std::abs(mu_d), std::abs(c));
+    const cplx cs = mu_d / r, sn = c / r;  // G = [conj(cs) sn; -sn cs] (sn real)
+    for (int j = k; j < n; ++j) {
+      const cplx x = T(k, j), y = T(k + 1, j);
+      T(k, j) = std::conj(cs) * x + sn * y;
+      T(k + 1, j) = -sn * x + cs * y;
+    }
+    auto right = [&](CMat& M, int rows) {  // M[:, k:k+2] *= G^H
+      for (int i = 0; i < rows; ++i) {
+        const cplx x = M(i, k), y = M(i, k + 1);
+        M(i, k) = cs * x + std::conj(sn) * y;
+        M(i, k + 1) = -sn * x + std::conj(cs) * y;
+      }
+    };
+    right(T, k + 2);
+    right(Z, n);
+    T(k + 1, k) = 0.0;
+    ++k;
+  }
   return true;
 }
 

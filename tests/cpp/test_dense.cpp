@@ -14,9 +14,40 @@ int main() {
   std::mt19937_64 g(1);
   std::normal_distribution<double> N;
   int fails = 0;
-  for (int n : {2, 5, 21, 41, 80}) {
+  const std::pair<int, bool> cases[] = {{2, false}, {5, false}, {21, false}, {41, false}, {80, false},
+                                         {40, true}, {41, true}};
+  for (const auto& cs : cases) {
+    const int n = cs.first;
     std::vector<double> A(n * n);
     for (auto& x : A) x = N(g);
+    if (cs.second) {
+      // degenerate cluster: Q blockdiag([a b; -b a] x k (+ one real)) Q^T
+      // with a random orthogonal Q (repeated complex pair, as in the QEP)
+      std::vector<double> D(n * n, 0.0), Q(n * n);
+      for (int i = 0; i + 1 < n; i += 2) {
+        D[i + i * n] = D[(i + 1) + (i + 1) * n] = -0.03;
+        D[i + (i + 1) * n] = 0.9995;
+        D[(i + 1) + i * n] = -0.9995;
+      }
+      if (n % 2) D[(n - 1) * (n + 1)] = 0.5;
+      for (auto& x : Q) x = N(g);
+      for (int j = 0; j < n; ++j) {  // MGS -> orthogonal
+        for (int t = 0; t < j; ++t) {
+          double d = 0;
+          for (int i = 0; i < n; ++i) d += Q[i + t * n] * Q[i + j * n];
+          for (int i = 0; i < n; ++i) Q[i + j * n] -= d * Q[i + t * n];
+        }
+        double nr = 0;
+        for (int i = 0; i < n; ++i) nr += Q[i + j * n] * Q[i + j * n];
+        for (int i = 0; i < n; ++i) Q[i + j * n] /= std::sqrt(nr);
+      }
+      std::vector<double> QD(n * n, 0.0);
+      for (int j = 0; j < n; ++j) for (int t = 0; t < n; ++t) for (int i = 0; i < n; ++i)
+        QD[i + j * n] += Q[i + t * n] * D[t + j * n];
+      std::fill(A.begin(), A.end(), 0.0);
+      for (int j = 0; j < n; ++j) for (int t = 0; t < n; ++t) for (int i = 0; i < n; ++i)
+        A[i + j * n] += QD[i + t * n] * Q[j + t * n];
+    }
     CMat T, Z;
     if (!complex_schur(A, n, T, Z)) { std::printf("qr fail n=%d\n", n); return 1; }
     auto defect = [&](const CMat& T, const CMat& Z) {
@@ -71,7 +102,7 @@ int main() {
       inv = std::max(inv, std::fabs(s));
     }
     const bool ok = d0 < 1e-12 * n && d1 < 1e-12 * n && lead && rank == p && inv < 1e-11 * n;
-    std::printf("n=%d p=%d schur=%.2e reorder=%.2e rank=%d invariance=%.2e %s\n", n, p, d0, d1, rank,
+    std::printf("n=%d%s p=%d schur=%.2e reorder=%.2e rank=%d invariance=%.2e %s\n", n, cs.second ? " (degenerate)" : "", p, d0, d1, rank,
                 inv, ok ? "ok" : "FAIL");
     fails += !ok;
   }

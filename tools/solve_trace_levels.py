@@ -33,3 +33,11 @@ if len(sys.argv) > 4:
         print(name, "items of level", L, "(t0 t1 t2 t3 waited, us)")
         for i in idx:
             print(f"   item {i:6d} front {fr[i]:5d} {T[i,0]/1e3:8.2f} {T[i,1]/1e3:8.2f} {T[i,2]/1e3:8.2f} {T[i,3]/1e3:8.2f} w {T[i,5]/1e3:6.2f} detect {T[i,4]/1e3:8.2f} streamed {T[i,6]/1e3:8.2f} tri {T[i,7]/1e3:8.2f}")
+if len(sys.argv) > 5:
+    L = int(sys.argv[5])
+    for name, T, fr in (("fwd", t[:nf_], ffront), ("bwd", t[nf_:], bfront)):
+        m = level[fr] == L
+        T = T[m].astype(float)
+        ph = {"t0-t1 (pop..prologue)": T[:,1]-T[:,0], "t1-t6 (stream)": T[:,6]-T[:,1], "t6-t7 (tri)": T[:,7]-T[:,6],
+              "t7-t2 (rest)": T[:,2]-T[:,7], "t2-t3 (publish)": T[:,3]-T[:,2]}
+        print(name, "level", L, " ".join(f"{k}: {np.median(v)/1e3:.2f}" for k, v in ph.items()), "us (median)")
