@@ -195,7 +195,9 @@ rq_factor_t* rq_operator_factor(rq_operator_t* op); /* borrowed */
 /* Device time per call (CUDA events, device-resident buffers, after warm-up):
  * what = 0 apply_operator, 1 solve_factored, 2 fused C/M SpMV, 3 CGS GEMV-T
  * over `param` basis vectors, 4 GEMV-N over `param` vectors, 5 numeric
- * factorization (graph replay), 6 M SpMV. */
+ * factorization (graph replay), 6 M SpMV, 7 restart DGEMM (2n x param) x
+ * (param x param), 8 batched pencil residual of `param` candidates.
+ * what | 0x100: scrub L2 (256 MiB) before every call. */
 int rq_operator_time(rq_operator_t* op, int what, int iters, int param, double* ms_per_call);
 void rq_operator_destroy(rq_operator_t* op);
 

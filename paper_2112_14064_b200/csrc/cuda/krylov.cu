@@ -10,10 +10,14 @@
 //                   partials + fixed-order final reduction (deterministic)
 //   gemv_n          r -= V h (kern::axpy, kernels.cpp:19-21, fused)
 //   normalize       B-norm and v = r / ||r||_B (kern::nrm2sq/scal fused)
-//   combine         V Q (Krylov-Schur restart / Ritz vectors)
-//   residual_part   ||Q(lambda) u||^2 and ||u||^2 for complex (lambda, u)
+//   combine         V Q (Krylov-Schur restart / Ritz vectors): cuBLAS DGEMM
+//   ritz_residual   ||Q(lambda_c) x_c||^2, ||x_c||^2 for a batch of Ritz vectors
+//                   (row-major, from one DGEMM): SpMM over K, C, M
 #include <cmath>
 #include <cstring>
+#include <vector>
+
+#include <cublas_v2.h>
 
 #include "device.cuh"
 
@@ -71,36 +75,50 @@ __global__ void spmv_op_k(int64_t n, const int64_t* __restrict__ rowptr,
 }
 
 // part[b * k + i] = sum over block b's slice of V[i] . w  (w given as two halves)
+// part[b*k + i] = V[i][chunk b] . w[chunk b]: the block stages its chunk of
+// w in shared memory once; each warp then owns basis vectors i = warp (mod 8),
+// two at a time, streaming their contiguous chunk segments (8 independent
+// loads in flight per lane and row) and reducing with shuffles only.
 __global__ void __launch_bounds__(kRedThreads) gemv_t_part(const double* __restrict__ V, int k,
                                                          int64_t n2, const double* __restrict__ wu,
                                                          const double* __restrict__ wl, int64_t n,
-                                                         double* __restrict__ part) {
-  __shared__ double sh[8][kRedThreads / 32];
-  const int64_t chunk = (n2 + gridDim.x - 1) / gridDim.x;
-  const int64_t e0 = blockIdx.x * chunk, e1 = min(n2, e0 + chunk);
+                                                         int64_t chunk, double* __restrict__ part) {
+  extern __shared__ double xs[];
+  const int64_t e0 = blockIdx.x * chunk;
+  const int len = static_cast<int>(min(chunk, n2 - e0));
+  for (int t = threadIdx.x; t < len; t += kRedThreads) {
+    const int64_t e = e0 + t;
+    xs[t] = e < n ? wu[e] : wl[e - n];
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i0 = 0; i0 < k; i0 += 8) {
-    double acc[8];
+  constexpr int kW = kRedThreads / 32;
+  for (int i = warp; i < k; i += 2 * kW) {
+    const bool two = i + kW < k;
+    const double* va = V + (int64_t)i * n2 + e0;
+    const double* vb = V + (int64_t)(two ? i + kW : i) * n2 + e0;
+    double sa0 = 0.0, sa1 = 0.0, sb0 = 0.0, sb1 = 0.0;
+    int t = lane;
+    for (; t + 32 * 3 < len; t += 32 * 4) {
+      double a[4], bb[4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    for (int64_t e = e0 + threadIdx.x; e < e1; e += kRedThreads) {
-      const double x = e < n ? wu[e] : wl[e - n];
+      for (int u = 0; u < 4; ++u) a[u] = va[t + 32 * u];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (i0 + q < k) acc[q] += V[(int64_t)(i0 + q) * n2 + e] * x;
+      for (int u = 0; u < 4; ++u) bb[u] = vb[t + 32 * u];
+      sa0 += a[0] * xs[t] + a[2] * xs[t + 64];
+      sa1 += a[1] * xs[t + 32] + a[3] * xs[t + 96];
+      sb0 += bb[0] * xs[t] + bb[2] * xs[t + 64];
+      sb1 += bb[1] * xs[t + 32] + bb[3] * xs[t + 96];
     }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const double v = warp_sum(acc[q]);
-      if (lane == 0) sh[q][warp] = v;
+    for (; t < len; t += 32) {
+      sa0 += va[t] * xs[t];
+      sb0 += vb[t] * xs[t];
     }
-    __syncthreads();
-    if (threadIdx.x < 8 && i0 + threadIdx.x < k) {
-      double s = 0.0;
-      for (int wq = 0; wq < kRedThreads / 32; ++wq) s += sh[threadIdx.x][wq];
-      part[(int64_t)blockIdx.x * k + i0 + threadIdx.x] = s;
+    const double sa = warp_sum(sa0 + sa1), sb = warp_sum(sb0 + sb1);
+    if (lane == 0) {
+      part[(int64_t)blockIdx.x * k + i] = sa;
+      if (two) part[(int64_t)blockIdx.x * k + i + kW] = sb;
     }
-    __syncthreads();
   }
 }
 
@@ -179,85 +197,118 @@ __global__ void sum_parts(const double* __restrict__ part, int nb, double* __res
 }
 
 // Vout[c][e] = sum_i V[i][e] Q[i + c*ldq], c in [c0, c0+8)
-__global__ void combine_k(const double* __restrict__ V, int k, int64_t n2,
-                          const double* __restrict__ Q, int ldq, int ncols,
-                          double* __restrict__ Vout) {
-  extern __shared__ double qs[];  // k x 8
-  const int c0 = blockIdx.y * 8;
-  for (int idx = threadIdx.x; idx < k * 8; idx += blockDim.x) {
-    const int i = idx % k, c = idx / k;
-    qs[i + c * k] = c0 + c < ncols ? Q[i + (int64_t)(c0 + c) * ldq] : 0.0;
-  }
-  __syncthreads();
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    double acc[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-    for (int i = 0; i < k; ++i) {
-      const double v = V[(int64_t)i * n2 + e];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc[c] += v * qs[i + c * k];
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (c0 + c < ncols) Vout[(int64_t)(c0 + c) * n2 + e] = acc[c];
-  }
-}
 
 // per-row complex pencil residual of (lambda, u = ur + i ui); parts of
 // ||Q(lambda)u||^2 (out[b]) and ||u||^2 (out[nb + b])
-__global__ void __launch_bounds__(kRedThreads) residual_part(
+
+
+// Pencil residuals of a batch of Ritz vectors held ROW-major (X[e * ldx + 2c]
+// = Re x_c[e], X[e * ldx + 2c + 1] = Im x_c[e], e < 2n): an SpMM over the
+// shared pattern of K, C, M. Lane l owns candidates c0 + l and c0 + 32 + l of
+// the block's 64; the warp loads 32 nonzeros (col, K, C, M) coalesced and
+// broadcasts them, each candidate gathering one 16-byte {re, im} pair per
+// nonzero (the 64 candidates of a nonzero are one contiguous 1 KiB row).
+// part[(2c + {0,1}) * gridDim.x + block] = partial {||Q(lambda_c) u_c||^2, ||u_c||^2}.
+__global__ void __launch_bounds__(kRedThreads) ritz_residual_k(
     int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     const double* __restrict__ K, const double* __restrict__ C, const double* __restrict__ M,
-    const double* __restrict__ ur, const double* __restrict__ ui, double lr, double li,
-    double* __restrict__ part) {
-  __shared__ double sh[kRedThreads / 32];
-  const int lane = threadIdx.x & 31;
-  const int wpb = kRedThreads / 32;
-  const double sr = lr * lr - li * li, si = 2.0 * lr * li;
-  double acc = 0.0, accu = 0.0;
-  for (int64_t row = blockIdx.x * (int64_t)wpb + (threadIdx.x >> 5); row < n;
-       row += (int64_t)gridDim.x * wpb) {
-    double a = 0, b = 0, c = 0, d = 0, e = 0, f = 0;
-    for (int64_t k = rowptr[row] + lane; k < rowptr[row + 1]; k += 32) {
-      const int j = col[k];
-      const double xr = ur[j], xi = ui[j];
-      a += K[k] * xr;
-      b += K[k] * xi;
-      c += C[k] * xr;
-      d += C[k] * xi;
-      e += M[k] * xr;
-      f += M[k] * xi;
+    const double* __restrict__ X, int ldx, int nc, const double* __restrict__ lam,
+    const int* __restrict__ blk, double* __restrict__ part) {
+  constexpr int kW = kRedThreads / 32;
+  __shared__ double sred[kW][4][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double lr[2], li[2], sr[2], si[2], acc[2] = {0.0, 0.0}, accu[2] = {0.0, 0.0};
+  const double* xb[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = min(nc - 1, (int)blockIdx.y * 64 + 32 * h + lane);
+    lr[h] = lam[2 * c];
+    li[h] = lam[2 * c + 1];
+    sr[h] = lr[h] * lr[h] - li[h] * li[h];
+    si[h] = 2.0 * lr[h] * li[h];
+    xb[h] = X + (int64_t)blk[c] * n * ldx + 2 * c;
+  }
+  for (int64_t row = blockIdx.x * (int64_t)kW + warp; row < n; row += (int64_t)gridDim.x * kW) {
+    double a[2][6];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int t = 0; t < 6; ++t) a[h][t] = 0.0;
+    const int64_t k0 = rowptr[row], k1 = rowptr[row + 1];
+    for (int64_t kb = k0; kb < k1; kb += 32) {
+      const int cnt = static_cast<int>(k1 - kb < 32 ? k1 - kb : 32);
+      int jl = 0;
+      double kl = 0.0, cl = 0.0, ml = 0.0;
+      if (lane < cnt) {
+        jl = col[kb + lane];
+        kl = K[kb + lane];
+        cl = C[kb + lane];
+        ml = M[kb + lane];
+      }
+#pragma unroll 4
+      for (int t = 0; t < cnt; ++t) {
+        const int64_t j = __shfl_sync(0xffffffffu, jl, t);
+        const double kv = __shfl_sync(0xffffffffu, kl, t);
+        const double cv = __shfl_sync(0xffffffffu, cl, t);
+        const double mv = __shfl_sync(0xffffffffu, ml, t);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 x = *reinterpret_cast<const double2*>(xb[h] + j * ldx);
+          a[h][0] += kv * x.x;
+          a[h][1] += kv * x.y;
+          a[h][2] += cv * x.x;
+          a[h][3] += cv * x.y;
+          a[h][4] += mv * x.x;
+          a[h][5] += mv * x.y;
+        }
+      }
     }
-    a = warp_sum(a);
-    b = warp_sum(b);
-    c = warp_sum(c);
-    d = warp_sum(d);
-    e = warp_sum(e);
-    f = warp_sum(f);
-    if (lane == 0) {
-      const double re = a + (lr * c - li * d) + (sr * e - si * f);
-      const double im = b + (lr * d + li * c) + (sr * f + si * e);
-      acc += re * re + im * im;
-      accu += ur[row] * ur[row] + ui[row] * ui[row];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double re = a[h][0] + (lr[h] * a[h][2] - li[h] * a[h][3]) + (sr[h] * a[h][4] - si[h] * a[h][5]);
+      const double im = a[h][1] + (lr[h] * a[h][3] + li[h] * a[h][2]) + (sr[h] * a[h][5] + si[h] * a[h][4]);
+      const double2 u = *reinterpret_cast<const double2*>(xb[h] + row * ldx);
+      acc[h] += re * re + im * im;
+      accu[h] += u.x * u.x + u.y * u.y;
     }
   }
-  const double s = block_sum(acc, sh);
-  const double su = block_sum(accu, sh);
-  if (threadIdx.x == 0) {
-    part[blockIdx.x] = s;
-    part[gridDim.x + blockIdx.x] = su;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    sred[warp][2 * h][lane] = acc[h];
+    sred[warp][2 * h + 1][lane] = accu[h];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = (int)blockIdx.y * 64 + 32 * h + lane;
+      double s0 = 0.0, s1 = 0.0;
+      for (int w = 0; w < kW; ++w) s0 += sred[w][2 * h][lane], s1 += sred[w][2 * h + 1][lane];
+      if (c < nc) {
+        part[(int64_t)(2 * c) * gridDim.x + blockIdx.x] = s0;
+        part[(int64_t)(2 * c + 1) * gridDim.x + blockIdx.x] = s1;
+      }
+    }
   }
 }
 
-__global__ void residual_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
-  double s = 0.0, su = 0.0;
-  for (int b = threadIdx.x; b < nb; b += 32) s += part[b], su += part[nb + b];
-  s = warp_sum(s);
-  su = warp_sum(su);
-  if (threadIdx.x == 0) out[0] = s, out[1] = su;
+// out[j] = X[(blk_c n + j) * ldx + 2c + part] (one Ritz vector of a row-major
+// batch back to a contiguous vector; part 0 real, 1 imaginary)
+__global__ void ritz_extract_k(const double* __restrict__ X, int ldx, int64_t n, const int* __restrict__ blk,
+                               int c, int part_im, double* __restrict__ out) {
+  const double* src = X + (int64_t)blk[c] * n * ldx + 2 * c + part_im;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = src[j * ldx];
 }
+
+// out[i] = sum_b part[i * nb + b], one warp per output (fixed order)
+__global__ void sum_rows(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 32) s += part[(int64_t)blockIdx.x * nb + b];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
 
 // ---------------------------------------------------------------------------
 OperatorEngine::OperatorEngine(int64_t n_, const int64_t* rowptr, const int32_t* col,
@@ -293,13 +344,24 @@ OperatorEngine::OperatorEngine(int64_t n_, const int64_t* rowptr, const int32_t*
   d_w.alloc(sizeof(double) * 2 * n);
   d_t.alloc(sizeof(double) * 2 * n);
   nparts = kRedBlocks;
-  d_part.alloc(sizeof(double) * kRedBlocks * 512);
+  // CGS projection: chunks of 256..4096 entries, about 4 blocks per SM when n is large
+  gemv_t_chunk = std::min<int64_t>(4096, std::max<int64_t>(256, ((2 * n + kRedBlocks - 1) / kRedBlocks + 255) / 256 * 256));
+  gemv_t_blocks = static_cast<int>((2 * n + gemv_t_chunk - 1) / gemv_t_chunk);
+  d_part.alloc(sizeof(double) * std::max(kRedBlocks, gemv_t_blocks) * 512);
   d_scal.alloc(sizeof(double) * 64);
+  {
+    cublasHandle_t h = nullptr;
+    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(errc::config, "cublasCreate failed");
+    blas = h;
+    cublasSetStream(h, stream);
+  }
   RQB_CUDA(cudaStreamSynchronize(stream));
   fac->factor();
 }
 
-OperatorEngine::~OperatorEngine() = default;
+OperatorEngine::~OperatorEngine() {
+  if (blas) cublasDestroy(static_cast<cublasHandle_t>(blas));
+}
 
 void OperatorEngine::spmv(int which, const double* x, double* y) {
   const double* val = which == 0 ? d_K.as<double>()
@@ -330,9 +392,9 @@ void OperatorEngine::bvec(const double* r, double* w) {
 void OperatorEngine::gemv_t(const double* V, int k, const double* w, double* h) {
   if (k <= 0) return;
   if (k > 512) fail(errc::config, "Krylov dimension above 512");
-  const int nb = kRedBlocks;
-  gemv_t_part<<<nb, kRedThreads, 0, stream>>>(V, k, 2 * n, w, w + n, n, d_part.as<double>());
-  reduce_parts<<<k, 32, 0, stream>>>(d_part.as<double>(), nb, k, h, nullptr);
+  gemv_t_part<<<gemv_t_blocks, kRedThreads, sizeof(double) * gemv_t_chunk, stream>>>(
+      V, k, 2 * n, w, w + n, n, gemv_t_chunk, d_part.as<double>());
+  reduce_parts<<<k, 32, 0, stream>>>(d_part.as<double>(), gemv_t_blocks, k, h, nullptr);
   launches += 2;
 }
 
@@ -361,20 +423,50 @@ void OperatorEngine::bnorm_normalize(const double* r, const double* w, double* b
 void OperatorEngine::combine(const double* V, int k, const double* Q_dev, int ldq, int ncols,
                              double* Vout) {
   if (ncols <= 0 || k <= 0) return;
-  dim3 grid(std::min(div_up(2 * n, 256), 148 * 4), div_up(ncols, 8));
-  combine_k<<<grid, 256, sizeof(double) * k * 8, stream>>>(V, k, 2 * n, Q_dev, ldq, ncols, Vout);
+  // Vout (2n x ncols) = V (2n x k, basis vectors contiguous) * Q (k x ncols):
+  // a plain DGEMM (FP64 tensor cores), arithmetic intensity ~ncols/4 flop/byte
+  const double one = 1.0, zero = 0.0;
+  const int64_t n2 = 2 * n;
+  if (cublasDgemm(static_cast<cublasHandle_t>(blas), CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(n2), ncols, k, &one,
+                  V, static_cast<int>(n2), Q_dev, ldq, &zero, Vout, static_cast<int>(n2)) != CUBLAS_STATUS_SUCCESS)
+    fail(errc::solver, "cublasDgemm (Krylov-Schur combine) failed");
   ++launches;
 }
 
-void OperatorEngine::pencil_residual(const double* ur, const double* ui, double lr, double li,
-                                     double* out) {
-  residual_part<<<kRedBlocks, kRedThreads, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
-                                                       d_K.as<double>(), d_C.as<double>(),
-                                                       d_M.as<double>(), ur, ui, lr, li,
-                                                       d_part.as<double>());
-  residual_final<<<1, 32, 0, stream>>>(d_part.as<double>(), kRedBlocks, out);
-  launches += 2;
+
+void OperatorEngine::ritz_residuals(const double* V, int m, const double* Y, int nc, const double* lam,
+                                    const int* blk, double* Xrm, double* out) {
+  if (nc <= 0) return;
+  const int64_t n2 = 2 * n;
+  const int ldx = 2 * nc;
+  // Xrm (2nc x 2n, column-major == 2n x 2nc row-major) = Y^T V^T
+  const double one = 1.0, zero = 0.0;
+  if (cublasDgemm(static_cast<cublasHandle_t>(blas), CUBLAS_OP_T, CUBLAS_OP_T, ldx, static_cast<int>(n2), m, &one, Y,
+                  m, V, static_cast<int>(n2), &zero, Xrm, ldx) != CUBLAS_STATUS_SUCCESS)
+    fail(errc::solver, "cublasDgemm (Ritz vectors) failed");
+  if (d_rcand.bytes < sizeof(double) * 2 * nc + sizeof(int) * nc) d_rcand.alloc(sizeof(double) * 2 * nc + sizeof(int) * nc);
+  const int nbx = kRedBlocks;
+  if (d_rpart.bytes < sizeof(double) * 2 * nc * nbx) d_rpart.alloc(sizeof(double) * 2 * nc * nbx);
+  std::vector<char> hbuf(sizeof(double) * 2 * nc + sizeof(int) * nc);
+  std::memcpy(hbuf.data(), lam, sizeof(double) * 2 * nc);
+  std::memcpy(hbuf.data() + sizeof(double) * 2 * nc, blk, sizeof(int) * nc);
+  RQB_CUDA(cudaMemcpyAsync(d_rcand.p, hbuf.data(), hbuf.size(), cudaMemcpyHostToDevice, stream));
+  const double* dlam = d_rcand.as<double>();
+  const int* dblk = reinterpret_cast<const int*>(dlam + 2 * nc);
+  dim3 grid(nbx, (nc + 63) / 64);
+  ritz_residual_k<<<grid, kRedThreads, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_K.as<double>(),
+                                                   d_C.as<double>(), d_M.as<double>(), Xrm, ldx, nc, dlam, dblk,
+                                                   d_rpart.as<double>());
+  sum_rows<<<2 * nc, 32, 0, stream>>>(d_rpart.as<double>(), nbx, out);
+  launches += 3;
 }
+
+void OperatorEngine::ritz_extract(const double* Xrm, int nc, int c, int part_im, double* out) {
+  const int* dblk = reinterpret_cast<const int*>(d_rcand.as<double>() + 2 * nc);
+  ritz_extract_k<<<std::min(div_up(n, 256), kRedBlocks), 256, 0, stream>>>(Xrm, 2 * nc, n, dblk, c, part_im, out);
+  ++launches;
+}
+
 
 double OperatorEngine::time_op(int what, int iters, int param) {
   const bool flush_l2 = (what & 0x100) != 0;
@@ -384,6 +476,18 @@ double OperatorEngine::time_op(int what, int iters, int param) {
   DeviceBuffer a, b, V, h;
   a.alloc(sizeof(double) * n2);
   b.alloc(sizeof(double) * n2);
+  DeviceBuffer Q, X;
+  std::vector<double> lamh;
+  std::vector<int> blkh;
+  if (what == 7 || what == 8) {  // restart DGEMM 2n x k x k / batched residual of k candidates
+    V.alloc(sizeof(double) * k * n2);
+    Q.alloc(sizeof(double) * k * k);
+    X.alloc(sizeof(double) * k * n2);
+    RQB_CUDA(cudaMemsetAsync(V.p, 0, V.bytes, stream));
+    RQB_CUDA(cudaMemsetAsync(Q.p, 0, Q.bytes, stream));
+    for (int c = 0; c < k; ++c) lamh.push_back(0.1), lamh.push_back(0.2), blkh.push_back(c & 1);
+    h.alloc(sizeof(double) * 2 * k);
+  }
   if (what == 3 || what == 4) {
     V.alloc(sizeof(double) * (k + 1) * n2);
     h.alloc(sizeof(double) * (k + 1));
@@ -404,6 +508,8 @@ double OperatorEngine::time_op(int what, int iters, int param) {
       case 4: gemv_n(V.as<double>(), k, h.as<double>(), a.as<double>(), nullptr); break;
       case 5: RQB_CUDA(cudaGraphLaunch(fac->graph_factor_exec, stream)); break;
       case 6: spmv(2, a.as<double>(), b.as<double>()); break;
+      case 7: combine(V.as<double>(), k, Q.as<double>(), k, k, X.as<double>()); break;
+      case 8: ritz_residuals(V.as<double>(), k, Q.as<double>(), k / 2, lamh.data(), blkh.data(), X.as<double>(), h.as<double>()); break;
       default: fail(errc::config, "unknown timing target");
     }
   };

@@ -205,6 +205,16 @@ __device__ __forceinline__ void load_diag(double* D, double* rinv, const double*
   }
 }
 
+// partial of one pivot block, summed in a fixed order (u ascending): the
+// sweeps add these per-block partials in block order, so results do not
+// depend on how publication rounds happened to group the blocks
+__device__ __forceinline__ double block_dot(const double* lp, int64_t ld, const double* xs, int c0, int c1,
+                                            int grp) {
+  double r[kRB / 4];
+  load_block(r, lp, ld, true, c0, c1, grp);
+  return fma_block(r, xs + c0, c1 - c0, grp);
+}
+
 // forward: unit-lower 64x64 substitution in warp 0; lane holds rows lane, lane+32
 __device__ __forceinline__ void fwd_triangle(const double* D, int lane, double& v0, double& v1) {
 #pragma unroll
@@ -311,9 +321,9 @@ __global__ void __launch_bounds__(kST, 3) fwd_sweep(SweepArgs A) {
             if (row < nr) {
               if (base == done) {
                 s += fma_block(lr, stg, b1 - done, grp);
-                s += stream_cols(lp, ld, stg - base, b1, hi, grp);
+                for (int c = b1; c < hi; c += kRB) s += block_dot(lp, ld, stg - base, c, min(hi, c + kRB), grp);
               } else {
-                s += stream_cols(lp, ld, stg - base, base, hi, grp);
+                for (int c = base; c < hi; c += kRB) s += block_dot(lp, ld, stg - base, c, min(hi, c + kRB), grp);
               }
             }
             __syncthreads();
@@ -435,16 +445,17 @@ __global__ void __launch_bounds__(kST, 3) bwd_sweep(SweepArgs A) {
           }
           __syncthreads();
           const int avail_lo = avail_s;
-          for (int top = done_hi; top > avail_lo; top -= kStage) {
-            const int bot = max(avail_lo, top - kStage);
+          for (int top = done_hi, bot; top > avail_lo; top = bot) {
+            bot = max(avail_lo, (top - kStage + kRB - 1) / kRB * kRB);  // block aligned
             for (int c = tid; c < top - bot; c += kST) stg[c] = __ldcg(&A.xnew[I.start + bot + c]);
             __syncthreads();
             if (row < nr) {
               if (top == done_hi) {
                 s += fma_block(ur, stg + (b0 - bot), done_hi - b0, grp);
-                s += stream_cols(up, ld, stg - bot, bot, b0, grp);
+                for (int c = b0; c > bot; c -= kRB) s += block_dot(up, ld, stg - bot, c - kRB, c, grp);
               } else {
-                s += stream_cols(up, ld, stg - bot, bot, top, grp);
+                for (int chi = top; chi > bot; chi = max(bot, (chi - 1) / kRB * kRB))
+                  s += block_dot(up, ld, stg - bot, max(bot, (chi - 1) / kRB * kRB), chi, grp);
               }
             }
             __syncthreads();

@@ -145,9 +145,13 @@ struct OperatorEngine {
   std::unique_ptr<FactorEngine> fac;
   DeviceBuffer d_rowptr, d_col, d_K, d_C, d_M, d_Q;
   DeviceBuffer d_w, d_t, d_part, d_scal;  // workspaces
+  DeviceBuffer d_rcand, d_rpart;          // batched residual candidates / partials
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   int64_t nparts = 0;
+  int64_t gemv_t_chunk = 256;  // CGS projection: entries per block, blocks
+  int gemv_t_blocks = 1;
+  void* blas = nullptr;  // cublasHandle_t on `stream` (restart / Ritz-vector DGEMMs)
 
   OperatorEngine(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
                  const double* C, const double* M, const Symbolic& s, double sigma,
@@ -166,9 +170,15 @@ struct OperatorEngine {
   void dot2n(const double* x, const double* y, double* out);  // out = x.y (2n)
   // Vout[c] = sum_k V[k] Q[k + c*ldq] for c < ncols (restart compression)
   void combine(const double* V, int k, const double* Q_dev, int ldq, int ncols, double* Vout);
-  // Pencil residual pieces for complex u = ur + i ui at lambda = lr + i li:
-  // out[0] = ||Q(lambda) u||_2^2 (device scalar)
-  void pencil_residual(const double* ur, const double* ui, double lr, double li, double* out);
+  // Ritz vectors X = V^T-combination with Y (m x 2nc: columns Re y_c, Im y_c),
+  // stored row-major in Xrm (2n x 2nc), and their pencil residuals:
+  // out[2c] = ||Q(lambda_c) x_c||^2, out[2c+1] = ||x_c||^2 over block blk[c]
+  // (lam: host {re, im} pairs of the scaled-pencil eigenvalues).
+  void ritz_residuals(const double* V, int m, const double* Y, int nc, const double* lam, const int* blk,
+                      double* Xrm, double* out);
+  // contiguous copy (n entries) of part (0 re, 1 im) of Ritz vector c of the
+  // last ritz_residuals batch, block blk[c]
+  void ritz_extract(const double* Xrm, int nc, int c, int part_im, double* out);
   // Average device ms of one call of an operation (see rq_operator_time).
   double time_op(int what, int iters, int param);
 };

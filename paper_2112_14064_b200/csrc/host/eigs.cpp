@@ -158,6 +158,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   std::vector<double> ha((m + 1) * (m + 1)), hb((m + 1) * (m + 1)), betas(m + 1);
   double t_solve = 0, t_orth = 0, t_ritz = 0, t_check = 0, t_restart = 0, t_sync = 0;
   double check_gate = o.est_factor * o.tol;
+  int last_nchk = 0;  // candidates of the last explicit check (row-major Ritz batch in dX)
   int since_check = 0;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms_since = [](std::chrono::steady_clock::time_point a) {
@@ -334,25 +335,33 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     if (maybe) {
       // Ritz vectors X = V_m [Re y, Im y] (y = Z Y[:, i])
       std::vector<double> Yr(static_cast<size_t>(m) * 2 * nchk);
+      std::vector<cplx> ycol(m);
       for (int c = 0; c < nchk; ++c) {
         const int i = chk[c];
+        std::fill(ycol.begin(), ycol.end(), cplx(0.0));
+        for (int t = 0; t <= i; ++t) {  // y = Z[:, 0..i] Y[0..i, i] (Y upper triangular)
+          const cplx yt = Y(t, i);
+          const cplx* zc = &Z.a[static_cast<size_t>(t) * m];
+          for (int row = 0; row < m; ++row) ycol[row] += zc[row] * yt;
+        }
         for (int row = 0; row < m; ++row) {
-          cplx y = 0.0;
-          for (int t = 0; t <= i; ++t) y += Z(row, t) * Y(t, i);
-          Yr[row + static_cast<size_t>(2 * c) * m] = y.real();
-          Yr[row + static_cast<size_t>(2 * c + 1) * m] = y.imag();
+          Yr[row + static_cast<size_t>(2 * c) * m] = ycol[row].real();
+          Yr[row + static_cast<size_t>(2 * c + 1) * m] = ycol[row].imag();
         }
       }
       cuda_check(cudaMemcpyAsync(dQ.p, Yr.data(), sizeof(double) * Yr.size(), cudaMemcpyHostToDevice, st),
                  "H2D Y");
-      op.combine(V, m, dQ.as<double>(), m, 2 * nchk, dX.as<double>());
+      std::vector<double> lam(2 * nchk);
       for (int c = 0; c < nchk; ++c) {
         const cplx gam = rz[chk[c]].lambda / vs;  // eigenvalue of the scaled pencil
-        const int blk = std::abs(gam) > 1.0 ? 1 : 0;  // larger-norm block
-        cblock[c] = blk;
-        const double* xr = dX.as<double>() + static_cast<int64_t>(2 * c) * n2 + blk * n;
-        op.pencil_residual(xr, xr + n2, gam.real(), gam.imag(), dRes.as<double>() + 2 * c);
+        cblock[c] = std::abs(gam) > 1.0 ? 1 : 0;  // larger-norm block
+        lam[2 * c] = gam.real();
+        lam[2 * c + 1] = gam.imag();
       }
+      // X = V_m [Re y, Im y] (one DGEMM, row-major) + all residuals in one SpMM pass
+      op.ritz_residuals(V, m, dQ.as<double>(), nchk, lam.data(), cblock.data(), dX.as<double>(),
+                        dRes.as<double>());
+      last_nchk = nchk;
       std::vector<double> rr(2 * nchk);
       cuda_check(cudaMemcpyAsync(rr.data(), dRes.p, sizeof(double) * 2 * nchk, cudaMemcpyDeviceToHost, st),
                  "D2H res");
@@ -388,11 +397,12 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         final_vecs_re.assign(static_cast<size_t>(n) * nev, 0.0);
         final_vecs_im.assign(static_cast<size_t>(n) * nev, 0.0);
         for (int c = 0; c < nev; ++c) {
-          const double* xr = dX.as<double>() + static_cast<int64_t>(2 * c) * n2 + cblock[c] * n;
-          cuda_check(cudaMemcpy(final_vecs_re.data() + static_cast<size_t>(c) * n, xr,
-                                sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H x");
-          cuda_check(cudaMemcpy(final_vecs_im.data() + static_cast<size_t>(c) * n, xr + n2,
-                                sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H x");
+          for (int part = 0; part < 2; ++part) {
+            op.ritz_extract(dX.as<double>(), last_nchk, c, part, dW.as<double>());
+            cuda_check(cudaMemcpyAsync((part ? final_vecs_im : final_vecs_re).data() + static_cast<size_t>(c) * n,
+                                       dW.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H x");
+          }
+          cuda_check(cudaStreamSynchronize(st), "sync");
           double nr = 0;
           for (int64_t i = 0; i < n; ++i)
             nr += final_vecs_re[c * n + i] * final_vecs_re[c * n + i] +

@@ -15,4 +15,4 @@ def test_dense_kernels(tmp_path):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout
-    assert r.stdout.count(" ok") == 5
+    assert r.stdout.count(" ok") == 7  # 5 random + 2 degenerate-cluster matrices
