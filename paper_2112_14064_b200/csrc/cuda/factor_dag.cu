@@ -35,6 +35,7 @@
 // __threadfence + atomic.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -50,6 +51,14 @@ constexpr int kTile = 64;         // big-front tile edge
 constexpr int kTSP = kTile + 4;   // padded smem stride of DMMA operand tiles
 constexpr double kLmax = 10.0 * (1.0 - 1e-14);  // 1/threshold, conservative
 constexpr int kCnt = 5;  // per-front counters: tasks, asm, diag, rc, released
+#ifndef RQB_DAG_OCC
+#define RQB_DAG_OCC 1
+#endif
+#ifndef RQB_DAG_SMALL_NF
+#define RQB_DAG_SMALL_NF 160
+#endif
+constexpr int kDagOcc = RQB_DAG_OCC;           // resident CTAs per SM the register budget targets
+constexpr int kDagSmallNf = RQB_DAG_SMALL_NF;  // SMALL tasks: whole front in shared memory up to this nf
 
 enum : int16_t { T_SMALL = 0, T_ASM = 1, T_DIAG = 2, T_ROWS = 3, T_COLS = 4, T_UPD = 5 };
 
@@ -93,6 +102,7 @@ struct DagArgs {
   unsigned long long* flagbits;
   int* flags;   // [0] singular, [1] swaps
   unsigned long long* prof;  // optional: per task type {work cycles, wait cycles, count}
+  unsigned long long* trace; // optional (RQB_DAG_TRACE): per task {start, end} globaltimer ns
   double* small_backup;      // per CTA: 160 x 16 panel backup of the SMALL path
   int* deps;                 // remaining predecessors per task
   int* queue;                // ready queue (task ids, -1 = not yet pushed)
@@ -179,7 +189,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
   __shared__ double red_s[kDT / 32];
   __shared__ double urow_s[2][kPB];
   __shared__ int any_swap_s;
-  double* pbk = A.small_backup + (int64_t)blockIdx.x * kSmallNf * kPB;
+  double* pbk = A.small_backup + (int64_t)blockIdx.x * kDagSmallNf * kPB;
   for (int k0 = 0; k0 < np; k0 += kPB) {
     const int pw = min(kPB, np - k0);
     // ---- speculative unpivoted panel: thread t owns row t in registers; the
@@ -195,7 +205,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
       if (own)
 #pragma unroll
         for (int c = 0; c < kPB; ++c)
-          if (c < pw) pbk[i + c * kSmallNf] = a[c];
+          if (c < pw) pbk[i + c * kDagSmallNf] = a[c];
 #pragma unroll
       for (int jj = 0; jj < kPB; ++jj) {
         if (jj < pw) {
@@ -237,7 +247,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
     } else {
       // restore the panel, redo it with exact threshold pivoting (warp 0)
       if (tid < nf && tid >= k0)
-        for (int c = 0; c < pw; ++c) sm[tid + (k0 + c) * lds] = pbk[tid + c * kSmallNf];
+        for (int c = 0; c < pw; ++c) sm[tid + (k0 + c) * lds] = pbk[tid + c * kDagSmallNf];
       __syncthreads();
       if (tid == 0) any_swap_s = 1;
     }
@@ -733,7 +743,7 @@ __device__ int pop_task(const DagArgs& A) {
   return t;
 }
 
-__global__ void __launch_bounds__(kDT, 1) factor_dag_kernel(DagArgs A) {
+__global__ void __launch_bounds__(kDT, kDagOcc) factor_dag_kernel(DagArgs A) {
   extern __shared__ double sm[];
   __shared__ int task_s, last_s, done_s;
   __shared__ int piv_sh[kPB];
@@ -755,6 +765,11 @@ __global__ void __launch_bounds__(kDT, 1) factor_dag_kernel(DagArgs A) {
     const FrontDag D = A.dag[f];
     int* cnt = A.cnt + kCnt * f;
     const long long t_work = A.prof ? clock64() : 0;
+    if (A.trace && tid == 0) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+      A.trace[2 * (size_t)t] = gt;
+    }
     // ---- work (every predecessor has completed: no waits)
     switch (T.type) {
       case T_SMALL: small_front(A, F, sm, piv_sh); break;
@@ -832,6 +847,11 @@ __global__ void __launch_bounds__(kDT, 1) factor_dag_kernel(DagArgs A) {
         for (int x = tid; x < PD.nasm; x += kDT) notify(A, PD.task_base + x);
       }
     }
+    if (A.trace && tid == 0) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+      A.trace[2 * (size_t)t + 1] = gt;
+    }
     if (tid == 0 && A.prof) {
       const long long t_end = clock64();
       atomicAdd(&A.prof[3 * T.type + 0], (unsigned long long)(t_end - t_work));
@@ -846,7 +866,7 @@ int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
 struct DagPlan {
   DeviceBuffer d_tasks, d_dag, d_cnt, d_tile, d_rc, d_flagbits, d_backup, d_prof, d_bnd,
-      d_small_backup, d_deps0, d_deps, d_queue0, d_queue, d_qctl, d_qctl0, d_sb;
+      d_small_backup, d_deps0, d_deps, d_queue0, d_queue, d_qctl, d_qctl0, d_sb, d_trace;
   int ntasks = 0, nfronts = 0, ntile = 0, nflag = 0, grid = 148, nready = 0;
   size_t smem = 0;
   double flops_upd = 0;
@@ -870,7 +890,7 @@ void rqb_dag_build(FactorEngine& fe) {
     D.slot = -1;
     D.parent = F.parent;
     const int nch = static_cast<int>(F.children.size());
-    if (F.nf <= kSmallNf) {
+    if (F.nf <= kDagSmallNf) {
       tasks.push_back({f, T_SMALL, 0, 0, 0});
       deps.push_back(nch);
       D.ntasks = 1;
@@ -981,7 +1001,7 @@ void rqb_dag_build(FactorEngine& fe) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
   RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_dag_kernel, kDT, P->smem));
   P->grid = std::max(1, std::min(P->ntasks, nsm * std::max(1, occ)));
-  P->d_small_backup.alloc(sizeof(double) * P->grid * kSmallNf * kPB);
+  P->d_small_backup.alloc(sizeof(double) * P->grid * kDagSmallNf * kPB);
   fe.dag_ntasks = P->ntasks;
   fe.dag.reset(P.release());
 }
@@ -1017,10 +1037,15 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   A.step_base = P.d_sb.as<int32_t>();
   A.small_backup = P.d_small_backup.as<double>();
   A.prof = nullptr;
+  A.trace = nullptr;
   if (fe.dag_prof_enabled) {
     if (!P.d_prof.p) P.d_prof.alloc(sizeof(unsigned long long) * 32);
     RQB_CUDA(cudaMemsetAsync(P.d_prof.p, 0, P.d_prof.bytes, fe.stream));
     A.prof = P.d_prof.as<unsigned long long>();
+    if (std::getenv("RQB_DAG_TRACE")) {
+      if (!P.d_trace.p) P.d_trace.alloc(sizeof(unsigned long long) * 2 * P.ntasks);
+      A.trace = P.d_trace.as<unsigned long long>();
+    }
   }
   factor_dag_kernel<<<P.grid, kDT, P.smem, fe.stream>>>(A);
   RQB_CUDA(cudaGetLastError());
@@ -1047,6 +1072,20 @@ void rqb_dag_profile(FactorEngine& fe, double* out) {
   out[19] = fe.dag->ntasks;
   out[20] = h[20] / (clk_khz * 1.0);  // ready-queue pop wait, summed over CTAs
   for (int i = 21; i < 24; ++i) out[i] = h[i] / (clk_khz * 1.0);  // DIAG phases (LU, inv L, inv U)
+  if (const char* path = std::getenv("RQB_DAG_TRACE")) {  // development trace: tasks + timestamps
+    DagPlan& P = *fe.dag;
+    std::vector<unsigned long long> tr(2 * static_cast<size_t>(P.ntasks));
+    std::vector<Task> tk(P.ntasks);
+    RQB_CUDA(cudaMemcpy(tr.data(), P.d_trace.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
+    RQB_CUDA(cudaMemcpy(tk.data(), P.d_tasks.p, sizeof(Task) * tk.size(), cudaMemcpyDeviceToHost));
+    if (FILE* fp = std::fopen(path, "wb")) {
+      const int32_t nt = P.ntasks;
+      std::fwrite(&nt, sizeof(nt), 1, fp);
+      std::fwrite(tk.data(), sizeof(Task), tk.size(), fp);
+      std::fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fp);
+      std::fclose(fp);
+    }
+  }
 }
 
 void DagPlanDeleter::operator()(DagPlan* p) const { delete p; }
