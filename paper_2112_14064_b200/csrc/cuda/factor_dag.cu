@@ -362,51 +362,56 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
 // DIAG: 32x32 diagonal block of panel s, unpivoted (speculative), in the
 // registers of warp 0 (row `lane` per thread; shuffles broadcast the pivot row).
 // The factored block goes back to the front; ROWS/COLS solve against it.
+// Code size matters here: every task type lives in one persistent kernel, so
+// the panel tasks below are written as rolled loops (a fully unrolled 32-step
+// substitution is tens of KB of SASS and thrashes the instruction cache).
+
+// DIAG: unpivoted LU of the w x w diagonal block in shared memory, all
+// threads: thread (i = tid & 31, columns cb + 8q) updates its 4 entries of row
+// i per step (one barrier per step); the multipliers of column j are scaled
+// after the barrier (the next step does not read column j).
 __device__ void diag_task(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s, double* sm) {
   const int k = s * kNB, w = min(kNB, F.npiv - k);
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr unsigned FULL = 0xffffffffu;
-  double* T = sm;               // 32 x 33
+  const int tid = threadIdx.x, i = tid & 31, cb = tid >> 5;
+  double* T = sm;  // 32 x 33
   double* red = sm + 32 * 33;
   double* bk = A.backup + D.backup_off;
   {
     double v[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int idx = tid + i * kDT, r = idx % 32, c = idx / 32;
-      v[i] = (r < w && c < w) ? __ldcg(&g[(k + r) + (int64_t)(k + c) * ld]) : (r == c ? 1.0 : 0.0);
+    for (int q = 0; q < 4; ++q) {
+      const int c = cb + 8 * q;
+      v[q] = (i < w && c < w) ? __ldcg(&g[(k + i) + (int64_t)(k + c) * ld]) : (i == c ? 1.0 : 0.0);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int idx = tid + i * kDT, r = idx % 32, c = idx / 32;
-      T[r + c * 33] = v[i];
-      if (r < w && c < w) bk[(k + r) + (int64_t)c * F.nf] = v[i];
+    for (int q = 0; q < 4; ++q) {
+      const int c = cb + 8 * q;
+      T[i + c * 33] = v[q];
+      if (i < w && c < w) bk[(k + i) + (int64_t)c * F.nf] = v[q];
     }
   }
   __syncthreads();
   double lm = 0.0;
-  // unpivoted LU, all threads: step j updates the (w-1-j)^2 trailing entries
-  // (one barrier per step); the multipliers of column j are stored after the
-  // barrier, which the next step does not read
-  (void)warp;
-  (void)lane;
-  (void)FULL;
   bool sing = false;
+#pragma unroll 1
   for (int j = 0; j < w; ++j) {
     const double ujj = T[j + j * 33];
     if (!(fabs(ujj) >= kSingularTiny)) sing = true;
     const double rinv = 1.0 / ujj;
-    const int m = w - 1 - j;
-    for (int e = tid; e < m * m; e += kDT) {
-      const int i = j + 1 + e % m, c = j + 1 + e / m;
-      T[i + c * 33] = fma(-T[i + j * 33] * rinv, T[j + c * 33], T[i + c * 33]);
+    if (i > j && i < w) {
+      const double l = T[i + j * 33] * rinv;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = cb + 8 * q;
+        if (c > j && c < w) T[i + c * 33] = fma(-l, T[j + c * 33], T[i + c * 33]);
+      }
     }
     __syncthreads();
-    if (tid < m) {
-      const double l = T[j + 1 + tid + j * 33] * rinv;
-      T[j + 1 + tid + j * 33] = l;
+    if (tid < w && tid > j) {
+      const double l = T[tid + j * 33] * rinv;
+      T[tid + j * 33] = l;
       lm = fmax(lm, fabs(l));
     }
   }
@@ -414,9 +419,9 @@ __device__ void diag_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   __syncthreads();
   lm = block_max(lm, red);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int idx = tid + i * kDT, rr = idx % 32, c = idx / 32;
-    if (rr < w && c < w) g[(k + rr) + (int64_t)(k + c) * ld] = T[rr + c * 33];
+  for (int q = 0; q < 4; ++q) {
+    const int c = cb + 8 * q;
+    if (i < w && c < w) g[(k + i) + (int64_t)(k + c) * ld] = T[i + c * 33];
   }
   for (int j = tid; j < w; j += kDT) A.ipiv[F.start + k + j] = k + j;
   if (tid == 0) atomicMax(&A.flagbits[D.flag_off + s], (unsigned long long)__double_as_longlong(lm));
@@ -465,13 +470,17 @@ __device__ void rows_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   __syncthreads();
   double lm = 0.0;
   if (tid < nr) {
+    // x U11 = p, right-looking: x_j = s_j * (1/u_jj), then s_c -= x_j u_jc
+    // (serial chain: one multiply + one FMA per column; the reciprocals are
+    // independent of it)
     double x[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      double sv = P[tid + j * kPS];
+    for (int j = 0; j < 32; ++j) x[j] = P[tid + j * kPS];
 #pragma unroll
-      for (int t = 0; t < j; ++t) sv = fma(-x[t], U[t + j * 33], sv);
-      x[j] = j < w ? sv / U[j + j * 33] : 0.0;
+    for (int j = 0; j < 32; ++j) {
+      x[j] = j < w ? x[j] * (1.0 / U[j + j * 33]) : 0.0;
+#pragma unroll
+      for (int c = j + 1; c < 32; ++c) x[c] = fma(-x[j], U[j + c * 33], x[c]);
     }
     const bool cand = r0 + tid < np;
 #pragma unroll
@@ -524,14 +533,14 @@ __device__ void cols_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   }
   __syncthreads();
   if (tid < nc) {
+    // L11 x = p (unit lower), right-looking: x_i final, then s_r -= l_ri x_i
     double x[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      double sv = P[i + tid * 33];
+    for (int i = 0; i < 32; ++i) x[i] = P[i + tid * 33];
 #pragma unroll
-      for (int t = 0; t < i; ++t) sv = fma(-L[i + t * 33], x[t], sv);
-      x[i] = sv;
-    }
+    for (int i = 0; i < 32; ++i)
+#pragma unroll
+      for (int r = i + 1; r < 32; ++r) x[r] = fma(-L[r + i * 33], x[i], x[r]);
 #pragma unroll
     for (int i = 0; i < 32; ++i)
       if (i < w) g[(k + i) + (int64_t)(c0 + tid) * ld] = x[i];
