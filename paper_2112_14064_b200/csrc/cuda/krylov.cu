@@ -412,6 +412,40 @@ void OperatorEngine::dot2n(const double* x, const double* y, double* out) {
   launches += 2;
 }
 
+// w = B r from one M-product (t = M r_l), beta = sqrt(r . w), and both
+// v = r / beta and B v = w / beta written in one pass
+__global__ void normalize_b_k(const double* __restrict__ part, int nb, const double* __restrict__ r,
+                              const double* __restrict__ t, int64_t n, double* __restrict__ beta_out,
+                              double* __restrict__ v, double* __restrict__ bv) {
+  __shared__ double beta_s;
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nb; b += 32) s += part[b];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) {
+      const double beta = sqrt(fmax(s, 0.0));
+      beta_s = beta;
+      if (blockIdx.x == 0 && beta_out) *beta_out = beta;
+    }
+  }
+  __syncthreads();
+  const double inv = beta_s > 0.0 ? 1.0 / beta_s : 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 2 * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const double re = r[e];
+    v[e] = re * inv;
+    bv[e] = (e < n ? re : t[e - n]) * inv;
+  }
+}
+
+void OperatorEngine::bnorm_normalize_b(const double* r, double* beta_out, double* v_next, double* bv_next) {
+  double* t = d_t.as<double>();
+  spmv(2, r + n, t);  // t = M r_l
+  dot_part<<<kRedBlocks, kRedThreads, 0, stream>>>(r, r + n, r, t, n, 2 * n, d_part.as<double>());
+  normalize_b_k<<<std::min(div_up(2 * n, 256), 148 * 8), 256, 0, stream>>>(d_part.as<double>(), kRedBlocks, r, t,
+                                                                          n, beta_out, v_next, bv_next);
+  launches += 2;
+}
+
 void OperatorEngine::bnorm_normalize(const double* r, const double* w, double* beta_out,
                                      double* v_next) {
   dot_part<<<kRedBlocks, kRedThreads, 0, stream>>>(r, r + n, w, w + n, n, 2 * n, d_part.as<double>());

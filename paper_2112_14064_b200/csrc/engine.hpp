@@ -167,6 +167,8 @@ struct OperatorEngine {
   void gemv_n(const double* V, int k, const double* h, double* r, double* h_acc);
   // out = ||r||_B computed with w = B r; v_next = r / out
   void bnorm_normalize(const double* r, const double* w, double* beta_out, double* v_next);
+  // beta = ||r||_B with B r from one M-product; v_next = r / beta, bv_next = B r / beta
+  void bnorm_normalize_b(const double* r, double* beta_out, double* v_next, double* bv_next);
   void dot2n(const double* x, const double* y, double* out);  // out = x.y (2n)
   // Vout[c] = sum_k V[k] Q[k + c*ldq] for c < ncols (restart compression)
   void combine(const double* V, int k, const double* Q_dev, int ldq, int ncols, double* Vout);

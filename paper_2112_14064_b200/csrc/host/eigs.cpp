@@ -100,9 +100,14 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   const double fb_macs = static_cast<double>(op.fac->sym.nnz_l + op.fac->sym.nnz_u);
   const double nnz = static_cast<double>(op.nnz);
 
-  DeviceBuffer dV, dV2, dR, dW, dHa, dHb, dBeta, dQ, dX, dRes;
+  // V: Krylov basis; BV = B V kept alongside, so every B-inner product of CGS2
+  // is a plain projection h = (BV)^T r (B = diag(I, M) symmetric) and each
+  // step needs one M-product (for the new vector) instead of three
+  DeviceBuffer dV, dV2, dBV, dBV2, dR, dW, dHa, dHb, dBeta, dQ, dX, dRes;
   dV.alloc(sizeof(double) * (m + 1) * n2);
   dV2.alloc(sizeof(double) * (m + 1) * n2);
+  dBV.alloc(sizeof(double) * (m + 1) * n2);
+  dBV2.alloc(sizeof(double) * (m + 1) * n2);
   dR.alloc(sizeof(double) * n2);
   dW.alloc(sizeof(double) * n2);
   dHa.alloc(sizeof(double) * (m + 1) * (m + 1));
@@ -113,6 +118,8 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   dRes.alloc(sizeof(double) * 4 * (m + 1));
   double* V = dV.as<double>();
   double* V2 = dV2.as<double>();
+  double* BV = dBV.as<double>();
+  double* BV2 = dBV2.as<double>();
   double* r = dR.as<double>();
   double* w = dW.as<double>();
 
@@ -121,22 +128,20 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   cuda_check(cudaEventCreate(&e_b), "event");
 
   // Start vector v = splitmix64(seed) uniform[-1,1]^{2N}, B-normalised.
-  auto fresh_vector = [&](uint64_t seed, int nlock, double* dst) {
+  auto fresh_vector = [&](uint64_t seed, int nlock, double* dst, double* dst_b) {
     std::vector<double> v(n2);
     uint64_t s = seed;
     for (int64_t i = 0; i < n2; ++i) v[i] = splitmix_uniform(s);
     cuda_check(cudaMemcpyAsync(r, v.data(), sizeof(double) * n2, cudaMemcpyHostToDevice, st), "H2D v0");
     for (int pass = 0; pass < 2 && nlock > 0; ++pass) {
-      op.bvec(r, w);
-      op.gemv_t(V, nlock, w, dHa.as<double>());
+      op.gemv_t(BV, nlock, r, dHa.as<double>());
       op.gemv_n(V, nlock, dHa.as<double>(), r, nullptr);
-      L.n_mv += 1;
+      L.n_mv += 1;  // ledger: the reference algorithm's B-product
       L.macs_mv += nnz;
       L.n_vv += 2 * nlock;
       L.macs_vv += 2.0 * nlock * n2;
     }
-    op.bvec(r, w);
-    op.bnorm_normalize(r, w, dBeta.as<double>() + m, dst);
+    op.bnorm_normalize_b(r, dBeta.as<double>() + m, dst, dst_b);
     L.n_mv += 1;
     L.macs_mv += nnz;
     L.n_vv += 2;
@@ -146,7 +151,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0);  // column-major (m+1) x m
   auto Hc = [&](int i, int j) -> double& { return H[i + static_cast<size_t>(j) * (m + 1)]; };
 
-  fresh_vector(o.seed, 0, V);
+  fresh_vector(o.seed, 0, V, BV);
   int k = 0;
   int cycles = 0, guard_passes = 0, pass_cycles = 0;
   bool converged_final = false;
@@ -194,14 +199,14 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         }
         double* hA = dHa.as<double>() + static_cast<int64_t>(j) * (m + 1);
         double* hB = dHb.as<double>() + static_cast<int64_t>(j) * (m + 1);
-        op.bvec(r, w);
-        op.gemv_t(V, j + 1, w, hA);
+        // CGS2 with the stored B-images: h = (BV)^T r, r -= V h (twice),
+        // then ||r||_B, v_{j+1} = r / beta and B v_{j+1} from one M-product
+        op.gemv_t(BV, j + 1, r, hA);
         op.gemv_n(V, j + 1, hA, r, nullptr);
-        op.bvec(r, w);
-        op.gemv_t(V, j + 1, w, hB);
+        op.gemv_t(BV, j + 1, r, hB);
         op.gemv_n(V, j + 1, hB, r, nullptr);
-        op.bvec(r, w);
-        op.bnorm_normalize(r, w, dBeta.as<double>() + j, V + static_cast<int64_t>(j + 1) * n2);
+        op.bnorm_normalize_b(r, dBeta.as<double>() + j, V + static_cast<int64_t>(j + 1) * n2,
+                             BV + static_cast<int64_t>(j + 1) * n2);
         if (prof) {
           cuda_check(cudaEventRecord(e_b, st), "ev");
           cuda_check(cudaEventSynchronize(e_b), "ev");
@@ -501,19 +506,24 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     }
     cuda_check(cudaMemcpyAsync(dQ.p, Qp.data(), sizeof(double) * m * p, cudaMemcpyHostToDevice, st), "H2D Q");
     op.combine(V, m, dQ.as<double>(), m, p, V2);
+    op.combine(BV, m, dQ.as<double>(), m, p, BV2);
     L.n_restart += 1;
     L.macs_restart += static_cast<double>(m) * p * n2;
     std::fill(H.begin(), H.end(), 0.0);
     for (int c = 0; c < p; ++c)
       for (int i = 0; i < p; ++i) Hc(i, c) = Tp[i + static_cast<size_t>(c) * p];
     std::swap(V, V2);
+    std::swap(BV, BV2);
     if (deflate) {
       // b = 0 (converged directions deflated); fresh seeded continuation vector
-      fresh_vector(o.seed + 0x1000003ull * guard_passes, p, V + static_cast<int64_t>(p) * n2);
+      fresh_vector(o.seed + 0x1000003ull * guard_passes, p, V + static_cast<int64_t>(p) * n2,
+                   BV + static_cast<int64_t>(p) * n2);
     } else {
       for (int c = 0; c < p; ++c) Hc(p, c) = beta_m * Qp[(m - 1) + static_cast<size_t>(c) * m];
       cuda_check(cudaMemcpyAsync(V + static_cast<int64_t>(p) * n2, V2 + static_cast<int64_t>(m) * n2,
                                  sizeof(double) * n2, cudaMemcpyDeviceToDevice, st), "D2D v");
+      cuda_check(cudaMemcpyAsync(BV + static_cast<int64_t>(p) * n2, BV2 + static_cast<int64_t>(m) * n2,
+                                 sizeof(double) * n2, cudaMemcpyDeviceToDevice, st), "D2D Bv");
     }
     t_restart += ms_since(trs0);
     k = p;
