@@ -264,11 +264,16 @@ def run_b200(args):
                "kind": kind, "sample": f"{len(ts)} full factorizations of {args.config} "
                                        f"({sum(ts):.1f} s, complex cdouble arithmetic: 4x the real work)"}
 
-    traffic = None
+    # DRAM bytes per launch of the dominant kernel from a committed ncu --set
+    # full capture (profiles/ncu_traffic.json, written by tools/ncu_summary.py)
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get(KINDS[dom])
+            kname = {"factor_dag": "factor_dag_kernel"}.get(KINDS[dom], KINDS[dom])
+            ent = json.load(open(tpath)).get(args.config, {}).get(kname)
+            if ent:
+                traffic, traffic_src = ent["dram_bytes_per_launch"], ent["source"]
         except Exception:  # noqa: BLE001
             traffic = None
     bound = "tensor" if KINDS[dom] == "schur_dmma" else ("hbm" if dom in (0, 1) else "tensor")
@@ -281,6 +286,9 @@ def run_b200(args):
         ach = work_k[dom] / (ms_k[dom] * 1e9)  # TFLOP/s
         roof = {"bound": bound, "achieved": round(ach, 4), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(ach / peak, 5), "traffic": traffic}
+    if traffic_src:
+        roof["traffic_unit"] = "bytes/launch"
+        roof["traffic_source"] = traffic_src
     roof.update({"kernel": KINDS[dom], "launches_per_step": int(cnt_k[dom]),
                  "share_of_step": round(float(ms_k[dom] / ms_k.sum()), 4),
                  "peak_source": "hbm: MEASURED_PEAKS.json; fp64: measured tools/fp64_peak.cu "
