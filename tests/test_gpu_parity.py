@@ -259,3 +259,32 @@ def test_cfg3_solve_residual_and_cluster(name):
     lam = np.array([p.lam for p in pairs])
     assert np.all(np.minimum(np.abs(lam - ref), np.abs(lam - np.conj(ref))) <= 1e-8 * abs(ref))
     assert max(p.residual for p in pairs) <= 1e-10
+
+
+# --------------------------------------------------------------------------- sweeps
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_riga"])
+def test_solve_whole_front_items_and_determinism(name, monkeypatch):
+    """The triangular sweeps' two item layouts (64-row blocks with in-front
+    waits; whole small fronts per CTA, enabled by default only on levels with
+    >= 2 x grid fronts, i.e. the large configs) give the oracle's solution, and
+    repeated solves are bitwise identical (per-block partial sums are added in
+    block order, independent of publication timing)."""
+    P = rq.baseline_config(name)
+    o = rq.nested_dissection_order(P)
+    Q = P.q_values(SIGMA)
+    of = oracle.Factor(P.n, P.rowptr, P.col, Q, P.box, P.elems)
+    b = np.random.default_rng(11).standard_normal((P.n, 2))
+    xo = np.stack([of.solve(b[:, i]).real for i in range(2)], 1)
+    xs = []
+    for whole_min in (None, "1"):
+        if whole_min is None:
+            monkeypatch.delenv("RQB_WHOLE_MIN", raising=False)
+        else:
+            monkeypatch.setenv("RQB_WHOLE_MIN", whole_min)
+        f = rq.lu_factorize((P.rowptr, P.col, Q), o)
+        x1, x2 = f.solve(b), f.solve(b)
+        assert np.array_equal(x1, x2)
+        assert np.max(np.abs(x1 - xo)) <= 1e-9 * np.max(np.abs(xo))
+        xs.append(x1)
+    monkeypatch.delenv("RQB_WHOLE_MIN", raising=False)
+    assert np.max(np.abs(xs[0] - xs[1])) <= 1e-12 * np.max(np.abs(xs[0]))
