@@ -108,6 +108,11 @@ def baseline_config(name: str) -> QuadraticPencil:
         "cfg3_iga": (CURL, 4, 128, 0), "cfg3_riga": (CURL, 4, 128, 3),
         "cfg4_iga": (DIV, 3, 512, 0), "cfg4_riga": (DIV, 3, 512, 5),
     }
+    # BASELINE configs[4] (cfg5): H(curl) 256^2, p = 2..5, IGA vs rIGA with C^0
+    # separators every 8 elements (L = log2(256/8) = 5)
+    for p in (2, 3, 4, 5):
+        table[f"cfg5_p{p}_iga"] = (CURL, p, 256, 0)
+        table[f"cfg5_p{p}_riga"] = (CURL, p, 256, 5)
     if name not in table:
         raise RqError(2, f"unknown config {name!r}")
     return assemble(*table[name])

@@ -65,10 +65,37 @@ def test_supports_and_mask_match_reference(kind, p, ne, L):
     ("cfg1", 2244, 2112, 61628),
     ("cfg2_iga", 8844, 8580, 581976),
     ("cfg2_riga", 10804, 10512, 669308),
+    ("cfg3_iga", 34584, 34060, 4195068),
+    ("cfg3_riga", 42340, 41760, 4782956),
+    ("cfg4_iga", 529420, 527364, 37227480),
+    ("cfg4_riga", 595140, 592960, 40271308),
+    ("cfg5_p2_iga", 132612, 131584, 4048380),
+    ("cfg5_p2_riga", 132612, 131584, 4048380),  # p = 2: rIGA == IGA (App. B D4)
 ])
 def test_config_sizes(name, nfull, nfree, nnz):
     P = rq.baseline_config(name)
     assert (P.n_full, P.n, P.nnz) == (nfull, nfree, nnz)
+
+
+# SURVEY.md App. A (cfg5 = BASELINE configs[4], H(curl) 256^2, p = 2..5): N
+# exact; pattern nnz, nnz(L), F_LU as printed there (3 / 3 / 2 significant
+# digits); the largest front exact.
+@pytest.mark.parametrize("name,nfull,nfree,nnz,nnzl,flu,maxf", [
+    ("cfg5_p3_iga", 133644, 132612, 9.31e6, 51.9e6, 7.5e10, 1926),
+    ("cfg5_p3_riga", 167620, 166464, 10.86e6, 33.2e6, 2.6e10, 1297),
+    ("cfg5_p4_iga", 134680, 133644, 16.7e6, 86.1e6, 2.0e11, 2703),
+    ("cfg5_p4_riga", 206724, 205440, 22.1e6, 46.2e6, 3.7e10, 1441),
+    ("cfg5_p5_iga", 135720, 134680, 26.3e6, 128.2e6, 4.0e11, 3484),
+    ("cfg5_p5_riga", 249924, 248512, 38.9e6, 62.6e6, 5.3e10, 1585),
+])
+def test_cfg5_sweep_sizes_and_symbolic(name, nfull, nfree, nnz, nnzl, flu, maxf):
+    P = rq.baseline_config(name)
+    assert (P.n_full, P.n) == (nfull, nfree)
+    assert abs(P.nnz - nnz) <= 0.005 * nnz
+    st = rq.nested_dissection_order(P).stats
+    assert abs(st["nnz_l"] - nnzl) <= 0.0051 * nnzl
+    assert abs(st["flops_lu"] - flu) <= 0.051 * flu
+    assert st["max_front"] == maxf
 
 
 def test_p2_riga_equals_iga():
