@@ -348,54 +348,63 @@ CMat triangular_eigvecs(const CMat& T) {
 }
 
 int real_basis(const CMat& Z, int p, std::vector<double>& Q) {
-  const int n = Z.n;
-  std::vector<std::vector<double>> cols;
-  cols.reserve(2 * p);
-  for (int j = 0; j < p; ++j) {
-    std::vector<double> re(n), im(n);
-    for (int i = 0; i < n; ++i) re[i] = Z(i, j).real(), im[i] = Z(i, j).imag();
-    cols.push_back(std::move(re));
-    cols.push_back(std::move(im));
-  }
+  // Column-pivoted Gram-Schmidt over the 2p candidates {Re z_j, Im z_j}: the
+  // candidate of largest remaining norm is taken, re-orthogonalised once more
+  // against the basis (every candidate is deflated against each new basis
+  // vector as it is accepted, so with the extra pass this is CGS2), and the
+  // remaining norms are downdated (recomputed once they lost 90% of their
+  // last exact value).
+  const int n = Z.n, nc = 2 * p;
+  std::vector<double> C(static_cast<size_t>(n) * nc);
+  for (int j = 0; j < p; ++j)
+    for (int i = 0; i < n; ++i) {
+      C[i + static_cast<size_t>(2 * j) * n] = Z(i, j).real();
+      C[i + static_cast<size_t>(2 * j + 1) * n] = Z(i, j).imag();
+    }
+  auto col = [&](int j) { return C.data() + static_cast<size_t>(j) * n; };
+  auto nrm2 = [&](const double* x) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += x[i] * x[i];
+    return s;
+  };
   Q.assign(static_cast<size_t>(n) * p, 0.0);
-  std::vector<char> used(cols.size(), 0);
-  int rank = 0;
+  std::vector<char> used(nc, 0);
+  std::vector<double> nrm(nc), nrm_ref(nc);
   double maxn0 = 0.0;
-  for (auto& c : cols) {
-    double s = 0;
-    for (double x : c) s += x * x;
-    maxn0 = std::max(maxn0, std::sqrt(s));
+  for (int j = 0; j < nc; ++j) {
+    nrm[j] = nrm_ref[j] = nrm2(col(j));
+    maxn0 = std::max(maxn0, std::sqrt(nrm[j]));
   }
+  std::vector<double> q(n);
+  int rank = 0;
   while (rank < p) {
     int best = -1;
     double bn = 0.0;
-    for (size_t j = 0; j < cols.size(); ++j) {
-      if (used[j]) continue;
-      double s = 0;
-      for (double x : cols[j]) s += x * x;
-      if (s > bn) bn = s, best = static_cast<int>(j);
-    }
+    for (int j = 0; j < nc; ++j)
+      if (!used[j] && nrm[j] > bn) bn = nrm[j], best = j;
     if (best < 0 || std::sqrt(bn) <= 1e-10 * maxn0) break;
     used[best] = 1;
-    std::vector<double> q = cols[best];
-    for (int pass = 0; pass < 2; ++pass)
-      for (int r = 0; r < rank; ++r) {
-        double d = 0;
-        for (int i = 0; i < n; ++i) d += Q[i + static_cast<size_t>(r) * n] * q[i];
-        for (int i = 0; i < n; ++i) q[i] -= d * Q[i + static_cast<size_t>(r) * n];
-      }
-    double s = 0;
-    for (double x : q) s += x * x;
-    s = std::sqrt(s);
-    if (s <= 1e-12 * maxn0) continue;
-    for (int i = 0; i < n; ++i) Q[i + static_cast<size_t>(rank) * n] = q[i] / s;
-    ++rank;
-    // deflate remaining candidates
-    for (size_t j = 0; j < cols.size(); ++j) {
-      if (used[j]) continue;
+    std::copy(col(best), col(best) + n, q.begin());
+    for (int r = 0; r < rank; ++r) {  // second Gram-Schmidt pass
+      const double* qr = Q.data() + static_cast<size_t>(r) * n;
       double d = 0;
-      for (int i = 0; i < n; ++i) d += Q[i + static_cast<size_t>(rank - 1) * n] * cols[j][i];
-      for (int i = 0; i < n; ++i) cols[j][i] -= d * Q[i + static_cast<size_t>(rank - 1) * n];
+      for (int i = 0; i < n; ++i) d += qr[i] * q[i];
+      for (int i = 0; i < n; ++i) q[i] -= d * qr[i];
+    }
+    double s = std::sqrt(nrm2(q.data()));
+    if (s <= 1e-12 * maxn0) continue;
+    double* qn = Q.data() + static_cast<size_t>(rank) * n;
+    for (int i = 0; i < n; ++i) qn[i] = q[i] / s;
+    ++rank;
+    // deflate the remaining candidates, downdate their norms
+    for (int j = 0; j < nc; ++j) {
+      if (used[j]) continue;
+      double* cj = col(j);
+      double d = 0;
+      for (int i = 0; i < n; ++i) d += qn[i] * cj[i];
+      for (int i = 0; i < n; ++i) cj[i] -= d * qn[i];
+      nrm[j] -= d * d;
+      if (nrm[j] <= 0.1 * nrm_ref[j]) nrm[j] = nrm_ref[j] = nrm2(cj);
     }
   }
   return rank;

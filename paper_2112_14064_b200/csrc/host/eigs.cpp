@@ -121,7 +121,6 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   double* BV = dBV.as<double>();
   double* BV2 = dBV2.as<double>();
   double* r = dR.as<double>();
-  double* w = dW.as<double>();
 
   cudaEvent_t e_a, e_b;
   cuda_check(cudaEventCreate(&e_a), "event");
@@ -479,29 +478,40 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     if (rank < p) p = rank;
     if (p <= 0) fail(errc::solver, "Krylov-Schur restart lost its basis");
     // T_p = Q_p^T H_m Q_p, b_p = beta_m e_m^T Q_p
+    // (column-oriented loops: every inner loop is a contiguous axpy / dot)
     std::vector<double> HQ(static_cast<size_t>(m) * p, 0.0), Tp(static_cast<size_t>(p) * p, 0.0);
-    for (int c = 0; c < p; ++c)
+    for (int c = 0; c < p; ++c) {
+      double* hq = HQ.data() + static_cast<size_t>(c) * m;
       for (int t = 0; t < m; ++t) {
         const double q = Qp[t + static_cast<size_t>(c) * m];
         if (q == 0.0) continue;
-        for (int i = 0; i < m; ++i) HQ[i + static_cast<size_t>(c) * m] += Hm[i + static_cast<size_t>(t) * m] * q;
+        const double* ht = Hm.data() + static_cast<size_t>(t) * m;
+        for (int i = 0; i < m; ++i) hq[i] += ht[i] * q;
       }
-    for (int c = 0; c < p; ++c)
+    }
+    for (int c = 0; c < p; ++c) {
+      const double* hq = HQ.data() + static_cast<size_t>(c) * m;
       for (int i = 0; i < p; ++i) {
+        const double* qi = Qp.data() + static_cast<size_t>(i) * m;
         double s = 0;
-        for (int t = 0; t < m; ++t) s += Qp[t + static_cast<size_t>(i) * m] * HQ[t + static_cast<size_t>(c) * m];
+        for (int t = 0; t < m; ++t) s += qi[t] * hq[t];
         Tp[i + static_cast<size_t>(c) * p] = s;
       }
+    }
     {
       // invariance defect ||H Q_p - Q_p T_p|| / ||H|| (exact restart needs ~eps)
       double dmax = 0, hmax = 0;
       for (double x : Hm) hmax = std::max(hmax, std::fabs(x));
-      for (int c = 0; c < p; ++c)
-        for (int i = 0; i < m; ++i) {
-          double s = HQ[i + static_cast<size_t>(c) * m];
-          for (int t = 0; t < p; ++t) s -= Qp[i + static_cast<size_t>(t) * m] * Tp[t + static_cast<size_t>(c) * p];
-          dmax = std::max(dmax, std::fabs(s));
+      std::vector<double> rc(m);
+      for (int c = 0; c < p; ++c) {
+        std::copy(HQ.begin() + static_cast<size_t>(c) * m, HQ.begin() + static_cast<size_t>(c + 1) * m, rc.begin());
+        for (int t = 0; t < p; ++t) {
+          const double tc = Tp[t + static_cast<size_t>(c) * p];
+          const double* qt = Qp.data() + static_cast<size_t>(t) * m;
+          for (int i = 0; i < m; ++i) rc[i] -= tc * qt[i];
         }
+        for (int i = 0; i < m; ++i) dmax = std::max(dmax, std::fabs(rc[i]));
+      }
       res.max_restart_defect = std::max(res.max_restart_defect, dmax / std::max(hmax, 1e-300));
     }
     cuda_check(cudaMemcpyAsync(dQ.p, Qp.data(), sizeof(double) * m * p, cudaMemcpyHostToDevice, st), "H2D Q");
