@@ -142,34 +142,80 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 __device__ void extend_add(const DagArgs& A, const FrontDev& F, const int* lo, const int* hi,
                            double* dst, int64_t ldd, bool dst_global) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kW = kDT / 32;
   for (int ch = 0; ch < F.nchild; ++ch) {
     const FrontDev C = A.fronts[ch == 0 ? F.child0 : F.child1];
     const int32_t* rel = A.rel + C.rel_off;
     const int ncb = C.nf - C.npiv;
     const double* cp = A.pool + C.off + C.npiv + (int64_t)C.npiv * C.ld;  // CB block origin
-    for (int ic = lo[ch] + warp; ic < hi[ch]; ic += kDT / 32) {
-      const int pc = __ldg(&rel[ic]);
-      const double* src = cp + (int64_t)ic * C.ld;
-      double* dcol = dst + (int64_t)pc * ldd;
-      for (int k0 = 0; k0 < ncb; k0 += 128) {
-        int pr[4];
-        double v[4], d[4];
+    if (ncb <= 128) {
+      // the child's row map is the same for every column: load it once; two
+      // columns per warp iteration keep eight child loads in flight per lane
+      int pr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kk = lane + 32 * u;
+        pr[u] = kk < ncb ? __ldg(&rel[kk]) : -1;
+      }
+      for (int ic = lo[ch] + warp; ic < hi[ch]; ic += 2 * kW) {
+        const int ic2 = ic + kW;
+        const bool two = ic2 < hi[ch];
+        const int pc1 = __ldg(&rel[ic]), pc2 = two ? __ldg(&rel[ic2]) : pc1;
+        const double* s1 = cp + (int64_t)ic * C.ld;
+        const double* s2 = cp + (int64_t)(two ? ic2 : ic) * C.ld;
+        double v1[4], v2[4], d1[4], d2[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int kk = k0 + lane + 32 * u;
-          pr[u] = kk < ncb ? __ldg(&rel[kk]) : -1;
-          v[u] = kk < ncb ? __ldcg(&src[kk]) : 0.0;
+          v1[u] = pr[u] >= 0 ? __ldcg(&s1[lane + 32 * u]) : 0.0;
+          v2[u] = (two && pr[u] >= 0) ? __ldcg(&s2[lane + 32 * u]) : 0.0;
         }
+        double* dc1 = dst + (int64_t)pc1 * ldd;
+        double* dc2 = dst + (int64_t)pc2 * ldd;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (pr[u] >= 0) d[u] = dst_global ? __ldcg(&dcol[pr[u]]) : dcol[pr[u]];
+          if (pr[u] >= 0) {
+            d1[u] = dst_global ? __ldcg(&dc1[pr[u]]) : dc1[pr[u]];
+            if (two) d2[u] = dst_global ? __ldcg(&dc2[pr[u]]) : dc2[pr[u]];
+          }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (pr[u] >= 0) dcol[pr[u]] = d[u] + v[u];
+          if (pr[u] >= 0) {
+            dc1[pr[u]] = d1[u] + v1[u];
+            if (two) dc2[pr[u]] = d2[u] + v2[u];
+          }
+      }
+    } else {
+      for (int ic = lo[ch] + warp; ic < hi[ch]; ic += kW) {
+        const int pc = __ldg(&rel[ic]);
+        const double* src = cp + (int64_t)ic * C.ld;
+        double* dcol = dst + (int64_t)pc * ldd;
+        for (int k0 = 0; k0 < ncb; k0 += 128) {
+          int pr[4];
+          double v[4], d[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int kk = k0 + lane + 32 * u;
+            pr[u] = kk < ncb ? __ldg(&rel[kk]) : -1;
+            v[u] = kk < ncb ? __ldcg(&src[kk]) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (pr[u] >= 0) d[u] = dst_global ? __ldcg(&dcol[pr[u]]) : dcol[pr[u]];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (pr[u] >= 0) dcol[pr[u]] = d[u] + v[u];
+        }
       }
     }
     __syncthreads();  // two children may touch the same entries
   }
+}
+
+// asynchronous 8-byte global -> shared copy (L1-allocating: the front's
+// region was written by the scatter kernel, never read before in this launch)
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -177,8 +223,10 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
   const int nf = F.nf, np = F.npiv, lds = nf | 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* g = A.pool + F.off;
+  // the whole front in flight at once (no register staging, one latency)
   for (int c = warp; c < nf; c += kDT / 32)
-    for (int r = lane; r < nf; r += 32) sm[r + c * lds] = __ldcg(&g[r + (int64_t)c * F.ld]);
+    for (int r = lane; r < nf; r += 32) cp_async8(&sm[r + c * lds], &g[r + (int64_t)c * F.ld]);
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   {
     int lo[2] = {0, 0}, hi[2] = {0, 0};
