@@ -846,10 +846,24 @@ __global__ void __launch_bounds__(kDT, kDagOcc) factor_dag_kernel(DagArgs A) {
       case T_UPD: upd_task(A, F, T.step, T.a, T.b, sm); break;
     }
     __syncthreads();
+    if (A.trace && tid == 0) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+      A.trace[2 * (size_t)A.ntasks + 2 * (size_t)t] = gt;  // work done
+    }
     if (tid == 0) __threadfence();
     __syncthreads();
+    if (A.trace && tid == 0) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+      A.trace[2 * (size_t)A.ntasks + 2 * (size_t)t + 1] = gt;  // fence done
+    }
     // ---- successors
     const int steps = (F.npiv + kNB - 1) / kNB;
+    // tasks that never redo data after this point count towards front
+    // completion right away (overlaps the round trip with the notifications)
+    const bool early_done = T.type == T_SMALL || T.type == T_ASM || T.type == T_UPD;
+    if (early_done && tid == 32) done_s = (atomicAdd(&cnt[0], 1) + 1 == D.ntasks);
     if (T.type == T_DIAG || T.type == T_ROWS || T.type == T_COLS) {
       if (T.type == T_DIAG) {
         const int a0 = a0_of(F, T.step);
@@ -864,10 +878,12 @@ __global__ void __launch_bounds__(kDT, kDagOcc) factor_dag_kernel(DagArgs A) {
         if (tid == 0) __threadfence();
         __syncthreads();
         const unsigned long long bits = atomicAdd(&A.flagbits[D.flag_off + T.step], 0ull);
-        if (!(__longlong_as_double((long long)bits) <= kLmax)) panel_fallback(A, F, D, T.step, sm);
-        __syncthreads();
-        if (tid == 0) __threadfence();
-        __syncthreads();
+        if (!(__longlong_as_double((long long)bits) <= kLmax)) {
+          panel_fallback(A, F, D, T.step, sm);
+          __syncthreads();
+          if (tid == 0) __threadfence();  // publish the redone panel before releasing the updates
+          __syncthreads();
+        }
         const int a0 = a0_of(F, T.step), nr = D.tiles - a0;
         // lookahead first: the next panel's tile row and column, then the bulk
         for (int x = tid; x < 2 * nr - 1; x += kDT) {
@@ -894,7 +910,7 @@ __global__ void __launch_bounds__(kDT, kDagOcc) factor_dag_kernel(DagArgs A) {
       if (tid == 0 && steps > 0) notify(A, idx_diag(A, D, 0));
     }
     // front completion releases the parent's SMALL / ASM tasks
-    if (tid == 0) done_s = (atomicAdd(&cnt[0], 1) + 1 == D.ntasks);
+    if (!early_done && tid == 0) done_s = (atomicAdd(&cnt[0], 1) + 1 == D.ntasks);
     __syncthreads();
     if (done_s && D.parent >= 0) {
       const FrontDag PD = A.dag[D.parent];
@@ -1050,7 +1066,7 @@ void rqb_dag_build(FactorEngine& fe) {
   const size_t small_smem = sizeof(double) * static_cast<size_t>(max_small | 1) * max_small;
   const size_t tile_smem = sizeof(double) * 2 * kNB * kTSP;
   const size_t rows_smem = sizeof(double) * ((kTile + 1) * kNB + kNB * kNB + 64);
-  const size_t diag_smem = sizeof(double) * (3 * 32 * 33 + 64);
+  const size_t diag_smem = sizeof(double) * (3 * 32 * 33 + 128);
   P->smem = std::max({small_smem, tile_smem, rows_smem, diag_smem, size_t(16 * 1024)});
   RQB_CUDA(cudaFuncSetAttribute(factor_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(P->smem)));
@@ -1100,7 +1116,7 @@ void rqb_dag_enqueue(FactorEngine& fe) {
     RQB_CUDA(cudaMemsetAsync(P.d_prof.p, 0, P.d_prof.bytes, fe.stream));
     A.prof = P.d_prof.as<unsigned long long>();
     if (std::getenv("RQB_DAG_TRACE")) {
-      if (!P.d_trace.p) P.d_trace.alloc(sizeof(unsigned long long) * 2 * P.ntasks);
+      if (!P.d_trace.p) P.d_trace.alloc(sizeof(unsigned long long) * 4 * P.ntasks);
       A.trace = P.d_trace.as<unsigned long long>();
     }
   }
@@ -1131,7 +1147,7 @@ void rqb_dag_profile(FactorEngine& fe, double* out) {
   for (int i = 21; i < 24; ++i) out[i] = h[i] / (clk_khz * 1.0);  // DIAG phases (LU, inv L, inv U)
   if (const char* path = std::getenv("RQB_DAG_TRACE")) {  // development trace: tasks + timestamps
     DagPlan& P = *fe.dag;
-    std::vector<unsigned long long> tr(2 * static_cast<size_t>(P.ntasks));
+    std::vector<unsigned long long> tr(4 * static_cast<size_t>(P.ntasks));
     std::vector<Task> tk(P.ntasks);
     RQB_CUDA(cudaMemcpy(tr.data(), P.d_trace.p, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost));
     RQB_CUDA(cudaMemcpy(tk.data(), P.d_tasks.p, sizeof(Task) * tk.size(), cudaMemcpyDeviceToHost));

@@ -18,8 +18,12 @@ _lib.check(_lib.lib.rq_factor_dag_profile(f._h, prof))
 raw = open(out, "rb").read()
 nt = int(np.frombuffer(raw, np.int32, 1, 0)[0])
 tk = np.frombuffer(raw, np.dtype([("front", "<i4"), ("type", "<i2"), ("step", "<i2"), ("a", "<i4"), ("b", "<i4")]), nt, 4)
-tr = np.frombuffer(raw, np.uint64, 2 * nt, 4 + 16 * nt).reshape(-1, 2).astype(np.int64)
-tr -= tr[:, 0].min()
+allt = np.frombuffer(raw, np.uint64, 4 * nt, 4 + 16 * nt).astype(np.int64)
+tr = allt[:2 * nt].reshape(-1, 2).copy()
+ph = allt[2 * nt:].reshape(-1, 2).copy()  # {work done, fence done}
+t00 = tr[:, 0].min()
+tr -= t00
+ph -= t00
 names = ["SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD"]
 nfr = len(o.parent)
 fs = np.full(nfr, 1 << 62); fe = np.zeros(nfr, np.int64)
@@ -49,4 +53,4 @@ if len(sys.argv) > 2:  # task list of one front
     idx = np.nonzero(tk["front"] == ff)[0]
     idx = idx[np.argsort(tr[idx, 0])]
     for i in idx[:200]:
-        print(f"     {names[tk['type'][i]]:5s} s{tk['step'][i]:3d} a{tk['a'][i]:3d} b{tk['b'][i]:3d}  {tr[i,0]/1e3:8.2f} -> {tr[i,1]/1e3:8.2f}  ({(tr[i,1]-tr[i,0])/1e3:6.2f})")
+        print(f"     {names[tk['type'][i]]:5s} s{tk['step'][i]:3d} a{tk['a'][i]:3d} b{tk['b'][i]:3d}  {tr[i,0]/1e3:8.2f} -> {tr[i,1]/1e3:8.2f}  ({(tr[i,1]-tr[i,0])/1e3:6.2f})  work {(ph[i,0]-tr[i,0])/1e3:6.2f} fence {(ph[i,1]-ph[i,0])/1e3:6.2f} succ {(tr[i,1]-ph[i,1])/1e3:6.2f}")
