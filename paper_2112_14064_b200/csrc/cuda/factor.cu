@@ -742,6 +742,8 @@ void FactorEngine::factor() {
   RQB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
   last_ms = ms;
   last_swaps = flags[1];
+  if (flags[2])
+    fail(errc::solver, std::string("factorization task DAG stalled (watchdog): ") + rqb_dag_stall_report(*this));
   if (flags[0]) fail(errc::singular, "Q(sigma) is numerically singular: every pivot candidate below 1e-300");
 }
 

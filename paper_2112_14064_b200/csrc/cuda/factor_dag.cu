@@ -51,14 +51,15 @@ constexpr int kTile = 64;         // big-front tile edge
 constexpr int kTSP = kTile + 4;   // padded smem stride of DMMA operand tiles
 constexpr double kLmax = 10.0 * (1.0 - 1e-14);  // 1/threshold, conservative
 constexpr int kCnt = 5;  // per-front counters: tasks, asm, diag, rc, released
-#ifndef RQB_DAG_OCC
-#define RQB_DAG_OCC 1
-#endif
-#ifndef RQB_DAG_SMALL_NF
-#define RQB_DAG_SMALL_NF 160
-#endif
-constexpr int kDagOcc = RQB_DAG_OCC;           // resident CTAs per SM the register budget targets
-constexpr int kDagSmallNf = RQB_DAG_SMALL_NF;  // SMALL tasks: whole front in shared memory up to this nf
+// Two configurations of the persistent kernel, chosen per factorization
+// (rqb_dag_build): small problems are critical-path bound and want big SMALL
+// fronts (nf <= 160 factored whole in 206 KB of shared memory, one CTA per
+// SM); large problems are throughput bound and want two CTAs per SM (task
+// latency of one hidden behind the other: 113 KB of shared memory and 128
+// registers each, SMALL fronts up to nf = 118).
+constexpr int kSmallNfLatency = 160;
+constexpr int kSmallNfThroughput = 118;
+constexpr double kThroughputFlops = 2e9;  // F_LU above which the two-CTA variant is used
 
 enum : int16_t { T_SMALL = 0, T_ASM = 1, T_DIAG = 2, T_ROWS = 3, T_COLS = 4, T_UPD = 5 };
 
@@ -100,7 +101,8 @@ struct DagArgs {
   int* tile_step;
   const int32_t* rc_prefix;
   unsigned long long* flagbits;
-  int* flags;   // [0] singular, [1] swaps
+  int* flags;   // [0] singular, [1] swaps, [2] stall watchdog (1 queue, 2 fallback wait)
+  int small_nf; // SMALL threshold of this plan (stride of the per-CTA panel backup)
   unsigned long long* prof;  // optional: per task type {work cycles, wait cycles, count}
   unsigned long long* trace; // optional (RQB_DAG_TRACE): per task {start, end} globaltimer ns
   double* small_backup;      // per CTA: 160 x 16 panel backup of the SMALL path
@@ -110,9 +112,27 @@ struct DagArgs {
   const int32_t* step_base;  // FrontDag::sb_off: first task of every panel step
 };
 
-__device__ __forceinline__ void spin_ge(const int* p, int target) {
-  if (*((volatile const int*)p) >= target) return;
-  while (*((volatile const int*)p) < target) __nanosleep(64);
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin waits give up after kStallNs (a dependency that never resolves is a
+// bug): the watchdog flag makes every CTA leave and the host reports a stall
+// instead of hanging the device.
+constexpr unsigned long long kStallNs = 4000000000ull;
+
+__device__ __forceinline__ bool spin_ge(const int* p, int target, int* flags) {
+  if (*((volatile const int*)p) >= target) return true;
+  const unsigned long long t0 = gtimer();
+  while (*((volatile const int*)p) < target) {
+    __nanosleep(64);
+    if (gtimer() - t0 > kStallNs || *((volatile int*)&flags[2])) {
+      atomicCAS(&flags[2], 0, 2);
+      return false;
+    }
+  }
+  return true;
 }
 
 __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
@@ -237,7 +257,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
   __shared__ double red_s[kDT / 32];
   __shared__ double urow_s[2][kPB];
   __shared__ int any_swap_s;
-  double* pbk = A.small_backup + (int64_t)blockIdx.x * kDagSmallNf * kPB;
+  double* pbk = A.small_backup + (int64_t)blockIdx.x * A.small_nf * kPB;
   for (int k0 = 0; k0 < np; k0 += kPB) {
     const int pw = min(kPB, np - k0);
     // ---- speculative unpivoted panel: thread t owns row t in registers; the
@@ -253,7 +273,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
       if (own)
 #pragma unroll
         for (int c = 0; c < kPB; ++c)
-          if (c < pw) pbk[i + c * kDagSmallNf] = a[c];
+          if (c < pw) pbk[i + c * A.small_nf] = a[c];
 #pragma unroll
       for (int jj = 0; jj < kPB; ++jj) {
         if (jj < pw) {
@@ -295,7 +315,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
     } else {
       // restore the panel, redo it with exact threshold pivoting (warp 0)
       if (tid < nf && tid >= k0)
-        for (int c = 0; c < pw; ++c) sm[tid + (k0 + c) * lds] = pbk[tid + c * kDagSmallNf];
+        for (int c = 0; c < pw; ++c) sm[tid + (k0 + c) * lds] = pbk[tid + c * A.small_nf];
       __syncthreads();
       if (tid == 0) any_swap_s = 1;
     }
@@ -688,7 +708,7 @@ __device__ void panel_fallback(const DagArgs& A, const FrontDev& F, const FrontD
   if (tid == 0) {
     const int a0 = k / kTile;
     for (int a = a0; a < D.tiles; ++a)
-      for (int b = a0; b < D.tiles; ++b) spin_ge(&A.tile_step[D.tile_off + a * D.tiles + b], s);
+      for (int b = a0; b < D.tiles; ++b) spin_ge(&A.tile_step[D.tile_off + a * D.tiles + b], s, A.flags);
     __threadfence();
   }
   __syncthreads();
@@ -761,6 +781,13 @@ __device__ __forceinline__ int a0_of(const FrontDev& F, int s) {
   return (k + w) / kTile;
 }
 
+// trailing tile rows/cols of step s (0 when the panel ends the front: npiv ==
+// nf), identical to the host's task layout in rqb_dag_build
+__device__ __forceinline__ int nr_of(const FrontDev& F, const FrontDag& D, int s) {
+  const int k = s * kNB, t0 = k + min(kNB, F.npiv - k);
+  return t0 < F.nf ? D.tiles - t0 / kTile : 0;
+}
+
 __device__ __forceinline__ int idx_diag(const DagArgs& A, const FrontDag& D, int s) {
   return A.step_base[D.sb_off + s];
 }
@@ -771,11 +798,11 @@ __device__ __forceinline__ int idx_rows(const DagArgs& A, const FrontDag& D, con
 __device__ __forceinline__ int idx_cols(const DagArgs& A, const FrontDag& D, const FrontDev& F, int s,
                                          int b) {
   const int a0 = a0_of(F, s);
-  return A.step_base[D.sb_off + s] + 1 + (D.tiles - a0) + (b - a0);
+  return A.step_base[D.sb_off + s] + 1 + nr_of(F, D, s) + (b - a0);
 }
 __device__ __forceinline__ int idx_upd(const DagArgs& A, const FrontDag& D, const FrontDev& F, int s, int a,
                                         int b) {
-  const int a0 = a0_of(F, s), nr = D.tiles - a0;
+  const int a0 = a0_of(F, s), nr = nr_of(F, D, s);
   return A.step_base[D.sb_off + s] + 1 + 2 * nr + (a - a0) * nr + (b - a0);
 }
 
@@ -795,12 +822,23 @@ __device__ int pop_task(const DagArgs& A) {
   if (h >= A.ntasks) return -1;
   volatile int* q = A.queue;
   int t;
-  while ((t = q[h]) < 0) __nanosleep(32);
+  if ((t = q[h]) < 0) {
+    const unsigned long long t0 = gtimer();
+    while ((t = q[h]) < 0) {
+      __nanosleep(32);
+      if (*((volatile int*)&A.flags[2])) return -1;
+      if (gtimer() - t0 > kStallNs) {
+        atomicCAS(&A.flags[2], 0, 1);
+        return -1;
+      }
+    }
+  }
   __threadfence();
   return t;
 }
 
-__global__ void __launch_bounds__(kDT, kDagOcc) factor_dag_kernel(DagArgs A) {
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) {
   extern __shared__ double sm[];
   __shared__ int task_s, last_s, done_s;
   __shared__ int piv_sh[kPB];
@@ -866,8 +904,8 @@ __global__ void __launch_bounds__(kDT, kDagOcc) factor_dag_kernel(DagArgs A) {
     if (early_done && tid == 32) done_s = (atomicAdd(&cnt[0], 1) + 1 == D.ntasks);
     if (T.type == T_DIAG || T.type == T_ROWS || T.type == T_COLS) {
       if (T.type == T_DIAG) {
-        const int a0 = a0_of(F, T.step);
-        for (int x = a0 + tid; x < D.tiles; x += kDT) {
+        const int a0 = a0_of(F, T.step), nr = nr_of(F, D, T.step);
+        for (int x = a0 + tid; x < a0 + nr; x += kDT) {
           notify(A, idx_rows(A, D, F, T.step, x));
           notify(A, idx_cols(A, D, F, T.step, x));
         }
@@ -884,14 +922,14 @@ __global__ void __launch_bounds__(kDT, kDagOcc) factor_dag_kernel(DagArgs A) {
           if (tid == 0) __threadfence();  // publish the redone panel before releasing the updates
           __syncthreads();
         }
-        const int a0 = a0_of(F, T.step), nr = D.tiles - a0;
+        const int a0 = a0_of(F, T.step), nr = nr_of(F, D, T.step);
         // lookahead first: the next panel's tile row and column, then the bulk
         for (int x = tid; x < 2 * nr - 1; x += kDT) {
           const int ua = x < nr ? a0 : a0 + (x - nr + 1), ub = x < nr ? a0 + x : a0;
           notify(A, idx_upd(A, D, F, T.step, ua, ub));
         }
         __syncthreads();
-        for (int x = tid; x < (nr - 1) * (nr - 1); x += kDT)
+        for (int x = tid; x < (nr > 1 ? (nr - 1) * (nr - 1) : 0); x += kDT)
           notify(A, idx_upd(A, D, F, T.step, a0 + 1 + x / (nr - 1), a0 + 1 + x % (nr - 1)));
       }
     } else if (T.type == T_UPD) {
@@ -900,10 +938,11 @@ __global__ void __launch_bounds__(kDT, kDagOcc) factor_dag_kernel(DagArgs A) {
         const int s1 = T.step + 1;
         if (s1 < steps) {
           const int a1 = a0_of(F, s1), an = (s1 * kNB) / kTile;
-          if (T.a >= a1 && T.b >= a1) notify(A, idx_upd(A, D, F, s1, T.a, T.b));
+          const bool trail = nr_of(F, D, s1) > 0;  // step s1 has trailing rows / columns
+          if (trail && T.a >= a1 && T.b >= a1) notify(A, idx_upd(A, D, F, s1, T.a, T.b));
           if (T.a == an && T.b == an) notify(A, idx_diag(A, D, s1));
-          if (T.b == an && T.a >= a1) notify(A, idx_rows(A, D, F, s1, T.a));
-          if (T.a == an && T.b >= a1) notify(A, idx_cols(A, D, F, s1, T.b));
+          if (trail && T.b == an && T.a >= a1) notify(A, idx_rows(A, D, F, s1, T.a));
+          if (trail && T.a == an && T.b >= a1) notify(A, idx_cols(A, D, F, s1, T.b));
         }
       }
     } else if (T.type == T_ASM) {
@@ -941,6 +980,7 @@ struct DagPlan {
   DeviceBuffer d_tasks, d_dag, d_cnt, d_tile, d_rc, d_flagbits, d_backup, d_prof, d_bnd,
       d_small_backup, d_deps0, d_deps, d_queue0, d_queue, d_qctl, d_qctl0, d_sb, d_trace;
   int ntasks = 0, nfronts = 0, ntile = 0, nflag = 0, grid = 148, nready = 0;
+  int occ = 1, small_nf = 160;  // kernel variant (see kSmallNfLatency / kSmallNfThroughput)
   size_t smem = 0;
   double flops_upd = 0;
 };
@@ -955,6 +995,10 @@ void rqb_dag_build(FactorEngine& fe) {
   int tile_off = 0, flag_off = 0, slot = 0;
   int64_t backup = 0;
   int max_small = 0;
+  P->occ = S.flops_lu >= kThroughputFlops ? 2 : 1;
+  if (const char* e = std::getenv("RQB_DAG_OCC")) P->occ = std::atoi(e) == 2 ? 2 : 1;
+  const int small_max = P->occ == 2 ? kSmallNfThroughput : kSmallNfLatency;
+  P->small_nf = small_max;
   // tasks of a front are contiguous; fronts in postorder
   for (int f = 0; f < nfr; ++f) {
     const Front& F = S.fronts[f];
@@ -963,7 +1007,7 @@ void rqb_dag_build(FactorEngine& fe) {
     D.slot = -1;
     D.parent = F.parent;
     const int nch = static_cast<int>(F.children.size());
-    if (F.nf <= kDagSmallNf) {
+    if (F.nf <= small_max) {
       tasks.push_back({f, T_SMALL, 0, 0, 0});
       deps.push_back(nch);
       D.ntasks = 1;
@@ -1068,13 +1112,13 @@ void rqb_dag_build(FactorEngine& fe) {
   const size_t rows_smem = sizeof(double) * ((kTile + 1) * kNB + kNB * kNB + 64);
   const size_t diag_smem = sizeof(double) * (3 * 32 * 33 + 128);
   P->smem = std::max({small_smem, tile_smem, rows_smem, diag_smem, size_t(16 * 1024)});
-  RQB_CUDA(cudaFuncSetAttribute(factor_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(P->smem)));
+  auto kern = P->occ == 2 ? factor_dag_kernel<2> : factor_dag_kernel<1>;
+  RQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)));
   int nsm = 148, occ = 1;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
-  RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, factor_dag_kernel, kDT, P->smem));
+  RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDT, P->smem));
   P->grid = std::max(1, std::min(P->ntasks, nsm * std::max(1, occ)));
-  P->d_small_backup.alloc(sizeof(double) * P->grid * kDagSmallNf * kPB);
+  P->d_small_backup.alloc(sizeof(double) * P->grid * P->small_nf * kPB);
   fe.dag_ntasks = P->ntasks;
   fe.dag.reset(P.release());
 }
@@ -1120,7 +1164,11 @@ void rqb_dag_enqueue(FactorEngine& fe) {
       A.trace = P.d_trace.as<unsigned long long>();
     }
   }
-  factor_dag_kernel<<<P.grid, kDT, P.smem, fe.stream>>>(A);
+  A.small_nf = P.small_nf;
+  if (P.occ == 2)
+    factor_dag_kernel<2><<<P.grid, kDT, P.smem, fe.stream>>>(A);
+  else
+    factor_dag_kernel<1><<<P.grid, kDT, P.smem, fe.stream>>>(A);
   RQB_CUDA(cudaGetLastError());
 }
 
@@ -1159,6 +1207,31 @@ void rqb_dag_profile(FactorEngine& fe, double* out) {
       std::fclose(fp);
     }
   }
+}
+
+// After a watchdog stall: the tasks whose dependency counters never reached
+// zero (first few, in task order), for the error message.
+std::string rqb_dag_stall_report(FactorEngine& fe) {
+  DagPlan& P = *fe.dag;
+  std::vector<int32_t> deps(P.ntasks);
+  std::vector<Task> tk(P.ntasks);
+  cudaMemcpy(deps.data(), P.d_deps.p, sizeof(int32_t) * P.ntasks, cudaMemcpyDeviceToHost);
+  cudaMemcpy(tk.data(), P.d_tasks.p, sizeof(Task) * P.ntasks, cudaMemcpyDeviceToHost);
+  static const char* names[] = {"SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD"};
+  std::string out;
+  int shown = 0, pending = 0;
+  for (int t = 0; t < P.ntasks; ++t) {
+    if (deps[t] == 0) continue;
+    ++pending;
+    if (shown < 6) {
+      const Task& T = tk[t];
+      out += std::string(shown ? ", " : "") + names[T.type] + "(front " + std::to_string(T.front) + ", step " +
+             std::to_string(T.step) + ", " + std::to_string(T.a) + "," + std::to_string(T.b) + ") deps=" +
+             std::to_string(deps[t]);
+      ++shown;
+    }
+  }
+  return std::to_string(pending) + " tasks never ready: " + out;
 }
 
 void DagPlanDeleter::operator()(DagPlan* p) const { delete p; }

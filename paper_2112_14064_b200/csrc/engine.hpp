@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "host/common.hpp"
@@ -137,6 +138,7 @@ void rqb_dag_build(FactorEngine& fe);
 void rqb_dag_enqueue(FactorEngine& fe);
 void rqb_dag_profile(FactorEngine& fe, double* out);
 void rqb_rowperm_enqueue(FactorEngine& fe);
+std::string rqb_dag_stall_report(FactorEngine& fe);
 
 // Shift-invert operator on the linearised pencil, real FP64, device resident.
 struct OperatorEngine {
