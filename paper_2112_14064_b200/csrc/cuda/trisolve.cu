@@ -71,6 +71,7 @@ struct SweepArgs {
   double sigma;
   double* xl_out;
   unsigned long long* trace;  // development trace (RQB_SOLVE_TRACE): per item 4 timestamps, SM, ns waited
+  int* stall;                 // watchdog flag (persistent, checked by the host at its sync points)
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -133,15 +134,30 @@ __device__ __forceinline__ void front_ready(const SweepArgs& A, int f) {
   }
 }
 
-__device__ __forceinline__ void wait_ge(const int* p, int target) {
-  while (ld_acquire(p) < target) __nanosleep(20);
+// Spin waits give up after kSweepStallNs (a dependency that never resolves is
+// a bug): the flag is raised, every CTA drains, the host reports the stall.
+constexpr unsigned long long kSweepStallNs = 4000000000ull;
+__device__ __forceinline__ bool stalled(const SweepArgs& A, unsigned long long& t0) {
+  if (*((volatile int*)A.stall)) return true;
+  const unsigned long long t = gtime();
+  if (t0 == 0) t0 = t;
+  if (t - t0 > kSweepStallNs) {
+    atomicExch(A.stall, 1);
+    return true;
+  }
+  return false;
 }
+
 
 __device__ __forceinline__ int pop_item(const SweepArgs& A) {
   const int h = atomicAdd(&A.qctl[0], 1);
   if (h >= A.nitems) return -1;
   int t;
-  while ((t = ld_acquire(&A.queue[h])) < 0) __nanosleep(20);
+  unsigned long long t0 = 0;
+  while ((t = ld_acquire(&A.queue[h])) < 0) {
+    __nanosleep(20);
+    if (stalled(A, t0)) return -1;
+  }
   return t;
 }
 
@@ -248,7 +264,8 @@ __device__ __forceinline__ void red_release(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kST, 3) fwd_sweep(SweepArgs A) {
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
   __shared__ double D[kRB * (kRB + 1)];
   __shared__ double stg[kStage];  // staged y (whole-front items: the front's own y)
   __shared__ double part[4][kRB];
@@ -304,7 +321,14 @@ __global__ void __launch_bounds__(kST, 3) fwd_sweep(SweepArgs A) {
           if (tid == 0) {
             const unsigned long long w0 = A.trace ? gtime() : 0;
             int p;
-            while ((p = ld_acquire(&A.pub[I.front])) * kRB <= done) __nanosleep(20);
+            unsigned long long ts0 = 0;
+            while ((p = ld_acquire(&A.pub[I.front])) * kRB <= done) {
+              __nanosleep(20);
+              if (stalled(A, ts0)) {
+                p = (ncol + kRB - 1) / kRB;  // drain: give up on the dependency
+                break;
+              }
+            }
             avail_s = min(ncol, p * kRB);
             if (A.trace) {
               const unsigned long long w1 = gtime();
@@ -370,7 +394,8 @@ __global__ void __launch_bounds__(kST, 3) fwd_sweep(SweepArgs A) {
   }
 }
 
-__global__ void __launch_bounds__(kST, 3) bwd_sweep(SweepArgs A) {
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
   __shared__ double D[kRB * (kRB + 1)];
   // staged x; whole-front items: [0, np) the front's own x, [kWholeNpb*64, ...) the ancestors' x_cb
   __shared__ double stg[kStage];
@@ -435,7 +460,14 @@ __global__ void __launch_bounds__(kST, 3) bwd_sweep(SweepArgs A) {
           if (tid == 0) {
             const unsigned long long w0 = A.trace ? gtime() : 0;
             int p;
-            while (max(lo, (I.npb - (p = ld_acquire(&A.pub[I.front]))) * kRB) >= done_hi) __nanosleep(20);
+            unsigned long long ts0 = 0;
+            while (max(lo, (I.npb - (p = ld_acquire(&A.pub[I.front]))) * kRB) >= done_hi) {
+              __nanosleep(20);
+              if (stalled(A, ts0)) {
+                p = I.npb;  // drain: give up on the dependency
+                break;
+              }
+            }
             avail_s = max(lo, (I.npb - p) * kRB);
             if (A.trace) {
               const unsigned long long w1 = gtime();
@@ -557,6 +589,16 @@ void FactorEngine::solve_device(const double* b, double* x, double scale_out) {
   rqb_solve_enqueue(*this, b, x, scale_out, nullptr, 0.0, nullptr);
 }
 
+void FactorEngine::check_sweeps() {
+  int st = 0;
+  RQB_CUDA(cudaMemcpyAsync(&st, d_sweep_stall.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  RQB_CUDA(cudaStreamSynchronize(stream));
+  if (st) {
+    RQB_CUDA(cudaMemsetAsync(d_sweep_stall.p, 0, sizeof(int), stream));
+    fail(errc::solver, "triangular sweep stalled (watchdog): a dependency of the solve never resolved");
+  }
+}
+
 void rqb_solve_prepare(FactorEngine& fe) {
   const Symbolic& S = fe.sym;
   const int nfr = static_cast<int>(S.fronts.size());
@@ -609,9 +651,17 @@ void rqb_solve_prepare(FactorEngine& fe) {
     return it;
   };
   {
+    // large trees are throughput bound (3 CTAs/SM, 80 registers); small ones
+    // are latency bound along the tree and prefer 2 CTAs/SM without spills
+    int items = 0;
+    for (int f = 0; f < nfr; ++f) items += npb[f] + ncbb[f];
+    fe.sweep_occ = items >= 10000 ? 3 : 2;
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_sweep, kST, 0);
+    if (fe.sweep_occ == 3)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_sweep<3>, kST, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_sweep<2>, kST, 0);
     fe.solve_grid = std::max(1, nsm * std::max(1, occ));
   }
   // whole-front items only on levels wide enough to keep every CTA busy
@@ -699,6 +749,8 @@ void rqb_solve_prepare(FactorEngine& fe) {
   fe.d_state0.upload(st.data(), sizeof(int32_t) * st.size(), fe.stream);
   fe.d_state.alloc(fe.d_state0.bytes);
   fe.d_rowperm.alloc(sizeof(int32_t) * std::max<int64_t>(1, fe.n));
+  fe.d_sweep_stall.alloc(sizeof(int));
+  RQB_CUDA(cudaMemsetAsync(fe.d_sweep_stall.p, 0, sizeof(int), fe.stream));
 }
 
 void rqb_rowperm_enqueue(FactorEngine& fe) {
@@ -728,6 +780,7 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
   A.trace = trace;
   A.ech = fe.d_ech.as<int32_t>();
   A.gsrc = fe.d_gsrc.as<int4>();
+  A.stall = fe.d_sweep_stall.as<int>();
   A.pool = fe.d_pool.as<double>();
   A.perm = fe.d_perm.as<int32_t>();
   A.rows = fe.d_rows.as<int32_t>();
@@ -752,8 +805,12 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
   F.fbase = fe.d_sf.as<int32_t>();
   F.fcnt = F.fbase + nfr;
   F.npb = fe.d_sf.as<int32_t>() + 4 * nfr;
-  if (fe.n_fwd_items > 0)
-    fwd_sweep<<<std::min(fe.solve_grid, fe.n_fwd_items), kST, 0, st>>>(F);
+  if (fe.n_fwd_items > 0) {
+    if (fe.sweep_occ == 3)
+      fwd_sweep<3><<<std::min(fe.solve_grid, fe.n_fwd_items), kST, 0, st>>>(F);
+    else
+      fwd_sweep<2><<<std::min(fe.solve_grid, fe.n_fwd_items), kST, 0, st>>>(F);
+  }
   SweepArgs B = A;
   B.items = fe.d_items_bwd.as<SolveItem>();
   B.nitems = fe.n_bwd_items;
@@ -767,8 +824,12 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
   B.fbase = fe.d_sf.as<int32_t>() + 2 * nfr;
   B.fcnt = B.fbase + nfr;
   B.npb = B.fcnt;
-  if (fe.n_bwd_items > 0)
-    bwd_sweep<<<std::min(fe.solve_grid, fe.n_bwd_items), kST, 0, st>>>(B);
+  if (fe.n_bwd_items > 0) {
+    if (fe.sweep_occ == 3)
+      bwd_sweep<3><<<std::min(fe.solve_grid, fe.n_bwd_items), kST, 0, st>>>(B);
+    else
+      bwd_sweep<2><<<std::min(fe.solve_grid, fe.n_bwd_items), kST, 0, st>>>(B);
+  }
   RQB_CUDA(cudaGetLastError());
   fe.launches_solve = 2;
   if (trace) {  // development trace: dump forward and backward item timings once per call

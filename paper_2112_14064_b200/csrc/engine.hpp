@@ -100,9 +100,9 @@ struct FactorEngine {
   // dataflow state of the two sweeps in one int32 buffer (template + live
   // copy, reset by one D2D copy per solve): front deps fwd/bwd, ready queues
   // fwd/bwd, {head, tail} x2, per-front published/finished counters
-  DeviceBuffer d_state0, d_state;
+  DeviceBuffer d_state0, d_state, d_sweep_stall;
   int64_t st_dep_fwd = 0, st_dep_bwd = 0, st_q_fwd = 0, st_q_bwd = 0, st_qctl = 0, st_cnt = 0;
-  int n_fwd_items = 0, n_bwd_items = 0, solve_grid = 148;
+  int n_fwd_items = 0, n_bwd_items = 0, solve_grid = 148, sweep_occ = 2;
   std::vector<FrontDev> fronts_h;
   std::vector<LevelPlan> plans;
   int64_t nscratch = 0;
@@ -122,6 +122,8 @@ struct FactorEngine {
   void set_values_device(const double* aval_dev);
   // x = A^{-1} b on device vectors (original ordering), enqueued on `stream`.
   void solve_device(const double* b, double* x, double scale_out = 1.0);
+  // raise errc::solver if a triangular sweep hit its stall watchdog (syncs the stream)
+  void check_sweeps();
   void enqueue_factor(KernelTimer* kt = nullptr);
   // One un-graphed factorization with per-launch events: device ms, launch
   // count and algorithmic work (flops; bytes for classes 0-1) per kernel class.

@@ -272,6 +272,7 @@ int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs) {
                                       fe.stream), "D2H x");
     }
     rqb::cuda_check(cudaStreamSynchronize(fe.stream), "solve sync");
+    fe.check_sweeps();
   });
 }
 
@@ -371,6 +372,7 @@ int rq_operator_apply(rq_operator_t* o, const double* v, double* r) {
     op.apply(o->d_a.as<double>(), o->d_b.as<double>());
     rqb::cuda_check(cudaMemcpyAsync(r, o->d_b.p, sizeof(double) * n2, cudaMemcpyDeviceToHost, op.stream), "D2H");
     rqb::cuda_check(cudaStreamSynchronize(op.stream), "sync");
+    op.fac->check_sweeps();
   });
 }
 

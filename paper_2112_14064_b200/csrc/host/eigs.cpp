@@ -251,6 +251,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       const auto ts0 = now();
       cuda_check(cudaStreamSynchronize(st), "sync");
       t_sync += ms_since(ts0);  // host blocked on the cycle's Arnoldi steps
+      op.fac->check_sweeps();
     }
     for (int j = k; j < m; ++j) {
       for (int i = 0; i <= j; ++i)
