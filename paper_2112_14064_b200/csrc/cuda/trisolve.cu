@@ -50,6 +50,7 @@ struct SweepArgs {
   int* deps;      // per front: unfinished predecessor fronts
   int* queue;
   int* qctl;      // {head, tail}
+  int* done;      // items finished (termination of pop_item)
   int* pub;       // per front: pivot blocks published (forward: first first; backward: last first)
   int* fin;       // per front: forward items finished
   int fwd;        // 1 forward, 0 backward (item layout of front_ready)
@@ -108,29 +109,42 @@ constexpr int kWholeCb = kStage - kWholeNpb * kRB;
 constexpr int kWhole = -2;  // SolveItem::blk of a whole-front item
 
 __device__ __forceinline__ void push_items(const SweepArgs& A, int i0, int n) {
+  if (n <= 0) return;
   const int slot = atomicAdd(&A.qctl[1], n);
   for (int i = 0; i < n; ++i) atomicExch(&A.queue[slot + i], i0 + i);
 }
 
-// push virtual items [v0, v1] of front f (clipped to what exists)
-__device__ __forceinline__ void push_window(const SweepArgs& A, int f, int v0, int v1) {
+// push virtual items [v0, v1] of front f (clipped to what exists); with keep,
+// the first of them is handed to the calling CTA instead (it never waits:
+// nothing of its front precedes it), the rest go on the queue
+__device__ __forceinline__ void push_window(const SweepArgs& A, int f, int v0, int v1, int* keep = nullptr) {
   const int npb = A.npb[f], base = A.fbase[f];
+  int i0, n;
   if (A.fwd) {
     v1 = min(v1, npb);
     if (v0 > v1) return;
     const int end = v1 == npb ? base + A.fcnt[f] : base + v1 + 1;
-    if (base + v0 < end) push_items(A, base + v0, end - base - v0);
+    i0 = base + v0;
+    n = end - i0;
   } else {
     v1 = min(v1, npb - 1);
-    if (v0 <= v1) push_items(A, base + v0, v1 - v0 + 1);
+    i0 = base + v0;
+    n = v1 - v0 + 1;
   }
+  if (n <= 0) return;
+  if (keep) {
+    *keep = i0;
+    ++i0;
+    --n;
+  }
+  push_items(A, i0, n);
 }
 
 // one predecessor front of f finished; the last one opens f's window
-__device__ __forceinline__ void front_ready(const SweepArgs& A, int f) {
+__device__ __forceinline__ void front_ready(const SweepArgs& A, int f, int* keep = nullptr) {
   if (atomicSub(&A.deps[f], 1) == 1) {
     __threadfence();
-    push_window(A, f, 0, kWin - 1);
+    push_window(A, f, 0, kWin - 1, keep);
   }
 }
 
@@ -149,12 +163,16 @@ __device__ __forceinline__ bool stalled(const SweepArgs& A, unsigned long long& 
 }
 
 
+// Claim the next queue slot and wait for it; -1 once every item has finished
+// (items kept by a CTA never pass through the queue, so the last claimed
+// slots stay empty).
 __device__ __forceinline__ int pop_item(const SweepArgs& A) {
   const int h = atomicAdd(&A.qctl[0], 1);
   if (h >= A.nitems) return -1;
   int t;
   unsigned long long t0 = 0;
   while ((t = ld_acquire(&A.queue[h])) < 0) {
+    if (ld_acquire(A.done) >= A.nitems) return -1;
     __nanosleep(20);
     if (stalled(A, t0)) return -1;
   }
@@ -270,11 +288,15 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
   __shared__ double stg[kStage];  // staged y (whole-front items: the front's own y)
   __shared__ double part[4][kRB];
   __shared__ double wv[kRB];
-  __shared__ int item_s, avail_s;
+  __shared__ int item_s, avail_s, keep_s;
   const int tid = threadIdx.x, row = tid & (kRB - 1), grp = tid >> 6;
+  if (tid == 0) keep_s = -1;
   for (;;) {
     __syncthreads();
-    if (tid == 0) item_s = pop_item(A);
+    if (tid == 0) {
+      item_s = keep_s >= 0 ? keep_s : pop_item(A);
+      keep_s = -1;
+    }
     __syncthreads();
     const int it = item_s;
     if (it < 0) return;
@@ -389,7 +411,8 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
       __threadfence();
       RQB_TRACE(3);
       const bool last = whole || atomicAdd(&A.fin[I.front], 1) + 1 == I.npb + I.ncbb;
-      if (last && I.parent >= 0) front_ready(A, I.parent);
+      if (last && I.parent >= 0) front_ready(A, I.parent, &keep_s);  // depth first: run the parent's first item
+      atomicAdd(A.done, 1);
     }
   }
 }
@@ -401,11 +424,15 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
   __shared__ double stg[kStage];
   __shared__ double part[4][kRB];
   __shared__ double rinv[kRB];
-  __shared__ int item_s, avail_s;
+  __shared__ int item_s, avail_s, keep_s;
   const int tid = threadIdx.x, row = tid & (kRB - 1), grp = tid >> 6;
+  if (tid == 0) keep_s = -1;
   for (;;) {
     __syncthreads();
-    if (tid == 0) item_s = pop_item(A);
+    if (tid == 0) {
+      item_s = keep_s >= 0 ? keep_s : pop_item(A);
+      keep_s = -1;
+    }
     __syncthreads();
     const int it = item_s;
     if (it < 0) return;
@@ -534,8 +561,10 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
       }
       RQB_TRACE(3);
     }
-    if (I.blk <= 0)
-      for (int x = tid; x < I.nech; x += kST) front_ready(A, A.ech[I.ech_off + x]);
+    if (I.blk <= 0)  // the first effective child's first item runs here next
+      for (int x = tid; x < I.nech; x += kST) front_ready(A, A.ech[I.ech_off + x], x == 0 ? &keep_s : nullptr);
+    __syncthreads();
+    if (tid == 0) atomicAdd(A.done, 1);
   }
 }
 
@@ -743,7 +772,7 @@ void rqb_solve_prepare(FactorEngine& fe) {
   fe.st_q_bwd = static_cast<int64_t>(st.size());
   st.insert(st.end(), qb.begin(), qb.end());
   fe.st_qctl = static_cast<int64_t>(st.size());
-  st.insert(st.end(), {0, nf0, 0, nb0});
+  st.insert(st.end(), {0, nf0, 0, nb0, 0, 0});  // {head, tail} fwd, bwd; items done fwd, bwd
   fe.st_cnt = static_cast<int64_t>(st.size());  // fwd published, fwd finished, bwd published
   st.resize(st.size() + 3 * static_cast<size_t>(nfr), 0);
   fe.d_state0.upload(st.data(), sizeof(int32_t) * st.size(), fe.stream);
@@ -799,6 +828,7 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
   F.deps = sb + fe.st_dep_fwd;
   F.queue = sb + fe.st_q_fwd;
   F.qctl = sb + fe.st_qctl;
+  F.done = sb + fe.st_qctl + 4;
   F.pub = sb + fe.st_cnt;
   F.fin = sb + fe.st_cnt + nfr;
   F.fwd = 1;
@@ -817,6 +847,7 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
   B.deps = sb + fe.st_dep_bwd;
   B.queue = sb + fe.st_q_bwd;
   B.qctl = sb + fe.st_qctl + 2;
+  B.done = sb + fe.st_qctl + 5;
   B.pub = sb + fe.st_cnt + 2 * nfr;
   B.fin = nullptr;
   B.fwd = 0;
