@@ -254,6 +254,47 @@ def run_b200(args):
     e2e_nev_ms = (time.perf_counter() - t0) * 1e3
     del op2
 
+    # ---- large config (rank 0, N = 1): the regime of the north-star targets
+    #      (large-front Schur updates on FP64 tensor cores, HBM-bound sweeps)
+    large = None
+    if rank == 0 and ws == 1 and args.large:
+        PL = rq.baseline_config(args.large)
+        oL = rq.nested_dissection_order(PL)
+        stL = oL.stats
+        opL = rq.build_operator(PL, SIGMA, oL)
+
+        def time_large(what, iters, param=0):
+            ms = C.c_double()
+            _lib.check(_lib.lib.rq_operator_time(opL._h, what, iters, param, C.byref(ms)))
+            return ms.value
+        time_large(5 | 0x100, 2)
+        f_ms = time_large(5 | 0x100, 3)
+        s_ms = time_large(1 | 0x100, 5)
+        sp_ms = time_large(2 | 0x100, 10)
+        kL = 2 * NEV.get(args.large, 100) + 1
+        gt_ms = time_large(3 | 0x100, 5, kL)
+        gn_ms = time_large(4 | 0x100, 5, kL)
+        gf_l = stL["flops_lu"] / (f_ms * 1e6)
+        sb = stL["trisolve_bytes"]
+        spb = 20.0 * PL.nnz + 8.0 * (PL.n + 1) + 24.0 * PL.n
+        gb = 8.0 * 2 * PL.n * kL
+        large = {
+            "workload": args.large, "n": PL.n, "nnz": PL.nnz, "flops_lu": stL["flops_lu"],
+            "max_front": int(stL["max_front"]),
+            "factor": {"ms": round(f_ms, 3), "gflops": round(gf_l, 1),
+                       "frac_fp64": round(gf_l / 1e3 / FP64_PEAK_TFLOPS, 4)},
+            "trisolve": {"ms": round(s_ms, 4), "gbs": round(sb / (s_ms * 1e6), 1),
+                         "frac_hbm": round(sb / (s_ms * 1e6) / hbm, 4)},
+            "spmv_fused_cm": {"ms": round(sp_ms, 4), "gbs": round(spb / (sp_ms * 1e6), 1),
+                              "frac_hbm": round(spb / (sp_ms * 1e6) / hbm, 4)},
+            "cgs_gemv_t": {"k": kL, "ms": round(gt_ms, 4), "gbs": round(gb / (gt_ms * 1e6), 1),
+                           "frac_hbm": round(gb / (gt_ms * 1e6) / hbm, 4)},
+            "cgs_gemv_n": {"k": kL, "ms": round(gn_ms, 4), "gbs": round(gb / (gn_ms * 1e6), 1),
+                           "frac_hbm": round(gb / (gn_ms * 1e6) / hbm, 4)},
+            "l2": "scrubbed (256 MiB) before every timed call",
+        }
+        del opL
+
     # ---- CPU baseline (rank 0, N = 1 only): bounded oracle factorization sample
     cpu = None
     if rank == 0 and ws == 1 and args.cpu_sample_s > 0:
@@ -316,6 +357,7 @@ def run_b200(args):
                            "frac_hbm": round(gemv_bytes / t_gemv / 1e6 / hbm, 4)},
         },
         "roofline": roof,
+        "large_config": large,
         "cpu_baseline": cpu,
         "e2e": {"value": round(ws * flu / (e2e_ms * 1e6), 3), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * P.nnz, "d2h_bytes_per_step": 16,
@@ -339,6 +381,8 @@ def main():
     ap.add_argument("--max-restarts", type=int, default=1000)
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--nev-cpu", type=int, default=1)
+    ap.add_argument("--large", default="cfg4_riga",
+                    help="secondary large config for the large-front / HBM roofline section ('' to skip)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
