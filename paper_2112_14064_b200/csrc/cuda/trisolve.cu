@@ -308,20 +308,41 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
     const bool whole = I.blk == kWhole;
     const int nck = whole ? I.npb + I.ncbb : 1;
     unsigned long long waited = 0;
-    for (int ck = 0; ck < nck; ++ck) {
-      int r0 = I.r0, nr = I.nr, blk = I.blk;
+    // rows of chunk ck: pivot blocks first, then 64-row contribution chunks
+    auto chunk_rows = [&](int ck, int& r0, int& nr, int& blk) {
+      r0 = I.r0, nr = I.nr, blk = I.blk;
       if (whole) {
         blk = ck < I.npb ? ck : -1;
         r0 = ck < I.npb ? ck * kRB : np + (ck - I.npb) * kRB;
         nr = (ck < I.npb ? min(np, r0 + kRB) : min(I.nf, r0 + kRB)) - r0;
       }
-      // w = b + children's contributions (children complete: the front is ready)
+    };
+    // w = b + children's contributions (children complete: the front is ready);
+    // the gather of the next chunk is issued while the current one is processed
+    auto gather_w = [&](int r0, int nr) {
+      double v = 0.0;
       if (tid < nr) {
         const int4 src = __ldg(&A.gsrc[I.rows_off + r0 + tid]);
-        double v = src.x >= 0 ? A.b[src.x] : 0.0;
+        if (src.x >= 0) v = A.b[src.x];
         if (src.y >= 0) v += __ldcg(&A.cbvec[src.y]);
         if (src.z >= 0) v += __ldcg(&A.cbvec[src.z]);
-        wv[tid] = v;
+      }
+      return v;
+    };
+    double wnext;
+    {
+      int r0, nr, blk;
+      chunk_rows(0, r0, nr, blk);
+      wnext = gather_w(r0, nr);
+    }
+    for (int ck = 0; ck < nck; ++ck) {
+      int r0, nr, blk;
+      chunk_rows(ck, r0, nr, blk);
+      if (tid < nr) wv[tid] = wnext;
+      if (ck + 1 < nck) {
+        int r1, nr1, b1;
+        chunk_rows(ck + 1, r1, nr1, b1);
+        wnext = gather_w(r1, nr1);
       }
       if (blk >= 0) load_diag<false>(D, nullptr, g, ld, r0, nr, tid);
       __syncthreads();
