@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     // tasks that never redo data after this point count towards front
     // completion right away (overlaps the round trip with the notifications)
     const bool early_done = T.type == T_SMALL || T.type == T_ASM || T.type == T_UPD;
-    if (early_done && tid == 32) done_s = (atomicAdd(&cnt[0], 1) + 1 == D.ntasks);
+    if (early_done && tid == 160) done_s = (atomicAdd(&cnt[0], 1) + 1 == D.ntasks);
     if (T.type == T_DIAG || T.type == T_ROWS || T.type == T_COLS) {
       if (T.type == T_DIAG) {
         const int a0 = a0_of(F, T.step), nr = nr_of(F, D, T.step);
@@ -933,16 +933,25 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
           notify(A, idx_upd(A, D, F, T.step, a0 + 1 + x / (nr - 1), a0 + 1 + x % (nr - 1)));
       }
     } else if (T.type == T_UPD) {
-      if (tid == 0) {
-        atomicAdd(&A.tile_step[D.tile_off + T.a * D.tiles + T.b], 1);
-        const int s1 = T.step + 1;
-        if (s1 < steps) {
-          const int a1 = a0_of(F, s1), an = (s1 * kNB) / kTile;
-          const bool trail = nr_of(F, D, s1) > 0;  // step s1 has trailing rows / columns
-          if (trail && T.a >= a1 && T.b >= a1) notify(A, idx_upd(A, D, F, s1, T.a, T.b));
-          if (T.a == an && T.b == an) notify(A, idx_diag(A, D, s1));
-          if (trail && T.b == an && T.a >= a1) notify(A, idx_rows(A, D, F, s1, T.a));
-          if (trail && T.a == an && T.b >= a1) notify(A, idx_cols(A, D, F, s1, T.b));
+      // one notification per warp: the atomic round trips overlap
+      const int s1 = T.step + 1;
+      if (tid == 64) atomicAdd(&A.tile_step[D.tile_off + T.a * D.tiles + T.b], 1);
+      if (s1 < steps && (tid & 31) == 0 && tid < 4 * 32 + 1) {
+        const int a1 = a0_of(F, s1), an = (s1 * kNB) / kTile;
+        const bool trail = nr_of(F, D, s1) > 0;  // step s1 has trailing rows / columns
+        switch (tid >> 5) {
+          case 0:
+            if (T.a == an && T.b == an) notify(A, idx_diag(A, D, s1));
+            break;
+          case 1:
+            if (trail && T.b == an && T.a >= a1) notify(A, idx_rows(A, D, F, s1, T.a));
+            break;
+          case 2:
+            if (trail && T.a == an && T.b >= a1) notify(A, idx_cols(A, D, F, s1, T.b));
+            break;
+          case 3:
+            if (trail && T.a >= a1 && T.b >= a1) notify(A, idx_upd(A, D, F, s1, T.a, T.b));
+            break;
         }
       }
     } else if (T.type == T_ASM) {
