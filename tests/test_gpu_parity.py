@@ -288,3 +288,42 @@ def test_solve_whole_front_items_and_determinism(name, monkeypatch):
         xs.append(x1)
     monkeypatch.delenv("RQB_WHOLE_MIN", raising=False)
     assert np.max(np.abs(xs[0] - xs[1])) <= 1e-12 * np.max(np.abs(xs[0]))
+
+
+@pytest.mark.parametrize("name,occ", [("cfg1", "1"), ("cfg1", "2"), ("cfg2_riga", "1")])
+def test_pivoting_in_every_front_vs_oracle(name, occ, monkeypatch):
+    """Threshold pivoting inside a multifrontal tree (the BASELINE pencils never
+    swap): cfg1's pattern with random values and a weak diagonal, so most
+    fronts swap. Both kernel variants: occ 1 (SMALL fronts up to nf 160, the
+    exact warp-shuffle panel), occ 2 (SMALL up to 118: the 119..145 fronts take
+    the tiled path, whose speculative panel fails and is redone by the exact
+    fallback with contribution rows and children present); cfg2 rIGA's fronts
+    up to nf 325 take the tiled path in either variant. Pivots bit-exact, factor
+    entries and the solution against the oracle."""
+    P = rq.baseline_config(name)
+    o = rq.nested_dissection_order(P)
+    rng = np.random.default_rng(5)
+    Q = rng.standard_normal(P.nnz)
+    rows = np.repeat(np.arange(P.n), np.diff(P.rowptr))
+    Q[P.col == rows] *= 0.01
+    monkeypatch.setenv("RQB_DAG_OCC", occ)
+    f = rq.lu_factorize((P.rowptr, P.col, Q), o)
+    monkeypatch.delenv("RQB_DAG_OCC")
+    of = oracle.Factor(P.n, P.rowptr, P.col, Q, P.box, P.elems)
+    assert f.info()["swaps"] == of.swaps > 0
+    worst = 0.0
+    for fr in range(len(o.nf)):
+        nf, npv = int(o.nf[fr]), int(o.npiv[fr])
+        F, ipiv, _ = f.front(fr)
+        Fo, ipo, _ = of.front(fr, nf, npv)
+        assert np.array_equal(ipiv, ipo), f"front {fr} (nf {nf}, npiv {npv})"
+        mask = np.zeros((nf, nf), bool)
+        mask[:, :npv] = True
+        mask[:npv, :] = True
+        d = np.max(np.abs((F[:nf, :nf] - Fo.real)[mask])) / max(np.max(np.abs(Fo.real[mask])), 1e-300)
+        worst = max(worst, d)
+    assert worst <= 1e-9
+    b = rng.standard_normal(P.n)
+    x = f.solve(b)
+    xo = of.solve(b).real
+    assert np.max(np.abs(x - xo)) <= 1e-8 * np.max(np.abs(xo))
