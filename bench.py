@@ -112,9 +112,32 @@ def barrier(ws):
         dist.barrier()
 
 
+def host_info():
+    """nproc and CPU model of the box the CPU baseline ran on."""
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "pinned_core": 0}
+
+
+def pin_core0():
+    """The reference path is single-threaded (taskset -c 0)."""
+    try:
+        os.sched_setaffinity(0, {0})
+    except (AttributeError, OSError):
+        pass
+
+
 def cpu_factor_sample(P, kind, budget_s):
-    """Oracle factorization timed on the host (1 thread), bounded sample."""
+    """Oracle factorization timed on the host (1 thread, pinned), bounded sample."""
     import oracle
+    old = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    pin_core0()
     Q = P.q_values(SIGMA)
     ts = []
     t_end = time.perf_counter() + budget_s
@@ -125,6 +148,8 @@ def cpu_factor_sample(P, kind, budget_s):
         del f
         if time.perf_counter() > t_end or len(ts) >= 50:
             break
+    if old is not None:
+        os.sched_setaffinity(0, old)
     return ts
 
 
@@ -132,6 +157,7 @@ def run_reference(args):
     rank, ws, _ = dist_init()
     if rank != 0:
         return
+    pin_core0()
     import oracle
     import paper_2112_14064_b200 as rq
     kind = "reference" if oracle.ref() is not None else "port"
@@ -164,7 +190,8 @@ def run_reference(args):
                    "n": P.n, "nnz": P.nnz, "flops_lu_real": flu, "parallelism": "1 host thread"},
         "time_to_nev_ms": tnev,
         "cpu_baseline": {"value": round(gf, 4), "unit": "GFLOP/s", "cores": 1, "kind": kind,
-                         "sample": f"{args.steps} full factorizations of {args.config}"},
+                         "sample": f"{args.steps} full factorizations of {args.config}",
+                         "host": host_info()},
         "e2e": {"value": round(gf, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -303,7 +330,8 @@ def run_b200(args):
         ts = cpu_factor_sample(P, kind, args.cpu_sample_s)
         cpu = {"value": round(flu / (sum(ts) / len(ts)) / 1e9, 4), "unit": "GFLOP/s", "cores": 1,
                "kind": kind, "sample": f"{len(ts)} full factorizations of {args.config} "
-                                       f"({sum(ts):.1f} s, complex cdouble arithmetic: 4x the real work)"}
+                                       f"({sum(ts):.1f} s, complex cdouble arithmetic: 4x the real work)",
+               "host": host_info()}
 
     # DRAM bytes per launch of the dominant kernel from a committed ncu --set
     # full capture (profiles/ncu_traffic.json, written by tools/ncu_summary.py)
