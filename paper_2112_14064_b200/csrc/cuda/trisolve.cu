@@ -720,7 +720,9 @@ void rqb_solve_prepare(FactorEngine& fe) {
     if (F.level >= static_cast<int>(lvl_count.size())) lvl_count.resize(F.level + 1, 0);
     ++lvl_count[F.level];
   }
-  const int whole_min = std::getenv("RQB_WHOLE_MIN") ? std::atoi(std::getenv("RQB_WHOLE_MIN")) : 2 * fe.solve_grid;
+  // (measured: 128 fronts for small trees, 256 for large ones)
+  const int whole_min = std::getenv("RQB_WHOLE_MIN") ? std::atoi(std::getenv("RQB_WHOLE_MIN"))
+                                                      : (fe.sweep_occ == 3 ? 256 : 128);
   std::vector<char> whole(nfr);
   std::vector<int32_t> vnpb_f(nfr);
   for (int f = 0; f < nfr; ++f) {
