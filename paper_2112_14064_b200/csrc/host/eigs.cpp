@@ -159,7 +159,22 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   std::vector<double> final_res, last_res;
   std::vector<int> final_block;  // 0 upper, 1 lower
   std::vector<double> final_vecs_re, final_vecs_im;
-  std::vector<double> ha((m + 1) * (m + 1)), hb((m + 1) * (m + 1)), betas(m + 1);
+  // pinned: the cycle's H / beta copies are truly asynchronous, so the host
+  // can start on them while the GPU already applies the operator to the
+  // continuation vector of the next cycle
+  struct Pinned {
+    double* p = nullptr;
+    explicit Pinned(size_t n) {
+      cuda_check(cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(double) * std::max<size_t>(n, 1)), "pinned");
+    }
+    ~Pinned() { cudaFreeHost(p); }
+    double& operator[](size_t i) { return p[i]; }
+    double* data() { return p; }
+  };
+  Pinned ha((m + 1) * (m + 1)), hb((m + 1) * (m + 1)), betas(m + 1);
+  cudaEvent_t e_h;
+  cuda_check(cudaEventCreateWithFlags(&e_h, cudaEventDisableTiming), "event");
+  bool pre_applied = false;  // r already holds apply(V[k]) (speculative, see below)
   double t_solve = 0, t_orth = 0, t_ritz = 0, t_check = 0, t_restart = 0, t_sync = 0;
   double check_gate = o.est_factor * o.tol;
   int last_nchk = 0;  // candidates of the last explicit check (row-major Ritz batch in dX)
@@ -183,11 +198,11 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     ++cycles;
     ++pass_cycles;
     // ---- Arnoldi steps k .. m-1: one CUDA graph per (start, basis buffer) ----
-    auto enqueue_steps = [&](bool prof) {
+    auto enqueue_steps = [&](bool prof, bool skip_first) {
       for (int j = k; j < m; ++j) {
         double* vj = V + static_cast<int64_t>(j) * n2;
         if (prof) cuda_check(cudaEventRecord(e_a, st), "ev");
-        op.apply(vj, r);
+        if (!(skip_first && j == k)) op.apply(vj, r);
         if (prof) {
           cuda_check(cudaEventRecord(e_b, st), "ev");
           cuda_check(cudaEventSynchronize(e_b), "ev");
@@ -216,14 +231,14 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       }
     };
     if (o.profile) {
-      enqueue_steps(true);
+      enqueue_steps(true, false);
     } else {
-      const std::pair<int, const double*> key{k, V};
+      const std::pair<int, const double*> key{pre_applied ? -1 - k : k, V};
       auto it = graphs.find(key);
       if (it == graphs.end()) {
         cudaGraph_t gr;
         cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
-        enqueue_steps(false);
+        enqueue_steps(false, pre_applied);
         cuda_check(cudaStreamEndCapture(st, &gr), "capture end");
         cudaGraphExec_t ex;
         cuda_check(cudaGraphInstantiate(&ex, gr, 0), "graph instantiate");
@@ -247,11 +262,16 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
                                cudaMemcpyDeviceToHost, st), "D2H H");
     cuda_check(cudaMemcpyAsync(betas.data(), dBeta.p, sizeof(double) * (m + 1),
                                cudaMemcpyDeviceToHost, st), "D2H beta");
+    cuda_check(cudaEventRecord(e_h, st), "ev");
+    // Speculatively apply the operator to v_m: unless the cycle ends in a
+    // deflated restart (fresh vector), v_m is the next cycle's continuation
+    // vector V[p], so the solve overlaps the host's Ritz / restart work.
+    pre_applied = !o.profile;
+    if (pre_applied) op.apply(V + static_cast<int64_t>(m) * n2, r);
     {
       const auto ts0 = now();
-      cuda_check(cudaStreamSynchronize(st), "sync");
+      cuda_check(cudaEventSynchronize(e_h), "sync");
       t_sync += ms_since(ts0);  // host blocked on the cycle's Arnoldi steps
-      op.fac->check_sweeps();
     }
     for (int j = k; j < m; ++j) {
       for (int i = 0; i <= j; ++i)
@@ -527,6 +547,8 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     std::swap(BV, BV2);
     if (deflate) {
       // b = 0 (converged directions deflated); fresh seeded continuation vector
+      // (the speculative apply of v_m is discarded)
+      pre_applied = false;
       fresh_vector(o.seed + 0x1000003ull * guard_passes, p, V + static_cast<int64_t>(p) * n2,
                    BV + static_cast<int64_t>(p) * n2);
     } else {
@@ -539,6 +561,8 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     t_restart += ms_since(trs0);
     k = p;
   }
+  op.fac->check_sweeps();  // watchdog of the triangular sweeps (syncs the stream)
+  cudaEventDestroy(e_h);
   cudaEventDestroy(e_a);
   cudaEventDestroy(e_b);
   // keep the last candidate set if the run stopped early
