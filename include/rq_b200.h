@@ -72,6 +72,15 @@ typedef struct {
 } rq_space_desc;
 
 int rq_pencil_assemble(const rq_space_desc* desc, rq_pencil_t** out);
+/* The same pencil, bit for bit, assembled on the current CUDA device
+ * (pattern, per-element Gauss quadrature, colour-ordered
+ * gather; no atomics). resident = 1 keeps K, C, M in device memory only
+ * (rq_pencil_csr copies them out on demand; rq_operator_create_pencil uses
+ * them in place); the pattern is always copied to the host. ms (nullable,
+ * double[5]) receives the device ms of the three stages {pattern, element
+ * matrices, gather}, then the host ms of the O(n) preparation (free
+ * numbering, supports, Gauss tables) and of the copy back. */
+int rq_pencil_assemble_device(const rq_space_desc* desc, int resident, rq_pencil_t** out, double* ms);
 /* n_full = all DOFs, n_free = after BC elimination, nnz = shared-pattern nnz */
 int rq_pencil_dims(const rq_pencil_t* p, int64_t* n_full, int64_t* n_free, int64_t* nnz);
 /* Shared CSR pattern (rowptr int64[n+1], col int32[nnz], sorted per row) and
@@ -180,6 +189,12 @@ typedef struct {
 int rq_operator_create(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
                        const double* C, const double* M, const rq_symbolic_t* s,
                        const rq_operator_opts* opts, rq_operator_t** out);
+/* The same operator from a pencil handle: a device-resident pencil
+ * (rq_pencil_assemble_device, resident = 1) is used in place — scaling,
+ * Q(s) and the residual norms are formed on the device with the host path's
+ * rounding, so the results equal rq_operator_create's on the same pencil. */
+int rq_operator_create_pencil(const rq_pencil_t* p, const rq_symbolic_t* s,
+                              const rq_operator_opts* opts, rq_operator_t** out);
 double rq_operator_varsigma(const rq_operator_t* op);
 /* r = L(s)^{-1} B v : r_u = -Q(s)^{-1}(s M v_u + C v_u + M v_l), r_l = s r_u + v_u
  * (of the possibly scaled pencil). */

@@ -40,6 +40,18 @@ f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 vp = C.c_void_p
 
 
+def _nullable(base):
+    """ndpointer argtype that also accepts None (NULL)."""
+    class _N(base):
+        @classmethod
+        def from_param(cls, obj):
+            return None if obj is None else base.from_param(obj)
+    return _N
+
+
+i32n, i64n, f64n = _nullable(i32p), _nullable(i64p), _nullable(f64p)
+
+
 class SpaceDesc(C.Structure):
     _fields_ = [("kind", C.c_int), ("degree", C.c_int), ("elems", C.c_int),
                 ("levels", C.c_int), ("alpha", C.c_double), ("beta", C.c_double)]
@@ -92,9 +104,10 @@ _sig("rq_last_error", C.c_char_p)
 _sig("rq_version", C.c_char_p)
 _sig("rq_set_device", C.c_int, C.c_int)
 _sig("rq_pencil_assemble", C.c_int, C.POINTER(SpaceDesc), C.POINTER(vp))
+_sig("rq_pencil_assemble_device", C.c_int, C.POINTER(SpaceDesc), C.c_int, C.POINTER(vp), f64p)
 _sig("rq_pencil_dims", C.c_int, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64))
-_sig("rq_pencil_csr", C.c_int, vp, i64p, i32p, f64p, f64p, f64p)
-_sig("rq_pencil_supports", C.c_int, vp, i32p, i64p)
+_sig("rq_pencil_csr", C.c_int, vp, i64n, i32n, f64n, f64n, f64n)
+_sig("rq_pencil_supports", C.c_int, vp, i32n, i64n)
 _sig("rq_pencil_destroy", None, vp)
 _sig("rq_space_dims", C.c_int, C.POINTER(SpaceDesc), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
      C.POINTER(C.c_int64), C.POINTER(C.c_int64))
@@ -115,6 +128,7 @@ _sig("rq_factor_dag_profile", C.c_int, vp, f64p)
 _sig("rq_factor_destroy", None, vp)
 _sig("rq_operator_create", C.c_int, C.c_int64, i64p, i32p, f64p, f64p, f64p, vp,
      C.POINTER(OperatorOpts), C.POINTER(vp))
+_sig("rq_operator_create_pencil", C.c_int, vp, vp, C.POINTER(OperatorOpts), C.POINTER(vp))
 _sig("rq_operator_varsigma", C.c_double, vp)
 _sig("rq_operator_apply", C.c_int, vp, f64p, f64p)
 _sig("rq_operator_b_inner", C.c_int, vp, f64p, f64p, C.POINTER(C.c_double))
@@ -128,13 +142,14 @@ _sig("rq_eigs_ledger_json", C.c_int, vp, C.c_char_p, C.c_size_t)
 
 # every symbol include/rq_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = [
-    "rq_last_error", "rq_version", "rq_set_device", "rq_pencil_assemble", "rq_pencil_dims", "rq_pencil_csr",
+    "rq_last_error", "rq_version", "rq_set_device", "rq_pencil_assemble", "rq_pencil_assemble_device",
+    "rq_pencil_dims", "rq_pencil_csr",
     "rq_pencil_supports", "rq_pencil_destroy", "rq_space_dims", "rq_space_boundary_mask",
     "rq_nd_order", "rq_symbolic_stats_get", "rq_symbolic_perm", "rq_symbolic_fronts",
     "rq_symbolic_front_rows", "rq_symbolic_destroy", "rq_factor_create", "rq_factor_refactor",
     "rq_factor_get_info", "rq_factor_solve", "rq_factor_front_export", "rq_factor_profile", "rq_factor_dag_profile",
     "rq_factor_destroy",
-    "rq_operator_create", "rq_operator_varsigma", "rq_operator_apply", "rq_operator_b_inner",
+    "rq_operator_create", "rq_operator_create_pencil", "rq_operator_varsigma", "rq_operator_apply", "rq_operator_b_inner",
     "rq_operator_spmv", "rq_operator_arnoldi", "rq_operator_factor", "rq_operator_destroy",
     "rq_operator_time",
     "rq_eigs_run", "rq_eigs_ledger_json",

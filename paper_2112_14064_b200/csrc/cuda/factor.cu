@@ -577,7 +577,10 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
     }
   }
   d_pool.alloc(sizeof(double) * sym.pool);
-  d_aval.upload(aval, sizeof(double) * nnz, stream);
+  if (aval)
+    d_aval.upload(aval, sizeof(double) * nnz, stream);
+  else
+    d_aval.alloc(sizeof(double) * nnz);  // values arrive by set_values_device
   d_qdst.upload(dst.data(), sizeof(int64_t) * nnz, stream);
   d_rows.upload(sym.rows.data(), sizeof(int32_t) * sym.rows.size(), stream);
   d_fronts.upload(fronts_h.data(), sizeof(FrontDev) * fronts_h.size(), stream);

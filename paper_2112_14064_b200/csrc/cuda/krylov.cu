@@ -341,6 +341,126 @@ OperatorEngine::OperatorEngine(int64_t n_, const int64_t* rowptr, const int32_t*
   d_C.upload(Cs.data(), sizeof(double) * nnz, stream);
   d_M.upload(Ms.data(), sizeof(double) * nnz, stream);
   d_Q.upload(Q.data(), sizeof(double) * nnz, stream);
+  init_workspaces();
+}
+
+namespace {
+
+// max |K|, max |M| (non-negative doubles order like their bit patterns:
+// exact and order independent)
+__global__ void maxabs2_k(int64_t nnz, const double* K, const double* M, unsigned long long* out) {
+  double a = 0.0, b = 0.0;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    a = fmax(a, fabs(K[k]));
+    b = fmax(b, fabs(M[k]));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(a)));
+    atomicMax(out + 1, static_cast<unsigned long long>(__double_as_longlong(b)));
+  }
+}
+
+// Cs = v C, Ms = v2 M (when scaling), Q = K + s C + s^2 M: the host
+// constructor's expressions, each product / sum rounded separately
+__global__ void pencil_scale_k(int64_t nnz, const double* K, const double* C, const double* M,
+                               int scaling, double v, double v2, double s, double* Cs, double* Ms,
+                               double* Q) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double c = C[k], m = M[k];
+    Cs[k] = scaling ? __dmul_rn(v, c) : c;
+    Ms[k] = scaling ? __dmul_rn(v2, m) : m;
+    Q[k] = __dadd_rn(__dadd_rn(K[k], __dmul_rn(s, c)), __dmul_rn(__dmul_rn(s, s), m));
+  }
+}
+
+// 1-norm of f A for the three (A, f) = (K, 1), (C, v), (M, v*v): column sums
+// of a symmetric matrix = row sums, each row summed sequentially in column
+// order — the same sequence the host's column accumulation adds
+__global__ void norm1_sym_k(int64_t n, const int64_t* rowptr, const double* K, const double* C,
+                            const double* M, double v, unsigned long long* out) {
+  double a[3] = {0.0, 0.0, 0.0};
+  const double vv = __dmul_rn(v, v);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double sk = 0.0, sc = 0.0, sm = 0.0;
+    for (int64_t k = rowptr[r]; k < rowptr[r + 1]; ++k) {
+      sk = __dadd_rn(sk, fabs(K[k]));
+      sc = __dadd_rn(sc, fabs(__dmul_rn(v, C[k])));
+      sm = __dadd_rn(sm, fabs(__dmul_rn(vv, M[k])));
+    }
+    a[0] = fmax(a[0], sk);
+    a[1] = fmax(a[1], sc);
+    a[2] = fmax(a[2], sm);
+  }
+  for (int i = 0; i < 3; ++i) {
+    double x = a[i];
+    for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out + i, static_cast<unsigned long long>(__double_as_longlong(x)));
+  }
+}
+
+}  // namespace
+
+OperatorEngine::OperatorEngine(const DevicePencil& dp, const int64_t* rowptr_h, const int32_t* col_h,
+                               const Symbolic& s, double sigma_, bool scaling, double* norms1)
+    : n(dp.n) {
+  nnz = dp.nnz;
+  int dev = 0;
+  RQB_CUDA(cudaGetDevice(&dev));
+  if (dev != dp.device) fail(errc::config, "device pencil lives on another CUDA device");
+  if (rowptr_h[n] != nnz) fail(errc::config, "device pencil / host pattern mismatch");
+  fac = std::make_unique<FactorEngine>(s, n, rowptr_h, col_h, nullptr);
+  stream = fac->stream;
+  d_rowptr.alloc(sizeof(int64_t) * (n + 1));
+  d_col.alloc(sizeof(int32_t) * nnz);
+  RQB_CUDA(cudaMemcpyAsync(d_rowptr.p, dp.d_rowptr.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, stream));
+  RQB_CUDA(cudaMemcpyAsync(d_col.p, dp.d_col.p, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, stream));
+  d_K.alloc(sizeof(double) * nnz);
+  RQB_CUDA(cudaMemcpyAsync(d_K.p, dp.K(), sizeof(double) * nnz, cudaMemcpyDeviceToDevice, stream));
+  d_C.alloc(sizeof(double) * nnz);
+  d_M.alloc(sizeof(double) * nnz);
+  d_Q.alloc(sizeof(double) * nnz);
+  DeviceBuffer d_red;
+  d_red.alloc(sizeof(unsigned long long) * 8);
+  unsigned long long* red = d_red.as<unsigned long long>();
+  unsigned long long h_red[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  RQB_CUDA(cudaMemsetAsync(red, 0, sizeof(unsigned long long) * 8, stream));
+  const int grid = 148 * 8;
+  varsigma = 1.0;
+  if (scaling) {
+    maxabs2_k<<<grid, 256, 0, stream>>>(nnz, dp.K(), dp.M(), red);
+    RQB_CUDA(cudaGetLastError());
+    RQB_CUDA(cudaMemcpyAsync(h_red, red, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, stream));
+    RQB_CUDA(cudaStreamSynchronize(stream));
+    double mk, mm;
+    std::memcpy(&mk, &h_red[0], sizeof(double));
+    std::memcpy(&mm, &h_red[1], sizeof(double));
+    if (!(mm > 0)) fail(errc::domain, "scale_pencil: zero M norm");
+    varsigma = std::sqrt(mk / mm);
+  }
+  sigma = sigma_ / varsigma;
+  const double v = varsigma, v2 = varsigma * varsigma;
+  pencil_scale_k<<<grid, 256, 0, stream>>>(nnz, dp.K(), dp.C(), dp.M(), scaling ? 1 : 0, v, v2, sigma_,
+                                           d_C.as<double>(), d_M.as<double>(), d_Q.as<double>());
+  RQB_CUDA(cudaGetLastError());
+  norm1_sym_k<<<div_up(n, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), dp.K(), dp.C(), dp.M(), v,
+                                                  red + 2);
+  RQB_CUDA(cudaGetLastError());
+  RQB_CUDA(cudaMemcpyAsync(h_red + 2, red + 2, sizeof(unsigned long long) * 3, cudaMemcpyDeviceToHost, stream));
+  fac->set_values_device(d_Q.as<double>());
+  RQB_CUDA(cudaStreamSynchronize(stream));
+  if (norms1)
+    for (int i = 0; i < 3; ++i) std::memcpy(&norms1[i], &h_red[2 + i], sizeof(double));
+  init_workspaces();
+}
+
+void OperatorEngine::init_workspaces() {
   d_w.alloc(sizeof(double) * 2 * n);
   d_t.alloc(sizeof(double) * 2 * n);
   nparts = kRedBlocks;

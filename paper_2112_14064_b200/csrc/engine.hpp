@@ -142,6 +142,17 @@ void rqb_dag_profile(FactorEngine& fe, double* out);
 void rqb_rowperm_enqueue(FactorEngine& fe);
 std::string rqb_dag_stall_report(FactorEngine& fe);
 
+// Device-resident pencil (device assembly): CSR pattern and
+// K, C, M values in HBM of the device that assembled them.
+struct DevicePencil {
+  int64_t n = 0, nnz = 0;
+  int device = 0;
+  DeviceBuffer d_rowptr, d_col, d_val;  // d_val: K | C | M, nnz each
+  const double* K() const { return d_val.as<double>(); }
+  const double* C() const { return d_val.as<double>() + nnz; }
+  const double* M() const { return d_val.as<double>() + 2 * nnz; }
+};
+
 // Shift-invert operator on the linearised pencil, real FP64, device resident.
 struct OperatorEngine {
   int64_t n = 0, nnz = 0;
@@ -160,6 +171,11 @@ struct OperatorEngine {
   OperatorEngine(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
                  const double* C, const double* M, const Symbolic& s, double sigma,
                  bool scaling);
+  // From a device-resident pencil (host copy of the pattern for the symbolic
+  // scatter maps): scaling, C/M scaling, Q(s) and the 1-norms of K, vC, v^2 M
+  // (norms1) are formed on the device with the host constructor's rounding.
+  OperatorEngine(const DevicePencil& dp, const int64_t* rowptr_h, const int32_t* col_h,
+                 const Symbolic& s, double sigma, bool scaling, double* norms1);
   ~OperatorEngine();
   // Device vector ops (2n vectors: upper; lower), all enqueued on `stream`.
   void spmv(int which, const double* x, double* y);          // y = A x
@@ -187,6 +203,9 @@ struct OperatorEngine {
   void ritz_extract(const double* Xrm, int nc, int c, int part_im, double* out);
   // Average device ms of one call of an operation (see rq_operator_time).
   double time_op(int what, int iters, int param);
+
+ private:
+  void init_workspaces();
 };
 
 }  // namespace rqb

@@ -17,6 +17,7 @@
 
 struct rq_pencil {
   rqb::Pencil P;
+  std::unique_ptr<rqb::DevicePencil> dev;  // device-resident K, C, M (P.K/C/M empty)
 };
 struct rq_symbolic {
   rqb::Symbolic S;
@@ -99,6 +100,17 @@ int rq_pencil_assemble(const rq_space_desc* desc, rq_pencil_t** out) {
   });
 }
 
+int rq_pencil_assemble_device(const rq_space_desc* desc, int resident, rq_pencil_t** out, double* ms) {
+  return guarded([&] {
+    need(out, "out");
+    const rqb::VectorSpace vs = space_of(desc);
+    auto p = std::make_unique<rq_pencil>();
+    if (resident) p->dev = std::make_unique<rqb::DevicePencil>();
+    p->P = rqb::assemble_pencil_device(vs, desc->alpha, desc->beta, ms, p->dev.get());
+    *out = p.release();
+  });
+}
+
 int rq_pencil_dims(const rq_pencil_t* p, int64_t* n_full, int64_t* n_free, int64_t* nnz) {
   return guarded([&] {
     need(p, "pencil");
@@ -115,6 +127,18 @@ int rq_pencil_csr(const rq_pencil_t* p, int64_t* rowptr, int32_t* col, double* K
     const rqb::Pencil& P = p->P;
     if (rowptr) std::memcpy(rowptr, P.rowptr.data(), sizeof(int64_t) * P.rowptr.size());
     if (col) std::memcpy(col, P.col.data(), sizeof(int32_t) * P.col.size());
+    if (p->dev) {
+      const rqb::DevicePencil& D = *p->dev;
+      const size_t b = sizeof(double) * D.nnz;
+      int cur = 0;
+      rqb::cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+      rqb::cuda_check(cudaSetDevice(D.device), "cudaSetDevice");
+      if (K) rqb::cuda_check(cudaMemcpy(K, D.K(), b, cudaMemcpyDeviceToHost), "pencil K D2H");
+      if (C) rqb::cuda_check(cudaMemcpy(C, D.C(), b, cudaMemcpyDeviceToHost), "pencil C D2H");
+      if (M) rqb::cuda_check(cudaMemcpy(M, D.M(), b, cudaMemcpyDeviceToHost), "pencil M D2H");
+      rqb::cuda_check(cudaSetDevice(cur), "cudaSetDevice");
+      return;
+    }
     if (K) std::memcpy(K, P.K.data(), sizeof(double) * P.K.size());
     if (C) std::memcpy(C, P.C.data(), sizeof(double) * P.C.size());
     if (M) std::memcpy(M, P.M.data(), sizeof(double) * P.M.size());
@@ -315,6 +339,14 @@ int rq_factor_dag_profile(rq_factor_t* f, double* out) {
 
 void rq_factor_destroy(rq_factor_t* f) { delete f; }
 
+namespace {
+void finish_operator(rq_operator* o) {
+  o->fac_view.fe = o->op->fac.get();
+  o->d_a.alloc(sizeof(double) * 2 * o->op->n);
+  o->d_b.alloc(sizeof(double) * 2 * o->op->n);
+}
+}  // namespace
+
 int rq_operator_create(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
                        const double* C, const double* M, const rq_symbolic_t* s,
                        const rq_operator_opts* opts, rq_operator_t** out) {
@@ -339,9 +371,26 @@ int rq_operator_create(int64_t n, const int64_t* rowptr, const int32_t* col, con
     o->norms1[1] = norm1(n, rowptr, col, tmp);
     for (int64_t k = 0; k < nnz; ++k) tmp[k] = v * v * M[k];
     o->norms1[2] = norm1(n, rowptr, col, tmp);
-    o->fac_view.fe = o->op->fac.get();
-    o->d_a.alloc(sizeof(double) * 2 * n);
-    o->d_b.alloc(sizeof(double) * 2 * n);
+    finish_operator(o.get());
+    *out = o.release();
+  });
+}
+
+int rq_operator_create_pencil(const rq_pencil_t* p, const rq_symbolic_t* s,
+                              const rq_operator_opts* opts, rq_operator_t** out) {
+  if (p && !p->dev)
+    return rq_operator_create(p->P.n, p->P.rowptr.data(), p->P.col.data(), p->P.K.data(),
+                              p->P.C.data(), p->P.M.data(), s, opts, out);
+  return guarded([&] {
+    need(p, "pencil");
+    need(s, "symbolic");
+    need(opts, "opts");
+    need(out, "out");
+    if (!std::isfinite(opts->sigma)) rqb::fail(rqb::errc::config, "shift must be finite and real");
+    auto o = std::make_unique<rq_operator>();
+    o->op = std::make_unique<rqb::OperatorEngine>(*p->dev, p->P.rowptr.data(), p->P.col.data(), s->S,
+                                                  opts->sigma, opts->scaling != 0, o->norms1);
+    finish_operator(o.get());
     *out = o.release();
   });
 }

@@ -86,6 +86,37 @@ struct Pencil {
 
 Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta);
 
+// Pieces shared by the host assembler and the device one (cuda/assembly.cu).
+// Free numbering: full_to_free[g] = free id or -1 (constrained), free_to_full.
+void free_numbering(const VectorSpace& vs, std::vector<int64_t>* full_to_free,
+                    std::vector<int64_t>* free_to_full);
+// Inclusive element support box {x0, x1, y0, y1} of every free DOF.
+std::vector<int32_t> support_boxes(const VectorSpace& vs, const std::vector<int64_t>& free_to_full);
+
+// Gauss tables of one direction of one component: values / first derivatives
+// of the p+1 bases active on element e at point q ([e][q][a]), weights [e][q].
+struct QuadTable {
+  int p = 0, nq = 0;
+  std::vector<double> val, der, wq;
+  void build(const Univariate& u, const double* gx, const double* gw, int nq_);
+  const double* v(int e, int q) const { return &val[(static_cast<size_t>(e) * nq + q) * (p + 1)]; }
+  const double* d(int e, int q) const { return &der[(static_cast<size_t>(e) * nq + q) * (p + 1)]; }
+  double w(int e, int q) const { return wq[static_cast<size_t>(e) * nq + q]; }
+};
+// (p+1)-point Gauss tables, tab[component][direction].
+void quad_tables(const VectorSpace& vs, QuadTable tab[2][2]);
+constexpr int kMaxAsmDegree = 12;
+
+// Device assembly (f1): the same pencil, bit for bit, computed on the current
+// CUDA device (pattern, element matrices, colour-ordered gather) and copied
+// back. ms[0..5) (nullable): device ms of the pattern / element / gather
+// stages, host ms of the O(n) preparation and of the copy back.
+// keep (nullable): receives the device copies and K, C, M are then NOT copied
+// back (P.K/C/M stay empty; the pattern is always copied).
+struct DevicePencil;
+Pencil assemble_pencil_device(const VectorSpace& vs, double alpha, double beta, double* ms,
+                              DevicePencil* keep = nullptr);
+
 // ---------------------------------------------------------------------------
 // Symbolic multifrontal structure.
 struct Front {

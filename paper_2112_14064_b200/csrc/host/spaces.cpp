@@ -136,7 +136,7 @@ std::vector<int64_t> boundary_mask(const VectorSpace& vs) {
 
 namespace {
 
-constexpr int kMaxP = 12;
+constexpr int kMaxP = kMaxAsmDegree;
 
 // Gauss-Legendre nodes/weights on [-1,1] (Newton on P_n).
 void gauss_legendre(int n, double* x, double* w) {
@@ -211,33 +211,6 @@ void basis_eval(const std::vector<double>& U, int p, int s, double u, double* va
   }
 }
 
-// Basis tables of one direction: for element e, point q, local basis a.
-struct DirTable {
-  int p = 0, nq = 0;
-  std::vector<double> val, der, wq;  // [e][q][a], [e][q][a], [e][q]
-  void build(const Univariate& u, const double* gx, const double* gw, int nq_) {
-    p = u.degree;
-    nq = nq_;
-    const int ne = u.elems;
-    val.assign(static_cast<size_t>(ne) * nq * (p + 1), 0.0);
-    der.assign(val.size(), 0.0);
-    wq.assign(static_cast<size_t>(ne) * nq, 0.0);
-    for (int e = 0; e < ne; ++e) {
-      const double x0 = static_cast<double>(e) / ne, x1 = static_cast<double>(e + 1) / ne;
-      const double h = x1 - x0;
-      for (int q = 0; q < nq; ++q) {
-        const double x = x0 + 0.5 * (gx[q] + 1.0) * h;
-        const size_t o = (static_cast<size_t>(e) * nq + q) * (p + 1);
-        basis_eval(u.knots, p, u.elem_span[e], x, &val[o], &der[o]);
-        wq[static_cast<size_t>(e) * nq + q] = 0.5 * h * gw[q];
-      }
-    }
-  }
-  const double* v(int e, int q) const { return &val[(static_cast<size_t>(e) * nq + q) * (p + 1)]; }
-  const double* d(int e, int q) const { return &der[(static_cast<size_t>(e) * nq + q) * (p + 1)]; }
-  double w(int e, int q) const { return wq[static_cast<size_t>(e) * nq + q]; }
-};
-
 // First basis index whose support reaches element lo / last reaching hi.
 void overlap_range(const Univariate& u, int lo, int hi, int* first, int* last) {
   const int nb = u.nbasis();
@@ -251,41 +224,87 @@ void overlap_range(const Univariate& u, int lo, int hi, int* first, int* last) {
 
 }  // namespace
 
+void QuadTable::build(const Univariate& u, const double* gx, const double* gw, int nq_) {
+  p = u.degree;
+  nq = nq_;
+  const int ne = u.elems;
+  val.assign(static_cast<size_t>(ne) * nq * (p + 1), 0.0);
+  der.assign(val.size(), 0.0);
+  wq.assign(static_cast<size_t>(ne) * nq, 0.0);
+  for (int e = 0; e < ne; ++e) {
+    const double x0 = static_cast<double>(e) / ne, x1 = static_cast<double>(e + 1) / ne;
+    const double h = x1 - x0;
+    for (int q = 0; q < nq; ++q) {
+      const double x = x0 + 0.5 * (gx[q] + 1.0) * h;
+      const size_t o = (static_cast<size_t>(e) * nq + q) * (p + 1);
+      basis_eval(u.knots, p, u.elem_span[e], x, &val[o], &der[o]);
+      wq[static_cast<size_t>(e) * nq + q] = 0.5 * h * gw[q];
+    }
+  }
+}
+
+void quad_tables(const VectorSpace& vs, QuadTable tab[2][2]) {
+  if (vs.degree > kMaxP) fail(errc::domain, "degree too large for assembly tables");
+  const int nq = vs.degree + 1;
+  double gx[kMaxP + 1], gw[kMaxP + 1];
+  gauss_legendre(nq, gx, gw);
+  const Tensor2* comp[2] = {&vs.cx, &vs.cy};
+  for (int c = 0; c < 2; ++c) {
+    tab[c][0].build(comp[c]->sx, gx, gw, nq);
+    tab[c][1].build(comp[c]->sy, gx, gw, nq);
+  }
+}
+
+void free_numbering(const VectorSpace& vs, std::vector<int64_t>* full_to_free,
+                    std::vector<int64_t>* free_to_full) {
+  const std::vector<int64_t> mask = boundary_mask(vs);
+  const int64_t N = vs.N();
+  full_to_free->assign(N, -1);
+  free_to_full->clear();
+  free_to_full->reserve(N - mask.size());
+  size_t mi = 0;
+  for (int64_t g = 0; g < N; ++g) {
+    if (mi < mask.size() && mask[mi] == g) {
+      ++mi;
+      continue;
+    }
+    (*full_to_free)[g] = static_cast<int64_t>(free_to_full->size());
+    free_to_full->push_back(g);
+  }
+}
+
+std::vector<int32_t> support_boxes(const VectorSpace& vs, const std::vector<int64_t>& free_to_full) {
+  const Tensor2* comp[2] = {&vs.cx, &vs.cy};
+  const int64_t base[2] = {0, vs.Nx()};
+  const int64_t n = static_cast<int64_t>(free_to_full.size());
+  std::vector<int32_t> box(4 * n);
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t g = free_to_full[k];
+    const int c = g >= vs.Nx() ? 1 : 0;
+    const int64_t l = g - base[c];
+    const int i = static_cast<int>(l % comp[c]->nx()), j = static_cast<int>(l / comp[c]->nx());
+    box[4 * k + 0] = comp[c]->sx.sup_first[i];
+    box[4 * k + 1] = comp[c]->sx.sup_last[i];
+    box[4 * k + 2] = comp[c]->sy.sup_first[j];
+    box[4 * k + 3] = comp[c]->sy.sup_last[j];
+  }
+  return box;
+}
+
 Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta) {
   if (vs.degree > kMaxP) fail(errc::domain, "degree too large for assembly tables");
   Pencil P;
   P.elems = vs.elems;
   P.n_full = vs.N();
-  const std::vector<int64_t> mask = boundary_mask(vs);
-  std::vector<int64_t> full_to_free(P.n_full, -1);
-  {
-    size_t mi = 0;
-    for (int64_t g = 0; g < P.n_full; ++g) {
-      if (mi < mask.size() && mask[mi] == g) {
-        ++mi;
-        continue;
-      }
-      full_to_free[g] = static_cast<int64_t>(P.free_to_full.size());
-      P.free_to_full.push_back(g);
-    }
-  }
+  std::vector<int64_t> full_to_free;
+  free_numbering(vs, &full_to_free, &P.free_to_full);
   P.n = static_cast<int64_t>(P.free_to_full.size());
   const Tensor2* comp[2] = {&vs.cx, &vs.cy};
   const int64_t base[2] = {0, vs.Nx()};
 
   // Support boxes and shared pattern (all support-overlapping free pairs).
-  P.box.resize(4 * P.n);
+  P.box = support_boxes(vs, P.free_to_full);
   P.rowptr.assign(P.n + 1, 0);
-  for (int64_t k = 0; k < P.n; ++k) {
-    const int64_t g = P.free_to_full[k];
-    const int c = g >= vs.Nx() ? 1 : 0;
-    const int64_t l = g - base[c];
-    const int i = static_cast<int>(l % comp[c]->nx()), j = static_cast<int>(l / comp[c]->nx());
-    P.box[4 * k + 0] = comp[c]->sx.sup_first[i];
-    P.box[4 * k + 1] = comp[c]->sx.sup_last[i];
-    P.box[4 * k + 2] = comp[c]->sy.sup_first[j];
-    P.box[4 * k + 3] = comp[c]->sy.sup_last[j];
-  }
   auto row_cols = [&](int64_t k, std::vector<int32_t>& out) {
     out.clear();
     const int32_t* b = &P.box[4 * k];
@@ -325,13 +344,8 @@ Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta) {
 
   // Quadrature tables.
   const int nq = vs.degree + 1;
-  double gx[kMaxP + 1], gw[kMaxP + 1];
-  gauss_legendre(nq, gx, gw);
-  DirTable tab[2][2];  // [component][direction]
-  for (int c = 0; c < 2; ++c) {
-    tab[c][0].build(comp[c]->sx, gx, gw, nq);
-    tab[c][1].build(comp[c]->sy, gx, gw, nq);
-  }
+  QuadTable tab[2][2];  // [component][direction]
+  quad_tables(vs, tab);
   const bool curl = vs.kind == SpaceKind::curl;
   const int ne = vs.elems;
 
@@ -359,8 +373,8 @@ Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta) {
           const double w = tab[0][0].w(ex, qx) * tab[0][1].w(ey, qy);
           int o = 0;
           for (int c = 0; c < 2; ++c) {
-            const DirTable& TX = tab[c][0];
-            const DirTable& TY = tab[c][1];
+            const QuadTable& TX = tab[c][0];
+            const QuadTable& TY = tab[c][1];
             const double* vx = TX.v(ex, qx);
             const double* dx = TX.d(ex, qx);
             const double* vy = TY.v(ey, qy);

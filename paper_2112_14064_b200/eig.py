@@ -33,20 +33,26 @@ class ShiftInvertOperator:
             if s.imag != 0:
                 raise RqError(2, "the B200 path takes real shifts only")
             s = s.real
-        for arr in (pencil.K, pencil.C, pencil.M):
-            if np.iscomplexobj(arr) and np.any(arr.imag != 0):
-                raise RqError(2, "the B200 path takes real pencils only")
+        resident = getattr(pencil, "device_resident", False)
+        if not resident:
+            for arr in (pencil.K, pencil.C, pencil.M):
+                if np.iscomplexobj(arr) and np.any(arr.imag != 0):
+                    raise RqError(2, "the B200 path takes real pencils only")
         self.pencil = pencil
         self.s = float(s)
         self.ordering = ordering if ordering is not None else nested_dissection_order(pencil)
         self.n = pencil.n
         opts = OperatorOpts(float(s), 1 if scaling else 0)
         self._h = C.c_void_p()
-        check(_lib.lib.rq_operator_create(
-            pencil.n, np.ascontiguousarray(pencil.rowptr, np.int64),
-            np.ascontiguousarray(pencil.col, np.int32), np.ascontiguousarray(pencil.K, np.float64),
-            np.ascontiguousarray(pencil.C, np.float64), np.ascontiguousarray(pencil.M, np.float64),
-            self.ordering.handle, C.byref(opts), C.byref(self._h)))
+        if resident:  # device-assembled K, C, M used in place
+            check(_lib.lib.rq_operator_create_pencil(pencil.handle, self.ordering.handle, C.byref(opts),
+                                                     C.byref(self._h)))
+        else:
+            check(_lib.lib.rq_operator_create(
+                pencil.n, np.ascontiguousarray(pencil.rowptr, np.int64),
+                np.ascontiguousarray(pencil.col, np.int32), np.ascontiguousarray(pencil.K, np.float64),
+                np.ascontiguousarray(pencil.C, np.float64), np.ascontiguousarray(pencil.M, np.float64),
+                self.ordering.handle, C.byref(opts), C.byref(self._h)))
         self.varsigma = _lib.lib.rq_operator_varsigma(self._h)
         self.last_info: dict = {}
         self.ledger: dict = {}

@@ -55,6 +55,42 @@ class QuadraticPencil:
         return sp.csr_matrix((vals, self.col, self.rowptr), shape=(self.n, self.n))
 
 
+class DevicePencil(QuadraticPencil):
+    """A device-assembled pencil whose K, C, M stay in HBM.
+
+    The pattern, supports and numbering are on the host as usual; K, C, M are
+    copied to host arrays on first access only. build_operator uses the
+    device values in place (rq_operator_create_pencil)."""
+
+    device_resident = True
+
+    def __init__(self, handle, **kw):
+        self._handle = handle
+        self._vals = {}
+        super().__init__(K=None, C=None, M=None, **kw)
+
+    def _get(self, which):
+        if which not in self._vals:
+            arrs = {w: np.empty(self.nnz) for w in "KCM"}
+            check(_lib.lib.rq_pencil_csr(self._handle, None, None, arrs["K"], arrs["C"], arrs["M"]))
+            self._vals.update(arrs)
+        return self._vals[which]
+
+    K = property(lambda self: self._get("K"), lambda self, v: None)
+    C = property(lambda self: self._get("C"), lambda self, v: None)
+    M = property(lambda self: self._get("M"), lambda self, v: None)
+
+    @property
+    def handle(self):
+        return self._handle
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            _lib.lib.rq_pencil_destroy(h)
+            self._handle = None
+
+
 def _desc(kind, degree, elems, levels, alpha=0.05, beta=0.01) -> SpaceDesc:
     return SpaceDesc(int(kind), int(degree), int(elems), int(levels), float(alpha), float(beta))
 
@@ -78,11 +114,38 @@ def boundary_mask(kind: int, degree: int, elems: int, levels: int = 0) -> np.nda
 
 
 def assemble(kind: int, degree: int, elems: int, levels: int = 0, alpha: float = 0.05,
-             beta: float = 0.01) -> QuadraticPencil:
-    """Assemble the BASELINE pencil (host C++, untimed input construction)."""
+             beta: float = 0.01, device: bool = False, resident: bool = False,
+             stage_ms=None) -> QuadraticPencil:
+    """Assemble the BASELINE pencil: host C++ (default) or, with device=True,
+    on the current CUDA device (bit-identical result; stage_ms, a float64
+    array of 5, receives the device ms of pattern / element / gather and the
+    host ms of the O(n) preparation and of the copy back). resident=True
+    (device only) returns a DevicePencil whose K, C, M stay in HBM."""
     d = _desc(kind, degree, elems, levels, alpha, beta)
     h = C.c_void_p()
-    check(_lib.lib.rq_pencil_assemble(C.byref(d), C.byref(h)))
+    if resident and not device:
+        raise RqError(2, "resident=True needs device=True")
+    if device:
+        ms = np.zeros(5) if stage_ms is None else stage_ms
+        check(_lib.lib.rq_pencil_assemble_device(C.byref(d), 1 if resident else 0, C.byref(h), ms))
+    else:
+        check(_lib.lib.rq_pencil_assemble(C.byref(d), C.byref(h)))
+    if resident:
+        try:
+            nf, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+            check(_lib.lib.rq_pencil_dims(h, C.byref(nf), C.byref(n), C.byref(nnz)))
+            rowptr = np.empty(n.value + 1, np.int64)
+            col = np.empty(nnz.value, np.int32)
+            check(_lib.lib.rq_pencil_csr(h, rowptr, col, None, None, None))
+            box = np.empty(4 * n.value, np.int32)
+            f2f = np.empty(n.value, np.int64)
+            check(_lib.lib.rq_pencil_supports(h, box, f2f))
+        except Exception:
+            _lib.lib.rq_pencil_destroy(h)
+            raise
+        return DevicePencil(h, kind=kind, degree=degree, elems=elems, levels=levels, n_full=nf.value,
+                            n=n.value, rowptr=rowptr, col=col, box=box.reshape(-1, 4),
+                            free_to_full=f2f, alpha=alpha, beta=beta)
     try:
         nf, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
         check(_lib.lib.rq_pencil_dims(h, C.byref(nf), C.byref(n), C.byref(nnz)))
@@ -101,7 +164,7 @@ def assemble(kind: int, degree: int, elems: int, levels: int = 0, alpha: float =
                            box.reshape(-1, 4), f2f, alpha, beta)
 
 
-def baseline_config(name: str) -> QuadraticPencil:
+def baseline_config(name: str, device: bool = False, resident: bool = False) -> QuadraticPencil:
     """The BASELINE.json configurations by short name."""
     table = {
         "cfg1": (DIV, 2, 32, 0), "cfg2_iga": (DIV, 3, 64, 0), "cfg2_riga": (DIV, 3, 64, 3),
@@ -115,4 +178,4 @@ def baseline_config(name: str) -> QuadraticPencil:
         table[f"cfg5_p{p}_riga"] = (CURL, p, 256, 5)
     if name not in table:
         raise RqError(2, f"unknown config {name!r}")
-    return assemble(*table[name])
+    return assemble(*table[name], device=device, resident=resident)

@@ -94,8 +94,12 @@ def test_singular_is_reported():
     assert e.value.category == "singular"
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2_riga", "cfg2_iga"])
-def test_multifrontal_vs_oracle(name):
+@pytest.mark.parametrize("name,sched", [("cfg1", "dag"), ("cfg2_riga", "dag"), ("cfg2_iga", "dag"),
+                                        ("cfg2_riga", "level")])
+def test_multifrontal_vs_oracle(name, sched, monkeypatch):
+    """Default task-DAG schedule, and the level-synchronous A/B path (RQB_FACTOR=level)."""
+    if sched == "level":
+        monkeypatch.setenv("RQB_FACTOR", "level")
     P = rq.baseline_config(name)
     o = rq.nested_dissection_order(P)
     Q = P.q_values(SIGMA)
