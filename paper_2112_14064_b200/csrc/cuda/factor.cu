@@ -27,6 +27,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -40,6 +41,19 @@ namespace rqb {
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     fail(errc::config, std::string("CUDA error: ") + cudaGetErrorString(e) + " in " + what);
+}
+
+static double wall_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+SetupTrace::SetupTrace(const char* w) : who(w), on(std::getenv("RQB_SETUP_TRACE") != nullptr), t0(wall_ms()) {}
+
+void SetupTrace::mark(const char* phase) {
+  if (!on) return;
+  const double t = wall_ms();
+  std::fprintf(stderr, "[setup] %s %s %.1f ms\n", who, phase, t - t0);
+  t0 = t;
 }
 
 DeviceBuffer::~DeviceBuffer() {
@@ -476,8 +490,51 @@ int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
 }  // namespace
 
+namespace {
+
+// Destination of every CSR entry in the front pool (the symbolic scatter map):
+// entry (i, j) goes to the front owning pivot min(p(i), p(j)), at the local
+// positions of p(i), p(j) in its sorted row list. One warp per matrix row.
+__global__ void scatter_map_k(int64_t n, const int64_t* __restrict__ rowptr,
+                              const int32_t* __restrict__ col, const int32_t* __restrict__ iperm,
+                              const int32_t* __restrict__ owner, const FrontDev* __restrict__ fronts,
+                              const int32_t* __restrict__ rows, int64_t* __restrict__ dst, int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+    const int32_t ni = iperm[i];
+    for (int64_t k = rowptr[i] + lane; k < rowptr[i + 1]; k += 32) {
+      const int32_t nj = iperm[col[k]];
+      const FrontDev F = fronts[owner[min(ni, nj)]];
+      const int32_t* rb = rows + F.rows_off;
+      int a = 0, b = F.nf;
+      while (a < b) {
+        const int m = (a + b) >> 1;
+        if (rb[m] < ni) a = m + 1; else b = m;
+      }
+      const int pi = a;
+      a = 0;
+      b = F.nf;
+      while (a < b) {
+        const int m = (a + b) >> 1;
+        if (rb[m] < nj) a = m + 1; else b = m;
+      }
+      const int pj = a;
+      if (pi == F.nf || rb[pi] != ni || pj == F.nf || rb[pj] != nj) {
+        atomicExch(bad, 1);
+        dst[k] = 0;
+      } else {
+        dst[k] = F.off + pi + static_cast<int64_t>(pj) * F.ld;
+      }
+    }
+  }
+}
+
+}  // namespace
+
 FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
-                           const int32_t* col, const double* aval)
+                           const int32_t* col, const double* aval, const int64_t* rowptr_dev,
+                           const int32_t* col_dev)
     : sym(s), n(n_) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -490,7 +547,8 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
   RQB_CUDA(cudaEventCreate(&ev0));
   RQB_CUDA(cudaEventCreate(&ev1));
   nnz = rowptr[n];
-  const std::vector<int64_t> dst = scatter_map(sym, n, rowptr, col);
+  SetupTrace tr("FactorEngine");
+  if (n != sym.n) fail(errc::dimension, "matrix size differs from the symbolic analysis");
 
   // Front descriptors, extend-add inverse maps, launch plans.
   const int nfr = static_cast<int>(sym.fronts.size());
@@ -576,12 +634,12 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
       P.off_panel[s] = push_list(P.panel_fronts[s]);
     }
   }
+  tr.mark("fronts+plans");
   d_pool.alloc(sizeof(double) * sym.pool);
   if (aval)
     d_aval.upload(aval, sizeof(double) * nnz, stream);
   else
     d_aval.alloc(sizeof(double) * nnz);  // values arrive by set_values_device
-  d_qdst.upload(dst.data(), sizeof(int64_t) * nnz, stream);
   d_rows.upload(sym.rows.data(), sizeof(int32_t) * sym.rows.size(), stream);
   d_fronts.upload(fronts_h.data(), sizeof(FrontDev) * fronts_h.size(), stream);
   if (inv.empty()) inv.push_back(-1);
@@ -597,12 +655,46 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
   d_xnew.alloc(sizeof(double) * n);
   d_cbvec.alloc(sizeof(double) * std::max<int64_t>(1, sym.cbvec));
   d_perm.upload(sym.perm.data(), sizeof(int32_t) * n, stream);
+  tr.mark("uploads");
+  {
+    // scatter map on the device (pattern from the caller's device copy when given)
+    std::vector<int32_t> owner(n);
+    for (size_t f = 0; f < sym.fronts.size(); ++f)
+      for (int k = 0; k < sym.fronts[f].npiv; ++k) owner[sym.fronts[f].start + k] = static_cast<int32_t>(f);
+    DeviceBuffer d_rp, d_cl, d_own, d_ip, d_bad;
+    if (!rowptr_dev) {
+      d_rp.upload(rowptr, sizeof(int64_t) * (n + 1), stream);
+      rowptr_dev = d_rp.as<int64_t>();
+    }
+    if (!col_dev) {
+      d_cl.upload(col, sizeof(int32_t) * std::max<int64_t>(nnz, 1), stream);
+      col_dev = d_cl.as<int32_t>();
+    }
+    d_own.upload(owner.data(), sizeof(int32_t) * n, stream);
+    d_ip.upload(sym.iperm.data(), sizeof(int32_t) * n, stream);
+    d_bad.alloc(sizeof(int));
+    RQB_CUDA(cudaMemsetAsync(d_bad.p, 0, sizeof(int), stream));
+    d_qdst.alloc(sizeof(int64_t) * std::max<int64_t>(nnz, 1));
+    const int64_t blocks = std::min<int64_t>(div_up(n, 8), 148 * 16);
+    if (n > 0)
+      scatter_map_k<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, stream>>>(
+          n, rowptr_dev, col_dev, d_ip.as<int32_t>(), d_own.as<int32_t>(), d_fronts.as<FrontDev>(),
+          d_rows.as<int32_t>(), d_qdst.as<int64_t>(), d_bad.as<int>());
+    RQB_CUDA(cudaGetLastError());
+    int bad = 0;
+    RQB_CUDA(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    RQB_CUDA(cudaStreamSynchronize(stream));
+    if (bad) fail(errc::dimension, "matrix entry outside the symbolic front structure");
+  }
+  tr.mark("scatter_map");
   rqb_solve_prepare(*this);
+  tr.mark("solve_prepare");
   {
     const char* mode = std::getenv("RQB_FACTOR");
     use_dag = !(mode && std::string(mode) == "level");
   }
   if (use_dag) rqb_dag_build(*this);
+  tr.mark("dag_build");
   RQB_CUDA(cudaFuncSetAttribute(front_lu_smem<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmallNf * kSmallNf * 8));
   RQB_CUDA(cudaFuncSetAttribute(panel_lu<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,

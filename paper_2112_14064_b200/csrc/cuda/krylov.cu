@@ -325,6 +325,7 @@ OperatorEngine::OperatorEngine(int64_t n_, const int64_t* rowptr, const int32_t*
     varsigma = std::sqrt(mk / mm);
   }
   sigma = sigma_ / varsigma;
+  SetupTrace tr("OperatorEngine(host)");
   std::vector<double> Cs(nnz), Ms(nnz), Q(nnz);
   const double v = varsigma, v2 = varsigma * varsigma;
   for (int64_t k = 0; k < nnz; ++k) {
@@ -333,14 +334,20 @@ OperatorEngine::OperatorEngine(int64_t n_, const int64_t* rowptr, const int32_t*
   }
   // Q(s) on the shared pattern, formed on the host once: K + s C + s^2 M
   for (int64_t k = 0; k < nnz; ++k) Q[k] = K[k] + sigma_ * C[k] + sigma_ * sigma_ * M[k];
-  fac = std::make_unique<FactorEngine>(s, n, rowptr, col, Q.data());
+  tr.mark("scale+Q");
+  d_rowptr.alloc(sizeof(int64_t) * (n + 1));
+  d_col.alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  RQB_CUDA(cudaMemcpy(d_rowptr.p, rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+  RQB_CUDA(cudaMemcpy(d_col.p, col, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+  fac = std::make_unique<FactorEngine>(s, n, rowptr, col, Q.data(), d_rowptr.as<int64_t>(),
+                                       d_col.as<int32_t>());
+  tr.mark("FactorEngine");
   stream = fac->stream;
-  d_rowptr.upload(rowptr, sizeof(int64_t) * (n + 1), stream);
-  d_col.upload(col, sizeof(int32_t) * nnz, stream);
   d_K.upload(K, sizeof(double) * nnz, stream);
   d_C.upload(Cs.data(), sizeof(double) * nnz, stream);
   d_M.upload(Ms.data(), sizeof(double) * nnz, stream);
   d_Q.upload(Q.data(), sizeof(double) * nnz, stream);
+  tr.mark("uploads");
   init_workspaces();
 }
 
@@ -415,7 +422,10 @@ OperatorEngine::OperatorEngine(const DevicePencil& dp, const int64_t* rowptr_h, 
   RQB_CUDA(cudaGetDevice(&dev));
   if (dev != dp.device) fail(errc::config, "device pencil lives on another CUDA device");
   if (rowptr_h[n] != nnz) fail(errc::config, "device pencil / host pattern mismatch");
-  fac = std::make_unique<FactorEngine>(s, n, rowptr_h, col_h, nullptr);
+  SetupTrace tr("OperatorEngine(device)");
+  fac = std::make_unique<FactorEngine>(s, n, rowptr_h, col_h, nullptr, dp.d_rowptr.as<int64_t>(),
+                                       dp.d_col.as<int32_t>());
+  tr.mark("FactorEngine");
   stream = fac->stream;
   d_rowptr.alloc(sizeof(int64_t) * (n + 1));
   d_col.alloc(sizeof(int32_t) * nnz);
@@ -457,10 +467,12 @@ OperatorEngine::OperatorEngine(const DevicePencil& dp, const int64_t* rowptr_h, 
   RQB_CUDA(cudaStreamSynchronize(stream));
   if (norms1)
     for (int i = 0; i < 3; ++i) std::memcpy(&norms1[i], &h_red[2 + i], sizeof(double));
+  tr.mark("scale+Q+norms");
   init_workspaces();
 }
 
 void OperatorEngine::init_workspaces() {
+  SetupTrace tr("init_workspaces");
   d_w.alloc(sizeof(double) * 2 * n);
   d_t.alloc(sizeof(double) * 2 * n);
   nparts = kRedBlocks;
@@ -476,7 +488,9 @@ void OperatorEngine::init_workspaces() {
     cublasSetStream(h, stream);
   }
   RQB_CUDA(cudaStreamSynchronize(stream));
+  tr.mark("alloc+cublas");
   fac->factor();
+  tr.mark("factor");
 }
 
 OperatorEngine::~OperatorEngine() {

@@ -29,6 +29,15 @@ struct FrontDev {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// Host setup phase timer (RQB_SETUP_TRACE=1: one stderr line per phase).
+struct SetupTrace {
+  const char* who;
+  bool on;
+  double t0;
+  explicit SetupTrace(const char* w);
+  void mark(const char* phase);
+};
+
 struct DeviceBuffer {
   void* p = nullptr;
   size_t bytes = 0;
@@ -112,8 +121,12 @@ struct FactorEngine {
   cudaGraph_t graph_factor = nullptr;
   cudaGraphExec_t graph_factor_exec = nullptr;
 
+  // rowptr/col: host pattern; rowptr_dev/col_dev: optional device copy of it
+  // (the scatter map is built on the device); aval: host values or nullptr
+  // (then set_values_device before factor()).
   FactorEngine(const Symbolic& s, int64_t n, const int64_t* rowptr, const int32_t* col,
-               const double* aval);
+               const double* aval, const int64_t* rowptr_dev = nullptr,
+               const int32_t* col_dev = nullptr);
   ~FactorEngine();
   // Numeric factorization of the values currently in d_aval (device time in
   // last_ms). Returns the singular flag.

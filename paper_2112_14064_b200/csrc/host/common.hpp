@@ -145,9 +145,8 @@ struct Symbolic {
 
 Symbolic nested_dissection(int64_t n, const int32_t* box, int elems, int leaf);
 
-// Per-CSR-entry destination in the front pool for A(i,j) (original ids).
-std::vector<int64_t> scatter_map(const Symbolic& s, int64_t n, const int64_t* rowptr,
-                                 const int32_t* col);
+// (The per-CSR-entry destination in the front pool — the scatter map — is
+// built on the device: cuda/factor.cu scatter_map_k.)
 
 inline uint64_t splitmix64(uint64_t& x) {
   uint64_t z = (x += 0x9E3779B97F4A7C15ull);

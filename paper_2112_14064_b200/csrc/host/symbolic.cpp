@@ -177,29 +177,4 @@ Symbolic nested_dissection(int64_t n, const int32_t* box, int elems, int leaf) {
   return S;
 }
 
-std::vector<int64_t> scatter_map(const Symbolic& s, int64_t n, const int64_t* rowptr,
-                                 const int32_t* col) {
-  if (n != s.n) fail(errc::dimension, "matrix size differs from the symbolic analysis");
-  std::vector<int32_t> owner(n);
-  for (size_t f = 0; f < s.fronts.size(); ++f)
-    for (int k = 0; k < s.fronts[f].npiv; ++k) owner[s.fronts[f].start + k] = static_cast<int32_t>(f);
-  const int64_t nnz = rowptr[n];
-  std::vector<int64_t> dst(nnz);
-  for (int64_t i = 0; i < n; ++i) {
-    const int32_t ni = s.iperm[i];
-    for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
-      const int32_t nj = s.iperm[col[k]];
-      const Front& F = s.fronts[owner[std::min(ni, nj)]];
-      const int32_t* rb = s.rows.data() + F.rows_off;
-      const int32_t* re = rb + F.nf;
-      const int32_t* pi = std::lower_bound(rb, re, ni);
-      const int32_t* pj = std::lower_bound(rb, re, nj);
-      if (pi == re || *pi != ni || pj == re || *pj != nj)
-        fail(errc::dimension, "matrix entry outside the symbolic front structure");
-      dst[k] = F.off + (pi - rb) + static_cast<int64_t>(pj - rb) * F.ld;
-    }
-  }
-  return dst;
-}
-
 }  // namespace rqb
