@@ -107,17 +107,24 @@ __global__ void asm_fill(AsmArgs A, const int64_t* rowptr, int32_t* col) {
        r += nwarps) {
     const RowRange R = row_range(A, r);
     int64_t pos = rowptr[r];
-    for (int c = 0; c < 2; ++c)
-      for (int j = R.j0[c]; j <= R.j1[c]; ++j) {
-        const int32_t* f = A.f2f + A.base[c] + static_cast<int64_t>(j) * A.nbx[c];
-        for (int i0 = R.i0[c]; i0 <= R.i1[c]; i0 += 32) {
-          const int i = i0 + lane;
-          const int32_t v = i <= R.i1[c] ? f[i] : -1;
-          const unsigned m = __ballot_sync(0xffffffffu, v >= 0);
-          if (v >= 0) col[pos + __popc(m & ((1u << lane) - 1u))] = v;
-          pos += __popc(m);
+    // the (j, i) box of each component flattened j-major: lanes cover whole
+    // box rows at once, and the flattened order is the sorted column order
+    for (int c = 0; c < 2; ++c) {
+      const int w = R.i1[c] - R.i0[c] + 1, h = R.j1[c] - R.j0[c] + 1;
+      if (w <= 0 || h <= 0) continue;
+      const int32_t* f = A.f2f + A.base[c] + static_cast<int64_t>(R.j0[c]) * A.nbx[c] + R.i0[c];
+      for (int t0 = 0; t0 < w * h; t0 += 32) {
+        const int t = t0 + lane;
+        int32_t v = -1;
+        if (t < w * h) {
+          const int jj = t / w;
+          v = f[static_cast<int64_t>(jj) * A.nbx[c] + (t - jj * w)];
         }
+        const unsigned m = __ballot_sync(0xffffffffu, v >= 0);
+        if (v >= 0) col[pos + __popc(m & ((1u << lane) - 1u))] = v;
+        pos += __popc(m);
       }
+    }
   }
 }
 
