@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librq_b200.so")
+# RQB_LIB: alternative build of the same library (development A/B runs only)
+LIB_PATH = os.environ.get("RQB_LIB") or os.path.join(_HERE, "librq_b200.so")
 
 # rq::errc (reference proj/include/rigaqep/types.hpp:14-23)
 ERRC = {1: "generic", 2: "config", 3: "assembly", 4: "solver", 5: "verification",

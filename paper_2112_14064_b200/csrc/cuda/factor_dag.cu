@@ -15,7 +15,12 @@
 //                      over fully-summed rows -> per-panel flag (panel backed up)
 //   COLS(f, s, b)      64-column tile column right of the block: U12 = inv(L11) A12
 //   UPD(f, s, a, b)    64x64 tile -= L21 U12 on FP64 tensor cores (mma.sync
-//                      m16n8k4 f64 -> DMMA.8x8x4)
+//                      m16n8k4 f64 -> DMMA.8x8x4), for tiles that hold pivot
+//                      rows or pivot columns (they feed later panels)
+//   UPDCB(f, a, b)     64x64 tile of the contribution block (rows and columns
+//                      past npiv): ONE update with K = npiv after the last
+//                      panel (cp.async double-buffered K loop, DMMA), instead
+//                      of one K = 32 read-modify-write per panel step
 // The last of DIAG/ROWS/COLS of a panel to finish checks the flag. If every
 // multiplier of a fully-summed row satisfies |l| <= 10 (1 - 1e-14), the
 // threshold-0.1 rule would have kept every
@@ -56,12 +61,14 @@ constexpr int kCnt = 5;  // per-front counters: tasks, asm, diag, rc, released
 // fronts (nf <= 160 factored whole in 206 KB of shared memory, one CTA per
 // SM); large problems are throughput bound and want two CTAs per SM (task
 // latency of one hidden behind the other: 113 KB of shared memory and 128
-// registers each, SMALL fronts up to nf = 118).
+// registers each, SMALL fronts up to nf = 256 whose pivot cross fits 112 KB).
 constexpr int kSmallNfLatency = 160;
-constexpr int kSmallNfThroughput = 118;
+constexpr int kSmallNfThroughput = kDT;  // any front whose pivot cross fits 112 KB
+constexpr size_t kSmallBytesLatency = 160 * 161 * 8;     // 206 KB: one CTA per SM
+constexpr size_t kSmallBytesThroughput = 118 * 119 * 8;  // 112 KB: two CTAs per SM
 constexpr double kThroughputFlops = 2e9;  // F_LU above which the two-CTA variant is used
 
-enum : int16_t { T_SMALL = 0, T_ASM = 1, T_DIAG = 2, T_ROWS = 3, T_COLS = 4, T_UPD = 5 };
+enum : int16_t { T_SMALL = 0, T_ASM = 1, T_DIAG = 2, T_ROWS = 3, T_COLS = 4, T_UPD = 5, T_UPDCB = 6 };
 
 struct Task {
   int32_t front;
@@ -81,7 +88,9 @@ struct FrontDag {
   int32_t task_base;   // first task of this front
   int32_t sb_off;      // offset into step_base[] (steps + 1 entries)
   int32_t parent;      // parent front (-1 root)
-  int32_t pad2;
+  int32_t acb;         // first contribution-block tile (rows / columns >= npiv)
+  int32_t cb_base;     // first UPDCB task ((tiles - acb)^2 of them, row-major)
+  int32_t pad3;
   int64_t backup_off;  // panel backup nf x 32, then A12 backup 32 x nf
 };
 
@@ -158,73 +167,49 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 // Children's Schur blocks into front F (child-centric scatter, atomic-free:
 // rel is injective, children are applied one after the other). For child ch
 // only its CB columns [lo[ch], hi[ch]) are applied; parent column c lives at
-// dst + c * ldd (shared or global memory).
+// dst + c * ldd (shared or global memory). Latency: a warp takes four child
+// columns x 64 rows per iteration, all 16 loads (8 child values, 8 parent
+// values) in flight before the first add.
 __device__ void extend_add(const DagArgs& A, const FrontDev& F, const int* lo, const int* hi,
                            double* dst, int64_t ldd, bool dst_global) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kW = kDT / 32;
+  constexpr int kW = kDT / 32, kC = 4, kU = 2;
   for (int ch = 0; ch < F.nchild; ++ch) {
     const FrontDev C = A.fronts[ch == 0 ? F.child0 : F.child1];
     const int32_t* rel = A.rel + C.rel_off;
     const int ncb = C.nf - C.npiv;
     const double* cp = A.pool + C.off + C.npiv + (int64_t)C.npiv * C.ld;  // CB block origin
-    if (ncb <= 128) {
-      // the child's row map is the same for every column: load it once; two
-      // columns per warp iteration keep eight child loads in flight per lane
-      int pr[4];
+    for (int ic0 = lo[ch] + warp * kC; ic0 < hi[ch]; ic0 += kW * kC) {
+      const double* src[kC];
+      double* dcol[kC];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int kk = lane + 32 * u;
-        pr[u] = kk < ncb ? __ldg(&rel[kk]) : -1;
+      for (int j = 0; j < kC; ++j) {
+        const int ic = min(ic0 + j, hi[ch] - 1);
+        src[j] = cp + (int64_t)ic * C.ld;
+        dcol[j] = dst + (int64_t)__ldg(&rel[ic]) * ldd;
       }
-      for (int ic = lo[ch] + warp; ic < hi[ch]; ic += 2 * kW) {
-        const int ic2 = ic + kW;
-        const bool two = ic2 < hi[ch];
-        const int pc1 = __ldg(&rel[ic]), pc2 = two ? __ldg(&rel[ic2]) : pc1;
-        const double* s1 = cp + (int64_t)ic * C.ld;
-        const double* s2 = cp + (int64_t)(two ? ic2 : ic) * C.ld;
-        double v1[4], v2[4], d1[4], d2[4];
+      const int ncol = min(kC, hi[ch] - ic0);
+      for (int k0 = 0; k0 < ncb; k0 += 32 * kU) {
+        int pr[kU];
+        double v[kC][kU], d[kC][kU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          v1[u] = pr[u] >= 0 ? __ldcg(&s1[lane + 32 * u]) : 0.0;
-          v2[u] = (two && pr[u] >= 0) ? __ldcg(&s2[lane + 32 * u]) : 0.0;
+        for (int u = 0; u < kU; ++u) {
+          const int kk = k0 + lane + 32 * u;
+          pr[u] = kk < ncb ? __ldg(&rel[kk]) : -1;
         }
-        double* dc1 = dst + (int64_t)pc1 * ldd;
-        double* dc2 = dst + (int64_t)pc2 * ldd;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (pr[u] >= 0) {
-            d1[u] = dst_global ? __ldcg(&dc1[pr[u]]) : dc1[pr[u]];
-            if (two) d2[u] = dst_global ? __ldcg(&dc2[pr[u]]) : dc2[pr[u]];
+        for (int j = 0; j < kC; ++j)
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const bool ok = j < ncol && pr[u] >= 0;
+            v[j][u] = ok ? __ldcg(&src[j][k0 + lane + 32 * u]) : 0.0;
+            d[j][u] = ok ? (dst_global ? __ldcg(&dcol[j][pr[u]]) : dcol[j][pr[u]]) : 0.0;
           }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (pr[u] >= 0) {
-            dc1[pr[u]] = d1[u] + v1[u];
-            if (two) dc2[pr[u]] = d2[u] + v2[u];
-          }
-      }
-    } else {
-      for (int ic = lo[ch] + warp; ic < hi[ch]; ic += kW) {
-        const int pc = __ldg(&rel[ic]);
-        const double* src = cp + (int64_t)ic * C.ld;
-        double* dcol = dst + (int64_t)pc * ldd;
-        for (int k0 = 0; k0 < ncb; k0 += 128) {
-          int pr[4];
-          double v[4], d[4];
+        for (int j = 0; j < kC; ++j)
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int kk = k0 + lane + 32 * u;
-            pr[u] = kk < ncb ? __ldg(&rel[kk]) : -1;
-            v[u] = kk < ncb ? __ldcg(&src[kk]) : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (pr[u] >= 0) d[u] = dst_global ? __ldcg(&dcol[pr[u]]) : dcol[pr[u]];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (pr[u] >= 0) dcol[pr[u]] = d[u] + v[u];
-        }
+          for (int u = 0; u < kU; ++u)
+            if (j < ncol && pr[u] >= 0) dcol[j][pr[u]] = d[j][u] + v[j][u];
       }
     }
     __syncthreads();  // two children may touch the same entries
@@ -239,25 +224,87 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
 }
 
 // ---------------------------------------------------------------------------
+// dst(r, c) -= sum_{k0 <= k < k0 + kw} L(r, k) U(k, c) over r in [r0, r1),
+// c in [c0, c1), DMMA on 16 x 32 warp tiles: L(r, k) = Lb[r + k * ldl],
+// U(k, c) = Ub[k + (c - uoff) * ldu], dst(r, c) = D[r + (c - doff) * ldd]
+// (shared memory, or the front in global memory when kGlobal).
+template <bool kGlobal>
+__device__ __forceinline__ void cross_update(const double* Lb, int ldl, const double* Ub, int ldu, int uoff,
+                                             double* D, int64_t ldd, int doff, int r0, int r1, int c0,
+                                             int c1, int k0, int kw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int mt = (r1 - r0 + 15) / 16, nt = (c1 - c0 + 31) / 32;
+  for (int tile = warp; tile < mt * nt; tile += kDT / 32) {
+    const int rr = r0 + (tile % mt) * 16, cc = c0 + (tile / mt) * 32;
+    double acc[4][4];
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[y][e] = 0.0;
+    const int ra = rr + gid, rb = rr + gid + 8;
+#pragma unroll 4
+    for (int kk = 0; kk < kw; kk += 4) {
+      const int kc = k0 + kk + tig;
+      const bool kin = kk + tig < kw;
+      const double a0 = (kin && ra < r1) ? Lb[ra + kc * ldl] : 0.0;
+      const double a1 = (kin && rb < r1) ? Lb[rb + kc * ldl] : 0.0;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int cb = cc + y * 8 + gid;
+        const double b0 = (kin && cb < c1) ? Ub[kc + (cb - uoff) * ldu] : 0.0;
+        dmma(acc[y], a0, a1, b0);
+      }
+    }
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = rr + gid + (e >> 1) * 8, c = cc + y * 8 + 2 * tig + (e & 1);
+        if (r < r1 && c < c1) {
+          double* p = &D[r + (int64_t)(c - doff) * ldd];
+          *p = (kGlobal ? __ldcg(p) : *p) - acc[y][e];
+        }
+      }
+  }
+}
+
+// SMALL front (nf <= 256 = one thread per row): the pivot "cross" lives in
+// shared memory — the column block Cb (all nf rows x npiv columns) and the row
+// block Rb (npiv rows x the ncb contribution columns) — so the shared memory
+// need is npiv (2 nf - npiv) doubles instead of nf^2. Children's Schur blocks
+// are added in global memory first, the cross is factored with 16-column
+// panels (one warp-shuffle-free row per thread, speculative unpivoted panel
+// with exact threshold-pivoted redo), and the contribution block gets ONE
+// K = npiv DMMA update straight from the cross to global memory.
 __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int* piv_sh) {
-  const int nf = F.nf, np = F.npiv, lds = nf | 1;
+  const int nf = F.nf, np = F.npiv;
+  const int ldc = nf | 1, ldr = np | 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* g = A.pool + F.off;
-  // the whole front in flight at once (no register staging, one latency)
-  for (int c = warp; c < nf; c += kDT / 32)
-    for (int r = lane; r < nf; r += 32) cp_async8(&sm[r + c * lds], &g[r + (int64_t)c * F.ld]);
+  const int64_t ld = F.ld;
+  double* Cb = sm;                             // (r, c < np)   -> Cb[r + c * ldc]
+  double* Rb = sm + (int64_t)ldc * np;         // (r < np, c >= np) -> Rb[r + (c - np) * ldr]
+  if (F.nchild > 0) {
+    int lo[2] = {0, 0}, hi[2] = {0, 0};
+    hi[0] = A.fronts[F.child0].nf - A.fronts[F.child0].npiv;
+    if (F.nchild > 1) hi[1] = A.fronts[F.child1].nf - A.fronts[F.child1].npiv;
+    extend_add(A, F, lo, hi, g, ld, true);  // ends with a barrier
+  }
+  // the cross in flight at once (one latency); the lines were never read
+  // through L1 in this launch (extend_add reads with ld.cg)
+  for (int c = warp; c < nf; c += kDT / 32) {
+    const int rows = c < np ? nf : np;
+    double* dst = c < np ? Cb + (int64_t)c * ldc : Rb + (int64_t)(c - np) * ldr;
+    for (int r = lane; r < rows; r += 32) cp_async8(&dst[r], &g[r + (int64_t)c * ld]);
+  }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  {
-    int lo[2] = {0, 0}, hi[2] = {0, 0};
-    if (F.nchild > 0) hi[0] = A.fronts[F.child0].nf - A.fronts[F.child0].npiv;
-    if (F.nchild > 1) hi[1] = A.fronts[F.child1].nf - A.fronts[F.child1].npiv;
-    extend_add(A, F, lo, hi, sm, lds, false);
-  }
   __shared__ double red_s[kDT / 32];
   __shared__ double urow_s[2][kPB];
   __shared__ int any_swap_s;
   double* pbk = A.small_backup + (int64_t)blockIdx.x * A.small_nf * kPB;
+  auto at = [&](int r, int c) -> double& { return c < np ? Cb[r + c * ldc] : Rb[r + (c - np) * ldr]; };
   for (int k0 = 0; k0 < np; k0 += kPB) {
     const int pw = min(kPB, np - k0);
     // ---- speculative unpivoted panel: thread t owns row t in registers; the
@@ -269,7 +316,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
       const bool own = i >= k0 && i < nf;
       double a[kPB];
 #pragma unroll
-      for (int c = 0; c < kPB; ++c) a[c] = (own && c < pw) ? sm[i + (k0 + c) * lds] : 0.0;
+      for (int c = 0; c < kPB; ++c) a[c] = (own && c < pw) ? Cb[i + (k0 + c) * ldc] : 0.0;
       if (own)
 #pragma unroll
         for (int c = 0; c < kPB; ++c)
@@ -296,7 +343,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
       if (own)
 #pragma unroll
         for (int c = 0; c < kPB; ++c)
-          if (c < pw) sm[i + (k0 + c) * lds] = a[c];
+          if (c < pw) Cb[i + (k0 + c) * ldc] = a[c];
     }
     __syncthreads();
     if (sing) lm = 1e300;
@@ -315,7 +362,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
     } else {
       // restore the panel, redo it with exact threshold pivoting (warp 0)
       if (tid < nf && tid >= k0)
-        for (int c = 0; c < pw; ++c) sm[tid + (k0 + c) * lds] = pbk[tid + c * A.small_nf];
+        for (int c = 0; c < pw; ++c) Cb[tid + (k0 + c) * ldc] = pbk[tid + c * A.small_nf];
       __syncthreads();
       if (tid == 0) any_swap_s = 1;
     }
@@ -325,11 +372,11 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
         double best = -1.0;
         int bi = j;
         for (int i = j + lane; i < np; i += 32) {
-          const double v = fabs(sm[i + j * lds]);
+          const double v = fabs(Cb[i + j * ldc]);
           if (v > best) best = v, bi = i;
         }
         warp_argmax(best, bi);
-        const double diag = fabs(sm[j + j * lds]);
+        const double diag = fabs(Cb[j + j * ldc]);
         int p = diag >= kPivThreshold * best ? j : bi;
         if (!(best >= kSingularTiny)) {
           if (lane == 0) atomicOr(&A.flags[0], 1);
@@ -342,89 +389,65 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
         }
         if (p != j && lane < pw) {
           const int c = k0 + lane;
-          const double t = sm[j + c * lds];
-          sm[j + c * lds] = sm[p + c * lds];
-          sm[p + c * lds] = t;
+          const double t = Cb[j + c * ldc];
+          Cb[j + c * ldc] = Cb[p + c * ldc];
+          Cb[p + c * ldc] = t;
         }
         __syncwarp();
-        const double ujj = sm[j + j * lds];
+        const double ujj = Cb[j + j * ldc];
         for (int i = j + 1 + lane; i < nf; i += 32) {
-          const double l = sm[i + j * lds] / ujj;
-          sm[i + j * lds] = l;
-          for (int c = j + 1; c < k0 + pw; ++c) sm[i + c * lds] -= l * sm[j + c * lds];
+          const double l = Cb[i + j * ldc] / ujj;
+          Cb[i + j * ldc] = l;
+          for (int c = j + 1; c < k0 + pw; ++c) Cb[i + c * ldc] -= l * Cb[j + c * ldc];
         }
         __syncwarp();
       }
     }
     __syncthreads();
-    if (any_swap_s)
+    if (any_swap_s)  // pivot rows (< np) swapped across the other columns of the cross
       for (int c = tid; c < nf; c += kDT) {
         if (c >= k0 && c < k0 + pw) continue;
         for (int jj = 0; jj < pw; ++jj) {
           const int p = piv_sh[jj], j = k0 + jj;
           if (p != j) {
-            const double t = sm[j + c * lds];
-            sm[j + c * lds] = sm[p + c * lds];
-            sm[p + c * lds] = t;
+            const double t = at(j, c);
+            at(j, c) = at(p, c);
+            at(p, c) = t;
           }
         }
       }
     __syncthreads();
-    // U12 = inv(L11) A12: thread per column, the 16-row segment in registers
+    // U12 = inv(L11) A12 over the panel rows, all columns right of the panel
     for (int c = k0 + pw + tid; c < nf; c += kDT) {
       double u[kPB];
 #pragma unroll
-      for (int jj = 0; jj < kPB; ++jj) u[jj] = jj < pw ? sm[k0 + jj + c * lds] : 0.0;
+      for (int jj = 0; jj < kPB; ++jj) u[jj] = jj < pw ? at(k0 + jj, c) : 0.0;
 #pragma unroll
       for (int jj = 1; jj < kPB; ++jj) {
         double sv = u[jj];
 #pragma unroll
-        for (int t = 0; t < jj; ++t) sv -= sm[k0 + jj + (k0 + t) * lds] * u[t];
+        for (int t = 0; t < jj; ++t) sv -= Cb[k0 + jj + (k0 + t) * ldc] * u[t];
         u[jj] = sv;
       }
 #pragma unroll
       for (int jj = 0; jj < kPB; ++jj)
-        if (jj < pw) sm[k0 + jj + c * lds] = u[jj];
+        if (jj < pw) at(k0 + jj, c) = u[jj];
     }
     __syncthreads();
-    const int t0 = k0 + pw, T = nf - t0;
-    if (T > 0) {
-      const int mt = (T + 15) / 16, nt = (T + 31) / 32;
-      const int gid = lane >> 2, tig = lane & 3;
-      for (int tile = warp; tile < mt * nt; tile += kDT / 32) {
-        const int r0 = t0 + (tile % mt) * 16, c0 = t0 + (tile / mt) * 32;
-        double acc[4][4];
-#pragma unroll
-        for (int y = 0; y < 4; ++y)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[y][e] = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < kPB; kk += 4) {
-          const int kc = k0 + kk + tig;
-          const bool kin = kk + tig < pw;
-          const int ra = r0 + gid, rb = r0 + gid + 8;
-          const double a0 = (kin && ra < nf) ? sm[ra + kc * lds] : 0.0;
-          const double a1 = (kin && rb < nf) ? sm[rb + kc * lds] : 0.0;
-#pragma unroll
-          for (int y = 0; y < 4; ++y) {
-            const int cb = c0 + y * 8 + gid;
-            const double b0 = (kin && cb < nf) ? sm[kc + cb * lds] : 0.0;
-            dmma(acc[y], a0, a1, b0);
-          }
-        }
-#pragma unroll
-        for (int y = 0; y < 4; ++y)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int r = r0 + gid + (e >> 1) * 8, c = c0 + y * 8 + 2 * tig + (e & 1);
-            if (r < nf && c < nf) sm[r + c * lds] -= acc[y][e];
-          }
-      }
-    }
+    // trailing update of the cross only: pivot columns (all rows) and the
+    // pivot rows of the contribution columns
+    const int t0 = k0 + pw;
+    if (t0 < np) cross_update<false>(Cb, ldc, Cb, ldc, 0, Cb, ldc, 0, t0, nf, t0, np, k0, pw);
+    if (t0 < np && np < nf) cross_update<false>(Cb, ldc, Rb, ldr, np, Rb, ldr, np, t0, np, np, nf, k0, pw);
     __syncthreads();
   }
-  for (int c = warp; c < nf; c += kDT / 32)
-    for (int r = lane; r < nf; r += 32) g[r + (int64_t)c * F.ld] = sm[r + c * lds];
+  for (int c = warp; c < nf; c += kDT / 32) {
+    const int rows = c < np ? nf : np;
+    const double* src = c < np ? Cb + (int64_t)c * ldc : Rb + (int64_t)(c - np) * ldr;
+    for (int r = lane; r < rows; r += 32) g[r + (int64_t)c * ld] = src[r];
+  }
+  // contribution block: one K = npiv pass, operands from the cross
+  if (np < nf) cross_update<true>(Cb, ldc, Rb, ldr, np, g, ld, 0, np, nf, np, nf, 0, np);
 }
 
 // DIAG: 32x32 diagonal block of panel s, unpivoted (speculative), in the
@@ -694,6 +717,107 @@ __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int 
       }
 }
 
+__device__ __forceinline__ void cp_async8z(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 8 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
+
+// Contribution-block tile (a, b): C -= L(rows a, 0:npiv) U(0:npiv, cols b) in
+// one pass, K in chunks of 32 staged by cp.async (two buffers: the next chunk
+// is in flight while DMMA consumes the current one), C read once and written
+// once. Runs after the front's last panel is released: every L and U column
+// is final (pivot swaps never touch contribution-block rows).
+__device__ void updcb_task(const DagArgs& A, const FrontDev& F, int a, int b, double* sm) {
+  const int r0 = a * kTile, r1 = min(r0 + kTile, F.nf);
+  const int c0 = b * kTile, c1 = min(c0 + kTile, F.nf);
+  const int K = F.npiv;
+  double* g = A.pool + F.off;
+  const int64_t ld = F.ld;
+  const int tid = threadIdx.x;
+  const int nr = r1 - r0, nc = c1 - c0;
+  const int lane = tid & 31, warp = tid >> 5;  // 8 warps: 2 (m) x 4 (n) of 32 x 16
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int gid = lane >> 2, tig = lane & 3;
+  constexpr int kStage = 2 * kNB * kTSP;  // As [kk][m] then Bs [kk][n]
+  auto issue = [&](int chunk, int buf) {
+    double* As = sm + buf * kStage;
+    double* Bs = As + kNB * kTSP;
+    const int k0 = chunk * kNB;
+#pragma unroll
+    for (int i = 0; i < kNB * kTile / kDT; ++i) {
+      const int idx = tid + i * kDT;
+      const int kk = idx / kTile, m = idx % kTile;
+      const bool ok = k0 + kk < K && m < nr;
+      cp_async8z(&As[kk * kTSP + m], ok ? &g[(r0 + m) + (int64_t)(k0 + kk) * ld] : g, ok);
+    }
+#pragma unroll
+    for (int i = 0; i < kNB * kTile / kDT; ++i) {
+      const int idx = tid + i * kDT;
+      const int kk = idx % kNB, n = idx / kNB;
+      const bool ok = k0 + kk < K && n < nc;
+      cp_async8z(&Bs[kk * kTSP + n], ok ? &g[(k0 + kk) + (int64_t)(c0 + n) * ld] : g, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int nchunks = (K + kNB - 1) / kNB;
+  issue(0, 0);
+  double cv[2][2][4];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = wm + x * 16 + gid + (e >> 1) * 8, c = wn + y * 8 + 2 * tig + (e & 1);
+        cv[x][y][e] = (r < nr && c < nc) ? __ldcg(&g[(r0 + r) + (int64_t)(c0 + c) * ld]) : 0.0;
+      }
+  double acc[2][2][4];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[x][y][e] = 0.0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    if (ch + 1 < nchunks) {
+      issue(ch + 1, (ch + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* As = sm + (ch & 1) * kStage;
+    const double* Bs = As + kNB * kTSP;
+#pragma unroll
+    for (int ks = 0; ks < kNB / 4; ++ks) {
+      const int kr = ks * 4 + tig;
+      double af[2][2], bf[2];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        af[x][0] = As[kr * kTSP + wm + x * 16 + gid];
+        af[x][1] = As[kr * kTSP + wm + x * 16 + gid + 8];
+      }
+#pragma unroll
+      for (int y = 0; y < 2; ++y) bf[y] = Bs[kr * kTSP + wn + y * 8 + gid];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) dmma(acc[x][y], af[x][0], af[x][1], bf[y]);
+    }
+    __syncthreads();  // buffer (ch & 1) is refilled by the issue of chunk ch + 2
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = wm + x * 16 + gid + (e >> 1) * 8, c = wn + y * 8 + 2 * tig + (e & 1);
+        if (r < nr && c < nc) g[(r0 + r) + (int64_t)(c0 + c) * ld] = cv[x][y][e] - acc[x][y][e];
+      }
+}
+
 // Exact threshold-pivoted redo of panel s (rare path, one CTA).
 __device__ void panel_fallback(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s,
                                double* sm) {
@@ -708,7 +832,9 @@ __device__ void panel_fallback(const DagArgs& A, const FrontDev& F, const FrontD
   if (tid == 0) {
     const int a0 = k / kTile;
     for (int a = a0; a < D.tiles; ++a)
-      for (int b = a0; b < D.tiles; ++b) spin_ge(&A.tile_step[D.tile_off + a * D.tiles + b], s, A.flags);
+      for (int b = a0; b < D.tiles; ++b)
+        if (a < D.acb || b < D.acb)  // contribution-block tiles are not updated per step
+          spin_ge(&A.tile_step[D.tile_off + a * D.tiles + b], s, A.flags);
     __threadfence();
   }
   __syncthreads();
@@ -800,10 +926,16 @@ __device__ __forceinline__ int idx_cols(const DagArgs& A, const FrontDag& D, con
   const int a0 = a0_of(F, s);
   return A.step_base[D.sb_off + s] + 1 + nr_of(F, D, s) + (b - a0);
 }
+// UPD tasks of step s: the trailing tiles (a, b) with a < acb or b < acb, in
+// the order: pivot-region tile rows in full, then contribution-block rows
+// restricted to pivot-region columns (same layout as rqb_dag_build)
+__device__ __forceinline__ bool eager_tile(const FrontDag& D, int a, int b) { return a < D.acb || b < D.acb; }
 __device__ __forceinline__ int idx_upd(const DagArgs& A, const FrontDag& D, const FrontDev& F, int s, int a,
                                         int b) {
   const int a0 = a0_of(F, s), nr = nr_of(F, D, s);
-  return A.step_base[D.sb_off + s] + 1 + 2 * nr + (a - a0) * nr + (b - a0);
+  const int np = max(0, D.acb - a0), x = a - a0, y = b - a0;
+  const int base = A.step_base[D.sb_off + s] + 1 + 2 * nr;
+  return x < np ? base + x * nr + y : base + np * nr + (x - np) * np + y;
 }
 
 // One predecessor of task t completed: the last one pushes t on the ready queue.
@@ -882,6 +1014,7 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
       case T_ROWS: rows_task(A, F, D, T.step, T.a, sm); break;
       case T_COLS: cols_task(A, F, D, T.step, T.b, sm); break;
       case T_UPD: upd_task(A, F, T.step, T.a, T.b, sm); break;
+      case T_UPDCB: updcb_task(A, F, T.a, T.b, sm); break;
     }
     __syncthreads();
     if (A.trace && tid == 0) {
@@ -900,7 +1033,7 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     const int steps = (F.npiv + kNB - 1) / kNB;
     // tasks that never redo data after this point count towards front
     // completion right away (overlaps the round trip with the notifications)
-    const bool early_done = T.type == T_SMALL || T.type == T_ASM || T.type == T_UPD;
+    const bool early_done = T.type == T_SMALL || T.type == T_ASM || T.type == T_UPD || T.type == T_UPDCB;
     if (early_done && tid == 160) done_s = (atomicAdd(&cnt[0], 1) + 1 == D.ntasks);
     if (T.type == T_DIAG || T.type == T_ROWS || T.type == T_COLS) {
       if (T.type == T_DIAG) {
@@ -926,11 +1059,17 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
         // lookahead first: the next panel's tile row and column, then the bulk
         for (int x = tid; x < 2 * nr - 1; x += kDT) {
           const int ua = x < nr ? a0 : a0 + (x - nr + 1), ub = x < nr ? a0 + x : a0;
-          notify(A, idx_upd(A, D, F, T.step, ua, ub));
+          if (eager_tile(D, ua, ub)) notify(A, idx_upd(A, D, F, T.step, ua, ub));
         }
         __syncthreads();
-        for (int x = tid; x < (nr > 1 ? (nr - 1) * (nr - 1) : 0); x += kDT)
-          notify(A, idx_upd(A, D, F, T.step, a0 + 1 + x / (nr - 1), a0 + 1 + x % (nr - 1)));
+        for (int x = tid; x < (nr > 1 ? (nr - 1) * (nr - 1) : 0); x += kDT) {
+          const int ua = a0 + 1 + x / (nr - 1), ub = a0 + 1 + x % (nr - 1);
+          if (eager_tile(D, ua, ub)) notify(A, idx_upd(A, D, F, T.step, ua, ub));
+        }
+        if (T.step == steps - 1) {  // last panel: the contribution block in one pass per tile
+          const int ncb = D.tiles - D.acb;
+          for (int x = tid; x < ncb * ncb; x += kDT) notify(A, D.cb_base + x);
+        }
       }
     } else if (T.type == T_UPD) {
       // one notification per warp: the atomic round trips overlap
@@ -975,8 +1114,9 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     }
     if (tid == 0 && A.prof) {
       const long long t_end = clock64();
-      atomicAdd(&A.prof[3 * T.type + 0], (unsigned long long)(t_end - t_work));
-      atomicAdd(&A.prof[3 * T.type + 2], 1ull);
+      const int pt = T.type == T_UPDCB ? T_UPD : T.type;  // profiled with the updates
+      atomicAdd(&A.prof[3 * pt + 0], (unsigned long long)(t_end - t_work));
+      atomicAdd(&A.prof[3 * pt + 2], 1ull);
     }
   }
 }
@@ -1006,8 +1146,20 @@ void rqb_dag_build(FactorEngine& fe) {
   int max_small = 0;
   P->occ = S.flops_lu >= kThroughputFlops ? 2 : 1;
   if (const char* e = std::getenv("RQB_DAG_OCC")) P->occ = std::atoi(e) == 2 ? 2 : 1;
-  const int small_max = P->occ == 2 ? kSmallNfThroughput : kSmallNfLatency;
-  P->small_nf = small_max;
+  int small_max = P->occ == 2 ? kSmallNfThroughput : kSmallNfLatency;
+  if (const char* e = std::getenv("RQB_SMALL_NF")) small_max = std::min(kDT, std::atoi(e));
+  // shared memory of a SMALL front: the pivot cross (see small_front)
+  auto small_bytes = [](const Front& F) {
+    const size_t ldc = F.nf | 1, ldr = F.npiv | 1;
+    return sizeof(double) * (ldc * F.npiv + ldr * (F.nf - F.npiv));
+  };
+  const size_t small_budget = P->occ == 2 ? kSmallBytesThroughput : kSmallBytesLatency;
+  size_t max_small_bytes = 0;
+  // deferred contribution blocks pay in the throughput regime (cfg4_riga
+  // factor 44.1 -> 36.3 ms); the latency variant keeps per-step updates, which
+  // overlap the panel chain (cfg2_riga 0.85 -> 0.83 ms)
+  int cb_min_steps = P->occ == 2 ? 1 : (1 << 30);
+  if (const char* e = std::getenv("RQB_CB_MIN_STEPS")) cb_min_steps = std::atoi(e);
   // tasks of a front are contiguous; fronts in postorder
   for (int f = 0; f < nfr; ++f) {
     const Front& F = S.fronts[f];
@@ -1016,14 +1168,19 @@ void rqb_dag_build(FactorEngine& fe) {
     D.slot = -1;
     D.parent = F.parent;
     const int nch = static_cast<int>(F.children.size());
-    if (F.nf <= small_max) {
+    if (F.nf <= small_max && small_bytes(F) <= small_budget) {
       tasks.push_back({f, T_SMALL, 0, 0, 0});
       deps.push_back(nch);
       D.ntasks = 1;
       max_small = std::max(max_small, F.nf);
+      max_small_bytes = std::max(max_small_bytes, small_bytes(F));
       continue;
     }
     D.tiles = div_up(F.nf, kTile);
+    // contribution block deferred to one K = npiv pass per tile when the front
+    // has at least cb_min_steps panels (else its tiles are updated per step)
+    D.acb = div_up(F.npiv, kTile) < D.tiles && div_up(F.npiv, kNB) >= cb_min_steps ? div_up(F.npiv, kTile)
+                                                                                      : D.tiles;
     D.tile_off = tile_off;
     tile_off += D.tiles * D.tiles;
     const int steps = div_up(F.npiv, kNB);
@@ -1065,18 +1222,34 @@ void rqb_dag_build(FactorEngine& fe) {
         tasks.push_back({f, T_COLS, (int16_t)s, an, b});
         deps.push_back(s == 0 ? 1 : 2);
       }
-      for (int a = a0; a < a0 + nr; ++a)
-        for (int b = a0; b < a0 + nr; ++b) {
-          tasks.push_back({f, T_UPD, (int16_t)s, a, b});
-          deps.push_back(s == 0 ? 1 : 2);
-          const double rr = std::min(F.nf, (a + 1) * kTile) - std::max(a * kTile, t0);
-          const double cc = std::min(F.nf, (b + 1) * kTile) - std::max(b * kTile, t0);
-          P->flops_upd += 2.0 * w * rr * cc;
-        }
+      // eager tiles (pivot rows or pivot columns), layout of idx_upd
+      const int np = std::max(0, D.acb - a0);
+      auto push_upd = [&](int a, int b) {
+        tasks.push_back({f, T_UPD, (int16_t)s, a, b});
+        deps.push_back(s == 0 ? 1 : 2);
+        const double rr = std::min(F.nf, (a + 1) * kTile) - std::max(a * kTile, t0);
+        const double cc = std::min(F.nf, (b + 1) * kTile) - std::max(b * kTile, t0);
+        P->flops_upd += 2.0 * w * rr * cc;
+      };
+      for (int x = 0; x < std::min(np, nr); ++x)
+        for (int y = 0; y < nr; ++y) push_upd(a0 + x, a0 + y);
+      for (int x = np; x < nr; ++x)
+        for (int y = 0; y < np; ++y) push_upd(a0 + x, a0 + y);
       acc += 1 + 2 * nr;
       rc_prefix.push_back(acc);
     }
     step_base.push_back(static_cast<int32_t>(tasks.size()));
+    // contribution-block tiles: one K = npiv update each, released by the last panel
+    D.cb_base = static_cast<int32_t>(tasks.size());
+    if (steps > 0)
+      for (int a = D.acb; a < D.tiles; ++a)
+        for (int b = D.acb; b < D.tiles; ++b) {
+          tasks.push_back({f, T_UPDCB, 0, a, b});
+          deps.push_back(1);
+          const double rr = std::min(F.nf, (a + 1) * kTile) - a * kTile;
+          const double cc = std::min(F.nf, (b + 1) * kTile) - b * kTile;
+          P->flops_upd += 2.0 * F.npiv * rr * cc;
+        }
     D.ntasks = static_cast<int32_t>(tasks.size()) - D.task_base;
   }
   // initial ready queue: tasks without predecessors (SMALL / ASM of leaf fronts)
@@ -1116,8 +1289,9 @@ void rqb_dag_build(FactorEngine& fe) {
   P->d_flagbits.alloc(sizeof(unsigned long long) * P->nflag);
   P->d_backup.alloc(sizeof(double) * std::max<int64_t>(1, backup));
   fe.d_scratch.alloc(sizeof(double) * std::max(1, slot) * 2 * kNB * kNB);
-  const size_t small_smem = sizeof(double) * static_cast<size_t>(max_small | 1) * max_small;
-  const size_t tile_smem = sizeof(double) * 2 * kNB * kTSP;
+  const size_t small_smem = max_small_bytes;
+  P->small_nf = std::max(1, max_small);
+  const size_t tile_smem = sizeof(double) * 4 * kNB * kTSP;  // UPDCB: two stages
   const size_t rows_smem = sizeof(double) * ((kTile + 1) * kNB + kNB * kNB + 64);
   const size_t diag_smem = sizeof(double) * (3 * 32 * 33 + 128);
   P->smem = std::max({small_smem, tile_smem, rows_smem, diag_smem, size_t(16 * 1024)});
@@ -1226,7 +1400,7 @@ std::string rqb_dag_stall_report(FactorEngine& fe) {
   std::vector<Task> tk(P.ntasks);
   cudaMemcpy(deps.data(), P.d_deps.p, sizeof(int32_t) * P.ntasks, cudaMemcpyDeviceToHost);
   cudaMemcpy(tk.data(), P.d_tasks.p, sizeof(Task) * P.ntasks, cudaMemcpyDeviceToHost);
-  static const char* names[] = {"SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD"};
+  static const char* names[] = {"SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD", "UPDCB"};
   std::string out;
   int shown = 0, pending = 0;
   for (int t = 0; t < P.ntasks; ++t) {

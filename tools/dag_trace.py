@@ -24,7 +24,7 @@ ph = allt[2 * nt:].reshape(-1, 2).copy()  # {work done, fence done}
 t00 = tr[:, 0].min()
 tr -= t00
 ph -= t00
-names = ["SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD"]
+names = ["SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD", "UPDCB"]
 nfr = len(o.parent)
 fs = np.full(nfr, 1 << 62); fe = np.zeros(nfr, np.int64)
 np.minimum.at(fs, tk["front"], tr[:, 0]); np.maximum.at(fe, tk["front"], tr[:, 1])
@@ -44,7 +44,7 @@ print("  critical chain (front nf npiv: ready -> start -> end, us):")
 while True:
     ready = child_end.get(f_, (0, -1))[0]
     ty = tk["type"][tk["front"] == f_]
-    cnts = {names[t]: int((ty == t).sum()) for t in range(6) if (ty == t).sum()}
+    cnts = {names[t]: int((ty == t).sum()) for t in range(7) if (ty == t).sum()}
     print(f"    front {f_:5d} nf {o.nf[f_]:5d} npiv {o.npiv[f_]:5d} level {lv[f_]:2d}: ready {ready/1e3:8.1f} start {fs[f_]/1e3:8.1f} end {fe[f_]/1e3:8.1f}  {cnts}")
     if f_ not in child_end: break
     f_ = child_end[f_][1]
