@@ -55,6 +55,7 @@ constexpr int kPB = 16;           // small-front panel width
 constexpr int kTile = 64;         // big-front tile edge
 constexpr int kTSP = kTile + 4;   // padded smem stride of DMMA operand tiles
 constexpr double kLmax = 10.0 * (1.0 - 1e-14);  // 1/threshold, conservative
+constexpr int kAsmRowTiles = 8;  // parent rows per extend-add task: 8 tiles
 constexpr int kCnt = 5;  // per-front counters: tasks, asm, diag, rc, released
 // Two configurations of the persistent kernel, chosen per factorization
 // (rqb_dag_build): small problems are critical-path bound and want big SMALL
@@ -166,14 +167,14 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 
 // Children's Schur blocks into front F (child-centric scatter, atomic-free:
 // rel is injective, children are applied one after the other). For child ch
-// only its CB columns [lo[ch], hi[ch]) are applied; parent column c lives at
-// dst + c * ldd (shared or global memory). Latency: a warp takes four child
-// columns x 64 rows per iteration, all 16 loads (8 child values, 8 parent
+// only its CB columns [lo[ch], hi[ch]) and CB rows [rlo[ch], rhi[ch]) are
+// applied; parent column c lives at dst + c * ldd (shared or global memory). Latency: a warp takes four child
+// columns x 128 rows per iteration, all 32 loads (16 child values, 16 parent
 // values) in flight before the first add.
 __device__ void extend_add(const DagArgs& A, const FrontDev& F, const int* lo, const int* hi,
-                           double* dst, int64_t ldd, bool dst_global) {
+                           const int* rlo, const int* rhi, double* dst, int64_t ldd, bool dst_global) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kW = kDT / 32, kC = 4, kU = 2;
+  constexpr int kW = kDT / 32, kC = 4, kU = 4;
   for (int ch = 0; ch < F.nchild; ++ch) {
     const FrontDev C = A.fronts[ch == 0 ? F.child0 : F.child1];
     const int32_t* rel = A.rel + C.rel_off;
@@ -189,13 +190,13 @@ __device__ void extend_add(const DagArgs& A, const FrontDev& F, const int* lo, c
         dcol[j] = dst + (int64_t)__ldg(&rel[ic]) * ldd;
       }
       const int ncol = min(kC, hi[ch] - ic0);
-      for (int k0 = 0; k0 < ncb; k0 += 32 * kU) {
+      for (int k0 = rlo[ch]; k0 < rhi[ch]; k0 += 32 * kU) {
         int pr[kU];
         double v[kC][kU], d[kC][kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const int kk = k0 + lane + 32 * u;
-          pr[u] = kk < ncb ? __ldg(&rel[kk]) : -1;
+          pr[u] = kk < rhi[ch] ? __ldg(&rel[kk]) : -1;
         }
 #pragma unroll
         for (int j = 0; j < kC; ++j)
@@ -289,7 +290,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
     int lo[2] = {0, 0}, hi[2] = {0, 0};
     hi[0] = A.fronts[F.child0].nf - A.fronts[F.child0].npiv;
     if (F.nchild > 1) hi[1] = A.fronts[F.child1].nf - A.fronts[F.child1].npiv;
-    extend_add(A, F, lo, hi, g, ld, true);  // ends with a barrier
+    extend_add(A, F, lo, hi, lo, hi, g, ld, true);  // ends with a barrier
   }
   // the cross in flight at once (one latency); the lines were never read
   // through L1 in this launch (extend_add reads with ld.cg)
@@ -1000,14 +1001,16 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     // ---- work (every predecessor has completed: no waits)
     switch (T.type) {
       case T_SMALL: small_front(A, F, sm, piv_sh); break;
-      case T_ASM: {
-        int lo[2] = {0, 0}, hi[2] = {0, 0};
+      case T_ASM: {  // parent column block b, parent row block a (kAsmRowTiles tiles)
+        int lo[2] = {0, 0}, hi[2] = {0, 0}, rlo[2] = {0, 0}, rhi[2] = {0, 0};
         for (int ch = 0; ch < F.nchild; ++ch) {
           const int32_t* bd = A.bnd + D.bnd_off + ch * (D.tiles + 1);
           lo[ch] = bd[T.b];
           hi[ch] = bd[T.b + 1];
+          rlo[ch] = bd[min(T.a * kAsmRowTiles, D.tiles)];
+          rhi[ch] = bd[min((T.a + 1) * kAsmRowTiles, D.tiles)];
         }
-        extend_add(A, F, lo, hi, A.pool + F.off, F.ld, true);
+        extend_add(A, F, lo, hi, rlo, rhi, A.pool + F.off, F.ld, true);
         break;
       }
       case T_DIAG: diag_task(A, F, D, T.step, sm); break;
@@ -1189,7 +1192,7 @@ void rqb_dag_build(FactorEngine& fe) {
     D.slot = slot++;
     D.backup_off = backup;
     backup += 2LL * F.nf * kNB;
-    D.nasm = D.tiles;
+    D.nasm = D.tiles * div_up(D.tiles, kAsmRowTiles);
     D.bnd_off = static_cast<int32_t>(bnd.size());
     for (int32_t c : F.children) {
       const Front& C = S.fronts[c];
@@ -1198,10 +1201,14 @@ void rqb_dag_build(FactorEngine& fe) {
       for (int b = 0; b <= D.tiles; ++b)
         bnd.push_back(static_cast<int32_t>(std::lower_bound(rel, rel + ncb, b * kTile) - rel));
     }
-    for (int b = 0; b < D.tiles; ++b) {
-      tasks.push_back({f, T_ASM, 0, 0, b});
-      deps.push_back(nch);
-    }
+    // extend-add tasks: 64-column block x kAsmRowTiles-tile row block of the
+    // parent (children's rows are a sorted map: each parent block is a
+    // contiguous child range, so concurrent tasks never touch the same entry)
+    for (int a = 0; a < div_up(D.tiles, kAsmRowTiles); ++a)
+      for (int b = 0; b < D.tiles; ++b) {
+        tasks.push_back({f, T_ASM, 0, a, b});
+        deps.push_back(nch);
+      }
     D.rc_off = static_cast<int32_t>(rc_prefix.size());
     D.sb_off = static_cast<int32_t>(step_base.size());
     rc_prefix.push_back(0);
