@@ -181,7 +181,8 @@ __device__ __forceinline__ int pop_item(const SweepArgs& A) {
 
 // s += sum_{c in [cb, ce)} L[row, c] xs[c] for this thread's column class
 // (c = grp mod 4): eight independent column loads in flight per iteration,
-// each a 512-byte coalesced segment across the 64 rows of the item.
+// each a 512-byte coalesced segment across the 64 rows of the item; the last
+// (partial) iteration is predicated, not a serial tail of dependent loads.
 __device__ __forceinline__ double stream_cols(const double* lp, int64_t ld, const double* xs, int cb, int ce,
                                               int grp) {
   double s0 = 0.0, s1 = 0.0;
@@ -196,7 +197,14 @@ __device__ __forceinline__ double stream_cols(const double* lp, int64_t ld, cons
       s1 += a[u + 1] * xs[c + 4 * u + 4];
     }
   }
-  for (; c < ce; c += 4) s0 += lp[(int64_t)c * ld] * xs[c];
+  if (c < ce) {  // fewer than 8 columns of this class left: one predicated batch
+    double a[7];
+#pragma unroll
+    for (int u = 0; u < 7; ++u) a[u] = c + 4 * u < ce ? lp[(int64_t)(c + 4 * u) * ld] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 7; ++u)
+      if (c + 4 * u < ce) s0 += a[u] * xs[c + 4 * u];
+  }
   return s0 + s1;
 }
 

@@ -20,6 +20,8 @@
 // nothing.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -183,6 +185,8 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   auto ms_since = [](std::chrono::steady_clock::time_point a) {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
   };
+  double t_graph_build = 0;
+  const double t_setup = ms_since(t0);
   std::map<std::pair<int, const double*>, cudaGraphExec_t> graphs;
   struct GraphFree {
     std::map<std::pair<int, const double*>, cudaGraphExec_t>* g;
@@ -236,6 +240,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       const std::pair<int, const double*> key{pre_applied ? -1 - k : k, V};
       auto it = graphs.find(key);
       if (it == graphs.end()) {
+        const auto tg = now();
         cudaGraph_t gr;
         cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
         enqueue_steps(false, pre_applied);
@@ -244,6 +249,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         cuda_check(cudaGraphInstantiate(&ex, gr, 0), "graph instantiate");
         cudaGraphDestroy(gr);
         it = graphs.emplace(key, ex).first;
+        t_graph_build += ms_since(tg);
       }
       cuda_check(cudaGraphLaunch(it->second, st), "graph launch");
       res.graph_launches += 1;
@@ -581,6 +587,9 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   res.vec_im = std::move(final_vecs_im);
   res.launches = op.launches - launches0;
   res.t_total_ms = std::chrono::duration<double, std::milli>(clock::now() - t0).count();
+  if (std::getenv("RQB_SETUP_TRACE"))
+    std::fprintf(stderr, "[setup] eigs: buffers %.1f ms, %zu graphs built in %.1f ms, total %.1f ms\n", t_setup,
+                 graphs.size(), t_graph_build, res.t_total_ms);
   res.t_solve_ms = t_solve;
   res.t_orth_ms = t_orth;
   res.t_ritz_ms = t_ritz;
