@@ -250,6 +250,30 @@ int rq_eigs_run(rq_operator_t* op, const rq_eigs_opts* opts, double* lam_re, dou
 /* CostLedger::to_json-compatible snapshot (sparse.cpp:80-97) of the last run. */
 int rq_eigs_ledger_json(const rq_operator_t* op, char* buf, size_t len);
 
+/* ------------------------------------------------------------------------ */
+/* Wire formats (reference sparse.cpp:121-174,         */
+/* SPEC.md:269, 371, 503). Host only.                                       */
+/* ------------------------------------------------------------------------ */
+/* write_matrix_market: coordinate real|complex general, 1-based, "%.17g";  */
+/* im may be NULL (real). Same bytes as the reference writer.               */
+int rq_mm_write(int64_t n, const int64_t* rowptr, const int32_t* col, const double* re, const double* im,
+                const char* path);
+/* write_matrix_market_vector: array complex general, one "re im" per line  */
+int rq_mm_write_vector(int64_t n, const double* re, const double* im, const char* path);
+/* read_matrix_market: sorted CSR with duplicate entries summed
+ * (from_triplets). Returns a handle; rq_mm_dims / rq_mm_csr copy it out.  */
+typedef struct rq_mm rq_mm_t;
+int rq_mm_read(const char* path, rq_mm_t** out);
+int rq_mm_dims(const rq_mm_t* m, int64_t* n, int64_t* nnz, int* complex_values);
+int rq_mm_csr(const rq_mm_t* m, int64_t* rowptr, int32_t* col, double* re, double* im);
+void rq_mm_destroy(rq_mm_t* m);
+/* Pencil export: <prefix>K.mtx, <prefix>C.mtx, <prefix>M.mtx */
+int rq_pencil_write_mm(const rq_pencil_t* p, const char* prefix);
+/* Eigenpair dump: JSON array of {re, im, residual}. *len
+ * receives the length (without NUL); buf may be NULL to query it. */
+int rq_eigenpairs_json(int n, const double* re, const double* im, const double* residual, char* buf,
+                       int64_t cap, int64_t* len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,13 @@ def ref():
         lib.ref_kern_elim.restype = C.c_uint64
         lib.ref_select_backend.argtypes = [C.c_char_p]
         lib.ref_select_backend.restype = C.c_int
+        if hasattr(lib, "ref_mm_write"):  # Matrix Market through the reference's sparse.cpp
+            lib.ref_mm_write.argtypes = [C.c_int64, i64p, i32p, f64p, vp, C.c_char_p]
+            lib.ref_mm_write.restype = C.c_int
+            lib.ref_mm_write_vector.argtypes = [C.c_int64, f64p, vp, C.c_char_p]
+            lib.ref_mm_write_vector.restype = C.c_int
+            lib.ref_mm_read.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), vp, vp, vp, vp]
+            lib.ref_mm_read.restype = C.c_int
         _ref = lib
     return _ref
 

@@ -7,8 +7,12 @@
 #include <cstdint>
 #include <cstring>
 
+#include <string>
+#include <vector>
+
 #include "rigaqep/kernels.hpp"
 #include "rigaqep/spaces.hpp"
+#include "rigaqep/sparse.hpp"
 
 extern "C" {
 
@@ -69,6 +73,53 @@ uint64_t ref_kern_elim(double* tile_c, int64_t ld, const double* lcol_c, const d
 int ref_select_backend(const char* name) {
   try {
     rq::kern::select_backend(name);
+    return 0;
+  } catch (const rq::Error& e) {
+    return static_cast<int>(e.code());
+  }
+}
+
+// Matrix Market through the reference's own sparse module (sparse.cpp:121-174).
+int ref_mm_write(int64_t n, const int64_t* rowptr, const int32_t* col, const double* re, const double* im,
+                 const char* path) {
+  try {
+    rq::SparseMatrix a;
+    a.n = n;
+    a.rowptr.assign(rowptr, rowptr + n + 1);
+    a.col.assign(col, col + rowptr[n]);
+    a.val.resize(rowptr[n]);
+    for (int64_t k = 0; k < rowptr[n]; ++k) a.val[k] = rq::cdouble(re[k], im ? im[k] : 0.0);
+    rq::write_matrix_market(a, path);
+    return 0;
+  } catch (const rq::Error& e) {
+    return static_cast<int>(e.code());
+  }
+}
+
+int ref_mm_write_vector(int64_t n, const double* re, const double* im, const char* path) {
+  try {
+    std::vector<rq::cdouble> x(n);
+    for (int64_t i = 0; i < n; ++i) x[i] = rq::cdouble(re[i], im ? im[i] : 0.0);
+    rq::write_matrix_market_vector(x, path);
+    return 0;
+  } catch (const rq::Error& e) {
+    return static_cast<int>(e.code());
+  }
+}
+
+// two calls: arrays NULL -> sizes; then the CSR (re / im split)
+int ref_mm_read(const char* path, int64_t* n, int64_t* nnz, int64_t* rowptr, int32_t* col, double* re,
+                double* im) {
+  try {
+    const rq::SparseMatrix a = rq::read_matrix_market(path);
+    *n = a.n;
+    *nnz = a.nnz();
+    if (rowptr)
+      for (size_t i = 0; i < a.rowptr.size(); ++i) rowptr[i] = a.rowptr[i];
+    if (col)
+      for (int64_t k = 0; k < a.nnz(); ++k) col[k] = a.col[k];
+    if (re)
+      for (int64_t k = 0; k < a.nnz(); ++k) re[k] = a.val[k].real(), im[k] = a.val[k].imag();
     return 0;
   } catch (const rq::Error& e) {
     return static_cast<int>(e.code());

@@ -6,5 +6,7 @@ from ._lib import LIB_PATH, RqError  # noqa: F401
 from .eig import (EigenPair, ShiftInvertOperator, apply_operator, arnoldi_run,  # noqa: F401
                   b_inner, build_operator, solve_quadratic)
 from .pencil import CURL, DIV, QuadraticPencil, assemble, baseline_config  # noqa: F401
+from .io import (eigenpairs_json, load_eigenpairs, read_matrix_market,  # noqa: F401
+                 write_eigenpairs, write_matrix_market, write_matrix_market_vector, write_pencil)
 from .sparsela import (Factorization, Ordering, lu_factorize,  # noqa: F401
                        nested_dissection_order, solve_factored)

@@ -127,6 +127,14 @@ _sig("rq_factor_front_export", C.c_int, vp, C.c_int64, vp, vp, C.POINTER(C.c_int
 _sig("rq_factor_profile", C.c_int, vp, f64p, i64p, f64p)
 _sig("rq_factor_dag_profile", C.c_int, vp, f64p)
 _sig("rq_factor_destroy", None, vp)
+_sig("rq_mm_write", C.c_int, C.c_int64, i64p, i32p, f64p, f64n, C.c_char_p)
+_sig("rq_mm_write_vector", C.c_int, C.c_int64, f64p, f64n, C.c_char_p)
+_sig("rq_mm_read", C.c_int, C.c_char_p, C.POINTER(vp))
+_sig("rq_mm_dims", C.c_int, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int))
+_sig("rq_mm_csr", C.c_int, vp, i64n, i32n, f64n, f64n)
+_sig("rq_mm_destroy", None, vp)
+_sig("rq_pencil_write_mm", C.c_int, vp, C.c_char_p)
+_sig("rq_eigenpairs_json", C.c_int, C.c_int, f64n, f64n, f64n, C.c_char_p, C.c_int64, C.POINTER(C.c_int64))
 _sig("rq_operator_create", C.c_int, C.c_int64, i64p, i32p, f64p, f64p, f64p, vp,
      C.POINTER(OperatorOpts), C.POINTER(vp))
 _sig("rq_operator_create_pencil", C.c_int, vp, vp, C.POINTER(OperatorOpts), C.POINTER(vp))
@@ -150,7 +158,8 @@ EXPORTS = [
     "rq_symbolic_front_rows", "rq_symbolic_destroy", "rq_factor_create", "rq_factor_refactor",
     "rq_factor_get_info", "rq_factor_solve", "rq_factor_front_export", "rq_factor_profile", "rq_factor_dag_profile",
     "rq_factor_destroy",
-    "rq_operator_create", "rq_operator_create_pencil", "rq_operator_varsigma", "rq_operator_apply", "rq_operator_b_inner",
+    "rq_operator_create", "rq_operator_create_pencil", "rq_mm_write", "rq_mm_write_vector", "rq_mm_read",
+    "rq_mm_dims", "rq_mm_csr", "rq_mm_destroy", "rq_pencil_write_mm", "rq_eigenpairs_json", "rq_operator_varsigma", "rq_operator_apply", "rq_operator_b_inner",
     "rq_operator_spmv", "rq_operator_arnoldi", "rq_operator_factor", "rq_operator_destroy",
     "rq_operator_time",
     "rq_eigs_run", "rq_eigs_ledger_json",

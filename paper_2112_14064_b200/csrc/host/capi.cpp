@@ -13,11 +13,15 @@
 #include "../../../include/rq_b200.h"
 #include "../engine.hpp"
 #include "common.hpp"
+#include "io.hpp"
 #include "eigs.hpp"
 
 struct rq_pencil {
   rqb::Pencil P;
   std::unique_ptr<rqb::DevicePencil> dev;  // device-resident K, C, M (P.K/C/M empty)
+};
+struct rq_mm {
+  rqb::CsrFile m;
 };
 struct rq_symbolic {
   rqb::Symbolic S;
@@ -584,6 +588,106 @@ int rq_eigs_ledger_json(const rq_operator_t* o, char* buf, size_t len) {
     const std::string s = o->ledger.to_json();
     if (s.size() + 1 > len) rqb::fail(rqb::errc::dimension, "buffer too small");
     std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+
+int rq_mm_write(int64_t n, const int64_t* rowptr, const int32_t* col, const double* re, const double* im,
+                const char* path) {
+  return guarded([&] {
+    need(rowptr, "rowptr");
+    need(path, "path");
+    if (n < 0) rqb::fail(rqb::errc::dimension, "negative dimension");
+    if (rowptr[n] > 0) {
+      need(col, "col");
+      need(re, "re");
+    }
+    rqb::write_mm_csr(n, rowptr, col, re, im, path);
+  });
+}
+
+int rq_mm_write_vector(int64_t n, const double* re, const double* im, const char* path) {
+  return guarded([&] {
+    need(path, "path");
+    if (n < 0) rqb::fail(rqb::errc::dimension, "negative dimension");
+    if (n > 0) need(re, "re");
+    rqb::write_mm_vector(n, re, im, path);
+  });
+}
+
+int rq_mm_read(const char* path, rq_mm_t** out) {
+  return guarded([&] {
+    need(path, "path");
+    need(out, "out");
+    auto m = std::make_unique<rq_mm>();
+    m->m = rqb::read_mm_csr(path);
+    *out = m.release();
+  });
+}
+
+int rq_mm_dims(const rq_mm_t* m, int64_t* n, int64_t* nnz, int* complex_values) {
+  return guarded([&] {
+    need(m, "mm");
+    if (n) *n = m->m.n;
+    if (nnz) *nnz = static_cast<int64_t>(m->m.col.size());
+    if (complex_values) *complex_values = m->m.complex_values ? 1 : 0;
+  });
+}
+
+int rq_mm_csr(const rq_mm_t* m, int64_t* rowptr, int32_t* col, double* re, double* im) {
+  return guarded([&] {
+    need(m, "mm");
+    const rqb::CsrFile& c = m->m;
+    if (rowptr) std::memcpy(rowptr, c.rowptr.data(), sizeof(int64_t) * c.rowptr.size());
+    if (col) std::memcpy(col, c.col.data(), sizeof(int32_t) * c.col.size());
+    if (re) std::memcpy(re, c.re.data(), sizeof(double) * c.re.size());
+    if (im) std::memcpy(im, c.im.data(), sizeof(double) * c.im.size());
+  });
+}
+
+void rq_mm_destroy(rq_mm_t* m) { delete m; }
+
+int rq_pencil_write_mm(const rq_pencil_t* p, const char* prefix) {
+  return guarded([&] {
+    need(p, "pencil");
+    need(prefix, "prefix");
+    const rqb::Pencil& P = p->P;
+    const int64_t nnz = P.rowptr.back();
+    std::vector<double> vals[3];
+    const double* src[3] = {P.K.data(), P.C.data(), P.M.data()};
+    if (p->dev) {  // device-resident values: one copy out
+      int cur = 0;
+      rqb::cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+      rqb::cuda_check(cudaSetDevice(p->dev->device), "cudaSetDevice");
+      const double* d[3] = {p->dev->K(), p->dev->C(), p->dev->M()};
+      for (int w = 0; w < 3; ++w) {
+        vals[w].resize(nnz);
+        rqb::cuda_check(cudaMemcpy(vals[w].data(), d[w], sizeof(double) * nnz, cudaMemcpyDeviceToHost), "D2H");
+        src[w] = vals[w].data();
+      }
+      rqb::cuda_check(cudaSetDevice(cur), "cudaSetDevice");
+    }
+    const char* names[3] = {"K.mtx", "C.mtx", "M.mtx"};
+    for (int w = 0; w < 3; ++w)
+      rqb::write_mm_csr(P.n, P.rowptr.data(), P.col.data(), src[w], nullptr, std::string(prefix) + names[w]);
+  });
+}
+
+int rq_eigenpairs_json(int n, const double* re, const double* im, const double* residual, char* buf,
+                       int64_t cap, int64_t* len) {
+  return guarded([&] {
+    if (n < 0) rqb::fail(rqb::errc::dimension, "negative count");
+    if (n > 0) {
+      need(re, "re");
+      need(im, "im");
+      need(residual, "residual");
+    }
+    const std::string s = rqb::eigenpairs_json(n, re, im, residual);
+    if (len) *len = static_cast<int64_t>(s.size());
+    if (buf) {
+      if (cap < static_cast<int64_t>(s.size()) + 1) rqb::fail(rqb::errc::dimension, "buffer too small");
+      std::memcpy(buf, s.c_str(), s.size() + 1);
+    }
   });
 }
 

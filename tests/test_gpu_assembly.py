@@ -84,3 +84,14 @@ def test_resident_operator_equals_host_operator(name, scaling):
     pd = od.solve_quadratic(8, eps=1e-10, seed=0)
     assert [p.lam for p in ph] == [p.lam for p in pd]
     assert [p.residual for p in ph] == [p.residual for p in pd]
+
+
+def test_device_pencil_export_matches_host_export(tmp_path):
+    """f3 pencil export straight from a device-resident pencil (one copy out of
+    HBM) writes the same bytes as the host pencil's export."""
+    H = rq.baseline_config("cfg1")
+    D = rq.baseline_config("cfg1", device=True, resident=True)
+    fh = rq.write_pencil(H, str(tmp_path / "h_"))
+    fd = rq.write_pencil(D, str(tmp_path / "d_"))
+    for a, b in zip(fh, fd):
+        assert open(a, "rb").read() == open(b, "rb").read()
