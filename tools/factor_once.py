@@ -1,0 +1,8 @@
+"""One numeric factorization of a config (ncu capture target; development aid)."""
+import sys
+sys.path.insert(0, ".")
+import paper_2112_14064_b200 as rq
+P = rq.baseline_config(sys.argv[1] if len(sys.argv) > 1 else "cfg2_riga")
+o = rq.nested_dissection_order(P)
+f = rq.lu_factorize((P.rowptr, P.col, P.q_values(-0.5)), o)
+print(f.info())
