@@ -238,11 +238,19 @@ __device__ __forceinline__ void cross_update(const double* Lb, int ldl, const do
   const int mt = (r1 - r0 + 15) / 16, nt = (c1 - c0 + 31) / 32;
   for (int tile = warp; tile < mt * nt; tile += kDT / 32) {
     const int rr = r0 + (tile % mt) * 16, cc = c0 + (tile / mt) * 32;
-    double acc[4][4];
+    double acc[4][4], cv[4][4];
 #pragma unroll
     for (int y = 0; y < 4; ++y)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[y][e] = 0.0;
+    if (kGlobal)  // destination values in flight during the K loop
+#pragma unroll
+      for (int y = 0; y < 4; ++y)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = rr + gid + (e >> 1) * 8, c = cc + y * 8 + 2 * tig + (e & 1);
+          cv[y][e] = (r < r1 && c < c1) ? __ldcg(&D[r + (int64_t)(c - doff) * ldd]) : 0.0;
+        }
     const int ra = rr + gid, rb = rr + gid + 8;
 #pragma unroll 4
     for (int kk = 0; kk < kw; kk += 4) {
@@ -264,7 +272,7 @@ __device__ __forceinline__ void cross_update(const double* Lb, int ldl, const do
         const int r = rr + gid + (e >> 1) * 8, c = cc + y * 8 + 2 * tig + (e & 1);
         if (r < r1 && c < c1) {
           double* p = &D[r + (int64_t)(c - doff) * ldd];
-          *p = (kGlobal ? __ldcg(p) : *p) - acc[y][e];
+          *p = (kGlobal ? cv[y][e] : *p) - acc[y][e];
         }
       }
   }
@@ -1382,7 +1390,7 @@ void rqb_dag_profile(FactorEngine& fe, double* out) {
   out[18] = fe.dag->grid;
   out[19] = fe.dag->ntasks;
   out[20] = h[20] / (clk_khz * 1.0);  // ready-queue pop wait, summed over CTAs
-  for (int i = 21; i < 24; ++i) out[i] = h[i] / (clk_khz * 1.0);  // DIAG phases (LU, inv L, inv U)
+  for (int i = 21; i < 24; ++i) out[i] = h[i] / (clk_khz * 1.0);  // spare profiling slots
   if (const char* path = std::getenv("RQB_DAG_TRACE")) {  // development trace: tasks + timestamps
     DagPlan& P = *fe.dag;
     std::vector<unsigned long long> tr(4 * static_cast<size_t>(P.ntasks));
