@@ -100,6 +100,7 @@ struct DagArgs {
   const FrontDag* dag;
   const Task* tasks;
   int ntasks;
+  int nqueued;  // tasks that pass through the ready queue (DIAG of steps >= 1 never do)
   const int32_t* inv;
   const int32_t* rel;   // child CB row -> parent-local row (FrontDev::rel_off)
   const int32_t* bnd;   // FrontDag::bnd_off
@@ -960,7 +961,7 @@ __device__ __forceinline__ void notify(const DagArgs& A, int t) {
 
 __device__ int pop_task(const DagArgs& A) {
   const int h = atomicAdd(&A.qctl[0], 1);
-  if (h >= A.ntasks) return -1;
+  if (h >= A.nqueued) return -1;
   volatile int* q = A.queue;
   int t;
   if ((t = q[h]) < 0) {
@@ -981,14 +982,18 @@ __device__ int pop_task(const DagArgs& A) {
 template <int kMinBlocks>
 __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) {
   extern __shared__ double sm[];
-  __shared__ int task_s, last_s, done_s;
+  __shared__ int task_s, last_s, done_s, next_s;
   __shared__ int piv_sh[kPB];
   const int tid = threadIdx.x;
+  if (tid == 0) next_s = -1;
   for (;;) {
     __syncthreads();
     if (tid == 0) {
       const long long t0 = A.prof ? clock64() : 0;
-      const int t = pop_task(A);
+      // DIAG(s + 1) runs in the CTA that finished its only predecessor (the
+      // update of the diagonal tile): no queue round trip on the panel chain
+      const int t = next_s >= 0 ? next_s : pop_task(A);
+      next_s = -1;
       task_s = t;
       if (A.prof && t >= 0) atomicAdd(&A.prof[20], (unsigned long long)(clock64() - t0));
     }
@@ -1090,8 +1095,8 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
         const int a1 = a0_of(F, s1), an = (s1 * kNB) / kTile;
         const bool trail = nr_of(F, D, s1) > 0;  // step s1 has trailing rows / columns
         switch (tid >> 5) {
-          case 0:
-            if (T.a == an && T.b == an) notify(A, idx_diag(A, D, s1));
+          case 0:  // tid 0: the next panel's diagonal block runs here next
+            if (T.a == an && T.b == an) next_s = idx_diag(A, D, s1);
             break;
           case 1:
             if (trail && T.b == an && T.a >= a1) notify(A, idx_rows(A, D, F, s1, T.a));
@@ -1139,7 +1144,7 @@ int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 struct DagPlan {
   DeviceBuffer d_tasks, d_dag, d_cnt, d_tile, d_rc, d_flagbits, d_backup, d_prof, d_bnd,
       d_small_backup, d_deps0, d_deps, d_queue0, d_queue, d_qctl, d_qctl0, d_sb, d_trace;
-  int ntasks = 0, nfronts = 0, ntile = 0, nflag = 0, grid = 148, nready = 0;
+  int ntasks = 0, nqueued = 0, nfronts = 0, ntile = 0, nflag = 0, grid = 148, nready = 0;
   int occ = 1, small_nf = 160;  // kernel variant (see kSmallNfLatency / kSmallNfThroughput)
   size_t smem = 0;
   double flops_upd = 0;
@@ -1154,7 +1159,7 @@ void rqb_dag_build(FactorEngine& fe) {
   std::vector<Task> tasks;
   int tile_off = 0, flag_off = 0, slot = 0;
   int64_t backup = 0;
-  int max_small = 0;
+  int max_small = 0, nfused = 0;
   P->occ = S.flops_lu >= kThroughputFlops ? 2 : 1;
   if (const char* e = std::getenv("RQB_DAG_OCC")) P->occ = std::atoi(e) == 2 ? 2 : 1;
   int small_max = P->occ == 2 ? kSmallNfThroughput : kSmallNfLatency;
@@ -1228,7 +1233,8 @@ void rqb_dag_build(FactorEngine& fe) {
       const int an = k / kTile;
       step_base.push_back(static_cast<int32_t>(tasks.size()));
       tasks.push_back({f, T_DIAG, (int16_t)s, an, an});
-      deps.push_back(s == 0 ? D.nasm : 1);
+      deps.push_back(s == 0 ? D.nasm : 1);  // s >= 1: run by its predecessor's CTA, never queued
+      if (s > 0) ++nfused;
       for (int a = a0; a < a0 + nr; ++a) {
         tasks.push_back({f, T_ROWS, (int16_t)s, a, an});
         deps.push_back(s == 0 ? 1 : 2);
@@ -1274,6 +1280,7 @@ void rqb_dag_build(FactorEngine& fe) {
     if (deps[t] == 0) queue0[nready++] = static_cast<int32_t>(t);
   P->nready = nready;
   P->ntasks = static_cast<int>(tasks.size());
+  P->nqueued = P->ntasks - nfused;
   P->nfronts = nfr;
   P->ntile = std::max(1, tile_off);
   P->nflag = std::max(1, flag_off);
@@ -1334,6 +1341,7 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   A.dag = P.d_dag.as<FrontDag>();
   A.tasks = P.d_tasks.as<Task>();
   A.ntasks = P.ntasks;
+  A.nqueued = P.nqueued;
   A.inv = fe.d_inv.as<int32_t>();
   A.rel = fe.d_rel.as<int32_t>();
   A.bnd = P.d_bnd.as<int32_t>();
@@ -1419,7 +1427,7 @@ std::string rqb_dag_stall_report(FactorEngine& fe) {
   std::string out;
   int shown = 0, pending = 0;
   for (int t = 0; t < P.ntasks; ++t) {
-    if (deps[t] == 0) continue;
+    if (deps[t] == 0 || (tk[t].type == T_DIAG && tk[t].step > 0)) continue;  // fused DIAGs are never counted down
     ++pending;
     if (shown < 6) {
       const Task& T = tk[t];
