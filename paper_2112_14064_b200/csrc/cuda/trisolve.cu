@@ -286,6 +286,17 @@ __device__ __forceinline__ void bwd_triangle(const double* E, int lane, double& 
   }
 }
 
+// L2 prefetch of a contiguous byte range (TMA bulk prefetch, 16-byte granules)
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  while (a < e) {
+    const unsigned n = static_cast<unsigned>(e - a < (uintptr_t(1) << 20) ? e - a : (uintptr_t(1) << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+    a += n;
+  }
+}
+
 __device__ __forceinline__ void red_release(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -315,6 +326,9 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
     const int64_t ld = I.ld;
     const bool whole = I.blk == kWhole;
     const int nck = whole ? I.npb + I.ncbb : 1;
+    // whole-front item: its L columns (all rows) are one contiguous range;
+    // in L2 before the chunk loop reaches them
+    if (whole && tid == 0) prefetch_l2(g, sizeof(double) * (size_t)np * ld);
     unsigned long long waited = 0;
     // rows of chunk ck: pivot blocks first, then 64-row contribution chunks
     auto chunk_rows = [&](int ck, int& r0, int& nr, int& blk) {
@@ -473,6 +487,8 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
     const int32_t* rw = A.rows + I.rows_off;
     const bool whole = I.blk == kWhole;
     constexpr int kCbBase = kWholeNpb * kRB;
+    if (whole)  // the item's U12 columns (rows < np of the contribution columns) into L2
+      for (int c = np + tid; c < nf; c += kST) prefetch_l2(g + (int64_t)c * ld, sizeof(double) * np);
     if (whole)
       for (int c = tid; c < nf - np; c += kST) stg[kCbBase + c] = __ldcg(&A.xnew[rw[np + c]]);
     const int nck = whole ? I.npb : 1;
