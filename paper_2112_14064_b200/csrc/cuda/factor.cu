@@ -747,7 +747,7 @@ void FactorEngine::enqueue_factor(KernelTimer* kt) {
     B(4);
     rqb_rowperm_enqueue(*this);
     E();
-    launches += 2;
+    launches += 3;
     RQB_CUDA(cudaGetLastError());
     launches_factor = launches;
     return;
@@ -815,7 +815,7 @@ void FactorEngine::enqueue_factor(KernelTimer* kt) {
   B(4);
   rqb_rowperm_enqueue(*this);
   E();
-  ++launches;
+  launches += 2;
   RQB_CUDA(cudaGetLastError());
   launches_factor = launches;
 }

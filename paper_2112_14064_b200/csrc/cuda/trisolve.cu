@@ -41,7 +41,7 @@ struct SolveItem {
   int32_t front, r0, nr, blk;     // local rows [r0, r0+nr); pivot-block index, -1 contribution rows
   int32_t ld, np, nf, start;
   int32_t npb, ncbb, parent, rows_off;
-  int32_t cbvec_off, ech_off, nech, pad;
+  int32_t cbvec_off, ech_off, nech, doff;  // doff: the front's first diagonal-inverse block
 };
 
 struct SweepArgs {
@@ -60,6 +60,7 @@ struct SweepArgs {
   const int32_t* ech;
   const int4* gsrc;      // forward gather sources per front row {b, child0 cb, child1 cb, -}
   const double* pool;
+  const double* dinv;    // diagonal-block inverses (FactorEngine::d_dinv)
   const int32_t* perm;
   const int32_t* rows;
   const double* b;
@@ -227,23 +228,30 @@ __device__ __forceinline__ double fma_block(const double (&r)[kRB / 4], const do
   return s;
 }
 
-// Diagonal block of an item into shared memory, padded to 64 x 64 with
-// zeros (rows/columns >= nr), so the triangles below run a fixed, fully
-// unrolled 64-step schedule. Backward: columns pre-scaled by the reciprocal
-// diagonal (E[r][c] = U[r][c] / U[c][c], rinv[r] = 1 / U[r][r]) so the serial
-// chain of the substitution is one shuffle + one FMA per step.
+// Inverse of an item's diagonal tile into shared memory, padded to 64 x 64
+// with zeros (rows/columns >= nr): forward inv(L11) with its unit diagonal,
+// backward inv(U11). The tiles are contiguous nr x nr squares (diag_inverse),
+// so this is one coalesced read; the substitution becomes a 64 x 64 product
+// with no serial chain.
 template <bool kUpper>
-__device__ __forceinline__ void load_diag(double* D, double* rinv, const double* g, int64_t ld, int r0, int nr,
-                                          int tid) {
-  if (kUpper) {
-    if (tid < kRB) rinv[tid] = tid < nr ? 1.0 / g[(r0 + tid) + (int64_t)(r0 + tid) * ld] : 0.0;
-    __syncthreads();
+__device__ __forceinline__ void load_dinv(double* D, const double* src, int nr, int tid) {
+  constexpr int kPer = kRB * kRB / kST;
+  double v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {  // every load in flight before the first store
+    const int idx = tid + u * kST, r = idx & (kRB - 1), c = idx >> 6;
+    v[u] = 0.0;
+    if (r < nr && c < nr) {
+      if (kUpper)
+        v[u] = r <= c ? src[r + c * nr] : 0.0;
+      else
+        v[u] = r > c ? src[r + c * nr] : (r == c ? 1.0 : 0.0);
+    }
   }
-  for (int idx = tid; idx < kRB * kRB; idx += kST) {
-    const int r = idx & (kRB - 1), c = idx >> 6;
-    double v = (r < nr && c < nr) ? g[(r0 + r) + (int64_t)(r0 + c) * ld] : 0.0;
-    if (kUpper) v *= rinv[c];
-    D[r + c * (kRB + 1)] = v;
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int idx = tid + u * kST;
+    D[(idx & (kRB - 1)) + (idx >> 6) * (kRB + 1)] = v[u];
   }
 }
 
@@ -257,33 +265,21 @@ __device__ __forceinline__ double block_dot(const double* lp, int64_t ld, const 
   return fma_block(r, xs + c0, c1 - c0, grp);
 }
 
-// forward: unit-lower 64x64 substitution in warp 0; lane holds rows lane, lane+32
-__device__ __forceinline__ void fwd_triangle(const double* D, int lane, double& v0, double& v1) {
+// diagonal tile solve in warp 0 (lane holds rows lane, lane + 32): v <- D v
+// with D the tile's inverse; 64 broadcasts, two independent FMA chains per row
+__device__ __forceinline__ void tile_apply(const double* D, int lane, double& v0, double& v1) {
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
-  for (int c = 0; c < kRB; ++c) {
-    const double yc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
-    if (c < 32) {
-      if (lane > c) v0 -= D[lane + c * (kRB + 1)] * yc;
-      v1 -= D[lane + 32 + c * (kRB + 1)] * yc;
-    } else if (lane + 32 > c) {
-      v1 -= D[lane + 32 + c * (kRB + 1)] * yc;
-    }
+  for (int c = 0; c < kRB; c += 2) {
+    const double x0 = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
+    const double x1 = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, (c + 1) & 31);
+    a0 += D[lane + c * (kRB + 1)] * x0;
+    b0 += D[lane + 32 + c * (kRB + 1)] * x0;
+    a1 += D[lane + (c + 1) * (kRB + 1)] * x1;
+    b1 += D[lane + 32 + (c + 1) * (kRB + 1)] * x1;
   }
-}
-
-// backward: upper substitution on the column-scaled block; on return v0/v1
-// are the right-hand sides after all updates (x = v * rinv[row])
-__device__ __forceinline__ void bwd_triangle(const double* E, int lane, double& v0, double& v1) {
-#pragma unroll
-  for (int c = kRB - 1; c >= 0; --c) {
-    const double vc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
-    if (c >= 32) {
-      v0 -= E[lane + c * (kRB + 1)] * vc;
-      if (lane + 32 < c) v1 -= E[lane + 32 + c * (kRB + 1)] * vc;
-    } else if (lane < c) {
-      v0 -= E[lane + c * (kRB + 1)] * vc;
-    }
-  }
+  v0 = a0 + a1;
+  v1 = b0 + b1;
 }
 
 // L2 prefetch of a contiguous byte range (TMA bulk prefetch, 16-byte granules)
@@ -299,6 +295,98 @@ __device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
 
 __device__ __forceinline__ void red_release(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// s_a, s_b += L[ra, c] y_c, L[rb, c] y_c over the columns c = grp mod 4 of
+// [0, ne) (contribution rows of a whole-front item; two rows per thread, 8
+// loads in flight per batch, the partial batch predicated)
+__device__ __forceinline__ void stream_rows2(const double* g, int64_t ld, const double* ys, int ne, int ra, bool oka,
+                                             int rb, bool okb, int grp, double& sa, double& sb) {
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  for (int c = grp; c < ne; c += 16) {
+    double la[4], lb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool okc = c + 4 * u < ne;
+      la[u] = oka && okc ? g[ra + (int64_t)(c + 4 * u) * ld] : 0.0;
+      lb[u] = okb && okc ? g[rb + (int64_t)(c + 4 * u) * ld] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u += 2) {
+      const double y0 = c + 4 * u < ne ? ys[c + 4 * u] : 0.0;
+      const double y1 = c + 4 * u + 4 < ne ? ys[c + 4 * u + 4] : 0.0;
+      a0 += la[u] * y0;
+      a1 += la[u + 1] * y1;
+      b0 += lb[u] * y0;
+      b1 += lb[u + 1] * y1;
+    }
+  }
+  sa = a0 + a1;
+  sb = b0 + b1;
+}
+
+// Forward sweep over one whole front (at most kWholeNpb pivot blocks) by one
+// CTA: w of every row gathered at once (b + the children's contribution
+// vectors) into wy, pivot blocks y = inv(L11) (w - L10 y) in warp 0 (y
+// replaces w in wy), then every
+// contribution row w - L y with four lanes per row (column classes reduced by
+// shuffles), 128 rows per pass, no barriers between passes.
+__device__ __forceinline__ void fwd_whole(const SweepArgs& A, const SolveItem& I, const double* g, int64_t ld,
+                                          double* D, double* wy, double (*part)[kRB], int tid) {
+  const int np = I.np, nf = I.nf;
+  if (tid == 0) prefetch_l2(g, sizeof(double) * (size_t)np * ld);  // L columns: one contiguous range
+  {
+    constexpr int kQ = kStage / kST;
+    int4 src[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int r = tid + q * kST;
+      src[q] = r < nf ? __ldg(&A.gsrc[I.rows_off + r]) : make_int4(-1, -1, -1, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      double v = 0.0;
+      if (src[q].x >= 0) v = A.b[src[q].x];
+      if (src[q].y >= 0) v += __ldcg(&A.cbvec[src[q].y]);
+      if (src[q].z >= 0) v += __ldcg(&A.cbvec[src[q].z]);
+      if (tid + q * kST < nf) wy[tid + q * kST] = v;
+    }
+  }
+  const int row = tid & (kRB - 1), grp = tid >> 6;
+  if (I.npb == 0) __syncthreads();
+  for (int blk = 0; blk < I.npb; ++blk) {
+    const int r0 = blk * kRB, nr = min(np, r0 + kRB) - r0;
+    load_dinv<false>(D, A.dinv + I.doff + (int64_t)kRB * kRB * blk, nr, tid);
+    double s = 0.0;
+    if (row < nr && r0 > 0) s = stream_cols(g + r0 + row, ld, wy, 0, r0, grp);
+    part[grp][row] = s;
+    __syncthreads();
+    if (tid < 32) {
+      double v0 = tid < nr ? wy[r0 + tid] - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]) : 0.0;
+      double v1 = tid + 32 < nr ? wy[r0 + tid + 32] -
+                                      (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32])
+                                : 0.0;
+      tile_apply(D, tid, v0, v1);
+      if (tid < nr) A.y[I.start + r0 + tid] = wy[r0 + tid] = v0;
+      if (tid + 32 < nr) A.y[I.start + r0 + tid + 32] = wy[r0 + tid + 32] = v1;
+    }
+    __syncthreads();
+  }
+  const int rr = tid >> 2, cg = tid & 3;
+  for (int p0 = np; p0 < nf; p0 += 2 * kRB) {
+    const int ra = p0 + rr, rb = ra + kRB;
+    double sa = 0.0, sb = 0.0;
+    if (np > 0) stream_rows2(g, ld, wy, np, ra, ra < nf, rb, rb < nf, cg, sa, sb);
+    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+    sb += __shfl_xor_sync(0xffffffffu, sb, 1);
+    sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+    sb += __shfl_xor_sync(0xffffffffu, sb, 2);
+    if (cg == 0) {
+      if (ra < nf) A.cbvec[I.cbvec_off + ra - np] = wy[ra] - sa;
+      if (rb < nf) A.cbvec[I.cbvec_off + rb - np] = wy[rb] - sb;
+    }
+  }
+  __syncthreads();  // every row written before thread 0 publishes
 }
 
 template <int kMinBlocks>
@@ -325,10 +413,11 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
     const double* g = A.pool + I.goff;
     const int64_t ld = I.ld;
     const bool whole = I.blk == kWhole;
-    const int nck = whole ? I.npb + I.ncbb : 1;
-    // whole-front item: its L columns (all rows) are one contiguous range;
-    // in L2 before the chunk loop reaches them
-    if (whole && tid == 0) prefetch_l2(g, sizeof(double) * (size_t)np * ld);
+    const int nck = whole ? 0 : 1;
+    if (whole) {
+      fwd_whole(A, I, g, ld, D, stg, part, tid);
+      if (A.trace && tid == 0) A.trace[8 * (size_t)it + 1] = A.trace[8 * (size_t)it + 6] = A.trace[8 * (size_t)it + 7] = gtime();
+    }
     unsigned long long waited = 0;
     // rows of chunk ck: pivot blocks first, then 64-row contribution chunks
     auto chunk_rows = [&](int ck, int& r0, int& nr, int& blk) {
@@ -351,8 +440,8 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
       }
       return v;
     };
-    double wnext;
-    {
+    double wnext = 0.0;
+    if (!whole) {
       int r0, nr, blk;
       chunk_rows(0, r0, nr, blk);
       wnext = gather_w(r0, nr);
@@ -366,7 +455,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
         chunk_rows(ck + 1, r1, nr1, b1);
         wnext = gather_w(r1, nr1);
       }
-      if (blk >= 0) load_diag<false>(D, nullptr, g, ld, r0, nr, tid);
+      if (blk >= 0) load_dinv<false>(D, A.dinv + I.doff + (int64_t)kRB * kRB * blk, nr, tid);
       __syncthreads();
       if (ck == 0) RQB_TRACE(1);
       // s = L[rows, 0:ncol) y
@@ -429,7 +518,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
           double v1 = tid + 32 < nr
                           ? wv[tid + 32] - (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32])
                           : 0.0;
-          fwd_triangle(D, tid, v0, v1);
+          tile_apply(D, tid, v0, v1);
           if (A.trace && tid == 0) A.trace[8 * (size_t)it + 7] = gtime();
           if (tid < nr) A.y[I.start + r0 + tid] = v0;
           if (tid + 32 < nr) A.y[I.start + r0 + tid + 32] = v1;
@@ -466,7 +555,6 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
   // staged x; whole-front items: [0, np) the front's own x, [kWholeNpb*64, ...) the ancestors' x_cb
   __shared__ double stg[kStage];
   __shared__ double part[4][kRB];
-  __shared__ double rinv[kRB];
   __shared__ int item_s, avail_s, keep_s;
   const int tid = threadIdx.x, row = tid & (kRB - 1), grp = tid >> 6;
   if (tid == 0) keep_s = -1;
@@ -496,7 +584,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
     for (int ck = 0; ck < nck; ++ck) {
       const int blk = whole ? I.npb - 1 - ck : I.blk;
       const int r0 = blk * kRB, nr = min(np, r0 + kRB) - r0;
-      load_diag<true>(D, rinv, g, ld, r0, nr, tid);
+      load_dinv<true>(D, A.dinv + I.doff + (int64_t)kRB * kRB * blk, nr, tid);
       double y0 = 0.0, y1 = 0.0;
       if (tid < 32) {
         if (tid < nr) y0 = A.y[I.start + r0 + tid];
@@ -575,9 +663,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
         if (tid < nr) v0 = y0 - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]);
         if (tid + 32 < nr)
           v1 = y1 - (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32]);
-        bwd_triangle(D, tid, v0, v1);
-        v0 *= rinv[tid];
-        v1 *= rinv[tid + 32];
+        tile_apply(D, tid, v0, v1);
         if (A.trace && tid == 0) A.trace[8 * (size_t)it + 7] = gtime();
         for (int h = 0; h < 2; ++h) {
           const int r = tid + 32 * h;
@@ -621,10 +707,31 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
 __global__ void net_rowperm(const FrontDev* __restrict__ fronts, const int32_t* __restrict__ ipiv,
                             const int32_t* __restrict__ perm, const int32_t* __restrict__ inv,
                             int32_t* __restrict__ rowperm, int4* __restrict__ gsrc) {
+  // the swap sequence is replayed in shared memory (one thread; fronts above
+  // kNetSmem pivots fall back to global memory)
+  constexpr int kNetSmem = 4096;
+  __shared__ int32_t sp[kNetSmem], sq[kNetSmem];
   const int f = blockIdx.x;
   const FrontDev F = fronts[f];
   int32_t* rp = rowperm + F.start;
-  if (threadIdx.x == 0) {
+  if (F.npiv <= kNetSmem) {
+    for (int k = threadIdx.x; k < F.npiv; k += blockDim.x) {
+      sp[k] = k;
+      sq[k] = ipiv[F.start + k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < F.npiv; ++k) {
+        const int p = sq[k];
+        if (p != k) {
+          const int32_t t = sp[k];
+          sp[k] = sp[p];
+          sp[p] = t;
+        }
+      }
+    __syncthreads();
+    for (int k = threadIdx.x; k < F.npiv; k += blockDim.x) rp[k] = sp[k];
+  } else if (threadIdx.x == 0) {
     for (int k = 0; k < F.npiv; ++k) rp[k] = k;
     for (int k = 0; k < F.npiv; ++k) {
       const int p = ipiv[F.start + k];
@@ -656,6 +763,85 @@ __global__ void net_rowperm(const FrontDev* __restrict__ fronts, const int32_t* 
       if (ir >= 0) v.z = static_cast<int>(c1off + ir);
     }
     gsrc[F.rows_off + r] = v;
+  }
+}
+
+// Inverse of every pivot block's diagonal tile, one CTA per tile, after the
+// factorization. Both triangles are inverted as lower-triangular matrices:
+// L11 itself (unit diagonal) and J U11 J (J the 64 x 64 reversal), zero padded
+// to 64 x 64 with a unit diagonal in the padding, in shared memory. Each lane
+// owns one column of an inverse in registers and eliminates with broadcast
+// reads (no barriers); all four warps run the same straight-line code (one
+// instruction stream for the whole CTA). The two halves of one square are
+// written back (strictly lower = inv(L11), upper incl. the diagonal =
+// inv(U11)), contiguous, column-major, ld = nr.
+constexpr int kDinvSmem = 2 * kRB * kRB * sizeof(double);
+struct DiagBlk {
+  int64_t goff;
+  int32_t ld, r0, nr, doff;
+};
+
+// x = column jj of inv(M), M lower triangular (column-major 64 x 64), rd[k] = 1 / M[k][k]
+__device__ __forceinline__ void inv_lower_col(const double* M, const double* rd, int jj, double (&x)[kRB]) {
+#pragma unroll
+  for (int i = 0; i < kRB; ++i) x[i] = i == jj ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < kRB; ++k) {
+    x[k] *= rd[k];
+#pragma unroll
+    for (int i = k + 1; i < kRB; ++i) x[i] -= M[i + k * kRB] * x[k];
+  }
+}
+
+__global__ void __launch_bounds__(128) diag_inverse(const DiagBlk* __restrict__ blks, const double* __restrict__ pool,
+                                                    double* __restrict__ dinv) {
+  extern __shared__ double dsm[];  // L11, J U11 J (64 x 64 each); afterwards the inverse square
+  __shared__ double rd[2][kRB];    // 1 (unit L), 1 / diag(J U11 J)
+  double* DL = dsm;
+  double* DU = dsm + kRB * kRB;
+  const DiagBlk B = blks[blockIdx.x];
+  const int nr = B.nr, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* g = pool + B.goff;
+  {
+    double v[kRB * kRB / 128];
+#pragma unroll
+    for (int u = 0; u < kRB * kRB / 128; ++u) {  // all loads in flight, then the stores
+      const int idx = tid + u * 128, r = idx & (kRB - 1), c = idx >> 6;
+      v[u] = (r < nr && c < nr) ? g[(B.r0 + r) + (int64_t)(B.r0 + c) * B.ld] : (r == c ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < kRB * kRB / 128; ++u) {
+      const int idx = tid + u * 128, r = idx & (kRB - 1), c = idx >> 6;
+      if (r > c) DL[idx] = v[u];
+      else if (r == c) DL[idx] = 1.0;
+      if (r <= c) DU[(kRB - 1 - r) + (kRB - 1 - c) * kRB] = v[u];  // (J U J)[63-r][63-c] = U[r][c]
+    }
+  }
+  __syncthreads();
+  if (tid < kRB) {
+    rd[0][tid] = 1.0;
+    rd[1][tid] = 1.0 / DU[tid + tid * kRB];
+  }
+  __syncthreads();
+  const int up = warp >> 1, jj = lane + 32 * (warp & 1);
+  double x[kRB];
+  inv_lower_col(up ? DU : DL, rd[up], jj, x);
+  __syncthreads();
+  double* X = dsm;
+  if (!up) {
+#pragma unroll
+    for (int i = 0; i < kRB; ++i)
+      if (i > jj) X[i + jj * kRB] = x[i];
+  } else {  // inv(U)[63-i][63-jj] = inv(J U J)[i][jj]
+#pragma unroll
+    for (int i = 0; i < kRB; ++i)
+      if (i >= jj) X[(kRB - 1 - i) + (kRB - 1 - jj) * kRB] = x[i];
+  }
+  __syncthreads();
+  double* out = dinv + B.doff;
+  for (int idx = tid; idx < nr * nr; idx += 128) {
+    const int r = idx % nr, c = idx / nr;
+    out[idx] = X[r + c * kRB];
   }
 }
 
@@ -695,6 +881,25 @@ void rqb_solve_prepare(FactorEngine& fe) {
   }
   if (static_cast<int64_t>(S.rows.size()) > INT32_MAX || cbtot > INT32_MAX || fe.n > INT32_MAX)
     throw Error(errc::solver, "solve: index range exceeds int32");
+  // diagonal-tile inverses: per front its pivot blocks' squares, contiguous
+  std::vector<int32_t> doff_f(nfr);
+  std::vector<DiagBlk> dblk;
+  int64_t dtot = 0;
+  for (int f = 0; f < nfr; ++f) {
+    const Front& F = S.fronts[f];
+    doff_f[f] = static_cast<int32_t>(dtot);
+    for (int b = 0; b < npb[f]; ++b) {
+      const int nr = std::min(F.npiv, (b + 1) * kRB) - b * kRB;
+      dblk.push_back(DiagBlk{fe.fronts_h[f].off, fe.fronts_h[f].ld, b * kRB, nr, static_cast<int32_t>(dtot)});
+      dtot += static_cast<int64_t>(nr) * nr;
+      if (dtot > INT32_MAX) throw Error(errc::solver, "solve: diagonal-tile inverses exceed int32 offsets");
+    }
+  }
+  fe.n_dblk = static_cast<int>(dblk.size());
+  RQB_CUDA(cudaFuncSetAttribute(diag_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, kDinvSmem));
+  if (dblk.empty()) dblk.push_back(DiagBlk{});
+  fe.d_dblk.upload(dblk.data(), sizeof(DiagBlk) * dblk.size(), fe.stream);
+  fe.d_dinv.alloc(sizeof(double) * std::max<int64_t>(1, dtot));
   int32_t eoff = 0;
   std::vector<int32_t> ech_off(nfr);
   for (int f = 0; f < nfr; ++f) {
@@ -722,6 +927,7 @@ void rqb_solve_prepare(FactorEngine& fe) {
     it.cbvec_off = static_cast<int32_t>(D.cbvec_off);
     it.ech_off = ech_off[f];
     it.nech = static_cast<int32_t>(echl[f].size());
+    it.doff = doff_f[f];
     return it;
   };
   {
@@ -834,6 +1040,9 @@ void rqb_rowperm_enqueue(FactorEngine& fe) {
   net_rowperm<<<nfr, 128, 0, fe.stream>>>(fe.d_fronts.as<FrontDev>(), fe.d_ipiv.as<int32_t>(),
                                           fe.d_perm.as<int32_t>(), fe.d_inv.as<int32_t>(),
                                           fe.d_rowperm.as<int32_t>(), fe.d_gsrc.as<int4>());
+  if (fe.n_dblk > 0)
+    diag_inverse<<<fe.n_dblk, 128, kDinvSmem, fe.stream>>>(fe.d_dblk.as<DiagBlk>(), fe.d_pool.as<double>(),
+                                                   fe.d_dinv.as<double>());
 }
 
 void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scale, const double* vu,
@@ -858,6 +1067,7 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
   A.gsrc = fe.d_gsrc.as<int4>();
   A.stall = fe.d_sweep_stall.as<int>();
   A.pool = fe.d_pool.as<double>();
+  A.dinv = fe.d_dinv.as<double>();
   A.perm = fe.d_perm.as<int32_t>();
   A.rows = fe.d_rows.as<int32_t>();
   A.b = b;

@@ -106,6 +106,11 @@ struct FactorEngine {
   // sync-free solve: work items, per-front item counts, dependency counters,
   // net row permutation of each front's pivot block
   DeviceBuffer d_items_fwd, d_items_bwd, d_rowperm, d_sf, d_ech, d_gsrc;
+  // inverses of the pivot blocks' 64x64 diagonal tiles (computed after each
+  // factorization): per block an nr x nr column-major square, strictly lower =
+  // inv(L11) (unit diagonal implied), upper = inv(U11); d_dblk lists the blocks
+  DeviceBuffer d_dinv, d_dblk;
+  int n_dblk = 0;
   // dataflow state of the two sweeps in one int32 buffer (template + live
   // copy, reset by one D2D copy per solve): front deps fwd/bwd, ready queues
   // fwd/bwd, {head, tail} x2, per-front published/finished counters
