@@ -419,14 +419,8 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
       if (A.trace && tid == 0) A.trace[8 * (size_t)it + 1] = A.trace[8 * (size_t)it + 6] = A.trace[8 * (size_t)it + 7] = gtime();
     }
     unsigned long long waited = 0;
-    // rows of chunk ck: pivot blocks first, then 64-row contribution chunks
-    auto chunk_rows = [&](int ck, int& r0, int& nr, int& blk) {
+    auto chunk_rows = [&](int, int& r0, int& nr, int& blk) {
       r0 = I.r0, nr = I.nr, blk = I.blk;
-      if (whole) {
-        blk = ck < I.npb ? ck : -1;
-        r0 = ck < I.npb ? ck * kRB : np + (ck - I.npb) * kRB;
-        nr = (ck < I.npb ? min(np, r0 + kRB) : min(I.nf, r0 + kRB)) - r0;
-      }
     };
     // w = b + children's contributions (children complete: the front is ready);
     // the gather of the next chunk is issued while the current one is processed
@@ -462,9 +456,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
       const int ncol = min(np, (blk >= 0 ? blk : I.npb) * kRB);
       const double* lp = g + (r0 + row);
       double s = 0.0;
-      if (whole) {  // y of the earlier blocks is this CTA's own (stg): no waits
-        if (row < nr) s = stream_cols(lp, ld, stg, 0, ncol, grp);
-      } else {
+      {
         // rounds: take every block published so far, stage its y, stream it;
         // the L of the first block not yet seen published is in flight during the wait
         int done = 0;
@@ -522,10 +514,6 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
           if (A.trace && tid == 0) A.trace[8 * (size_t)it + 7] = gtime();
           if (tid < nr) A.y[I.start + r0 + tid] = v0;
           if (tid + 32 < nr) A.y[I.start + r0 + tid + 32] = v1;
-          if (whole) {
-            if (tid < nr) stg[r0 + tid] = v0;
-            if (tid + 32 < nr) stg[r0 + tid + 32] = v1;
-          }
         }
       } else if (tid < nr) {
         A.cbvec[I.cbvec_off + r0 + tid - np] = wv[tid] - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]);
@@ -549,12 +537,132 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
   }
 }
 
+// x of one pivot row: xnew (ND order, read by descendants), caller order
+// scaled, and the fused lower block of apply_operator
+__device__ __forceinline__ void store_x(const SweepArgs& A, int gi, double v) {
+  A.xnew[gi] = v;
+  const int o = A.perm[gi];
+  const double sv = A.scale * v;
+  A.xout[o] = sv;
+  if (A.xl_out) A.xl_out[o] = A.sigma * sv + A.vu[o];
+}
+
+// acc[q] = sum over this warp's columns c (c = warp mod 8) of U12[lane + 32 q, c] x_c:
+// one warp reads whole columns (np contiguous values), 16 / kRPL columns per
+// iteration, i.e. 16 loads in flight per lane
+template <int kRPL>
+__device__ __forceinline__ void u12_cols(const double* g, int64_t ld, int np, int ncb, const double* xc, int lane,
+                                         int warp, double (&acc)[4]) {
+  constexpr int kU = 16 / kRPL, kW = kST / 32;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] = 0.0;
+  const double* up = g + (int64_t)np * ld + lane;
+  for (int c0 = warp; c0 < ncb; c0 += kW * kU) {
+    double a[kU][kRPL];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int q = 0; q < kRPL; ++q) {
+        const int c = c0 + kW * u;
+        a[u][q] = c < ncb && lane + 32 * q < np ? up[(int64_t)c * ld + 32 * q] : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int c = c0 + kW * u;
+      const double xv = c < ncb ? xc[c] : 0.0;
+#pragma unroll
+      for (int q = 0; q < kRPL; ++q) acc[q] += a[u][q] * xv;
+    }
+  }
+}
+
+// L2 prefetch (one line per thread-iteration, no bulk op per column) of the
+// U12 block: rows [0, np) of the columns [np, nf)
+__device__ __forceinline__ void prefetch_u12(const double* g, int64_t ld, int np, int nf, int tid) {
+  const int nl = (np * 8 + 127) / 128 + 1;  // lines per column (unaligned start)
+  for (int i = tid; i < (nf - np) * nl; i += kST) {
+    const int c = np + i / nl, l = i % nl;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(g + (int64_t)c * ld);
+    const uintptr_t a = (a0 & ~uintptr_t(127)) + 128 * l;
+    if (a < a0 + 8 * np) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+  }
+}
+
+// Backward sweep over one whole front (at most kWholeNpb pivot blocks) by one
+// CTA: the ancestors' x_cb gathered at once, U12 x_cb for every pivot row
+// (warp per column class, partials reduced in shared memory), then the pivot
+// blocks last first: x = inv(U11) (y - U12 x_cb - U[blk, later] x_later) in warp 0.
+__device__ __forceinline__ void bwd_whole(const SweepArgs& A, const SolveItem& I, const double* g, int64_t ld,
+                                          const int32_t* rw, double* D, double* xs, double* pv,
+                                          double (*part)[kRB], int tid) {
+  constexpr int kCbBase = kWholeNpb * kRB;  // xs: [0, np) this front's x, [kCbBase, ...) x_cb
+  const int np = I.np, nf = I.nf, ncb = nf - np;
+  prefetch_u12(g, ld, np, nf, tid);
+  {
+    constexpr int kQ = kStage / kST;
+    int src[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) src[q] = tid + q * kST < ncb ? __ldg(&rw[np + tid + q * kST]) : -1;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q)
+      if (src[q] >= 0) xs[kCbBase + tid + q * kST] = __ldcg(&A.xnew[src[q]]);
+  }
+  const double yv = tid < np ? A.y[I.start + tid] : 0.0;
+  __syncthreads();
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    double acc[4];
+    if (np <= 32)
+      u12_cols<1>(g, ld, np, ncb, xs + kCbBase, lane, warp, acc);
+    else if (np <= 64)
+      u12_cols<2>(g, ld, np, ncb, xs + kCbBase, lane, warp, acc);
+    else
+      u12_cols<4>(g, ld, np, ncb, xs + kCbBase, lane, warp, acc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) D[warp * 128 + lane + 32 * q] = acc[q];  // D as scratch
+    __syncthreads();
+    if (tid < np) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kST / 32; ++w) s += D[w * 128 + tid];
+      pv[tid] = yv - s;
+    }
+    __syncthreads();
+  }
+  const int row = tid & (kRB - 1), grp = tid >> 6;
+  for (int blk = I.npb - 1; blk >= 0; --blk) {
+    const int r0 = blk * kRB, nr = min(np, r0 + kRB) - r0, lo = r0 + kRB;
+    load_dinv<true>(D, A.dinv + I.doff + (int64_t)kRB * kRB * blk, nr, tid);
+    double s = 0.0;
+    if (row < nr && lo < np) s = stream_cols(g + r0 + row, ld, xs, lo, np, grp);
+    part[grp][row] = s;
+    __syncthreads();
+    if (tid < 32) {
+      double v0 = tid < nr ? pv[r0 + tid] - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]) : 0.0;
+      double v1 = tid + 32 < nr ? pv[r0 + tid + 32] -
+                                      (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32])
+                                : 0.0;
+      tile_apply(D, tid, v0, v1);
+      if (tid < nr) {
+        xs[r0 + tid] = v0;
+        store_x(A, I.start + r0 + tid, v0);
+      }
+      if (tid + 32 < nr) {
+        xs[r0 + tid + 32] = v1;
+        store_x(A, I.start + r0 + tid + 32, v1);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <int kMinBlocks>
 __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
   __shared__ double D[kRB * (kRB + 1)];
   // staged x; whole-front items: [0, np) the front's own x, [kWholeNpb*64, ...) the ancestors' x_cb
   __shared__ double stg[kStage];
   __shared__ double part[4][kRB];
+  __shared__ double pv[kWholeNpb * kRB];  // whole-front items: y - U12 x_cb of the pivot rows
   __shared__ int item_s, avail_s, keep_s;
   const int tid = threadIdx.x, row = tid & (kRB - 1), grp = tid >> 6;
   if (tid == 0) keep_s = -1;
@@ -574,15 +682,14 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
     const int64_t ld = I.ld;
     const int32_t* rw = A.rows + I.rows_off;
     const bool whole = I.blk == kWhole;
-    constexpr int kCbBase = kWholeNpb * kRB;
-    if (whole)  // the item's U12 columns (rows < np of the contribution columns) into L2
-      for (int c = np + tid; c < nf; c += kST) prefetch_l2(g + (int64_t)c * ld, sizeof(double) * np);
-    if (whole)
-      for (int c = tid; c < nf - np; c += kST) stg[kCbBase + c] = __ldcg(&A.xnew[rw[np + c]]);
-    const int nck = whole ? I.npb : 1;
+    if (whole) {
+      bwd_whole(A, I, g, ld, rw, D, stg, pv, part, tid);
+      if (A.trace && tid == 0) A.trace[8 * (size_t)it + 1] = A.trace[8 * (size_t)it + 6] = A.trace[8 * (size_t)it + 7] = gtime();
+    }
+    const int nck = whole ? 0 : 1;
     unsigned long long waited = 0;
     for (int ck = 0; ck < nck; ++ck) {
-      const int blk = whole ? I.npb - 1 - ck : I.blk;
+      const int blk = I.blk;
       const int r0 = blk * kRB, nr = min(np, r0 + kRB) - r0;
       load_dinv<true>(D, A.dinv + I.doff + (int64_t)kRB * kRB * blk, nr, tid);
       double y0 = 0.0, y1 = 0.0;
@@ -597,12 +704,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
       const double* up = g + (r0 + row);
       const int lo = (blk + 1) * kRB;
       double s = 0.0;
-      if (whole) {
-        if (row < nr) {
-          s = stream_cols(up, ld, stg + kCbBase - np, np, nf, grp);
-          s += stream_cols(up, ld, stg, lo, np, grp);
-        }
-      } else {
+      {
         for (int base = np; base < nf; base += kStage) {
           const int hi = min(nf, base + kStage);
           for (int c = tid; c < hi - base; c += kST) stg[c] = __ldcg(&A.xnew[rw[base + c]]);
@@ -671,7 +773,6 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
             const double v = h ? v1 : v0;
             const int gi = I.start + r0 + r;
             A.xnew[gi] = v;
-            if (whole) stg[r0 + r] = v;
             const int o = A.perm[gi];
             const double sv = A.scale * v;
             A.xout[o] = sv;
@@ -766,82 +867,114 @@ __global__ void net_rowperm(const FrontDev* __restrict__ fronts, const int32_t* 
   }
 }
 
-// Inverse of every pivot block's diagonal tile, one CTA per tile, after the
-// factorization. Both triangles are inverted as lower-triangular matrices:
-// L11 itself (unit diagonal) and J U11 J (J the 64 x 64 reversal), zero padded
-// to 64 x 64 with a unit diagonal in the padding, in shared memory. Each lane
-// owns one column of an inverse in registers and eliminates with broadcast
-// reads (no barriers); all four warps run the same straight-line code (one
-// instruction stream for the whole CTA). The two halves of one square are
-// written back (strictly lower = inv(L11), upper incl. the diagonal =
-// inv(U11)), contiguous, column-major, ld = nr.
-constexpr int kDinvSmem = 2 * kRB * kRB * sizeof(double);
+// Inverse of every pivot block's diagonal tile after the factorization.
+// Persistent CTAs take (tile, triangle) items: L11 itself (unit diagonal) and
+// J U11 J (J the nr x nr reversal), both lower triangular, zero padded to
+// 64 x 64 with a unit diagonal in the padding. Blocked in 32 x 32 halves:
+// the diagonal halves are inverted by warps 0 / 1 (a lane owns one column in
+// registers, broadcast reads, straight-line code small enough to stay in the
+// instruction cache), then X21 = -X22 (M21 X11) by all four warps. The L item
+// writes the strictly lower part of the tile's square, the U item the upper
+// part incl. the diagonal (contiguous, column-major, ld = nr).
 struct DiagBlk {
   int64_t goff;
   int32_t ld, r0, nr, doff;
 };
+constexpr int kInvT = 128;   // threads per CTA
+constexpr int kML = kRB + 1;  // leading dimension of the tile in shared memory
 
-// x = column jj of inv(M), M lower triangular (column-major 64 x 64), rd[k] = 1 / M[k][k]
-__device__ __forceinline__ void inv_lower_col(const double* M, const double* rd, int jj, double (&x)[kRB]) {
+__global__ void __launch_bounds__(kInvT, 4) diag_inverse(const DiagBlk* __restrict__ blks, int ntiles,
+                                                      const double* __restrict__ pool, double* __restrict__ dinv) {
+  __shared__ double M[kRB * kML];
+  __shared__ double T[32 * 33];
+  __shared__ double rd[kRB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int item = blockIdx.x; item < 2 * ntiles; item += gridDim.x) {
+    const int up = item & 1;
+    const DiagBlk B = blks[item >> 1];
+    const int nr = B.nr;
+    const bool two = nr > 32;
+    const int nb = two ? kRB : 32, lnb = two ? 6 : 5;  // padded size, log2
+    const double* g = pool + B.goff + B.r0 + (int64_t)B.r0 * B.ld;
+    __syncthreads();  // the previous item is done with shared memory
+    for (int i0 = 0; i0 < nb * nb; i0 += 16 * kInvT) {
+      double v[16];
 #pragma unroll
-  for (int i = 0; i < kRB; ++i) x[i] = i == jj ? 1.0 : 0.0;
+      for (int u = 0; u < 16; ++u) {  // all loads in flight, then the stores
+        const int idx = i0 + tid + u * kInvT, r = idx & (nb - 1), c = idx >> lnb;
+        v[u] = 0.0;
+        if (idx < nb * nb && r >= c) {
+          if (r >= nr || c >= nr)
+            v[u] = r == c ? 1.0 : 0.0;
+          else if (!up)
+            v[u] = r == c ? 1.0 : g[r + (int64_t)c * B.ld];
+          else
+            v[u] = g[(nr - 1 - r) + (int64_t)(nr - 1 - c) * B.ld];
+        }
+      }
 #pragma unroll
-  for (int k = 0; k < kRB; ++k) {
-    x[k] *= rd[k];
-#pragma unroll
-    for (int i = k + 1; i < kRB; ++i) x[i] -= M[i + k * kRB] * x[k];
-  }
-}
-
-__global__ void __launch_bounds__(128) diag_inverse(const DiagBlk* __restrict__ blks, const double* __restrict__ pool,
-                                                    double* __restrict__ dinv) {
-  extern __shared__ double dsm[];  // L11, J U11 J (64 x 64 each); afterwards the inverse square
-  __shared__ double rd[2][kRB];    // 1 (unit L), 1 / diag(J U11 J)
-  double* DL = dsm;
-  double* DU = dsm + kRB * kRB;
-  const DiagBlk B = blks[blockIdx.x];
-  const int nr = B.nr, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double* g = pool + B.goff;
-  {
-    double v[kRB * kRB / 128];
-#pragma unroll
-    for (int u = 0; u < kRB * kRB / 128; ++u) {  // all loads in flight, then the stores
-      const int idx = tid + u * 128, r = idx & (kRB - 1), c = idx >> 6;
-      v[u] = (r < nr && c < nr) ? g[(B.r0 + r) + (int64_t)(B.r0 + c) * B.ld] : (r == c ? 1.0 : 0.0);
+      for (int u = 0; u < 16; ++u) {
+        const int idx = i0 + tid + u * kInvT;
+        if (idx < nb * nb) M[(idx & (nb - 1)) + (idx >> lnb) * kML] = v[u];
+      }
     }
+    __syncthreads();
+    if (tid < nb) rd[tid] = 1.0 / M[tid + tid * kML];
+    __syncthreads();
+    const int o = 32 * warp;
+    double x[32];
+    if (warp == 0 || (warp == 1 && two)) {  // X_ww = inv(M_ww), column `lane`
 #pragma unroll
-    for (int u = 0; u < kRB * kRB / 128; ++u) {
-      const int idx = tid + u * 128, r = idx & (kRB - 1), c = idx >> 6;
-      if (r > c) DL[idx] = v[u];
-      else if (r == c) DL[idx] = 1.0;
-      if (r <= c) DU[(kRB - 1 - r) + (kRB - 1 - c) * kRB] = v[u];  // (J U J)[63-r][63-c] = U[r][c]
+      for (int i = 0; i < 32; ++i) x[i] = i == lane ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        x[k] *= rd[o + k];
+#pragma unroll
+        for (int i = k + 1; i < 32; ++i) x[i] -= M[(o + i) + (o + k) * kML] * x[k];
+      }
     }
-  }
-  __syncthreads();
-  if (tid < kRB) {
-    rd[0][tid] = 1.0;
-    rd[1][tid] = 1.0 / DU[tid + tid * kRB];
-  }
-  __syncthreads();
-  const int up = warp >> 1, jj = lane + 32 * (warp & 1);
-  double x[kRB];
-  inv_lower_col(up ? DU : DL, rd[up], jj, x);
-  __syncthreads();
-  double* X = dsm;
-  if (!up) {
+    __syncthreads();
+    if (warp == 0 || (warp == 1 && two)) {
 #pragma unroll
-    for (int i = 0; i < kRB; ++i)
-      if (i > jj) X[i + jj * kRB] = x[i];
-  } else {  // inv(U)[63-i][63-jj] = inv(J U J)[i][jj]
+      for (int i = 0; i < 32; ++i)
+        if (i >= lane) M[(o + i) + (o + lane) * kML] = x[i];
+    }
+    __syncthreads();
+    if (two) {
+      // T = M21 X11 (X11 lower): thread = column lane, rows warp*8 .. +8
+      double acc[8];
 #pragma unroll
-    for (int i = 0; i < kRB; ++i)
-      if (i >= jj) X[(kRB - 1 - i) + (kRB - 1 - jj) * kRB] = x[i];
-  }
-  __syncthreads();
-  double* out = dinv + B.doff;
-  for (int idx = tid; idx < nr * nr; idx += 128) {
-    const int r = idx % nr, c = idx / nr;
-    out[idx] = X[r + c * kRB];
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+      for (int m = lane; m < 32; ++m) {
+        const double xm = M[m + lane * kML];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] += M[(32 + warp * 8 + q) + m * kML] * xm;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) T[(warp * 8 + q) + lane * 33] = acc[q];
+      __syncthreads();
+      // X21 = -X22 T (X22 lower), written over M21
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+      for (int m = 0; m < 32; ++m) {
+        const double t = T[m + lane * 33];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (m <= warp * 8 + q) acc[q] += M[(32 + warp * 8 + q) + (32 + m) * kML] * t;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) M[(32 + warp * 8 + q) + lane * kML] = -acc[q];
+      __syncthreads();
+    }
+    double* out = dinv + B.doff;
+    {
+      const int r = tid & (kRB - 1);
+      if (r < nr)
+        for (int c = tid >> 6; c < nr; c += kInvT / kRB) {
+          if (!up && r > c) out[r + c * nr] = M[r + c * kML];
+          if (up && r <= c) out[r + c * nr] = M[(nr - 1 - r) + (nr - 1 - c) * kML];
+        }
+    }
   }
 }
 
@@ -896,7 +1029,6 @@ void rqb_solve_prepare(FactorEngine& fe) {
     }
   }
   fe.n_dblk = static_cast<int>(dblk.size());
-  RQB_CUDA(cudaFuncSetAttribute(diag_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, kDinvSmem));
   if (dblk.empty()) dblk.push_back(DiagBlk{});
   fe.d_dblk.upload(dblk.data(), sizeof(DiagBlk) * dblk.size(), fe.stream);
   fe.d_dinv.alloc(sizeof(double) * std::max<int64_t>(1, dtot));
@@ -1040,9 +1172,14 @@ void rqb_rowperm_enqueue(FactorEngine& fe) {
   net_rowperm<<<nfr, 128, 0, fe.stream>>>(fe.d_fronts.as<FrontDev>(), fe.d_ipiv.as<int32_t>(),
                                           fe.d_perm.as<int32_t>(), fe.d_inv.as<int32_t>(),
                                           fe.d_rowperm.as<int32_t>(), fe.d_gsrc.as<int4>());
-  if (fe.n_dblk > 0)
-    diag_inverse<<<fe.n_dblk, 128, kDinvSmem, fe.stream>>>(fe.d_dblk.as<DiagBlk>(), fe.d_pool.as<double>(),
-                                                   fe.d_dinv.as<double>());
+  if (fe.n_dblk > 0) {
+    int nsm = 148, occ = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, diag_inverse, kInvT, 0);
+    const int grid = std::min(2 * fe.n_dblk, nsm * std::max(1, occ));
+    diag_inverse<<<grid, kInvT, 0, fe.stream>>>(fe.d_dblk.as<DiagBlk>(), fe.n_dblk, fe.d_pool.as<double>(),
+                                               fe.d_dinv.as<double>());
+  }
 }
 
 void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scale, const double* vu,
