@@ -86,6 +86,22 @@ __device__ __forceinline__ unsigned long long gtime() {
     A.trace[8 * (size_t)it + (k)] = gtime();                               \
   }
 
+// Solution entries of pivot blocks are published by value: the solve resets
+// y and x to an all-ones bit pattern (a NaN no FP64 operation produces; NaN
+// results are canonical) and a waiting item polls the entries of the block it
+// needs directly (relaxed loads of relaxed stores, 8-byte single-copy atomic):
+// no fence or flag round trip on the chain of pivot blocks. The per-front
+// counters stay for everything off the chain (windows, earlier blocks).
+constexpr long long kUnset = -1LL;
+__device__ __forceinline__ void st_relaxed(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -163,6 +179,28 @@ __device__ __forceinline__ bool stalled(const SweepArgs& A, unsigned long long& 
   return false;
 }
 
+
+// Warp 0: wait until entries [0, n) of v (n <= 64) are published, stage them
+// in dst. Returns false if the watchdog fired.
+__device__ __forceinline__ bool poll_block(const SweepArgs& A, const double* v, int n, double* dst, int lane) {
+  unsigned long long t0 = 0;
+  for (;;) {
+    const double a = lane < n ? ld_relaxed(v + lane) : 0.0;
+    const double b = lane + 32 < n ? ld_relaxed(v + lane + 32) : 0.0;
+    const bool ok = __double_as_longlong(a) != kUnset && __double_as_longlong(b) != kUnset;
+    if (__all_sync(0xffffffffu, ok)) {
+      if (lane < n) dst[lane] = a;
+      if (lane + 32 < n) dst[lane + 32] = b;
+      return true;
+    }
+    int st = 0;
+    if (lane == 0) {
+      __nanosleep(20);
+      st = stalled(A, t0);
+    }
+    if (__shfl_sync(0xffffffffu, st, 0)) return false;
+  }
+}
 
 // Claim the next queue slot and wait for it; -1 once every item has finished
 // (items kept by a CTA never pass through the queue, so the last claimed
@@ -395,7 +433,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
   __shared__ double stg[kStage];  // staged y (whole-front items: the front's own y)
   __shared__ double part[4][kRB];
   __shared__ double wv[kRB];
-  __shared__ int item_s, avail_s, keep_s;
+  __shared__ int item_s, avail_s, keep_s, staged_s;
   const int tid = threadIdx.x, row = tid & (kRB - 1), grp = tid >> 6;
   if (tid == 0) keep_s = -1;
   for (;;) {
@@ -464,29 +502,33 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
           const int b1 = min(ncol, done + kRB);
           double lr[kRB / 4];
           load_block(lr, lp, ld, row < nr, done, b1, grp);
-          if (tid == 0) {
+          if (tid < 32) {  // blocks published so far (counter), else poll the next block's values
             const unsigned long long w0 = A.trace ? gtime() : 0;
-            int p;
-            unsigned long long ts0 = 0;
-            while ((p = ld_acquire(&A.pub[I.front])) * kRB <= done) {
-              __nanosleep(20);
-              if (stalled(A, ts0)) {
-                p = (ncol + kRB - 1) / kRB;  // drain: give up on the dependency
-                break;
-              }
+            int p = tid == 0 ? ld_acquire(&A.pub[I.front]) : 0;
+            p = __shfl_sync(0xffffffffu, p, 0);
+            int av = min(ncol, p * kRB), stgd = 0;
+            if (av <= done) {
+              if (!poll_block(A, A.y + I.start + done, b1 - done, stg, tid)) p = -1;
+              av = b1;
+              stgd = 1;
             }
-            avail_s = min(ncol, p * kRB);
-            if (A.trace) {
-              const unsigned long long w1 = gtime();
-              waited += w1 - w0;
-              A.trace[8 * (size_t)it + 4] = w1;
+            if (tid == 0) {
+              avail_s = av;
+              staged_s = stgd;
+              if (A.trace) {
+                const unsigned long long w1 = gtime();
+                waited += w1 - w0;
+                A.trace[8 * (size_t)it + 4] = w1;
+              }
             }
           }
           __syncthreads();
           const int avail = avail_s;
+          const bool stgd = staged_s;
           for (int base = done; base < avail; base += kStage) {
             const int hi = min(avail, base + kStage);
-            for (int c = tid; c < hi - base; c += kST) stg[c] = __ldcg(&A.y[I.start + base + c]);
+            if (!stgd)
+              for (int c = tid; c < hi - base; c += kST) stg[c] = __ldcg(&A.y[I.start + base + c]);
             __syncthreads();
             if (row < nr) {
               if (base == done) {
@@ -512,8 +554,8 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
                           : 0.0;
           tile_apply(D, tid, v0, v1);
           if (A.trace && tid == 0) A.trace[8 * (size_t)it + 7] = gtime();
-          if (tid < nr) A.y[I.start + r0 + tid] = v0;
-          if (tid + 32 < nr) A.y[I.start + r0 + tid + 32] = v1;
+          if (tid < nr) st_relaxed(&A.y[I.start + r0 + tid], v0);
+          if (tid + 32 < nr) st_relaxed(&A.y[I.start + r0 + tid + 32], v1);
         }
       } else if (tid < nr) {
         A.cbvec[I.cbvec_off + r0 + tid - np] = wv[tid] - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]);
@@ -663,7 +705,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
   __shared__ double stg[kStage];
   __shared__ double part[4][kRB];
   __shared__ double pv[kWholeNpb * kRB];  // whole-front items: y - U12 x_cb of the pivot rows
-  __shared__ int item_s, avail_s, keep_s;
+  __shared__ int item_s, avail_s, keep_s, staged_s;
   const int tid = threadIdx.x, row = tid & (kRB - 1), grp = tid >> 6;
   if (tid == 0) keep_s = -1;
   for (;;) {
@@ -719,29 +761,33 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
           const int b0 = max(lo, ((done_hi - 1) / kRB) * kRB);
           double ur[kRB / 4];
           load_block(ur, up, ld, row < nr, b0, done_hi, grp);
-          if (tid == 0) {
+          if (tid < 32) {  // blocks published so far (counter), else poll the next block's values
             const unsigned long long w0 = A.trace ? gtime() : 0;
-            int p;
-            unsigned long long ts0 = 0;
-            while (max(lo, (I.npb - (p = ld_acquire(&A.pub[I.front]))) * kRB) >= done_hi) {
-              __nanosleep(20);
-              if (stalled(A, ts0)) {
-                p = I.npb;  // drain: give up on the dependency
-                break;
-              }
+            int p = tid == 0 ? ld_acquire(&A.pub[I.front]) : 0;
+            p = __shfl_sync(0xffffffffu, p, 0);
+            int av = max(lo, (I.npb - p) * kRB), stgd = 0;
+            if (av >= done_hi) {
+              poll_block(A, A.xnew + I.start + b0, done_hi - b0, stg, tid);
+              av = b0;
+              stgd = 1;
             }
-            avail_s = max(lo, (I.npb - p) * kRB);
-            if (A.trace) {
-              const unsigned long long w1 = gtime();
-              waited += w1 - w0;
-              A.trace[8 * (size_t)it + 4] = w1;
+            if (tid == 0) {
+              avail_s = av;
+              staged_s = stgd;
+              if (A.trace) {
+                const unsigned long long w1 = gtime();
+                waited += w1 - w0;
+                A.trace[8 * (size_t)it + 4] = w1;
+              }
             }
           }
           __syncthreads();
           const int avail_lo = avail_s;
+          const bool stgd = staged_s;
           for (int top = done_hi, bot; top > avail_lo; top = bot) {
             bot = max(avail_lo, (top - kStage + kRB - 1) / kRB * kRB);  // block aligned
-            for (int c = tid; c < top - bot; c += kST) stg[c] = __ldcg(&A.xnew[I.start + bot + c]);
+            if (!stgd)
+              for (int c = tid; c < top - bot; c += kST) stg[c] = __ldcg(&A.xnew[I.start + bot + c]);
             __syncthreads();
             if (row < nr) {
               if (top == done_hi) {
@@ -772,7 +818,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
           if (r < nr) {
             const double v = h ? v1 : v0;
             const int gi = I.start + r0 + r;
-            A.xnew[gi] = v;
+            st_relaxed(&A.xnew[gi], v);
             const int o = A.perm[gi];
             const double sv = A.scale * v;
             A.xout[o] = sv;
@@ -1187,6 +1233,9 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
   const int nfr = static_cast<int>(fe.fronts_h.size());
   cudaStream_t st = fe.stream;
   RQB_CUDA(cudaMemcpyAsync(fe.d_state.p, fe.d_state0.p, fe.d_state0.bytes, cudaMemcpyDeviceToDevice, st));
+  // published-by-value entries start unset (all-ones bit pattern, kUnset)
+  RQB_CUDA(cudaMemsetAsync(fe.d_y.p, 0xff, sizeof(double) * fe.n, st));
+  RQB_CUDA(cudaMemsetAsync(fe.d_xnew.p, 0xff, sizeof(double) * fe.n, st));
   int* sb = fe.d_state.as<int>();
   SweepArgs A{};
   unsigned long long* trace = nullptr;
