@@ -165,6 +165,18 @@ __device__ __forceinline__ void front_ready(const SweepArgs& A, int f, int* keep
   }
 }
 
+// forward: one item of a child of f finished (deps counts the children's items);
+// the acq_rel atomic publishes this CTA's contribution vector (ordered by the
+// preceding barrier) and acquires the other items' on the last arrival
+__device__ __forceinline__ void item_done_fwd(const SweepArgs& A, int f, int* keep) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(A.deps + f) : "memory");
+  if (old == 1) {
+    __threadfence();
+    push_window(A, f, 0, kWin - 1, keep);
+  }
+}
+
 // Spin waits give up after kSweepStallNs (a dependency that never resolves is
 // a bug): the flag is raised, every CTA drains, the host reports the stall.
 constexpr unsigned long long kSweepStallNs = 4000000000ull;
@@ -570,10 +582,11 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
         red_release(&A.pub[I.front], 1);
         push_window(A, I.front, I.blk + kWin, I.blk + kWin);
       }
-      __threadfence();
       RQB_TRACE(3);
-      const bool last = whole || atomicAdd(&A.fin[I.front], 1) + 1 == I.npb + I.ncbb;
-      if (last && I.parent >= 0) front_ready(A, I.parent, &keep_s);  // depth first: run the parent's first item
+      if (I.parent >= 0)
+        item_done_fwd(A, I.parent, &keep_s);  // depth first: the parent's first item runs here next
+      else
+        __threadfence();
       atomicAdd(A.done, 1);
     }
   }
@@ -1164,7 +1177,8 @@ void rqb_solve_prepare(FactorEngine& fe) {
   int nf0 = 0, nb0 = 0;
   for (int f = 0; f < nfr; ++f) {
     const Front& F = S.fronts[f];
-    dfwd[f] = static_cast<int32_t>(F.children.size());
+    dfwd[f] = 0;  // forward: items of the children still to finish
+    for (int32_t c : F.children) dfwd[f] += fcnt_f[c];
     int a = F.parent;
     while (a >= 0 && S.fronts[a].npiv == 0) a = S.fronts[a].parent;
     dbwd[f] = a >= 0 ? 1 : 0;
