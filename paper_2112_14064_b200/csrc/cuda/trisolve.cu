@@ -56,7 +56,10 @@ struct SweepArgs {
   int fwd;        // 1 forward, 0 backward (item layout of front_ready)
   const int32_t* fbase;  // per front: first item of this sweep
   const int32_t* fcnt;   // per front: items of this sweep
-  const int32_t* npb;    // per front: pivot blocks
+  const int32_t* npb;    // per front: pivot blocks (forward window: 0 for whole fronts)
+  const int32_t* npart;  // backward: per front, contribution-column partial items ahead of its blocks
+  int* pdone;            // backward: per front, partial items finished
+  double* bpart;         // backward: partial sums U[blk rows, chunk] x_chunk (64 per partial item)
   const int32_t* ech;
   const int4* gsrc;      // forward gather sources per front row {b, child0 cb, child1 cb, -}
   const double* pool;
@@ -124,6 +127,12 @@ constexpr int kStage = 1024;  // staged solution entries per round (8 KB)
 constexpr int kWholeNpb = 2;
 constexpr int kWholeCb = kStage - kWholeNpb * kRB;
 constexpr int kWhole = -2;  // SolveItem::blk of a whole-front item
+// Backward items of fronts with more than kCbChunk contribution columns are
+// split: per pivot block, one partial item per kCbChunk columns (U[blk rows,
+// chunk] x_chunk into bpart, no waits) ahead of the block item, which then only
+// streams the later pivot blocks and adds its partials before the triangle.
+constexpr int kCbChunk = 256;
+constexpr int kPart = -3;  // SolveItem::blk of a partial item (cbvec_off/ncbb: column range, ech_off: slot)
 
 __device__ __forceinline__ void push_items(const SweepArgs& A, int i0, int n) {
   if (n <= 0) return;
@@ -143,10 +152,16 @@ __device__ __forceinline__ void push_window(const SweepArgs& A, int f, int v0, i
     const int end = v1 == npb ? base + A.fcnt[f] : base + v1 + 1;
     i0 = base + v0;
     n = end - i0;
-  } else {
+  } else {  // [partial items] then the pivot blocks, last first; the partials enter with the window
+    const int npart = A.npart[f];
     v1 = min(v1, npb - 1);
-    i0 = base + v0;
+    if (v0 > v1) return;
+    i0 = base + npart + v0;
     n = v1 - v0 + 1;
+    if (v0 == 0) {
+      i0 = base;
+      n += npart;
+    }
   }
   if (n <= 0) return;
   if (keep) {
@@ -736,6 +751,23 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
     const double* g = A.pool + I.goff;
     const int64_t ld = I.ld;
     const int32_t* rw = A.rows + I.rows_off;
+    if (I.blk == kPart) {  // contribution-column chunk of one pivot block: partial sums only
+      const int c0 = np + I.cbvec_off, c1 = np + I.ncbb, nr = I.nr;
+      for (int c = tid; c < c1 - c0; c += kST) stg[c] = __ldcg(&A.xnew[rw[c0 + c]]);
+      __syncthreads();
+      double s = 0.0;
+      if (row < nr) s = stream_cols(g + I.r0 + row, ld, stg - c0, c0, c1, grp);
+      part[grp][row] = s;
+      __syncthreads();
+      if (tid < nr) A.bpart[I.ech_off + tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(&A.pdone[I.front], 1);
+        atomicAdd(A.done, 1);
+      }
+      continue;
+    }
     const bool whole = I.blk == kWhole;
     if (whole) {
       bwd_whole(A, I, g, ld, rw, D, stg, pv, part, tid);
@@ -760,7 +792,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
       const int lo = (blk + 1) * kRB;
       double s = 0.0;
       {
-        for (int base = np; base < nf; base += kStage) {
+        for (int base = I.ncbb > 0 ? nf : np; base < nf; base += kStage) {  // chunked fronts: partial items
           const int hi = min(nf, base + kStage);
           for (int c = tid; c < hi - base; c += kST) stg[c] = __ldcg(&A.xnew[rw[base + c]]);
           __syncthreads();
@@ -815,6 +847,18 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
           }
           done_hi = avail_lo;
         }
+      }
+      if (I.ncbb > 0) {  // chunked: the contribution-column partials of this block (fixed order)
+        if (tid == 0) {
+          unsigned long long t0 = 0;
+          while (ld_acquire(&A.pdone[I.front]) < A.npart[I.front]) {
+            __nanosleep(20);
+            if (stalled(A, t0)) break;
+          }
+        }
+        __syncthreads();
+        if (grp == 0 && row < nr)
+          for (int k = 0; k < I.ncbb; ++k) s += __ldcg(&A.bpart[I.cbvec_off + k * kRB + row]);
       }
       part[grp][row] = s;
       if (A.trace && tid == 0) A.trace[8 * (size_t)it + 6] = gtime();
@@ -1159,13 +1203,49 @@ void rqb_solve_prepare(FactorEngine& fe) {
     }
     fcnt_f[f] = static_cast<int32_t>(fwd.size()) - fbase_f[f];
   }
+  std::vector<int32_t> npart_b(nfr, 0), vnpb_b(nfr, 0);
+  int64_t pslots = 0;
+  // contribution-column chunk width of the backward partial items (RQB_CB_CHUNK, 64..kStage)
+  const int cb_chunk = std::getenv("RQB_CB_CHUNK")
+                           ? std::min(kStage, std::max(kRB, std::atoi(std::getenv("RQB_CB_CHUNK"))))
+                           : kCbChunk;
   for (int f = nfr - 1; f >= 0; --f) {
     const Front& F = S.fronts[f];
     fbase_b[f] = static_cast<int32_t>(bwd.size());
+    vnpb_b[f] = whole[f] ? (npb[f] > 0 ? 1 : 0) : npb[f];
+    const int ncb = F.nf - F.npiv;
+    if (!whole[f] && npb[f] > 0 && ncb > cb_chunk) {  // contribution-column partial items
+      const int nck = (ncb + cb_chunk - 1) / cb_chunk;
+      for (int b = npb[f] - 1; b >= 0; --b)
+        for (int k = 0; k < nck; ++k) {
+          SolveItem it = item(f, b * kRB, std::min(F.npiv, (b + 1) * kRB), kPart);
+          it.cbvec_off = k * cb_chunk;
+          it.ncbb = std::min(ncb, (k + 1) * cb_chunk);
+          it.ech_off = static_cast<int32_t>(pslots + (static_cast<int64_t>(b) * nck + k) * kRB);
+          it.nech = 0;
+          it.parent = -1;
+          bwd.push_back(it);
+        }
+      npart_b[f] = npb[f] * nck;
+      for (int b = npb[f] - 1; b >= 0; --b) {
+        SolveItem it = item(f, b * kRB, std::min(F.npiv, (b + 1) * kRB), b);
+        it.ncbb = nck;
+        it.cbvec_off = static_cast<int32_t>(pslots + static_cast<int64_t>(b) * nck * kRB);
+        bwd.push_back(it);
+      }
+      pslots += static_cast<int64_t>(npb[f]) * nck * kRB;
+      if (pslots > INT32_MAX) throw Error(errc::solver, "solve: partial-sum slots exceed int32");
+      fcnt_b[f] = static_cast<int32_t>(bwd.size()) - fbase_b[f];
+      continue;
+    }
     if (whole[f] && npb[f] > 0) {
       bwd.push_back(item(f, 0, F.npiv, kWhole));
     } else {
-      for (int b = npb[f] - 1; b >= 0; --b) bwd.push_back(item(f, b * kRB, std::min(F.npiv, (b + 1) * kRB), b));
+      for (int b = npb[f] - 1; b >= 0; --b) {
+        SolveItem it = item(f, b * kRB, std::min(F.npiv, (b + 1) * kRB), b);
+        it.ncbb = 0;  // contribution columns streamed by the block item itself
+        bwd.push_back(it);
+      }
     }
     fcnt_b[f] = static_cast<int32_t>(bwd.size()) - fbase_b[f];
   }
@@ -1189,7 +1269,7 @@ void rqb_solve_prepare(FactorEngine& fe) {
       for (int i = 0; i < n; ++i) qf[nf0++] = fbase_f[f] + i;
     }
     if (dbwd[f] == 0)
-      for (int i = 0; i < std::min(fcnt_b[f], kWin); ++i) qb[nb0++] = fbase_b[f] + i;
+      for (int i = 0; i < npart_b[f] + std::min(vnpb_b[f], kWin); ++i) qb[nb0++] = fbase_b[f] + i;
   }
   fe.n_fwd_items = static_cast<int>(fwd.size());
   fe.n_bwd_items = static_cast<int>(bwd.size());
@@ -1204,6 +1284,9 @@ void rqb_solve_prepare(FactorEngine& fe) {
   fmeta.insert(fmeta.end(), fbase_b.begin(), fbase_b.end());
   fmeta.insert(fmeta.end(), fcnt_b.begin(), fcnt_b.end());
   fmeta.insert(fmeta.end(), vnpb_f.begin(), vnpb_f.end());
+  fmeta.insert(fmeta.end(), vnpb_b.begin(), vnpb_b.end());
+  fmeta.insert(fmeta.end(), npart_b.begin(), npart_b.end());
+  fe.d_bpart.alloc(sizeof(double) * std::max<int64_t>(1, pslots));
   fe.d_sf.upload(fmeta.data(), sizeof(int32_t) * fmeta.size(), fe.stream);
   fe.d_ech.upload(ech.data(), sizeof(int32_t) * ech.size(), fe.stream);
   fe.d_gsrc.alloc(sizeof(int4) * std::max<size_t>(1, S.rows.size()));
@@ -1219,7 +1302,7 @@ void rqb_solve_prepare(FactorEngine& fe) {
   fe.st_qctl = static_cast<int64_t>(st.size());
   st.insert(st.end(), {0, nf0, 0, nb0, 0, 0});  // {head, tail} fwd, bwd; items done fwd, bwd
   fe.st_cnt = static_cast<int64_t>(st.size());  // fwd published, fwd finished, bwd published
-  st.resize(st.size() + 3 * static_cast<size_t>(nfr), 0);
+  st.resize(st.size() + 4 * static_cast<size_t>(nfr), 0);  // + bwd partial items done
   fe.d_state0.upload(st.data(), sizeof(int32_t) * st.size(), fe.stream);
   fe.d_state.alloc(fe.d_state0.bytes);
   fe.d_rowperm.alloc(sizeof(int32_t) * std::max<int64_t>(1, fe.n));
@@ -1311,7 +1394,10 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
   B.trace = trace ? trace + 8 * (size_t)fe.n_fwd_items : nullptr;
   B.fbase = fe.d_sf.as<int32_t>() + 2 * nfr;
   B.fcnt = B.fbase + nfr;
-  B.npb = B.fcnt;
+  B.npb = fe.d_sf.as<int32_t>() + 5 * nfr;
+  B.npart = fe.d_sf.as<int32_t>() + 6 * nfr;
+  B.pdone = sb + fe.st_cnt + 3 * nfr;
+  B.bpart = fe.d_bpart.as<double>();
   if (fe.n_bwd_items > 0) {
     if (fe.sweep_occ == 3)
       bwd_sweep<3><<<std::min(fe.solve_grid, fe.n_bwd_items), kST, 0, st>>>(B);

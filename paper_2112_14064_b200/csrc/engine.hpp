@@ -109,7 +109,7 @@ struct FactorEngine {
   // inverses of the pivot blocks' 64x64 diagonal tiles (computed after each
   // factorization): per block an nr x nr column-major square, strictly lower =
   // inv(L11) (unit diagonal implied), upper = inv(U11); d_dblk lists the blocks
-  DeviceBuffer d_dinv, d_dblk;
+  DeviceBuffer d_dinv, d_dblk, d_bpart;
   int n_dblk = 0;
   // dataflow state of the two sweeps in one int32 buffer (template + live
   // copy, reset by one D2D copy per solve): front deps fwd/bwd, ready queues

@@ -268,9 +268,10 @@ def test_cfg3_solve_residual_and_cluster(name):
 # --------------------------------------------------------------------------- sweeps
 @pytest.mark.parametrize("name", ["cfg1", "cfg2_riga"])
 def test_solve_whole_front_items_and_determinism(name, monkeypatch):
-    """The triangular sweeps' two item layouts (64-row blocks with in-front
-    waits; whole small fronts per CTA, enabled by default only on levels with
-    >= 2 x grid fronts, i.e. the large configs) give the oracle's solution, and
+    """The triangular sweeps' item layouts (64-row blocks with in-front waits;
+    whole small fronts per CTA, enabled by default only on levels with >= 2 x
+    grid fronts; backward partial items over contribution-column chunks, forced
+    here with 64-column chunks) give the oracle's solution, and
     repeated solves are bitwise identical (per-block partial sums are added in
     block order, independent of publication timing)."""
     P = rq.baseline_config(name)
@@ -280,18 +281,24 @@ def test_solve_whole_front_items_and_determinism(name, monkeypatch):
     b = np.random.default_rng(11).standard_normal((P.n, 2))
     xo = np.stack([of.solve(b[:, i]).real for i in range(2)], 1)
     xs = []
-    for whole_min in (None, "1"):
+    for whole_min, chunk in ((None, None), ("1", None), (None, "64")):
         if whole_min is None:
             monkeypatch.delenv("RQB_WHOLE_MIN", raising=False)
         else:
             monkeypatch.setenv("RQB_WHOLE_MIN", whole_min)
+        if chunk is None:  # backward partial items over contribution-column chunks (default: > 256 columns)
+            monkeypatch.delenv("RQB_CB_CHUNK", raising=False)
+        else:
+            monkeypatch.setenv("RQB_CB_CHUNK", chunk)
         f = rq.lu_factorize((P.rowptr, P.col, Q), o)
         x1, x2 = f.solve(b), f.solve(b)
         assert np.array_equal(x1, x2)
         assert np.max(np.abs(x1 - xo)) <= 1e-9 * np.max(np.abs(xo))
         xs.append(x1)
     monkeypatch.delenv("RQB_WHOLE_MIN", raising=False)
-    assert np.max(np.abs(xs[0] - xs[1])) <= 1e-12 * np.max(np.abs(xs[0]))
+    monkeypatch.delenv("RQB_CB_CHUNK", raising=False)
+    for x in xs[1:]:
+        assert np.max(np.abs(xs[0] - x)) <= 1e-12 * np.max(np.abs(xs[0]))
 
 
 @pytest.mark.parametrize("name,occ", [("cfg1", "1"), ("cfg1", "2"), ("cfg2_riga", "1")])
