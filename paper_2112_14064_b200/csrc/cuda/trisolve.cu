@@ -54,6 +54,7 @@ struct SweepArgs {
   int* pub;       // per front: pivot blocks published (forward: first first; backward: last first)
   int* fin;       // per front: forward items finished
   int fwd;        // 1 forward, 0 backward (item layout of front_ready)
+  int win;        // window of pivot blocks in the queue per front (kWin; RQB_WIN_F / RQB_WIN_B)
   const int32_t* fbase;  // per front: first item of this sweep
   const int32_t* fcnt;   // per front: items of this sweep
   const int32_t* npb;    // per front: pivot blocks (forward window: 0 for whole fronts)
@@ -116,9 +117,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // backward: the v-th block from the end) is pushed when the front becomes
 // ready (v < kWin) or when the front's item v - kWin publishes. An item then
 // waits for at most kWin - 1 blocks instead of holding a CTA through the
-// whole pivot chain. Pushes of one front happen in item order, so every wait
+// whole pivot chain, yet starts early enough to stream the blocks published
+// before it (measured: 32; 8 leaves the chain of the large top fronts waiting
+// on the streaming). Pushes of one front happen in item order, so every wait
 // targets an earlier queue slot (deadlock freedom of the FIFO claim order).
-constexpr int kWin = 8;
+constexpr int kWin = 32;
 constexpr int kStage = 1024;  // staged solution entries per round (8 KB)
 // Fronts with at most kWholeNpb pivot blocks and kWholeCb contribution rows
 // are one item per sweep (a single CTA walks the whole front, its y / x kept
@@ -176,7 +179,7 @@ __device__ __forceinline__ void push_window(const SweepArgs& A, int f, int v0, i
 __device__ __forceinline__ void front_ready(const SweepArgs& A, int f, int* keep = nullptr) {
   if (atomicSub(&A.deps[f], 1) == 1) {
     __threadfence();
-    push_window(A, f, 0, kWin - 1, keep);
+    push_window(A, f, 0, A.win - 1, keep);
   }
 }
 
@@ -188,7 +191,7 @@ __device__ __forceinline__ void item_done_fwd(const SweepArgs& A, int f, int* ke
   asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(A.deps + f) : "memory");
   if (old == 1) {
     __threadfence();
-    push_window(A, f, 0, kWin - 1, keep);
+    push_window(A, f, 0, A.win - 1, keep);
   }
 }
 
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
     if (tid == 0) {
       if (I.blk >= 0) {
         red_release(&A.pub[I.front], 1);
-        push_window(A, I.front, I.blk + kWin, I.blk + kWin);
+        push_window(A, I.front, I.blk + A.win, I.blk + A.win);
       }
       RQB_TRACE(3);
       if (I.parent >= 0)
@@ -891,7 +894,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
     if (tid == 0) {
       if (!whole) {
         red_release(&A.pub[I.front], 1);
-        const int v = I.npb - 1 - I.blk + kWin;
+        const int v = I.npb - 1 - I.blk + A.win;
         push_window(A, I.front, v, v);
       }
       RQB_TRACE(3);
@@ -1103,6 +1106,8 @@ void rqb_solve_prepare(FactorEngine& fe) {
   std::vector<std::vector<int32_t>> echl(nfr);
   std::vector<int32_t> npb(nfr), ncbb(nfr);
   int64_t cbtot = 0;
+  fe.win_f = std::getenv("RQB_WIN_F") ? std::max(1, std::atoi(std::getenv("RQB_WIN_F"))) : kWin;
+  fe.win_b = std::getenv("RQB_WIN_B") ? std::max(1, std::atoi(std::getenv("RQB_WIN_B"))) : kWin;
   for (int f = 0; f < nfr; ++f) {
     const Front& F = S.fronts[f];
     npb[f] = (F.npiv + kRB - 1) / kRB;
@@ -1264,12 +1269,12 @@ void rqb_solve_prepare(FactorEngine& fe) {
     dbwd[f] = a >= 0 ? 1 : 0;
   }
   for (int f = 0; f < nfr; ++f) {
-    if (dfwd[f] == 0) {  // window: pivot blocks [0, kWin) (+ contribution items if npb < kWin)
-      const int n = vnpb_f[f] < kWin ? fcnt_f[f] : kWin;
+    if (dfwd[f] == 0) {  // window: pivot blocks [0, win) (+ contribution items if npb < win)
+      const int n = vnpb_f[f] < fe.win_f ? fcnt_f[f] : fe.win_f;
       for (int i = 0; i < n; ++i) qf[nf0++] = fbase_f[f] + i;
     }
     if (dbwd[f] == 0)
-      for (int i = 0; i < npart_b[f] + std::min(vnpb_b[f], kWin); ++i) qb[nb0++] = fbase_b[f] + i;
+      for (int i = 0; i < npart_b[f] + std::min(vnpb_b[f], fe.win_b); ++i) qb[nb0++] = fbase_b[f] + i;
   }
   fe.n_fwd_items = static_cast<int>(fwd.size());
   fe.n_bwd_items = static_cast<int>(bwd.size());
@@ -1372,6 +1377,7 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
   F.pub = sb + fe.st_cnt;
   F.fin = sb + fe.st_cnt + nfr;
   F.fwd = 1;
+  F.win = fe.win_f;
   F.fbase = fe.d_sf.as<int32_t>();
   F.fcnt = F.fbase + nfr;
   F.npb = fe.d_sf.as<int32_t>() + 4 * nfr;
@@ -1391,6 +1397,7 @@ void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scal
   B.pub = sb + fe.st_cnt + 2 * nfr;
   B.fin = nullptr;
   B.fwd = 0;
+  B.win = fe.win_b;
   B.trace = trace ? trace + 8 * (size_t)fe.n_fwd_items : nullptr;
   B.fbase = fe.d_sf.as<int32_t>() + 2 * nfr;
   B.fcnt = B.fbase + nfr;

@@ -116,7 +116,7 @@ struct FactorEngine {
   // fwd/bwd, {head, tail} x2, per-front published/finished counters
   DeviceBuffer d_state0, d_state, d_sweep_stall;
   int64_t st_dep_fwd = 0, st_dep_bwd = 0, st_q_fwd = 0, st_q_bwd = 0, st_qctl = 0, st_cnt = 0;
-  int n_fwd_items = 0, n_bwd_items = 0, solve_grid = 148, sweep_occ = 2;
+  int n_fwd_items = 0, n_bwd_items = 0, solve_grid = 148, sweep_occ = 2, win_f = 8, win_b = 8;
   std::vector<FrontDev> fronts_h;
   std::vector<LevelPlan> plans;
   int64_t nscratch = 0;

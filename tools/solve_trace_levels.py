@@ -12,7 +12,9 @@ whole = (npb <= kWholeNpb) & (nf - npiv <= kWholeCb)
 if len(sys.argv) > 3: whole &= lvl_count[level] >= int(sys.argv[3])
 fcnt = np.where(whole, 1, npb + ncbb)
 ffront = np.repeat(np.arange(nfr), fcnt)
-bcnt = np.where(whole & (npb > 0), 1, npb)
+ncb = nf - npiv
+nck = np.where((~whole) & (npb > 0) & (ncb > 256), (ncb + 255) // 256, 0)
+bcnt = np.where(whole & (npb > 0), 1, npb + npb * nck)  # backward partial items (RQB_CB_CHUNK default 256)
 bfront = np.repeat(np.arange(nfr)[::-1], bcnt[::-1])
 for name, T, fr in (("fwd", t[:nf_], ffront), ("bwd", t[nf_:], bfront)):
     T = T.copy(); T[:, :4] -= T[:, 0].min()
