@@ -172,6 +172,13 @@ int rq_factor_profile(rq_factor_t* f, double* ms, int64_t* launches, double* wor
  * grid size, out[19] tasks, out[20] ready-queue wait ms summed over CTAs.
  * double[24]. */
 int rq_factor_dag_profile(rq_factor_t* f, double* out);
+/* Evidence entry (development): the contribution-block Schur update of ONE
+ * front (front < 0: the largest), i.e. the factorization's own UPDCB task code
+ * (C -= L21 U12 with K = npiv on FP64 tensor cores) as a plain grid, timed over
+ * `reps` launches. Overwrites that front's contribution block: refactor after.
+ * out[0] ms per launch, out[1] flops per launch, out[2] front, out[3] tiles,
+ * out[4] K, out[5] grid. double[6]. */
+int rq_factor_bench_updcb(rq_factor_t* f, int front, int reps, double* out);
 void rq_factor_destroy(rq_factor_t* f);
 
 /* ------------------------------------------------------------------------ */

@@ -126,6 +126,7 @@ _sig("rq_factor_solve", C.c_int, vp, f64p, f64p, C.c_int)
 _sig("rq_factor_front_export", C.c_int, vp, C.c_int64, vp, vp, C.POINTER(C.c_int64))
 _sig("rq_factor_profile", C.c_int, vp, f64p, i64p, f64p)
 _sig("rq_factor_dag_profile", C.c_int, vp, f64p)
+_sig("rq_factor_bench_updcb", C.c_int, vp, C.c_int, C.c_int, f64p)
 _sig("rq_factor_destroy", None, vp)
 _sig("rq_mm_write", C.c_int, C.c_int64, i64p, i32p, f64p, f64n, C.c_char_p)
 _sig("rq_mm_write_vector", C.c_int, C.c_int64, f64p, f64n, C.c_char_p)
@@ -156,7 +157,7 @@ EXPORTS = [
     "rq_pencil_supports", "rq_pencil_destroy", "rq_space_dims", "rq_space_boundary_mask",
     "rq_nd_order", "rq_symbolic_stats_get", "rq_symbolic_perm", "rq_symbolic_fronts",
     "rq_symbolic_front_rows", "rq_symbolic_destroy", "rq_factor_create", "rq_factor_refactor",
-    "rq_factor_get_info", "rq_factor_solve", "rq_factor_front_export", "rq_factor_profile", "rq_factor_dag_profile",
+    "rq_factor_get_info", "rq_factor_solve", "rq_factor_front_export", "rq_factor_profile", "rq_factor_dag_profile", "rq_factor_bench_updcb",
     "rq_factor_destroy",
     "rq_operator_create", "rq_operator_create_pencil", "rq_mm_write", "rq_mm_write_vector", "rq_mm_read",
     "rq_mm_dims", "rq_mm_csr", "rq_mm_destroy", "rq_pencil_write_mm", "rq_eigenpairs_json", "rq_operator_varsigma", "rq_operator_apply", "rq_operator_b_inner",

@@ -1146,6 +1146,7 @@ struct DagPlan {
       d_small_backup, d_deps0, d_deps, d_queue0, d_queue, d_qctl, d_qctl0, d_sb, d_trace;
   int ntasks = 0, nqueued = 0, nfronts = 0, ntile = 0, nflag = 0, grid = 148, nready = 0;
   int occ = 1, small_nf = 160;  // kernel variant (see kSmallNfLatency / kSmallNfThroughput)
+  std::vector<FrontDag> dag_h;   // host copy of the per-front plan (tile counts, acb)
   size_t smem = 0;
   double flops_upd = 0;
 };
@@ -1325,7 +1326,69 @@ void rqb_dag_build(FactorEngine& fe) {
   P->grid = std::max(1, std::min(P->ntasks, nsm * std::max(1, occ)));
   P->d_small_backup.alloc(sizeof(double) * P->grid * P->small_nf * kPB);
   fe.dag_ntasks = P->ntasks;
+  P->dag_h = dag;
   fe.dag.reset(P.release());
+}
+
+// Evidence entry for the large-front Schur update: every UPDCB tile of ONE
+// front (contribution block -= L21 U12, K = npiv, the DAG kernel's own
+// updcb_task code) as a plain grid, so ncu's DMMA-pipe counters see the Schur
+// update alone. Overwrites that front's contribution block (development use:
+// refactor afterwards).
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kDT, kMinBlocks) updcb_bench_kernel(double* pool, const FrontDev* fronts, int f,
+                                                                     int acb, int tiles) {
+  extern __shared__ double sm[];
+  DagArgs A{};
+  A.pool = pool;
+  const FrontDev F = fronts[f];
+  const int n = tiles - acb;
+  for (int t = blockIdx.x; t < n * n; t += gridDim.x) {
+    updcb_task(A, F, acb + t % n, acb + t / n, sm);
+    __syncthreads();
+  }
+}
+
+void rqb_dag_bench_updcb(FactorEngine& fe, int front, int reps, double* out) {
+  if (!fe.dag) fail(errc::config, "the task-DAG factorization is not active");
+  DagPlan& P = *fe.dag;
+  const Symbolic& S = fe.sym;
+  if (front < 0) {  // the front with the most contribution-block update flops
+    double best = -1.0;
+    for (int f = 0; f < static_cast<int>(S.fronts.size()); ++f) {
+      const FrontDag& D = P.dag_h[f];
+      if (D.acb >= D.tiles) continue;
+      const double m = static_cast<double>(S.fronts[f].nf - D.acb * kTile);
+      const double w = 2.0 * S.fronts[f].npiv * m * m;
+      if (w > best) best = w, front = f;
+    }
+  }
+  if (front < 0 || front >= static_cast<int>(S.fronts.size()) || P.dag_h[front].acb >= P.dag_h[front].tiles)
+    fail(errc::config, "bench_updcb: the front has no contribution-block tiles");
+  const FrontDag& D = P.dag_h[front];
+  const int n = D.tiles - D.acb;
+  auto kern = updcb_bench_kernel<2>;
+  RQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.smem)));
+  int nsm = 148, occ = 1;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
+  RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDT, P.smem));
+  const int grid = std::max(1, std::min(n * n, nsm * std::max(1, occ)));
+  kern<<<grid, kDT, P.smem, fe.stream>>>(fe.d_pool.as<double>(), fe.d_fronts.as<FrontDev>(), front, D.acb, D.tiles);
+  RQB_CUDA(cudaGetLastError());
+  RQB_CUDA(cudaEventRecord(fe.ev0, fe.stream));
+  for (int r = 0; r < reps; ++r)
+    kern<<<grid, kDT, P.smem, fe.stream>>>(fe.d_pool.as<double>(), fe.d_fronts.as<FrontDev>(), front, D.acb, D.tiles);
+  RQB_CUDA(cudaEventRecord(fe.ev1, fe.stream));
+  RQB_CUDA(cudaEventSynchronize(fe.ev1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, fe.ev0, fe.ev1);
+  const double m = static_cast<double>(S.fronts[front].nf - D.acb * kTile);
+  out[0] = ms / std::max(1, reps);
+  out[1] = 2.0 * S.fronts[front].npiv * m * m;
+  out[2] = front;
+  out[3] = static_cast<double>(n) * n;
+  out[4] = S.fronts[front].npiv;
+  out[5] = grid;
 }
 
 void rqb_dag_enqueue(FactorEngine& fe) {

@@ -157,6 +157,7 @@ void rqb_solve_prepare(FactorEngine& fe);
 void rqb_dag_build(FactorEngine& fe);
 void rqb_dag_enqueue(FactorEngine& fe);
 void rqb_dag_profile(FactorEngine& fe, double* out);
+void rqb_dag_bench_updcb(FactorEngine& fe, int front, int reps, double* out);
 void rqb_rowperm_enqueue(FactorEngine& fe);
 std::string rqb_dag_stall_report(FactorEngine& fe);
 

@@ -341,6 +341,14 @@ int rq_factor_dag_profile(rq_factor_t* f, double* out) {
   });
 }
 
+int rq_factor_bench_updcb(rq_factor_t* f, int front, int reps, double* out) {
+  return guarded([&] {
+    need(f, "factor");
+    need(out, "out");
+    rqb::rqb_dag_bench_updcb(*f->fe, front, reps, out);
+  });
+}
+
 void rq_factor_destroy(rq_factor_t* f) { delete f; }
 
 namespace {
