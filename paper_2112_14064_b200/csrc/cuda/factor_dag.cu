@@ -733,6 +733,13 @@ __device__ __forceinline__ void cp_async8z(double* smem, const double* gmem, boo
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
 }
 
+// 16-byte cp.async of two consecutive doubles, `n` of them valid (zero fill)
+__device__ __forceinline__ void cp_async16z(double* smem, const double* gmem, int n) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(8 * n) : "memory");
+}
+constexpr int kBLD = kNB + 4;  // UPDCB: B stage stored [n][kk] (conflict-free fragment reads)
+
 // Contribution-block tile (a, b): C -= L(rows a, 0:npiv) U(0:npiv, cols b) in
 // one pass, K in chunks of 32 staged by cp.async (two buffers: the next chunk
 // is in flight while DMMA consumes the current one), C read once and written
@@ -749,24 +756,26 @@ __device__ void updcb_task(const DagArgs& A, const FrontDev& F, int a, int b, do
   const int lane = tid & 31, warp = tid >> 5;  // 8 warps: 2 (m) x 4 (n) of 32 x 16
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
   const int gid = lane >> 2, tig = lane & 3;
-  constexpr int kStage = 2 * kNB * kTSP;  // As [kk][m] then Bs [kk][n]
+  // stage: As [kk][m] (stride kTSP) then Bs [n][kk] (stride kBLD); both filled
+  // with 16-byte copies (pairs along m of an L column, along kk of a U column)
+  constexpr int kStage = kNB * kTSP + kTile * kBLD;
   auto issue = [&](int chunk, int buf) {
     double* As = sm + buf * kStage;
     double* Bs = As + kNB * kTSP;
     const int k0 = chunk * kNB;
 #pragma unroll
-    for (int i = 0; i < kNB * kTile / kDT; ++i) {
+    for (int i = 0; i < kNB * kTile / 2 / kDT; ++i) {
       const int idx = tid + i * kDT;
-      const int kk = idx / kTile, m = idx % kTile;
-      const bool ok = k0 + kk < K && m < nr;
-      cp_async8z(&As[kk * kTSP + m], ok ? &g[(r0 + m) + (int64_t)(k0 + kk) * ld] : g, ok);
+      const int kk = idx / (kTile / 2), m = 2 * (idx % (kTile / 2));
+      const int n = (k0 + kk < K) ? max(0, min(2, nr - m)) : 0;
+      cp_async16z(&As[kk * kTSP + m], n ? &g[(r0 + m) + (int64_t)(k0 + kk) * ld] : g, n);
     }
 #pragma unroll
-    for (int i = 0; i < kNB * kTile / kDT; ++i) {
+    for (int i = 0; i < kNB * kTile / 2 / kDT; ++i) {
       const int idx = tid + i * kDT;
-      const int kk = idx % kNB, n = idx / kNB;
-      const bool ok = k0 + kk < K && n < nc;
-      cp_async8z(&Bs[kk * kTSP + n], ok ? &g[(k0 + kk) + (int64_t)(c0 + n) * ld] : g, ok);
+      const int kk = 2 * (idx % (kNB / 2)), c = idx / (kNB / 2);
+      const int n = c < nc ? max(0, min(2, K - k0 - kk)) : 0;
+      cp_async16z(&Bs[c * kBLD + kk], n ? &g[(k0 + kk) + (int64_t)(c0 + c) * ld] : g, n);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -809,7 +818,7 @@ __device__ void updcb_task(const DagArgs& A, const FrontDev& F, int a, int b, do
         af[x][1] = As[kr * kTSP + wm + x * 16 + gid + 8];
       }
 #pragma unroll
-      for (int y = 0; y < 2; ++y) bf[y] = Bs[kr * kTSP + wn + y * 8 + gid];
+      for (int y = 0; y < 2; ++y) bf[y] = Bs[(wn + y * 8 + gid) * kBLD + kr];
 #pragma unroll
       for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -1314,7 +1323,7 @@ void rqb_dag_build(FactorEngine& fe) {
   fe.d_scratch.alloc(sizeof(double) * std::max(1, slot) * 2 * kNB * kNB);
   const size_t small_smem = max_small_bytes;
   P->small_nf = std::max(1, max_small);
-  const size_t tile_smem = sizeof(double) * 4 * kNB * kTSP;  // UPDCB: two stages
+  const size_t tile_smem = sizeof(double) * std::max(4 * kNB * kTSP, 2 * (kNB * kTSP + kTile * kBLD));  // UPD / UPDCB: two stages
   const size_t rows_smem = sizeof(double) * ((kTile + 1) * kNB + kNB * kNB + 64);
   const size_t diag_smem = sizeof(double) * (3 * 32 * 33 + 128);
   P->smem = std::max({small_smem, tile_smem, rows_smem, diag_smem, size_t(16 * 1024)});
