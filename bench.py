@@ -321,6 +321,22 @@ def run_b200(args):
             "l2": "scrubbed (256 MiB) before every timed call",
         }
         del opL
+        # the large-front Schur update alone (north-star FP64 tensor target):
+        # the factorization's own UPDCB code over every contribution-block tile
+        # of the largest front, on a throwaway factorization (it overwrites
+        # that front's contribution block)
+        try:
+            fL = rq.lu_factorize((PL.rowptr, PL.col, PL.q_values(SIGMA)), oL)
+            ub = np.zeros(6)
+            _lib.check(_lib.lib.rq_factor_bench_updcb(fL._h, -1, 5, ub))
+            tf = ub[1] / (ub[0] * 1e9)
+            large["schur_update_top_front"] = {
+                "kernel": "updcb (factor_dag UPDCB task code, plain grid)", "front": int(ub[2]), "K": int(ub[4]),
+                "tiles": int(ub[3]), "ms": round(ub[0], 4), "tflops": round(tf, 2),
+                "frac_fp64": round(tf / FP64_PEAK_TFLOPS, 4)}
+            del fL
+        except Exception as e:  # noqa: BLE001
+            large["schur_update_top_front"] = {"error": str(e)[:200]}
 
     # ---- CPU baseline (rank 0, N = 1 only): bounded oracle factorization sample
     cpu = None
