@@ -121,6 +121,7 @@ struct DagArgs {
   int* queue;                // ready queue (task ids, -1 = not yet pushed)
   int* qctl;                 // {head, tail}
   const int32_t* step_base;  // FrontDag::sb_off: first task of every panel step
+  int upd_cp16;              // UPD operands by 16-byte cp.async (RQB_UPD_CP16=0: 8-byte copies)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -648,6 +649,19 @@ __device__ void cols_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   }
 }
 
+__device__ __forceinline__ void cp_async8z(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 8 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
+
+// 16-byte cp.async of two consecutive doubles, `n` of them valid (zero fill)
+__device__ __forceinline__ void cp_async16z(double* smem, const double* gmem, int n) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(8 * n) : "memory");
+}
+constexpr int kBLD = kNB + 4;  // UPD / UPDCB: B stage stored [n][kk] (conflict-free fragment reads)
+
 __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int b, double* sm) {
   const int k = s * kNB, w = min(kNB, F.npiv - k);
   const int r0 = max(a * kTile, k + w), r1 = min(a * kTile + kTile, F.nf);
@@ -655,28 +669,41 @@ __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int 
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
   double* As = sm;              // [kk][m]
-  double* Bs = sm + kNB * kTSP; // [kk][n]
+  double* Bs = sm + kNB * kTSP; // [n][kk], stride kBLD
   const int tid = threadIdx.x;
   const int nr = r1 - r0, nc = c1 - c0;
   const int lane = tid & 31, warp = tid >> 5;  // 8 warps: 2 (m) x 4 (n) of 32 x 16
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
   const int gid = lane >> 2, tig = lane & 3;
-  // issue every global load of the task up front (A, B panels and this
-  // thread's C fragment) so their latencies overlap
-  constexpr int kLd = kNB * kTile / kDT;  // 8 per operand
-  double va[kLd], vb[kLd], cv[2][2][4];
+  // every global load of the task in flight at once: the A and B panels by
+  // 16-byte cp.async straight into shared memory (B stored [n][kk]), this
+  // thread's C fragment into registers
+  double cv[2][2][4];
+  if ((r0 & 1) == 0 && A.upd_cp16) {  // 16-byte source alignment (r0 = k + w can be odd after the last panel)
 #pragma unroll
-  for (int i = 0; i < kLd; ++i) {
-    const int idx = tid + i * kDT;
-    const int kk = idx / kTile, m = idx % kTile;
-    va[i] = (kk < w && m < nr) ? __ldcg(&g[(r0 + m) + (int64_t)(k + kk) * ld]) : 0.0;
+    for (int i = 0; i < kNB * kTile / 2 / kDT; ++i) {
+      const int idx = tid + i * kDT;
+      const int kk = idx / (kTile / 2), m = 2 * (idx % (kTile / 2));
+      const int n = kk < w ? max(0, min(2, nr - m)) : 0;
+      cp_async16z(&As[kk * kTSP + m], n ? &g[(r0 + m) + (int64_t)(k + kk) * ld] : g, n);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kNB * kTile / kDT; ++i) {
+      const int idx = tid + i * kDT;
+      const int kk = idx / kTile, m = idx % kTile;
+      const bool ok = kk < w && m < nr;
+      cp_async8z(&As[kk * kTSP + m], ok ? &g[(r0 + m) + (int64_t)(k + kk) * ld] : g, ok);
+    }
   }
 #pragma unroll
-  for (int i = 0; i < kLd; ++i) {
+  for (int i = 0; i < kNB * kTile / 2 / kDT; ++i) {
     const int idx = tid + i * kDT;
-    const int kk = idx % kNB, n = idx / kNB;
-    vb[i] = (kk < w && n < nc) ? __ldcg(&g[(k + kk) + (int64_t)(c0 + n) * ld]) : 0.0;
+    const int kk = 2 * (idx % (kNB / 2)), c = idx / (kNB / 2);
+    const int n = c < nc ? max(0, min(2, w - kk)) : 0;
+    cp_async16z(&Bs[c * kBLD + kk], n ? &g[(k + kk) + (int64_t)(c0 + c) * ld] : g, n);
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
 #pragma unroll
   for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -686,12 +713,7 @@ __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int 
         const int r = wm + x * 16 + gid + (e >> 1) * 8, c = wn + y * 8 + 2 * tig + (e & 1);
         cv[x][y][e] = (r < nr && c < nc) ? __ldcg(&g[(r0 + r) + (int64_t)(c0 + c) * ld]) : 0.0;
       }
-#pragma unroll
-  for (int i = 0; i < kLd; ++i) {
-    const int idx = tid + i * kDT;
-    As[(idx / kTile) * kTSP + idx % kTile] = va[i];
-    Bs[(idx % kNB) * kTSP + idx / kNB] = vb[i];
-  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   double acc[2][2][4];
 #pragma unroll
@@ -710,7 +732,7 @@ __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int 
       af[x][1] = As[kr * kTSP + wm + x * 16 + gid + 8];
     }
 #pragma unroll
-    for (int y = 0; y < 2; ++y) bf[y] = Bs[kr * kTSP + wn + y * 8 + gid];
+    for (int y = 0; y < 2; ++y) bf[y] = Bs[(wn + y * 8 + gid) * kBLD + kr];
 #pragma unroll
     for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -727,18 +749,7 @@ __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int 
       }
 }
 
-__device__ __forceinline__ void cp_async8z(double* smem, const double* gmem, bool valid) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int n = valid ? 8 : 0;  // src-size 0: zero fill
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
-}
 
-// 16-byte cp.async of two consecutive doubles, `n` of them valid (zero fill)
-__device__ __forceinline__ void cp_async16z(double* smem, const double* gmem, int n) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(8 * n) : "memory");
-}
-constexpr int kBLD = kNB + 4;  // UPDCB: B stage stored [n][kk] (conflict-free fragment reads)
 
 // Contribution-block tile (a, b): C -= L(rows a, 0:npiv) U(0:npiv, cols b) in
 // one pass, K in chunks of 32 staged by cp.async (two buffers: the next chunk
@@ -1409,6 +1420,7 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   RQB_CUDA(cudaMemcpyAsync(P.d_queue.p, P.d_queue0.p, P.d_queue0.bytes, cudaMemcpyDeviceToDevice, fe.stream));
   RQB_CUDA(cudaMemcpyAsync(P.d_qctl.p, P.d_qctl0.p, P.d_qctl0.bytes, cudaMemcpyDeviceToDevice, fe.stream));
   DagArgs A;
+  A.upd_cp16 = std::getenv("RQB_UPD_CP16") ? std::atoi(std::getenv("RQB_UPD_CP16")) : 1;
   A.fronts = fe.d_fronts.as<FrontDev>();
   A.dag = P.d_dag.as<FrontDag>();
   A.tasks = P.d_tasks.as<Task>();
