@@ -77,8 +77,8 @@ __global__ void spmv_op_k(int64_t n, const int64_t* __restrict__ rowptr,
 // part[b * k + i] = sum over block b's slice of V[i] . w  (w given as two halves)
 // part[b*k + i] = V[i][chunk b] . w[chunk b]: the block stages its chunk of
 // w in shared memory once; each warp then owns basis vectors i = warp (mod 8),
-// two at a time, streaming their contiguous chunk segments (8 independent
-// loads in flight per lane and row) and reducing with shuffles only.
+// four at a time, streaming their contiguous chunk segments (16 independent
+// loads in flight per lane) and reducing with shuffles only.
 __global__ void __launch_bounds__(kRedThreads) gemv_t_part(const double* __restrict__ V, int k,
                                                          int64_t n2, const double* __restrict__ wu,
                                                          const double* __restrict__ wl, int64_t n,
@@ -92,32 +92,35 @@ __global__ void __launch_bounds__(kRedThreads) gemv_t_part(const double* __restr
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kW = kRedThreads / 32;
-  for (int i = warp; i < k; i += 2 * kW) {
-    const bool two = i + kW < k;
-    const double* va = V + (int64_t)i * n2 + e0;
-    const double* vb = V + (int64_t)(two ? i + kW : i) * n2 + e0;
-    double sa0 = 0.0, sa1 = 0.0, sb0 = 0.0, sb1 = 0.0;
+  constexpr int kW = kRedThreads / 32, kV = 4;  // basis vectors per warp pass
+  for (int i = warp; i < k; i += kV * kW) {
+    const double* vp[kV];
+#pragma unroll
+    for (int q = 0; q < kV; ++q) vp[q] = V + (int64_t)(i + q * kW < k ? i + q * kW : i) * n2 + e0;
+    double s0[kV], s1[kV];
+#pragma unroll
+    for (int q = 0; q < kV; ++q) s0[q] = s1[q] = 0.0;
     int t = lane;
-    for (; t + 32 * 3 < len; t += 32 * 4) {
-      double a[4], bb[4];
+    for (; t + 32 * 3 < len; t += 32 * 4) {  // 16 loads in flight per lane
+      double a[kV][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = va[t + 32 * u];
+      for (int q = 0; q < kV; ++q)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) bb[u] = vb[t + 32 * u];
-      sa0 += a[0] * xs[t] + a[2] * xs[t + 64];
-      sa1 += a[1] * xs[t + 32] + a[3] * xs[t + 96];
-      sb0 += bb[0] * xs[t] + bb[2] * xs[t + 64];
-      sb1 += bb[1] * xs[t + 32] + bb[3] * xs[t + 96];
+        for (int u = 0; u < 4; ++u) a[q][u] = vp[q][t + 32 * u];
+      const double x0 = xs[t], x1 = xs[t + 32], x2 = xs[t + 64], x3 = xs[t + 96];
+#pragma unroll
+      for (int q = 0; q < kV; ++q) {
+        s0[q] += a[q][0] * x0 + a[q][2] * x2;
+        s1[q] += a[q][1] * x1 + a[q][3] * x3;
+      }
     }
-    for (; t < len; t += 32) {
-      sa0 += va[t] * xs[t];
-      sb0 += vb[t] * xs[t];
-    }
-    const double sa = warp_sum(sa0 + sa1), sb = warp_sum(sb0 + sb1);
-    if (lane == 0) {
-      part[(int64_t)blockIdx.x * k + i] = sa;
-      if (two) part[(int64_t)blockIdx.x * k + i + kW] = sb;
+    for (; t < len; t += 32)
+#pragma unroll
+      for (int q = 0; q < kV; ++q) s0[q] += vp[q][t] * xs[t];
+#pragma unroll
+    for (int q = 0; q < kV; ++q) {
+      const double sq = warp_sum(s0[q] + s1[q]);
+      if (lane == 0 && i + q * kW < k) part[(int64_t)blockIdx.x * k + i + q * kW] = sq;
     }
   }
 }
