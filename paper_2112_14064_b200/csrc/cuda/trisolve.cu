@@ -1176,6 +1176,7 @@ void rqb_solve_prepare(FactorEngine& fe) {
     int items = 0;
     for (int f = 0; f < nfr; ++f) items += npb[f] + ncbb[f];
     fe.sweep_occ = items >= 10000 ? 3 : 2;
+    if (const char* e = std::getenv("RQB_SWEEP_OCC")) fe.sweep_occ = std::atoi(e) >= 3 ? 3 : 2;
     int nsm = 148, occ = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
     if (fe.sweep_occ == 3)
