@@ -338,3 +338,27 @@ def test_pivoting_in_every_front_vs_oracle(name, occ, monkeypatch):
     x = f.solve(b)
     xo = of.solve(b).real
     assert np.max(np.abs(x - xo)) <= 1e-8 * np.max(np.abs(xo))
+
+
+# --------------------------------------------------------------------------- evidence entry
+def test_schur_update_bench_entry():
+    """rq_factor_bench_updcb (the factorization's own contribution-block Schur
+    update over one front, timed alone) runs on a large-front problem, reports
+    the front's update work, and a refactorization afterwards restores a
+    factorization that solves to the oracle's accuracy."""
+    from paper_2112_14064_b200 import _lib
+    P = rq.baseline_config("cfg3_riga")
+    o = rq.nested_dissection_order(P)
+    Q = P.q_values(SIGMA)
+    f = rq.lu_factorize((P.rowptr, P.col, Q), o)
+    out = np.zeros(6)
+    _lib.check(_lib.lib.rq_factor_bench_updcb(f._h, -1, 2, out))
+    front, K = int(out[2]), int(out[4])
+    assert out[0] > 0 and out[3] >= 1 and K == o.npiv[front]
+    m = o.nf[front] - (o.npiv[front] + 63) // 64 * 64  # rows/columns of the contribution-block tiles
+    assert out[1] == pytest.approx(2.0 * K * m * m)
+    f.refactor(Q)
+    b = np.random.default_rng(5).standard_normal(P.n)
+    x = f.solve(b)
+    r = P.to_scipy("K") @ x - 0.5 * (P.to_scipy("C") @ x) + 0.25 * (P.to_scipy("M") @ x) - b
+    assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(b)
