@@ -179,6 +179,9 @@ struct OperatorEngine {
   std::unique_ptr<FactorEngine> fac;
   DeviceBuffer d_rowptr, d_col, d_K, d_C, d_M, d_Q;
   DeviceBuffer d_w, d_t, d_part, d_scal;  // workspaces
+  // Krylov-Schur workspace kept across solve_quadratic calls (eigs.cpp
+  // EigWorkspace: basis buffers + the cycle graphs captured over them)
+  std::shared_ptr<void> eig_ws;
   DeviceBuffer d_rcand, d_rpart;          // batched residual candidates / partials
   cudaStream_t stream = nullptr;
   int64_t launches = 0;

@@ -69,6 +69,52 @@ std::string Ledger::to_json() const {
   return os.str();
 }
 
+// pinned: the cycle's H / beta copies are truly asynchronous, so the host
+// can start on them while the GPU already applies the operator to the
+// continuation vector of the next cycle
+struct Pinned {
+  double* p = nullptr;
+  explicit Pinned(size_t n) {
+    cuda_check(cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(double) * std::max<size_t>(n, 1)), "pinned");
+  }
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+  ~Pinned() { cudaFreeHost(p); }
+  double& operator[](size_t i) { return p[i]; }
+  double* data() { return p; }
+};
+
+// Krylov-Schur workspace kept by the operator across solve_quadratic calls
+// (OperatorEngine::eig_ws): the basis buffers and the cycle graphs captured
+// over them stay valid as long as m does; no allocation, free or graph build
+// in a repeated solve.
+struct EigWorkspace {
+  int m = -1;
+  int64_t n2 = 0;
+  DeviceBuffer dV, dV2, dBV, dBV2, dR, dW, dHa, dHb, dBeta, dQ, dX, dRes;
+  Pinned ha, hb, betas;
+  std::map<std::pair<int, const double*>, cudaGraphExec_t> graphs;
+  EigWorkspace(int m_, int64_t n2_)
+      : m(m_), n2(n2_), ha(static_cast<size_t>(m_ + 1) * (m_ + 1)), hb(static_cast<size_t>(m_ + 1) * (m_ + 1)),
+        betas(m_ + 1) {
+    dV.alloc(sizeof(double) * (m + 1) * n2);
+    dV2.alloc(sizeof(double) * (m + 1) * n2);
+    dBV.alloc(sizeof(double) * (m + 1) * n2);
+    dBV2.alloc(sizeof(double) * (m + 1) * n2);
+    dR.alloc(sizeof(double) * n2);
+    dW.alloc(sizeof(double) * n2);
+    dHa.alloc(sizeof(double) * (m + 1) * (m + 1));
+    dHb.alloc(sizeof(double) * (m + 1) * (m + 1));
+    dBeta.alloc(sizeof(double) * (m + 1));
+    dQ.alloc(sizeof(double) * (m + 1) * (2 * m + 2));
+    dX.alloc(sizeof(double) * n2 * 2 * (m + 1));
+    dRes.alloc(sizeof(double) * 4 * (m + 1));
+  }
+  ~EigWorkspace() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+  }
+};
+
 EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledger& L,
                                   const double norms1[3]) {
   using clock = std::chrono::steady_clock;
@@ -105,19 +151,16 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   // V: Krylov basis; BV = B V kept alongside, so every B-inner product of CGS2
   // is a plain projection h = (BV)^T r (B = diag(I, M) symmetric) and each
   // step needs one M-product (for the new vector) instead of three
-  DeviceBuffer dV, dV2, dBV, dBV2, dR, dW, dHa, dHb, dBeta, dQ, dX, dRes;
-  dV.alloc(sizeof(double) * (m + 1) * n2);
-  dV2.alloc(sizeof(double) * (m + 1) * n2);
-  dBV.alloc(sizeof(double) * (m + 1) * n2);
-  dBV2.alloc(sizeof(double) * (m + 1) * n2);
-  dR.alloc(sizeof(double) * n2);
-  dW.alloc(sizeof(double) * n2);
-  dHa.alloc(sizeof(double) * (m + 1) * (m + 1));
-  dHb.alloc(sizeof(double) * (m + 1) * (m + 1));
-  dBeta.alloc(sizeof(double) * (m + 1));
-  dQ.alloc(sizeof(double) * (m + 1) * (2 * m + 2));
-  dX.alloc(sizeof(double) * n2 * 2 * (m + 1));
-  dRes.alloc(sizeof(double) * 4 * (m + 1));
+  EigWorkspace* wsp = static_cast<EigWorkspace*>(op.eig_ws.get());
+  if (!wsp || wsp->m != m || wsp->n2 != n2) {
+    op.eig_ws.reset();
+    auto fresh = std::make_shared<EigWorkspace>(m, n2);
+    wsp = fresh.get();
+    op.eig_ws = fresh;
+  }
+  EigWorkspace& W = *wsp;
+  DeviceBuffer &dV = W.dV, &dV2 = W.dV2, &dBV = W.dBV, &dBV2 = W.dBV2, &dR = W.dR, &dW = W.dW, &dHa = W.dHa, &dHb = W.dHb,
+               &dBeta = W.dBeta, &dQ = W.dQ, &dX = W.dX, &dRes = W.dRes;
   double* V = dV.as<double>();
   double* V2 = dV2.as<double>();
   double* BV = dBV.as<double>();
@@ -161,19 +204,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   std::vector<double> final_res, last_res;
   std::vector<int> final_block;  // 0 upper, 1 lower
   std::vector<double> final_vecs_re, final_vecs_im;
-  // pinned: the cycle's H / beta copies are truly asynchronous, so the host
-  // can start on them while the GPU already applies the operator to the
-  // continuation vector of the next cycle
-  struct Pinned {
-    double* p = nullptr;
-    explicit Pinned(size_t n) {
-      cuda_check(cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(double) * std::max<size_t>(n, 1)), "pinned");
-    }
-    ~Pinned() { cudaFreeHost(p); }
-    double& operator[](size_t i) { return p[i]; }
-    double* data() { return p; }
-  };
-  Pinned ha((m + 1) * (m + 1)), hb((m + 1) * (m + 1)), betas(m + 1);
+  Pinned &ha = W.ha, &hb = W.hb, &betas = W.betas;
   cudaEvent_t e_h;
   cuda_check(cudaEventCreateWithFlags(&e_h, cudaEventDisableTiming), "event");
   bool pre_applied = false;  // r already holds apply(V[k]) (speculative, see below)
@@ -187,13 +218,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   };
   double t_graph_build = 0;
   const double t_setup = ms_since(t0);
-  std::map<std::pair<int, const double*>, cudaGraphExec_t> graphs;
-  struct GraphFree {
-    std::map<std::pair<int, const double*>, cudaGraphExec_t>* g;
-    ~GraphFree() {
-      for (auto& kv : *g) cudaGraphExecDestroy(kv.second);
-    }
-  } graph_free{&graphs};
+  auto& graphs = W.graphs;
 
   while (true) {
     // max_restarts bounds each Krylov-Schur pass (the main run and every guard
