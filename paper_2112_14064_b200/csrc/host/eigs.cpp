@@ -93,10 +93,12 @@ struct EigWorkspace {
   int64_t n2 = 0;
   DeviceBuffer dV, dV2, dBV, dBV2, dR, dW, dHa, dHb, dBeta, dQ, dX, dRes;
   Pinned ha, hb, betas;
+  Pinned hv, hq, hy;  // staging of the host -> device copies (start vectors, restart Q, Ritz Y)
   std::map<std::pair<int, const double*>, cudaGraphExec_t> graphs;
   EigWorkspace(int m_, int64_t n2_)
       : m(m_), n2(n2_), ha(static_cast<size_t>(m_ + 1) * (m_ + 1)), hb(static_cast<size_t>(m_ + 1) * (m_ + 1)),
-        betas(m_ + 1) {
+        betas(m_ + 1), hv(static_cast<size_t>(n2_)), hq(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)),
+        hy(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)) {
     dV.alloc(sizeof(double) * (m + 1) * n2);
     dV2.alloc(sizeof(double) * (m + 1) * n2);
     dBV.alloc(sizeof(double) * (m + 1) * n2);
@@ -176,7 +178,8 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     std::vector<double> v(n2);
     uint64_t s = seed;
     for (int64_t i = 0; i < n2; ++i) v[i] = splitmix_uniform(s);
-    cuda_check(cudaMemcpyAsync(r, v.data(), sizeof(double) * n2, cudaMemcpyHostToDevice, st), "H2D v0");
+    std::memcpy(W.hv.data(), v.data(), sizeof(double) * n2);
+    cuda_check(cudaMemcpyAsync(r, W.hv.data(), sizeof(double) * n2, cudaMemcpyHostToDevice, st), "H2D v0");
     for (int pass = 0; pass < 2 && nlock > 0; ++pass) {
       op.gemv_t(BV, nlock, r, dHa.as<double>());
       op.gemv_n(V, nlock, dHa.as<double>(), r, nullptr);
@@ -405,8 +408,12 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
           Yr[row + static_cast<size_t>(2 * c + 1) * m] = ycol[row].imag();
         }
       }
-      cuda_check(cudaMemcpyAsync(dQ.p, Yr.data(), sizeof(double) * Yr.size(), cudaMemcpyHostToDevice, st),
-                 "H2D Y");
+      const double* ysrc = Yr.data();
+      if (Yr.size() <= static_cast<size_t>(m + 1) * (2 * m + 2)) {
+        std::memcpy(W.hy.data(), Yr.data(), sizeof(double) * Yr.size());
+        ysrc = W.hy.data();
+      }
+      cuda_check(cudaMemcpyAsync(dQ.p, ysrc, sizeof(double) * Yr.size(), cudaMemcpyHostToDevice, st), "H2D Y");
       std::vector<double> lam(2 * nchk);
       for (int c = 0; c < nchk; ++c) {
         const cplx gam = rz[chk[c]].lambda / vs;  // eigenvalue of the scaled pencil
@@ -566,7 +573,8 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       }
       res.max_restart_defect = std::max(res.max_restart_defect, dmax / std::max(hmax, 1e-300));
     }
-    cuda_check(cudaMemcpyAsync(dQ.p, Qp.data(), sizeof(double) * m * p, cudaMemcpyHostToDevice, st), "H2D Q");
+    std::memcpy(W.hq.data(), Qp.data(), sizeof(double) * m * p);
+    cuda_check(cudaMemcpyAsync(dQ.p, W.hq.data(), sizeof(double) * m * p, cudaMemcpyHostToDevice, st), "H2D Q");
     op.combine(V, m, dQ.as<double>(), m, p, V2);
     op.combine(BV, m, dQ.as<double>(), m, p, BV2);
     L.n_restart += 1;
