@@ -218,3 +218,57 @@ class Eig:
         if getattr(self, "h", None) is not None and self.h.value:
             self.lib.oracle_eig_destroy(self.h)
             self.h = None
+
+
+# --------------------------------------------------------------------------- assembly
+# BASELINE.json configs by short name: (kind 0 curl / 1 div, p, ne, rIGA levels);
+# restated here so the reference CPU arm never loads the product library.
+CONFIGS = {
+    "cfg1": (1, 2, 32, 0), "cfg2_iga": (1, 3, 64, 0), "cfg2_riga": (1, 3, 64, 3),
+    "cfg3_iga": (0, 4, 128, 0), "cfg3_riga": (0, 4, 128, 3),
+    "cfg4_iga": (1, 3, 512, 0), "cfg4_riga": (1, 3, 512, 5),
+}
+for _p in (2, 3, 4, 5):
+    CONFIGS[f"cfg5_p{_p}_iga"] = (0, _p, 256, 0)
+    CONFIGS[f"cfg5_p{_p}_riga"] = (0, _p, 256, 5)
+
+
+class RefPencil:
+    """BASELINE pencil assembled by oracle/ref_assembly.cpp on the reference's
+    own spaces / splines / Piola code (an independent second route to the
+    product's assembler). Same attribute names as the product's pencil."""
+
+    def __init__(self, kind, degree, elems, levels=0, alpha=0.05, beta=0.01):
+        lib = ref()
+        if lib is None:
+            raise ImportError("oracle/_ref/liboracle_ref.so not built")
+        lib.ref_assemble.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.POINTER(vp)]
+        lib.ref_assemble.restype = C.c_int
+        lib.ref_assemble_last_error.restype = C.c_char_p
+        lib.ref_assemble_dims.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        lib.ref_assemble_dims.restype = None
+        lib.ref_assemble_copy.argtypes = [vp, i64p, i32p, f64p, f64p, f64p, i32p]
+        lib.ref_assemble_copy.restype = None
+        lib.ref_assemble_destroy.argtypes = [vp]
+        lib.ref_assemble_destroy.restype = None
+        h = vp()
+        rc = lib.ref_assemble(kind, degree, elems, levels, alpha, beta, C.byref(h))
+        if rc != 0:
+            raise OracleError(rc, lib.ref_assemble_last_error().decode())
+        nf, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        lib.ref_assemble_dims(h, C.byref(nf), C.byref(n), C.byref(nnz))
+        self.n_full, self.n, self.nnz = nf.value, n.value, nnz.value
+        self.rowptr = np.zeros(self.n + 1, np.int64)
+        self.col = np.zeros(self.nnz, np.int32)
+        self.K, self.C, self.M = (np.zeros(self.nnz) for _ in range(3))
+        self.box = np.zeros((self.n, 4), np.int32)
+        lib.ref_assemble_copy(h, self.rowptr, self.col, self.K, self.C, self.M, self.box)
+        lib.ref_assemble_destroy(h)
+        self.elems, self.degree, self.kind, self.levels = elems, degree, kind, levels
+
+    def q_values(self, sigma):
+        return self.K + sigma * self.C + sigma * sigma * self.M
+
+
+def ref_config(name):
+    return RefPencil(*CONFIGS[name])

@@ -30,6 +30,8 @@
 #include <string>
 #include <vector>
 
+#include <omp.h>
+
 #ifdef ORACLE_REF_KERN
 #include "rigaqep/kernels.hpp"
 #endif
@@ -249,8 +251,28 @@ Symbolic symbolic(int64_t n, const int64_t* rp, const int32_t* col, const int32_
 struct FrontF {
   int32_t npiv = 0, nf = 0;
   std::vector<int32_t> rows;
-  std::vector<cd> F;        // nf x nf row-major: L\U and (consumed) CB
+  std::vector<cd> F;        // nf x nf row-major while the front is live: L\U and its CB
+  std::vector<cd> U, Lc;    // after the parent consumed the CB: rows 0..npiv-1 (npiv x nf)
+                            // and rows npiv..nf-1 of columns 0..npiv-1 ((nf-npiv) x npiv)
   std::vector<int32_t> ipiv;
+  int64_t swaps = 0;
+  uint64_t macs = 0;
+  bool compacted = false;
+  // L\U entry (i, c) with i < npiv or c < npiv
+  cd lu(int i, int c) const {
+    if (!compacted) return F[static_cast<size_t>(i) * nf + c];
+    return i < npiv ? U[static_cast<size_t>(i) * nf + c] : Lc[static_cast<size_t>(i - npiv) * npiv + c];
+  }
+  void compact() {
+    if (compacted) return;
+    U.assign(F.begin(), F.begin() + static_cast<size_t>(npiv) * nf);
+    Lc.resize(static_cast<size_t>(nf - npiv) * npiv);
+    for (int i = npiv; i < nf; ++i)
+      std::copy(F.begin() + static_cast<size_t>(i) * nf, F.begin() + static_cast<size_t>(i) * nf + npiv,
+                Lc.begin() + static_cast<size_t>(i - npiv) * npiv);
+    std::vector<cd>().swap(F);
+    compacted = true;
+  }
 };
 
 struct Factor {
@@ -266,14 +288,108 @@ struct OracleError {
   std::string msg;
 };
 
+// Factor one front: assemble the original entries and the children's
+// contribution blocks (extend-add, children in ascending order), then
+// right-looking threshold-pivoted elimination with kern::elim_step. Rows of a
+// rank-1 step are independent (each row scales its multiplier, then
+// row -= l * urow), so large trailing blocks split into row chunks executed as
+// OpenMP tasks: every entry sees the same operations in the same order, the
+// factors are bit-identical for any thread count (SPEC.md:366 allows concurrent
+// subtree factorization).
+void factor_front(Factor& R, int f, const std::vector<std::vector<std::pair<int64_t, cd>>>& orig,
+                  const std::vector<std::vector<int>>& kids) {
+  const Symbolic& S = *R.S;
+  FrontF& Fr = R.fr[f];
+  Fr.rows = S.node_rows[f];
+  Fr.nf = static_cast<int32_t>(Fr.rows.size());
+  Fr.npiv = S.node_npiv[f];
+  const int nf = Fr.nf, np = Fr.npiv;
+  Fr.F.assign(static_cast<size_t>(nf) * nf, cd{});
+  auto loc = [&](int32_t g) {
+    const auto it = std::lower_bound(Fr.rows.begin(), Fr.rows.end(), g);
+    if (it == Fr.rows.end() || *it != g) throw OracleError{7, "entry outside front"};
+    return static_cast<int>(it - Fr.rows.begin());
+  };
+  for (auto& e : orig[f]) {
+    const int r = loc(static_cast<int32_t>(e.first / S.n)), c = loc(static_cast<int32_t>(e.first % S.n));
+    Fr.F[static_cast<size_t>(r) * nf + c] += e.second;
+  }
+  for (int c : kids[f]) {  // extend-add
+    FrontF& K = R.fr[c];
+    const int knp = K.npiv, knf = K.nf;
+    std::vector<int> map(knf - knp);
+    for (int t = knp; t < knf; ++t) map[t - knp] = loc(K.rows[t]);
+    for (int a = knp; a < knf; ++a)
+      for (int b = knp; b < knf; ++b)
+        Fr.F[static_cast<size_t>(map[a - knp]) * nf + map[b - knp]] += K.F[static_cast<size_t>(a) * knf + b];
+    K.compact();  // the child's CB is consumed
+  }
+  Fr.ipiv.assign(np, 0);
+  std::vector<cd> lcol(nf);
+  for (int k = 0; k < np; ++k) {
+    double best = -1.0;
+    int bi = k;
+    for (int i = k; i < np; ++i) {
+      const double v = std::abs(Fr.F[static_cast<size_t>(i) * nf + k]);
+      if (v > best) best = v, bi = i;
+    }
+    if (!(best >= 1e-300)) throw OracleError{8, "singular pivot block"};
+    const double diag = std::abs(Fr.F[static_cast<size_t>(k) * nf + k]);
+    const int p = diag >= 0.1 * best ? k : bi;
+    Fr.ipiv[k] = p;
+    if (p != k) {
+      ++Fr.swaps;
+      for (int c = 0; c < nf; ++c)
+        std::swap(Fr.F[static_cast<size_t>(k) * nf + c], Fr.F[static_cast<size_t>(p) * nf + c]);
+    }
+    const cd piv = Fr.F[static_cast<size_t>(k) * nf + k];
+    const int rows = nf - k - 1, cols = nf - k - 1;
+    cd* F = Fr.F.data();
+    cd* lc = lcol.data();
+    auto chunk = [F, lc, piv, k, nf, cols](int r0, int r1) -> uint64_t {
+      for (int i = k + 1 + r0; i < k + 1 + r1; ++i) {
+        cd& a = F[static_cast<size_t>(i) * nf + k];
+        a /= piv;
+        lc[i - k - 1] = a;
+      }
+      return k_elim(&F[static_cast<size_t>(k + 1 + r0) * nf + k + 1], nf, lc + r0,
+                    &F[static_cast<size_t>(k) * nf + k + 1], r1 - r0, cols);
+    };
+    const int64_t work = static_cast<int64_t>(rows) * cols;
+    if (work < (int64_t{1} << 17) || omp_get_num_threads() == 1) {
+      Fr.macs += chunk(0, rows);
+    } else {
+      const int g = 32;
+      uint64_t m = 0;
+#pragma omp taskloop grainsize(1) reduction(+ : m)
+      for (int b = 0; b < (rows + g - 1) / g; ++b) m += chunk(b * g, std::min(rows, (b + 1) * g));
+      Fr.macs += m;
+    }
+  }
+}
+
+void factor_subtree(Factor& R, int f, const std::vector<std::vector<std::pair<int64_t, cd>>>& orig,
+                    const std::vector<std::vector<int>>& kids) {
+  for (int c : kids[f]) {
+#pragma omp task default(shared) firstprivate(c)
+    factor_subtree(R, c, orig, kids);
+  }
+#pragma omp taskwait
+  factor_front(R, f, orig, kids);
+}
+
 Factor lu_factorize(const Symbolic& S, const Csr& A, Ledger* L) {
   Factor R;
   R.S = &S;
   const int nn = static_cast<int>(S.node_rows.size());
   R.fr.resize(nn);
   std::vector<std::vector<int>> kids(nn);
+  std::vector<int> roots;
   for (int f = 0; f < nn; ++f)
-    if (S.node_parent[f] >= 0) kids[S.node_parent[f]].push_back(f);
+    if (S.node_parent[f] >= 0)
+      kids[S.node_parent[f]].push_back(f);
+    else
+      roots.push_back(f);
   std::vector<int32_t> owner(S.n);
   for (int f = 0; f < nn; ++f)
     for (int k = 0; k < S.node_npiv[f]; ++k) owner[S.node_start[f] + k] = f;
@@ -284,60 +400,31 @@ Factor lu_factorize(const Symbolic& S, const Csr& A, Ledger* L) {
       const int64_t r = S.iperm[i], c = S.iperm[A.col[k]];
       orig[owner[std::min(r, c)]].push_back({r * S.n + c, A.val[k]});
     }
+  std::string err;
+  int err_code = 0;
+#pragma omp parallel
+#pragma omp single
+  {
+    for (int r : roots) {
+#pragma omp task default(shared) firstprivate(r)
+      {
+        try {
+          factor_subtree(R, r, orig, kids);
+        } catch (const OracleError& e) {
+#pragma omp critical
+          if (!err_code) err_code = e.code, err = e.msg;
+        }
+      }
+    }
+  }
+  if (err_code) throw OracleError{err_code, err};
   uint64_t macs = 0;
   for (int f = 0; f < nn; ++f) {
-    FrontF& Fr = R.fr[f];
-    Fr.rows = S.node_rows[f];
-    Fr.nf = static_cast<int32_t>(Fr.rows.size());
-    Fr.npiv = S.node_npiv[f];
-    const int nf = Fr.nf, np = Fr.npiv;
-    Fr.F.assign(static_cast<size_t>(nf) * nf, cd{});
-    auto loc = [&](int32_t g) {
-      const auto it = std::lower_bound(Fr.rows.begin(), Fr.rows.end(), g);
-      if (it == Fr.rows.end() || *it != g) throw OracleError{7, "entry outside front"};
-      return static_cast<int>(it - Fr.rows.begin());
-    };
-    for (auto& e : orig[f]) {
-      const int r = loc(static_cast<int32_t>(e.first / S.n)), c = loc(static_cast<int32_t>(e.first % S.n));
-      Fr.F[static_cast<size_t>(r) * nf + c] += e.second;
-    }
-    for (int c : kids[f]) {  // extend-add
-      FrontF& K = R.fr[c];
-      const int knp = K.npiv, knf = K.nf;
-      std::vector<int> map(knf - knp);
-      for (int t = knp; t < knf; ++t) map[t - knp] = loc(K.rows[t]);
-      for (int a = knp; a < knf; ++a)
-        for (int b = knp; b < knf; ++b)
-          Fr.F[static_cast<size_t>(map[a - knp]) * nf + map[b - knp]] += K.F[static_cast<size_t>(a) * knf + b];
-    }
-    Fr.ipiv.assign(np, 0);
-    std::vector<cd> lcol(nf);
-    for (int k = 0; k < np; ++k) {
-      double best = -1.0;
-      int bi = k;
-      for (int i = k; i < np; ++i) {
-        const double v = std::abs(Fr.F[static_cast<size_t>(i) * nf + k]);
-        if (v > best) best = v, bi = i;
-      }
-      if (!(best >= 1e-300)) throw OracleError{8, "singular pivot block"};
-      const double diag = std::abs(Fr.F[static_cast<size_t>(k) * nf + k]);
-      const int p = diag >= 0.1 * best ? k : bi;
-      Fr.ipiv[k] = p;
-      if (p != k) {
-        ++R.swaps;
-        for (int c = 0; c < nf; ++c)
-          std::swap(Fr.F[static_cast<size_t>(k) * nf + c], Fr.F[static_cast<size_t>(p) * nf + c]);
-      }
-      const cd piv = Fr.F[static_cast<size_t>(k) * nf + k];
-      for (int i = k + 1; i < nf; ++i) {
-        cd& a = Fr.F[static_cast<size_t>(i) * nf + k];
-        a /= piv;
-        lcol[i - k - 1] = a;
-      }
-      macs += k_elim(&Fr.F[static_cast<size_t>(k + 1) * nf + k + 1], nf, lcol.data(),
-                     &Fr.F[static_cast<size_t>(k) * nf + k + 1], nf - k - 1, nf - k - 1);
-    }
-    R.fb_macs += static_cast<double>(np) * np + 2.0 * np * (nf - np);
+    R.fr[f].compact();
+    macs += R.fr[f].macs;
+    R.swaps += R.fr[f].swaps;
+    const double np = R.fr[f].npiv, nf = R.fr[f].nf;
+    R.fb_macs += np * np + 2.0 * np * (nf - np);
   }
   R.fa_macs = static_cast<double>(macs);
   if (L) L->add(FA, R.fa_macs);
@@ -360,7 +447,7 @@ void solve_factored(const Factor& R, const cd* b, cd* x, Ledger* L) {
     }
     for (int k = 0; k < np; ++k) {
       const cd yk = y[Fr.rows[k]];
-      for (int i = k + 1; i < nf; ++i) y[Fr.rows[i]] -= Fr.F[static_cast<size_t>(i) * nf + k] * yk;
+      for (int i = k + 1; i < nf; ++i) y[Fr.rows[i]] -= Fr.lu(i, k) * yk;
     }
   }
   // backward, reverse postorder
@@ -369,8 +456,8 @@ void solve_factored(const Factor& R, const cd* b, cd* x, Ledger* L) {
     const int nf = Fr.nf, np = Fr.npiv;
     for (int k = np - 1; k >= 0; --k) {
       cd s = y[Fr.rows[k]];
-      for (int c = k + 1; c < nf; ++c) s -= Fr.F[static_cast<size_t>(k) * nf + c] * y[Fr.rows[c]];
-      y[Fr.rows[k]] = s / Fr.F[static_cast<size_t>(k) * nf + k];
+      for (int c = k + 1; c < nf; ++c) s -= Fr.lu(k, c) * y[Fr.rows[c]];
+      y[Fr.rows[k]] = s / Fr.lu(k, k);
     }
   }
   for (int64_t i = 0; i < S.n; ++i) x[S.perm[i]] = y[i];
@@ -746,6 +833,11 @@ extern "C" {
 
 const char* oracle_last_error() { return g_err.c_str(); }
 
+// Host threads of the oracle's factorization (OpenMP; <= 0: all cores).
+// Results are bit-identical for every thread count.
+void oracle_set_threads(int n) { omp_set_num_threads(n > 0 ? n : omp_get_num_procs()); }
+int oracle_get_threads() { return omp_get_max_threads(); }
+
 int oracle_kind() {
 #ifdef ORACLE_REF_KERN
   return 1;
@@ -797,7 +889,12 @@ int oracle_factor_front(void* h, int f, double* dense_c, int32_t* ipiv, int32_t*
   return guarded([&] {
     auto* F = static_cast<OracleFactor*>(h);
     const auto& Fr = F->F.fr.at(f);
-    if (dense_c) std::memcpy(dense_c, Fr.F.data(), sizeof(cd) * Fr.F.size());
+    if (dense_c) {  // L\U (the consumed contribution block reads as zero)
+      cd* D = reinterpret_cast<cd*>(dense_c);
+      for (int i = 0; i < Fr.nf; ++i)
+        for (int c = 0; c < Fr.nf; ++c)
+          D[static_cast<size_t>(i) * Fr.nf + c] = (i < Fr.npiv || c < Fr.npiv) ? Fr.lu(i, c) : cd{};
+    }
     if (ipiv) std::copy(Fr.ipiv.begin(), Fr.ipiv.end(), ipiv);
     if (rows) std::copy(Fr.rows.begin(), Fr.rows.end(), rows);
   });
