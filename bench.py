@@ -3,16 +3,27 @@
 
 Arms:
   default (B200)        librq_b200.so on cuda:LOCAL_RANK through the C-ABI.
-  --impl reference      the reference's CPU path: oracle/_ref/liboracle_ref.so
-                        (reference kern:: kernels compiled from /root/reference +
-                        the SPEC restatement), else the oracle port; 1 thread
-                        (the reference has no threading); rank 0 only.
+  --impl reference      the reference's CPU path on the host cores: the pencil
+                        from oracle/ref_assembly.cpp (the reference's own spaces,
+                        splines and Piola code), the oracle's multifrontal LU
+                        whose inner loop is the reference's kern::elim_step
+                        (oracle/_ref/liboracle_ref.so, AVX2 backend where the
+                        host has it), OpenMP over all host threads; rank 0 only.
+                        The product library is never loaded on this arm.
 
-One step = one numeric multifrontal LU of Q(sigma) of the configured pencil
-(BASELINE metric "FP64 LU-factor GFLOP/s"); the same line reports the time to
-nev eigenpairs (factor + Krylov-Schur to converged pairs) and the per-kernel
-rooflines. Multi-GPU: replicas only - every rank factors its
-own copy, value = sum of per-rank work / max-over-ranks time.
+Workload (BASELINE configs[3], the largest single-GPU config and the one the
+north-star targets are quoted on): cfg4_riga = H(div) p=3 512^2 rIGA (C^1
+separators every 16 elements), N = 592,960, nnz = 40.3M, sigma = -0.5,
+nev = 100, m = 201. cfg4_iga (same mesh, maximum continuity) is measured in
+the same line, with the IGA/rIGA factor ratio beside PAPER.md:916's 3.634.
+
+One step = one numeric multifrontal LU of Q(sigma) (BASELINE metric "FP64
+LU-factor GFLOP/s"): device-resident values, CUDA graph replay, L2 scrubbed
+(256 MiB) before every timed step. The same line carries the time to nev
+eigenpairs (factor + Krylov-Schur to converged pairs) and the per-kernel
+rooflines. Multi-GPU: replicas only - every rank factors its own
+copy, value = sum of per-rank work / max-over-ranks time; `--gpus N` without a
+launcher re-executes itself under torch.distributed.run with N processes.
 """
 import argparse
 import json
@@ -29,17 +40,18 @@ METRIC = "FP64 LU-factor GFLOP/s + time to nev eigenpairs, as % of FP64/HBM roof
 SIGMA = -0.5
 NEV = {"cfg1": 10, "cfg2_riga": 20, "cfg2_iga": 20, "cfg3_riga": 50, "cfg3_iga": 50,
        "cfg4_riga": 100, "cfg4_iga": 100}
+COMPANION = {"cfg4_riga": "cfg4_iga", "cfg2_riga": "cfg2_iga", "cfg3_riga": "cfg3_iga"}
+PAPER_RATIO = {"cfg4": 3.634}  # PAPER.md:916, LU-FLOP improvement IGA/rIGA at p=3 (ne=1024)
 FP64_PEAK_TFLOPS = 37.2   # measured DMMA m16n8k4 issue rate, profiles/fp64_peak_r01.jsonl
-FP64_DFMA_TFLOPS = 36.7   # measured DFMA rate (same file)
 KINDS = ["scatter_original", "extend_add", "front_lu_smem", "panel_lu", "panel_apply+rowperm",
          "schur_dmma", "factor_dag"]
 
 
 def measured_peaks():
     try:
-        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
     except Exception:  # noqa: BLE001
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
 class ClockSampler:
@@ -63,7 +75,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:  # noqa: BLE001
                 pass
-            self.stop.wait(0.2)
+            self.stop.wait(0.1)
 
     def __enter__(self):
         self.t.start()
@@ -92,7 +104,7 @@ def dist_init():
     if ws > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("gloo")
+        dist.init_process_group("gloo")  # barrier + max only: replicas exchange no data
     return rank, ws, local
 
 
@@ -122,105 +134,129 @@ def host_info():
                 break
     except OSError:
         pass
-    return {"nproc": os.cpu_count(), "cpu_model": model, "pinned_core": 0}
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
-def pin_core0():
-    """The reference path is single-threaded (taskset -c 0)."""
-    try:
-        os.sched_setaffinity(0, {0})
-    except (AttributeError, OSError):
-        pass
-
-
-def cpu_factor_sample(P, kind, budget_s):
-    """Oracle factorization timed on the host (1 thread, pinned), bounded sample."""
+def cpu_factor_sample(kind, P, flu, nsamples=1, symbolic=None):
+    """Oracle numeric factorization(s) on all host threads; symbolic excluded."""
     import oracle
-    old = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
-    pin_core0()
+    lib = oracle.lib_for(kind)
+    lib.oracle_set_threads(0)
+    threads = lib.oracle_get_threads()
+    S = symbolic or oracle.Symbolic(P.n, P.rowptr, P.col, P.box, P.elems, kind=kind)
     Q = P.q_values(SIGMA)
     ts = []
-    t_end = time.perf_counter() + budget_s
-    while True:
+    for _ in range(nsamples):
         t0 = time.perf_counter()
-        f = oracle.Factor(P.n, P.rowptr, P.col, Q, P.box, P.elems, kind=kind)
+        f = oracle.Factor(P.n, P.rowptr, P.col, Q, kind=kind, symbolic=S)
         ts.append(time.perf_counter() - t0)
         del f
-        if time.perf_counter() > t_end or len(ts) >= 50:
-            break
-    if old is not None:
-        os.sched_setaffinity(0, old)
-    return ts
+    return ts, threads, S
 
 
+def cpu_step_split(kind, P, j0, nsteps, threads, symbolic=None):
+    """Per-category split of Arnoldi steps of the reference CPU path."""
+    import oracle
+    lib = oracle.lib_for(kind)
+    lib.oracle_set_threads(threads)
+    E = oracle.Eig(P, SIGMA, kind=kind, symbolic=symbolic)
+    t = E.step_profile(j0, nsteps)
+    per = {k: round(v / nsteps, 2) for k, v in t.items()}
+    per["total"] = round(sum(t.values()) / nsteps, 2)
+    return per
+
+
+# =============================================================================== reference arm
 def run_reference(args):
     rank, ws, _ = dist_init()
     if rank != 0:
         return
-    pin_core0()
     import oracle
-    import paper_2112_14064_b200 as rq
     kind = "reference" if oracle.ref() is not None else "port"
-    P = rq.baseline_config(args.config)
-    o = rq.nested_dissection_order(P)
-    flu = o.stats["flops_lu"]
+    cfg = args.config
+    t0 = time.perf_counter()
+    P = oracle.ref_config(cfg)  # the reference's spaces + splines; no product library
+    t_asm = time.perf_counter() - t0
+    lib = oracle.lib_for(kind)
+    lib.oracle_set_threads(0)
+    threads = lib.oracle_get_threads()
+    t0 = time.perf_counter()
+    S = oracle.Symbolic(P.n, P.rowptr, P.col, P.box, P.elems, kind=kind)
+    t_sym = time.perf_counter() - t0
+    flu = S.flops_lu()
     Q = P.q_values(SIGMA)
-    for _ in range(args.warmup):
-        oracle.Factor(P.n, P.rowptr, P.col, Q, P.box, P.elems, kind=kind)
+    # warm-up: one factorization (a CPU has no JIT / graph to warm; more would
+    # only spend the run's time budget)
+    oracle.Factor(P.n, P.rowptr, P.col, Q, kind=kind, symbolic=S)
     ts = []
+    t_end = time.perf_counter() + args.ref_budget_s
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        oracle.Factor(P.n, P.rowptr, P.col, Q, P.box, P.elems, kind=kind)
-        ts.append(time.perf_counter() - t0)
+        t1 = time.perf_counter()
+        oracle.Factor(P.n, P.rowptr, P.col, Q, kind=kind, symbolic=S)
+        ts.append(time.perf_counter() - t1)
+        if time.perf_counter() > t_end:
+            break
     sec = sum(ts) / len(ts)
     gf = flu / sec / 1e9
-    tnev = None
-    if args.nev_cpu:
-        t0 = time.perf_counter()
-        E = oracle.Eig(P, SIGMA, kind=kind)
-        E.solve_quadratic(NEV.get(args.config, 20), tol=1e-10, max_restarts=args.max_restarts)
-        tnev = (time.perf_counter() - t0) * 1e3
+    split = None
+    if args.cpu_step_split:
+        split = cpu_step_split(kind, P, NEV.get(cfg, 20), 2, threads, S)
+    sample = (f"{len(ts)} of {args.steps} requested full numeric factorizations of {cfg} "
+              f"(one untimed warm-up; symbolic analysis excluded; {args.ref_budget_s:.0f} s budget), "
+              f"{threads} OpenMP threads over subtrees and row chunks; complex cdouble arithmetic "
+              f"(the reference type): 4x the real work of the real F_LU the rate is quoted in")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gf, 4), "unit": "GFLOP/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": len(ts), "steps_requested": args.steps, "warmup": 1,
         "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "c128 (reference cdouble; real-flop count F_LU)",
-        "data": "synthetic (deterministic BASELINE assembly)",
-        "config": {"workload": args.config, "sigma": SIGMA, "nev": NEV.get(args.config, 20),
-                   "n": P.n, "nnz": P.nnz, "flops_lu_real": flu, "parallelism": "1 host thread"},
-        "time_to_nev_ms": tnev,
-        "cpu_baseline": {"value": round(gf, 4), "unit": "GFLOP/s", "cores": 1, "kind": kind,
-                         "sample": f"{args.steps} full factorizations of {args.config}",
-                         "host": host_info()},
+        "vs_baseline": None, "dtype": "c128 (reference cdouble; rate in real-flop F_LU)",
+        "data": "synthetic (deterministic BASELINE assembly on the reference's spaces code)",
+        "config": {"workload": cfg, "sigma": SIGMA, "nev": NEV.get(cfg, 20), "n": P.n, "nnz": P.nnz,
+                   "flops_lu_real": flu, "parallelism": f"{threads} host threads",
+                   "assembly_s": round(t_asm, 2), "symbolic_s": round(t_sym, 2)},
+        "time_to_nev_ms": None,
+        "time_to_nev_note": "not run: one Krylov-Schur cycle of the CPU path at this size is minutes; "
+                            "per-step split below",
+        "cpu_step_ms": split,
+        "cpu_baseline": {"value": round(gf, 4), "unit": "GFLOP/s", "cores": threads, "kind": kind,
+                         "sample": sample, "host": host_info()},
         "e2e": {"value": round(gf, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# =============================================================================== B200 arm
 def run_b200(args):
     rank, ws, local = dist_init()
+    import ctypes as C
+
     import numpy as np
 
     import paper_2112_14064_b200 as rq
     from paper_2112_14064_b200 import _lib
-    import ctypes as C
     _lib.check(_lib.lib.rq_set_device(local))
-    peaks = measured_peaks()
-    P = rq.baseline_config(args.config)
-    nev = args.nev or NEV.get(args.config, 20)
+    peaks, peak_src = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    cfg = args.config
+    nev = args.nev or NEV.get(cfg, 20)
+    m = 2 * nev + 1
+    P = rq.baseline_config(cfg, device=True)  # device assembly (f1), copied to host arrays
     o = rq.nested_dissection_order(P)
     st = o.stats
     flu = st["flops_lu"]
     op = rq.build_operator(P, SIGMA, o)
     fh = _lib.lib.rq_operator_factor(op._h)
 
-    def time_what(what, iters, param=0):
-        ms = C.c_double()
-        _lib.check(_lib.lib.rq_operator_time(op._h, what, iters, param, C.byref(ms)))
-        return ms.value
+    def timer(h):
+        def time_what(what, iters, param=0):
+            ms = C.c_double()
+            _lib.check(_lib.lib.rq_operator_time(h._h, what, iters, param, C.byref(ms)))
+            return ms.value
+        return time_what
+    time_what = timer(op)
 
-    # ---- device-resident steps: numeric factorization (graph replay), L2 flushed between steps
+    # ---- timed steps: numeric factorization (graph replay), L2 scrubbed between steps
     time_what(5 | 0x100, max(args.warmup, 3))
     barrier(ws)
     with ClockSampler(local) as clk:
@@ -228,16 +264,39 @@ def run_b200(args):
     ms_max = allreduce_max(ms_step, ws)
     value = ws * flu / (ms_max * 1e6)  # GFLOP/s, whole job
 
+    single = rank == 0 and ws == 1
+    line = {}
+    # ---- IGA companion on the same mesh (factor only) and the IGA/rIGA ratio
+    companion = None
+    comp = COMPANION.get(cfg)
+    if single and comp and args.companion:
+        PI = rq.baseline_config(comp, device=True)
+        oI = rq.nested_dissection_order(PI)
+        opI = rq.build_operator(PI, SIGMA, oI)
+        tI = timer(opI)
+        tI(5 | 0x100, 3)
+        msI = tI(5 | 0x100, max(3, args.steps // 2))
+        fI = oI.stats["flops_lu"]
+        companion = {"workload": comp, "n": PI.n, "nnz": PI.nnz, "flops_lu_real": fI,
+                     "max_front": int(oI.stats["max_front"]), "factor_ms": round(msI, 3),
+                     "gflops": round(fI / (msI * 1e6), 1),
+                     "frac_fp64": round(fI / (msI * 1e9) / FP64_PEAK_TFLOPS, 4),
+                     "flops_ratio_iga_over_riga": round(fI / flu, 3),
+                     "time_ratio_iga_over_riga": round(msI / ms_step, 3),
+                     "paper_flops_ratio": PAPER_RATIO.get(cfg.split("_")[0]),
+                     "paper_ratio_note": "PAPER.md:916: LU-FLOP improvement IGA/rIGA, p=3, ne=1024 (MUMPS/METIS)"}
+        del opI, PI
+
     # ---- time to nev eigenpairs (device-resident pencil; factor + Krylov-Schur)
-    t_nev = []
-    info = {}
+    t_nev, infos = [], []
     for _ in range(max(1, args.nev_runs)):
         t0 = time.perf_counter()
         pairs = op.solve_quadratic(nev, eps=1e-10, seed=0, max_restarts=args.max_restarts,
                                    raise_partial=False)
         t_nev.append((time.perf_counter() - t0) * 1e3 + op.factor_info()["factor_ms"])
-        info = op.last_info
+        infos.append(op.last_info)
     resid_max = max(p.residual for p in pairs)
+    info = infos[-1]
 
     # ---- per-kernel profile of one factorization (un-graphed, events per launch)
     ms_k = np.zeros(7)
@@ -245,15 +304,47 @@ def run_b200(args):
     work_k = np.zeros(7)
     _lib.check(_lib.lib.rq_factor_profile(fh, ms_k, cnt_k, work_k))
     dom = int(np.argmax(ms_k))
-    # ---- memory-bound kernels of the Krylov step
-    t_solve = time_what(1 | 0x100, 20)
-    t_spmv = time_what(2 | 0x100, 50)
-    m = 2 * nev + 1
-    t_gemv = time_what(3 | 0x100, 20, m)
+    # ---- memory-bound kernels of the Krylov step (L2 scrubbed before every call)
+    t_solve = time_what(1 | 0x100, 10)
+    t_spmv = time_what(2 | 0x100, 20)
+    t_gt = time_what(3 | 0x100, 10, m)
+    t_gn = time_what(4 | 0x100, 10, m)
+    t_rst = time_what(7 | 0x100, 5, m)
     solve_bytes = st["trisolve_bytes"]
     spmv_bytes = 20.0 * P.nnz + 8.0 * (P.n + 1) + 24.0 * P.n
     gemv_bytes = 8.0 * 2 * P.n * m
-    hbm = peaks.get("hbm_gbs", 6650.0)
+    keep = nev + min(20, m - nev - 1)
+    rst_flops = 2.0 * 2 * P.n * m * keep
+    rst_bytes = 8.0 * 2 * P.n * (m + keep)
+
+    def hb(ms, b):
+        return {"ms": round(ms, 4), "gbs": round(b / (ms * 1e6), 1), "frac_hbm": round(b / (ms * 1e6) / hbm, 4)}
+    kernels = {
+        "factor_profile_ms": {KINDS[i]: round(float(ms_k[i]), 4) for i in range(7)},
+        "trisolve": hb(t_solve, solve_bytes),
+        "spmv_fused_cm": hb(t_spmv, spmv_bytes),
+        "cgs_gemv_t": dict(hb(t_gt, gemv_bytes), k=m),
+        "cgs_gemv_n": dict(hb(t_gn, gemv_bytes), k=m),
+        "restart_vq": {"ms": round(t_rst, 4), "m": m, "keep": keep,
+                       "tflops": round(rst_flops / (t_rst * 1e9), 2),
+                       "gbs": round(rst_bytes / (t_rst * 1e6), 1)},
+    }
+    if single:
+        # the large-front Schur update alone (north-star FP64 tensor target): the
+        # factorization's own UPDCB code over every contribution-block tile of the
+        # largest front, on a throwaway factorization (it overwrites that front's CB)
+        try:
+            fL = rq.lu_factorize((P.rowptr, P.col, P.q_values(SIGMA)), o)
+            ub = np.zeros(6)
+            _lib.check(_lib.lib.rq_factor_bench_updcb(fL._h, -1, 5, ub))
+            tf = ub[1] / (ub[0] * 1e9)
+            kernels["schur_update_top_front"] = {
+                "kernel": "updcb (factor_dag UPDCB task code, plain grid)", "front": int(ub[2]),
+                "K": int(ub[4]), "tiles": int(ub[3]), "ms": round(ub[0], 4), "tflops": round(tf, 2),
+                "frac_fp64": round(tf / FP64_PEAK_TFLOPS, 4)}
+            del fL
+        except Exception as e:  # noqa: BLE001
+            kernels["schur_update_top_front"] = {"error": str(e)[:200]}
 
     # ---- e2e through the public API with host buffers (pinned), H2D + D2H inside
     Q = P.q_values(SIGMA)
@@ -274,79 +365,33 @@ def run_b200(args):
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     e2e_ms = allreduce_max(e2e_ms, ws)
     launches = fac.info()["launches"]
-    # e2e time to nev from host arrays: operator creation (H2D of K, C, M, Q, factor) + eigs
-    t0 = time.perf_counter()
-    op2 = rq.build_operator(P, SIGMA, o)
-    op2.solve_quadratic(nev, eps=1e-10, seed=0, max_restarts=args.max_restarts, raise_partial=False)
-    e2e_nev_ms = (time.perf_counter() - t0) * 1e3
-    del op2
+    del fac
+    # time to nev from host arrays: operator creation (H2D of K, C, M, Q, factor) + eigensolve
+    e2e_nev_ms = None
+    if single:
+        PH = rq.QuadraticPencil(**{k: getattr(P, k) for k in (
+            "kind", "degree", "elems", "levels", "n_full", "n", "rowptr", "col", "K", "C", "M", "box",
+            "free_to_full")})
+        t0 = time.perf_counter()
+        op2 = rq.build_operator(PH, SIGMA, o)
+        op2.solve_quadratic(nev, eps=1e-10, seed=0, max_restarts=args.max_restarts, raise_partial=False)
+        e2e_nev_ms = (time.perf_counter() - t0) * 1e3
+        del op2
 
-    # ---- large config (rank 0, N = 1): the regime of the north-star targets
-    #      (large-front Schur updates on FP64 tensor cores, HBM-bound sweeps)
-    large = None
-    if rank == 0 and ws == 1 and args.large:
-        PL = rq.baseline_config(args.large)
-        oL = rq.nested_dissection_order(PL)
-        stL = oL.stats
-        opL = rq.build_operator(PL, SIGMA, oL)
-
-        def time_large(what, iters, param=0):
-            ms = C.c_double()
-            _lib.check(_lib.lib.rq_operator_time(opL._h, what, iters, param, C.byref(ms)))
-            return ms.value
-        time_large(5 | 0x100, 2)
-        f_ms = time_large(5 | 0x100, 3)
-        s_ms = time_large(1 | 0x100, 5)
-        sp_ms = time_large(2 | 0x100, 10)
-        kL = 2 * NEV.get(args.large, 100) + 1
-        gt_ms = time_large(3 | 0x100, 5, kL)
-        gn_ms = time_large(4 | 0x100, 5, kL)
-        gf_l = stL["flops_lu"] / (f_ms * 1e6)
-        sb = stL["trisolve_bytes"]
-        spb = 20.0 * PL.nnz + 8.0 * (PL.n + 1) + 24.0 * PL.n
-        gb = 8.0 * 2 * PL.n * kL
-        large = {
-            "workload": args.large, "n": PL.n, "nnz": PL.nnz, "flops_lu": stL["flops_lu"],
-            "max_front": int(stL["max_front"]),
-            "factor": {"ms": round(f_ms, 3), "gflops": round(gf_l, 1),
-                       "frac_fp64": round(gf_l / 1e3 / FP64_PEAK_TFLOPS, 4)},
-            "trisolve": {"ms": round(s_ms, 4), "gbs": round(sb / (s_ms * 1e6), 1),
-                         "frac_hbm": round(sb / (s_ms * 1e6) / hbm, 4)},
-            "spmv_fused_cm": {"ms": round(sp_ms, 4), "gbs": round(spb / (sp_ms * 1e6), 1),
-                              "frac_hbm": round(spb / (sp_ms * 1e6) / hbm, 4)},
-            "cgs_gemv_t": {"k": kL, "ms": round(gt_ms, 4), "gbs": round(gb / (gt_ms * 1e6), 1),
-                           "frac_hbm": round(gb / (gt_ms * 1e6) / hbm, 4)},
-            "cgs_gemv_n": {"k": kL, "ms": round(gn_ms, 4), "gbs": round(gb / (gn_ms * 1e6), 1),
-                           "frac_hbm": round(gb / (gn_ms * 1e6) / hbm, 4)},
-            "l2": "scrubbed (256 MiB) before every timed call",
-        }
-        del opL
-        # the large-front Schur update alone (north-star FP64 tensor target):
-        # the factorization's own UPDCB code over every contribution-block tile
-        # of the largest front, on a throwaway factorization (it overwrites
-        # that front's contribution block)
-        try:
-            fL = rq.lu_factorize((PL.rowptr, PL.col, PL.q_values(SIGMA)), oL)
-            ub = np.zeros(6)
-            _lib.check(_lib.lib.rq_factor_bench_updcb(fL._h, -1, 5, ub))
-            tf = ub[1] / (ub[0] * 1e9)
-            large["schur_update_top_front"] = {
-                "kernel": "updcb (factor_dag UPDCB task code, plain grid)", "front": int(ub[2]), "K": int(ub[4]),
-                "tiles": int(ub[3]), "ms": round(ub[0], 4), "tflops": round(tf, 2),
-                "frac_fp64": round(tf / FP64_PEAK_TFLOPS, 4)}
-            del fL
-        except Exception as e:  # noqa: BLE001
-            large["schur_update_top_front"] = {"error": str(e)[:200]}
-
-    # ---- CPU baseline (rank 0, N = 1 only): bounded oracle factorization sample
+    # ---- CPU baseline (rank 0, N = 1 only): the oracle on the host cores
     cpu = None
-    if rank == 0 and ws == 1 and args.cpu_sample_s > 0:
+    if single and args.cpu_samples > 0:
         import oracle
         kind = "reference" if oracle.ref() is not None else "port"
-        ts = cpu_factor_sample(P, kind, args.cpu_sample_s)
-        cpu = {"value": round(flu / (sum(ts) / len(ts)) / 1e9, 4), "unit": "GFLOP/s", "cores": 1,
-               "kind": kind, "sample": f"{len(ts)} full factorizations of {args.config} "
-                                       f"({sum(ts):.1f} s, complex cdouble arithmetic: 4x the real work)",
+        ts, threads, S = cpu_factor_sample(kind, P, flu, args.cpu_samples)
+        split = cpu_step_split(kind, P, m // 2, 2, threads, S) if args.cpu_step_split else None
+        cpu = {"value": round(flu / (sum(ts) / len(ts)) / 1e9, 4), "unit": "GFLOP/s", "cores": threads,
+               "kind": kind,
+               "sample": f"{len(ts)} full numeric factorization(s) of {cfg} ({sum(ts):.1f} s; symbolic "
+                         f"excluded; {threads} OpenMP threads over subtrees and row chunks; complex "
+                         f"cdouble arithmetic: 4x the real work)",
+               "step_ms": split, "step_note": "Arnoldi step at j = m/2 of the CPU path, ms per step by "
+                                              "category (spmv / solve / cgs2 / other)",
                "host": host_info()}
 
     # DRAM bytes per launch of the dominant kernel from a committed ncu --set
@@ -356,62 +401,72 @@ def run_b200(args):
     if os.path.exists(tpath):
         try:
             kname = {"factor_dag": "factor_dag_kernel"}.get(KINDS[dom], KINDS[dom])
-            ent = json.load(open(tpath)).get(args.config, {}).get(kname)
+            ent = json.load(open(tpath)).get(cfg, {}).get(kname)
             if ent:
                 traffic, traffic_src = ent["dram_bytes_per_launch"], ent["source"]
         except Exception:  # noqa: BLE001
             traffic = None
-    bound = "tensor" if KINDS[dom] == "schur_dmma" else ("hbm" if dom in (0, 1) else "tensor")
     if dom in (0, 1):
         ach = work_k[dom] / (ms_k[dom] * 1e6)  # GB/s
         roof = {"bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 5), "traffic": traffic}
     else:
-        peak = FP64_PEAK_TFLOPS if KINDS[dom] in ("schur_dmma", "factor_dag") else FP64_DFMA_TFLOPS
         ach = work_k[dom] / (ms_k[dom] * 1e9)  # TFLOP/s
-        roof = {"bound": bound, "achieved": round(ach, 4), "peak": peak, "unit": "TFLOP/s",
-                "frac": round(ach / peak, 5), "traffic": traffic}
+        roof = {"bound": "tensor", "achieved": round(ach, 4), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(ach / FP64_PEAK_TFLOPS, 5), "traffic": traffic}
     if traffic_src:
         roof["traffic_unit"] = "bytes/launch"
         roof["traffic_source"] = traffic_src
     roof.update({"kernel": KINDS[dom], "launches_per_step": int(cnt_k[dom]),
                  "share_of_step": round(float(ms_k[dom] / ms_k.sum()), 4),
-                 "peak_source": "hbm: MEASURED_PEAKS.json; fp64: measured tools/fp64_peak.cu "
-                                "(MEASURED_PEAKS.json has no FP64 entry)"})
+                 "work_per_launch": float(work_k[dom]),
+                 "peak_source": f"fp64: measured DMMA m16n8k4 rate, tools/fp64_peak.cu "
+                                f"(MEASURED_PEAKS.json has no FP64 entry); hbm: {peak_src} "
+                                f"MEASURED_PEAKS.json"})
+    first, rest = t_nev[0], t_nev[1:] or t_nev
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (deterministic BASELINE assembly; no dataset)",
-        "config": {"workload": args.config, "sigma": SIGMA, "nev": nev, "m": m, "n": P.n,
-                   "nnz": P.nnz, "flops_lu_real": flu, "nnz_l_stored": st["nnz_l"],
-                   "max_front": st["max_front"], "nfronts": st["nfronts"],
-                   "parallelism": f"replicas x{ws}", "l2": "flushed (256 MiB scrub) before every timed step"},
+        "config": {"workload": cfg, "baseline_config": "configs[3]" if cfg.startswith("cfg4") else cfg,
+                   "sigma": SIGMA, "nev": nev, "m": m, "n": P.n, "nnz": P.nnz, "flops_lu_real": flu,
+                   "nnz_l_stored": st["nnz_l"], "max_front": st["max_front"], "nfronts": st["nfronts"],
+                   "parallelism": f"replicas x{ws}",
+                   "l2": "flushed (256 MiB scrub) before every timed step"},
         "factor_frac_fp64": round(value / ws / (FP64_PEAK_TFLOPS * 1e3), 5),
-        "time_to_nev_ms": round(min(t_nev), 3), "time_to_nev_runs_ms": [round(t, 2) for t in t_nev],
+        "iga_companion": companion,
+        "time_to_nev_ms": round(min(rest), 3), "time_to_nev_first_call_ms": round(first, 3),
+        "time_to_nev_runs_ms": [round(t, 2) for t in t_nev],
+        "time_to_nev_note": "factor + Krylov-Schur to nev converged pairs on the device-resident operator; "
+                            "the first call also allocates the Krylov workspace and captures the cycle graphs",
         "eigs_residual_max": resid_max,
         "eigs": {k: info.get(k) for k in ("restarts", "guard_passes", "n_fb", "n_mv", "n_vv",
                                           "launches", "restart_defect")},
-        "kernels": {
-            "factor_profile_ms": {KINDS[i]: round(float(ms_k[i]), 4) for i in range(7)},
-            "trisolve": {"ms": round(t_solve, 5), "gbs": round(solve_bytes / t_solve / 1e6, 1),
-                         "frac_hbm": round(solve_bytes / t_solve / 1e6 / hbm, 4)},
-            "spmv_fused_cm": {"ms": round(t_spmv, 5), "gbs": round(spmv_bytes / t_spmv / 1e6, 1),
-                              "frac_hbm": round(spmv_bytes / t_spmv / 1e6 / hbm, 4)},
-            "cgs_gemv_t": {"ms": round(t_gemv, 5), "k": m, "gbs": round(gemv_bytes / t_gemv / 1e6, 1),
-                           "frac_hbm": round(gemv_bytes / t_gemv / 1e6 / hbm, 4)},
-        },
+        "kernels": kernels,
         "roofline": roof,
-        "large_config": large,
         "cpu_baseline": cpu,
         "e2e": {"value": round(ws * flu / (e2e_ms * 1e6), 3), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * P.nnz, "d2h_bytes_per_step": 16,
-                "time_to_nev_ms_from_host": round(e2e_nev_ms, 3)},
+                "note": "rq_factor_refactor from pinned host Q(sigma) values: H2D + factor + D2H of flags",
+                "time_to_nev_ms_from_host": None if e2e_nev_ms is None else round(e2e_nev_ms, 3)},
         "gpu_launches": int(launches * args.steps),
         "clocks": clk.summary(),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def spawn_replicas(args):
+    """`--gpus N` without a launcher: re-run under torch.distributed.run."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -420,17 +475,19 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg2_riga", choices=sorted(NEV))
+    ap.add_argument("--config", default="cfg4_riga", choices=sorted(NEV))
     ap.add_argument("--nev", type=int, default=0)
     ap.add_argument("--nev-runs", type=int, default=3)
     ap.add_argument("--max-restarts", type=int, default=1000)
-    ap.add_argument("--cpu-sample-s", type=float, default=10.0)
-    ap.add_argument("--nev-cpu", type=int, default=1)
-    ap.add_argument("--large", default="cfg4_riga",
-                    help="secondary large config for the large-front / HBM roofline section ('' to skip)")
+    ap.add_argument("--cpu-samples", type=int, default=1)
+    ap.add_argument("--cpu-step-split", type=int, default=1)
+    ap.add_argument("--companion", type=int, default=1)
+    ap.add_argument("--ref-budget-s", type=float, default=150.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_replicas(args))
     if args.impl == "reference":
         run_reference(args)
     else:

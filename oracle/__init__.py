@@ -48,6 +48,16 @@ def _bind(lib):
     s("oracle_eig_solve_quadratic", C.c_int, vp, C.c_int, C.c_int, C.c_double, C.c_uint64,
       C.c_int, C.c_int, f64p, f64p, vp, i32p, f64p)
     s("oracle_eig_destroy", None, vp)
+    s("oracle_eig_create2", C.c_int, vp, C.c_int64, i64p, i32p, f64p, f64p, f64p, i32p, C.c_int,
+      C.c_int, C.c_double, C.c_int, C.POINTER(vp))
+    s("oracle_eig_varsigma", C.c_double, vp)
+    s("oracle_scale_pencil", C.c_int, C.c_int64, i64p, i32p, f64p, f64p, f64p, C.POINTER(C.c_double))
+    s("oracle_symbolic_fronts", C.c_int, vp, C.POINTER(C.c_int32), vp, vp)
+    s("oracle_eig_step_profile", C.c_int, vp, C.c_int, C.c_int, C.c_uint64, f64p)
+    s("oracle_symbolic_create", C.c_int, C.c_int64, i64p, i32p, i32p, C.c_int, C.c_int, C.POINTER(vp))
+    s("oracle_symbolic_destroy", None, vp)
+    s("oracle_factor_numeric", C.c_int, vp, C.c_int64, i64p, i32p, f64p, C.POINTER(vp),
+      C.POINTER(C.c_int64), C.POINTER(C.c_double))
     s("oracle_kern_spmv", None, C.c_int64, i64p, i32p, f64p, f64p, f64p)
     s("oracle_kern_dotc", None, f64p, f64p, C.c_int64, f64p)
     s("oracle_kern_elim", C.c_uint64, f64p, C.c_int64, f64p, f64p, C.c_int64, C.c_int64)
@@ -139,18 +149,69 @@ def symbolic(pencil, leaf=64, kind="port"):
             "struct_nnz_l": snnz.value}
 
 
+class Symbolic:
+    """Oracle symbolic analysis (ND ordering + elimination-tree fronts) as a
+    handle, reused by numeric factorizations (Factor(..., symbolic=S))."""
+
+    def __init__(self, n, rowptr, col, box, elems, leaf=64, kind="port"):
+        self.lib = lib_for(kind)
+        self.n = n
+        self.h = vp()
+        _chk(self.lib, self.lib.oracle_symbolic_create(
+            n, np.ascontiguousarray(rowptr, np.int64), np.ascontiguousarray(col, np.int32),
+            np.ascontiguousarray(np.asarray(box).ravel(), np.int32), elems, leaf, C.byref(self.h)))
+
+    def fronts(self):
+        """(npiv, nf) per front, postorder."""
+        k = C.c_int32()
+        _chk(self.lib, self.lib.oracle_symbolic_fronts(self.h, C.byref(k), None, None))
+        npiv, nf = np.zeros(k.value, np.int32), np.zeros(k.value, np.int32)
+        _chk(self.lib, self.lib.oracle_symbolic_fronts(self.h, C.byref(k), npiv.ctypes.data_as(vp),
+                                                       nf.ctypes.data_as(vp)))
+        return npiv, nf
+
+    def flops_lu(self):
+        """F_LU = sum_f sum_{k<npiv} (nf-k-1) + 2 (nf-k-1)^2 (real flops)."""
+        npiv, nf = self.fronts()
+        tot = 0.0
+        for p, n in zip(npiv.tolist(), nf.tolist()):
+            r = np.arange(n - 1, n - 1 - p, -1, dtype=np.float64)
+            tot += float(np.sum(r + 2 * r * r))
+        return tot
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.oracle_symbolic_destroy(self.h)
+            self.h = None
+
+
+def scale_pencil(n, rowptr, col, K, C_, M, kind="port"):
+    """scale_pencil: (varsigma, varsigma C, varsigma^2 M)."""
+    lib = lib_for(kind)
+    c, m = cplx(C_), cplx(M)
+    vs = C.c_double()
+    _chk(lib, lib.oracle_scale_pencil(n, np.ascontiguousarray(rowptr, np.int64), np.ascontiguousarray(col, np.int32),
+                                      cplx(K), c, m, C.byref(vs)))
+    return vs.value, uncplx(c), uncplx(m)
+
+
 class Factor:
     """Oracle multifrontal LU (complex, reference elim_step inner loop)."""
 
-    def __init__(self, n, rowptr, col, values, box, elems, leaf=64, kind="port"):
+    def __init__(self, n, rowptr, col, values, box=None, elems=None, leaf=64, kind="port", symbolic=None):
         self.lib = lib_for(kind)
         self.n = n
         self.h = vp()
         sw, macs = C.c_int64(), C.c_double()
-        _chk(self.lib, self.lib.oracle_factor_create(
-            n, np.ascontiguousarray(rowptr, np.int64), np.ascontiguousarray(col, np.int32),
-            cplx(values), np.ascontiguousarray(np.asarray(box).ravel(), np.int32), elems, leaf,
-            C.byref(self.h), C.byref(sw), C.byref(macs)))
+        if symbolic is not None:
+            _chk(self.lib, self.lib.oracle_factor_numeric(
+                symbolic.h, n, np.ascontiguousarray(rowptr, np.int64), np.ascontiguousarray(col, np.int32),
+                cplx(values), C.byref(self.h), C.byref(sw), C.byref(macs)))
+        else:
+            _chk(self.lib, self.lib.oracle_factor_create(
+                n, np.ascontiguousarray(rowptr, np.int64), np.ascontiguousarray(col, np.int32),
+                cplx(values), np.ascontiguousarray(np.asarray(box).ravel(), np.int32), elems, leaf,
+                C.byref(self.h), C.byref(sw), C.byref(macs)))
         self.swaps, self.fa_macs = sw.value, macs.value
 
     def solve(self, b):
@@ -175,23 +236,32 @@ class Factor:
 class Eig:
     """Oracle quadratic eigensolver (complex Krylov-Schur, CGS2, guard)."""
 
-    def __init__(self, pencil, sigma, leaf=64, kind="port", K=None, C_=None, M=None):
+    def __init__(self, pencil, sigma, leaf=64, kind="port", K=None, C_=None, M=None, scaling=False,
+                 symbolic=None):
         self.lib = lib_for(kind)
         self.n = pencil.n
         self.h = vp()
         K = pencil.K if K is None else K
         C_ = pencil.C if C_ is None else C_
         M = pencil.M if M is None else M
-        _chk(self.lib, self.lib.oracle_eig_create(
-            pencil.n, pencil.rowptr, pencil.col, cplx(K), cplx(C_), cplx(M),
-            np.ascontiguousarray(pencil.box.ravel(), np.int32), pencil.elems, leaf, float(sigma),
-            C.byref(self.h)))
+        _chk(self.lib, self.lib.oracle_eig_create2(
+            None if symbolic is None else symbolic.h, pencil.n, np.ascontiguousarray(pencil.rowptr, np.int64),
+            np.ascontiguousarray(pencil.col, np.int32), cplx(K), cplx(C_), cplx(M),
+            np.ascontiguousarray(np.asarray(pencil.box).ravel(), np.int32), pencil.elems, leaf, float(sigma),
+            int(bool(scaling)), C.byref(self.h)))
         self.factor_ms = self.lib.oracle_eig_factor_ms(self.h)
+        self.varsigma = self.lib.oracle_eig_varsigma(self.h)
 
     def apply(self, v):
         r = np.zeros(4 * self.n)
         _chk(self.lib, self.lib.oracle_eig_apply(self.h, cplx(v), r))
         return uncplx(r)
+
+    def step_profile(self, j0, nsteps, seed=0):
+        """ms in {spmv, solve, cgs2, other} over Arnoldi steps j0..j0+nsteps-1."""
+        out = np.zeros(4)
+        _chk(self.lib, self.lib.oracle_eig_step_profile(self.h, j0, nsteps, seed, out))
+        return dict(zip(("spmv", "solve", "cgs2", "other"), out.tolist()))
 
     def solve_quadratic(self, nev, m=0, tol=1e-10, seed=0, max_restarts=100, guard=1,
                         vectors=False):

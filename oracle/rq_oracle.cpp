@@ -113,8 +113,17 @@ struct Csr {
 };
 
 // rq::spmv / dot / axpy (sparse.cpp:59-72): ledger-charging wrappers
+// Row chunks of kern::spmv_csr in parallel: each row's sum is the kernel's
+// own sequential accumulation, so y is bit-identical for any thread count.
 void spmv(const Csr& A, const cd* x, cd* y, Ledger* L) {
-  k_spmv(A.n, A.rp.data(), A.col.data(), A.val.data(), x, y);
+  const int64_t n = A.n, chunk = 4096;
+  if (omp_get_max_threads() == 1 || n < 2 * chunk) {
+    k_spmv(n, A.rp.data(), A.col.data(), A.val.data(), x, y);
+  } else {
+#pragma omp parallel for schedule(static)
+    for (int64_t r0 = 0; r0 < n; r0 += chunk)
+      k_spmv(std::min(chunk, n - r0), A.rp.data() + r0, A.col.data(), A.val.data(), x, y + r0);
+  }
   if (L) L->add(MV, static_cast<double>(A.rp[A.n]));
 }
 cd dot(const cd* x, const cd* y, size_t n, Ledger* L) {
@@ -124,6 +133,26 @@ cd dot(const cd* x, const cd* y, size_t n, Ledger* L) {
 void axpy(cd a, const cd* x, cd* y, size_t n, Ledger* L) {
   if (L) L->add(VV, n);
   k_axpy(a, x, y, n);
+}
+// CGS projections over a basis: h_i = dot(V_i, w) for i < k (one kern::dotc
+// per basis vector, vectors in parallel), then r -= sum_i h_i V_i as k
+// kern::axpy calls in basis order over row chunks in parallel. Same
+// arithmetic per entry as the sequential loops; charges k vv ops each.
+void dots(const std::vector<std::vector<cd>>& V, int k, const cd* w, size_t n, cd* h, Ledger* L) {
+#pragma omp parallel for schedule(dynamic, 1) if (k > 1)
+  for (int i = 0; i < k; ++i) h[i] = k_dotc(V[i].data(), w, n);
+  if (L)
+    for (int i = 0; i < k; ++i) L->add(VV, n);
+}
+void axpys(const std::vector<std::vector<cd>>& V, int k, const cd* h, cd* r, size_t n, double sign, Ledger* L) {
+  const size_t chunk = 8192;
+#pragma omp parallel for schedule(static) if (n > 2 * chunk)
+  for (size_t r0 = 0; r0 < n; r0 += chunk) {
+    const size_t len = std::min(chunk, n - r0);
+    for (int i = 0; i < k; ++i) k_axpy(sign * h[i], V[i].data() + r0, r + r0, len);
+  }
+  if (L)
+    for (int i = 0; i < k; ++i) L->add(VV, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -431,7 +460,18 @@ Factor lu_factorize(const Symbolic& S, const Csr& A, Ledger* L) {
   return R;
 }
 
-// solve_factored: permute, L solve, U solve (original order)
+// solve_factored: permute, L solve, U solve (original order).
+// Row-oriented traversal of the stored L\U (contiguous rows): each y entry
+// receives its updates in the same (ascending pivot) order as the
+// column-oriented substitution, so the result is the same bit for bit; the
+// contribution rows of a front are independent and run in parallel.
+// a * b for finite operands: the value std::complex's operator* returns
+// (re = ac - bd, im = ad + bc, no contraction) without the __muldc3
+// inf/nan-recovery call
+inline cd cmul(cd a, cd b) {
+  return {a.real() * b.real() - a.imag() * b.imag(), a.real() * b.imag() + a.imag() * b.real()};
+}
+
 void solve_factored(const Factor& R, const cd* b, cd* x, Ledger* L) {
   const Symbolic& S = *R.S;
   const int nn = static_cast<int>(R.fr.size());
@@ -445,9 +485,21 @@ void solve_factored(const Factor& R, const cd* b, cd* x, Ledger* L) {
       const int p = Fr.ipiv[k];
       if (p != k) std::swap(y[Fr.rows[k]], y[Fr.rows[p]]);
     }
-    for (int k = 0; k < np; ++k) {
-      const cd yk = y[Fr.rows[k]];
-      for (int i = k + 1; i < nf; ++i) y[Fr.rows[i]] -= Fr.lu(i, k) * yk;
+    for (int i = 1; i < np; ++i) {
+      cd s = y[Fr.rows[i]];
+      for (int k = 0; k < i; ++k) s -= cmul(Fr.lu(i, k), y[Fr.rows[k]]);
+      y[Fr.rows[i]] = s;
+    }
+    auto cb_row = [&](int i) {
+      cd s = y[Fr.rows[i]];
+      for (int k = 0; k < np; ++k) s -= cmul(Fr.lu(i, k), y[Fr.rows[k]]);
+      y[Fr.rows[i]] = s;
+    };
+    if (static_cast<int64_t>(nf - np) * np > (1 << 16) && omp_get_max_threads() > 1) {
+#pragma omp parallel for schedule(static)
+      for (int i = np; i < nf; ++i) cb_row(i);
+    } else {
+      for (int i = np; i < nf; ++i) cb_row(i);
     }
   }
   // backward, reverse postorder
@@ -456,7 +508,7 @@ void solve_factored(const Factor& R, const cd* b, cd* x, Ledger* L) {
     const int nf = Fr.nf, np = Fr.npiv;
     for (int k = np - 1; k >= 0; --k) {
       cd s = y[Fr.rows[k]];
-      for (int c = k + 1; c < nf; ++c) s -= Fr.lu(k, c) * y[Fr.rows[c]];
+      for (int c = k + 1; c < nf; ++c) s -= cmul(Fr.lu(k, c), y[Fr.rows[c]]);
       y[Fr.rows[k]] = s / Fr.lu(k, k);
     }
   }
@@ -635,8 +687,8 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
     for (int pass = 0; pass < 2 && nlock > 0; ++pass) {
       op.bvec(r.data(), w.data(), L);
       std::vector<cd> h(nlock);
-      for (int i = 0; i < nlock; ++i) h[i] = dot(V[i].data(), w.data(), n2, L);
-      for (int i = 0; i < nlock; ++i) axpy(-h[i], V[i].data(), r.data(), n2, L);
+      dots(V, nlock, w.data(), n2, h.data(), L);
+      axpys(V, nlock, h.data(), r.data(), n2, -1.0, L);
     }
     op.bvec(r.data(), w.data(), L);
     const double b = std::sqrt(std::max(0.0, dot(r.data(), w.data(), n2, L).real()));
@@ -655,8 +707,8 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
       for (int pass = 0; pass < 2; ++pass) {  // CGS2
         op.bvec(r.data(), w.data(), L);
         std::vector<cd> h(j + 1);
-        for (int i = 0; i <= j; ++i) h[i] = dot(V[i].data(), w.data(), n2, L);
-        for (int i = 0; i <= j; ++i) axpy(-h[i], V[i].data(), r.data(), n2, L);
+        dots(V, j + 1, w.data(), n2, h.data(), L);
+        axpys(V, j + 1, h.data(), r.data(), n2, -1.0, L);
         for (int i = 0; i <= j; ++i) H(i, j) += h[i];
       }
       op.bvec(r.data(), w.data(), L);
@@ -708,7 +760,7 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
         std::vector<cd> y(m, 0.0), x(n2, 0.0);
         for (int row = 0; row < m; ++row)
           for (int t = 0; t <= i; ++t) y[row] += Z(row, t) * Y(t, i);
-        for (int t = 0; t < m; ++t) axpy(y[t], V[t].data(), x.data(), n2, nullptr);
+        axpys(V, m, y.data(), x.data(), n2, 1.0, nullptr);
         const bool low = std::abs(lam[i]) > 1.0;  // larger-norm block
         std::vector<cd> u(x.begin() + (low ? n : 0), x.begin() + (low ? n2 : n));
         // explicit pencil residual
@@ -759,6 +811,7 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
     std::vector<int> s2 = sel;
     schur_move_front(T, Z, s2);
     // V <- V Z[:, :p]; H <- [T_p; b^T]
+#pragma omp parallel for schedule(dynamic, 1)
     for (int c = 0; c < p; ++c) {
       std::fill(V2[c].begin(), V2[c].end(), cd{});
       for (int t = 0; t < m; ++t) k_axpy(Z(t, c), V[t].data(), V2[c].data(), n2);
@@ -782,6 +835,80 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
   out.nconv = 0;
   for (double x : out.res) out.nconv += x <= tol;
   return out;
+}
+
+// Per-category timing of Arnoldi steps j0 .. j0+nsteps-1 (SURVEY.md §8(d)
+// d4: the CPU path's per-cycle split). The basis is filled with seeded
+// uniform vectors: the work per step (operator application, two CGS passes
+// over j+1 vectors with their B-products, B-norm) equals a real step's, only
+// the values differ. out[0..3] = ms in {SpMV, triangular solves, CGS2
+// dot/axpy, other vector work}.
+void step_profile(Operator& op, int j0, int nsteps, uint64_t seed, double* out) {
+  using clk = std::chrono::steady_clock;
+  auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const int64_t n = op.n, n2 = 2 * n;
+  std::vector<std::vector<cd>> V(j0 + nsteps + 1, std::vector<cd>(n2));
+  uint64_t st = seed;
+  for (auto& v : V)
+    for (auto& x : v) x = uni(st);
+  std::vector<cd> r(n2), w(n2), t1(n), t2(n);
+  double tsp = 0, tso = 0, tcg = 0, tot = 0;
+  for (int j = j0; j < j0 + nsteps; ++j) {
+    const cd* v = V[j].data();
+    auto a = clk::now();
+    spmv(op.P->C, v, t1.data(), nullptr);
+    spmv(op.P->M, v, t2.data(), nullptr);
+    auto b = clk::now();
+    axpy(op.s, t2.data(), t1.data(), n, nullptr);
+    auto c = clk::now();
+    spmv(op.P->M, v + n, t2.data(), nullptr);
+    auto d = clk::now();
+    axpy(1.0, t2.data(), t1.data(), n, nullptr);
+    auto e = clk::now();
+    solve_factored(*op.F, t1.data(), r.data(), nullptr);
+    auto f = clk::now();
+    k_scal(-1.0, r.data(), n);
+    for (int64_t i = 0; i < n; ++i) r[n + i] = v[i];
+    axpy(op.s, r.data(), r.data() + n, n, nullptr);
+    auto g = clk::now();
+    tsp += ms(a, b) + ms(c, d);
+    tot += ms(b, c) + ms(d, e) + ms(f, g);
+    tso += ms(e, f);
+    std::vector<cd> h(j + 1);
+    for (int pass = 0; pass < 2; ++pass) {
+      a = clk::now();
+      op.bvec(r.data(), w.data(), nullptr);
+      b = clk::now();
+      dots(V, j + 1, w.data(), n2, h.data(), nullptr);
+      axpys(V, j + 1, h.data(), r.data(), n2, -1.0, nullptr);
+      c = clk::now();
+      tsp += ms(a, b);
+      tcg += ms(b, c);
+    }
+    a = clk::now();
+    op.bvec(r.data(), w.data(), nullptr);
+    b = clk::now();
+    const double beta = std::sqrt(std::max(0.0, k_dotc(r.data(), w.data(), n2).real()));
+    for (int64_t i = 0; i < n2; ++i) V[j + 1][i] = r[i] / beta;
+    c = clk::now();
+    tsp += ms(a, b);
+    tcg += ms(b, c);
+  }
+  out[0] = tsp, out[1] = tso, out[2] = tcg, out[3] = tot;
+}
+
+// scale_pencil: varsigma = sqrt(maxabs K /
+// maxabs M); the scaled pencil is (K, varsigma C,
+// varsigma^2 M), whose eigenvalues are gamma = lambda / varsigma. Zero M -> errc 6.
+double scale_pencil(Pencil& P) {
+  double mk = 0, mm = 0;
+  for (const cd& v : P.K.val) mk = std::max(mk, std::abs(v));
+  for (const cd& v : P.M.val) mm = std::max(mm, std::abs(v));
+  if (!(mm > 0)) throw OracleError{6, "scale_pencil: zero M norm"};
+  const double s = std::sqrt(mk / mm), s2 = s * s;
+  for (cd& v : P.C.val) v *= s;
+  for (cd& v : P.M.val) v *= s2;
+  return s;
 }
 
 }  // namespace oracle
@@ -814,13 +941,14 @@ oracle::Csr make_csr(int64_t n, const int64_t* rp, const int32_t* col, const dou
   return A;
 }
 struct OracleFactor {
-  oracle::Symbolic S;
+  std::shared_ptr<oracle::Symbolic> S;
   oracle::Csr A;
   oracle::Factor F;
 };
 struct OracleEig {
-  oracle::Symbolic S;
-  oracle::Pencil P;
+  std::shared_ptr<oracle::Symbolic> S;
+  oracle::Pencil P;  // the (possibly scaled) pencil the Krylov iteration sees
+  double varsigma = 1.0;
   oracle::Csr Q;
   oracle::Factor F;
   oracle::Ledger L;
@@ -869,8 +997,35 @@ int oracle_factor_create(int64_t n, const int64_t* rp, const int32_t* col, const
   return guarded([&] {
     auto h = std::make_unique<OracleFactor>();
     h->A = make_csr(n, rp, col, val_c);
-    h->S = oracle::symbolic(n, rp, col, box, elems, leaf);
-    h->F = oracle::lu_factorize(h->S, h->A, nullptr);
+    h->S = std::make_shared<oracle::Symbolic>(oracle::symbolic(n, rp, col, box, elems, leaf));
+    h->F = oracle::lu_factorize(*h->S, h->A, nullptr);
+    if (swaps) *swaps = h->F.swaps;
+    if (fa_macs) *fa_macs = h->F.fa_macs;
+    *out = h.release();
+  });
+}
+
+// Symbolic analysis kept as a handle, so a timed numeric factorization
+// (bench.py --impl reference) excludes the ordering / elimination tree.
+int oracle_symbolic_create(int64_t n, const int64_t* rp, const int32_t* col, const int32_t* box, int elems,
+                           int leaf, void** out) {
+  return guarded([&] {
+    *out = new std::shared_ptr<oracle::Symbolic>(
+        std::make_shared<oracle::Symbolic>(oracle::symbolic(n, rp, col, box, elems, leaf)));
+  });
+}
+void oracle_symbolic_destroy(void* s) { delete static_cast<std::shared_ptr<oracle::Symbolic>*>(s); }
+
+// Numeric multifrontal LU of A on a symbolic handle (the values' pattern must
+// be the one the symbolic analysis saw).
+int oracle_factor_numeric(void* sym, int64_t n, const int64_t* rp, const int32_t* col, const double* val_c,
+                          void** out, int64_t* swaps, double* fa_macs) {
+  return guarded([&] {
+    auto h = std::make_unique<OracleFactor>();
+    h->S = *static_cast<std::shared_ptr<oracle::Symbolic>*>(sym);
+    if (h->S->n != n) throw oracle::OracleError{7, "symbolic / matrix dimension mismatch"};
+    h->A = make_csr(n, rp, col, val_c);
+    h->F = oracle::lu_factorize(*h->S, h->A, nullptr);
     if (swaps) *swaps = h->F.swaps;
     if (fa_macs) *fa_macs = h->F.fa_macs;
     *out = h.release();
@@ -903,30 +1058,72 @@ int oracle_factor_front(void* h, int f, double* dense_c, int32_t* ipiv, int32_t*
 void oracle_factor_destroy(void* h) { delete static_cast<OracleFactor*>(h); }
 
 // Quadratic eigensolve. K, C, M real or complex interleaved; sigma real.
-int oracle_eig_create(int64_t n, const int64_t* rp, const int32_t* col, const double* K_c,
-                      const double* C_c, const double* M_c, const int32_t* box, int elems, int leaf,
-                      double sigma, void** out) {
+// Quadratic eigensolve. K, C, M real or complex interleaved; sigma real.
+// sym: an oracle_symbolic_create handle (NULL: analyse here from box/elems).
+int oracle_eig_create2(void* sym, int64_t n, const int64_t* rp, const int32_t* col, const double* K_c,
+                       const double* C_c, const double* M_c, const int32_t* box, int elems, int leaf,
+                       double sigma, int scaling, void** out) {
   return guarded([&] {
     auto h = std::make_unique<OracleEig>();
     h->P.K = make_csr(n, rp, col, K_c);
     h->P.C = make_csr(n, rp, col, C_c);
     h->P.M = make_csr(n, rp, col, M_c);
+    if (scaling) h->varsigma = oracle::scale_pencil(h->P);
+    const double s = sigma / h->varsigma;  // the shift in the scaled variable gamma
     h->P.nK = oracle::norm1(h->P.K);
     h->P.nC = oracle::norm1(h->P.C);
     h->P.nM = oracle::norm1(h->P.M);
     h->Q = h->P.K;
     for (size_t k = 0; k < h->Q.val.size(); ++k)
-      h->Q.val[k] = h->P.K.val[k] + sigma * h->P.C.val[k] + sigma * sigma * h->P.M.val[k];
-    h->S = oracle::symbolic(n, rp, col, box, elems, leaf);
+      h->Q.val[k] = h->P.K.val[k] + s * h->P.C.val[k] + s * s * h->P.M.val[k];
+    if (sym) {
+      h->S = *static_cast<std::shared_ptr<oracle::Symbolic>*>(sym);
+      if (h->S->n != n) throw oracle::OracleError{7, "symbolic / pencil dimension mismatch"};
+    } else {
+      h->S = std::make_shared<oracle::Symbolic>(oracle::symbolic(n, rp, col, box, elems, leaf));
+    }
     const auto t0 = std::chrono::steady_clock::now();
-    h->F = oracle::lu_factorize(h->S, h->Q, &h->L);
+    h->F = oracle::lu_factorize(*h->S, h->Q, &h->L);
     h->t_factor_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     h->op = std::make_unique<oracle::Operator>();
     h->op->P = &h->P;
     h->op->F = &h->F;
-    h->op->s = sigma;
+    h->op->s = s;
     h->op->n = n;
     *out = h.release();
+  });
+}
+
+int oracle_eig_create(int64_t n, const int64_t* rp, const int32_t* col, const double* K_c, const double* C_c,
+                      const double* M_c, const int32_t* box, int elems, int leaf, double sigma, void** out) {
+  return oracle_eig_create2(nullptr, n, rp, col, K_c, C_c, M_c, box, elems, leaf, sigma, 0, out);
+}
+
+// scale_pencil on its own: C, M (complex interleaved) scaled in place.
+int oracle_scale_pencil(int64_t n, const int64_t* rp, const int32_t* col, const double* K_c, double* C_c,
+                        double* M_c, double* varsigma) {
+  return guarded([&] {
+    oracle::Pencil P;
+    P.K = make_csr(n, rp, col, K_c);
+    P.C = make_csr(n, rp, col, C_c);
+    P.M = make_csr(n, rp, col, M_c);
+    *varsigma = oracle::scale_pencil(P);
+    std::memcpy(C_c, P.C.val.data(), sizeof(cd) * P.C.val.size());
+    std::memcpy(M_c, P.M.val.data(), sizeof(cd) * P.M.val.size());
+  });
+}
+
+double oracle_eig_varsigma(void* h) { return static_cast<OracleEig*>(h)->varsigma; }
+
+// Front sizes of a symbolic handle (postorder): npiv, nf (either may be NULL).
+int oracle_symbolic_fronts(void* sym, int32_t* nfronts, int32_t* npiv, int32_t* nf) {
+  return guarded([&] {
+    const oracle::Symbolic& S = **static_cast<std::shared_ptr<oracle::Symbolic>*>(sym);
+    *nfronts = static_cast<int32_t>(S.node_rows.size());
+    for (size_t f = 0; f < S.node_rows.size(); ++f) {
+      if (npiv) npiv[f] = S.node_npiv[f];
+      if (nf) nf[f] = static_cast<int32_t>(S.node_rows[f].size());
+    }
   });
 }
 
@@ -947,8 +1144,8 @@ int oracle_eig_solve_quadratic(void* h, int nev, int m, double tol, uint64_t see
     const oracle::EigOut o = oracle::solve_quadratic(*E->op, nev, m > 0 ? m : 2 * nev + 1, tol, seed,
                                                      max_restarts, guard, &E->L);
     for (int i = 0; i < nev && i < static_cast<int>(o.lam.size()); ++i) {
-      lam_c[2 * i] = o.lam[i].real();
-      lam_c[2 * i + 1] = o.lam[i].imag();
+      lam_c[2 * i] = o.lam[i].real() * E->varsigma;  // lambda = varsigma gamma
+      lam_c[2 * i + 1] = o.lam[i].imag() * E->varsigma;
       res[i] = o.res[i];
       if (vec_c && !o.vec[i].empty())
         std::memcpy(vec_c + 2 * i * E->op->n, o.vec[i].data(), sizeof(cd) * E->op->n);
@@ -961,6 +1158,10 @@ int oracle_eig_solve_quadratic(void* h, int nev, int m, double tol, uint64_t see
 }
 
 void oracle_eig_destroy(void* h) { delete static_cast<OracleEig*>(h); }
+
+int oracle_eig_step_profile(void* h, int j0, int nsteps, uint64_t seed, double* out) {
+  return guarded([&] { oracle::step_profile(*static_cast<OracleEig*>(h)->op, j0, nsteps, seed, out); });
+}
 
 // Raw kern:: entry points (for checking the restated kernels against the
 // reference build and the product's SpMV).

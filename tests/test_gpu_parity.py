@@ -246,6 +246,27 @@ def test_scaling_does_not_change_spectrum(cfg1):
     assert np.max(np.abs(la - lb) / np.abs(la)) <= 1e-6
 
 
+def test_scale_pencil_vs_oracle():
+    """scale_pencil: the product's varsigma equals the
+    oracle's bit for bit, and the scaled solve's eigenvalues match the oracle's
+    scaled solve (perturbed damping: a non-degenerate spectrum)."""
+    P = rq.assemble(rq.DIV, 2, 8, 0)
+    diag = np.array([P.rowptr[i] + np.searchsorted(P.col[P.rowptr[i]:P.rowptr[i + 1]], i) for i in range(P.n)])
+    P.C = P.C.copy()
+    P.C[diag] += 0.5 * np.random.default_rng(9).random(P.n) * P.M[diag]
+    op = rq.build_operator(P, SIGMA, scaling=True)
+    vs, Cs, Ms = oracle.scale_pencil(P.n, P.rowptr, P.col, P.K, P.C, P.M)
+    assert op.varsigma == vs and vs != 1.0
+    assert np.max(np.abs(Ms.real - vs * vs * P.M)) == 0.0
+    pairs = op.solve_quadratic(6, eps=1e-10, max_restarts=400)
+    E = oracle.Eig(P, SIGMA, C_=P.C, scaling=True)
+    assert E.varsigma == vs
+    lo, ro = E.solve_quadratic(6, tol=1e-10, max_restarts=400)
+    lam = sorted_lams([p.lam for p in pairs])
+    assert np.max(np.abs(lam - sorted_lams(lo)) / np.abs(lo)) <= 1e-8
+    assert max(p.residual for p in pairs) <= 1e-10 and np.max(ro) <= 1e-10
+
+
 # --------------------------------------------------------------------------- larger sizes
 @pytest.mark.parametrize("name", ["cfg3_riga", "cfg3_iga"])
 def test_cfg3_solve_residual_and_cluster(name):

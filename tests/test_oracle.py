@@ -190,3 +190,23 @@ def test_oracle_cluster_closed_form(cfg1):
     assert np.all(np.minimum(np.abs(lam - ref), np.abs(lam - np.conj(ref))) <= 1e-8)
     assert np.sum(lam.imag > 0) == 5 and np.all(res <= 1e-10)
     assert E.ledger["fa"]["ops"] == 1
+
+
+def test_scale_pencil_known_answer():
+    """SPEC.md:406: K = 4I, C = M = I -> varsigma = 2, scaled pencil (4I, 2I, 4I);
+    roots of 4 + 2 gamma + 4 gamma^2 are those of 4 + lambda + lambda^2 over 2."""
+    n = 3
+    rp = np.arange(n + 1, dtype=np.int64)
+    col = np.arange(n, dtype=np.int32)
+    vs, Cs, Ms = oracle.scale_pencil(n, rp, col, 4 * np.ones(n), np.ones(n), np.ones(n))
+    assert vs == 2.0
+    assert np.array_equal(Cs, 2 * np.ones(n)) and np.array_equal(Ms, 4 * np.ones(n))
+    g = np.sort_complex(np.roots([4, 2, 4]))
+    lam = np.sort_complex(np.roots([1, 1, 4]))
+    assert np.allclose(2 * g, lam, rtol=1e-14)
+    # equal norms -> varsigma = 1, pencil unchanged (SPEC.md:405)
+    vs1, C1, M1 = oracle.scale_pencil(n, rp, col, np.ones(n), 3 * np.ones(n), np.ones(n))
+    assert vs1 == 1.0 and np.array_equal(C1, 3 * np.ones(n))
+    with pytest.raises(oracle.OracleError) as e:  # zero M
+        oracle.scale_pencil(n, rp, col, np.ones(n), np.ones(n), np.zeros(n))
+    assert e.value.code == 6
