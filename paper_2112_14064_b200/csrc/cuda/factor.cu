@@ -41,6 +41,14 @@ namespace rqb {
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     fail(errc::config, std::string("CUDA error: ") + cudaGetErrorString(e) + " in " + what);
+  // RQB_CHECK_LAST=1 (debugging): a pending launch error is reported at the
+  // first checked call after it
+  static const bool check_last = std::getenv("RQB_CHECK_LAST") != nullptr;
+  if (check_last) {
+    const cudaError_t p = cudaPeekAtLastError();
+    if (p != cudaSuccess)
+      fail(errc::config, std::string("CUDA error (pending): ") + cudaGetErrorString(p) + " seen at " + what);
+  }
 }
 
 static double wall_ms() {

@@ -1341,7 +1341,7 @@ void rqb_dag_build(FactorEngine& fe) {
   auto kern = P->occ == 2 ? factor_dag_kernel<2> : factor_dag_kernel<1>;
   RQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)));
   int nsm = 148, occ = 1;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
+  RQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device));
   RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDT, P->smem));
   P->grid = std::max(1, std::min(P->ntasks, nsm * std::max(1, occ)));
   P->d_small_backup.alloc(sizeof(double) * P->grid * P->small_nf * kPB);
@@ -1390,7 +1390,7 @@ void rqb_dag_bench_updcb(FactorEngine& fe, int front, int reps, double* out) {
   auto kern = updcb_bench_kernel<2>;
   RQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.smem)));
   int nsm = 148, occ = 1;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
+  RQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device));
   RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDT, P.smem));
   const int grid = std::max(1, std::min(n * n, nsm * std::max(1, occ)));
   kern<<<grid, kDT, P.smem, fe.stream>>>(fe.d_pool.as<double>(), fe.d_fronts.as<FrontDev>(), front, D.acb, D.tiles);

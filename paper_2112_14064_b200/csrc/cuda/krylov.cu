@@ -17,7 +17,6 @@
 #include <cstring>
 #include <vector>
 
-#include <cublas_v2.h>
 
 #include "device.cuh"
 
@@ -484,20 +483,13 @@ void OperatorEngine::init_workspaces() {
   gemv_t_blocks = static_cast<int>((2 * n + gemv_t_chunk - 1) / gemv_t_chunk);
   d_part.alloc(sizeof(double) * std::max(kRedBlocks, gemv_t_blocks) * 512);
   d_scal.alloc(sizeof(double) * 64);
-  {
-    cublasHandle_t h = nullptr;
-    if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) fail(errc::config, "cublasCreate failed");
-    blas = h;
-    cublasSetStream(h, stream);
-  }
   RQB_CUDA(cudaStreamSynchronize(stream));
-  tr.mark("alloc+cublas");
+  tr.mark("alloc");
   fac->factor();
   tr.mark("factor");
 }
 
 OperatorEngine::~OperatorEngine() {
-  if (blas) cublasDestroy(static_cast<cublasHandle_t>(blas));
 }
 
 void OperatorEngine::spmv(int which, const double* x, double* y) {
@@ -594,13 +586,9 @@ void OperatorEngine::bnorm_normalize(const double* r, const double* w, double* b
 void OperatorEngine::combine(const double* V, int k, const double* Q_dev, int ldq, int ncols,
                              double* Vout) {
   if (ncols <= 0 || k <= 0) return;
-  // Vout (2n x ncols) = V (2n x k, basis vectors contiguous) * Q (k x ncols):
-  // a plain DGEMM (FP64 tensor cores), arithmetic intensity ~ncols/4 flop/byte
-  const double one = 1.0, zero = 0.0;
+  // Vout (2n x ncols, column-major) = V (2n x k, basis vectors contiguous) * Q (k x ncols)
   const int64_t n2 = 2 * n;
-  if (cublasDgemm(static_cast<cublasHandle_t>(blas), CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(n2), ncols, k, &one,
-                  V, static_cast<int>(n2), Q_dev, ldq, &zero, Vout, static_cast<int>(n2)) != CUBLAS_STATUS_SUCCESS)
-    fail(errc::solver, "cublasDgemm (Krylov-Schur combine) failed");
+  vq_gemm(V, n2, n2, k, Q_dev, ldq, ncols, Vout, n2, false, stream);
   ++launches;
 }
 
@@ -610,11 +598,8 @@ void OperatorEngine::ritz_residuals(const double* V, int m, const double* Y, int
   if (nc <= 0) return;
   const int64_t n2 = 2 * n;
   const int ldx = 2 * nc;
-  // Xrm (2nc x 2n, column-major == 2n x 2nc row-major) = Y^T V^T
-  const double one = 1.0, zero = 0.0;
-  if (cublasDgemm(static_cast<cublasHandle_t>(blas), CUBLAS_OP_T, CUBLAS_OP_T, ldx, static_cast<int>(n2), m, &one, Y,
-                  m, V, static_cast<int>(n2), &zero, Xrm, ldx) != CUBLAS_STATUS_SUCCESS)
-    fail(errc::solver, "cublasDgemm (Ritz vectors) failed");
+  // Xrm (2n x 2nc, row-major) = V (2n x m) Y (m x 2nc)
+  vq_gemm(V, n2, n2, m, Y, m, ldx, Xrm, ldx, true, stream);
   if (d_rcand.bytes < sizeof(double) * 2 * nc + sizeof(int) * nc) d_rcand.alloc(sizeof(double) * 2 * nc + sizeof(int) * nc);
   const int nbx = kRedBlocks;
   if (d_rpart.bytes < sizeof(double) * 2 * nc * nbx) d_rpart.alloc(sizeof(double) * 2 * nc * nbx);

@@ -1178,11 +1178,11 @@ void rqb_solve_prepare(FactorEngine& fe) {
     fe.sweep_occ = items >= 10000 ? 3 : 2;
     if (const char* e = std::getenv("RQB_SWEEP_OCC")) fe.sweep_occ = std::atoi(e) >= 3 ? 3 : 2;
     int nsm = 148, occ = 1;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
+    RQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device));
     if (fe.sweep_occ == 3)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_sweep<3>, kST, 0);
+      RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_sweep<3>, kST, 0));
     else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_sweep<2>, kST, 0);
+      RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fwd_sweep<2>, kST, 0));
     fe.solve_grid = std::max(1, nsm * std::max(1, occ));
   }
   // whole-front items only on levels wide enough to keep every CTA busy
@@ -1323,8 +1323,8 @@ void rqb_rowperm_enqueue(FactorEngine& fe) {
                                           fe.d_rowperm.as<int32_t>(), fe.d_gsrc.as<int4>());
   if (fe.n_dblk > 0) {
     int nsm = 148, occ = 1;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, diag_inverse, kInvT, 0);
+    RQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device));
+    RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, diag_inverse, kInvT, 0));
     const int grid = std::min(2 * fe.n_dblk, nsm * std::max(1, occ));
     diag_inverse<<<grid, kInvT, 0, fe.stream>>>(fe.d_dblk.as<DiagBlk>(), fe.n_dblk, fe.d_pool.as<double>(),
                                                fe.d_dinv.as<double>());

@@ -159,6 +159,10 @@ void rqb_dag_enqueue(FactorEngine& fe);
 void rqb_dag_profile(FactorEngine& fe, double* out);
 void rqb_dag_bench_updcb(FactorEngine& fe, int front, int reps, double* out);
 void rqb_rowperm_enqueue(FactorEngine& fe);
+// X = V Q on FP64 tensor cores (csrc/cuda/gemm.cu): V n2 x k (vector j at
+// V + j ldv), Q k x c column-major, X column-major (ldx >= n2) or row-major.
+void vq_gemm(const double* V, int64_t ldv, int64_t n2, int k, const double* Q, int ldq, int c, double* X,
+             int64_t ldx, bool row_major_out, cudaStream_t stream);
 std::string rqb_dag_stall_report(FactorEngine& fe);
 
 // Device-resident pencil (device assembly): CSR pattern and
@@ -188,7 +192,6 @@ struct OperatorEngine {
   int64_t nparts = 0;
   int64_t gemv_t_chunk = 256;  // CGS projection: entries per block, blocks
   int gemv_t_blocks = 1;
-  void* blas = nullptr;  // cublasHandle_t on `stream` (restart / Ritz-vector DGEMMs)
 
   OperatorEngine(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
                  const double* C, const double* M, const Symbolic& s, double sigma,
