@@ -389,9 +389,7 @@ Pencil assemble_pencil_device(const VectorSpace& vs, double alpha, double beta, 
   const size_t budget = 160 * 1024;
   const int rows = static_cast<int>(std::max<size_t>(1, std::min<size_t>(nq, budget / line)));
   const size_t smem = (size_t((rows * nq + 1) & ~1) + size_t(rows) * nq * A.nloc * 2) * sizeof(double);
-  if (smem > 48 * 1024)
-    RQB_CUDA(cudaFuncSetAttribute(asm_element, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+  if (smem > 48 * 1024) smem_at_least(asm_element, smem);
   const int threads = A.ntri >= 512 ? 256 : 128;
   asm_element<<<static_cast<unsigned>(nel), threads, smem, st>>>(A, rows);
   RQB_CUDA(cudaGetLastError());

@@ -18,6 +18,18 @@ constexpr double kSingularTiny = 1e-300;
 
 #define RQB_CUDA(x) ::rqb::cuda_check((x), #x)
 
+// Dynamic shared memory limit of a kernel, raised (never lowered) to `bytes`.
+// The limit is per-function process state: another engine with a smaller plan
+// must not lower it under a launch configured earlier, so every launch site
+// calls this right before launching.
+template <class Kernel>
+inline void smem_at_least(Kernel kern, size_t bytes) {
+  cudaFuncAttributes a{};
+  RQB_CUDA(cudaFuncGetAttributes(&a, kern));
+  if (static_cast<size_t>(a.maxDynamicSharedSizeBytes) < bytes)
+    RQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+}
+
 __device__ __forceinline__ void warp_argmax(double& v, int& i) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

@@ -1339,7 +1339,7 @@ void rqb_dag_build(FactorEngine& fe) {
   const size_t diag_smem = sizeof(double) * (3 * 32 * 33 + 128);
   P->smem = std::max({small_smem, tile_smem, rows_smem, diag_smem, size_t(16 * 1024)});
   auto kern = P->occ == 2 ? factor_dag_kernel<2> : factor_dag_kernel<1>;
-  RQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)));
+  smem_at_least(kern, P->smem);
   int nsm = 148, occ = 1;
   RQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device));
   RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDT, P->smem));
@@ -1388,7 +1388,7 @@ void rqb_dag_bench_updcb(FactorEngine& fe, int front, int reps, double* out) {
   const FrontDag& D = P.dag_h[front];
   const int n = D.tiles - D.acb;
   auto kern = updcb_bench_kernel<2>;
-  RQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.smem)));
+  smem_at_least(kern, P.smem);
   int nsm = 148, occ = 1;
   RQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device));
   RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kDT, P.smem));
@@ -1455,6 +1455,7 @@ void rqb_dag_enqueue(FactorEngine& fe) {
     }
   }
   A.small_nf = P.small_nf;
+  smem_at_least(P.occ == 2 ? factor_dag_kernel<2> : factor_dag_kernel<1>, P.smem);
   if (P.occ == 2)
     factor_dag_kernel<2><<<P.grid, kDT, P.smem, fe.stream>>>(A);
   else

@@ -179,7 +179,7 @@ void vq_gemm(const double* V, int64_t ldv, int64_t n2, int k, const double* Q, i
     return;
   }
   auto kern = row_major_out ? vq_gemm_k<true> : vq_gemm_k<false>;
-  RQB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem)));
+  smem_at_least(kern, kSmem);
   const int64_t blocks = (n2 + kBM - 1) / kBM * ((c + kBN - 1) / kBN);
   if (blocks > 2147483647LL) fail(errc::config, "vq_gemm: too many blocks");
   const dim3 grid(static_cast<unsigned>(blocks));
