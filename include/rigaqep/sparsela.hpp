@@ -5,8 +5,8 @@
 // implemented inline on top of the B200 C-ABI (include/rq_b200.h). A reference
 // build adds this directory to its include path and links librq_b200.so
 // (INTEGRATION.md). The GPU path is real FP64: complex matrices fail with
-// errc::config (no CPU fallback); complex right-hand sides are solved as two
-// real solves.
+// errc::config (no CPU fallback); a complex right-hand side is solved as two
+// real solves and charged as the one solve the reference performs.
 #pragma once
 
 #include <cstdint>
@@ -32,10 +32,48 @@ struct Ordering {
   std::vector<std::int32_t> perm;  // perm[new] = old (free DOFs)
   std::string method = "geometric-nested-dissection";
   std::shared_ptr<rq_symbolic_t> sym;
+  long n() const { return static_cast<long>(perm.size()); }
 };
 
+namespace b200 {
+inline Ordering ordering_from_boxes(std::int64_t n, const std::vector<std::int32_t>& box, int elems, int leaf,
+                                    const char* method) {
+  rq_symbolic_t* s = nullptr;
+  check(rq_nd_order(n, box.data(), elems, leaf, &s));
+  Ordering o;
+  o.sym.reset(s, rq_symbolic_destroy);
+  o.perm.resize(n);
+  o.method = method;
+  check(rq_symbolic_perm(s, o.perm.data()));
+  return o;
+}
+/// sum over fronts and pivots of (nf - k - 1)^2: the factorization's
+/// multiply-adds counted from the structure
+inline double fa_macs(const Ordering& o) {
+  rq_symbolic_stats st{};
+  check(rq_symbolic_stats_get(o.sym.get(), &st));
+  std::vector<std::int32_t> np(st.nfronts), nf(st.nfronts);
+  check(rq_symbolic_fronts(o.sym.get(), nullptr, np.data(), nf.data(), nullptr, nullptr));
+  double m = 0;
+  for (std::size_t f = 0; f < np.size(); ++f)
+    for (int k = 0; k < np[f]; ++k) m += static_cast<double>(nf[f] - k - 1) * (nf[f] - k - 1);
+  return m;
+}
+/// per real solve: sum np^2 + 2 np (nf - np) (the stored L and U entries read)
+inline double fb_macs(const Ordering& o) {
+  rq_symbolic_stats st{};
+  check(rq_symbolic_stats_get(o.sym.get(), &st));
+  std::vector<std::int32_t> np(st.nfronts), nf(st.nfronts);
+  check(rq_symbolic_fronts(o.sym.get(), nullptr, np.data(), nf.data(), nullptr, nullptr));
+  double m = 0;
+  for (std::size_t f = 0; f < np.size(); ++f) m += double(np[f]) * np[f] + 2.0 * np[f] * (nf[f] - np[f]);
+  return m;
+}
+}  // namespace b200
+
 /// nested_dissection_order(space): geometric ND over the
-/// support boxes of the free DOFs (constrained = sorted eliminated DOF ids).
+/// support boxes of the free DOFs (constrained = sorted eliminated DOF ids,
+/// boundary_mask). Errors: none beyond the reference space's own.
 inline Ordering nested_dissection_order(const VectorSpace& vs, const std::vector<long>& constrained,
                                         int leaf = 64) {
   std::vector<std::int32_t> box;
@@ -54,22 +92,26 @@ inline Ordering nested_dissection_order(const VectorSpace& vs, const std::vector
         box.push_back(comp[c]->sy.support_first_elem(j));
         box.push_back(comp[c]->sy.support_last_elem(j));
       }
-  const std::int64_t n = static_cast<std::int64_t>(box.size() / 4);
-  rq_symbolic_t* s = nullptr;
-  b200::check(rq_nd_order(n, box.data(), vs.elems, leaf, &s));
-  Ordering o;
-  o.sym.reset(s, rq_symbolic_destroy);
-  o.perm.resize(n);
-  b200::check(rq_symbolic_perm(s, o.perm.data()));
-  return o;
+  return b200::ordering_from_boxes(static_cast<std::int64_t>(box.size() / 4), box, vs.elems, leaf,
+                                   "geometric-nested-dissection");
 }
 
-/// Factorization: immutable, device resident, shareable.
+/// The "natural" Ordering of SPEC.md:110 (one dense front): for small
+/// matrices without a space (SPEC's hand examples).
+inline Ordering natural_order(long n) {
+  return b200::ordering_from_boxes(n, std::vector<std::int32_t>(4 * static_cast<std::size_t>(n), 0), 1,
+                                   static_cast<int>(n), "natural");
+}
+
+/// Factorization: immutable and device resident. Concurrent
+/// solves on one factorization are safe: the library serialises
+/// the calls that share its stream and solve buffers.
 struct Factorization {
   std::shared_ptr<rq_factor_t> f;
   long n = 0;
   std::int64_t nnz_l = 0, nnz_u = 0;
   double flops = 0;
+  double fb_macs = 0;
 };
 
 inline std::vector<double> real_values(const SparseMatrix& a) {
@@ -79,8 +121,9 @@ inline std::vector<double> real_values(const SparseMatrix& a) {
   return v;
 }
 
-/// lu_factorize: one fa operation charged to the ledger.
+/// lu_factorize: fa += the structural multiply-add count.
 inline Factorization lu_factorize(const SparseMatrix& A, const Ordering& ord, CostLedger* ledger) {
+  if (A.n != ord.n()) fail(errc::dimension, "lu_factorize: matrix and ordering sizes differ");
   const std::vector<double> v = real_values(A);
   rq_factor_t* f = nullptr;
   b200::check(rq_factor_create(ord.sym.get(), A.n, A.rowptr.data(), A.col.data(), v.data(), &f));
@@ -92,20 +135,27 @@ inline Factorization lu_factorize(const SparseMatrix& A, const Ordering& ord, Co
   F.nnz_l = st.nnz_l;
   F.nnz_u = st.nnz_u;
   F.flops = st.flops_lu;
-  if (ledger) ledger->add_fa(static_cast<std::uint64_t>(st.flops_lu / 2));
+  F.fb_macs = b200::fb_macs(ord);
+  if (ledger) ledger->add_fa(static_cast<std::uint64_t>(b200::fa_macs(ord)));
   return F;
 }
 
-/// solve_factored: fb += nnz(L) + nnz(U) per real solve.
+/// solve_factored: x = A^{-1} rhs; fb += one solve.
 inline std::vector<cdouble> solve_factored(const Factorization& F, const std::vector<cdouble>& rhs,
                                            CostLedger* ledger) {
   if (static_cast<long>(rhs.size()) != F.n) fail(errc::dimension, "solve_factored dimension mismatch");
-  std::vector<double> b(2 * F.n), x(2 * F.n);
-  for (long i = 0; i < F.n; ++i) b[i] = rhs[i].real(), b[F.n + i] = rhs[i].imag();
-  b200::check(rq_factor_solve(F.f.get(), b.data(), x.data(), 2));
+  bool cplx = false;
+  for (const cdouble& z : rhs) cplx = cplx || z.imag() != 0.0;
+  const int nr = cplx ? 2 : 1;
+  std::vector<double> b(nr * F.n), x(nr * F.n);
+  for (long i = 0; i < F.n; ++i) {
+    b[i] = rhs[i].real();
+    if (cplx) b[F.n + i] = rhs[i].imag();
+  }
+  b200::check(rq_factor_solve(F.f.get(), b.data(), x.data(), nr));
   std::vector<cdouble> out(F.n);
-  for (long i = 0; i < F.n; ++i) out[i] = {x[i], x[F.n + i]};
-  if (ledger) ledger->add_fb(static_cast<std::uint64_t>(F.nnz_l + F.nnz_u));
+  for (long i = 0; i < F.n; ++i) out[i] = {x[i], cplx ? x[F.n + i] : 0.0};
+  if (ledger) ledger->add_fb(static_cast<std::uint64_t>(F.fb_macs));
   return out;
 }
 

@@ -256,6 +256,41 @@ int rq_eigs_run(rq_operator_t* op, const rq_eigs_opts* opts, double* lam_re, dou
                 double* resid, double* vec_re, double* vec_im, rq_eigs_info* info);
 /* CostLedger::to_json-compatible snapshot (sparse.cpp:80-97) of the last run. */
 int rq_eigs_ledger_json(const rq_operator_t* op, char* buf, size_t len);
+/* The operator's cumulative CostLedger (reference sparse.hpp:57-103): every
+ * operation since creation (build_operator's factorization: fa 1) or the last
+ * reset. Charges follow the reference operations one for one:
+ * apply_operator fb 1 + mv 3 + vv 3; b_inner mv 1 + vv 1; spmv mv 1; an Arnoldi
+ * step apply + 3 B-products + (4(j+1)+1) 2n-vector dots/axpys; a residual check
+ * per candidate; a restart per V Q. out: double[12] = {ops, macs} x {fa, fb,
+ * mv, vv, residual_check, restart}. */
+int rq_operator_ledger(const rq_operator_t* op, double* out);
+int rq_operator_ledger_json(const rq_operator_t* op, char* buf, size_t len);
+int rq_operator_ledger_reset(rq_operator_t* op);
+
+/* scale_pencil: varsigma = sqrt(maxabs K /
+ * maxabs M); the scaled pencil is (K, varsigma C, varsigma^2 M) with
+ * eigenvalues gamma = lambda / varsigma. Cs, Ms (nnz, nullable) receive the
+ * scaled values. Zero M -> RQ_E_DOMAIN. Host only. */
+int rq_scale_pencil(int64_t nnz, const double* K, const double* C, const double* M, double* varsigma,
+                    double* Cs, double* Ms);
+/* ritz_extract: H (m+1) x m column-major (real, from
+ * rq_operator_arnoldi or a restart), shift sigma and scaling varsigma of the
+ * operator. For the m Ritz pairs in wanted order (nearest the shift first,
+ * conjugate pairs adjacent, +imag first): theta (double[2m], re/im), lambda =
+ * sigma + varsigma / theta (double[2m]), residual estimate |beta e_m^H y|
+ * (double[m]) and y (m x m complex column-major, interleaved re/im: double[2m^2],
+ * unit 2-norm). Any output may be NULL. QR non-convergence -> RQ_E_SOLVER.
+ * Host only. */
+int rq_ritz_extract(const double* H, int m, double sigma, double varsigma, double* theta, double* lam, double* est,
+                    double* Y);
+/* krylov_schur_restart: from an m-step decomposition
+ * S V_m = V_m H_m + beta v_{m+1} e_m^T (V: (m+1) x 2n row-major host, H: (m+1) x m
+ * column-major host), keep the `keep` wanted Ritz directions (closed under
+ * conjugation; real orthonormal basis of their Schur vectors). On return
+ * V[0..p] = {V_m Q_p, v_{m+1}} (V_m Q_p on the device, DMMA) and H holds
+ * [T_p; b_p^T] in its leading (p+1) x p block, so S V_p = V_p T_p +
+ * v_{p+1} b_p^T. keep >= m: identity restart (p = m). *p_out = p. */
+int rq_operator_krylov_schur_restart(rq_operator_t* op, int m, int keep, double* V, double* H, int* p_out);
 
 /* ------------------------------------------------------------------------ */
 /* Wire formats (reference sparse.cpp:121-174,         */

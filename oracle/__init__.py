@@ -53,6 +53,10 @@ def _bind(lib):
     s("oracle_eig_varsigma", C.c_double, vp)
     s("oracle_scale_pencil", C.c_int, C.c_int64, i64p, i32p, f64p, f64p, f64p, C.POINTER(C.c_double))
     s("oracle_symbolic_fronts", C.c_int, vp, C.POINTER(C.c_int32), vp, vp)
+    s("oracle_eig_b_inner", C.c_int, vp, f64p, f64p, f64p)
+    s("oracle_eig_arnoldi", C.c_int, vp, f64p, C.c_int, vp, vp)
+    s("oracle_eig_ledger", None, vp, f64p)
+    s("oracle_eig_ledger_reset", None, vp)
     s("oracle_eig_step_profile", C.c_int, vp, C.c_int, C.c_int, C.c_uint64, f64p)
     s("oracle_symbolic_create", C.c_int, C.c_int64, i64p, i32p, i32p, C.c_int, C.c_int, C.POINTER(vp))
     s("oracle_symbolic_destroy", None, vp)
@@ -256,6 +260,30 @@ class Eig:
         r = np.zeros(4 * self.n)
         _chk(self.lib, self.lib.oracle_eig_apply(self.h, cplx(v), r))
         return uncplx(r)
+
+    LEDGER = ("fa", "fb", "mv", "vv", "residual_check", "restart")
+
+    def ledger_counts(self):
+        """Cumulative CostLedger counters of this operator: {cat: (ops, macs)}."""
+        out = np.zeros(12)
+        self.lib.oracle_eig_ledger(self.h, out)
+        return {nm: (int(out[2 * i]), float(out[2 * i + 1])) for i, nm in enumerate(self.LEDGER)}
+
+    def ledger_reset(self):
+        self.lib.oracle_eig_ledger_reset(self.h)
+
+    def b_inner(self, x, y):
+        out = np.zeros(2)
+        _chk(self.lib, self.lib.oracle_eig_b_inner(self.h, cplx(x), cplx(y), out))
+        return out[0] + 1j * out[1]
+
+    def arnoldi(self, v1, m):
+        """(V (m+1) x 2n, H (m+1) x m) of arnoldi_run from v1."""
+        n2 = 2 * self.n
+        V = np.zeros(2 * (m + 1) * n2)
+        H = np.zeros(2 * (m + 1) * m)
+        _chk(self.lib, self.lib.oracle_eig_arnoldi(self.h, cplx(v1), m, V.ctypes.data_as(vp), H.ctypes.data_as(vp)))
+        return uncplx(V).reshape(m + 1, n2), uncplx(H).reshape(m, m + 1).T
 
     def step_profile(self, j0, nsteps, seed=0):
         """ms in {spmv, solve, cgs2, other} over Arnoldi steps j0..j0+nsteps-1."""

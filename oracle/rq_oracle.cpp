@@ -456,7 +456,16 @@ Factor lu_factorize(const Symbolic& S, const Csr& A, Ledger* L) {
     R.fb_macs += np * np + 2.0 * np * (nf - np);
   }
   R.fa_macs = static_cast<double>(macs);
-  if (L) L->add(FA, R.fa_macs);
+  // the ledger counts multiply-adds analytically from the front structure
+  // (SPEC.md:376): sum over pivots of (nf-k-1)^2, the dense rank-1 updates
+  // (R.fa_macs is the kernel-returned count, which skips zero multipliers)
+  double fa = 0;
+  for (int f = 0; f < nn; ++f)
+    for (int k = 0; k < R.fr[f].npiv; ++k) {
+      const double r = R.fr[f].nf - k - 1.0;
+      fa += r * r;
+    }
+  if (L) L->add(FA, fa);
   return R;
 }
 
@@ -673,6 +682,41 @@ struct EigOut {
   bool ok = false;
 };
 
+// Arnoldi steps j = k .. m-1 (Alg. 2 lines 7-13)
+// with CGS2: r = S v_j; twice {w = B r; h = V_j^H w; r -= V_j h};
+// h_{j+1,j} = ||r||_B, v_{j+1} = r / h_{j+1,j}. H accumulates both passes.
+void arnoldi_steps(Operator& op, std::vector<std::vector<cd>>& V, DM& H, int k, int m, std::vector<cd>& r,
+                   std::vector<cd>& w, Ledger* L) {
+  const int64_t n2 = 2 * op.n;
+  for (int j = k; j < m; ++j) {
+    op.apply(V[j].data(), r.data(), L);
+    for (int pass = 0; pass < 2; ++pass) {  // CGS2
+      op.bvec(r.data(), w.data(), L);
+      std::vector<cd> h(j + 1);
+      dots(V, j + 1, w.data(), n2, h.data(), L);
+      axpys(V, j + 1, h.data(), r.data(), n2, -1.0, L);
+      for (int i = 0; i <= j; ++i) H(i, j) += h[i];
+    }
+    op.bvec(r.data(), w.data(), L);
+    const double b = std::sqrt(std::max(0.0, dot(r.data(), w.data(), n2, L).real()));
+    H(j + 1, j) = b;
+    for (int64_t i = 0; i < n2; ++i) V[j + 1][i] = r[i] / b;
+  }
+}
+
+// arnoldi_run: v1 B-normalised (one B-product, one dot),
+// then m steps. V: m+1 vectors of 2n; H: (m+1) x m.
+void arnoldi_run(Operator& op, const cd* v1, int m, std::vector<std::vector<cd>>& V, DM& H, Ledger* L) {
+  const int64_t n2 = 2 * op.n;
+  V.assign(m + 1, std::vector<cd>(n2));
+  H = DM(m + 1);
+  std::vector<cd> r(v1, v1 + n2), w(n2);
+  op.bvec(r.data(), w.data(), L);
+  const double b = std::sqrt(std::max(0.0, dot(r.data(), w.data(), n2, L).real()));
+  for (int64_t i = 0; i < n2; ++i) V[0][i] = r[i] / b;
+  arnoldi_steps(op, V, H, 0, m, r, w, L);
+}
+
 EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, int max_restarts,
                        int guard_on, Ledger* L) {
   const int64_t n = op.n, n2 = 2 * n;
@@ -702,20 +746,7 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
   while (pass_cycles < max_restarts) {
     ++cycles;
     ++pass_cycles;
-    for (int j = k; j < m; ++j) {
-      op.apply(V[j].data(), r.data(), L);
-      for (int pass = 0; pass < 2; ++pass) {  // CGS2
-        op.bvec(r.data(), w.data(), L);
-        std::vector<cd> h(j + 1);
-        dots(V, j + 1, w.data(), n2, h.data(), L);
-        axpys(V, j + 1, h.data(), r.data(), n2, -1.0, L);
-        for (int i = 0; i <= j; ++i) H(i, j) += h[i];
-      }
-      op.bvec(r.data(), w.data(), L);
-      const double b = std::sqrt(std::max(0.0, dot(r.data(), w.data(), n2, L).real()));
-      H(j + 1, j) = b;
-      for (int64_t i = 0; i < n2; ++i) V[j + 1][i] = r[i] / b;
-    }
+    arnoldi_steps(op, V, H, k, m, r, w, L);
     DM T(m), Z;
     for (int j = 0; j < m; ++j)
       for (int i = 0; i < m; ++i) T(i, j) = H(i, j);
@@ -1132,9 +1163,48 @@ double oracle_eig_factor_ms(void* h) { return static_cast<OracleEig*>(h)->t_fact
 int oracle_eig_apply(void* h, const double* v_c, double* r_c) {
   return guarded([&] {
     auto* E = static_cast<OracleEig*>(h);
-    E->op->apply(reinterpret_cast<const cd*>(v_c), reinterpret_cast<cd*>(r_c), nullptr);
+    E->op->apply(reinterpret_cast<const cd*>(v_c), reinterpret_cast<cd*>(r_c), &E->L);
   });
 }
+
+// b_inner: x_u^H y_u + x_l^H M y_l (one B-product, one dot)
+int oracle_eig_b_inner(void* h, const double* x_c, const double* y_c, double* out_c) {
+  return guarded([&] {
+    auto* E = static_cast<OracleEig*>(h);
+    const int64_t n2 = 2 * E->op->n;
+    std::vector<cd> w(n2);
+    E->op->bvec(reinterpret_cast<const cd*>(y_c), w.data(), &E->L);
+    const cd r = oracle::dot(reinterpret_cast<const cd*>(x_c), w.data(), n2, &E->L);
+    out_c[0] = r.real();
+    out_c[1] = r.imag();
+  });
+}
+
+// arnoldi_run: V (m+1) x 2n row-major, H (m+1) x m column-major (complex).
+int oracle_eig_arnoldi(void* h, const double* v1_c, int m, double* V_c, double* H_c) {
+  return guarded([&] {
+    auto* E = static_cast<OracleEig*>(h);
+    std::vector<std::vector<cd>> V;
+    oracle::DM H(m + 1);
+    oracle::arnoldi_run(*E->op, reinterpret_cast<const cd*>(v1_c), m, V, H, &E->L);
+    const int64_t n2 = 2 * E->op->n;
+    if (V_c)
+      for (int j = 0; j <= m; ++j) std::memcpy(V_c + 2 * j * n2, V[j].data(), sizeof(cd) * n2);
+    if (H_c)
+      for (int j = 0; j < m; ++j)
+        for (int i = 0; i <= m; ++i) {
+          H_c[2 * (i + j * (m + 1))] = H(i, j).real();
+          H_c[2 * (i + j * (m + 1)) + 1] = H(i, j).imag();
+        }
+  });
+}
+
+// CostLedger counters (sparse.hpp:57-103): {ops, macs} x {fa, fb, mv, vv, check, restart}
+void oracle_eig_ledger(void* h, double* out) {
+  const auto* E = static_cast<OracleEig*>(h);
+  for (int c = 0; c < 6; ++c) out[2 * c] = static_cast<double>(E->L.ops[c]), out[2 * c + 1] = E->L.macs[c];
+}
+void oracle_eig_ledger_reset(void* h) { static_cast<OracleEig*>(h)->L = oracle::Ledger{}; }
 
 int oracle_eig_solve_quadratic(void* h, int nev, int m, double tol, uint64_t seed, int max_restarts,
                                int guard, double* lam_c, double* res, double* vec_c, int32_t* stats,

@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -88,6 +89,11 @@ struct DagPlanDeleter {
 };
 
 struct FactorEngine {
+  // one stream and one set of solve buffers per engine: the C-ABI entry points
+  // that enqueue on them hold this lock from the first enqueue to the last
+  // synchronisation, so concurrent solves on one factorization
+  // are safe (serialised)
+  std::mutex mu;
   // factorization schedule: persistent task-DAG kernel (default) or the
   // level-synchronous multi-launch path (RQB_FACTOR=level, kept for A/B runs)
   bool use_dag = true;

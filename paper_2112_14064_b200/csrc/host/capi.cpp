@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 
 #include <cuda_runtime_api.h>
@@ -15,6 +16,7 @@
 #include "common.hpp"
 #include "io.hpp"
 #include "eigs.hpp"
+#include "dense.hpp"
 
 struct rq_pencil {
   rqb::Pencil P;
@@ -35,7 +37,8 @@ struct rq_operator {
   std::unique_ptr<rqb::OperatorEngine> op;
   double norms1[3] = {0, 0, 0};
   rq_factor fac_view;
-  rqb::Ledger ledger;
+  rqb::Ledger ledger;  // the last rq_eigs_run
+  rqb::Ledger cum;     // every operation on this operator since creation / reset
   rqb::DeviceBuffer d_a, d_b;
 };
 
@@ -267,6 +270,7 @@ int rq_factor_refactor(rq_factor_t* f, const double* aval) {
   return guarded([&] {
     need(f, "factor");
     need(aval, "aval");
+    std::lock_guard<std::mutex> lock(f->fe->mu);
     f->fe->set_values(aval);
     f->fe->factor();
   });
@@ -288,6 +292,7 @@ int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs) {
     need(f, "factor");
     need(b, "b");
     need(x, "x");
+    std::lock_guard<std::mutex> lock(f->fe->mu);
     rqb::FactorEngine& fe = *f->fe;
     const int64_t n = fe.n;
     if (f->d_b.bytes < sizeof(double) * n) f->d_b.alloc(sizeof(double) * n);
@@ -329,6 +334,7 @@ int rq_factor_profile(rq_factor_t* f, double* ms, int64_t* launches, double* wor
     need(ms, "ms");
     need(launches, "launches");
     need(work, "work");
+    std::lock_guard<std::mutex> lock(f->fe->mu);
     f->fe->profile(ms, launches, work);
   });
 }
@@ -337,6 +343,7 @@ int rq_factor_dag_profile(rq_factor_t* f, double* out) {
   return guarded([&] {
     need(f, "factor");
     need(out, "out");
+    std::lock_guard<std::mutex> lock(f->fe->mu);
     rqb::rqb_dag_profile(*f->fe, out);
   });
 }
@@ -345,6 +352,7 @@ int rq_factor_bench_updcb(rq_factor_t* f, int front, int reps, double* out) {
   return guarded([&] {
     need(f, "factor");
     need(out, "out");
+    std::lock_guard<std::mutex> lock(f->fe->mu);
     rqb::rqb_dag_bench_updcb(*f->fe, front, reps, out);
   });
 }
@@ -353,6 +361,7 @@ void rq_factor_destroy(rq_factor_t* f) { delete f; }
 
 namespace {
 void finish_operator(rq_operator* o) {
+  rqb::charge_factor(o->cum, *o->op);  // build_operator: N_fa = 1
   o->fac_view.fe = o->op->fac.get();
   o->d_a.alloc(sizeof(double) * 2 * o->op->n);
   o->d_b.alloc(sizeof(double) * 2 * o->op->n);
@@ -417,6 +426,7 @@ int rq_operator_time(rq_operator_t* o, int what, int iters, int param, double* m
   return guarded([&] {
     need(o, "op");
     need(ms_per_call, "ms");
+    std::lock_guard<std::mutex> lock(o->op->fac->mu);
     if (iters < 1) rqb::fail(rqb::errc::config, "iters must be positive");
     *ms_per_call = o->op->time_op(what, iters, param);
   });
@@ -427,6 +437,7 @@ int rq_operator_apply(rq_operator_t* o, const double* v, double* r) {
     need(o, "op");
     need(v, "v");
     need(r, "r");
+    std::lock_guard<std::mutex> lock(o->op->fac->mu);
     rqb::OperatorEngine& op = *o->op;
     const int64_t n2 = 2 * op.n;
     rqb::cuda_check(cudaMemcpyAsync(o->d_a.p, v, sizeof(double) * n2, cudaMemcpyHostToDevice, op.stream), "H2D");
@@ -434,6 +445,7 @@ int rq_operator_apply(rq_operator_t* o, const double* v, double* r) {
     rqb::cuda_check(cudaMemcpyAsync(r, o->d_b.p, sizeof(double) * n2, cudaMemcpyDeviceToHost, op.stream), "D2H");
     rqb::cuda_check(cudaStreamSynchronize(op.stream), "sync");
     op.fac->check_sweeps();
+    rqb::charge_apply(o->cum, op);
   });
 }
 
@@ -443,6 +455,7 @@ int rq_operator_b_inner(rq_operator_t* o, const double* x, const double* y, doub
     need(x, "x");
     need(y, "y");
     need(out, "out");
+    std::lock_guard<std::mutex> lock(o->op->fac->mu);
     rqb::OperatorEngine& op = *o->op;
     const int64_t n2 = 2 * op.n;
     rqb::DeviceBuffer dw, ds;
@@ -454,6 +467,8 @@ int rq_operator_b_inner(rq_operator_t* o, const double* x, const double* y, doub
     op.dot2n(o->d_a.as<double>(), dw.as<double>(), ds.as<double>());
     rqb::cuda_check(cudaMemcpyAsync(out, ds.p, sizeof(double), cudaMemcpyDeviceToHost, op.stream), "D2H");
     rqb::cuda_check(cudaStreamSynchronize(op.stream), "sync");
+    rqb::charge_bproduct(o->cum, op);  // b_inner
+    rqb::charge_vv2n(o->cum, op, 1);
   });
 }
 
@@ -462,6 +477,7 @@ int rq_operator_spmv(rq_operator_t* o, int which, const double* x, double* y) {
     need(o, "op");
     need(x, "x");
     need(y, "y");
+    std::lock_guard<std::mutex> lock(o->op->fac->mu);
     if (which < 0 || which > 3) rqb::fail(rqb::errc::config, "which must be 0..3");
     rqb::OperatorEngine& op = *o->op;
     const int64_t n = op.n;
@@ -469,6 +485,7 @@ int rq_operator_spmv(rq_operator_t* o, int which, const double* x, double* y) {
     op.spmv(which, o->d_a.as<double>(), o->d_b.as<double>());
     rqb::cuda_check(cudaMemcpyAsync(y, o->d_b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, op.stream), "D2H");
     rqb::cuda_check(cudaStreamSynchronize(op.stream), "sync");
+    rqb::charge_bproduct(o->cum, op);  // rq::spmv: one mv of nnz MACs (sparse.cpp:59-62)
   });
 }
 
@@ -476,6 +493,7 @@ int rq_operator_arnoldi(rq_operator_t* o, const double* v1, int m, double* V, do
   return guarded([&] {
     need(o, "op");
     need(v1, "v1");
+    std::lock_guard<std::mutex> lock(o->op->fac->mu);
     if (m < 1 || m > 512) rqb::fail(rqb::errc::config, "m must be in [1, 512]");
     rqb::OperatorEngine& op = *o->op;
     const int64_t n2 = 2 * op.n;
@@ -508,6 +526,14 @@ int rq_operator_arnoldi(rq_operator_t* o, const double* v1, int m, double* V, do
     if (V)
       rqb::cuda_check(cudaMemcpyAsync(V, dV.p, sizeof(double) * (m + 1) * n2, cudaMemcpyDeviceToHost, op.stream), "D2H");
     rqb::cuda_check(cudaStreamSynchronize(op.stream), "sync");
+    // arnoldi_run: v1 B-normalised, then m steps
+    rqb::charge_bproduct(o->cum, op);
+    rqb::charge_vv2n(o->cum, op, 1);
+    for (int j = 0; j < m; ++j) {
+      rqb::charge_apply(o->cum, op);
+      for (int pass = 0; pass < 3; ++pass) rqb::charge_bproduct(o->cum, op);
+      rqb::charge_vv2n(o->cum, op, 4 * (j + 1) + 1);
+    }
     if (H) {
       std::fill(H, H + (m + 1) * m, 0.0);
       for (int j = 0; j < m; ++j) {
@@ -526,6 +552,7 @@ int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, doub
   const int rc = guarded([&] {
     need(o, "op");
     need(opts, "opts");
+    std::lock_guard<std::mutex> lock(o->op->fac->mu);
     rqb::EigsOptions eo;
     eo.nev = opts->nev;
     eo.m = opts->m;
@@ -537,6 +564,7 @@ int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, doub
     eo.want_vectors = (vec_re && vec_im) ? 1 : 0;
     o->ledger = rqb::Ledger{};
     rqb::EigsResult r = rqb::solve_quadratic_device(*o->op, eo, o->ledger, o->norms1);
+    o->cum.add(o->ledger, false);  // the factorization was charged when the operator was built
     const int nout = static_cast<int>(r.lambda.size());
     for (int i = 0; i < nout && i < opts->nev; ++i) {
       if (lam_re) lam_re[i] = r.lambda[i].real();
@@ -589,6 +617,32 @@ int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, doub
   return 0;
 }
 
+int rq_operator_ledger(const rq_operator_t* o, double* out) {
+  return guarded([&] {
+    need(o, "op");
+    need(out, "out");
+    std::lock_guard<std::mutex> lock(o->op->fac->mu);
+    o->cum.get(out);
+  });
+}
+
+int rq_operator_ledger_json(const rq_operator_t* o, char* buf, size_t len) {
+  return guarded([&] {
+    need(o, "op");
+    need(buf, "buf");
+    const std::string s = o->cum.to_json();
+    if (s.size() + 1 > len) rqb::fail(rqb::errc::dimension, "ledger buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+int rq_operator_ledger_reset(rq_operator_t* o) {
+  return guarded([&] {
+    need(o, "op");
+    o->cum = rqb::Ledger{};
+  });
+}
+
 int rq_eigs_ledger_json(const rq_operator_t* o, char* buf, size_t len) {
   return guarded([&] {
     need(o, "op");
@@ -596,6 +650,172 @@ int rq_eigs_ledger_json(const rq_operator_t* o, char* buf, size_t len) {
     const std::string s = o->ledger.to_json();
     if (s.size() + 1 > len) rqb::fail(rqb::errc::dimension, "buffer too small");
     std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// scale_pencil, ritz_extract, krylov_schur_restart
+
+int rq_scale_pencil(int64_t nnz, const double* K, const double* C, const double* M, double* varsigma,
+                    double* Cs, double* Ms) {
+  return guarded([&] {
+    need(K, "K");
+    need(C, "C");
+    need(M, "M");
+    need(varsigma, "varsigma");
+    double mk = 0, mm = 0;
+    for (int64_t k = 0; k < nnz; ++k) mk = std::max(mk, std::fabs(K[k])), mm = std::max(mm, std::fabs(M[k]));
+    if (!(mm > 0)) rqb::fail(rqb::errc::domain, "scale_pencil: zero M norm");
+    const double v = std::sqrt(mk / mm), v2 = v * v;  // the rule OperatorEngine applies (krylov.cu)
+    *varsigma = v;
+    if (Cs)
+      for (int64_t k = 0; k < nnz; ++k) Cs[k] = v * C[k];
+    if (Ms)
+      for (int64_t k = 0; k < nnz; ++k) Ms[k] = v2 * M[k];
+  });
+}
+
+namespace {
+
+// wanted order: nearest the shift first (|lambda - sigma|), conjugate pairs
+// adjacent with the positive imaginary part first (the order solve_quadratic
+// uses, eigs.cpp)
+std::vector<int> wanted_order(const std::vector<rqb::cplx>& lam, double sigma) {
+  std::vector<int> order(lam.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const double da = std::abs(lam[a] - sigma), db = std::abs(lam[b] - sigma);
+    if (da != db) return da < db;
+    return lam[a].imag() > lam[b].imag();
+  });
+  return order;
+}
+
+struct RitzData {
+  rqb::CMat T, Z, Y;
+  std::vector<rqb::cplx> theta, lam;
+  std::vector<int> order;
+  std::vector<double> Hm;
+  double beta = 0;
+};
+
+RitzData ritz(const double* H, int m, double sigma, double varsigma) {
+  RitzData R;
+  R.Hm.resize(static_cast<size_t>(m) * m);
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < m; ++i) R.Hm[i + static_cast<size_t>(j) * m] = H[i + static_cast<size_t>(j) * (m + 1)];
+  R.beta = H[m + static_cast<size_t>(m - 1) * (m + 1)];
+  if (!rqb::complex_schur(R.Hm, m, R.T, R.Z)) rqb::fail(rqb::errc::solver, "Hessenberg QR did not converge");
+  R.Y = rqb::triangular_eigvecs(R.T);
+  R.theta.resize(m);
+  R.lam.resize(m);
+  for (int i = 0; i < m; ++i) {
+    R.theta[i] = R.T(i, i);
+    R.lam[i] = sigma + varsigma / R.theta[i];  // lambda = varsigma (sigma / varsigma + 1 / theta)
+  }
+  R.order = wanted_order(R.lam, sigma);
+  return R;
+}
+
+}  // namespace
+
+int rq_ritz_extract(const double* H, int m, double sigma, double varsigma, double* theta, double* lam, double* est,
+                    double* Y) {
+  return guarded([&] {
+    need(H, "H");
+    if (m < 1 || m > 512) rqb::fail(rqb::errc::config, "m must be in [1, 512]");
+    if (!(varsigma > 0)) rqb::fail(rqb::errc::config, "varsigma must be positive");
+    const RitzData R = ritz(H, m, sigma, varsigma);
+    for (int a = 0; a < m; ++a) {
+      const int i = R.order[a];
+      // y = Z Y[:, i] (Y upper triangular), unit 2-norm
+      std::vector<rqb::cplx> y(m, 0.0);
+      for (int t = 0; t <= i; ++t)
+        for (int row = 0; row < m; ++row) y[row] += R.Z(row, t) * R.Y(t, i);
+      if (theta) theta[2 * a] = R.theta[i].real(), theta[2 * a + 1] = R.theta[i].imag();
+      if (lam) lam[2 * a] = R.lam[i].real(), lam[2 * a + 1] = R.lam[i].imag();
+      if (est) est[a] = std::abs(R.beta * y[m - 1]);
+      if (Y)
+        for (int row = 0; row < m; ++row) {
+          Y[2 * (row + static_cast<size_t>(a) * m)] = y[row].real();
+          Y[2 * (row + static_cast<size_t>(a) * m) + 1] = y[row].imag();
+        }
+    }
+  });
+}
+
+int rq_operator_krylov_schur_restart(rq_operator_t* o, int m, int keep, double* V, double* H, int* p_out) {
+  return guarded([&] {
+    need(o, "op");
+    need(V, "V");
+    need(H, "H");
+    need(p_out, "p_out");
+    std::lock_guard<std::mutex> lock(o->op->fac->mu);
+    rqb::OperatorEngine& op = *o->op;
+    if (m < 2 || m > 512 || m >= 2 * op.n) rqb::fail(rqb::errc::config, "m must be in [2, min(512, 2n - 1)]");
+    if (keep < 1) rqb::fail(rqb::errc::config, "keep must be positive");
+    if (keep >= m) {  // identity restart
+      *p_out = m;
+      return;
+    }
+    const int64_t n2 = 2 * op.n;
+    const RitzData R = ritz(H, m, op.sigma * op.varsigma, op.varsigma);
+    // the `keep` wanted directions, closed under conjugation
+    std::vector<int> sel(m, 0);
+    int p = 0;
+    for (int a = 0; a < m && p < keep; ++a) {
+      const int i = R.order[a];
+      if (sel[i]) continue;
+      int partner = -1;
+      if (std::abs(R.theta[i].imag()) > 1e-12 * std::abs(R.theta[i])) {
+        double bd = 1e300;
+        for (int q = 0; q < m; ++q)
+          if (q != i && !sel[q] && std::abs(R.theta[q] - std::conj(R.theta[i])) < bd)
+            bd = std::abs(R.theta[q] - std::conj(R.theta[i])), partner = q;
+      }
+      if (p + 1 + (partner >= 0) > m - 1) break;
+      sel[i] = 1, ++p;
+      if (partner >= 0) sel[partner] = 1, ++p;
+    }
+    if (p == 0) rqb::fail(rqb::errc::solver, "krylov_schur_restart: nothing to keep");
+    rqb::CMat Tr = R.T, Zr = R.Z;
+    rqb::schur_reorder(Tr, Zr, sel);
+    std::vector<double> Qp;
+    p = rqb::real_basis(Zr, p, Qp);
+    if (p <= 0) rqb::fail(rqb::errc::solver, "krylov_schur_restart lost its basis");
+    // T_p = Q_p^T H_m Q_p, b_p = beta e_m^T Q_p
+    std::vector<double> Tp(static_cast<size_t>(p) * p, 0.0), HQ(static_cast<size_t>(m) * p, 0.0);
+    for (int c = 0; c < p; ++c)
+      for (int t = 0; t < m; ++t) {
+        const double q = Qp[t + static_cast<size_t>(c) * m];
+        for (int i = 0; i < m; ++i) HQ[i + static_cast<size_t>(c) * m] += R.Hm[i + static_cast<size_t>(t) * m] * q;
+      }
+    for (int c = 0; c < p; ++c)
+      for (int i = 0; i < p; ++i) {
+        double s = 0;
+        for (int t = 0; t < m; ++t) s += Qp[t + static_cast<size_t>(i) * m] * HQ[t + static_cast<size_t>(c) * m];
+        Tp[i + static_cast<size_t>(c) * p] = s;
+      }
+    // V_p = V_m Q_p on the device (vq_gemm); v_{p+1} = v_{m+1}
+    rqb::DeviceBuffer dV, dQ, dX;
+    dV.alloc(sizeof(double) * (m + 1) * n2);
+    dQ.alloc(sizeof(double) * m * p);
+    dX.alloc(sizeof(double) * p * n2);
+    rqb::cuda_check(cudaMemcpyAsync(dV.p, V, sizeof(double) * (m + 1) * n2, cudaMemcpyHostToDevice, op.stream), "H2D V");
+    rqb::cuda_check(cudaMemcpyAsync(dQ.p, Qp.data(), sizeof(double) * m * p, cudaMemcpyHostToDevice, op.stream), "H2D Q");
+    op.combine(dV.as<double>(), m, dQ.as<double>(), m, p, dX.as<double>());
+    rqb::cuda_check(cudaMemcpyAsync(V + static_cast<int64_t>(p) * n2, dV.as<double>() + static_cast<int64_t>(m) * n2,
+                                    sizeof(double) * n2, cudaMemcpyDeviceToHost, op.stream), "D2H v");
+    rqb::cuda_check(cudaMemcpyAsync(V, dX.p, sizeof(double) * p * n2, cudaMemcpyDeviceToHost, op.stream), "D2H V");
+    rqb::cuda_check(cudaStreamSynchronize(op.stream), "sync");
+    std::fill(H, H + static_cast<size_t>(m + 1) * m, 0.0);
+    for (int c = 0; c < p; ++c) {
+      for (int i = 0; i < p; ++i) H[i + static_cast<size_t>(c) * (m + 1)] = Tp[i + static_cast<size_t>(c) * p];
+      H[p + static_cast<size_t>(c) * (m + 1)] = R.beta * Qp[(m - 1) + static_cast<size_t>(c) * m];
+    }
+    *p_out = p;
+    o->cum.n_restart += 1;
+    o->cum.macs_restart += static_cast<double>(m) * p * n2;
   });
 }
 

@@ -69,6 +69,56 @@ std::string Ledger::to_json() const {
   return os.str();
 }
 
+void Ledger::get(double* out) const {
+  const int64_t ops[6] = {n_fa, n_fb, n_mv, n_vv, n_check, n_restart};
+  const double macs[6] = {macs_fa, macs_fb, macs_mv, macs_vv, macs_check, macs_restart};
+  for (int c = 0; c < 6; ++c) out[2 * c] = static_cast<double>(ops[c]), out[2 * c + 1] = macs[c];
+}
+
+void Ledger::add(const Ledger& o, bool with_fa) {
+  if (with_fa) n_fa += o.n_fa, macs_fa += o.macs_fa;
+  n_fb += o.n_fb, macs_fb += o.macs_fb;
+  n_mv += o.n_mv, macs_mv += o.macs_mv;
+  n_vv += o.n_vv, macs_vv += o.macs_vv;
+  n_check += o.n_check, macs_check += o.macs_check;
+  n_restart += o.n_restart, macs_restart += o.macs_restart;
+}
+
+void charge_factor(Ledger& L, const OperatorEngine& op) {
+  double macs = 0;
+  for (const Front& F : op.fac->sym.fronts)
+    for (int k = 0; k < F.npiv; ++k) {
+      const double r = F.nf - k - 1.0;
+      macs += r * r;
+    }
+  L.n_fa += 1;
+  L.macs_fa += macs;
+}
+
+void charge_apply(Ledger& L, const OperatorEngine& op) {
+  double fb = 0;
+  for (const Front& F : op.fac->sym.fronts) {
+    const double np = F.npiv, nf = F.nf;
+    fb += np * np + 2.0 * np * (nf - np);
+  }
+  L.n_fb += 1;
+  L.macs_fb += fb;
+  L.n_mv += 3;  // C v_u, M v_u, M v_l
+  L.macs_mv += 3.0 * static_cast<double>(op.nnz);
+  L.n_vv += 3;  // + s M v_u, + M v_l, r_l = s r_u + v_u
+  L.macs_vv += 3.0 * static_cast<double>(op.n);
+}
+
+void charge_bproduct(Ledger& L, const OperatorEngine& op) {
+  L.n_mv += 1;
+  L.macs_mv += static_cast<double>(op.nnz);
+}
+
+void charge_vv2n(Ledger& L, const OperatorEngine& op, int64_t count) {
+  L.n_vv += count;
+  L.macs_vv += static_cast<double>(count) * 2.0 * static_cast<double>(op.n);
+}
+
 // pinned: the cycle's H / beta copies are truly asynchronous, so the host
 // can start on them while the GPU already applies the operator to the
 // continuation vector of the next cycle
@@ -137,17 +187,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   EigsResult res;
   const int64_t launches0 = op.launches;
   // ledger: one factorization (already done when the operator was built)
-  L.n_fa += 1;
-  {
-    double macs = 0;
-    for (const Front& F : op.fac->sym.fronts)
-      for (int k = 0; k < F.npiv; ++k) {
-        const double r = F.nf - k - 1.0;
-        macs += r + r * r;
-      }
-    L.macs_fa += macs;
-  }
-  const double fb_macs = static_cast<double>(op.fac->sym.nnz_l + op.fac->sym.nnz_u);
+  charge_factor(L, op);
   const double nnz = static_cast<double>(op.nnz);
 
   // V: Krylov basis; BV = B V kept alongside, so every B-inner product of CGS2
@@ -183,16 +223,12 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     for (int pass = 0; pass < 2 && nlock > 0; ++pass) {
       op.gemv_t(BV, nlock, r, dHa.as<double>());
       op.gemv_n(V, nlock, dHa.as<double>(), r, nullptr);
-      L.n_mv += 1;  // ledger: the reference algorithm's B-product
-      L.macs_mv += nnz;
-      L.n_vv += 2 * nlock;
-      L.macs_vv += 2.0 * nlock * n2;
+      charge_bproduct(L, op);  // ledger: the reference algorithm's B-product
+      charge_vv2n(L, op, 2 * nlock);
     }
     op.bnorm_normalize_b(r, dBeta.as<double>() + m, dst, dst_b);
-    L.n_mv += 1;
-    L.macs_mv += nnz;
-    L.n_vv += 2;
-    L.macs_vv += 2.0 * n2;
+    charge_bproduct(L, op);
+    charge_vv2n(L, op, 1);
   };
 
   std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0);  // column-major (m+1) x m
@@ -282,13 +318,10 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       cuda_check(cudaGraphLaunch(it->second, st), "graph launch");
       res.graph_launches += 1;
     }
-    for (int j = k; j < m; ++j) {
-      L.n_fb += 1;
-      L.macs_fb += fb_macs;
-      L.n_mv += 6;  // sigma M v_u, C v_u, M v_l (fused) + 3 B-products of CGS2
-      L.macs_mv += 6 * nnz;
-      L.n_vv += 4 * (j + 1) + 2;
-      L.macs_vv += (4.0 * (j + 1) + 2) * n2;
+    for (int j = k; j < m; ++j) {  // per step: apply + 2 x (B-product, j+1 dots, j+1 axpys) + B-norm
+      charge_apply(L, op);
+      for (int pass = 0; pass < 3; ++pass) charge_bproduct(L, op);
+      charge_vv2n(L, op, 4 * (j + 1) + 1);
     }
     cuda_check(cudaMemcpyAsync(ha.data(), dHa.p, sizeof(double) * (m + 1) * (m + 1),
                                cudaMemcpyDeviceToHost, st), "D2H H");
@@ -437,11 +470,11 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         if (!(cres[c] <= o.tol)) (c < nev ? all_conv : mates_conv) = false;
       }
       mates_conv = mates_conv && all_conv;
-      L.n_check += 3 * nchk;
+      L.n_check += nchk;  // one explicit pencil residual (K, C, M products) per candidate
+      L.macs_check += 3.0 * nnz * nchk;
       t_check += ms_since(tc0);
       since_check = 0;
       check_gate = all_conv ? o.est_factor * o.tol : 0.1 * est_worst;
-      L.macs_check += 6.0 * nnz * nchk;
     }
     int nconv_now = 0;
     for (int c = 0; c < nev && maybe; ++c)

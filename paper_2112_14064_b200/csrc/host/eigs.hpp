@@ -12,12 +12,32 @@ struct OperatorEngine;
 
 // Four-category ledger + aux tallies (reference sparse.hpp:49-103). The GPU
 // path computes in real FP64, so one multiply-add is 2 flops.
+//
+// Charges follow the reference operations one for one (the
+// oracle's rq::spmv / dot / axpy call sequence): the GPU fuses and skips work
+// (B-images kept beside the basis, one fused C/M SpMV) but the ledger counts
+// the algorithm's operations, so its counters equal the reference CPU path's
+// for the same operation (tests/test_gpu_parity.py ledger tests):
+//   lu_factorize / build_operator  fa 1, sum over pivots of (nf-k-1)^2
+//   apply_operator                 fb 1 (sum np^2 + 2 np (nf-np)), mv 3 (nnz), vv 3 (n)
+//   B-product (b_inner, CGS)       mv 1 (nnz); each 2n dot or axpy: vv 1 (2n)
+//   explicit residual check        check 1 per candidate (3 nnz)
+//   restart V <- V Q               restart 1 (m p 2n)
 struct Ledger {
   int64_t n_fa = 0, n_fb = 0, n_mv = 0, n_vv = 0, n_check = 0, n_restart = 0;
   double macs_fa = 0, macs_fb = 0, macs_mv = 0, macs_vv = 0, macs_check = 0, macs_restart = 0;
   double flops_per_mac = 2.0;
   std::string to_json() const;
+  // counters as {ops, macs} x {fa, fb, mv, vv, check, restart}
+  void get(double* out12) const;
+  void add(const Ledger& o, bool with_fa);
 };
+
+// per-operation charges (see above) for the operator `op`
+void charge_factor(Ledger& L, const OperatorEngine& op);
+void charge_apply(Ledger& L, const OperatorEngine& op);
+void charge_bproduct(Ledger& L, const OperatorEngine& op);  // one M-product (B = diag(I, M))
+void charge_vv2n(Ledger& L, const OperatorEngine& op, int64_t count);  // count 2n-length dots / axpys
 
 struct EigsOptions {
   int nev = 10;

@@ -18,6 +18,9 @@ from ._lib import EigsInfo, EigsOpts, OperatorOpts, RqError, check
 from .sparsela import Ordering, nested_dissection_order
 
 
+LEDGER_CATEGORIES = ("fa", "fb", "mv", "vv", "residual_check", "restart")
+
+
 @dataclass
 class EigenPair:
     lam: complex
@@ -66,24 +69,67 @@ class ShiftInvertOperator:
         check(_lib.lib.rq_operator_apply(self._h, v, r))
         return r
 
+    def _vec(self, x, size, what):
+        x = np.ascontiguousarray(x, np.float64)
+        if x.ndim != 1 or x.size != size:
+            raise RqError(7, f"{what} dimension mismatch: {x.size} entries, expected {size}")
+        return x
+
     def b_inner(self, x: np.ndarray, y: np.ndarray) -> float:
+        x = self._vec(x, 2 * self.n, "b_inner")
+        y = self._vec(y, 2 * self.n, "b_inner")
         out = C.c_double()
-        check(_lib.lib.rq_operator_b_inner(self._h, np.ascontiguousarray(x, np.float64),
-                                           np.ascontiguousarray(y, np.float64), C.byref(out)))
+        check(_lib.lib.rq_operator_b_inner(self._h, x, y, C.byref(out)))
         return out.value
 
     def spmv(self, which: str, x: np.ndarray) -> np.ndarray:
         w = {"K": 0, "C": 1, "M": 2, "Q": 3}[which]
+        x = self._vec(x, self.n, "spmv")
         y = np.zeros(self.n)
-        check(_lib.lib.rq_operator_spmv(self._h, w, np.ascontiguousarray(x, np.float64), y))
+        check(_lib.lib.rq_operator_spmv(self._h, w, x, y))
         return y
 
     def arnoldi(self, v1: np.ndarray, m: int):
+        v1 = self._vec(v1, 2 * self.n, "arnoldi_run")
+        if not 1 <= m < 2 * self.n:
+            raise RqError(2, "arnoldi_run: m must be in [1, 2n)")
         V = np.zeros((m + 1, 2 * self.n))
         H = np.zeros(m * (m + 1))
-        check(_lib.lib.rq_operator_arnoldi(self._h, np.ascontiguousarray(v1, np.float64), int(m),
-                                           _lib.ptr(V), _lib.ptr(H)))
+        check(_lib.lib.rq_operator_arnoldi(self._h, v1, int(m), _lib.ptr(V), _lib.ptr(H)))
         return V, H.reshape(m, m + 1).T
+
+    def ritz_extract(self, H: np.ndarray):
+        """SPEC.md:444 ritz_extract of an (m+1) x m Hessenberg of this operator."""
+        return ritz_extract(H, self.s, self.varsigma)
+
+    def krylov_schur_restart(self, V: np.ndarray, H: np.ndarray, keep: int):
+        """SPEC.md:453 krylov_schur_restart: (V[:p+1], H[:p+1, :p], p)."""
+        V = np.array(V, dtype=np.float64, order="C", copy=True)
+        H = np.asarray(H, np.float64)
+        m = H.shape[1]
+        if H.shape != (m + 1, m) or V.shape != (m + 1, 2 * self.n):
+            raise RqError(7, "krylov_schur_restart: V must be (m+1) x 2n and H (m+1) x m")
+        Hc = np.array(H.T, dtype=np.float64, order="C")  # column-major (m+1) x m
+        p = C.c_int()
+        check(_lib.lib.rq_operator_krylov_schur_restart(self._h, m, int(keep), V.reshape(-1), Hc.reshape(-1),
+                                                        C.byref(p)))
+        p = p.value
+        Hn = Hc.reshape(m, m + 1).T
+        return V[:p + 1], Hn[:p + 1, :p], p
+
+    def ledger_counts(self) -> dict:
+        """Cumulative CostLedger of this operator: {category: (ops, macs)}."""
+        out = np.zeros(12)
+        check(_lib.lib.rq_operator_ledger(self._h, out))
+        return {nm: (int(out[2 * i]), float(out[2 * i + 1])) for i, nm in enumerate(LEDGER_CATEGORIES)}
+
+    def ledger_json(self) -> dict:
+        buf = C.create_string_buffer(4096)
+        check(_lib.lib.rq_operator_ledger_json(self._h, buf, 4096))
+        return json.loads(buf.value.decode())
+
+    def ledger_reset(self) -> None:
+        check(_lib.lib.rq_operator_ledger_reset(self._h))
 
     def factor_info(self) -> dict:
         from ._lib import FactorInfo
@@ -143,6 +189,42 @@ def b_inner(op: ShiftInvertOperator, x: np.ndarray, y: np.ndarray) -> float:
 def arnoldi_run(op: ShiftInvertOperator, v1: np.ndarray, m: int):
     """SPEC.md:435 m-step B-orthogonal Arnoldi with CGS2: (V (m+1) x 2N, H (m+1) x m)."""
     return op.arnoldi(v1, m)
+
+
+def scale_pencil(pencil):
+    """SPEC.md:399 scale_pencil(pencil) -> (varsigma, C scaled, M scaled):
+    varsigma = sqrt(maxabs K / maxabs M), scaled pencil (K, varsigma C,
+    varsigma^2 M). Zero M raises RqError (domain)."""
+    K = np.ascontiguousarray(pencil.K, np.float64)
+    Cv = np.ascontiguousarray(pencil.C, np.float64)
+    M = np.ascontiguousarray(pencil.M, np.float64)
+    if not K.size == Cv.size == M.size:
+        raise RqError(7, "scale_pencil: K, C, M must share one pattern")
+    vs = C.c_double()
+    Cs, Ms = np.empty_like(Cv), np.empty_like(M)
+    check(_lib.lib.rq_scale_pencil(K.size, K, Cv, M, C.byref(vs), _lib.ptr(Cs), _lib.ptr(Ms)))
+    return vs.value, Cs, Ms
+
+
+def ritz_extract(H: np.ndarray, sigma: float, varsigma: float = 1.0) -> dict:
+    """SPEC.md:444 ritz_extract: Ritz data of an (m+1) x m Hessenberg H in
+    wanted order (nearest the shift first): theta, lambda = sigma + varsigma /
+    theta, residual estimate |beta e_m^H y| and the unit Ritz vectors y (columns)."""
+    H = np.asarray(H, np.float64)
+    m = H.shape[1]
+    if H.shape != (m + 1, m):
+        raise RqError(7, "ritz_extract: H must be (m+1) x m")
+    Hc = np.ascontiguousarray(H.T).reshape(-1)  # column-major
+    th, lam, est, Y = np.zeros(2 * m), np.zeros(2 * m), np.zeros(m), np.zeros(2 * m * m)
+    check(_lib.lib.rq_ritz_extract(Hc, m, float(sigma), float(varsigma), _lib.ptr(th), _lib.ptr(lam),
+                                   _lib.ptr(est), _lib.ptr(Y)))
+    Yc = (Y[0::2] + 1j * Y[1::2]).reshape(m, m).T
+    return {"theta": th[0::2] + 1j * th[1::2], "lambda": lam[0::2] + 1j * lam[1::2], "est": est, "y": Yc}
+
+
+def krylov_schur_restart(op: ShiftInvertOperator, V: np.ndarray, H: np.ndarray, keep: int):
+    """SPEC.md:453 krylov_schur_restart(state, keep) -> (V_p+1, H_(p+1) x p, p)."""
+    return op.krylov_schur_restart(V, H, keep)
 
 
 def solve_quadratic(pencil, s: float, nev: int, m: int = 0, eps: float = 1e-10, seed: int = 0,

@@ -65,14 +65,18 @@ def test_oracle_libraries_load():
         assert r.ref_kern_backend() in (b"avx2", b"scalar")
 
 
-def test_cxx_dropin_headers_compile(tmp_path):
-    """include/rigaqep/{sparsela,eig}.hpp compile against the reference types."""
-    ref_inc = "/root/reference/proj/include"
-    if not os.path.isdir(ref_inc):
-        pytest.skip("reference headers not present on this box")
+def test_cxx_dropin_links_against_reference_types():
+    """include/rigaqep/{sparsela,eig}.hpp compile against the reference's own
+    headers and link with its compiled sources (splines, spaces, sparse,
+    kernels from /root/reference) and librq_b200.so (tests/cpp/Makefile); the
+    GPU suite runs the binary (tests/test_boundary_cpp.py)."""
     import subprocess
-    src = tmp_path / "t.cpp"
-    src.write_text('#include "rigaqep/sparsela.hpp"\n#include "rigaqep/eig.hpp"\nint main(){return 0;}\n')
-    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", f"-I{os.path.join(ROOT, 'include')}",
-                        f"-I{ref_inc}", str(src)], capture_output=True, text=True)
-    assert r.returncode == 0, r.stderr
+    if not os.path.isdir("/root/reference/proj/include"):
+        pytest.skip("reference sources not present on this box (the prebuilt binary travels)")
+    r = subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "cpp")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    exe = os.path.join(ROOT, "tests", "cpp", "_build", "test_boundary")
+    assert os.access(exe, os.X_OK)
+    nm = subprocess.run(["nm", "-C", "-u", exe], capture_output=True, text=True).stdout
+    for sym in ("rq_operator_krylov_schur_restart", "rq_ritz_extract", "rq_eigs_run", "rq_operator_ledger"):
+        assert sym in nm  # resolved from librq_b200.so at run time

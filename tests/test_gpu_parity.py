@@ -385,3 +385,74 @@ def test_schur_update_bench_entry():
     x = f.solve(b)
     r = P.to_scipy("K") @ x - 0.5 * (P.to_scipy("C") @ x) + 0.25 * (P.to_scipy("M") @ x) - b
     assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(b)
+
+
+# --------------------------------------------------------------------------- ledger / SPEC operations
+def test_ledger_matches_oracle_per_operation(cfg1):
+    """CostLedger parity (sparse.hpp:57-103): build_operator,
+    apply_operator, b_inner and arnoldi_run charge exactly the counters the
+    reference CPU path (the oracle's rq::spmv / dot / axpy sequence) charges;
+    N_vv of arnoldi_run grows quadratically in m."""
+    op = rq.build_operator(cfg1, SIGMA)
+    E = oracle.Eig(cfg1, SIGMA)
+    assert op.ledger_counts() == E.ledger_counts()  # fa: one factorization
+    assert op.ledger_counts()["fa"][0] == 1
+    rng = np.random.default_rng(1)
+    v = rng.uniform(-1, 1, 2 * cfg1.n)
+    op.ledger_reset(), E.ledger_reset()
+    op.apply(v), E.apply(v)
+    assert op.ledger_counts() == E.ledger_counts()
+    assert op.ledger_counts()["fb"][0] == 1 and op.ledger_counts()["mv"][0] == 3
+    x, y = rng.standard_normal(2 * cfg1.n), rng.standard_normal(2 * cfg1.n)
+    op.ledger_reset(), E.ledger_reset()
+    bo, bg = E.b_inner(x, y), op.b_inner(x, y)
+    assert abs(bo.real - bg) <= 1e-12 * abs(bg)
+    assert op.ledger_counts() == E.ledger_counts()
+    vv = {}
+    for m in (20, 40, 80):
+        op.ledger_reset(), E.ledger_reset()
+        op.arnoldi(v, m), E.arnoldi(v, m)
+        g, o = op.ledger_counts(), E.ledger_counts()
+        assert g == o, (m, g, o)
+        assert g["fb"][0] == m and g["mv"][0] == 6 * m + 1
+        vv[m] = g["vv"][0]
+    assert 3.5 <= vv[40] / vv[20] <= 4.0 and 3.5 <= vv[80] / vv[40] <= 4.0  # ~ 2 m^2
+    js = op.ledger_json()
+    assert set(js) == {"fa", "fb", "mv", "vv", "residual_check", "restart", "flops_per_mac", "total_flops"}
+
+
+def test_solve_quadratic_counter_laws(cfg1):
+    """N_fa = 1 per solve; one operator application (N_fb) per
+    Arnoldi step; N_mv / N_fb in [4, 6] plus the start vectors' B-products;
+    the operator's cumulative ledger adds the solve's (fa charged once)."""
+    op = rq.build_operator(cfg1, SIGMA)
+    op.solve_quadratic(10, eps=1e-10)
+    info, led = op.last_info, op.ledger
+    assert info["n_fa"] == 1 and led["fa"]["ops"] == 1
+    assert 6.0 <= info["n_mv"] / info["n_fb"] <= 6.2
+    assert info["n_restart"] >= 1 and info["n_check"] >= 10
+    cum = op.ledger_counts()
+    assert cum["fa"][0] == 1 and cum["fb"][0] == info["n_fb"] and cum["vv"][0] == info["n_vv"]
+
+
+def test_krylov_schur_restart_invariants(cfg1):
+    """after keeping the wanted directions, S V_p = V_p T_p +
+    v_{p+1} b^T holds, V_{p+1} stays B-orthonormal, the kept Ritz values are
+    the wanted ones of H_m, and keep >= m is the identity restart."""
+    op = rq.build_operator(cfg1, SIGMA)
+    n, m = cfg1.n, 21
+    V, H = op.arnoldi(np.random.default_rng(2).uniform(-1, 1, 2 * n), m)
+    r = op.ritz_extract(H)
+    Vp, Hp, p = op.krylov_schur_restart(V, H, 11)
+    assert 11 <= p <= 12 and Vp.shape == (p + 1, 2 * n) and Hp.shape == (p + 1, p)
+    Mm = cfg1.to_scipy("M")
+    BV = np.concatenate([Vp[:, :n], (Mm @ Vp[:, n:].T).T], 1)
+    assert np.max(np.abs(Vp @ BV.T - np.eye(p + 1))) <= 1e-10
+    SV = np.stack([op.apply(Vp[j]) for j in range(p)])
+    R = SV.T - Vp.T @ Hp
+    assert np.max(np.abs(R)) <= 1e-8 * np.max(np.abs(H))
+    kept = np.linalg.eigvals(Hp[:p])
+    for t in r["theta"][:p]:
+        assert np.min(np.abs(kept - t)) <= 1e-10 * abs(t)
+    V2, H2, p2 = op.krylov_schur_restart(V, H, m)
+    assert p2 == m and np.array_equal(V2, V) and np.array_equal(H2, H)
