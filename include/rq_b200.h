@@ -254,6 +254,11 @@ typedef struct {
  * max_restarts is exhausted. */
 int rq_eigs_run(rq_operator_t* op, const rq_eigs_opts* opts, double* lam_re, double* lam_im,
                 double* resid, double* vec_re, double* vec_im, rq_eigs_info* info);
+/* The Krylov workspace (basis, B-images, pinned staging and the captured cycle
+ * graphs: ~6 (m+1) 2n doubles, 9 GB at cfg4 with m = 201) stays with the
+ * operator so repeated solves allocate nothing; this frees it (the next
+ * rq_eigs_run rebuilds it). */
+int rq_operator_release_workspace(rq_operator_t* op);
 /* CostLedger::to_json-compatible snapshot (sparse.cpp:80-97) of the last run. */
 int rq_eigs_ledger_json(const rq_operator_t* op, char* buf, size_t len);
 /* The operator's cumulative CostLedger (reference sparse.hpp:57-103): every

@@ -150,6 +150,7 @@ _sig("rq_operator_time", C.c_int, vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_d
 _sig("rq_eigs_run", C.c_int, vp, C.POINTER(EigsOpts), vp, vp, vp, vp, vp, C.POINTER(EigsInfo))
 _sig("rq_eigs_ledger_json", C.c_int, vp, C.c_char_p, C.c_size_t)
 _sig("rq_operator_ledger", C.c_int, vp, f64p)
+_sig("rq_operator_release_workspace", C.c_int, vp)
 _sig("rq_operator_ledger_json", C.c_int, vp, C.c_char_p, C.c_size_t)
 _sig("rq_operator_ledger_reset", C.c_int, vp)
 _sig("rq_scale_pencil", C.c_int, C.c_int64, f64p, f64p, f64p, C.POINTER(C.c_double), vp, vp)
@@ -169,7 +170,7 @@ EXPORTS = [
     "rq_mm_dims", "rq_mm_csr", "rq_mm_destroy", "rq_pencil_write_mm", "rq_eigenpairs_json", "rq_operator_varsigma", "rq_operator_apply", "rq_operator_b_inner",
     "rq_operator_spmv", "rq_operator_arnoldi", "rq_operator_factor", "rq_operator_destroy",
     "rq_operator_time",
-    "rq_eigs_run", "rq_eigs_ledger_json", "rq_operator_ledger", "rq_operator_ledger_json",
+    "rq_eigs_run", "rq_eigs_ledger_json", "rq_operator_ledger", "rq_operator_ledger_json", "rq_operator_release_workspace",
     "rq_operator_ledger_reset", "rq_scale_pencil", "rq_ritz_extract", "rq_operator_krylov_schur_restart",
 ]
 

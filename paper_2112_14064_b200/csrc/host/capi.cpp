@@ -617,6 +617,15 @@ int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, doub
   return 0;
 }
 
+int rq_operator_release_workspace(rq_operator_t* o) {
+  return guarded([&] {
+    need(o, "op");
+    std::lock_guard<std::mutex> lock(o->op->fac->mu);
+    rqb::cuda_check(cudaStreamSynchronize(o->op->stream), "sync");
+    o->op->eig_ws.reset();
+  });
+}
+
 int rq_operator_ledger(const rq_operator_t* o, double* out) {
   return guarded([&] {
     need(o, "op");

@@ -144,7 +144,8 @@ struct EigWorkspace {
   DeviceBuffer dV, dV2, dBV, dBV2, dR, dW, dHa, dHb, dBeta, dQ, dX, dRes;
   Pinned ha, hb, betas;
   Pinned hv, hq, hy;  // staging of the host -> device copies (start vectors, restart Q, Ritz Y)
-  std::map<std::pair<int, const double*>, cudaGraphExec_t> graphs;
+  // cycle graph per (start index, basis buffer) and the kernels it launches
+  std::map<std::pair<int, const double*>, std::pair<cudaGraphExec_t, int64_t>> graphs;
   EigWorkspace(int m_, int64_t n2_)
       : m(m_), n2(n2_), ha(static_cast<size_t>(m_ + 1) * (m_ + 1)), hb(static_cast<size_t>(m_ + 1) * (m_ + 1)),
         betas(m_ + 1), hv(static_cast<size_t>(n2_)), hq(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)),
@@ -163,7 +164,7 @@ struct EigWorkspace {
     dRes.alloc(sizeof(double) * 4 * (m + 1));
   }
   ~EigWorkspace() {
-    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
   }
 };
 
@@ -306,16 +307,20 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       if (it == graphs.end()) {
         const auto tg = now();
         cudaGraph_t gr;
+        const int64_t l0 = op.launches;
         cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
         enqueue_steps(false, pre_applied);
         cuda_check(cudaStreamEndCapture(st, &gr), "capture end");
+        const int64_t kernels = op.launches - l0;
+        op.launches = l0;  // counted per replay below
         cudaGraphExec_t ex;
         cuda_check(cudaGraphInstantiate(&ex, gr, 0), "graph instantiate");
         cudaGraphDestroy(gr);
-        it = graphs.emplace(key, ex).first;
+        it = graphs.emplace(key, std::make_pair(ex, kernels)).first;
         t_graph_build += ms_since(tg);
       }
-      cuda_check(cudaGraphLaunch(it->second, st), "graph launch");
+      cuda_check(cudaGraphLaunch(it->second.first, st), "graph launch");
+      op.launches += it->second.second;  // the same count on every call, cached graph or not
       res.graph_launches += 1;
     }
     for (int j = k; j < m; ++j) {  // per step: apply + 2 x (B-product, j+1 dots, j+1 axpys) + B-norm

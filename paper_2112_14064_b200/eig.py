@@ -128,6 +128,10 @@ class ShiftInvertOperator:
         check(_lib.lib.rq_operator_ledger_json(self._h, buf, 4096))
         return json.loads(buf.value.decode())
 
+    def release_workspace(self) -> None:
+        """Free the Krylov workspace kept across solve_quadratic calls."""
+        check(_lib.lib.rq_operator_release_workspace(self._h))
+
     def ledger_reset(self) -> None:
         check(_lib.lib.rq_operator_ledger_reset(self._h))
 

@@ -433,6 +433,13 @@ def test_solve_quadratic_counter_laws(cfg1):
     assert info["n_restart"] >= 1 and info["n_check"] >= 10
     cum = op.ledger_counts()
     assert cum["fa"][0] == 1 and cum["fb"][0] == info["n_fb"] and cum["vv"][0] == info["n_vv"]
+    # a repeated solve replays the cached cycle graphs: same launch count;
+    # after release_workspace the graphs are rebuilt: same again
+    op.solve_quadratic(10, eps=1e-10)
+    assert op.last_info["launches"] == info["launches"]
+    op.release_workspace()
+    op.solve_quadratic(10, eps=1e-10)
+    assert op.last_info["launches"] == info["launches"]
 
 
 def test_krylov_schur_restart_invariants(cfg1):
