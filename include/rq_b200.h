@@ -168,9 +168,9 @@ int rq_factor_front_export(const rq_factor_t* f, int64_t front, double* dense, i
 int rq_factor_profile(rq_factor_t* f, double* ms, int64_t* launches, double* work);
 /* Task-level profile of the persistent task-DAG factorization (profiling run):
  * out[3t+0] busy ms (summed over CTAs), out[3t+1] reserved (0), out[3t+2] task
- * count, for t = {SMALL, ASM, DIAG, ROWS, COLS, UPDATE}; out[18] persistent
- * grid size, out[19] tasks, out[20] ready-queue wait ms summed over CTAs.
- * double[24]. */
+ * count, for t = {SMALL, ASM, DIAG, ROWS, COLS, UPD (per-step updates)};
+ * out[18] persistent grid size, out[19] tasks, out[20] ready-queue wait ms
+ * summed over CTAs, out[21] UPDCB busy ms, out[23] UPDCB count. double[24]. */
 int rq_factor_dag_profile(rq_factor_t* f, double* out);
 /* Evidence entry (development): the contribution-block Schur update of ONE
  * front (front < 0: the largest), i.e. the factorization's own UPDCB task code

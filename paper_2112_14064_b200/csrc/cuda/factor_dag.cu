@@ -56,7 +56,8 @@ constexpr int kTile = 64;         // big-front tile edge
 constexpr int kTSP = kTile + 4;   // padded smem stride of DMMA operand tiles
 constexpr double kLmax = 10.0 * (1.0 - 1e-14);  // 1/threshold, conservative
 constexpr int kAsmRowTiles = 8;  // parent rows per extend-add task: 8 tiles
-constexpr int kCnt = 5;  // per-front counters: tasks, asm, diag, rc, released
+constexpr int kCnt = 7;  // per-front counters: tasks, asm, diag, rc, released, batches running, fallback
+constexpr int kCntRun = 5, kCntFb = 6;
 // Two configurations of the persistent kernel, chosen per factorization
 // (rqb_dag_build): small problems are critical-path bound and want big SMALL
 // fronts (nf <= 160 factored whole in 206 KB of shared memory, one CTA per
@@ -69,7 +70,7 @@ constexpr size_t kSmallBytesLatency = 160 * 161 * 8;     // 206 KB: one CTA per 
 constexpr size_t kSmallBytesThroughput = 118 * 119 * 8;  // 112 KB: two CTAs per SM
 constexpr double kThroughputFlops = 2e9;  // F_LU above which the two-CTA variant is used
 
-enum : int16_t { T_SMALL = 0, T_ASM = 1, T_DIAG = 2, T_ROWS = 3, T_COLS = 4, T_UPD = 5, T_UPDCB = 6 };
+enum : int16_t { T_SMALL = 0, T_ASM = 1, T_DIAG = 2, T_ROWS = 3, T_COLS = 4, T_UPD = 5, T_UPDCB = 6, T_UPDB = 7 };
 
 struct Task {
   int32_t front;
@@ -91,7 +92,7 @@ struct FrontDag {
   int32_t parent;      // parent front (-1 root)
   int32_t acb;         // first contribution-block tile (rows / columns >= npiv)
   int32_t cb_base;     // first UPDCB task ((tiles - acb)^2 of them, row-major)
-  int32_t pad3;
+  int32_t ub_off;      // offset into ubase[] (tiles^2): first UPDB task of each pivot-region tile
   int64_t backup_off;  // panel backup nf x 32, then A12 backup 32 x nf
 };
 
@@ -122,7 +123,20 @@ struct DagArgs {
   int* qctl;                 // {head, tail}
   const int32_t* step_base;  // FrontDag::sb_off: first task of every panel step
   int upd_cp16;              // UPD operands by 16-byte cp.async (RQB_UPD_CP16=0: 8-byte copies)
+  int upd_batch;             // deferred updates: panel steps per UPDB task (0: every update per step)
+  int upd_la;                // lookahead: the last upd_la steps before a tile's panel stay per step
+  const int32_t* ubase;      // FrontDag::ub_off
 };
+
+// Deferred updates of a pivot-region tile: its updates from steps
+// 0 .. lim - 1 run as UPDB tasks of upd_batch steps each (K = 32 upd_batch,
+// the UPDCB code over a K range); steps >= lim stay per step (UPD), so the
+// lookahead tiles on the panel chain keep their K = 32 latency. Must match
+// rqb_dag_build.
+__device__ __forceinline__ int upd_lim(const DagArgs& A, int a, int b, int steps) {
+  return A.upd_batch > 0 ? min(steps, max(0, 2 * min(a, b) - A.upd_la)) : 0;
+}
+
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -138,6 +152,18 @@ __device__ __forceinline__ bool spin_ge(const int* p, int target, int* flags) {
   if (*((volatile const int*)p) >= target) return true;
   const unsigned long long t0 = gtimer();
   while (*((volatile const int*)p) < target) {
+    __nanosleep(64);
+    if (gtimer() - t0 > kStallNs || *((volatile int*)&flags[2])) {
+      atomicCAS(&flags[2], 0, 2);
+      return false;
+    }
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool spin_le(const int* p, int target, int* flags) {
+  const unsigned long long t0 = gtimer();
+  while (*((volatile const int*)p) > target) {
     __nanosleep(64);
     if (gtimer() - t0 > kStallNs || *((volatile int*)&flags[2])) {
       atomicCAS(&flags[2], 0, 2);
@@ -756,10 +782,11 @@ __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int 
 // is in flight while DMMA consumes the current one), C read once and written
 // once. Runs after the front's last panel is released: every L and U column
 // is final (pivot swaps never touch contribution-block rows).
-__device__ void updcb_task(const DagArgs& A, const FrontDev& F, int a, int b, double* sm) {
+__device__ void updcb_task(const DagArgs& A, const FrontDev& F, int a, int b, double* sm, int kb = 0,
+                           int ke = -1) {
   const int r0 = a * kTile, r1 = min(r0 + kTile, F.nf);
   const int c0 = b * kTile, c1 = min(c0 + kTile, F.nf);
-  const int K = F.npiv;
+  const int K = ke < 0 ? F.npiv : ke;  // pivots kb .. K - 1
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
   const int tid = threadIdx.x;
@@ -773,7 +800,7 @@ __device__ void updcb_task(const DagArgs& A, const FrontDev& F, int a, int b, do
   auto issue = [&](int chunk, int buf) {
     double* As = sm + buf * kStage;
     double* Bs = As + kNB * kTSP;
-    const int k0 = chunk * kNB;
+    const int k0 = kb + chunk * kNB;
 #pragma unroll
     for (int i = 0; i < kNB * kTile / 2 / kDT; ++i) {
       const int idx = tid + i * kDT;
@@ -790,7 +817,7 @@ __device__ void updcb_task(const DagArgs& A, const FrontDev& F, int a, int b, do
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  const int nchunks = (K + kNB - 1) / kNB;
+  const int nchunks = (K - kb + kNB - 1) / kNB;
   issue(0, 0);
   double cv[2][2][4];
 #pragma unroll
@@ -850,7 +877,7 @@ __device__ void updcb_task(const DagArgs& A, const FrontDev& F, int a, int b, do
 
 // Exact threshold-pivoted redo of panel s (rare path, one CTA).
 __device__ void panel_fallback(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s,
-                               double* sm) {
+                               double* sm, int* cnt) {
   const int k = s * kNB, w = min(kNB, F.npiv - k), np = F.npiv, nf = F.nf;
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
@@ -858,12 +885,20 @@ __device__ void panel_fallback(const DagArgs& A, const FrontDev& F, const FrontD
   double* red = sm;
   int* redi = reinterpret_cast<int*>(sm + 32);
   __shared__ int piv_s;
-  // all trailing updates of earlier panels must be in place (rows are swapped across all columns)
+  // all per-step trailing updates of earlier panels must be in place (rows are
+  // swapped across all columns). Tiles with deferred (UPDB) updates may still
+  // owe some: a row swap moves their pending L rows with their C rows, so the
+  // later batch stays consistent; only a batch running right now must not
+  // overlap the swaps (fallback flag + running count, Dekker-style with the
+  // UPDB start in factor_dag_kernel)
   if (tid == 0) {
-    const int a0 = k / kTile;
+    atomicExch(&cnt[kCntFb], 1);
+    __threadfence();
+    spin_le(&cnt[kCntRun], 0, A.flags);
+    const int a0 = k / kTile, steps = (np + kNB - 1) / kNB;
     for (int a = a0; a < D.tiles; ++a)
       for (int b = a0; b < D.tiles; ++b)
-        if (a < D.acb || b < D.acb)  // contribution-block tiles are not updated per step
+        if ((a < D.acb || b < D.acb) && upd_lim(A, a, b, steps) <= s)  // per-step tiles
           spin_ge(&A.tile_step[D.tile_off + a * D.tiles + b], s, A.flags);
     __threadfence();
   }
@@ -904,12 +939,33 @@ __device__ void panel_fallback(const DagArgs& A, const FrontDev& F, const FrontD
     }
     __syncthreads();
     const int p = piv_s;
-    if (p != j)
+    if (p != j) {
       for (int c = tid; c < nf; c += kDT) {
         const double t = __ldcg(&g[j + (int64_t)c * ld]);
         g[j + (int64_t)c * ld] = __ldcg(&g[p + (int64_t)c * ld]);
         g[p + (int64_t)c * ld] = t;
       }
+      __syncthreads();
+      // Row p's tile (ap, b) may still owe deferred steps ts .. s-1 (pending
+      // UPDB batches; quiesced above) while row j's tile (s / 2, b) is current:
+      // after the swap, bring position j up to date and give position p back
+      // the debt its tile's batches will pay (same L rows, swapped with C)
+      const int ap = p / kTile;
+      if (A.upd_batch > 0 && ap != j / kTile)
+        for (int c = k + w + tid; c < nf; c += kDT) {
+          const int b = c / kTile;
+          const int ts = *((volatile const int*)&A.tile_step[D.tile_off + ap * D.tiles + b]);
+          if (ts >= s) continue;
+          double dj = 0.0, dp = 0.0;
+          for (int q = ts * kNB; q < k; ++q) {
+            const double u = __ldcg(&g[q + (int64_t)c * ld]);
+            dj = fma(__ldcg(&g[j + (int64_t)q * ld]), u, dj);
+            dp = fma(__ldcg(&g[p + (int64_t)q * ld]), u, dp);
+          }
+          g[j + (int64_t)c * ld] = __ldcg(&g[j + (int64_t)c * ld]) - dj;
+          g[p + (int64_t)c * ld] = __ldcg(&g[p + (int64_t)c * ld]) + dp;
+        }
+    }
     __syncthreads();
     const double ujj = __ldcg(&g[j + (int64_t)j * ld]);
     for (int i = j + 1 + tid; i < nf; i += kDT) {
@@ -976,6 +1032,19 @@ __device__ __forceinline__ void notify(const DagArgs& A, int t) {
     __threadfence();
     const int slot = atomicAdd(&A.qctl[1], 1);
     atomicExch(&A.queue[slot], t);
+  }
+}
+
+// release of panel step s for the eager tile (ua, ub): its per-step update,
+// or the batch that ends at step s
+__device__ __forceinline__ void release_tile(const DagArgs& A, const FrontDag& D, const FrontDev& F, int s,
+                                             int steps, int ua, int ub) {
+  const int lim = upd_lim(A, ua, ub, steps);
+  if (s >= lim) {
+    notify(A, idx_upd(A, D, F, s, ua, ub));
+  } else {
+    const int j = s / A.upd_batch;
+    if (s == min((j + 1) * A.upd_batch, lim) - 1) notify(A, A.ubase[D.ub_off + ua * D.tiles + ub] + j);
   }
 }
 
@@ -1051,6 +1120,28 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
       case T_COLS: cols_task(A, F, D, T.step, T.b, sm); break;
       case T_UPD: upd_task(A, F, T.step, T.a, T.b, sm); break;
       case T_UPDCB: updcb_task(A, F, T.a, T.b, sm); break;
+      case T_UPDB: {  // steps [j B, min((j + 1) B, lim)) of tile (a, b)
+        if (tid == 0) {  // not while a panel fallback swaps rows of this front (see panel_fallback)
+          for (;;) {
+            atomicAdd(&cnt[kCntRun], 1);
+            __threadfence();
+            if (atomicAdd(&cnt[kCntFb], 0) == 0) break;
+            atomicSub(&cnt[kCntRun], 1);
+            while (*((volatile int*)&cnt[kCntFb]) != 0) __nanosleep(256);
+          }
+        }
+        __syncthreads();
+        const int steps = (F.npiv + kNB - 1) / kNB;
+        const int lim = upd_lim(A, T.a, T.b, steps);
+        const int s0 = T.step * A.upd_batch, s1 = min(s0 + A.upd_batch, lim);
+        updcb_task(A, F, T.a, T.b, sm, s0 * kNB, min(s1 * kNB, F.npiv));
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          atomicSub(&cnt[kCntRun], 1);
+        }
+        break;
+      }
     }
     __syncthreads();
     if (A.trace && tid == 0) {
@@ -1069,7 +1160,8 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     const int steps = (F.npiv + kNB - 1) / kNB;
     // tasks that never redo data after this point count towards front
     // completion right away (overlaps the round trip with the notifications)
-    const bool early_done = T.type == T_SMALL || T.type == T_ASM || T.type == T_UPD || T.type == T_UPDCB;
+    const bool early_done =
+        T.type == T_SMALL || T.type == T_ASM || T.type == T_UPD || T.type == T_UPDCB || T.type == T_UPDB;
     if (early_done && tid == 160) done_s = (atomicAdd(&cnt[0], 1) + 1 == D.ntasks);
     if (T.type == T_DIAG || T.type == T_ROWS || T.type == T_COLS) {
       if (T.type == T_DIAG) {
@@ -1086,21 +1178,24 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
         __syncthreads();
         const unsigned long long bits = atomicAdd(&A.flagbits[D.flag_off + T.step], 0ull);
         if (!(__longlong_as_double((long long)bits) <= kLmax)) {
-          panel_fallback(A, F, D, T.step, sm);
+          panel_fallback(A, F, D, T.step, sm, cnt);
           __syncthreads();
-          if (tid == 0) __threadfence();  // publish the redone panel before releasing the updates
+          if (tid == 0) {
+            __threadfence();  // publish the redone panel before releasing the updates
+            atomicExch(&cnt[kCntFb], 0);  // deferred batches of this front may run again
+          }
           __syncthreads();
         }
         const int a0 = a0_of(F, T.step), nr = nr_of(F, D, T.step);
         // lookahead first: the next panel's tile row and column, then the bulk
         for (int x = tid; x < 2 * nr - 1; x += kDT) {
           const int ua = x < nr ? a0 : a0 + (x - nr + 1), ub = x < nr ? a0 + x : a0;
-          if (eager_tile(D, ua, ub)) notify(A, idx_upd(A, D, F, T.step, ua, ub));
+          if (eager_tile(D, ua, ub)) release_tile(A, D, F, T.step, steps, ua, ub);
         }
         __syncthreads();
         for (int x = tid; x < (nr > 1 ? (nr - 1) * (nr - 1) : 0); x += kDT) {
           const int ua = a0 + 1 + x / (nr - 1), ub = a0 + 1 + x % (nr - 1);
-          if (eager_tile(D, ua, ub)) notify(A, idx_upd(A, D, F, T.step, ua, ub));
+          if (eager_tile(D, ua, ub)) release_tile(A, D, F, T.step, steps, ua, ub);
         }
         if (T.step == steps - 1) {  // last panel: the contribution block in one pass per tile
           const int ncb = D.tiles - D.acb;
@@ -1131,6 +1226,14 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
       }
     } else if (T.type == T_ASM) {
       if (tid == 0 && steps > 0) notify(A, idx_diag(A, D, 0));
+    } else if (T.type == T_UPDB && tid == 0) {
+      const int lim = upd_lim(A, T.a, T.b, steps);
+      const int s0 = T.step * A.upd_batch, s1 = min(s0 + A.upd_batch, lim);
+      atomicAdd(&A.tile_step[D.tile_off + T.a * D.tiles + T.b], s1 - s0);
+      if (s1 < lim)
+        notify(A, A.ubase[D.ub_off + T.a * D.tiles + T.b] + T.step + 1);
+      else if (lim < steps)
+        notify(A, idx_upd(A, D, F, lim, T.a, T.b));
     }
     // front completion releases the parent's SMALL / ASM tasks
     if (!early_done && tid == 0) done_s = (atomicAdd(&cnt[0], 1) + 1 == D.ntasks);
@@ -1150,9 +1253,9 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     }
     if (tid == 0 && A.prof) {
       const long long t_end = clock64();
-      const int pt = T.type == T_UPDCB ? T_UPD : T.type;  // profiled with the updates
-      atomicAdd(&A.prof[3 * pt + 0], (unsigned long long)(t_end - t_work));
-      atomicAdd(&A.prof[3 * pt + 2], 1ull);
+      const int slot = (T.type == T_UPDCB || T.type == T_UPDB) ? 21 : 3 * T.type;  // K-batched: 21..23
+      atomicAdd(&A.prof[slot + 0], (unsigned long long)(t_end - t_work));
+      atomicAdd(&A.prof[slot + 2], 1ull);
     }
   }
 }
@@ -1166,6 +1269,8 @@ struct DagPlan {
       d_small_backup, d_deps0, d_deps, d_queue0, d_queue, d_qctl, d_qctl0, d_sb, d_trace;
   int ntasks = 0, nqueued = 0, nfronts = 0, ntile = 0, nflag = 0, grid = 148, nready = 0;
   int occ = 1, small_nf = 160;  // kernel variant (see kSmallNfLatency / kSmallNfThroughput)
+  int upd_batch = 0, upd_la = 2;  // deferred pivot-region updates (upd_lim)
+  DeviceBuffer d_ubase;
   std::vector<FrontDag> dag_h;   // host copy of the per-front plan (tile counts, acb)
   size_t smem = 0;
   double flops_upd = 0;
@@ -1197,6 +1302,18 @@ void rqb_dag_build(FactorEngine& fe) {
   // overlap the panel chain (cfg2_riga 0.85 -> 0.83 ms)
   int cb_min_steps = P->occ == 2 ? 1 : (1 << 30);
   if (const char* e = std::getenv("RQB_CB_MIN_STEPS")) cb_min_steps = std::atoi(e);
+  // deferred pivot-region updates (UPDB, see upd_lim): the throughput variant
+  // batches upd_batch panel steps per tile update and keeps the last upd_la
+  // steps before a tile's own panel per step
+  P->upd_batch = P->occ == 2 ? 8 : 0;  // measured: cfg4_riga 28.3 -> 26.8 ms, cfg4_iga 68.6 -> 61.0 ms (4: 27.0 / 62.2)
+  P->upd_la = 2;
+  if (const char* e = std::getenv("RQB_UPD_BATCH")) P->upd_batch = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("RQB_UPD_LOOKAHEAD")) P->upd_la = std::max(1, std::atoi(e));
+  std::vector<int32_t> ubase;
+  int ndead = 0;
+  auto lim_of = [&](int a, int b, int steps) {
+    return P->upd_batch > 0 ? std::min(steps, std::max(0, 2 * std::min(a, b) - P->upd_la)) : 0;
+  };
   // tasks of a front are contiguous; fronts in postorder
   for (int f = 0; f < nfr; ++f) {
     const Front& F = S.fronts[f];
@@ -1227,6 +1344,7 @@ void rqb_dag_build(FactorEngine& fe) {
     D.backup_off = backup;
     backup += 2LL * F.nf * kNB;
     D.nasm = D.tiles * div_up(D.tiles, kAsmRowTiles);
+    int front_dead = 0;
     D.bnd_off = static_cast<int32_t>(bnd.size());
     for (int32_t c : F.children) {
       const Front& C = S.fronts[c];
@@ -1268,6 +1386,11 @@ void rqb_dag_build(FactorEngine& fe) {
       const int np = std::max(0, D.acb - a0);
       auto push_upd = [&](int a, int b) {
         tasks.push_back({f, T_UPD, (int16_t)s, a, b});
+        if (s < lim_of(a, b, steps)) {  // this step's update runs inside an UPDB batch
+          deps.push_back(1 << 30);
+          ++ndead, ++front_dead;
+          return;
+        }
         deps.push_back(s == 0 ? 1 : 2);
         const double rr = std::min(F.nf, (a + 1) * kTile) - std::max(a * kTile, t0);
         const double cc = std::min(F.nf, (b + 1) * kTile) - std::max(b * kTile, t0);
@@ -1292,7 +1415,28 @@ void rqb_dag_build(FactorEngine& fe) {
           const double cc = std::min(F.nf, (b + 1) * kTile) - b * kTile;
           P->flops_upd += 2.0 * F.npiv * rr * cc;
         }
-    D.ntasks = static_cast<int32_t>(tasks.size()) - D.task_base;
+    // deferred updates: per pivot-region tile, batches of upd_batch steps over
+    // steps 0 .. lim - 1 (first batch released by its last panel, later ones
+    // also by the previous batch of the tile)
+    D.ub_off = static_cast<int32_t>(ubase.size());
+    ubase.resize(ubase.size() + static_cast<size_t>(D.tiles) * D.tiles, -1);
+    if (P->upd_batch > 0)
+      for (int a = 0; a < D.tiles; ++a)
+        for (int b = 0; b < D.tiles; ++b) {
+          if (!(a < D.acb || b < D.acb)) continue;
+          const int lim = lim_of(a, b, steps);
+          if (lim <= 0) continue;
+          ubase[D.ub_off + a * D.tiles + b] = static_cast<int32_t>(tasks.size());
+          for (int j = 0; j * P->upd_batch < lim; ++j) {
+            tasks.push_back({f, T_UPDB, (int16_t)j, a, b});
+            deps.push_back(j == 0 ? 1 : 2);
+            const int k0 = j * P->upd_batch * kNB, k1 = std::min(std::min((j + 1) * P->upd_batch, lim) * kNB, F.npiv);
+            const double rr = std::min(F.nf, (a + 1) * kTile) - a * kTile;
+            const double cc = std::min(F.nf, (b + 1) * kTile) - b * kTile;
+            P->flops_upd += 2.0 * (k1 - k0) * rr * cc;
+          }
+        }
+    D.ntasks = static_cast<int32_t>(tasks.size()) - D.task_base - front_dead;
   }
   // initial ready queue: tasks without predecessors (SMALL / ASM of leaf fronts)
   std::vector<int32_t> queue0(tasks.size(), -1);
@@ -1301,7 +1445,7 @@ void rqb_dag_build(FactorEngine& fe) {
     if (deps[t] == 0) queue0[nready++] = static_cast<int32_t>(t);
   P->nready = nready;
   P->ntasks = static_cast<int>(tasks.size());
-  P->nqueued = P->ntasks - nfused;
+  P->nqueued = P->ntasks - nfused - ndead;
   P->nfronts = nfr;
   P->ntile = std::max(1, tile_off);
   P->nflag = std::max(1, flag_off);
@@ -1318,6 +1462,8 @@ void rqb_dag_build(FactorEngine& fe) {
   P->d_rc.upload(rc_prefix.data(), sizeof(int32_t) * rc_prefix.size(), fe.stream);
   P->d_bnd.upload(bnd.data(), sizeof(int32_t) * bnd.size(), fe.stream);
   P->d_sb.upload(step_base.data(), sizeof(int32_t) * step_base.size(), fe.stream);
+  if (ubase.empty()) ubase.push_back(-1);
+  P->d_ubase.upload(ubase.data(), sizeof(int32_t) * ubase.size(), fe.stream);
   P->d_deps0.upload(deps.data(), sizeof(int32_t) * deps.size(), fe.stream);
   P->d_deps.alloc(sizeof(int32_t) * deps.size());
   P->d_queue0.upload(queue0.data(), sizeof(int32_t) * queue0.size(), fe.stream);
@@ -1421,6 +1567,9 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   RQB_CUDA(cudaMemcpyAsync(P.d_qctl.p, P.d_qctl0.p, P.d_qctl0.bytes, cudaMemcpyDeviceToDevice, fe.stream));
   DagArgs A;
   A.upd_cp16 = std::getenv("RQB_UPD_CP16") ? std::atoi(std::getenv("RQB_UPD_CP16")) : 1;
+  A.upd_batch = P.upd_batch;
+  A.upd_la = P.upd_la;
+  A.ubase = P.d_ubase.as<int32_t>();
   A.fronts = fe.d_fronts.as<FrontDev>();
   A.dag = P.d_dag.as<FrontDag>();
   A.tasks = P.d_tasks.as<Task>();
@@ -1483,7 +1632,9 @@ void rqb_dag_profile(FactorEngine& fe, double* out) {
   out[18] = fe.dag->grid;
   out[19] = fe.dag->ntasks;
   out[20] = h[20] / (clk_khz * 1.0);  // ready-queue pop wait, summed over CTAs
-  for (int i = 21; i < 24; ++i) out[i] = h[i] / (clk_khz * 1.0);  // spare profiling slots
+  out[21] = h[21] / (clk_khz * 1.0);  // UPDCB busy ms (UPD in slot 5 holds the per-step updates only)
+  out[22] = 0;
+  out[23] = static_cast<double>(h[23]);
   if (const char* path = std::getenv("RQB_DAG_TRACE")) {  // development trace: tasks + timestamps
     DagPlan& P = *fe.dag;
     std::vector<unsigned long long> tr(4 * static_cast<size_t>(P.ntasks));
@@ -1508,11 +1659,12 @@ std::string rqb_dag_stall_report(FactorEngine& fe) {
   std::vector<Task> tk(P.ntasks);
   cudaMemcpy(deps.data(), P.d_deps.p, sizeof(int32_t) * P.ntasks, cudaMemcpyDeviceToHost);
   cudaMemcpy(tk.data(), P.d_tasks.p, sizeof(Task) * P.ntasks, cudaMemcpyDeviceToHost);
-  static const char* names[] = {"SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD", "UPDCB"};
+  static const char* names[] = {"SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD", "UPDCB", "UPDB"};
   std::string out;
   int shown = 0, pending = 0;
   for (int t = 0; t < P.ntasks; ++t) {
     if (deps[t] == 0 || (tk[t].type == T_DIAG && tk[t].step > 0)) continue;  // fused DIAGs are never counted down
+    if (deps[t] >= (1 << 29)) continue;  // per-step update folded into an UPDB batch: never runs
     ++pending;
     if (shown < 6) {
       const Task& T = tk[t];

@@ -324,11 +324,14 @@ def test_solve_whole_front_items_and_determinism(name, monkeypatch):
         assert np.max(np.abs(xs[0] - x)) <= 1e-12 * np.max(np.abs(xs[0]))
 
 
-@pytest.mark.parametrize("name,occ", [("cfg1", "1"), ("cfg1", "2"), ("cfg2_riga", "1")])
-def test_pivoting_in_every_front_vs_oracle(name, occ, monkeypatch):
+@pytest.mark.parametrize("name,occ,batch", [("cfg1", "1", None), ("cfg1", "2", None), ("cfg2_riga", "1", None),
+                                            ("cfg2_riga", "2", "2"), ("cfg2_riga", "2", "4")])
+def test_pivoting_in_every_front_vs_oracle(name, occ, batch, monkeypatch):
     """Threshold pivoting inside a multifrontal tree (the BASELINE pencils never
     swap): cfg1's pattern with random values and a weak diagonal, so most
-    fronts swap. Both kernel variants: occ 1 (SMALL fronts up to nf 160, the
+    fronts swap. Both kernel variants (and the throughput variant's deferred
+    UPDB batches of 2 and 4 steps with a 1-step lookahead, so row swaps of the
+    fallback meet pending batches): occ 1 (SMALL fronts up to nf 160, the
     exact warp-shuffle panel), occ 2 (SMALL up to 118: the 119..145 fronts take
     the tiled path, whose speculative panel fails and is redone by the exact
     fallback with contribution rows and children present); cfg2 rIGA's fronts
@@ -341,8 +344,13 @@ def test_pivoting_in_every_front_vs_oracle(name, occ, monkeypatch):
     rows = np.repeat(np.arange(P.n), np.diff(P.rowptr))
     Q[P.col == rows] *= 0.01
     monkeypatch.setenv("RQB_DAG_OCC", occ)
+    if batch:  # deferred (UPDB) updates with threshold-pivoting fallbacks in flight
+        monkeypatch.setenv("RQB_UPD_BATCH", batch)
+        monkeypatch.setenv("RQB_UPD_LOOKAHEAD", "1")
     f = rq.lu_factorize((P.rowptr, P.col, Q), o)
     monkeypatch.delenv("RQB_DAG_OCC")
+    monkeypatch.delenv("RQB_UPD_BATCH", raising=False)
+    monkeypatch.delenv("RQB_UPD_LOOKAHEAD", raising=False)
     of = oracle.Factor(P.n, P.rowptr, P.col, Q, P.box, P.elems)
     assert f.info()["swaps"] == of.swaps > 0
     worst = 0.0

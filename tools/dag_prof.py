@@ -13,10 +13,12 @@ for cfg in sys.argv[1:]:
     out = np.zeros(24)
     _lib.check(_lib.lib.rq_factor_dag_profile(f._h, out))
     info = f.info()
-    names = ["SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD(+CB)"]
+    names = ["SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD"]
     print(f"{cfg}: factor {info['factor_ms']:.3f} ms {info['gflops']:.1f} GF/s grid {int(out[18])} tasks {int(out[19])} popwait {out[20]:.2f} ms"
           f" flops {o.stats['flops_lu']:.3e} max_front {o.stats['max_front']}")
     for t, nm in enumerate(names):
         busy, wait, cnt = out[3 * t:3 * t + 3]
         if cnt:
-            print(f"   {nm:6s} n={int(cnt):7d} busy={busy:9.3f} ms (avg {busy / cnt * 1e3:8.2f} us) wait={wait:9.3f} ms (avg {wait / cnt * 1e3:8.2f} us)")
+            print(f"   {nm:6s} n={int(cnt):7d} busy={busy:9.3f} ms (avg {busy / cnt * 1e3:8.2f} us)")
+    if out[23]:
+        print(f"   UPDCB  n={int(out[23]):7d} busy={out[21]:9.3f} ms (avg {out[21] / out[23] * 1e3:8.2f} us)")
