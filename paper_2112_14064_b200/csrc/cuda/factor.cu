@@ -742,12 +742,14 @@ void FactorEngine::enqueue_factor(KernelTimer* kt) {
   int32_t* ipiv = d_ipiv.as<int32_t>();
   int* flags = d_flags.as<int>();
   RQB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, stream));
-  RQB_CUDA(cudaMemsetAsync(pool, 0, sizeof(double) * sym.pool, stream));
-  B(0);
-  scatter_original<<<std::min<int64_t>(div_up(nnz, 256), 148 * 16), 256, 0, stream>>>(
-      d_aval.as<double>(), d_qdst.as<int64_t>(), nnz, pool);
-  E();
-  launches += 1;
+  if (!(use_dag && dag_lazy)) {
+    RQB_CUDA(cudaMemsetAsync(pool, 0, sizeof(double) * sym.pool, stream));
+    B(0);
+    scatter_original<<<std::min<int64_t>(div_up(nnz, 256), 148 * 16), 256, 0, stream>>>(
+        d_aval.as<double>(), d_qdst.as<int64_t>(), nnz, pool);
+    E();
+    launches += 1;
+  }
   if (use_dag) {
     B(6);
     rqb_dag_enqueue(*this);

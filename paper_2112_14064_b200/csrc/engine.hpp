@@ -97,6 +97,7 @@ struct FactorEngine {
   // factorization schedule: persistent task-DAG kernel (default) or the
   // level-synchronous multi-launch path (RQB_FACTOR=level, kept for A/B runs)
   bool use_dag = true;
+  bool dag_lazy = false;  // the DAG tasks zero + assemble their own regions (no pool memset / scatter launch)
   std::unique_ptr<DagPlan, DagPlanDeleter> dag;
   int dag_ntasks = 0;
   bool dag_prof_enabled = false;
