@@ -126,6 +126,7 @@ struct DagArgs {
   const int32_t* step_base;  // FrontDag::sb_off: first task of every panel step
   int upd_cp16;              // UPD operands by 16-byte cp.async (RQB_UPD_CP16=0: 8-byte copies)
   int upd_batch;             // deferred updates: panel steps per UPDB task (0: every update per step)
+  int upd_tma;               // UPDCB / UPDB operand stages by TMA bulk copies (RQB_UPD_TMA=1)
   int upd_la;                // lookahead: the last upd_la steps before a tile's panel stay per step
   const int32_t* ubase;      // FrontDag::ub_off
   // lazy assembly: the SMALL / ASM task that owns a pool region zeroes it and
@@ -812,6 +813,30 @@ __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int 
 
 
 
+// TMA bulk copies (cp.async.bulk, the copy engine: UBLKCP) completing on a
+// shared-memory mbarrier (transaction bytes)
+__device__ __forceinline__ void mbar_init(unsigned long long* mb, int count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(mb));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mb, unsigned bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(mb));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(mb));
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, unsigned long long* mb) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const unsigned m = static_cast<unsigned>(__cvta_generic_to_shared(mb));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+               "l"(gmem), "r"(bytes), "r"(m) : "memory");
+}
+
 // Contribution-block tile (a, b): C -= L(rows a, 0:npiv) U(0:npiv, cols b) in
 // one pass, K in chunks of 32 staged by cp.async (two buffers: the next chunk
 // is in flight while DMMA consumes the current one), C read once and written
@@ -829,13 +854,43 @@ __device__ void updcb_task(const DagArgs& A, const FrontDev& F, int a, int b, do
   const int lane = tid & 31, warp = tid >> 5;  // 8 warps: 2 (m) x 4 (n) of 32 x 16
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
   const int gid = lane >> 2, tig = lane & 3;
-  // stage: As [kk][m] (stride kTSP) then Bs [n][kk] (stride kBLD); both filled
-  // with 16-byte copies (pairs along m of an L column, along kk of a U column)
+  // stage: As [kk][m] (stride kTSP) then Bs [n][kk] (stride kBLD), filled by
+  // 16-byte cp.async (pairs along m of an L column, along kk of a U column)
+  // with zero fill; with RQB_UPD_TMA=1 full 64 x 64 tiles and full 32-pivot
+  // chunks arrive by TMA bulk copies instead (warp 0 issues the 32 L column
+  // segments of 512 B and the 64 U column segments of 256 B, completion on the
+  // stage's mbarrier)
   constexpr int kStage = kNB * kTSP + kTile * kBLD;
+  __shared__ unsigned long long mbar[2];
+  // measured (cfg4_riga): 96 bulk transfers of 256 / 512 B per chunk are slower
+  // than 256 threads of 16-byte cp.async (UPDCB tile 18.8 -> 29.4 us, factor
+  // 25.5 -> 28.5 ms), so the bulk path is opt-in (RQB_UPD_TMA=1)
+  const bool bulk_tile = A.upd_tma && nr == kTile && nc == kTile;
+  auto bulk_chunk = [&](int chunk) { return bulk_tile && kb + (chunk + 1) * kNB <= K; };
+  if (bulk_tile) {
+    if (tid == 0) {
+      mbar_init(&mbar[0], 1);
+      mbar_init(&mbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   auto issue = [&](int chunk, int buf) {
     double* As = sm + buf * kStage;
     double* Bs = As + kNB * kTSP;
     const int k0 = kb + chunk * kNB;
+    if (bulk_chunk(chunk)) {
+      if (tid < 32) {  // warp 0: one L column segment and two U column segments per lane
+        if (tid == 0) mbar_expect_tx(&mbar[buf], kNB * kTile * 8 * 2);
+        // the stage was last read through the generic proxy
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        bulk_g2s(&As[tid * kTSP], &g[r0 + (int64_t)(k0 + tid) * ld], kTile * 8, &mbar[buf]);
+        bulk_g2s(&Bs[tid * kBLD], &g[k0 + (int64_t)(c0 + tid) * ld], kNB * 8, &mbar[buf]);
+        bulk_g2s(&Bs[(tid + 32) * kBLD], &g[k0 + (int64_t)(c0 + tid + 32) * ld], kNB * 8, &mbar[buf]);
+      }
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < kNB * kTile / 2 / kDT; ++i) {
       const int idx = tid + i * kDT;
@@ -872,8 +927,10 @@ __device__ void updcb_task(const DagArgs& A, const FrontDev& F, int a, int b, do
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[x][y][e] = 0.0;
   for (int ch = 0; ch < nchunks; ++ch) {
-    if (ch + 1 < nchunks) {
-      issue(ch + 1, (ch + 1) & 1);
+    if (ch + 1 < nchunks) issue(ch + 1, (ch + 1) & 1);
+    if (bulk_chunk(ch)) {
+      mbar_wait(&mbar[ch & 1], (ch >> 1) & 1);
+    } else if (ch + 1 < nchunks && !bulk_chunk(ch + 1)) {
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -1698,6 +1755,7 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   DagArgs A;
   A.upd_cp16 = std::getenv("RQB_UPD_CP16") ? std::atoi(std::getenv("RQB_UPD_CP16")) : 1;
   A.upd_batch = P.upd_batch;
+  A.upd_tma = std::getenv("RQB_UPD_TMA") ? std::atoi(std::getenv("RQB_UPD_TMA")) : 0;
   A.upd_la = P.upd_la;
   A.ubase = P.d_ubase.as<int32_t>();
   A.lazy = P.lazy;

@@ -471,3 +471,21 @@ def test_krylov_schur_restart_invariants(cfg1):
         assert np.min(np.abs(kept - t)) <= 1e-10 * abs(t)
     V2, H2, p2 = op.krylov_schur_restart(V, H, m)
     assert p2 == m and np.array_equal(V2, V) and np.array_equal(H2, H)
+
+
+def test_tma_bulk_staging_path_matches_oracle(monkeypatch):
+    """The opt-in TMA bulk-copy staging of the K-batched Schur updates
+    (RQB_UPD_TMA=1, cp.async.bulk + mbarrier) gives the oracle's factors."""
+    P = rq.baseline_config("cfg3_iga")
+    o = rq.nested_dissection_order(P)
+    Q = P.q_values(SIGMA)
+    monkeypatch.setenv("RQB_UPD_TMA", "1")
+    f = rq.lu_factorize((P.rowptr, P.col, Q), o)
+    b = np.random.default_rng(8).standard_normal(P.n)
+    x = f.solve(b)
+    monkeypatch.delenv("RQB_UPD_TMA")
+    g = rq.lu_factorize((P.rowptr, P.col, Q), o)
+    x2 = g.solve(b)
+    assert np.max(np.abs(x - x2)) <= 1e-9 * np.max(np.abs(x2))
+    A = P.to_scipy("K") + SIGMA * P.to_scipy("C") + SIGMA ** 2 * P.to_scipy("M")
+    assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) <= 1e-9
