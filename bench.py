@@ -313,9 +313,9 @@ def run_b200(args):
     solve_bytes = st["trisolve_bytes"]
     spmv_bytes = 20.0 * P.nnz + 8.0 * (P.n + 1) + 24.0 * P.n
     gemv_bytes = 8.0 * 2 * P.n * m
-    keep = nev + min(20, m - nev - 1)
-    rst_flops = 2.0 * 2 * P.n * m * keep
-    rst_bytes = 8.0 * 2 * P.n * (m + keep)
+    # rq_operator_time(7, param m): X (2n x m) = V (2n x m) Q (m x m) on the DMMA GEMM (vq_gemm)
+    rst_flops = 2.0 * 2 * P.n * m * m
+    rst_bytes = 8.0 * 2 * P.n * (m + m)
 
     def hb(ms, b):
         return {"ms": round(ms, 4), "gbs": round(b / (ms * 1e6), 1), "frac_hbm": round(b / (ms * 1e6) / hbm, 4)}
@@ -325,8 +325,9 @@ def run_b200(args):
         "spmv_fused_cm": hb(t_spmv, spmv_bytes),
         "cgs_gemv_t": dict(hb(t_gt, gemv_bytes), k=m),
         "cgs_gemv_n": dict(hb(t_gn, gemv_bytes), k=m),
-        "restart_vq": {"ms": round(t_rst, 4), "m": m, "keep": keep,
+        "restart_vq": {"kernel": "vq_gemm (DMMA)", "ms": round(t_rst, 4), "shape": f"2n x {m} x {m}",
                        "tflops": round(rst_flops / (t_rst * 1e9), 2),
+                       "frac_fp64": round(rst_flops / (t_rst * 1e9) / FP64_PEAK_TFLOPS, 4),
                        "gbs": round(rst_bytes / (t_rst * 1e6), 1)},
     }
     if single:

@@ -257,6 +257,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
   };
   double t_graph_build = 0;
+  static const bool trace_cycles = std::getenv("RQB_EIGS_TRACE") != nullptr;  // per-cycle stderr line
   const double t_setup = ms_since(t0);
   auto& graphs = W.graphs;
 
@@ -636,6 +637,10 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
                                  sizeof(double) * n2, cudaMemcpyDeviceToDevice, st), "D2D Bv");
     }
     t_restart += ms_since(trs0);
+    if (trace_cycles)
+      std::fprintf(stderr, "[eigs] cycle %d: steps %d..%d, checked %d (maybe %d, nconv %d), groups %zu, kept %d%s, "
+                   "t ritz %.1f check %.1f restart %.1f sync %.1f ms\n", cycles, k, m, maybe ? nchk : 0, (int)maybe,
+                   nconv_now, groups.size(), p, deflate ? " (deflated restart)" : "", t_ritz, t_check, t_restart, t_sync);
     k = p;
   }
   op.fac->check_sweeps();  // watchdog of the triangular sweeps (syncs the stream)
