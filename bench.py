@@ -287,16 +287,22 @@ def run_b200(args):
                      "paper_ratio_note": "PAPER.md:916: LU-FLOP improvement IGA/rIGA, p=3, ne=1024 (MUMPS/METIS)"}
         del opI, PI
 
-    # ---- time to nev eigenpairs (device-resident pencil; factor + Krylov-Schur)
-    t_nev, infos = [], []
-    for _ in range(max(1, args.nev_runs)):
+    # ---- time to nev eigenpairs (device-resident pencil; factor + Krylov-Schur).
+    # The requested pairs are copies of one hugely degenerate eigenvalue, so a
+    # single-vector Krylov-Schur collects them through rounding and its cycle
+    # count moves with the start vector and the last bits of the factors
+    # (cfg4_riga: 16-61 cycles): the line reports the median over seeds
+    # 0 .. nev_seeds-1 (one run each after the first, cold call on seed 0).
+    t_nev, infos, resid_max = [], [], 0.0
+    seeds = [0] + list(range(max(1, args.nev_seeds)))
+    for s_ in seeds:
         t0 = time.perf_counter()
-        pairs = op.solve_quadratic(nev, eps=1e-10, seed=0, max_restarts=args.max_restarts,
+        pairs = op.solve_quadratic(nev, eps=1e-10, seed=s_, max_restarts=args.max_restarts,
                                    raise_partial=False)
         t_nev.append((time.perf_counter() - t0) * 1e3 + op.factor_info()["factor_ms"])
         infos.append(op.last_info)
-    resid_max = max(p.residual for p in pairs)
-    info = infos[-1]
+        resid_max = max(resid_max, max(p.residual for p in pairs))
+    info = infos[1]
 
     # ---- per-kernel profile of one factorization (un-graphed, events per launch)
     ms_k = np.zeros(7)
@@ -424,7 +430,7 @@ def run_b200(args):
                  "peak_source": f"fp64: measured DMMA m16n8k4 rate, tools/fp64_peak.cu "
                                 f"(MEASURED_PEAKS.json has no FP64 entry); hbm: {peak_src} "
                                 f"MEASURED_PEAKS.json"})
-    first, rest = t_nev[0], t_nev[1:] or t_nev
+    first, rest = t_nev[0], sorted(t_nev[1:])
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": ws,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 4),
@@ -437,11 +443,16 @@ def run_b200(args):
                    "l2": "flushed (256 MiB scrub) before every timed step"},
         "factor_frac_fp64": round(value / ws / (FP64_PEAK_TFLOPS * 1e3), 5),
         "iga_companion": companion,
-        "time_to_nev_ms": round(min(rest), 3), "time_to_nev_first_call_ms": round(first, 3),
-        "time_to_nev_runs_ms": [round(t, 2) for t in t_nev],
-        "time_to_nev_note": "factor + Krylov-Schur to nev converged pairs on the device-resident operator; "
-                            "the first call also allocates the Krylov workspace and captures the cycle graphs",
+        "time_to_nev_ms": round(rest[len(rest) // 2], 3), "time_to_nev_first_call_ms": round(first, 3),
+        "time_to_nev_min_ms": round(rest[0], 3), "time_to_nev_max_ms": round(rest[-1], 3),
+        "time_to_nev_seeds": {str(s_): {"ms": round(t, 1), "cycles": i.get("restarts"), "n_fb": i.get("n_fb")}
+                              for s_, t, i in zip(seeds[1:], t_nev[1:], infos[1:])},
+        "time_to_nev_note": "median over start-vector seeds of factor + Krylov-Schur to nev converged pairs on the "
+                            "device-resident operator (the degenerate cluster makes the cycle count seed- and "
+                            "rounding-dependent); first_call = seed 0 on a fresh operator, which also allocates "
+                            "the Krylov workspace and captures the cycle graphs",
         "eigs_residual_max": resid_max,
+        "eigs_residual_tol": 1e-10,
         "eigs": {k: info.get(k) for k in ("restarts", "guard_passes", "n_fb", "n_mv", "n_vv",
                                           "launches", "restart_defect")},
         "kernels": kernels,
@@ -478,7 +489,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg4_riga", choices=sorted(NEV))
     ap.add_argument("--nev", type=int, default=0)
-    ap.add_argument("--nev-runs", type=int, default=3)
+    ap.add_argument("--nev-seeds", type=int, default=5)
     ap.add_argument("--max-restarts", type=int, default=1000)
     ap.add_argument("--cpu-samples", type=int, default=1)
     ap.add_argument("--cpu-step-split", type=int, default=1)
