@@ -335,10 +335,12 @@ __device__ __forceinline__ double block_dot(const double* lp, int64_t ld, const 
 
 // diagonal tile solve in warp 0 (lane holds rows lane, lane + 32): v <- D v
 // with D the tile's inverse; 64 broadcasts, two independent FMA chains per row
-__device__ __forceinline__ void tile_apply(const double* D, int lane, double& v0, double& v1) {
+// (only the tile's nr columns: the padding of D is zero; small fronts near
+// the leaves have 20-40 pivots)
+__device__ __forceinline__ void tile_apply(const double* D, int lane, double& v0, double& v1, int nr = kRB) {
   double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-#pragma unroll
-  for (int c = 0; c < kRB; c += 2) {
+#pragma unroll 8
+  for (int c = 0; c < nr; c += 2) {
     const double x0 = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31);
     const double x1 = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, (c + 1) & 31);
     a0 += D[lane + c * (kRB + 1)] * x0;
@@ -402,7 +404,13 @@ __device__ __forceinline__ void stream_rows2(const double* g, int64_t ld, const 
 __device__ __forceinline__ void fwd_whole(const SweepArgs& A, const SolveItem& I, const double* g, int64_t ld,
                                           double* D, double* wy, double (*part)[kRB], int tid) {
   const int np = I.np, nf = I.nf;
-  if (tid == 0) prefetch_l2(g, sizeof(double) * (size_t)np * ld);  // L columns: one contiguous range
+  if (tid == 0) {
+    prefetch_l2(g, sizeof(double) * (size_t)np * ld);  // L columns: one contiguous range
+    for (int blk = 1; blk < I.npb; ++blk) {            // the later tile inverses
+      const int nr = min(np, blk * kRB + kRB) - blk * kRB;
+      prefetch_l2(A.dinv + I.doff + (int64_t)kRB * kRB * blk, sizeof(double) * nr * nr);
+    }
+  }
   {
     constexpr int kQ = kStage / kST;
     int4 src[kQ];
@@ -411,6 +419,9 @@ __device__ __forceinline__ void fwd_whole(const SweepArgs& A, const SolveItem& I
       const int r = tid + q * kST;
       src[q] = r < nf ? __ldg(&A.gsrc[I.rows_off + r]) : make_int4(-1, -1, -1, 0);
     }
+    // the first tile inverse travels with the gather table (one round trip
+    // instead of two before the first triangle)
+    if (I.npb > 0) load_dinv<false>(D, A.dinv + I.doff, min(np, kRB), tid);
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       double v = 0.0;
@@ -424,7 +435,7 @@ __device__ __forceinline__ void fwd_whole(const SweepArgs& A, const SolveItem& I
   if (I.npb == 0) __syncthreads();
   for (int blk = 0; blk < I.npb; ++blk) {
     const int r0 = blk * kRB, nr = min(np, r0 + kRB) - r0;
-    load_dinv<false>(D, A.dinv + I.doff + (int64_t)kRB * kRB * blk, nr, tid);
+    if (blk > 0) load_dinv<false>(D, A.dinv + I.doff + (int64_t)kRB * kRB * blk, nr, tid);
     double s = 0.0;
     if (row < nr && r0 > 0) s = stream_cols(g + r0 + row, ld, wy, 0, r0, grp);
     part[grp][row] = s;
@@ -434,7 +445,7 @@ __device__ __forceinline__ void fwd_whole(const SweepArgs& A, const SolveItem& I
       double v1 = tid + 32 < nr ? wy[r0 + tid + 32] -
                                       (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32])
                                 : 0.0;
-      tile_apply(D, tid, v0, v1);
+      tile_apply(D, tid, v0, v1, nr);
       if (tid < nr) A.y[I.start + r0 + tid] = wy[r0 + tid] = v0;
       if (tid + 32 < nr) A.y[I.start + r0 + tid + 32] = wy[r0 + tid + 32] = v1;
     }
@@ -469,8 +480,10 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
   for (;;) {
     __syncthreads();
     if (tid == 0) {
+      const unsigned long long tp = A.trace ? gtime() : 0;
       item_s = keep_s >= 0 ? keep_s : pop_item(A);
       keep_s = -1;
+      if (A.trace && item_s >= 0) A.trace[8 * (size_t)item_s + 4] = tp;  // pop began (whole items: slot 4 free)
     }
     __syncthreads();
     const int it = item_s;
@@ -582,7 +595,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) fwd_sweep(SweepArgs A) {
           double v1 = tid + 32 < nr
                           ? wv[tid + 32] - (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32])
                           : 0.0;
-          tile_apply(D, tid, v0, v1);
+          tile_apply(D, tid, v0, v1, nr);
           if (A.trace && tid == 0) A.trace[8 * (size_t)it + 7] = gtime();
           if (tid < nr) st_relaxed(&A.y[I.start + r0 + tid], v0);
           if (tid + 32 < nr) st_relaxed(&A.y[I.start + r0 + tid + 32], v1);
@@ -671,6 +684,11 @@ __device__ __forceinline__ void bwd_whole(const SweepArgs& A, const SolveItem& I
   constexpr int kCbBase = kWholeNpb * kRB;  // xs: [0, np) this front's x, [kCbBase, ...) x_cb
   const int np = I.np, nf = I.nf, ncb = nf - np;
   prefetch_u12(g, ld, np, nf, tid);
+  if (tid == 0)  // the tile inverses, needed after the U12 product
+    for (int blk = 0; blk < I.npb; ++blk) {
+      const int nr = min(np, blk * kRB + kRB) - blk * kRB;
+      prefetch_l2(A.dinv + I.doff + (int64_t)kRB * kRB * blk, sizeof(double) * nr * nr);
+    }
   {
     constexpr int kQ = kStage / kST;
     int src[kQ];
@@ -715,7 +733,7 @@ __device__ __forceinline__ void bwd_whole(const SweepArgs& A, const SolveItem& I
       double v1 = tid + 32 < nr ? pv[r0 + tid + 32] -
                                       (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32])
                                 : 0.0;
-      tile_apply(D, tid, v0, v1);
+      tile_apply(D, tid, v0, v1, nr);
       if (tid < nr) {
         xs[r0 + tid] = v0;
         store_x(A, I.start + r0 + tid, v0);
@@ -871,7 +889,7 @@ __global__ void __launch_bounds__(kST, kMinBlocks) bwd_sweep(SweepArgs A) {
         if (tid < nr) v0 = y0 - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]);
         if (tid + 32 < nr)
           v1 = y1 - (part[0][tid + 32] + part[1][tid + 32] + part[2][tid + 32] + part[3][tid + 32]);
-        tile_apply(D, tid, v0, v1);
+        tile_apply(D, tid, v0, v1, nr);
         if (A.trace && tid == 0) A.trace[8 * (size_t)it + 7] = gtime();
         for (int h = 0; h < 2; ++h) {
           const int r = tid + 32 * h;

@@ -4,7 +4,7 @@ import numpy as np
 sys.path.insert(0, ".")
 cfg = sys.argv[1]
 nf_, nb_, t, parent, npiv, nf, level = pickle.load(open(f"gpurun_out/solve_trace_{cfg}.pkl", "rb"))
-kWholeNpb, kWholeCb = int(sys.argv[2]) if len(sys.argv) > 2 else 2, 1024
+kWholeNpb, kWholeCb = int(sys.argv[2]) if len(sys.argv) > 2 else 2, 1024 - 2 * 64
 npb = (npiv + 63) // 64; ncbb = (nf - npiv + 63) // 64
 nfr = len(npb)
 lvl_count = np.bincount(level)
