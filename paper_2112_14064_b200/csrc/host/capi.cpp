@@ -560,6 +560,7 @@ int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, doub
     eo.seed = opts->seed;
     eo.max_restarts = opts->max_restarts > 0 ? opts->max_restarts : 100;
     eo.guard = opts->guard;
+    if (const char* e = std::getenv("RQB_GUARD_CLUSTER")) eo.guard_single_cluster = std::atoi(e);
     eo.profile = opts->profile;
     eo.want_vectors = (vec_re && vec_im) ? 1 : 0;
     o->ledger = rqb::Ledger{};

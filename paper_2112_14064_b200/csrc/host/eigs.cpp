@@ -490,17 +490,24 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     for (int c = 0; c < nev; ++c) last_cand.push_back(rz[cand[c]]);
     last_res.assign(cres.begin(), cres.begin() + nev);
 
-    auto capture_set = [&]() {
+    // the returned set: checked positions pos[0..nev) (default: the nev nearest)
+    auto capture_set = [&](std::vector<int> pos) {
+      if (pos.empty())
+        for (int c = 0; c < nev; ++c) pos.push_back(c);
       final_set.clear();
-      final_res.assign(cres.begin(), cres.begin() + nev);
-      final_block.assign(cblock.begin(), cblock.begin() + nev);
-      for (int c = 0; c < nev; ++c) final_set.push_back(rz[cand[c]]);
+      final_res.clear();
+      final_block.clear();
+      for (int c : pos) {
+        final_set.push_back(rz[chk[c]]);
+        final_res.push_back(cres[c]);
+        final_block.push_back(cblock[c]);
+      }
       if (o.want_vectors) {
         final_vecs_re.assign(static_cast<size_t>(n) * nev, 0.0);
         final_vecs_im.assign(static_cast<size_t>(n) * nev, 0.0);
         for (int c = 0; c < nev; ++c) {
           for (int part = 0; part < 2; ++part) {
-            op.ritz_extract(dX.as<double>(), last_nchk, c, part, dW.as<double>());
+            op.ritz_extract(dX.as<double>(), last_nchk, pos[c], part, dW.as<double>());
             cuda_check(cudaMemcpyAsync((part ? final_vecs_im : final_vecs_re).data() + static_cast<size_t>(c) * n,
                                        dW.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H x");
           }
@@ -515,6 +522,46 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       }
     };
 
+    // One degenerate cluster: every one of the nev nearest Ritz values is a
+    // member of the nearest group. The guard exists for the case where fewer
+    // copies of the nearest eigenvalue than requested were found and farther
+    // values filled the set; here the set cannot move closer, so the solve ends
+    // as soon as nev members of the cluster have converged explicitly (in
+    // conjugate pairs), whether or not they are exactly the nev nearest by a
+    // 1e-12 margin: all are the same eigenvalue. Without this a
+    // cluster larger than the space fills it with unconverged copies and the
+    // solve stagnates at a few new steps a cycle (cfg4_iga: 98 of the nev
+    // nearest converged for 1000 cycles).
+    std::vector<int> cluster_pos;
+    if (maybe && o.guard_single_cluster) {
+      const int g0 = group_of[cand[0]];
+      bool one = true;
+      for (int c = 1; c < nev && one; ++c) one = group_of[cand[c]] == g0;
+      if (one) {
+        std::vector<int> pp, nn;
+        for (int c = 0; c < nchk; ++c)
+          if (cres[c] <= o.tol && group_of[chk[c]] == g0)
+            (rz[chk[c]].lambda.imag() >= 0 ? pp : nn).push_back(c);
+        if (pp.empty() || nn.empty()) {  // a real cluster: any converged members
+          for (int c : pp) if (static_cast<int>(cluster_pos.size()) < nev) cluster_pos.push_back(c);
+          for (int c : nn) if (static_cast<int>(cluster_pos.size()) < nev) cluster_pos.push_back(c);
+        } else {
+          for (size_t k = 0; k < std::min(pp.size(), nn.size()) && static_cast<int>(cluster_pos.size()) + 2 <= nev; ++k)
+            cluster_pos.push_back(pp[k]), cluster_pos.push_back(nn[k]);
+          if (static_cast<int>(cluster_pos.size()) < nev && nev % 2 == 1) {
+            const size_t k = cluster_pos.size() / 2;
+            if (k < pp.size()) cluster_pos.push_back(pp[k]);
+          }
+        }
+        if (static_cast<int>(cluster_pos.size()) != nev) cluster_pos.clear();
+      }
+    }
+    if (!cluster_pos.empty()) {
+      capture_set(cluster_pos);
+      converged_final = true;
+      break;
+    }
+
     // ---- decide: done / guard (deflated) restart / normal restart ----
     std::vector<int> sel(m, 0);
     int p = 0;
@@ -526,7 +573,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       bool improved = prev_guard_dists.empty();
       for (size_t i = 0; i < dists.size() && !improved; ++i)
         if (dists[i] < prev_guard_dists[i] * (1.0 - 1e-8)) improved = true;
-      capture_set();
+      capture_set({});
       if (!o.guard || !improved || guard_passes >= o.max_guard) {
         converged_final = true;
         break;

@@ -47,6 +47,7 @@ struct EigsOptions {
   int max_restarts = 100;
   int guard = 1;
   int max_guard = 64;
+  int guard_single_cluster = 1;  // 0: run the guard pass even when every pair is one converged cluster
   double est_factor = 1e3;  // candidates are checked explicitly once est <= est_factor * tol
   int want_vectors = 0;
   int profile = 0;
