@@ -58,6 +58,10 @@ constexpr int kTile = 64;         // big-front tile edge
 constexpr int kTSP = kTile + 4;   // padded smem stride of DMMA operand tiles
 constexpr double kLmax = 10.0 * (1.0 - 1e-14);  // 1/threshold, conservative
 constexpr int kAsmRowTiles = 8;  // parent rows per extend-add task: 8 tiles
+// ROWS / COLS tasks cover up to kRCMax tiles (one row / column per thread:
+// with 64-row tiles only a quarter of the CTA worked and every tile paid the
+// task's fixed latency); DagArgs::rc_group <= kRCMax at run time
+constexpr int kRCMax = 4;
 constexpr int kCnt = 7;  // per-front counters: tasks, asm, diag, rc, released, batches running, fallback
 constexpr int kCntRun = 5, kCntFb = 6;
 // Two configurations of the persistent kernel, chosen per factorization
@@ -127,6 +131,7 @@ struct DagArgs {
   int upd_cp16;              // UPD operands by 16-byte cp.async (RQB_UPD_CP16=0: 8-byte copies)
   int upd_batch;             // deferred updates: panel steps per UPDB task (0: every update per step)
   int upd_tma;               // UPDCB / UPDB operand stages by TMA bulk copies (RQB_UPD_TMA=1)
+  int rc_group;              // tiles per ROWS / COLS task (1 .. kRCMax)
   int upd_la;                // lookahead: the last upd_la steps before a tile's panel stay per step
   const int32_t* ubase;      // FrontDag::ub_off
   // lazy assembly: the SMALL / ASM task that owns a pool region zeroes it and
@@ -269,6 +274,17 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
 // c in [c0, c1), DMMA on 16 x 32 warp tiles: L(r, k) = Lb[r + k * ldl],
 // U(k, c) = Ub[k + (c - uoff) * ldu], dst(r, c) = D[r + (c - doff) * ldd]
 // (shared memory, or the front in global memory when kGlobal).
+__device__ __forceinline__ void cp_async8z(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 8 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
+
+// 16-byte cp.async of two consecutive doubles, `n` of them valid (zero fill)
+__device__ __forceinline__ void cp_async16z(double* smem, const double* gmem, int n) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(8 * n) : "memory");
+}
 template <bool kGlobal>
 __device__ __forceinline__ void cross_update(const double* Lb, int ldl, const double* Ub, int ldu, int uoff,
                                              double* D, int64_t ldd, int doff, int r0, int r1, int c0,
@@ -595,15 +611,15 @@ __device__ void diag_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
 // row (forward substitution with the factored block), track max|l| over the
 // fully-summed rows (threshold verification), back the panel rows up first.
 __device__ void rows_task(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s, int a,
-                          double* sm) {
+                          double* sm, int ntl) {
   const int k = s * kNB, w = min(kNB, F.npiv - k), np = F.npiv;
-  const int r0 = max(a * kTile, k + w), r1 = min(a * kTile + kTile, F.nf);
-  const int nr = r1 - r0;
+  const int r0 = max(a * kTile, k + w), r1 = min((a + ntl) * kTile, F.nf);
+  const int nr = r1 - r0;  // <= kRCMax * 64 = kDT: one row per thread
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
   const int tid = threadIdx.x;
-  constexpr int kPS = kTile + 1;   // stride of the 64-row panel block
-  double* P = sm;                 // 64 rows x 32 columns
+  constexpr int kPS = kRCMax * kTile + 1;  // stride of the panel rows block
+  double* P = sm;                 // up to 256 rows x 32 columns
   double* U = sm + kPS * kNB;     // 32 x 33 factored diagonal block
   double* red = U + 32 * 33;
   double* bk = A.backup + D.backup_off;
@@ -615,20 +631,24 @@ __device__ void rows_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
       vu[i] = (r < w && c < w) ? __ldcg(&g[(k + r) + (int64_t)(k + c) * ld]) : (r == c ? 1.0 : 0.0);
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int idx = tid + i * kDT, r = idx % kTile, c = idx / kTile;
-      vp[i] = (r < nr && c < w) ? __ldcg(&g[(r0 + r) + (int64_t)(k + c) * ld]) : 0.0;
-    }
-#pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int idx = tid + i * kDT;
       U[(idx % 32) + (idx / 32) * 33] = vu[i];
     }
+    // the panel rows, kTile x 32 per round (a round's loads all in flight;
+    // measured: one cp.async pass over all rounds was slower)
+    for (int t = 0; t < ntl; ++t) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int idx = tid + i * kDT, r = idx % kTile, c = idx / kTile;
-      P[r + c * kPS] = vp[i];
-      if (r < nr && c < w) bk[(r0 + r) + (int64_t)c * F.nf] = vp[i];
+      for (int i = 0; i < 8; ++i) {
+        const int idx = tid + i * kDT, r = t * kTile + idx % kTile, c = idx / kTile;
+        vp[i] = (r < nr && c < w) ? __ldcg(&g[(r0 + r) + (int64_t)(k + c) * ld]) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int idx = tid + i * kDT, r = t * kTile + idx % kTile, c = idx / kTile;
+        P[r + c * kPS] = vp[i];
+        if (r < nr && c < w) bk[(r0 + r) + (int64_t)c * F.nf] = vp[i];
+      }
     }
   }
   __syncthreads();
@@ -661,15 +681,15 @@ __device__ void rows_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
 // COLS: columns of tile column b right of the block: U12 = inv(L11) A12 by
 // forward substitution with the unit-lower factored block (column per thread).
 __device__ void cols_task(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s, int b,
-                          double* sm) {
+                          double* sm, int ntl) {
   const int k = s * kNB, w = min(kNB, F.npiv - k);
-  const int c0 = max(b * kTile, k + w), c1 = min(b * kTile + kTile, F.nf);
+  const int c0 = max(b * kTile, k + w), c1 = min((b + ntl) * kTile, F.nf);
   const int nc = c1 - c0;
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
   const int tid = threadIdx.x;
-  double* P = sm;               // 32 rows x 64 columns (P[r + c*33])
-  double* L = sm + 64 * 33;     // 32 x 33 factored diagonal block
+  double* P = sm;               // 32 rows x up to 256 columns (P[r + c*33])
+  double* L = sm + kRCMax * kTile * 33;  // 32 x 33 factored diagonal block
   double* bk2 = A.backup + D.backup_off + (int64_t)F.nf * kNB;
   {
     double vl[4], vp[8];
@@ -679,20 +699,22 @@ __device__ void cols_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
       vl[i] = (r < w && c < w) ? __ldcg(&g[(k + r) + (int64_t)(k + c) * ld]) : 0.0;
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int idx = tid + i * kDT, r = idx % kNB, c = idx / kNB;
-      vp[i] = (r < w && c < nc) ? __ldcg(&g[(k + r) + (int64_t)(c0 + c) * ld]) : 0.0;
-    }
-#pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int idx = tid + i * kDT;
       L[(idx % 32) + (idx / 32) * 33] = vl[i];
     }
+    for (int t = 0; t < ntl; ++t) {  // 32 x kTile per round
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int idx = tid + i * kDT, r = idx % kNB, c = idx / kNB;
-      P[r + c * 33] = vp[i];
-      if (r < w && c < nc) bk2[r + (int64_t)(c0 + c) * kNB] = vp[i];
+      for (int i = 0; i < 8; ++i) {
+        const int idx = tid + i * kDT, r = idx % kNB, c = t * kTile + idx / kNB;
+        vp[i] = (r < w && c < nc) ? __ldcg(&g[(k + r) + (int64_t)(c0 + c) * ld]) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int idx = tid + i * kDT, r = idx % kNB, c = t * kTile + idx / kNB;
+        P[r + c * 33] = vp[i];
+        if (r < w && c < nc) bk2[r + (int64_t)(c0 + c) * kNB] = vp[i];
+      }
     }
   }
   __syncthreads();
@@ -711,17 +733,6 @@ __device__ void cols_task(const DagArgs& A, const FrontDev& F, const FrontDag& D
   }
 }
 
-__device__ __forceinline__ void cp_async8z(double* smem, const double* gmem, bool valid) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int n = valid ? 8 : 0;  // src-size 0: zero fill
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
-}
-
-// 16-byte cp.async of two consecutive doubles, `n` of them valid (zero fill)
-__device__ __forceinline__ void cp_async16z(double* smem, const double* gmem, int n) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(8 * n) : "memory");
-}
 constexpr int kBLD = kNB + 4;  // UPD / UPDCB: B stage stored [n][kk] (conflict-free fragment reads)
 
 __device__ void upd_task(const DagArgs& A, const FrontDev& F, int s, int a, int b, double* sm) {
@@ -1095,14 +1106,18 @@ __device__ __forceinline__ int nr_of(const FrontDev& F, const FrontDag& D, int s
 __device__ __forceinline__ int idx_diag(const DagArgs& A, const FrontDag& D, int s) {
   return A.step_base[D.sb_off + s];
 }
+// ROWS / COLS groups of step s: ceil(nr / rc_group) each
+__device__ __forceinline__ int ngr_of(const DagArgs& A, const FrontDev& F, const FrontDag& D, int s) {
+  return (nr_of(F, D, s) + A.rc_group - 1) / A.rc_group;
+}
 __device__ __forceinline__ int idx_rows(const DagArgs& A, const FrontDag& D, const FrontDev& F, int s,
                                          int a) {
-  return A.step_base[D.sb_off + s] + 1 + (a - a0_of(F, s));
+  return A.step_base[D.sb_off + s] + 1 + (a - a0_of(F, s)) / A.rc_group;
 }
 __device__ __forceinline__ int idx_cols(const DagArgs& A, const FrontDag& D, const FrontDev& F, int s,
                                          int b) {
   const int a0 = a0_of(F, s);
-  return A.step_base[D.sb_off + s] + 1 + nr_of(F, D, s) + (b - a0);
+  return A.step_base[D.sb_off + s] + 1 + ngr_of(A, F, D, s) + (b - a0) / A.rc_group;
 }
 // UPD tasks of step s: the trailing tiles (a, b) with a < acb or b < acb, in
 // the order: pivot-region tile rows in full, then contribution-block rows
@@ -1112,7 +1127,7 @@ __device__ __forceinline__ int idx_upd(const DagArgs& A, const FrontDag& D, cons
                                         int b) {
   const int a0 = a0_of(F, s), nr = nr_of(F, D, s);
   const int np = max(0, D.acb - a0), x = a - a0, y = b - a0;
-  const int base = A.step_base[D.sb_off + s] + 1 + 2 * nr;
+  const int base = A.step_base[D.sb_off + s] + 1 + 2 * ngr_of(A, F, D, s);
   return x < np ? base + x * nr + y : base + np * nr + (x - np) * np + y;
 }
 
@@ -1214,8 +1229,8 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
         break;
       }
       case T_DIAG: diag_task(A, F, D, T.step, sm); break;
-      case T_ROWS: rows_task(A, F, D, T.step, T.a, sm); break;
-      case T_COLS: cols_task(A, F, D, T.step, T.b, sm); break;
+      case T_ROWS: rows_task(A, F, D, T.step, T.a, sm, min(A.rc_group, a0_of(F, T.step) + nr_of(F, D, T.step) - T.a)); break;
+      case T_COLS: cols_task(A, F, D, T.step, T.b, sm, min(A.rc_group, a0_of(F, T.step) + nr_of(F, D, T.step) - T.b)); break;
       case T_UPD: upd_task(A, F, T.step, T.a, T.b, sm); break;
       case T_UPDCB: updcb_task(A, F, T.a, T.b, sm); break;
       case T_UPDB: {  // steps [j B, min((j + 1) B, lim)) of tile (a, b)
@@ -1264,7 +1279,7 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     if (T.type == T_DIAG || T.type == T_ROWS || T.type == T_COLS) {
       if (T.type == T_DIAG) {
         const int a0 = a0_of(F, T.step), nr = nr_of(F, D, T.step);
-        for (int x = a0 + tid; x < a0 + nr; x += kDT) {
+        for (int x = a0 + tid * A.rc_group; x < a0 + nr; x += kDT * A.rc_group) {  // one per group
           notify(A, idx_rows(A, D, F, T.step, x));
           notify(A, idx_cols(A, D, F, T.step, x));
         }
@@ -1405,6 +1420,7 @@ struct DagPlan {
   int ntasks = 0, nqueued = 0, nfronts = 0, ntile = 0, nflag = 0, grid = 148, nready = 0;
   int occ = 1, small_nf = 160;  // kernel variant (see kSmallNfLatency / kSmallNfThroughput)
   int upd_batch = 0, upd_la = 2;  // deferred pivot-region updates (upd_lim)
+  int rc_group = 1;               // tiles per ROWS / COLS task
   DeviceBuffer d_ubase;
   int lazy = 0;                   // lazy assembly (DagArgs::lazy)
   DeviceBuffer d_ent_src, d_ent_dst, d_ent_beg, d_ent_end;
@@ -1442,6 +1458,11 @@ void rqb_dag_build(FactorEngine& fe) {
   // deferred pivot-region updates (UPDB, see upd_lim): the throughput variant
   // batches upd_batch panel steps per tile update and keeps the last upd_la
   // steps before a tile's own panel per step
+  // measured (ms, group 1 / 2 / 4): cfg4_riga 26.3 / 25.3 / 25.3, cfg4_iga
+  // 62.9 / 59.6 / 58.9, cfg5_p5_riga 11.8 / 11.0 / 10.9, cfg3_iga 4.94 / 4.93 /
+  // 5.16 (its panel chain binds), cfg2_riga (latency variant) 0.83 / 0.84
+  P->rc_group = P->occ == 2 ? (S.flops_lu >= 4e10 ? kRCMax : 2) : 1;
+  if (const char* e = std::getenv("RQB_RC_GROUP")) P->rc_group = std::max(1, std::min(kRCMax, std::atoi(e)));
   P->upd_batch = P->occ == 2 ? 8 : 0;  // measured: cfg4_riga 28.3 -> 26.8 ms, cfg4_iga 68.6 -> 61.0 ms (4: 27.0 / 62.2)
   P->upd_la = 2;
   if (const char* e = std::getenv("RQB_UPD_BATCH")) P->upd_batch = std::max(0, std::atoi(e));
@@ -1511,13 +1532,15 @@ void rqb_dag_build(FactorEngine& fe) {
       tasks.push_back({f, T_DIAG, (int16_t)s, an, an});
       deps.push_back(s == 0 ? D.nasm : 1);  // s >= 1: run by its predecessor's CTA, never queued
       if (s > 0) ++nfused;
-      for (int a = a0; a < a0 + nr; ++a) {
+      // ROWS / COLS groups of rc_group tiles: DIAG(s) + each tile's UPD(s - 1)
+      const int G = P->rc_group, ngr = (nr + G - 1) / G;
+      for (int a = a0; a < a0 + nr; a += G) {
         tasks.push_back({f, T_ROWS, (int16_t)s, a, an});
-        deps.push_back(s == 0 ? 1 : 2);
+        deps.push_back(s == 0 ? 1 : 1 + std::min(G, a0 + nr - a));
       }
-      for (int b = a0; b < a0 + nr; ++b) {
+      for (int b = a0; b < a0 + nr; b += G) {
         tasks.push_back({f, T_COLS, (int16_t)s, an, b});
-        deps.push_back(s == 0 ? 1 : 2);
+        deps.push_back(s == 0 ? 1 : 1 + std::min(G, a0 + nr - b));
       }
       // eager tiles (pivot rows or pivot columns), layout of idx_upd
       const int np = std::max(0, D.acb - a0);
@@ -1537,7 +1560,7 @@ void rqb_dag_build(FactorEngine& fe) {
         for (int y = 0; y < nr; ++y) push_upd(a0 + x, a0 + y);
       for (int x = np; x < nr; ++x)
         for (int y = 0; y < np; ++y) push_upd(a0 + x, a0 + y);
-      acc += 1 + 2 * nr;
+      acc += 1 + 2 * ngr;
       rc_prefix.push_back(acc);
     }
     step_base.push_back(static_cast<int32_t>(tasks.size()));
@@ -1618,7 +1641,8 @@ void rqb_dag_build(FactorEngine& fe) {
   const size_t small_smem = max_small_bytes;
   P->small_nf = std::max(1, max_small);
   const size_t tile_smem = sizeof(double) * std::max(4 * kNB * kTSP, 2 * (kNB * kTSP + kTile * kBLD));  // UPD / UPDCB: two stages
-  const size_t rows_smem = sizeof(double) * ((kTile + 1) * kNB + kNB * kNB + 64);
+  const size_t rows_smem = sizeof(double) * std::max<size_t>((kRCMax * kTile + 1) * kNB + 33 * 32 + 64,
+                                                             kRCMax * kTile * 33 + 33 * 32);
   const size_t diag_smem = sizeof(double) * (3 * 32 * 33 + 128);
   P->smem = std::max({small_smem, tile_smem, rows_smem, diag_smem, size_t(16 * 1024)});
   auto kern = P->occ == 2 ? factor_dag_kernel<2> : factor_dag_kernel<1>;
@@ -1755,6 +1779,7 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   DagArgs A;
   A.upd_cp16 = std::getenv("RQB_UPD_CP16") ? std::atoi(std::getenv("RQB_UPD_CP16")) : 1;
   A.upd_batch = P.upd_batch;
+  A.rc_group = P.rc_group;
   A.upd_tma = std::getenv("RQB_UPD_TMA") ? std::atoi(std::getenv("RQB_UPD_TMA")) : 0;
   A.upd_la = P.upd_la;
   A.ubase = P.d_ubase.as<int32_t>();
