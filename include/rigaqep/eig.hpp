@@ -260,7 +260,7 @@ inline std::vector<EigenPair> solve_quadratic(const QuadraticPencil& p, cdouble 
                                               CostLedger* ledger, std::uint64_t seed = 0, int max_restarts = 100) {
   const Ordering ord = p.ordering ? *p.ordering : natural_order(p.N());
   const ShiftInvertOperator op = build_operator(p, s, ord, ledger);
-  rq_eigs_opts o{nev, m, eps, seed, max_restarts, 1, 0};
+  rq_eigs_opts o{nev, m, eps, seed, max_restarts, 1, 0, 1};
   std::vector<double> lr(nev), li(nev), res(nev), vr(static_cast<std::size_t>(op.n) * nev),
       vi(static_cast<std::size_t>(op.n) * nev);
   rq_eigs_info info{};

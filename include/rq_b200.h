@@ -155,8 +155,13 @@ int rq_factor_create(const rq_symbolic_t* s, int64_t n, const int64_t* rowptr,
 /* Re-run the numeric factorization with new values on the same pattern. */
 int rq_factor_refactor(rq_factor_t* f, const double* aval);
 int rq_factor_get_info(const rq_factor_t* f, rq_factor_info* out);
-/* x = A^{-1} b for nrhs right-hand sides (column-major n x nrhs, host). */
+/* x = A^{-1} b for nrhs right-hand sides (column-major n x nrhs, host).
+ * Several right-hand sides go through the multi-RHS sweeps (up to 8 vectors
+ * per pass over L and U). */
 int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs);
+/* Same with an explicit sweep width: block = right-hand sides per pass over
+ * the factors (1: the single-vector sweeps, 2..8: multi-RHS sweeps). */
+int rq_factor_solve_ex(rq_factor_t* f, const double* b, double* x, int nrhs, int block);
 /* Copy front f back: dense ld*nf column-major block holding L\U and the
  * Schur complement, ld = *ld_out; ipiv[npiv] local swap sequence. */
 int rq_factor_front_export(const rq_factor_t* f, int64_t front, double* dense, int32_t* ipiv,
@@ -218,7 +223,9 @@ rq_factor_t* rq_operator_factor(rq_operator_t* op); /* borrowed */
  * what = 0 apply_operator, 1 solve_factored, 2 fused C/M SpMV, 3 CGS GEMV-T
  * over `param` basis vectors, 4 GEMV-N over `param` vectors, 5 numeric
  * factorization (graph replay), 6 M SpMV, 7 restart DGEMM (2n x param) x
- * (param x param), 8 batched pencil residual of `param` candidates.
+ * (param x param), 8 batched pencil residual of `param` candidates,
+ * 9 block apply_operator of `param` (<= 8) vectors, 10 multi-RHS solve of
+ * `param` (<= 8) right-hand sides.
  * what | 0x100: scrub L2 (256 MiB) before every call. */
 int rq_operator_time(rq_operator_t* op, int what, int iters, int param, double* ms_per_call);
 void rq_operator_destroy(rq_operator_t* op);
@@ -231,6 +238,8 @@ typedef struct {
   int max_restarts;   /* default 100 */
   int guard;          /* completeness guard (deflated fresh restarts), 1 = on */
   int profile;        /* 1: time operator / orthogonalisation per step (synchronising) */
+  int block;          /* block Krylov-Schur block size b (2..8; multi-RHS sweeps, block CGS2);
+                         <= 1: single-vector Krylov-Schur */
 } rq_eigs_opts;
 
 typedef struct {

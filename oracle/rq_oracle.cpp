@@ -704,6 +704,48 @@ void arnoldi_steps(Operator& op, std::vector<std::vector<cd>>& V, DM& H, int k, 
   }
 }
 
+// Block Arnoldi steps (block Krylov-Schur; the B200
+// build's block mode, operation for operation): for kc = k, k+bs, ... while
+// kc + bs <= m: R_b = S v_{kc+b} (b < bs); CGS2 of the block against V[0, kt),
+// kt = kc + bs (per pass: w_b = B R_b for every member, then h_b = V^H w_b and
+// R_b -= V h_b); then the block's own CGS2 (member b against V[kt, kt+b)) and
+// B-normalisation into V[kt+b]. H(i, kc+b) accumulates the projections,
+// H(kt+b, kc+b) = ||R_b||_B.
+void arnoldi_block_steps(Operator& op, std::vector<std::vector<cd>>& V, DM& H, int k, int m, int bs,
+                         std::vector<std::vector<cd>>& R, std::vector<cd>& w, Ledger* L) {
+  const int64_t n2 = 2 * op.n;
+  for (int kc = k; kc + bs <= m; kc += bs) {
+    const int kt = kc + bs;
+    for (int b = 0; b < bs; ++b) op.apply(V[kc + b].data(), R[b].data(), L);
+    for (int pass = 0; pass < 2; ++pass) {
+      std::vector<std::vector<cd>> h(bs, std::vector<cd>(kt));
+      for (int b = 0; b < bs; ++b) {
+        op.bvec(R[b].data(), w.data(), L);
+        dots(V, kt, w.data(), n2, h[b].data(), L);
+      }
+      for (int b = 0; b < bs; ++b) {
+        axpys(V, kt, h[b].data(), R[b].data(), n2, -1.0, L);
+        for (int i = 0; i < kt; ++i) H(i, kc + b) += h[b][i];
+      }
+    }
+    for (int b = 0; b < bs; ++b) {
+      for (int pass = 0; pass < 2 && b > 0; ++pass) {
+        op.bvec(R[b].data(), w.data(), L);
+        std::vector<cd> h(b);
+        for (int i = 0; i < b; ++i) h[i] = dot(V[kt + i].data(), w.data(), n2, L);
+        for (int i = 0; i < b; ++i) {
+          axpy(-h[i], V[kt + i].data(), R[b].data(), n2, L);
+          H(kt + i, kc + b) += h[i];
+        }
+      }
+      op.bvec(R[b].data(), w.data(), L);
+      const double beta = std::sqrt(std::max(0.0, dot(R[b].data(), w.data(), n2, L).real()));
+      H(kt + b, kc + b) = beta;
+      for (int64_t i = 0; i < n2; ++i) V[kt + b][i] = R[b][i] / beta;
+    }
+  }
+}
+
 // arnoldi_run: v1 B-normalised (one B-product, one dot),
 // then m steps. V: m+1 vectors of 2n; H: (m+1) x m.
 void arnoldi_run(Operator& op, const cd* v1, int m, std::vector<std::vector<cd>>& V, DM& H, Ledger* L) {
@@ -717,15 +759,22 @@ void arnoldi_run(Operator& op, const cd* v1, int m, std::vector<std::vector<cd>>
   arnoldi_steps(op, V, H, 0, m, r, w, L);
 }
 
+// bs > 1: block Krylov-Schur: a basis of m accounted
+// vectors plus a frontier block of bs, steps of arnoldi_block_steps, the
+// residual of a Ritz vector y is ||E y|| with E the bs rows of H below the
+// accounted block, and a restart keeps the frontier block. Start / deflation
+// blocks: member b from splitmix64(seed + b * golden) (b = 0: the
+// single-vector start), CGS2 against everything before it.
 EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, int max_restarts,
-                       int guard_on, Ledger* L) {
+                       int guard_on, Ledger* L, int bs) {
   const int64_t n = op.n, n2 = 2 * n;
   const double sig = op.s.real();
   const int keep_t = nev + std::min(20, m - nev - 1);
-  std::vector<std::vector<cd>> V(m + 1, std::vector<cd>(n2)), V2 = V;
+  std::vector<std::vector<cd>> V(m + bs, std::vector<cd>(n2)), V2 = V;
+  std::vector<std::vector<cd>> R(bs, std::vector<cd>(n2));
   std::vector<cd> r(n2), w(n2);
-  DM H(m + 1);  // (m+1) x (m+1), columns 0..m-1 used
-  auto fresh = [&](uint64_t sd, int nlock, std::vector<cd>& dst) {
+  DM H(m + bs);  // (m+bs) x (m+bs), columns 0..m-1 used
+  auto fresh_one = [&](uint64_t sd, int nlock, std::vector<cd>& dst) {
     uint64_t st = sd;
     for (int64_t i = 0; i < n2; ++i) r[i] = uni(st);
     for (int pass = 0; pass < 2 && nlock > 0; ++pass) {
@@ -738,7 +787,10 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
     const double b = std::sqrt(std::max(0.0, dot(r.data(), w.data(), n2, L).real()));
     for (int64_t i = 0; i < n2; ++i) dst[i] = r[i] / b;
   };
-  fresh(seed, 0, V[0]);
+  auto fresh = [&](uint64_t sd, int nlock) {
+    for (int b = 0; b < bs; ++b) fresh_one(sd + 0x9E3779B97F4A7C15ull * static_cast<uint64_t>(b), nlock + b, V[nlock + b]);
+  };
+  fresh(seed, 0);
   int k = 0, cycles = 0, gp = 0;
   EigOut out;
   std::vector<double> prev;
@@ -746,16 +798,20 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
   while (pass_cycles < max_restarts) {
     ++cycles;
     ++pass_cycles;
-    arnoldi_steps(op, V, H, k, m, r, w, L);
-    DM T(m), Z;
-    for (int j = 0; j < m; ++j)
-      for (int i = 0; i < m; ++i) T(i, j) = H(i, j);
+    const int mm = k + bs * ((m - k) / bs), m0 = mm - bs;
+    if (bs == 1)
+      arnoldi_steps(op, V, H, k, m, r, w, L);
+    else
+      arnoldi_block_steps(op, V, H, k, m, bs, R, w, L);
+    DM T(mm), Z;
+    for (int j = 0; j < mm; ++j)
+      for (int i = 0; i < mm; ++i) T(i, j) = H(i, j);
     if (!schur(T, Z)) throw OracleError{4, "QR did not converge"};
     // eigenvectors of T, Ritz data
-    std::vector<cd> th(m), lam(m);
-    std::vector<double> est(m);
-    DM Y(m);
-    for (int j = 0; j < m; ++j) {
+    std::vector<cd> th(mm), lam(mm);
+    std::vector<double> est(mm);
+    DM Y(mm);
+    for (int j = 0; j < mm; ++j) {
       th[j] = T(j, j);
       lam[j] = op.s + 1.0 / th[j];
       Y(j, j) = 1;
@@ -769,11 +825,25 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
       double nr = 0;
       for (int i = 0; i <= j; ++i) nr += std::norm(Y(i, j));
       nr = std::sqrt(nr);
-      cd yl = 0;
-      for (int i = 0; i <= j; ++i) Y(i, j) /= nr, yl += Z(m - 1, i) * Y(i, j);
-      est[j] = std::abs(H(m, m - 1) * yl) / std::abs(th[j]);
+      for (int i = 0; i <= j; ++i) Y(i, j) /= nr;
+      if (bs == 1) {
+        cd yl = 0;
+        for (int i = 0; i <= j; ++i) yl += Z(m - 1, i) * Y(i, j);
+        est[j] = std::abs(H(m, m - 1) * yl) / std::abs(th[j]);
+      } else {  // ||E y|| / |theta|, E = H(mm.., m0..mm)
+        std::vector<cd> yl(bs, 0.0);
+        for (int q = 0; q < bs; ++q)
+          for (int i = 0; i <= j; ++i) yl[q] += Z(m0 + q, i) * Y(i, j);
+        double e2 = 0;
+        for (int a = 0; a < bs; ++a) {
+          cd t = 0;
+          for (int q = 0; q < bs; ++q) t += H(mm + a, m0 + q) * yl[q];
+          e2 += std::norm(t);
+        }
+        est[j] = std::sqrt(e2) / std::abs(th[j]);
+      }
     }
-    std::vector<int> ord(m);
+    std::vector<int> ord(mm);
     std::iota(ord.begin(), ord.end(), 0);
     std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
       const double da = std::abs(lam[a] - sig), db = std::abs(lam[b] - sig);
@@ -788,10 +858,10 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
     if (all) {
       for (int c = 0; c < nev; ++c) {
         const int i = ord[c];
-        std::vector<cd> y(m, 0.0), x(n2, 0.0);
-        for (int row = 0; row < m; ++row)
+        std::vector<cd> y(mm, 0.0), x(n2, 0.0);
+        for (int row = 0; row < mm; ++row)
           for (int t = 0; t <= i; ++t) y[row] += Z(row, t) * Y(t, i);
-        axpys(V, m, y.data(), x.data(), n2, 1.0, nullptr);
+        axpys(V, mm, y.data(), x.data(), n2, 1.0, nullptr);
         const bool low = std::abs(lam[i]) > 1.0;  // larger-norm block
         std::vector<cd> u(x.begin() + (low ? n : 0), x.begin() + (low ? n2 : n));
         // explicit pencil residual
@@ -816,7 +886,7 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
     out.res = cres;
     for (int c = 0; c < nev; ++c) out.lam.push_back(lam[ord[c]]);
     out.vec = cvec;
-    std::vector<int> sel(m, 0);
+    std::vector<int> sel(mm, 0);
     bool deflate = false;
     if (all) {
       std::vector<double> d;
@@ -835,7 +905,7 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
       deflate = true;
       for (int c = 0; c < nev; ++c) sel[ord[c]] = 1;
     } else {
-      for (int c = 0; c < std::min(keep_t, m - 1); ++c) sel[ord[c]] = 1;
+      for (int c = 0; c < std::min(keep_t, m - bs); ++c) sel[ord[c]] = 1;
     }
     int p = 0;
     for (int v : sel) p += v;
@@ -845,19 +915,24 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
 #pragma omp parallel for schedule(dynamic, 1)
     for (int c = 0; c < p; ++c) {
       std::fill(V2[c].begin(), V2[c].end(), cd{});
-      for (int t = 0; t < m; ++t) k_axpy(Z(t, c), V[t].data(), V2[c].data(), n2);
+      for (int t = 0; t < mm; ++t) k_axpy(Z(t, c), V[t].data(), V2[c].data(), n2);
     }
-    if (L) L->add(RST, static_cast<double>(m) * p * n2);
-    const cd beta = H(m, m - 1);
-    H = DM(m + 1);
+    if (L) L->add(RST, static_cast<double>(mm) * p * n2);
+    // new residual rows E Z_p (E = H(mm.., m0..mm); bs = 1: beta Z(m-1, :))
+    std::vector<cd> EZ(static_cast<size_t>(bs) * p, 0.0);
+    for (int a = 0; a < bs; ++a)
+      for (int c = 0; c < p; ++c)
+        for (int q = 0; q < bs; ++q) EZ[a + static_cast<size_t>(c) * bs] += H(mm + a, m0 + q) * Z(m0 + q, c);
+    H = DM(m + bs);
     for (int c = 0; c < p; ++c)
       for (int i = 0; i <= c; ++i) H(i, c) = T(i, c);
     for (int c = 0; c < p; ++c) V[c].swap(V2[c]);
     if (deflate) {
-      fresh(seed + 0x1000003ull * gp, p, V[p]);
+      fresh(seed + 0x1000003ull * gp, p);
     } else {
-      for (int c = 0; c < p; ++c) H(p, c) = beta * Z(m - 1, c);
-      V[p] = V[m];
+      for (int a = 0; a < bs; ++a)
+        for (int c = 0; c < p; ++c) H(p + a, c) = EZ[a + static_cast<size_t>(c) * bs];
+      for (int a = 0; a < bs; ++a) V[p + a] = V[mm + a];
     }
     k = p;
   }
@@ -1206,13 +1281,15 @@ void oracle_eig_ledger(void* h, double* out) {
 }
 void oracle_eig_ledger_reset(void* h) { static_cast<OracleEig*>(h)->L = oracle::Ledger{}; }
 
-int oracle_eig_solve_quadratic(void* h, int nev, int m, double tol, uint64_t seed, int max_restarts,
-                               int guard, double* lam_c, double* res, double* vec_c, int32_t* stats,
-                               double* ledger) {
+int oracle_eig_solve_quadratic_block(void* h, int nev, int m, double tol, uint64_t seed, int max_restarts,
+                                     int guard, int block, double* lam_c, double* res, double* vec_c,
+                                     int32_t* stats, double* ledger) {
   return guarded([&] {
     auto* E = static_cast<OracleEig*>(h);
-    const oracle::EigOut o = oracle::solve_quadratic(*E->op, nev, m > 0 ? m : 2 * nev + 1, tol, seed,
-                                                     max_restarts, guard, &E->L);
+    const int bs = std::max(1, block);
+    const int mk = m > 0 ? m : 2 * nev + 1;
+    if (bs > 1 && (mk < nev + bs || mk + bs > 2 * E->op->n)) throw oracle::OracleError{2, "oracle: m too small for the block"};
+    const oracle::EigOut o = oracle::solve_quadratic(*E->op, nev, mk, tol, seed, max_restarts, guard, &E->L, bs);
     for (int i = 0; i < nev && i < static_cast<int>(o.lam.size()); ++i) {
       lam_c[2 * i] = o.lam[i].real() * E->varsigma;  // lambda = varsigma gamma
       lam_c[2 * i + 1] = o.lam[i].imag() * E->varsigma;
@@ -1225,6 +1302,13 @@ int oracle_eig_solve_quadratic(void* h, int nev, int m, double tol, uint64_t see
       for (int c = 0; c < 6; ++c) ledger[2 * c] = static_cast<double>(E->L.ops[c]), ledger[2 * c + 1] = E->L.macs[c];
     if (!o.ok) throw oracle::OracleError{4, "oracle: not converged within max_restarts"};
   });
+}
+
+int oracle_eig_solve_quadratic(void* h, int nev, int m, double tol, uint64_t seed, int max_restarts,
+                               int guard, double* lam_c, double* res, double* vec_c, int32_t* stats,
+                               double* ledger) {
+  return oracle_eig_solve_quadratic_block(h, nev, m, tol, seed, max_restarts, guard, 1, lam_c, res, vec_c, stats,
+                                          ledger);
 }
 
 void oracle_eig_destroy(void* h) { delete static_cast<OracleEig*>(h); }

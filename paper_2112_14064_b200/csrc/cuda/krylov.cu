@@ -303,6 +303,163 @@ __global__ void ritz_extract_k(const double* __restrict__ X, int ldx, int64_t n,
     out[j] = src[j * ldx];
 }
 
+// ---- block Krylov-Schur: kernels over a block of bs <= 8 vectors ----
+
+// Xi[e * KB + j] = V[j * ldv + e] (j < bs; zero for bs <= j < KB), e < 2n:
+// the block row-interleaved, so a gather of one column index reads all the
+// block's values in one 32- or 64-byte segment
+template <int KB>
+__global__ void interleave_k(const double* __restrict__ V, int64_t ldv, int64_t n2, int bs, double* __restrict__ Xi) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2; e += (int64_t)gridDim.x * blockDim.x) {
+    double v[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) v[j] = j < bs ? V[j * ldv + e] : 0.0;
+    double2* o = reinterpret_cast<double2*>(Xi + e * KB);
+#pragma unroll
+    for (int q = 0; q < KB / 2; ++q) o[q] = make_double2(v[2 * q], v[2 * q + 1]);
+  }
+}
+
+// Ti[row * KB + j] = C v_u^j + M (s v_u^j + v_l^j) from the interleaved block
+// Xi (upper rows [0, n), lower [n, 2n)): one pass over the shared pattern
+// (col, C, M read once for all KB vectors), 2 x KB / 2 double2 gathers per nonzero
+template <int KB>
+__global__ void spmm_op_k(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                          const double* __restrict__ Cv, const double* __restrict__ Mv, double sigma,
+                          const double* __restrict__ Xi, double* __restrict__ Ti) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) s[j] = 0.0;
+  for (int64_t k = rowptr[row] + lane; k < rowptr[row + 1]; k += 32) {
+    const int64_t c = col[k];
+    const double cv = Cv[k], mv = Mv[k];
+    const double2* xu = reinterpret_cast<const double2*>(Xi + c * KB);
+    const double2* xl = reinterpret_cast<const double2*>(Xi + (n + c) * KB);
+#pragma unroll
+    for (int q = 0; q < KB / 2; ++q) {
+      const double2 u = xu[q], l = xl[q];
+      s[2 * q] += cv * u.x + mv * (sigma * u.x + l.x);
+      s[2 * q + 1] += cv * u.y + mv * (sigma * u.y + l.y);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KB; ++j) s[j] = warp_sum(s[j]);
+  if (lane == 0) {
+    double2* o = reinterpret_cast<double2*>(Ti + row * KB);
+#pragma unroll
+    for (int q = 0; q < KB / 2; ++q) o[q] = make_double2(s[2 * q], s[2 * q + 1]);
+  }
+}
+
+// part[(b * k + i) * bs + j] = V[i][chunk b] . R[j][chunk b]: the block stages
+// its chunk of the bs vectors of R in shared memory ([j][t], conflict-free),
+// each warp owns basis vectors i = warp (mod 8), four at a time; every basis
+// entry loaded from HBM feeds bs multiply-adds (block CGS projection)
+template <int KB>
+__global__ void __launch_bounds__(kRedThreads) gemm_t_part(const double* __restrict__ V, int k, int64_t n2,
+                                                         const double* __restrict__ R, int bs, int64_t chunk,
+                                                         double* __restrict__ part) {
+  extern __shared__ double rs[];
+  const int64_t e0 = blockIdx.x * chunk;
+  const int len = static_cast<int>(min(chunk, n2 - e0));
+  for (int j = 0; j < bs; ++j)
+    for (int t = threadIdx.x; t < len; t += kRedThreads) rs[j * chunk + t] = R[j * n2 + e0 + t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kW = kRedThreads / 32, kV = 4;
+  for (int i = warp; i < k; i += kV * kW) {
+    const double* vp[kV];
+#pragma unroll
+    for (int q = 0; q < kV; ++q) vp[q] = V + (int64_t)(i + q * kW < k ? i + q * kW : i) * n2 + e0;
+    double acc[kV][KB];
+#pragma unroll
+    for (int q = 0; q < kV; ++q)
+#pragma unroll
+      for (int j = 0; j < KB; ++j) acc[q][j] = 0.0;
+    int t = lane;
+    for (; t + 32 < len; t += 64) {
+      double a[kV][2];
+#pragma unroll
+      for (int q = 0; q < kV; ++q) a[q][0] = vp[q][t], a[q][1] = vp[q][t + 32];
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (j < bs) {
+          const double x0 = rs[j * chunk + t], x1 = rs[j * chunk + t + 32];
+#pragma unroll
+          for (int q = 0; q < kV; ++q) acc[q][j] += a[q][0] * x0 + a[q][1] * x1;
+        }
+    }
+    for (; t < len; t += 32) {
+      double a[kV];
+#pragma unroll
+      for (int q = 0; q < kV; ++q) a[q] = vp[q][t];
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (j < bs) {
+          const double x0 = rs[j * chunk + t];
+#pragma unroll
+          for (int q = 0; q < kV; ++q) acc[q][j] += a[q] * x0;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kV; ++q)
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const double sq = warp_sum(acc[q][j]);
+        if (lane == 0 && j < bs && i + q * kW < k) part[((int64_t)blockIdx.x * k + i + q * kW) * bs + j] = sq;
+      }
+  }
+}
+
+// H[i + j ldh] = sum_b part[(b * k + i) * bs + j] (fixed order), one warp per entry
+__global__ void reduce_parts_blk(const double* __restrict__ part, int nb, int k, int bs, double* __restrict__ H,
+                                 int ldh) {
+  const int i = blockIdx.x, j = blockIdx.y, lane = threadIdx.x;
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s += part[((int64_t)b * k + i) * bs + j];
+  s = warp_sum(s);
+  if (lane == 0) H[i + (int64_t)j * ldh] = s;
+}
+
+// R[:, j] -= V[:, 0:k] H[0:k, j], j < bs: one pass over V (each entry feeds bs
+// multiply-adds), H staged in shared memory
+template <int KB>
+__global__ void gemm_n_k(const double* __restrict__ V, int k, int64_t n2, const double* __restrict__ H, int ldh,
+                         int bs, double* __restrict__ R) {
+  extern __shared__ double hs[];  // [i][KB]
+  for (int idx = threadIdx.x; idx < k * KB; idx += blockDim.x) {
+    const int i = idx / KB, j = idx % KB;
+    hs[idx] = j < bs ? H[i + (int64_t)j * ldh] : 0.0;
+  }
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2; e += (int64_t)gridDim.x * blockDim.x) {
+    double s[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) s[j] = 0.0;
+    int i = 0;
+    for (; i + 3 < k; i += 4) {
+      double a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = V[(int64_t)(i + u) * n2 + e];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < KB; ++j) s[j] += a[u] * hs[(i + u) * KB + j];
+    }
+    for (; i < k; ++i) {
+      const double a = V[(int64_t)i * n2 + e];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) s[j] += a * hs[i * KB + j];
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < bs) R[j * n2 + e] -= s[j];
+  }
+}
+
 // out[i] = sum_b part[i * nb + b], one warp per output (fixed order)
 __global__ void sum_rows(const double* __restrict__ part, int nb, double* __restrict__ out) {
   double s = 0.0;
@@ -535,6 +692,65 @@ void OperatorEngine::gemv_n(const double* V, int k, const double* h, double* r, 
   (void)h_acc;
 }
 
+void OperatorEngine::apply_block(const double* V, int bs, double* R) {
+  if (bs <= 0) return;
+  if (bs > 8) fail(errc::config, "block size above 8");
+  if (d_tb.bytes < sizeof(double) * n * 8 * 3) d_tb.alloc(sizeof(double) * n * 8 * 3);
+  double* Xi = d_tb.as<double>();          // 2n x KB interleaved block
+  double* Ti = Xi + 2 * n * 8;             // n x KB interleaved SpMM output
+  const int64_t n2 = 2 * n;
+  const int grid = std::min(div_up(n2, 256), 148 * 8);
+  const int kb = bs <= 4 ? 4 : 8;
+  if (kb == 4) {
+    interleave_k<4><<<grid, 256, 0, stream>>>(V, n2, n2, bs, Xi);
+    spmm_op_k<4><<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
+                                                          d_C.as<double>(), d_M.as<double>(), sigma, Xi, Ti);
+  } else {
+    interleave_k<8><<<grid, 256, 0, stream>>>(V, n2, n2, bs, Xi);
+    spmm_op_k<8><<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
+                                                          d_C.as<double>(), d_M.as<double>(), sigma, Xi, Ti);
+  }
+  launches += 2;
+  // R_u = -Q(s)^{-1} T ; R_l = s R_u + V_u (fused in the backward sweep), bs vectors per pass
+  rqb_msolve_enqueue(*fac, Ti, 1, bs, R, n2, -1.0, V, n2, sigma, R + n, kb);
+  launches += fac->launches_solve;
+}
+
+void OperatorEngine::prepare_block(int kmax, int bs) {
+  rqb_msolve_prepare(*fac);
+  if (d_tb.bytes < sizeof(double) * n * 8 * 3) d_tb.alloc(sizeof(double) * n * 8 * 3);
+  const int64_t nb = (2 * n + 511) / 512;
+  const size_t need = sizeof(double) * static_cast<size_t>(nb) * kmax * bs;
+  if (d_bpart.bytes < need) d_bpart.alloc(need);
+}
+
+void OperatorEngine::gemm_t(const double* V, int k, const double* R, int bs, double* H, int ldh) {
+  if (k <= 0 || bs <= 0) return;
+  constexpr int64_t kChunk = 512;
+  const int64_t n2 = 2 * n;
+  const int nb = static_cast<int>((n2 + kChunk - 1) / kChunk);
+  const size_t need = sizeof(double) * static_cast<size_t>(nb) * k * bs;
+  if (d_bpart.bytes < need) d_bpart.alloc(need);
+  const size_t sm = sizeof(double) * kChunk * bs;
+  if (bs <= 4)
+    gemm_t_part<4><<<nb, kRedThreads, sm, stream>>>(V, k, n2, R, bs, kChunk, d_bpart.as<double>());
+  else
+    gemm_t_part<8><<<nb, kRedThreads, sm, stream>>>(V, k, n2, R, bs, kChunk, d_bpart.as<double>());
+  reduce_parts_blk<<<dim3(k, bs), 32, 0, stream>>>(d_bpart.as<double>(), nb, k, bs, H, ldh);
+  launches += 2;
+}
+
+void OperatorEngine::gemm_n(const double* V, int k, const double* H, int ldh, double* R, int bs) {
+  if (k <= 0 || bs <= 0) return;
+  const int64_t n2 = 2 * n;
+  const int grid = std::min(div_up(n2, 256), 148 * 8);
+  if (bs <= 4)
+    gemm_n_k<4><<<grid, 256, sizeof(double) * k * 4, stream>>>(V, k, n2, H, ldh, bs, R);
+  else
+    gemm_n_k<8><<<grid, 256, sizeof(double) * k * 8, stream>>>(V, k, n2, H, ldh, bs, R);
+  ++launches;
+}
+
 void OperatorEngine::dot2n(const double* x, const double* y, double* out) {
   dot_part<<<kRedBlocks, kRedThreads, 0, stream>>>(x, x + n, y, y + n, n, 2 * n, d_part.as<double>());
   sum_parts<<<1, 32, 0, stream>>>(d_part.as<double>(), kRedBlocks, out);
@@ -644,6 +860,13 @@ double OperatorEngine::time_op(int what, int iters, int param) {
     for (int c = 0; c < k; ++c) lamh.push_back(0.1), lamh.push_back(0.2), blkh.push_back(c & 1);
     h.alloc(sizeof(double) * 2 * k);
   }
+  DeviceBuffer Vb, Rb;
+  if (what == 9 || what == 10) {  // block apply / multi-RHS solve of param (<= 8) vectors
+    Vb.alloc(sizeof(double) * n2 * 8);
+    Rb.alloc(sizeof(double) * n2 * 8);
+    RQB_CUDA(cudaMemsetAsync(Vb.p, 0, Vb.bytes, stream));
+    prepare_block(8, 8);
+  }
   if (what == 3 || what == 4) {
     V.alloc(sizeof(double) * (k + 1) * n2);
     h.alloc(sizeof(double) * (k + 1));
@@ -666,6 +889,10 @@ double OperatorEngine::time_op(int what, int iters, int param) {
       case 6: spmv(2, a.as<double>(), b.as<double>()); break;
       case 7: combine(V.as<double>(), k, Q.as<double>(), k, k, X.as<double>()); break;
       case 8: ritz_residuals(V.as<double>(), k, Q.as<double>(), k / 2, lamh.data(), blkh.data(), X.as<double>(), h.as<double>()); break;
+      case 9: apply_block(Vb.as<double>(), std::min(k, 8), Rb.as<double>()); break;
+      case 10:
+        rqb_msolve_enqueue(*fac, Vb.as<double>(), n, std::min(k, 8), Rb.as<double>(), n, 1.0, nullptr, 0, 0.0, nullptr);
+        break;
       default: fail(errc::config, "unknown timing target");
     }
   };

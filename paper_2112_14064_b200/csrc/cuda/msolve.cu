@@ -1,0 +1,804 @@
+// SPDX-License-Identifier: Apache-2.0
+// Multi-right-hand-side forward/backward substitution over the device-resident
+// fronts (solve_factored, applied to up to 8 vectors at once;
+// the block Krylov-Schur reads L and U once per block of
+// vectors instead of once per vector).
+//
+// Same dataflow skeleton as the single-vector sweeps (trisolve.cu): persistent
+// CTAs claim work items from a FIFO ready queue; an item is a 64-row block of
+// a front (or a whole small front); a front's items are pushed in order when
+// the front becomes ready, and an item waits only on earlier items of its own
+// front (published per pivot block through a release counter). The
+// differences are in the data: every solution / contribution entry is a row
+// of KR values (y, x and the contribution vectors are stored row-interleaved,
+// [row][KR], one 32- or 64-byte segment per row), every L / U element loaded
+// from HBM feeds KR multiply-adds (staged right-hand sides broadcast from
+// shared memory, 8 column loads in flight per thread), and the 64x64 diagonal
+// tile inverse is applied to a 64 x KR block by all 256 threads.
+//
+//   forward   w = b(pivot rows, caller order via the net row permutation) +
+//             children's contribution rows; pivot block j: y_j = inv(L_jj)
+//             (w_j - L_j,<j y_<j); contribution rows: w - L_cb,piv y -> the
+//             front's contribution rows for the parent
+//   backward  x_j = inv(U_jj) (y_j - U_j,>j x_>j - U_j,cb x_cb); writes x
+//             (ND order, interleaved, read by descendants), the caller-order
+//             result scaled, and the fused r_l = s r_u + v_u of apply_operator
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "device.cuh"
+
+namespace rqb {
+
+namespace {
+
+constexpr int kMB = 64;         // rows per item
+constexpr int kMT = 256;        // threads per CTA
+constexpr int kMStage = 256;    // staged solution rows per round
+constexpr int kMWholeNf = 512;  // whole-front items: nf bound (their y / x live in shared memory)
+constexpr int kMWhole = -2;     // MItem::blk of a whole-front item
+constexpr int kDL = kMB + 1;    // leading dimension of the diagonal tile in shared memory
+
+struct MItem {
+  int64_t goff;  // front's pool offset (doubles)
+  int32_t front, r0, nr, blk;  // rows [r0, r0+nr); pivot block, -1 contribution rows, kMWhole
+  int32_t ld, np, nf, start;
+  int32_t npb, parent, rows_off, cbvec_off;
+  int32_t ech_off, nech, doff, pad;
+};
+
+struct MArgs {
+  const MItem* items;
+  int nitems;
+  int* deps;   // per front: unfinished predecessor items (fwd) / fronts (bwd)
+  int* queue;
+  int* qctl;   // {head, tail}
+  int* pub;    // per front: pivot blocks published
+  const int32_t* fbase;
+  const int32_t* fcnt;
+  const int32_t* ech;  // backward: effective children (nearest descendants with pivots)
+  const int4* gsrc;    // forward gather sources per front row {b, child0 cb, child1 cb, -}
+  const double* pool;
+  const double* dinv;
+  const int32_t* perm;
+  const int32_t* rows;
+  const double* b;
+  int64_t ldb, bsr;  // b[i * bsr + j * ldb]: column-major (bsr 1) or row-interleaved (ldb 1)
+  double* y;      // [n][KR]
+  double* cbvec;  // [cbvec][KR]
+  double* xnew;   // [n][KR]
+  double* xout;
+  int64_t ldx;
+  double scale;
+  const double* vu;
+  int64_t ldv;
+  double sigma;
+  double* xl;  // stride ldx
+  int nrhs;
+  int* stall;
+};
+
+__device__ __forceinline__ unsigned long long mtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ int ld_acq(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void red_rel(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+constexpr unsigned long long kMStallNs = 4000000000ull;
+__device__ __forceinline__ bool mstalled(const MArgs& A, unsigned long long& t0) {
+  if (*((volatile int*)A.stall)) return true;
+  const unsigned long long t = mtime();
+  if (t0 == 0) t0 = t;
+  if (t - t0 > kMStallNs) {
+    atomicExch(A.stall, 1);
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void mpush(const MArgs& A, int f) {
+  const int i0 = A.fbase[f], n = A.fcnt[f];
+  if (n <= 0) return;
+  const int slot = atomicAdd(&A.qctl[1], n);
+  for (int i = 0; i < n; ++i) atomicExch(&A.queue[slot + i], i0 + i);
+}
+
+__device__ __forceinline__ int mpop(const MArgs& A) {
+  const int h = atomicAdd(&A.qctl[0], 1);
+  if (h >= A.nitems) return -1;
+  int t;
+  unsigned long long t0 = 0;
+  while ((t = ld_acq(&A.queue[h])) < 0) {
+    __nanosleep(32);
+    if (mstalled(A, t0)) return -1;
+  }
+  return t;
+}
+
+// thread 0: wait until at least `need` pivot blocks of front f are published;
+// returns the published count (or -1 on a stall)
+__device__ __forceinline__ int wait_pub(const MArgs& A, int f, int need) {
+  int p = ld_acq(&A.pub[f]);
+  unsigned long long t0 = 0;
+  while (p < need) {
+    __nanosleep(32);
+    if (mstalled(A, t0)) return -1;
+    p = ld_acq(&A.pub[f]);
+  }
+  return p;
+}
+
+// acc[j] += sum over this thread's column class (c = cb + grp mod 4) of
+// A[row, c] xs[c][j]: eight column loads in flight per iteration, the staged
+// right-hand sides read as double2 broadcasts (every lane of a warp reads the
+// same column)
+template <int KR>
+__device__ __forceinline__ void mstream(const double* lp, int64_t ld, bool rowok, const double* xs, int cb, int ce,
+                                        int grp, double (&acc)[KR]) {
+  int c = cb + grp;
+  for (; c + 28 < ce; c += 32) {
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = rowok ? lp[(int64_t)(c + 4 * u) * ld] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double2* xp = reinterpret_cast<const double2*>(xs + (c + 4 * u) * KR);
+#pragma unroll
+      for (int q = 0; q < KR / 2; ++q) {
+        const double2 t = xp[q];
+        acc[2 * q] += a[u] * t.x;
+        acc[2 * q + 1] += a[u] * t.y;
+      }
+    }
+  }
+  if (c < ce) {
+    double a[7];
+#pragma unroll
+    for (int u = 0; u < 7; ++u) a[u] = (rowok && c + 4 * u < ce) ? lp[(int64_t)(c + 4 * u) * ld] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 7; ++u)
+      if (c + 4 * u < ce) {
+        const double2* xp = reinterpret_cast<const double2*>(xs + (c + 4 * u) * KR);
+#pragma unroll
+        for (int q = 0; q < KR / 2; ++q) {
+          const double2 t = xp[q];
+          acc[2 * q] += a[u] * t.x;
+          acc[2 * q + 1] += a[u] * t.y;
+        }
+      }
+  }
+}
+
+// diagonal tile inverse (forward: unit-lower inv(L11); backward: inv(U11)),
+// zero padded to 64 x 64, into D (leading dimension kDL)
+template <bool kUpper>
+__device__ __forceinline__ void mload_dinv(double* D, const double* src, int nr, int tid) {
+  constexpr int kPer = kMB * kMB / kMT;
+  double v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int idx = tid + u * kMT, r = idx & (kMB - 1), c = idx >> 6;
+    v[u] = 0.0;
+    if (r < nr && c < nr) {
+      if (kUpper)
+        v[u] = r <= c ? src[r + c * nr] : 0.0;
+      else
+        v[u] = r > c ? src[r + c * nr] : (r == c ? 1.0 : 0.0);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int idx = tid + u * kMT;
+    D[(idx & (kMB - 1)) + (idx >> 6) * kDL] = v[u];
+  }
+}
+
+// per-thread partials acc (row, grp) -> part[grp][row][KR]
+template <int KR>
+__device__ __forceinline__ void put_part(double* part, int grp, int row, const double (&acc)[KR]) {
+  double2* p = reinterpret_cast<double2*>(part + ((grp * kMB) + row) * KR);
+#pragma unroll
+  for (int q = 0; q < KR / 2; ++q) p[q] = make_double2(acc[2 * q], acc[2 * q + 1]);
+}
+
+// w[r][j] -= sum_g part[g][r][j] for the nr rows (all threads)
+template <int KR>
+__device__ __forceinline__ void sub_parts(double* w, const double* part, int nr, int tid) {
+  for (int idx = tid; idx < nr * KR; idx += kMT) {
+    const int r = idx / KR, j = idx % KR;
+    w[idx] -= (part[(0 * kMB + r) * KR + j] + part[(1 * kMB + r) * KR + j]) +
+              (part[(2 * kMB + r) * KR + j] + part[(3 * kMB + r) * KR + j]);
+  }
+}
+
+// out[j] = sum_c D[row, c] w[c][j] for this thread's columns j = jq * KR/4 + t
+template <int KR>
+__device__ __forceinline__ void tile_mul(const double* D, const double* w, int nr, int row, int jq,
+                                         double (&out)[KR / 4]) {
+  constexpr int kJ = KR / 4;
+#pragma unroll
+  for (int t = 0; t < kJ; ++t) out[t] = 0.0;
+  for (int c = 0; c < nr; ++c) {
+    const double d = D[row + c * kDL];
+#pragma unroll
+    for (int t = 0; t < kJ; ++t) out[t] += d * w[c * KR + jq * kJ + t];
+  }
+}
+
+// w rows [r0, r0 + nr) of the front: b (pivot rows) + children's contribution rows
+template <int KR>
+__device__ __forceinline__ void gather_w(const MArgs& A, const MItem& I, int r0, int nr, double* w, int tid) {
+  for (int idx = tid; idx < nr * KR; idx += kMT) {
+    const int r = idx / KR, j = idx % KR;
+    const int4 src = __ldg(&A.gsrc[I.rows_off + r0 + r]);
+    double v = 0.0;
+    if (src.x >= 0 && j < A.nrhs) v = A.b[src.x * A.bsr + j * A.ldb];
+    if (src.y >= 0) v += __ldcg(&A.cbvec[(int64_t)src.y * KR + j]);
+    if (src.z >= 0) v += __ldcg(&A.cbvec[(int64_t)src.z * KR + j]);
+    w[idx] = v;
+  }
+}
+
+template <int KR>
+struct MSmem {
+  double* D;     // 64 x kDL
+  double* part;  // 4 x 64 x KR
+  double* w;     // 64 x KR
+  double* stg;   // max(kMStage, kMWholeNf) x KR
+};
+
+template <int KR>
+__device__ __forceinline__ MSmem<KR> carve(double* sm) {
+  MSmem<KR> s;
+  s.D = sm;
+  s.part = s.D + kMB * kDL;
+  s.w = s.part + 4 * kMB * KR;
+  s.stg = s.w + kMB * KR;
+  return s;
+}
+
+template <int KR>
+constexpr size_t msmem_bytes() {
+  return sizeof(double) * (kMB * kDL + 4 * kMB * KR + kMB * KR + (kMStage > kMWholeNf ? kMStage : kMWholeNf) * KR);
+}
+
+// ---------------------------------------------------------------------------
+// forward sweep
+template <int KR>
+__device__ void mfwd_whole(const MArgs& A, const MItem& I, MSmem<KR>& S, int tid) {
+  const int np = I.np, nf = I.nf, row = tid & (kMB - 1), grp = tid >> 6, jq = tid >> 6;
+  const double* g = A.pool + I.goff;
+  const int64_t ld = I.ld;
+  double* wy = S.stg;  // [nf][KR]: w, then y over the pivot rows
+  gather_w<KR>(A, I, 0, nf, wy, tid);
+  const int npb = (np + kMB - 1) / kMB;
+  for (int blk = 0; blk < npb; ++blk) {
+    const int r0 = blk * kMB, nr = min(np, r0 + kMB) - r0;
+    mload_dinv<false>(S.D, A.dinv + I.doff + (int64_t)kMB * kMB * blk, nr, tid);
+    __syncthreads();  // wy complete (gather / previous block)
+    double acc[KR];
+#pragma unroll
+    for (int j = 0; j < KR; ++j) acc[j] = 0.0;
+    if (r0 > 0) mstream<KR>(g + r0 + row, ld, row < nr, wy, 0, r0, grp, acc);
+    put_part<KR>(S.part, grp, row, acc);
+    __syncthreads();
+    sub_parts<KR>(wy + r0 * KR, S.part, nr, tid);
+    __syncthreads();
+    double out[KR / 4];
+    tile_mul<KR>(S.D, wy + r0 * KR, nr, row, jq, out);
+    __syncthreads();  // every thread read wy's block before it is overwritten
+    if (row < nr)
+#pragma unroll
+      for (int t = 0; t < KR / 4; ++t) {
+        const int j = jq * (KR / 4) + t;
+        wy[(r0 + row) * KR + j] = out[t];
+        A.y[(int64_t)(I.start + r0 + row) * KR + j] = out[t];
+      }
+  }
+  __syncthreads();
+  for (int r0 = np; r0 < nf; r0 += kMB) {
+    const int nr = min(nf, r0 + kMB) - r0;
+    double acc[KR];
+#pragma unroll
+    for (int j = 0; j < KR; ++j) acc[j] = 0.0;
+    if (np > 0) mstream<KR>(g + r0 + row, ld, row < nr, wy, 0, np, grp, acc);
+    put_part<KR>(S.part, grp, row, acc);
+    __syncthreads();
+    for (int idx = tid; idx < nr * KR; idx += kMT) {
+      const int r = idx / KR, j = idx % KR;
+      const double s = (S.part[(0 * kMB + r) * KR + j] + S.part[(1 * kMB + r) * KR + j]) +
+                       (S.part[(2 * kMB + r) * KR + j] + S.part[(3 * kMB + r) * KR + j]);
+      A.cbvec[(int64_t)(I.cbvec_off + r0 + r - np) * KR + j] = wy[(r0 + r) * KR + j] - s;
+    }
+    __syncthreads();
+  }
+}
+
+template <int KR, int kMinBlocks>
+__global__ void __launch_bounds__(kMT, kMinBlocks) mfwd_sweep(MArgs A) {
+  extern __shared__ __align__(16) double msm[];
+  MSmem<KR> S = carve<KR>(msm);
+  __shared__ int item_s, avail_s;
+  const int tid = threadIdx.x, row = tid & (kMB - 1), grp = tid >> 6, jq = tid >> 6;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) item_s = mpop(A);
+    __syncthreads();
+    const int it = item_s;
+    if (it < 0) return;
+    const MItem I = A.items[it];
+    if (I.blk == kMWhole) {
+      mfwd_whole<KR>(A, I, S, tid);
+    } else {
+      const double* g = A.pool + I.goff;
+      const int64_t ld = I.ld;
+      const int nr = I.nr, blk = I.blk, np = I.np;
+      gather_w<KR>(A, I, I.r0, nr, S.w, tid);
+      if (blk >= 0) mload_dinv<false>(S.D, A.dinv + I.doff + (int64_t)kMB * kMB * blk, nr, tid);
+      const int ncol = blk >= 0 ? blk * kMB : np;  // y columns this item needs
+      double acc[KR];
+#pragma unroll
+      for (int j = 0; j < KR; ++j) acc[j] = 0.0;
+      int done = 0;
+      while (done < ncol) {
+        if (tid == 0) {
+          const int need = min(I.npb, done / kMB + 1);
+          const int p = wait_pub(A, I.front, need);
+          avail_s = p < 0 ? ncol : min(ncol, p * kMB);
+        }
+        __syncthreads();
+        const int avail = avail_s;
+        for (int base = done; base < avail; base += kMStage) {
+          const int hi = min(avail, base + kMStage);
+          for (int idx = tid; idx < (hi - base) * KR; idx += kMT)
+            S.stg[idx] = __ldcg(&A.y[(int64_t)(I.start + base) * KR + idx]);
+          __syncthreads();
+          mstream<KR>(g + I.r0 + row, ld, row < nr, S.stg - base * KR, base, hi, grp, acc);
+          __syncthreads();
+        }
+        done = avail;
+      }
+      put_part<KR>(S.part, grp, row, acc);
+      __syncthreads();
+      if (blk >= 0) {
+        sub_parts<KR>(S.w, S.part, nr, tid);
+        __syncthreads();
+        double out[KR / 4];
+        tile_mul<KR>(S.D, S.w, nr, row, jq, out);
+        if (row < nr)
+#pragma unroll
+          for (int t = 0; t < KR / 4; ++t)
+            A.y[(int64_t)(I.start + I.r0 + row) * KR + jq * (KR / 4) + t] = out[t];
+      } else {
+        for (int idx = tid; idx < nr * KR; idx += kMT) {
+          const int r = idx / KR, j = idx % KR;
+          const double s = (S.part[(0 * kMB + r) * KR + j] + S.part[(1 * kMB + r) * KR + j]) +
+                           (S.part[(2 * kMB + r) * KR + j] + S.part[(3 * kMB + r) * KR + j]);
+          A.cbvec[(int64_t)(I.cbvec_off + I.r0 + r - np) * KR + j] = S.w[idx] - s;
+        }
+      }
+    }
+    __syncthreads();  // every row written before thread 0 publishes
+    if (tid == 0) {
+      if (I.blk >= 0) {
+        __threadfence();
+        red_rel(&A.pub[I.front], 1);
+      }
+      if (I.parent >= 0) {
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(A.deps + I.parent) : "memory");
+        if (old == 1) {
+          __threadfence();
+          mpush(A, I.parent);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward sweep
+template <int KR>
+__device__ __forceinline__ void store_xm(const MArgs& A, int gi, int j, double v) {
+  A.xnew[(int64_t)gi * KR + j] = v;
+  if (j < A.nrhs) {
+    const int64_t o = A.perm[gi];
+    const double sv = A.scale * v;
+    A.xout[o + j * A.ldx] = sv;
+    if (A.xl) A.xl[o + j * A.ldx] = A.sigma * sv + A.vu[o + j * A.ldv];
+  }
+}
+
+template <int KR>
+__device__ void mbwd_whole(const MArgs& A, const MItem& I, MSmem<KR>& S, int tid) {
+  const int np = I.np, nf = I.nf, row = tid & (kMB - 1), grp = tid >> 6, jq = tid >> 6;
+  const double* g = A.pool + I.goff;
+  const int64_t ld = I.ld;
+  const int32_t* rw = A.rows + I.rows_off;
+  double* xs = S.stg;  // [nf][KR]: x of the pivot rows (as solved), x_cb of the ancestors
+  for (int idx = tid; idx < (nf - np) * KR; idx += kMT) {
+    const int c = np + idx / KR, j = idx % KR;
+    xs[c * KR + j] = __ldcg(&A.xnew[(int64_t)rw[c] * KR + j]);
+  }
+  const int npb = (np + kMB - 1) / kMB;
+  for (int blk = npb - 1; blk >= 0; --blk) {
+    const int r0 = blk * kMB, nr = min(np, r0 + kMB) - r0;
+    mload_dinv<true>(S.D, A.dinv + I.doff + (int64_t)kMB * kMB * blk, nr, tid);
+    for (int idx = tid; idx < nr * KR; idx += kMT) S.w[idx] = A.y[(int64_t)(I.start + r0) * KR + idx];
+    __syncthreads();
+    double acc[KR];
+#pragma unroll
+    for (int j = 0; j < KR; ++j) acc[j] = 0.0;
+    mstream<KR>(g + r0 + row, ld, row < nr, xs, r0 + nr, nf, grp, acc);
+    put_part<KR>(S.part, grp, row, acc);
+    __syncthreads();
+    sub_parts<KR>(S.w, S.part, nr, tid);
+    __syncthreads();
+    double out[KR / 4];
+    tile_mul<KR>(S.D, S.w, nr, row, jq, out);
+    if (row < nr)
+#pragma unroll
+      for (int t = 0; t < KR / 4; ++t) {
+        const int j = jq * (KR / 4) + t;
+        xs[(r0 + row) * KR + j] = out[t];
+        store_xm<KR>(A, I.start + r0 + row, j, out[t]);
+      }
+    __syncthreads();
+  }
+}
+
+template <int KR, int kMinBlocks>
+__global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
+  extern __shared__ __align__(16) double msm[];
+  MSmem<KR> S = carve<KR>(msm);
+  __shared__ int item_s, avail_s;
+  const int tid = threadIdx.x, row = tid & (kMB - 1), grp = tid >> 6, jq = tid >> 6;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) item_s = mpop(A);
+    __syncthreads();
+    const int it = item_s;
+    if (it < 0) return;
+    const MItem I = A.items[it];
+    if (I.blk == kMWhole) {
+      mbwd_whole<KR>(A, I, S, tid);
+    } else {
+      const double* g = A.pool + I.goff;
+      const int64_t ld = I.ld;
+      const int32_t* rw = A.rows + I.rows_off;
+      const int nr = I.nr, blk = I.blk, np = I.np, nf = I.nf;
+      const int r0 = I.r0, lo = r0 + nr;
+      mload_dinv<true>(S.D, A.dinv + I.doff + (int64_t)kMB * kMB * blk, nr, tid);
+      for (int idx = tid; idx < nr * KR; idx += kMT) S.w[idx] = A.y[(int64_t)(I.start + r0) * KR + idx];
+      double acc[KR];
+#pragma unroll
+      for (int j = 0; j < KR; ++j) acc[j] = 0.0;
+      // contribution columns: the ancestors' x (final: the front is ready)
+      for (int base = np; base < nf; base += kMStage) {
+        const int hi = min(nf, base + kMStage);
+        for (int idx = tid; idx < (hi - base) * KR; idx += kMT) {
+          const int c = base + idx / KR, j = idx % KR;
+          S.stg[idx] = __ldcg(&A.xnew[(int64_t)rw[c] * KR + j]);
+        }
+        __syncthreads();
+        mstream<KR>(g + r0 + row, ld, row < nr, S.stg - base * KR, base, hi, grp, acc);
+        __syncthreads();
+      }
+      // later pivot blocks of this front, published last first
+      int done_hi = np;
+      while (done_hi > lo) {
+        if (tid == 0) {
+          const int need = I.npb - (done_hi - 1) / kMB;  // blocks from the end down to the one holding done_hi-1
+          const int p = wait_pub(A, I.front, need);
+          avail_s = p < 0 ? lo : max(lo, (I.npb - p) * kMB);
+        }
+        __syncthreads();
+        const int avail_lo = avail_s;
+        // one partial per 64-column pivot block, added to acc from the last
+        // block down: the summation order does not depend on how publication
+        // rounds grouped the blocks (bitwise deterministic solves)
+        for (int top = done_hi; top > avail_lo;) {
+          const int bot = max(avail_lo, (max(0, top - kMStage) + kMB - 1) / kMB * kMB);
+          for (int idx = tid; idx < (top - bot) * KR; idx += kMT)
+            S.stg[idx] = __ldcg(&A.xnew[(int64_t)(I.start + bot) * KR + idx]);
+          __syncthreads();
+          for (int bh = top; bh > bot;) {
+            const int bl = max(bot, (bh - 1) / kMB * kMB);
+            double t[KR];
+#pragma unroll
+            for (int j = 0; j < KR; ++j) t[j] = 0.0;
+            mstream<KR>(g + r0 + row, ld, row < nr, S.stg - bot * KR, bl, bh, grp, t);
+#pragma unroll
+            for (int j = 0; j < KR; ++j) acc[j] += t[j];
+            bh = bl;
+          }
+          __syncthreads();
+          top = bot;
+        }
+        done_hi = avail_lo;
+      }
+      put_part<KR>(S.part, grp, row, acc);
+      __syncthreads();
+      sub_parts<KR>(S.w, S.part, nr, tid);
+      __syncthreads();
+      double out[KR / 4];
+      tile_mul<KR>(S.D, S.w, nr, row, jq, out);
+      if (row < nr)
+#pragma unroll
+        for (int t = 0; t < KR / 4; ++t) store_xm<KR>(A, I.start + r0 + row, jq * (KR / 4) + t, out[t]);
+    }
+    __syncthreads();
+    if (tid == 0 && I.blk != kMWhole) {
+      __threadfence();
+      red_rel(&A.pub[I.front], 1);
+    }
+    if (I.blk == 0 || I.blk == kMWhole) {  // the front is complete: its effective children are ready
+      if (tid == 0) __threadfence();
+      __syncthreads();
+      for (int x = tid; x < I.nech; x += kMT) {
+        const int f = A.ech[I.ech_off + x];
+        if (atomicSub(&A.deps[f], 1) == 1) {
+          __threadfence();
+          mpush(A, f);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct MSolvePlan {
+  int nfr = 0, n_fwd = 0, n_bwd = 0;
+  DeviceBuffer d_items_f, d_items_b, d_meta, d_ech, d_state0, d_state, d_stall;
+  DeviceBuffer d_y, d_x, d_cb;  // interleaved, sized for 8 right-hand sides
+  int64_t st_dep_f = 0, st_dep_b = 0, st_q_f = 0, st_q_b = 0, st_qctl = 0, st_pub = 0;
+  int grid4 = 148, grid8 = 148;
+};
+
+void MSolvePlanDeleter::operator()(MSolvePlan* p) const { delete p; }
+
+constexpr int kMaxRhs = 8;
+
+static void msolve_prepare(FactorEngine& fe) {
+  const Symbolic& S = fe.sym;
+  auto P = std::unique_ptr<MSolvePlan, MSolvePlanDeleter>(new MSolvePlan);
+  const int nfr = static_cast<int>(S.fronts.size());
+  P->nfr = nfr;
+  std::vector<int32_t> npb(nfr), doff(nfr), fbase_f(nfr), fcnt_f(nfr), fbase_b(nfr, 0), fcnt_b(nfr, 0), ech_off(nfr);
+  std::vector<std::vector<int32_t>> echl(nfr);
+  int64_t dtot = 0;
+  for (int f = 0; f < nfr; ++f) {
+    const Front& F = S.fronts[f];
+    npb[f] = (F.npiv + kMB - 1) / kMB;
+    doff[f] = static_cast<int32_t>(dtot);  // same layout as rqb_solve_prepare's diagonal-tile inverses
+    for (int b = 0; b < npb[f]; ++b) {
+      const int64_t nr = std::min(F.npiv, (b + 1) * kMB) - b * kMB;
+      dtot += nr * nr;
+    }
+    if (npb[f] > 0) {
+      int a = F.parent;
+      while (a >= 0 && S.fronts[a].npiv == 0) a = S.fronts[a].parent;
+      if (a >= 0) echl[a].push_back(f);
+    }
+  }
+  std::vector<int32_t> ech;
+  for (int f = 0; f < nfr; ++f) {
+    ech_off[f] = static_cast<int32_t>(ech.size());
+    ech.insert(ech.end(), echl[f].begin(), echl[f].end());
+  }
+  std::vector<int> lvl_count;
+  for (const Front& F : S.fronts) {
+    if (F.level >= static_cast<int>(lvl_count.size())) lvl_count.resize(F.level + 1, 0);
+    ++lvl_count[F.level];
+  }
+  const int whole_min = std::getenv("RQB_MWHOLE_MIN") ? std::atoi(std::getenv("RQB_MWHOLE_MIN")) : 128;
+  auto item = [&](int f, int r0, int r1, int blk) {
+    const Front& F = S.fronts[f];
+    const FrontDev& D = fe.fronts_h[f];
+    MItem it{};
+    it.goff = D.off;
+    it.front = f;
+    it.r0 = r0;
+    it.nr = r1 - r0;
+    it.blk = blk;
+    it.ld = D.ld;
+    it.np = F.npiv;
+    it.nf = F.nf;
+    it.start = D.start;
+    it.npb = npb[f];
+    it.parent = F.parent;
+    it.rows_off = static_cast<int32_t>(D.rows_off);
+    it.cbvec_off = static_cast<int32_t>(D.cbvec_off);
+    it.ech_off = ech_off[f];
+    it.nech = static_cast<int32_t>(echl[f].size());
+    it.doff = doff[f];
+    return it;
+  };
+  std::vector<MItem> fwd, bwd;
+  std::vector<char> whole(nfr);
+  for (int f = 0; f < nfr; ++f) {
+    const Front& F = S.fronts[f];
+    whole[f] = npb[f] <= 2 && F.nf <= kMWholeNf && lvl_count[F.level] >= whole_min;
+    fbase_f[f] = static_cast<int32_t>(fwd.size());
+    if (whole[f]) {
+      fwd.push_back(item(f, 0, F.nf, kMWhole));
+    } else {
+      for (int b = 0; b < npb[f]; ++b) fwd.push_back(item(f, b * kMB, std::min(F.npiv, (b + 1) * kMB), b));
+      for (int r = F.npiv; r < F.nf; r += kMB) fwd.push_back(item(f, r, std::min(F.nf, r + kMB), -1));
+    }
+    fcnt_f[f] = static_cast<int32_t>(fwd.size()) - fbase_f[f];
+  }
+  for (int f = nfr - 1; f >= 0; --f) {
+    const Front& F = S.fronts[f];
+    fbase_b[f] = static_cast<int32_t>(bwd.size());
+    if (npb[f] > 0) {
+      if (whole[f]) {
+        bwd.push_back(item(f, 0, F.npiv, kMWhole));
+      } else {
+        for (int b = npb[f] - 1; b >= 0; --b) bwd.push_back(item(f, b * kMB, std::min(F.npiv, (b + 1) * kMB), b));
+      }
+    }
+    fcnt_b[f] = static_cast<int32_t>(bwd.size()) - fbase_b[f];
+  }
+  std::vector<int32_t> dfwd(nfr, 0), dbwd(nfr, 0);
+  for (int f = 0; f < nfr; ++f) {
+    const Front& F = S.fronts[f];
+    for (int32_t c : F.children) dfwd[f] += fcnt_f[c];
+    int a = F.parent;
+    while (a >= 0 && S.fronts[a].npiv == 0) a = S.fronts[a].parent;
+    dbwd[f] = a >= 0 ? 1 : 0;
+  }
+  std::vector<int32_t> qf(std::max<size_t>(1, fwd.size()), -1), qb(std::max<size_t>(1, bwd.size()), -1);
+  int nq_f = 0, nq_b = 0;
+  for (int f = 0; f < nfr; ++f) {
+    if (dfwd[f] == 0)
+      for (int i = 0; i < fcnt_f[f]; ++i) qf[nq_f++] = fbase_f[f] + i;
+    if (dbwd[f] == 0)
+      for (int i = 0; i < fcnt_b[f]; ++i) qb[nq_b++] = fbase_b[f] + i;
+  }
+  P->n_fwd = static_cast<int>(fwd.size());
+  P->n_bwd = static_cast<int>(bwd.size());
+  if (fwd.empty()) fwd.push_back(MItem{});
+  if (bwd.empty()) bwd.push_back(MItem{});
+  if (ech.empty()) ech.push_back(0);
+  P->d_items_f.upload(fwd.data(), sizeof(MItem) * fwd.size(), fe.stream);
+  P->d_items_b.upload(bwd.data(), sizeof(MItem) * bwd.size(), fe.stream);
+  std::vector<int32_t> meta;
+  meta.insert(meta.end(), fbase_f.begin(), fbase_f.end());
+  meta.insert(meta.end(), fcnt_f.begin(), fcnt_f.end());
+  meta.insert(meta.end(), fbase_b.begin(), fbase_b.end());
+  meta.insert(meta.end(), fcnt_b.begin(), fcnt_b.end());
+  P->d_meta.upload(meta.data(), sizeof(int32_t) * meta.size(), fe.stream);
+  P->d_ech.upload(ech.data(), sizeof(int32_t) * ech.size(), fe.stream);
+  std::vector<int32_t> st;
+  P->st_dep_f = 0;
+  st.insert(st.end(), dfwd.begin(), dfwd.end());
+  P->st_dep_b = static_cast<int64_t>(st.size());
+  st.insert(st.end(), dbwd.begin(), dbwd.end());
+  P->st_q_f = static_cast<int64_t>(st.size());
+  st.insert(st.end(), qf.begin(), qf.end());
+  P->st_q_b = static_cast<int64_t>(st.size());
+  st.insert(st.end(), qb.begin(), qb.end());
+  P->st_qctl = static_cast<int64_t>(st.size());
+  st.insert(st.end(), {0, nq_f, 0, nq_b});
+  P->st_pub = static_cast<int64_t>(st.size());
+  st.resize(st.size() + 2 * static_cast<size_t>(nfr), 0);  // published blocks fwd, bwd
+  P->d_state0.upload(st.data(), sizeof(int32_t) * st.size(), fe.stream);
+  P->d_state.alloc(P->d_state0.bytes);
+  P->d_stall.alloc(sizeof(int));
+  RQB_CUDA(cudaMemsetAsync(P->d_stall.p, 0, sizeof(int), fe.stream));
+  P->d_y.alloc(sizeof(double) * kMaxRhs * std::max<int64_t>(1, fe.n));
+  P->d_x.alloc(sizeof(double) * kMaxRhs * std::max<int64_t>(1, fe.n));
+  P->d_cb.alloc(sizeof(double) * kMaxRhs * std::max<int64_t>(1, S.cbvec));
+  int nsm = 148, occ = 1;
+  RQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device));
+  smem_at_least(mfwd_sweep<4, 3>, msmem_bytes<4>());
+  smem_at_least(mbwd_sweep<4, 3>, msmem_bytes<4>());
+  smem_at_least(mfwd_sweep<8, 2>, msmem_bytes<8>());
+  smem_at_least(mbwd_sweep<8, 2>, msmem_bytes<8>());
+  RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mfwd_sweep<4, 3>, kMT, msmem_bytes<4>()));
+  P->grid4 = nsm * std::max(1, occ);
+  RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mfwd_sweep<8, 2>, kMT, msmem_bytes<8>()));
+  P->grid8 = nsm * std::max(1, occ);
+  fe.mplan.reset(P.release());
+}
+
+template <int KR, int kMinB>
+static void msolve_launch(FactorEngine& fe, MArgs A, int grid) {
+  MSolvePlan& P = *fe.mplan;
+  cudaStream_t st = fe.stream;
+  const int nfr = P.nfr;
+  int* sb = P.d_state.as<int>();
+  const int32_t* meta = P.d_meta.as<int32_t>();
+  smem_at_least(mfwd_sweep<KR, kMinB>, msmem_bytes<KR>());
+  smem_at_least(mbwd_sweep<KR, kMinB>, msmem_bytes<KR>());
+  MArgs F = A;
+  F.items = P.d_items_f.as<MItem>();
+  F.nitems = P.n_fwd;
+  F.deps = sb + P.st_dep_f;
+  F.queue = sb + P.st_q_f;
+  F.qctl = sb + P.st_qctl;
+  F.pub = sb + P.st_pub;
+  F.fbase = meta;
+  F.fcnt = meta + nfr;
+  if (P.n_fwd > 0) mfwd_sweep<KR, kMinB><<<std::min(grid, P.n_fwd), kMT, msmem_bytes<KR>(), st>>>(F);
+  MArgs B = A;
+  B.items = P.d_items_b.as<MItem>();
+  B.nitems = P.n_bwd;
+  B.deps = sb + P.st_dep_b;
+  B.queue = sb + P.st_q_b;
+  B.qctl = sb + P.st_qctl + 2;
+  B.pub = sb + P.st_pub + nfr;
+  B.fbase = meta + 2 * nfr;
+  B.fcnt = meta + 3 * nfr;
+  if (P.n_bwd > 0) mbwd_sweep<KR, kMinB><<<std::min(grid, P.n_bwd), kMT, msmem_bytes<KR>(), st>>>(B);
+  RQB_CUDA(cudaGetLastError());
+}
+
+void rqb_msolve_enqueue(FactorEngine& fe, const double* b, int64_t ldb, int nrhs, double* x, int64_t ldx,
+                        double scale, const double* vu, int64_t ldv, double sigma, double* xl, int64_t b_row_stride) {
+  if (nrhs <= 0) return;
+  if (nrhs > kMaxRhs) fail(errc::config, "multi-RHS sweep: at most 8 right-hand sides per call");
+  if (!fe.mplan) msolve_prepare(fe);
+  MSolvePlan& P = *fe.mplan;
+  cudaStream_t st = fe.stream;
+  RQB_CUDA(cudaMemcpyAsync(P.d_state.p, P.d_state0.p, P.d_state0.bytes, cudaMemcpyDeviceToDevice, st));
+  MArgs A{};
+  A.ech = P.d_ech.as<int32_t>();
+  A.gsrc = fe.d_gsrc.as<int4>();
+  A.pool = fe.d_pool.as<double>();
+  A.dinv = fe.d_dinv.as<double>();
+  A.perm = fe.d_perm.as<int32_t>();
+  A.rows = fe.d_rows.as<int32_t>();
+  A.b = b;
+  A.ldb = ldb;
+  A.bsr = b_row_stride;
+  A.y = P.d_y.as<double>();
+  A.cbvec = P.d_cb.as<double>();
+  A.xnew = P.d_x.as<double>();
+  A.xout = x;
+  A.ldx = ldx;
+  A.scale = scale;
+  A.vu = vu;
+  A.ldv = ldv;
+  A.sigma = sigma;
+  A.xl = xl;
+  A.nrhs = nrhs;
+  A.stall = P.d_stall.as<int>();
+  if (nrhs <= 4)
+    msolve_launch<4, 3>(fe, A, P.grid4);
+  else
+    msolve_launch<8, 2>(fe, A, P.grid8);
+  fe.launches_solve = 2;
+}
+
+void rqb_msolve_prepare(FactorEngine& fe) {
+  if (!fe.mplan) msolve_prepare(fe);
+}
+
+void rqb_msolve_check(FactorEngine& fe) {
+  if (!fe.mplan) return;
+  int stv = 0;
+  RQB_CUDA(cudaMemcpyAsync(&stv, fe.mplan->d_stall.p, sizeof(int), cudaMemcpyDeviceToHost, fe.stream));
+  RQB_CUDA(cudaStreamSynchronize(fe.stream));
+  if (stv) {
+    RQB_CUDA(cudaMemsetAsync(fe.mplan->d_stall.p, 0, sizeof(int), fe.stream));
+    fail(errc::solver, "multi-RHS triangular sweep stalled (watchdog): a dependency of the solve never resolved");
+  }
+}
+
+}  // namespace rqb

@@ -87,6 +87,10 @@ struct DagPlan;
 struct DagPlanDeleter {
   void operator()(DagPlan* p) const;
 };
+struct MSolvePlan;  // multi-RHS sweeps (cuda/msolve.cu)
+struct MSolvePlanDeleter {
+  void operator()(MSolvePlan* p) const;
+};
 
 struct FactorEngine {
   // one stream and one set of solve buffers per engine: the C-ABI entry points
@@ -124,6 +128,8 @@ struct FactorEngine {
   DeviceBuffer d_state0, d_state, d_sweep_stall;
   int64_t st_dep_fwd = 0, st_dep_bwd = 0, st_q_fwd = 0, st_q_bwd = 0, st_qctl = 0, st_cnt = 0;
   int n_fwd_items = 0, n_bwd_items = 0, solve_grid = 148, sweep_occ = 2, win_f = 8, win_b = 8;
+  // multi-RHS sweeps: items, dataflow state and interleaved workspaces (built on first use)
+  std::unique_ptr<MSolvePlan, MSolvePlanDeleter> mplan;
   std::vector<FrontDev> fronts_h;
   std::vector<LevelPlan> plans;
   int64_t nscratch = 0;
@@ -159,6 +165,19 @@ struct FactorEngine {
 // when xl != nullptr, xl = sigma * x + vu (fused lower block of apply_operator).
 void rqb_solve_enqueue(FactorEngine& fe, const double* b, double* x, double scale,
                        const double* vu, double sigma, double* xl);
+// Multi-RHS sweeps (up to 8 vectors, cuda/msolve.cu): for j < nrhs,
+// x[:, j] = scale * A^{-1} b[:, j] (columns at ldb / ldx) and, when xl !=
+// nullptr, xl[:, j] = sigma * x[:, j] + vu[:, j] (ldx / ldv). L and U are
+// streamed once for all nrhs vectors.
+// b[i * b_row_stride + j * ldb]: column-major right-hand sides (stride 1) or
+// row-interleaved ones (b_row_stride = width, ldb = 1).
+void rqb_msolve_enqueue(FactorEngine& fe, const double* b, int64_t ldb, int nrhs, double* x, int64_t ldx,
+                        double scale, const double* vu, int64_t ldv, double sigma, double* xl,
+                        int64_t b_row_stride = 1);
+// build the multi-RHS sweep plan now (not during a stream capture)
+void rqb_msolve_prepare(FactorEngine& fe);
+// raise errc::solver if a multi-RHS sweep hit its stall watchdog (syncs the stream)
+void rqb_msolve_check(FactorEngine& fe);
 void rqb_solve_set_attrs(int maxnf);
 void rqb_solve_prepare(FactorEngine& fe);
 void rqb_dag_build(FactorEngine& fe);
@@ -194,6 +213,7 @@ struct OperatorEngine {
   // EigWorkspace: basis buffers + the cycle graphs captured over them)
   std::shared_ptr<void> eig_ws;
   DeviceBuffer d_rcand, d_rpart;          // batched residual candidates / partials
+  DeviceBuffer d_tb, d_bpart;             // block Krylov: SpMM output (n x 8), block-projection partials
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   int64_t nparts = 0;
@@ -222,6 +242,15 @@ struct OperatorEngine {
   // beta = ||r||_B with B r from one M-product; v_next = r / beta, bv_next = B r / beta
   void bnorm_normalize_b(const double* r, double* beta_out, double* v_next, double* bv_next);
   void dot2n(const double* x, const double* y, double* out);  // out = x.y (2n)
+  // Block Krylov-Schur (bs <= 8 vectors, column j at V + j 2n):
+  // R[:, j] = L(s)^{-1} B V[:, j] through the multi-RHS sweeps
+  void apply_block(const double* V, int bs, double* R);
+  // allocate what apply_block / gemm_t need for bases up to kmax vectors (outside graph captures)
+  void prepare_block(int kmax, int bs);
+  // H[i + j ldh] = V[:, i] . R[:, j] for i < k, j < bs (deterministic two-stage reduction)
+  void gemm_t(const double* V, int k, const double* R, int bs, double* H, int ldh);
+  // R[:, j] -= sum_{i<k} V[:, i] H[i + j ldh], j < bs
+  void gemm_n(const double* V, int k, const double* H, int ldh, double* R, int bs);
   // Vout[c] = sum_k V[k] Q[k + c*ldq] for c < ncols (restart compression)
   void combine(const double* V, int k, const double* Q_dev, int ldq, int ncols, double* Vout);
   // Ritz vectors X = V^T-combination with Y (m x 2nc: columns Re y_c, Im y_c),

@@ -287,26 +287,39 @@ int rq_factor_get_info(const rq_factor_t* f, rq_factor_info* o) {
   });
 }
 
-int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs) {
+int rq_factor_solve_ex(rq_factor_t* f, const double* b, double* x, int nrhs, int block) {
   return guarded([&] {
     need(f, "factor");
     need(b, "b");
     need(x, "x");
+    if (nrhs < 0) rqb::fail(rqb::errc::dimension, "nrhs must be non-negative");
+    if (block < 1 || block > 8) rqb::fail(rqb::errc::config, "block must be 1..8");
     std::lock_guard<std::mutex> lock(f->fe->mu);
     rqb::FactorEngine& fe = *f->fe;
     const int64_t n = fe.n;
-    if (f->d_b.bytes < sizeof(double) * n) f->d_b.alloc(sizeof(double) * n);
-    if (f->d_x.bytes < sizeof(double) * n) f->d_x.alloc(sizeof(double) * n);
-    for (int r = 0; r < nrhs; ++r) {
-      rqb::cuda_check(cudaMemcpyAsync(f->d_b.p, b + r * n, sizeof(double) * n, cudaMemcpyHostToDevice,
-                                      fe.stream), "H2D b");
-      fe.solve_device(f->d_b.as<double>(), f->d_x.as<double>(), 1.0);
-      rqb::cuda_check(cudaMemcpyAsync(x + r * n, f->d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
-                                      fe.stream), "D2H x");
+    const int w = std::min(block, std::max(nrhs, 1));
+    if (f->d_b.bytes < sizeof(double) * n * w) f->d_b.alloc(sizeof(double) * n * w);
+    if (f->d_x.bytes < sizeof(double) * n * w) f->d_x.alloc(sizeof(double) * n * w);
+    for (int r = 0; r < nrhs; r += w) {
+      const int k = std::min(w, nrhs - r);
+      rqb::cuda_check(cudaMemcpyAsync(f->d_b.p, b + static_cast<int64_t>(r) * n, sizeof(double) * n * k,
+                                      cudaMemcpyHostToDevice, fe.stream), "H2D b");
+      if (block == 1)
+        fe.solve_device(f->d_b.as<double>(), f->d_x.as<double>(), 1.0);
+      else
+        rqb::rqb_msolve_enqueue(fe, f->d_b.as<double>(), n, k, f->d_x.as<double>(), n, 1.0, nullptr, 0, 0.0,
+                                nullptr);
+      rqb::cuda_check(cudaMemcpyAsync(x + static_cast<int64_t>(r) * n, f->d_x.p, sizeof(double) * n * k,
+                                      cudaMemcpyDeviceToHost, fe.stream), "D2H x");
     }
     rqb::cuda_check(cudaStreamSynchronize(fe.stream), "solve sync");
     fe.check_sweeps();
+    rqb::rqb_msolve_check(fe);
   });
+}
+
+int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs) {
+  return rq_factor_solve_ex(f, b, x, nrhs, nrhs > 1 ? 8 : 1);
 }
 
 int rq_factor_front_export(const rq_factor_t* f, int64_t front, double* dense, int32_t* ipiv,
@@ -562,6 +575,7 @@ int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, doub
     eo.guard = opts->guard;
     if (const char* e = std::getenv("RQB_GUARD_CLUSTER")) eo.guard_single_cluster = std::atoi(e);
     eo.profile = opts->profile;
+    eo.block = opts->block;
     eo.want_vectors = (vec_re && vec_im) ? 1 : 0;
     o->ledger = rqb::Ledger{};
     rqb::EigsResult r = rqb::solve_quadratic_device(*o->op, eo, o->ledger, o->norms1);

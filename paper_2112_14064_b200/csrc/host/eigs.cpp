@@ -139,26 +139,28 @@ struct Pinned {
 // over them stay valid as long as m does; no allocation, free or graph build
 // in a repeated solve.
 struct EigWorkspace {
-  int m = -1;
+  int m = -1, bs = 1;
   int64_t n2 = 0;
   DeviceBuffer dV, dV2, dBV, dBV2, dR, dW, dHa, dHb, dBeta, dQ, dX, dRes;
   Pinned ha, hb, betas;
   Pinned hv, hq, hy;  // staging of the host -> device copies (start vectors, restart Q, Ritz Y)
   // cycle graph per (start index, basis buffer) and the kernels it launches
   std::map<std::pair<int, const double*>, std::pair<cudaGraphExec_t, int64_t>> graphs;
-  EigWorkspace(int m_, int64_t n2_)
-      : m(m_), n2(n2_), ha(static_cast<size_t>(m_ + 1) * (m_ + 1)), hb(static_cast<size_t>(m_ + 1) * (m_ + 1)),
-        betas(m_ + 1), hv(static_cast<size_t>(n2_)), hq(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)),
-        hy(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)) {
-    dV.alloc(sizeof(double) * (m + 1) * n2);
-    dV2.alloc(sizeof(double) * (m + 1) * n2);
-    dBV.alloc(sizeof(double) * (m + 1) * n2);
-    dBV2.alloc(sizeof(double) * (m + 1) * n2);
-    dR.alloc(sizeof(double) * n2);
+  // basis of m + bs vectors (m accounted by H, a frontier block of bs), H
+  // (m + bs) x (m + bs) column-major
+  EigWorkspace(int m_, int64_t n2_, int bs_)
+      : m(m_), bs(bs_), n2(n2_), ha(static_cast<size_t>(m_ + bs_) * (m_ + bs_)),
+        hb(static_cast<size_t>(m_ + bs_) * (m_ + bs_)), betas(m_ + bs_), hv(static_cast<size_t>(n2_)),
+        hq(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)), hy(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)) {
+    dV.alloc(sizeof(double) * (m + bs) * n2);
+    dV2.alloc(sizeof(double) * (m + bs) * n2);
+    dBV.alloc(sizeof(double) * (m + bs) * n2);
+    dBV2.alloc(sizeof(double) * (m + bs) * n2);
+    dR.alloc(sizeof(double) * n2 * bs);
     dW.alloc(sizeof(double) * n2);
-    dHa.alloc(sizeof(double) * (m + 1) * (m + 1));
-    dHb.alloc(sizeof(double) * (m + 1) * (m + 1));
-    dBeta.alloc(sizeof(double) * (m + 1));
+    dHa.alloc(sizeof(double) * (m + bs) * (m + bs));
+    dHb.alloc(sizeof(double) * (m + bs) * (m + bs));
+    dBeta.alloc(sizeof(double) * (m + bs));
     dQ.alloc(sizeof(double) * (m + 1) * (2 * m + 2));
     dX.alloc(sizeof(double) * n2 * 2 * (m + 1));
     dRes.alloc(sizeof(double) * 4 * (m + 1));
@@ -178,8 +180,12 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   if (nev < 1) fail(errc::config, "nev must be positive");
   if (m <= nev) fail(errc::config, "Krylov dimension m must exceed nev");
   if (m > 512) fail(errc::config, "Krylov dimension above 512");
-  if (m >= n2) fail(errc::config, "Krylov dimension must be below 2N");
+  const int bs = std::max(1, o.block);  // block size (1: single-vector Krylov-Schur)
+  if (bs > 8) fail(errc::config, "block size above 8");
+  if (m + bs > n2) fail(errc::config, "Krylov dimension must be below 2N");
+  if (m < nev + bs) fail(errc::config, "block Krylov-Schur needs m >= nev + block");
   if (!(o.tol > 0)) fail(errc::config, "tolerance must be positive");
+  const int LDH = m + bs;  // leading dimension of H (rows: m accounted + the frontier block)
   const int keep_target = nev + std::min(20, m - nev - 1);
   const double sig = op.sigma;  // scaled shift
   const double vs = op.varsigma;
@@ -195,13 +201,14 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   // is a plain projection h = (BV)^T r (B = diag(I, M) symmetric) and each
   // step needs one M-product (for the new vector) instead of three
   EigWorkspace* wsp = static_cast<EigWorkspace*>(op.eig_ws.get());
-  if (!wsp || wsp->m != m || wsp->n2 != n2) {
+  if (!wsp || wsp->m != m || wsp->n2 != n2 || wsp->bs != bs) {
     op.eig_ws.reset();
-    auto fresh = std::make_shared<EigWorkspace>(m, n2);
+    auto fresh = std::make_shared<EigWorkspace>(m, n2, bs);
     wsp = fresh.get();
     op.eig_ws = fresh;
   }
   EigWorkspace& W = *wsp;
+  if (bs > 1) op.prepare_block(m + bs, bs);  // sweep plan + block workspaces before any graph capture
   DeviceBuffer &dV = W.dV, &dV2 = W.dV2, &dBV = W.dBV, &dBV2 = W.dBV2, &dR = W.dR, &dW = W.dW, &dHa = W.dHa, &dHb = W.dHb,
                &dBeta = W.dBeta, &dQ = W.dQ, &dX = W.dX, &dRes = W.dRes;
   double* V = dV.as<double>();
@@ -214,28 +221,36 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   cuda_check(cudaEventCreate(&e_a), "event");
   cuda_check(cudaEventCreate(&e_b), "event");
 
-  // Start vector v = splitmix64(seed) uniform[-1,1]^{2N}, B-normalised.
-  auto fresh_vector = [&](uint64_t seed, int nlock, double* dst, double* dst_b) {
-    std::vector<double> v(n2);
-    uint64_t s = seed;
-    for (int64_t i = 0; i < n2; ++i) v[i] = splitmix_uniform(s);
-    std::memcpy(W.hv.data(), v.data(), sizeof(double) * n2);
-    cuda_check(cudaMemcpyAsync(r, W.hv.data(), sizeof(double) * n2, cudaMemcpyHostToDevice, st), "H2D v0");
-    for (int pass = 0; pass < 2 && nlock > 0; ++pass) {
-      op.gemv_t(BV, nlock, r, dHa.as<double>());
-      op.gemv_n(V, nlock, dHa.as<double>(), r, nullptr);
-      charge_bproduct(L, op);  // ledger: the reference algorithm's B-product
-      charge_vv2n(L, op, 2 * nlock);
+  // Start block: vector i = splitmix64(seed + i * golden) uniform[-1,1]^{2N}
+  // (i = 0: the single-vector start), B-orthogonalised (CGS2) against the
+  // nlock vectors before it and the earlier members of the block, B-normalised
+  // into V[nlock + i].
+  auto fresh_block = [&](uint64_t seed, int nlock, int count) {
+    for (int b = 0; b < count; ++b) {
+      const int nb = nlock + b;
+      std::vector<double> v(n2);
+      uint64_t s = seed + 0x9E3779B97F4A7C15ull * static_cast<uint64_t>(b);
+      for (int64_t i = 0; i < n2; ++i) v[i] = splitmix_uniform(s);
+      cuda_check(cudaStreamSynchronize(st), "sync staging");  // the pinned staging buffer is free again
+      std::memcpy(W.hv.data(), v.data(), sizeof(double) * n2);
+      cuda_check(cudaMemcpyAsync(r, W.hv.data(), sizeof(double) * n2, cudaMemcpyHostToDevice, st), "H2D v0");
+      for (int pass = 0; pass < 2 && nb > 0; ++pass) {
+        op.gemv_t(BV, nb, r, dHa.as<double>());
+        op.gemv_n(V, nb, dHa.as<double>(), r, nullptr);
+        charge_bproduct(L, op);  // ledger: the reference algorithm's B-product
+        charge_vv2n(L, op, 2 * nb);
+      }
+      op.bnorm_normalize_b(r, dBeta.as<double>() + LDH - 1, V + static_cast<int64_t>(nb) * n2,
+                           BV + static_cast<int64_t>(nb) * n2);
+      charge_bproduct(L, op);
+      charge_vv2n(L, op, 1);
     }
-    op.bnorm_normalize_b(r, dBeta.as<double>() + m, dst, dst_b);
-    charge_bproduct(L, op);
-    charge_vv2n(L, op, 1);
   };
 
-  std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0);  // column-major (m+1) x m
-  auto Hc = [&](int i, int j) -> double& { return H[i + static_cast<size_t>(j) * (m + 1)]; };
+  std::vector<double> H(static_cast<size_t>(LDH) * m, 0.0);  // column-major (m+bs) x m
+  auto Hc = [&](int i, int j) -> double& { return H[i + static_cast<size_t>(j) * LDH]; };
 
-  fresh_vector(o.seed, 0, V, BV);
+  fresh_block(o.seed, 0, bs);
   int k = 0;
   int cycles = 0, guard_passes = 0, pass_cycles = 0;
   bool converged_final = false;
@@ -268,11 +283,22 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     ++cycles;
     ++pass_cycles;
     // ---- Arnoldi steps k .. m-1: one CUDA graph per (start, basis buffer) ----
+    // block step at kc (bs = 1: an Arnoldi step): R = S V[kc, kc+bs); CGS2
+    // against V[0, kt), kt = kc + bs (block projections: every basis vector
+    // read once per pass for the whole block); then the block's own
+    // Gram-Schmidt (CGS2 against its earlier members) and B-normalisation into
+    // V[kt + j]. H column kc + j: rows [0, kt + j) projections, row kt + j the
+    // B-norm. The cycle ends at mm = the last kc with kc + bs > m.
     auto enqueue_steps = [&](bool prof, bool skip_first) {
-      for (int j = k; j < m; ++j) {
+      for (int j = k; j + bs <= m; j += bs) {
         double* vj = V + static_cast<int64_t>(j) * n2;
         if (prof) cuda_check(cudaEventRecord(e_a, st), "ev");
-        if (!(skip_first && j == k)) op.apply(vj, r);
+        if (!(skip_first && j == k)) {
+          if (bs == 1)
+            op.apply(vj, r);
+          else
+            op.apply_block(vj, bs, r);
+        }
         if (prof) {
           cuda_check(cudaEventRecord(e_b, st), "ev");
           cuda_check(cudaEventSynchronize(e_b), "ev");
@@ -281,16 +307,39 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
           t_solve += ms;
           cuda_check(cudaEventRecord(e_a, st), "ev");
         }
-        double* hA = dHa.as<double>() + static_cast<int64_t>(j) * (m + 1);
-        double* hB = dHb.as<double>() + static_cast<int64_t>(j) * (m + 1);
-        // CGS2 with the stored B-images: h = (BV)^T r, r -= V h (twice),
-        // then ||r||_B, v_{j+1} = r / beta and B v_{j+1} from one M-product
-        op.gemv_t(BV, j + 1, r, hA);
-        op.gemv_n(V, j + 1, hA, r, nullptr);
-        op.gemv_t(BV, j + 1, r, hB);
-        op.gemv_n(V, j + 1, hB, r, nullptr);
-        op.bnorm_normalize_b(r, dBeta.as<double>() + j, V + static_cast<int64_t>(j + 1) * n2,
-                             BV + static_cast<int64_t>(j + 1) * n2);
+        double* hA = dHa.as<double>() + static_cast<int64_t>(j) * LDH;
+        double* hB = dHb.as<double>() + static_cast<int64_t>(j) * LDH;
+        const int kt = j + bs;
+        if (bs == 1) {
+          // CGS2 with the stored B-images: h = (BV)^T r, r -= V h (twice),
+          // then ||r||_B, v_{j+1} = r / beta and B v_{j+1} from one M-product
+          op.gemv_t(BV, kt, r, hA);
+          op.gemv_n(V, kt, hA, r, nullptr);
+          op.gemv_t(BV, kt, r, hB);
+          op.gemv_n(V, kt, hB, r, nullptr);
+          op.bnorm_normalize_b(r, dBeta.as<double>() + j, V + static_cast<int64_t>(kt) * n2,
+                               BV + static_cast<int64_t>(kt) * n2);
+        } else {
+          op.gemm_t(BV, kt, r, bs, hA, LDH);
+          op.gemm_n(V, kt, hA, LDH, r, bs);
+          op.gemm_t(BV, kt, r, bs, hB, LDH);
+          op.gemm_n(V, kt, hB, LDH, r, bs);
+          const double* BVn = BV + static_cast<int64_t>(kt) * n2;
+          const double* Vn = V + static_cast<int64_t>(kt) * n2;
+          for (int b = 0; b < bs; ++b) {
+            double* rb = r + static_cast<int64_t>(b) * n2;
+            if (b > 0) {
+              double* ha_b = hA + kt + static_cast<int64_t>(b) * LDH;
+              double* hb_b = hB + kt + static_cast<int64_t>(b) * LDH;
+              op.gemv_t(BVn, b, rb, ha_b);
+              op.gemv_n(Vn, b, ha_b, rb, nullptr);
+              op.gemv_t(BVn, b, rb, hb_b);
+              op.gemv_n(Vn, b, hb_b, rb, nullptr);
+            }
+            op.bnorm_normalize_b(rb, dBeta.as<double>() + j + b, V + static_cast<int64_t>(kt + b) * n2,
+                                 BV + static_cast<int64_t>(kt + b) * n2);
+          }
+        }
         if (prof) {
           cuda_check(cudaEventRecord(e_b, st), "ev");
           cuda_check(cudaEventSynchronize(e_b), "ev");
@@ -324,55 +373,92 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       op.launches += it->second.second;  // the same count on every call, cached graph or not
       res.graph_launches += 1;
     }
-    for (int j = k; j < m; ++j) {  // per step: apply + 2 x (B-product, j+1 dots, j+1 axpys) + B-norm
-      charge_apply(L, op);
-      for (int pass = 0; pass < 3; ++pass) charge_bproduct(L, op);
-      charge_vv2n(L, op, 4 * (j + 1) + 1);
+    const int mm = k + bs * ((m - k) / bs);  // columns of H after this cycle
+    for (int j = k; j + bs <= m; j += bs) {
+      // per step (bs = 1): apply + 2 x (B-product, j+1 dots, j+1 axpys) + B-norm;
+      // per block step: bs applies, 2 x (bs B-products, 2 kt bs dots/axpys),
+      // the block's own CGS2 (2 x (B-product, 2b dots/axpys) for member b > 0)
+      // and bs B-norms (B-product + dot) — the oracle's block mode, op for op
+      const int kt = j + bs;
+      for (int b = 0; b < bs; ++b) charge_apply(L, op);
+      if (bs == 1) {
+        for (int pass = 0; pass < 3; ++pass) charge_bproduct(L, op);
+        charge_vv2n(L, op, 4 * kt + 1);
+      } else {
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int b = 0; b < bs; ++b) charge_bproduct(L, op);
+          charge_vv2n(L, op, 2 * static_cast<int64_t>(kt) * bs);
+        }
+        for (int b = 0; b < bs; ++b) {
+          if (b > 0)
+            for (int pass = 0; pass < 2; ++pass) {
+              charge_bproduct(L, op);
+              charge_vv2n(L, op, 2 * b);
+            }
+          charge_bproduct(L, op);
+          charge_vv2n(L, op, 1);
+        }
+      }
     }
-    cuda_check(cudaMemcpyAsync(ha.data(), dHa.p, sizeof(double) * (m + 1) * (m + 1),
-                               cudaMemcpyDeviceToHost, st), "D2H H");
-    cuda_check(cudaMemcpyAsync(hb.data(), dHb.p, sizeof(double) * (m + 1) * (m + 1),
-                               cudaMemcpyDeviceToHost, st), "D2H H");
-    cuda_check(cudaMemcpyAsync(betas.data(), dBeta.p, sizeof(double) * (m + 1),
-                               cudaMemcpyDeviceToHost, st), "D2H beta");
+    cuda_check(cudaMemcpyAsync(ha.data(), dHa.p, sizeof(double) * LDH * LDH, cudaMemcpyDeviceToHost, st), "D2H H");
+    cuda_check(cudaMemcpyAsync(hb.data(), dHb.p, sizeof(double) * LDH * LDH, cudaMemcpyDeviceToHost, st), "D2H H");
+    cuda_check(cudaMemcpyAsync(betas.data(), dBeta.p, sizeof(double) * LDH, cudaMemcpyDeviceToHost, st),
+               "D2H beta");
     cuda_check(cudaEventRecord(e_h, st), "ev");
-    // Speculatively apply the operator to v_m: unless the cycle ends in a
-    // deflated restart (fresh vector), v_m is the next cycle's continuation
-    // vector V[p], so the solve overlaps the host's Ritz / restart work.
+    // Speculatively apply the operator to the frontier block V[mm, mm+bs):
+    // unless the cycle ends in a deflated restart (fresh vectors), it is the
+    // next cycle's continuation block V[p, p+bs), so the solve overlaps the
+    // host's Ritz / restart work.
     pre_applied = !o.profile;
-    if (pre_applied) op.apply(V + static_cast<int64_t>(m) * n2, r);
+    if (pre_applied) {
+      if (bs == 1)
+        op.apply(V + static_cast<int64_t>(mm) * n2, r);
+      else
+        op.apply_block(V + static_cast<int64_t>(mm) * n2, bs, r);
+    }
     {
       const auto ts0 = now();
       cuda_check(cudaEventSynchronize(e_h), "sync");
       t_sync += ms_since(ts0);  // host blocked on the cycle's Arnoldi steps
     }
-    for (int j = k; j < m; ++j) {
-      for (int i = 0; i <= j; ++i)
-        Hc(i, j) = ha[i + static_cast<size_t>(j) * (m + 1)] + hb[i + static_cast<size_t>(j) * (m + 1)];
-      Hc(j + 1, j) = betas[j];
+    for (int j = k; j < mm; ++j) {
+      const int jb = j - (j - k) % bs, kt = jb + bs, b = j - jb;  // block start, its kt, member
+      for (int i = 0; i < kt + b; ++i)
+        Hc(i, j) = ha[i + static_cast<size_t>(j) * LDH] + hb[i + static_cast<size_t>(j) * LDH];
+      Hc(kt + b, j) = betas[j];
     }
-    // ---- Ritz extraction ----
-    std::vector<double> Hm(static_cast<size_t>(m) * m);
-    for (int j = 0; j < m; ++j)
-      for (int i = 0; i < m; ++i) Hm[i + static_cast<size_t>(j) * m] = Hc(i, j);
+    // ---- Ritz extraction (H_mm is upper Hessenberg for bs = 1, banded with
+    // bs subdiagonals for a block; after a restart it is a full matrix) ----
+    std::vector<double> Hm(static_cast<size_t>(mm) * mm);
+    for (int j = 0; j < mm; ++j)
+      for (int i = 0; i < mm; ++i) Hm[i + static_cast<size_t>(j) * mm] = Hc(i, j);
     CMat T, Z;
     const auto tr0 = now();
-    if (!complex_schur(Hm, m, T, Z)) fail(errc::solver, "Hessenberg QR did not converge");
+    if (!complex_schur(Hm, mm, T, Z)) fail(errc::solver, "Hessenberg QR did not converge");
     const CMat Y = triangular_eigvecs(T);
     t_ritz += ms_since(tr0);
-    const double beta_m = Hc(m, m - 1);
-    std::vector<Ritz> rz(m);
-    for (int i = 0; i < m; ++i) {
+    // residual rows: S V_mm = V_mm H_mm + V[mm, mm+bs) E, E = H[mm.., 0..mm) (nonzero
+    // only in the last block's columns)
+    const int m0 = mm - bs;
+    std::vector<Ritz> rz(mm);
+    for (int i = 0; i < mm; ++i) {
       rz[i].theta = T(i, i);
       rz[i].lambda = (sig + 1.0 / rz[i].theta) * vs;
-      // y_i in the H basis = Z Y[:, i]; residual estimate |beta_m e_m^T y_i| / |theta|
-      cplx ylast = 0.0;
-      for (int t = 0; t <= i; ++t) ylast += Z(m - 1, t) * Y(t, i);
-      rz[i].est = std::abs(beta_m * ylast) / std::max(std::abs(rz[i].theta), 1e-300);
+      // y_i = Z Y[:, i]; residual estimate ||E y_i|| / |theta| (bs = 1: |beta_m e_m^T y_i| / |theta|)
+      std::vector<cplx> ylast(bs, 0.0);
+      for (int q = 0; q < bs; ++q)
+        for (int t = 0; t <= i; ++t) ylast[q] += Z(m0 + q, t) * Y(t, i);
+      double e2 = 0.0;
+      for (int a = 0; a < bs; ++a) {
+        cplx s = 0.0;
+        for (int q = 0; q < bs; ++q) s += Hc(mm + a, m0 + q) * ylast[q];
+        e2 += std::norm(s);
+      }
+      rz[i].est = std::sqrt(e2) / std::max(std::abs(rz[i].theta), 1e-300);
       rz[i].idx = i;
     }
     // wanted order: largest |theta| first; conjugate pairs adjacent (+imag first)
-    std::vector<int> order(m);
+    std::vector<int> order(mm);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
       const double da = dist(rz[a].lambda, sig * vs), db = dist(rz[b].lambda, sig * vs);
@@ -384,20 +470,20 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     // conjugation and never split a cluster: the real basis of the kept complex
     // Schur vectors then spans an invariant subspace to ~eps / 1e-4.
     std::vector<std::vector<int>> groups;
-    std::vector<int> group_of(m, -1);
+    std::vector<int> group_of(mm, -1);
     {
-      std::vector<int> par(m);
+      std::vector<int> par(mm);
       std::iota(par.begin(), par.end(), 0);
       std::function<int(int)> find = [&](int x) { return par[x] == x ? x : par[x] = find(par[x]); };
-      for (int i = 0; i < m; ++i)
-        for (int q = i + 1; q < m; ++q) {
+      for (int i = 0; i < mm; ++i)
+        for (int q = i + 1; q < mm; ++q) {
           const cplx a = rz[i].theta, b = rz[q].theta;
           const double scale = std::max(std::abs(a), std::abs(b));
           if (std::abs(a - b) <= kClusterGap * scale || std::abs(a - std::conj(b)) <= kClusterGap * scale)
             par[find(i)] = find(q);
         }
-      std::vector<int> root_group(m, -1);
-      for (int a = 0; a < m; ++a) {  // groups in wanted order of their best member
+      std::vector<int> root_group(mm, -1);
+      for (int a = 0; a < mm; ++a) {  // groups in wanted order of their best member
         const int i = order[a];
         const int r = find(i);
         if (root_group[r] < 0) {
@@ -412,7 +498,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     std::vector<int> cand(order.begin(), order.begin() + nev);
     std::vector<int> chk = cand;
     {
-      std::vector<int> in(m, 0);
+      std::vector<int> in(mm, 0);
       for (int i : cand) in[i] = 1;
       for (int i : cand)
         for (int q : groups[group_of[i]])
@@ -424,6 +510,23 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     // cycles passed) before checking again
     double est_worst = 0.0;
     for (int i : cand) est_worst = std::max(est_worst, rz[i].est);
+    if (bs > 1 && o.guard_single_cluster) {
+      // block mode: when the nev nearest are members of one (degenerate)
+      // cluster, which nev of its members rank "nearest" is arbitrary, and a
+      // block brings in up to 2 bs fresh copies per step; gate the explicit
+      // check on the nev-th best estimate among the cluster's members (all of
+      // them are checked: chk holds the whole group) instead of the worst of an
+      // arbitrary nev
+      const int g0 = group_of[cand[0]];
+      bool one = true;
+      for (int c = 1; c < nev && one; ++c) one = group_of[cand[c]] == g0;
+      if (one && static_cast<int>(groups[g0].size()) > nev) {
+        std::vector<double> e;
+        for (int i : groups[g0]) e.push_back(rz[i].est);
+        std::nth_element(e.begin(), e.begin() + (nev - 1), e.end());
+        est_worst = e[nev - 1];
+      }
+    }
     const bool maybe = est_worst <= check_gate || (est_worst <= o.est_factor * o.tol && since_check >= 8);
     ++since_check;
     bool all_conv = false, mates_conv = false;
@@ -432,19 +535,19 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     const auto tc0 = now();
     if (maybe) {
       // Ritz vectors X = V_m [Re y, Im y] (y = Z Y[:, i])
-      std::vector<double> Yr(static_cast<size_t>(m) * 2 * nchk);
-      std::vector<cplx> ycol(m);
+      std::vector<double> Yr(static_cast<size_t>(mm) * 2 * nchk);
+      std::vector<cplx> ycol(mm);
       for (int c = 0; c < nchk; ++c) {
         const int i = chk[c];
         std::fill(ycol.begin(), ycol.end(), cplx(0.0));
         for (int t = 0; t <= i; ++t) {  // y = Z[:, 0..i] Y[0..i, i] (Y upper triangular)
           const cplx yt = Y(t, i);
-          const cplx* zc = &Z.a[static_cast<size_t>(t) * m];
-          for (int row = 0; row < m; ++row) ycol[row] += zc[row] * yt;
+          const cplx* zc = &Z.a[static_cast<size_t>(t) * mm];
+          for (int row = 0; row < mm; ++row) ycol[row] += zc[row] * yt;
         }
-        for (int row = 0; row < m; ++row) {
-          Yr[row + static_cast<size_t>(2 * c) * m] = ycol[row].real();
-          Yr[row + static_cast<size_t>(2 * c + 1) * m] = ycol[row].imag();
+        for (int row = 0; row < mm; ++row) {
+          Yr[row + static_cast<size_t>(2 * c) * mm] = ycol[row].real();
+          Yr[row + static_cast<size_t>(2 * c + 1) * mm] = ycol[row].imag();
         }
       }
       const double* ysrc = Yr.data();
@@ -461,7 +564,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         lam[2 * c + 1] = gam.imag();
       }
       // X = V_m [Re y, Im y] (one DGEMM, row-major) + all residuals in one SpMM pass
-      op.ritz_residuals(V, m, dQ.as<double>(), nchk, lam.data(), cblock.data(), dX.as<double>(),
+      op.ritz_residuals(V, mm, dQ.as<double>(), nchk, lam.data(), cblock.data(), dX.as<double>(),
                         dRes.as<double>());
       last_nchk = nchk;
       std::vector<double> rr(2 * nchk);
@@ -563,7 +666,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     }
 
     // ---- decide: done / guard (deflated) restart / normal restart ----
-    std::vector<int> sel(m, 0);
+    std::vector<int> sel(mm, 0);
     int p = 0;
     bool deflate = false;
     if (all_conv) {
@@ -578,7 +681,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         converged_final = true;
         break;
       }
-      if (mates_conv && nchk <= m - 1) {
+      if (mates_conv && nchk <= m - bs) {
         // every kept direction is converged: deflate them (b = 0) and restart
         // the Krylov space from a fresh seeded vector (SPEC.md:457 fallback)
         prev_guard_dists = dists;
@@ -591,23 +694,23 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     }
     if (!deflate) {
       for (const auto& g : groups) {
-        if (p >= keep_target || p + static_cast<int>(g.size()) > m - 1) break;
+        if (p >= keep_target || p + static_cast<int>(g.size()) > m - bs) break;
         for (int i : g) sel[i] = 1;
         p += static_cast<int>(g.size());
       }
       if (p == 0) {  // one cluster fills the whole space: fall back to conjugate pairs
-        for (int a = 0; a < m && p < keep_target; ++a) {
+        for (int a = 0; a < mm && p < keep_target; ++a) {
           const int i = order[a];
           if (sel[i]) continue;
           int partner = -1;
           double bd = 1e300;
           if (std::abs(rz[i].theta.imag()) > 1e-12 * std::abs(rz[i].theta))
-            for (int q = 0; q < m; ++q)
+            for (int q = 0; q < mm; ++q)
               if (q != i && !sel[q]) {
                 const double d = std::abs(rz[q].theta - std::conj(rz[i].theta));
                 if (d < bd) bd = d, partner = q;
               }
-          if (p + 1 + (partner >= 0) > m - 1) break;
+          if (p + 1 + (partner >= 0) > m - bs) break;
           sel[i] = 1, ++p;
           if (partner >= 0) sel[partner] = 1, ++p;
         }
@@ -624,22 +727,22 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     if (p <= 0) fail(errc::solver, "Krylov-Schur restart lost its basis");
     // T_p = Q_p^T H_m Q_p, b_p = beta_m e_m^T Q_p
     // (column-oriented loops: every inner loop is a contiguous axpy / dot)
-    std::vector<double> HQ(static_cast<size_t>(m) * p, 0.0), Tp(static_cast<size_t>(p) * p, 0.0);
+    std::vector<double> HQ(static_cast<size_t>(mm) * p, 0.0), Tp(static_cast<size_t>(p) * p, 0.0);
     for (int c = 0; c < p; ++c) {
-      double* hq = HQ.data() + static_cast<size_t>(c) * m;
-      for (int t = 0; t < m; ++t) {
-        const double q = Qp[t + static_cast<size_t>(c) * m];
+      double* hq = HQ.data() + static_cast<size_t>(c) * mm;
+      for (int t = 0; t < mm; ++t) {
+        const double q = Qp[t + static_cast<size_t>(c) * mm];
         if (q == 0.0) continue;
-        const double* ht = Hm.data() + static_cast<size_t>(t) * m;
-        for (int i = 0; i < m; ++i) hq[i] += ht[i] * q;
+        const double* ht = Hm.data() + static_cast<size_t>(t) * mm;
+        for (int i = 0; i < mm; ++i) hq[i] += ht[i] * q;
       }
     }
     for (int c = 0; c < p; ++c) {
-      const double* hq = HQ.data() + static_cast<size_t>(c) * m;
+      const double* hq = HQ.data() + static_cast<size_t>(c) * mm;
       for (int i = 0; i < p; ++i) {
-        const double* qi = Qp.data() + static_cast<size_t>(i) * m;
+        const double* qi = Qp.data() + static_cast<size_t>(i) * mm;
         double s = 0;
-        for (int t = 0; t < m; ++t) s += qi[t] * hq[t];
+        for (int t = 0; t < mm; ++t) s += qi[t] * hq[t];
         Tp[i + static_cast<size_t>(c) * p] = s;
       }
     }
@@ -647,47 +750,57 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       // invariance defect ||H Q_p - Q_p T_p|| / ||H|| (exact restart needs ~eps)
       double dmax = 0, hmax = 0;
       for (double x : Hm) hmax = std::max(hmax, std::fabs(x));
-      std::vector<double> rc(m);
+      std::vector<double> rc(mm);
       for (int c = 0; c < p; ++c) {
-        std::copy(HQ.begin() + static_cast<size_t>(c) * m, HQ.begin() + static_cast<size_t>(c + 1) * m, rc.begin());
+        std::copy(HQ.begin() + static_cast<size_t>(c) * mm, HQ.begin() + static_cast<size_t>(c + 1) * mm, rc.begin());
         for (int t = 0; t < p; ++t) {
           const double tc = Tp[t + static_cast<size_t>(c) * p];
-          const double* qt = Qp.data() + static_cast<size_t>(t) * m;
-          for (int i = 0; i < m; ++i) rc[i] -= tc * qt[i];
+          const double* qt = Qp.data() + static_cast<size_t>(t) * mm;
+          for (int i = 0; i < mm; ++i) rc[i] -= tc * qt[i];
         }
-        for (int i = 0; i < m; ++i) dmax = std::max(dmax, std::fabs(rc[i]));
+        for (int i = 0; i < mm; ++i) dmax = std::max(dmax, std::fabs(rc[i]));
       }
       res.max_restart_defect = std::max(res.max_restart_defect, dmax / std::max(hmax, 1e-300));
     }
-    std::memcpy(W.hq.data(), Qp.data(), sizeof(double) * m * p);
-    cuda_check(cudaMemcpyAsync(dQ.p, W.hq.data(), sizeof(double) * m * p, cudaMemcpyHostToDevice, st), "H2D Q");
-    op.combine(V, m, dQ.as<double>(), m, p, V2);
-    op.combine(BV, m, dQ.as<double>(), m, p, BV2);
+    std::memcpy(W.hq.data(), Qp.data(), sizeof(double) * mm * p);
+    cuda_check(cudaMemcpyAsync(dQ.p, W.hq.data(), sizeof(double) * mm * p, cudaMemcpyHostToDevice, st), "H2D Q");
+    op.combine(V, mm, dQ.as<double>(), mm, p, V2);
+    op.combine(BV, mm, dQ.as<double>(), mm, p, BV2);
     L.n_restart += 1;
-    L.macs_restart += static_cast<double>(m) * p * n2;
+    L.macs_restart += static_cast<double>(mm) * p * n2;
+    // the new residual rows E Q_p before H is cleared (E: rows mm.., last block's columns)
+    std::vector<double> EQ(static_cast<size_t>(bs) * p, 0.0);
+    for (int a = 0; a < bs; ++a)
+      for (int c = 0; c < p; ++c) {
+        double s = 0.0;
+        for (int q = 0; q < bs; ++q) s += Hc(mm + a, m0 + q) * Qp[(m0 + q) + static_cast<size_t>(c) * mm];
+        EQ[a + static_cast<size_t>(c) * bs] = s;
+      }
     std::fill(H.begin(), H.end(), 0.0);
     for (int c = 0; c < p; ++c)
       for (int i = 0; i < p; ++i) Hc(i, c) = Tp[i + static_cast<size_t>(c) * p];
     std::swap(V, V2);
     std::swap(BV, BV2);
     if (deflate) {
-      // b = 0 (converged directions deflated); fresh seeded continuation vector
-      // (the speculative apply of v_m is discarded)
+      // b = 0 (converged directions deflated); fresh seeded continuation block
+      // (the speculative apply of the frontier block is discarded)
       pre_applied = false;
-      fresh_vector(o.seed + 0x1000003ull * guard_passes, p, V + static_cast<int64_t>(p) * n2,
-                   BV + static_cast<int64_t>(p) * n2);
+      fresh_block(o.seed + 0x1000003ull * guard_passes, p, bs);
     } else {
-      for (int c = 0; c < p; ++c) Hc(p, c) = beta_m * Qp[(m - 1) + static_cast<size_t>(c) * m];
-      cuda_check(cudaMemcpyAsync(V + static_cast<int64_t>(p) * n2, V2 + static_cast<int64_t>(m) * n2,
-                                 sizeof(double) * n2, cudaMemcpyDeviceToDevice, st), "D2D v");
-      cuda_check(cudaMemcpyAsync(BV + static_cast<int64_t>(p) * n2, BV2 + static_cast<int64_t>(m) * n2,
-                                 sizeof(double) * n2, cudaMemcpyDeviceToDevice, st), "D2D Bv");
+      for (int a = 0; a < bs; ++a)
+        for (int c = 0; c < p; ++c) Hc(p + a, c) = EQ[a + static_cast<size_t>(c) * bs];
+      cuda_check(cudaMemcpyAsync(V + static_cast<int64_t>(p) * n2, V2 + static_cast<int64_t>(mm) * n2,
+                                 sizeof(double) * n2 * bs, cudaMemcpyDeviceToDevice, st), "D2D v");
+      cuda_check(cudaMemcpyAsync(BV + static_cast<int64_t>(p) * n2, BV2 + static_cast<int64_t>(mm) * n2,
+                                 sizeof(double) * n2 * bs, cudaMemcpyDeviceToDevice, st), "D2D Bv");
     }
     t_restart += ms_since(trs0);
     if (trace_cycles)
-      std::fprintf(stderr, "[eigs] cycle %d: steps %d..%d, checked %d (maybe %d, nconv %d), groups %zu, kept %d%s, "
-                   "t ritz %.1f check %.1f restart %.1f sync %.1f ms\n", cycles, k, m, maybe ? nchk : 0, (int)maybe,
-                   nconv_now, groups.size(), p, deflate ? " (deflated restart)" : "", t_ritz, t_check, t_restart, t_sync);
+      std::fprintf(stderr, "[eigs] cycle %d: steps %d..%d, checked %d (maybe %d, nconv %d), est worst %.2e best %.2e, "
+                   "groups %zu (first %zu), kept %d%s, t ritz %.1f check %.1f restart %.1f sync %.1f ms\n", cycles, k,
+                   mm, maybe ? nchk : 0, (int)maybe, nconv_now, est_worst, rz[order[0]].est, groups.size(),
+                   groups.empty() ? size_t(0) : groups[0].size(), p, deflate ? " (deflated restart)" : "", t_ritz,
+                   t_check, t_restart, t_sync);
     k = p;
   }
   op.fac->check_sweeps();  // watchdog of the triangular sweeps (syncs the stream)

@@ -51,6 +51,7 @@ struct EigsOptions {
   double est_factor = 1e3;  // candidates are checked explicitly once est <= est_factor * tol
   int want_vectors = 0;
   int profile = 0;
+  int block = 1;  // block Krylov-Schur block size (1: single-vector; 2..8: SURVEY.md §8 f2)
 };
 
 struct EigsResult {

@@ -143,13 +143,15 @@ class ShiftInvertOperator:
 
     def solve_quadratic(self, nev: int, m: int = 0, eps: float = 1e-10, seed: int = 0,
                         max_restarts: int = 100, guard: bool = True, vectors: bool = False,
-                        raise_partial: bool = True, profile: bool = False):
+                        raise_partial: bool = True, profile: bool = False, block: int = 1):
+        """SPEC.md:462 solve_quadratic. block > 1 selects the block Krylov-Schur
+        (block size 2..8: multi-RHS sweeps, block CGS2)."""
         n = self.n
         lr, li, rs = np.zeros(nev), np.zeros(nev), np.ones(nev)
         vr = np.zeros(n * nev) if vectors else None
         vi = np.zeros(n * nev) if vectors else None
         opts = EigsOpts(int(nev), int(m), float(eps), int(seed), int(max_restarts), 1 if guard else 0,
-                        1 if profile else 0)
+                        1 if profile else 0, int(block))
         info = EigsInfo()
         rc = _lib.lib.rq_eigs_run(self._h, C.byref(opts), _lib.ptr(lr), _lib.ptr(li), _lib.ptr(rs),
                                   _lib.ptr(vr), _lib.ptr(vi), C.byref(info))

@@ -91,13 +91,18 @@ class Factorization:
     def refactor(self, values) -> None:
         check(_lib.lib.rq_factor_refactor(self._h, np.ascontiguousarray(values, np.float64)))
 
-    def solve(self, b: np.ndarray) -> np.ndarray:
+    def solve(self, b: np.ndarray, block: int | None = None) -> np.ndarray:
+        """x = A^{-1} b; b of shape (n,) or (n, nrhs). Several right-hand sides
+        pass through the multi-RHS sweeps, `block` (1..8, default 8) vectors per
+        pass over the factors; block=1 forces the single-vector sweeps."""
         b = np.asarray(b, dtype=np.float64)
         if b.shape[0] != self.n:
             raise RqError(7, "solve_factored dimension mismatch")
         bb = np.ascontiguousarray(b.reshape(self.n, -1).T)
         x = np.zeros_like(bb)
-        check(_lib.lib.rq_factor_solve(self._h, bb, x, bb.shape[0]))
+        if block is None:
+            block = 8 if bb.shape[0] > 1 else 1
+        check(_lib.lib.rq_factor_solve_ex(self._h, bb, x, bb.shape[0], int(block)))
         return x.T.reshape(b.shape)
 
     def front(self, f: int):
