@@ -303,6 +303,18 @@ def run_b200(args):
         infos.append(op.last_info)
         resid_max = max(resid_max, max(p.residual for p in pairs))
     info = infos[1]
+    # the same with the block Krylov-Schur (multi-RHS sweeps,
+    # block CGS2), block size args.block, same seeds
+    t_nev_b, infos_b, resid_b = [], [], 0.0
+    if args.block > 1:
+        for s_ in seeds:
+            t0 = time.perf_counter()
+            pairs = op.solve_quadratic(nev, eps=1e-10, seed=s_, max_restarts=args.max_restarts,
+                                       raise_partial=False, block=args.block)
+            t_nev_b.append((time.perf_counter() - t0) * 1e3 + op.factor_info()["factor_ms"])
+            infos_b.append(op.last_info)
+            resid_b = max(resid_b, max(p.residual for p in pairs))
+        op.release_workspace()
 
     # ---- per-kernel profile of one factorization (un-graphed, events per launch)
     ms_k = np.zeros(7)
@@ -316,6 +328,7 @@ def run_b200(args):
     t_gt = time_what(3 | 0x100, 10, m)
     t_gn = time_what(4 | 0x100, 10, m)
     t_rst = time_what(7 | 0x100, 5, m)
+    t_ms = {k: time_what(10 | 0x100, 10, k) for k in (1, 4, 8)}  # multi-RHS sweeps, k right-hand sides
     solve_bytes = st["trisolve_bytes"]
     spmv_bytes = 20.0 * P.nnz + 8.0 * (P.n + 1) + 24.0 * P.n
     gemv_bytes = 8.0 * 2 * P.n * m
@@ -328,6 +341,13 @@ def run_b200(args):
     kernels = {
         "factor_profile_ms": {KINDS[i]: round(float(ms_k[i]), 4) for i in range(7)},
         "trisolve": hb(t_solve, solve_bytes),
+        # multi-RHS sweeps: L/U read once for k vectors. frac_hbm counts the
+        # algorithmic bytes of ONE pass (factors + k solution/rhs vectors);
+        # per_vector_gbs = k single-vector solves' bytes over the pass time
+        "trisolve_multi_rhs": {str(k): dict(hb(t, solve_bytes + 8.0 * 4 * P.n * (k - 1)),
+                                            per_vector_gbs=round(k * solve_bytes / (t * 1e6), 1),
+                                            speedup_vs_single=round(k * t_solve / t, 3))
+                               for k, t in t_ms.items()},
         "spmv_fused_cm": hb(t_spmv, spmv_bytes),
         "cgs_gemv_t": dict(hb(t_gt, gemv_bytes), k=m),
         "cgs_gemv_n": dict(hb(t_gn, gemv_bytes), k=m),
@@ -451,6 +471,14 @@ def run_b200(args):
                             "device-resident operator (the degenerate cluster makes the cycle count seed- and "
                             "rounding-dependent); first_call = seed 0 on a fresh operator, which also allocates "
                             "the Krylov workspace and captures the cycle graphs",
+        "time_to_nev_block": None if not t_nev_b else {
+            "block": args.block, "ms": round(sorted(t_nev_b[1:])[len(t_nev_b[1:]) // 2], 3),
+            "first_call_ms": round(t_nev_b[0], 3), "min_ms": round(min(t_nev_b[1:]), 3),
+            "max_ms": round(max(t_nev_b[1:]), 3), "residual_max": resid_b,
+            "seeds": {str(s_): {"ms": round(t, 1), "cycles": i.get("restarts"), "n_fb": i.get("n_fb")}
+                      for s_, t, i in zip(seeds[1:], t_nev_b[1:], infos_b[1:])},
+            "note": "block Krylov-Schur (SURVEY.md 8 f2): block applies through the multi-RHS sweeps, block CGS2; "
+                    "median over the same seeds"},
         "eigs_residual_max": resid_max,
         "eigs_residual_tol": 1e-10,
         "eigs": {k: info.get(k) for k in ("restarts", "guard_passes", "n_fb", "n_mv", "n_vv",
@@ -490,6 +518,7 @@ def main():
     ap.add_argument("--config", default="cfg4_riga", choices=sorted(NEV))
     ap.add_argument("--nev", type=int, default=0)
     ap.add_argument("--nev-seeds", type=int, default=5)
+    ap.add_argument("--block", type=int, default=4, help="block size of the block Krylov-Schur line (<= 1: off)")
     ap.add_argument("--max-restarts", type=int, default=1000)
     ap.add_argument("--cpu-samples", type=int, default=1)
     ap.add_argument("--cpu-step-split", type=int, default=1)

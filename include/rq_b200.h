@@ -307,6 +307,40 @@ int rq_ritz_extract(const double* H, int m, double sigma, double varsigma, doubl
 int rq_operator_krylov_schur_restart(rq_operator_t* op, int m, int keep, double* V, double* H, int* p_out);
 
 /* ------------------------------------------------------------------------ */
+/* solve_generalized_hermitian (Alg. 1, Remark 3):  */
+/* A u = lambda B u, A symmetric, B symmetric positive definite, one CSR      */
+/* pattern, real shift s (the non-conductive Maxwell problem, Remark 2).      */
+/* Shift-invert Lanczos with thick restarts on S = (A - s B)^{-1} B: A - s B  */
+/* factored on the GPU (same multifrontal LU), N-vectors on the device,       */
+/* symmetric tridiagonal (arrowhead after a restart) projected matrix, real   */
+/* Ritz values, lambda = s + 1/theta. Converged on the explicit residual      */
+/* ||A u - lambda B u|| / ((||A||_1 + |lambda| ||B||_1) ||u||) <= tol.        */
+/* ------------------------------------------------------------------------ */
+typedef struct rq_gh rq_gh_t;
+typedef struct {
+  int nev;
+  int m;              /* Krylov dimension; <= 0: max(2 nev, nev + 20) */
+  double tol;
+  uint64_t seed;      /* splitmix64 start vector, uniform[-1,1] */
+  int max_restarts;   /* <= 0: 100 */
+} rq_gh_opts;
+typedef struct {
+  int nconv;
+  int cycles;
+  int restarts;
+  double lanczos_defect; /* max |v_i^T B S v_j| over i < j-1 (three-term structure) / ||T|| */
+  double sym_defect;     /* max |v_{j-1}^T B S v_j - beta_{j-1}| / ||T|| (symmetry of T) */
+  int64_t launches;
+  double t_total_ms;
+} rq_gh_info;
+int rq_gh_create(int64_t n, const int64_t* rowptr, const int32_t* col, const double* A, const double* B,
+                 const rq_symbolic_t* s, double shift, rq_gh_t** out);
+/* lam, resid: double[nev] (nearest the shift first); vec: n x nev column-major,
+ * unit 2-norm (may be NULL). Non-convergence -> RQ_E_SOLVER. */
+int rq_gh_run(rq_gh_t* h, const rq_gh_opts* opts, double* lam, double* resid, double* vec, rq_gh_info* info);
+void rq_gh_destroy(rq_gh_t* h);
+
+/* ------------------------------------------------------------------------ */
 /* Wire formats (reference sparse.cpp:121-174,         */
 /* SPEC.md:269, 371, 503). Host only.                                       */
 /* ------------------------------------------------------------------------ */

@@ -3,9 +3,9 @@ discretisations (arXiv 2112.14064). Host C++ + sm_100a CUDA behind the C-ABI in
 include/rq_b200.h; this package is the Python mirror of the reference's
 sparsela/eig operations."""
 from ._lib import LIB_PATH, RqError  # noqa: F401
-from .eig import (EigenPair, ShiftInvertOperator, apply_operator, arnoldi_run,  # noqa: F401
-                  b_inner, build_operator, krylov_schur_restart, ritz_extract, scale_pencil,
-                  solve_quadratic)
+from .eig import (EigenPair, GeneralizedHermitianSolver, ShiftInvertOperator, apply_operator,  # noqa: F401
+                  arnoldi_run, b_inner, build_operator, krylov_schur_restart, ritz_extract, scale_pencil,
+                  solve_generalized_hermitian, solve_quadratic)
 from .pencil import CURL, DIV, QuadraticPencil, assemble, baseline_config  # noqa: F401
 from .io import (eigenpairs_json, load_eigenpairs, read_matrix_market,  # noqa: F401
                  write_eigenpairs, write_matrix_market, write_matrix_market_vector, write_pencil)

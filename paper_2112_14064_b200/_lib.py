@@ -80,6 +80,17 @@ class EigsOpts(C.Structure):
                 ("max_restarts", C.c_int), ("guard", C.c_int), ("profile", C.c_int), ("block", C.c_int)]
 
 
+class GhOpts(C.Structure):
+    _fields_ = [("nev", C.c_int), ("m", C.c_int), ("tol", C.c_double), ("seed", C.c_uint64),
+                ("max_restarts", C.c_int)]
+
+
+class GhInfo(C.Structure):
+    _fields_ = [("nconv", C.c_int), ("cycles", C.c_int), ("restarts", C.c_int),
+                ("lanczos_defect", C.c_double), ("sym_defect", C.c_double), ("launches", C.c_int64),
+                ("t_total_ms", C.c_double)]
+
+
 class EigsInfo(C.Structure):
     _fields_ = [("nconv", C.c_int), ("restarts", C.c_int), ("guard_passes", C.c_int),
                 ("n_fa", C.c_int64), ("n_fb", C.c_int64), ("n_mv", C.c_int64),
@@ -158,6 +169,10 @@ _sig("rq_scale_pencil", C.c_int, C.c_int64, f64p, f64p, f64p, C.POINTER(C.c_doub
 _sig("rq_ritz_extract", C.c_int, f64p, C.c_int, C.c_double, C.c_double, vp, vp, vp, vp)
 _sig("rq_operator_krylov_schur_restart", C.c_int, vp, C.c_int, C.c_int, f64p, f64p, C.POINTER(C.c_int))
 
+_sig("rq_gh_create", C.c_int, C.c_int64, i64p, i32p, f64p, f64p, vp, C.c_double, C.POINTER(vp))
+_sig("rq_gh_run", C.c_int, vp, C.POINTER(GhOpts), f64p, f64p, vp, C.POINTER(GhInfo))
+_sig("rq_gh_destroy", None, vp)
+
 # every symbol include/rq_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = [
     "rq_last_error", "rq_version", "rq_set_device", "rq_pencil_assemble", "rq_pencil_assemble_device",
@@ -173,6 +188,7 @@ EXPORTS = [
     "rq_operator_time",
     "rq_eigs_run", "rq_eigs_ledger_json", "rq_operator_ledger", "rq_operator_ledger_json", "rq_operator_release_workspace",
     "rq_operator_ledger_reset", "rq_scale_pencil", "rq_ritz_extract", "rq_operator_krylov_schur_restart",
+    "rq_gh_create", "rq_gh_run", "rq_gh_destroy",
 ]
 
 

@@ -928,4 +928,141 @@ double OperatorEngine::time_op(int what, int iters, int param) {
   return total / iters;
 }
 
+// ---------------------------------------------------------------------------
+// Generalized Hermitian-definite path: A, B on one pattern,
+// factor of A - s B, operator S = (A - s B)^{-1} B on n-vectors.
+namespace {
+
+// q = A - s B on the shared pattern (each product and sum rounded separately)
+__global__ void gh_shifted_k(int64_t nnz, const double* A, const double* B, double s, double* Q) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    Q[k] = __dsub_rn(A[k], __dmul_rn(s, B[k]));
+}
+
+// r_c = A x_c - lam_c B x_c for one candidate per blockIdx.y, one warp per row;
+// partials of ||r||^2 and ||x||^2 per block (fixed order)
+__global__ void __launch_bounds__(kRedThreads) gh_residual_k(int64_t n, const int64_t* __restrict__ rowptr,
+                                                           const int32_t* __restrict__ col,
+                                                           const double* __restrict__ A,
+                                                           const double* __restrict__ B,
+                                                           const double* __restrict__ X,
+                                                           const double* __restrict__ lam,
+                                                           double* __restrict__ part) {
+  __shared__ double sr[kRedThreads / 32], sx[kRedThreads / 32];
+  const int c = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* x = X + (int64_t)c * n;
+  const double l = lam[c];
+  double accr = 0.0, accx = 0.0;
+  for (int64_t row = blockIdx.x * (int64_t)(kRedThreads / 32) + warp; row < n;
+       row += (int64_t)gridDim.x * (kRedThreads / 32)) {
+    double a = 0.0, b = 0.0;
+    for (int64_t k = rowptr[row] + lane; k < rowptr[row + 1]; k += 32) {
+      const double xv = x[col[k]];
+      a += A[k] * xv;
+      b += B[k] * xv;
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    const double r = a - l * b;
+    accr += r * r;
+    accx += x[row] * x[row];
+  }
+  if (lane == 0) sr[warp] = accr, sx[warp] = accx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) s0 += sr[w], s1 += sx[w];
+    part[(int64_t)(2 * c) * gridDim.x + blockIdx.x] = s0;
+    part[(int64_t)(2 * c + 1) * gridDim.x + blockIdx.x] = s1;
+  }
+}
+
+}  // namespace
+
+GhEngine::GhEngine(int64_t n_, const int64_t* rowptr, const int32_t* col, const double* A, const double* B,
+                   const Symbolic& s, double shift_)
+    : n(n_), shift(shift_) {
+  nnz = rowptr[n];
+  d_rowptr.alloc(sizeof(int64_t) * (n + 1));
+  d_col.alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  RQB_CUDA(cudaMemcpy(d_rowptr.p, rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+  RQB_CUDA(cudaMemcpy(d_col.p, col, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+  fac = std::make_unique<FactorEngine>(s, n, rowptr, col, nullptr, d_rowptr.as<int64_t>(), d_col.as<int32_t>());
+  stream = fac->stream;
+  d_A.upload(A, sizeof(double) * nnz, stream);
+  d_B.upload(B, sizeof(double) * nnz, stream);
+  DeviceBuffer q;
+  q.alloc(sizeof(double) * std::max<int64_t>(nnz, 1));
+  gh_shifted_k<<<148 * 8, 256, 0, stream>>>(nnz, d_A.as<double>(), d_B.as<double>(), shift, q.as<double>());
+  RQB_CUDA(cudaGetLastError());
+  fac->set_values_device(q.as<double>());
+  RQB_CUDA(cudaStreamSynchronize(stream));
+  d_t.alloc(sizeof(double) * std::max<int64_t>(n, 1));
+  gemv_t_chunk = std::min<int64_t>(4096, std::max<int64_t>(256, ((n + kRedBlocks - 1) / kRedBlocks + 255) / 256 * 256));
+  gemv_t_blocks = static_cast<int>((n + gemv_t_chunk - 1) / gemv_t_chunk);
+  d_part.alloc(sizeof(double) * std::max(kRedBlocks, gemv_t_blocks) * 512);
+  fac->factor();
+}
+
+void GhEngine::spmv(int which, const double* x, double* y) {
+  spmv_csr_k<<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
+                                                      which == 0 ? d_A.as<double>() : d_B.as<double>(), x, y);
+  ++launches;
+}
+
+void GhEngine::apply(const double* v, double* r) {
+  spmv(1, v, d_t.as<double>());
+  rqb_solve_enqueue(*fac, d_t.as<double>(), r, 1.0, nullptr, 0.0, nullptr);
+  launches += fac->launches_solve;
+}
+
+void GhEngine::gemv_t(const double* V, int k, const double* w, double* h) {
+  if (k <= 0) return;
+  if (k > 512) fail(errc::config, "Krylov dimension above 512");
+  gemv_t_part<<<gemv_t_blocks, kRedThreads, sizeof(double) * gemv_t_chunk, stream>>>(
+      V, k, n, w, w, n, gemv_t_chunk, d_part.as<double>());
+  reduce_parts<<<k, 32, 0, stream>>>(d_part.as<double>(), gemv_t_blocks, k, h, nullptr);
+  launches += 2;
+}
+
+void GhEngine::gemv_n(const double* V, int k, const double* h, double* r) {
+  if (k <= 0) return;
+  gemv_n_k<<<std::min(div_up(n, 256), 148 * 8), 256, sizeof(double) * k, stream>>>(V, k, n, h, r);
+  ++launches;
+}
+
+void GhEngine::bnorm_normalize(const double* r, double* beta_out, double* v, double* bv) {
+  double* t = d_t.as<double>();
+  spmv(1, r, t);  // t = B r
+  dot_part<<<kRedBlocks, kRedThreads, 0, stream>>>(r, r, t, t, n, n, d_part.as<double>());
+  // normalize_k writes v = r / beta; B v = t / beta by a second pass over t
+  normalize_k<<<std::min(div_up(n, 256), 148 * 8), 256, 0, stream>>>(d_part.as<double>(), kRedBlocks, r, n,
+                                                                    beta_out, v);
+  normalize_k<<<std::min(div_up(n, 256), 148 * 8), 256, 0, stream>>>(d_part.as<double>(), kRedBlocks, t, n,
+                                                                    nullptr, bv);
+  launches += 3;
+}
+
+void GhEngine::residuals(const double* X, int nc, const double* lam_host, double* out_host) {
+  if (nc <= 0) return;
+  const int nbx = kRedBlocks;
+  if (d_res.bytes < sizeof(double) * (2 * static_cast<size_t>(nc) * nbx + nc))
+    d_res.alloc(sizeof(double) * (2 * static_cast<size_t>(nc) * nbx + nc));
+  double* part = d_res.as<double>();
+  double* dlam = part + 2 * static_cast<size_t>(nc) * nbx;
+  RQB_CUDA(cudaMemcpyAsync(dlam, lam_host, sizeof(double) * nc, cudaMemcpyHostToDevice, stream));
+  gh_residual_k<<<dim3(nbx, nc), kRedThreads, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
+                                                           d_A.as<double>(), d_B.as<double>(), X, dlam, part);
+  std::vector<double> h(2 * static_cast<size_t>(nc) * nbx);
+  RQB_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, stream));
+  RQB_CUDA(cudaStreamSynchronize(stream));
+  launches += 1;
+  for (int c = 0; c < 2 * nc; ++c) {
+    double sacc = 0.0;
+    for (int b = 0; b < nbx; ++b) sacc += h[static_cast<size_t>(c) * nbx + b];
+    out_host[c] = sacc;
+  }
+}
+
 }  // namespace rqb

@@ -269,4 +269,31 @@ struct OperatorEngine {
   void init_workspaces();
 };
 
+// Generalized Hermitian-definite problem A u = lambda B u (SPEC.md:471-479,
+// solve_generalized_hermitian): A symmetric, B symmetric positive definite on
+// one CSR pattern, real shift s. The device holds A, B and the factorization
+// of A - s B; S = (A - s B)^{-1} B is B-self-adjoint, so its Krylov
+// decomposition is a Lanczos one (host driver: host/lanczos.cpp).
+struct GhEngine {
+  int64_t n = 0, nnz = 0;
+  double shift = 0.0;
+  std::unique_ptr<FactorEngine> fac;
+  DeviceBuffer d_rowptr, d_col, d_A, d_B, d_t, d_part, d_res;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  int64_t gemv_t_chunk = 256;
+  int gemv_t_blocks = 1;
+  GhEngine(int64_t n, const int64_t* rowptr, const int32_t* col, const double* A, const double* B,
+           const Symbolic& s, double shift);
+  void spmv(int which, const double* x, double* y);  // which 0: A, 1: B
+  void apply(const double* v, double* r);            // r = (A - s B)^{-1} B v
+  void gemv_t(const double* V, int k, const double* w, double* h);  // h = V[0..k)^T w
+  void gemv_n(const double* V, int k, const double* h, double* r);  // r -= V[0..k) h
+  // w = B r (one SpMV), beta = sqrt(r . w) -> *beta_out, v = r / beta, bv = w / beta
+  void bnorm_normalize(const double* r, double* beta_out, double* v, double* bv);
+  // out[2c] = ||A x_c - lam_c B x_c||^2, out[2c+1] = ||x_c||^2 for the nc
+  // column-major vectors X (ld n)
+  void residuals(const double* X, int nc, const double* lam_host, double* out_host);
+};
+
 }  // namespace rqb

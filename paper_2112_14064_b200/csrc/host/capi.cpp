@@ -3,6 +3,7 @@
 // boundary: every entry point returns an rq::errc value (reference
 // types.hpp:14-23) and leaves the message in rq_last_error().
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -16,6 +17,7 @@
 #include "common.hpp"
 #include "io.hpp"
 #include "eigs.hpp"
+#include "lanczos.hpp"
 #include "dense.hpp"
 
 struct rq_pencil {
@@ -944,3 +946,70 @@ int rq_eigenpairs_json(int n, const double* re, const double* im, const double* 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// solve_generalized_hermitian
+struct rq_gh {
+  std::unique_ptr<rqb::GhEngine> E;
+  double normA1 = 0.0, normB1 = 0.0;
+};
+
+int rq_gh_create(int64_t n, const int64_t* rowptr, const int32_t* col, const double* A, const double* B,
+                 const rq_symbolic_t* s, double shift, rq_gh_t** out) {
+  return guarded([&] {
+    need(rowptr, "rowptr");
+    need(col, "col");
+    need(A, "A");
+    need(B, "B");
+    need(s, "symbolic");
+    need(out, "out");
+    if (!std::isfinite(shift)) rqb::fail(rqb::errc::config, "shift must be finite and real");
+    if (s->S.n != n) rqb::fail(rqb::errc::dimension, "symbolic / matrix dimension mismatch");
+    auto h = std::make_unique<rq_gh>();
+    h->E = std::make_unique<rqb::GhEngine>(n, rowptr, col, A, B, s->S, shift);
+    const int64_t nnz = rowptr[n];
+    h->normA1 = norm1(n, rowptr, col, std::vector<double>(A, A + nnz));
+    h->normB1 = norm1(n, rowptr, col, std::vector<double>(B, B + nnz));
+    *out = h.release();
+  });
+}
+
+int rq_gh_run(rq_gh_t* h, const rq_gh_opts* opts, double* lam, double* resid, double* vec, rq_gh_info* info) {
+  return guarded([&] {
+    need(h, "handle");
+    need(opts, "opts");
+    need(lam, "lam");
+    need(resid, "resid");
+    std::lock_guard<std::mutex> lock(h->E->fac->mu);
+    rqb::GhOptions o;
+    o.nev = opts->nev;
+    o.m = opts->m;
+    o.tol = opts->tol;
+    o.seed = opts->seed;
+    o.max_restarts = opts->max_restarts > 0 ? opts->max_restarts : 100;
+    o.want_vectors = vec ? 1 : 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    const rqb::GhResult r = rqb::solve_generalized_hermitian_device(*h->E, o, h->normA1, h->normB1);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    const int nout = std::min(o.nev, static_cast<int>(r.lam.size()));
+    for (int i = 0; i < o.nev; ++i) {
+      lam[i] = i < nout ? r.lam[i] : 0.0;
+      resid[i] = i < nout ? r.resid[i] : 1.0;
+    }
+    if (vec && !r.vec.empty()) std::memcpy(vec, r.vec.data(), sizeof(double) * h->E->n * nout);
+    if (info) {
+      info->nconv = r.nconv;
+      info->cycles = r.cycles;
+      info->restarts = r.restarts;
+      info->lanczos_defect = r.lanczos_defect;
+      info->sym_defect = r.sym_defect;
+      info->launches = r.launches;
+      info->t_total_ms = ms;
+    }
+    if (!r.converged)
+      rqb::fail(rqb::errc::solver, "solve_generalized_hermitian: only " + std::to_string(r.nconv) +
+                                       " pairs converged within max_restarts");
+  });
+}
+
+void rq_gh_destroy(rq_gh_t* h) { delete h; }

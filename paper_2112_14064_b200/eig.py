@@ -238,3 +238,74 @@ def solve_quadratic(pencil, s: float, nev: int, m: int = 0, eps: float = 1e-10, 
     """SPEC.md:462 solve_quadratic(pencil, s, nev, m, eps) -> list of EigenPair."""
     op = build_operator(pencil, s, ordering, scaling)
     return op.solve_quadratic(nev, m, eps, seed, **kw), op
+
+
+class GeneralizedHermitianSolver:
+    """solve_generalized_hermitian on the device: A u = lambda B u,
+    A symmetric, B symmetric positive definite on one CSR pattern, real shift s.
+    A - s B is factored once (the multifrontal LU); shift-invert Lanczos with
+    thick restarts runs on the device."""
+
+    def __init__(self, rowptr, col, A, B, s: float, ordering: Ordering):
+        from ._lib import GhInfo  # noqa: F401
+        self.n = int(ordering.n)
+        self.rowptr = np.ascontiguousarray(rowptr, np.int64)
+        self.col = np.ascontiguousarray(col, np.int32)
+        A = np.asarray(A)
+        B = np.asarray(B)
+        for X in (A, B):
+            if np.iscomplexobj(X) and np.any(X.imag != 0):
+                raise RqError(2, "the B200 path solves real symmetric problems only")
+        A, B = np.ascontiguousarray(np.real(A), np.float64), np.ascontiguousarray(np.real(B), np.float64)
+        nnz = int(self.rowptr[-1]) if self.rowptr.size else 0
+        if self.rowptr.size != self.n + 1 or A.size != nnz or B.size != nnz or self.col.size != nnz:
+            raise RqError(7, "solve_generalized_hermitian dimension mismatch")
+        if not np.isfinite(s) or np.iscomplexobj(s):
+            raise RqError(2, "the shift must be real")
+        self.shift = float(s)
+        self.ordering = ordering
+        self._h = C.c_void_p()
+        check(_lib.lib.rq_gh_create(self.n, self.rowptr, self.col, A, B, ordering.handle, self.shift,
+                                    C.byref(self._h)))
+
+    def solve(self, nev: int, m: int = 0, eps: float = 1e-10, seed: int = 0, max_restarts: int = 100,
+              vectors: bool = False):
+        from ._lib import GhInfo, GhOpts
+        lam, res = np.zeros(nev), np.ones(nev)
+        vec = np.zeros(self.n * nev) if vectors else None
+        info = GhInfo()
+        opts = GhOpts(int(nev), int(m), float(eps), int(seed), int(max_restarts))
+        rc = _lib.lib.rq_gh_run(self._h, C.byref(opts), lam, res, _lib.ptr(vec), C.byref(info))
+        self.last_info = {k: getattr(info, k) for k, _ in GhInfo._fields_}
+        check(rc)
+        return [EigenPair(complex(lam[i], 0.0), float(res[i]),
+                          vec[i * self.n:(i + 1) * self.n].copy() if vectors else None) for i in range(nev)]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.lib.rq_gh_destroy(h)
+            self._h = None
+
+
+def solve_generalized_hermitian(A, B, s: float, nev: int, m: int = 0, eps: float = 1e-10,
+                                ordering: Ordering | None = None, seed: int = 0, max_restarts: int = 100,
+                                vectors: bool = False, pencil=None):
+    """SPEC.md:471 solve_generalized_hermitian(A, B, s_real, nev, m, eps, counter): A, B are
+    (rowptr, col, values) on one pattern (or value arrays with `pencil` giving the pattern
+    and the support boxes of the nested-dissection ordering)."""
+    if pencil is not None:
+        rowptr, col = pencil.rowptr, pencil.col
+        Av, Bv = A, B
+        if ordering is None:
+            ordering = Ordering(pencil.n, pencil.box, pencil.elems)
+    else:
+        rowptr, col, Av = A
+        _, _, Bv = B
+    if ordering is None:
+        raise RqError(2, "an Ordering (or a pencil) is required")
+    solver = GeneralizedHermitianSolver(rowptr, col, Av, Bv, s, ordering)
+    pairs = solver.solve(nev, m=m, eps=eps, seed=seed, max_restarts=max_restarts, vectors=vectors)
+    solve_generalized_hermitian.last_info = solver.last_info
+    return pairs
+
