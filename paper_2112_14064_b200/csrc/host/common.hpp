@@ -148,6 +148,12 @@ Symbolic nested_dissection(int64_t n, const int32_t* box, int elems, int leaf);
 // (The per-CSR-entry destination in the front pool — the scatter map — is
 // built on the device: cuda/factor.cu scatter_map_k.)
 
+// Threads of the host-side dense work (m x m Schur products, Ritz vectors):
+// half the processors, at most 8 (the GPU-feeding thread and the driver's own
+// threads keep the rest; spinning OpenMP workers on an oversubscribed host cost
+// far more than they save).
+int host_threads();
+
 inline uint64_t splitmix64(uint64_t& x) {
   uint64_t z = (x += 0x9E3779B97F4A7C15ull);
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

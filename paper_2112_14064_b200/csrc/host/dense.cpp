@@ -5,7 +5,16 @@
 #include <cmath>
 #include <limits>
 
+#include <omp.h>
+
+#include "common.hpp"
+
 namespace rqb {
+
+int host_threads() {
+  static const int t = std::max(1, std::min(8, omp_get_num_procs() / 2));
+  return t;
+}
 
 namespace {
 
@@ -329,6 +338,7 @@ CMat triangular_eigvecs(const CMat& T) {
   for (int j = 0; j < n; ++j)
     for (int i = 0; i <= j; ++i) tnorm = std::max(tnorm, std::abs(T(i, j)));
   const double smin = std::max(tnorm * std::numeric_limits<double>::epsilon(), 1e-300);
+#pragma omp parallel for schedule(dynamic, 8) num_threads(host_threads()) if (n >= 96)
   for (int j = 0; j < n; ++j) {
     Y(j, j) = 1.0;
     const cplx lam = T(j, j);
@@ -397,6 +407,7 @@ int real_basis(const CMat& Z, int p, std::vector<double>& Q) {
     for (int i = 0; i < n; ++i) qn[i] = q[i] / s;
     ++rank;
     // deflate the remaining candidates, downdate their norms
+#pragma omp parallel for schedule(static) num_threads(host_threads()) if (static_cast<int64_t>(n) * nc > 20000)
     for (int j = 0; j < nc; ++j) {
       if (used[j]) continue;
       double* cj = col(j);

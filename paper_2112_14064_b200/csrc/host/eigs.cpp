@@ -536,10 +536,10 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     if (maybe) {
       // Ritz vectors X = V_m [Re y, Im y] (y = Z Y[:, i])
       std::vector<double> Yr(static_cast<size_t>(mm) * 2 * nchk);
-      std::vector<cplx> ycol(mm);
+#pragma omp parallel for schedule(dynamic, 4) num_threads(host_threads()) if (static_cast<int64_t>(nchk) * mm * mm > 1000000)
       for (int c = 0; c < nchk; ++c) {
+        std::vector<cplx> ycol(mm, cplx(0.0));
         const int i = chk[c];
-        std::fill(ycol.begin(), ycol.end(), cplx(0.0));
         for (int t = 0; t <= i; ++t) {  // y = Z[:, 0..i] Y[0..i, i] (Y upper triangular)
           const cplx yt = Y(t, i);
           const cplx* zc = &Z.a[static_cast<size_t>(t) * mm];
@@ -728,6 +728,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     // T_p = Q_p^T H_m Q_p, b_p = beta_m e_m^T Q_p
     // (column-oriented loops: every inner loop is a contiguous axpy / dot)
     std::vector<double> HQ(static_cast<size_t>(mm) * p, 0.0), Tp(static_cast<size_t>(p) * p, 0.0);
+#pragma omp parallel for schedule(static) num_threads(host_threads()) if (static_cast<int64_t>(mm) * mm * p > 1000000)
     for (int c = 0; c < p; ++c) {
       double* hq = HQ.data() + static_cast<size_t>(c) * mm;
       for (int t = 0; t < mm; ++t) {
@@ -737,6 +738,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         for (int i = 0; i < mm; ++i) hq[i] += ht[i] * q;
       }
     }
+#pragma omp parallel for schedule(static) num_threads(host_threads()) if (static_cast<int64_t>(mm) * p * p > 1000000)
     for (int c = 0; c < p; ++c) {
       const double* hq = HQ.data() + static_cast<size_t>(c) * mm;
       for (int i = 0; i < p; ++i) {
@@ -750,9 +752,9 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       // invariance defect ||H Q_p - Q_p T_p|| / ||H|| (exact restart needs ~eps)
       double dmax = 0, hmax = 0;
       for (double x : Hm) hmax = std::max(hmax, std::fabs(x));
-      std::vector<double> rc(mm);
+#pragma omp parallel for schedule(static) reduction(max : dmax) num_threads(host_threads()) if (static_cast<int64_t>(mm) * p * p > 1000000)
       for (int c = 0; c < p; ++c) {
-        std::copy(HQ.begin() + static_cast<size_t>(c) * mm, HQ.begin() + static_cast<size_t>(c + 1) * mm, rc.begin());
+        std::vector<double> rc(HQ.begin() + static_cast<size_t>(c) * mm, HQ.begin() + static_cast<size_t>(c + 1) * mm);
         for (int t = 0; t < p; ++t) {
           const double tc = Tp[t + static_cast<size_t>(c) * p];
           const double* qt = Qp.data() + static_cast<size_t>(t) * mm;
