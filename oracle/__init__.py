@@ -48,7 +48,7 @@ def _bind(lib):
     s("oracle_eig_solve_quadratic", C.c_int, vp, C.c_int, C.c_int, C.c_double, C.c_uint64,
       C.c_int, C.c_int, f64p, f64p, vp, i32p, f64p)
     s("oracle_eig_solve_quadratic_block", C.c_int, vp, C.c_int, C.c_int, C.c_double, C.c_uint64,
-      C.c_int, C.c_int, C.c_int, f64p, f64p, vp, i32p, f64p)
+      C.c_int, C.c_int, C.c_int, C.c_int, f64p, f64p, vp, i32p, f64p)
     s("oracle_eig_destroy", None, vp)
     s("oracle_eig_create2", C.c_int, vp, C.c_int64, i64p, i32p, f64p, f64p, f64p, i32p, C.c_int,
       C.c_int, C.c_double, C.c_int, C.POINTER(vp))
@@ -294,7 +294,7 @@ class Eig:
         return dict(zip(("spmv", "solve", "cgs2", "other"), out.tolist()))
 
     def solve_quadratic(self, nev, m=0, tol=1e-10, seed=0, max_restarts=100, guard=1,
-                        vectors=False, block=1):
+                        vectors=False, block=1, block_min_steps=1):
         """block > 1: the block Krylov-Schur mode, the B200
         build's block algorithm operation for operation."""
         lam = np.zeros(2 * nev)
@@ -303,7 +303,7 @@ class Eig:
         st = np.zeros(4, np.int32)
         led = np.zeros(12)
         rc = self.lib.oracle_eig_solve_quadratic_block(self.h, nev, m, tol, seed, max_restarts, guard,
-                                                       int(block), lam, res,
+                                                       int(block), int(block_min_steps), lam, res,
                                                        None if vec is None else vec.ctypes.data_as(vp), st, led)
         self.stats = {"cycles": int(st[0]), "guard_passes": int(st[1]), "nconv": int(st[2]),
                       "ok": bool(st[3])}

@@ -711,37 +711,78 @@ void arnoldi_steps(Operator& op, std::vector<std::vector<cd>>& V, DM& H, int k, 
 // R_b -= V h_b); then the block's own CGS2 (member b against V[kt, kt+b)) and
 // B-normalisation into V[kt+b]. H(i, kc+b) accumulates the projections,
 // H(kt+b, kc+b) = ||R_b||_B.
+// Step plan (the B200 build's, eigs.cpp plan_steps): width bs while the cycle
+// has room for at least min_steps such steps, else width 1 (banded block
+// Arnoldi: S applied to the oldest frontier vector); a step of width wd
+// applies S to V[kc, kc+wd), projects against V[0, kc+bs) and appends
+// V[kc+bs, kc+bs+wd); the cycle ends at m accounted vectors.
 void arnoldi_block_steps(Operator& op, std::vector<std::vector<cd>>& V, DM& H, int k, int m, int bs,
-                         std::vector<std::vector<cd>>& R, std::vector<cd>& w, Ledger* L) {
+                         std::vector<std::vector<cd>>& R, std::vector<cd>& w, Ledger* L, int min_steps) {
   const int64_t n2 = 2 * op.n;
-  for (int kc = k; kc + bs <= m; kc += bs) {
+  const int wd0 = (m - k) >= bs * min_steps ? bs : 1;
+  for (int kc = k; kc < m; kc += wd0) {
+    const int wd = std::min(wd0, m - kc);
     const int kt = kc + bs;
-    for (int b = 0; b < bs; ++b) op.apply(V[kc + b].data(), R[b].data(), L);
+    for (int b = 0; b < wd; ++b) op.apply(V[kc + b].data(), R[b].data(), L);
+    if (wd == 1) {  // a width-1 step: the single-vector CGS2 step
+      for (int pass = 0; pass < 2; ++pass) {
+        op.bvec(R[0].data(), w.data(), L);
+        std::vector<cd> h(kt);
+        dots(V, kt, w.data(), n2, h.data(), L);
+        axpys(V, kt, h.data(), R[0].data(), n2, -1.0, L);
+        for (int i = 0; i < kt; ++i) H(i, kc) += h[i];
+      }
+      op.bvec(R[0].data(), w.data(), L);
+      const double beta = std::sqrt(std::max(0.0, dot(R[0].data(), w.data(), n2, L).real()));
+      H(kt, kc) = beta;
+      for (int64_t i = 0; i < n2; ++i) V[kt][i] = R[0][i] / beta;
+      continue;
+    }
+    // BCGS2: two passes of {project the block against V[0, kt), B-orthonormalise
+    // it member by member (CGS2 against the earlier members)}; pass 2 works on
+    // the normalised pass-1 block Q1: S V_blk = V (H1 + H2 R1) + Q2 R2 R1
+    std::vector<std::vector<cd>> Hp(2, std::vector<cd>(static_cast<size_t>(kt) * wd, 0.0));
+    std::vector<std::vector<cd>> Rq(2, std::vector<cd>(static_cast<size_t>(wd) * wd, 0.0));
     for (int pass = 0; pass < 2; ++pass) {
-      std::vector<std::vector<cd>> h(bs, std::vector<cd>(kt));
-      for (int b = 0; b < bs; ++b) {
-        op.bvec(R[b].data(), w.data(), L);
+      std::vector<std::vector<cd>>& X = R;  // pass 0: R; pass 1: Q1 (copied back into R)
+      std::vector<std::vector<cd>> h(wd, std::vector<cd>(kt));
+      for (int b = 0; b < wd; ++b) {
+        op.bvec(X[b].data(), w.data(), L);
         dots(V, kt, w.data(), n2, h[b].data(), L);
       }
-      for (int b = 0; b < bs; ++b) {
-        axpys(V, kt, h[b].data(), R[b].data(), n2, -1.0, L);
-        for (int i = 0; i < kt; ++i) H(i, kc + b) += h[b][i];
+      for (int b = 0; b < wd; ++b) {
+        axpys(V, kt, h[b].data(), X[b].data(), n2, -1.0, L);
+        for (int i = 0; i < kt; ++i) Hp[pass][i + static_cast<size_t>(b) * kt] = h[b][i];
       }
-    }
-    for (int b = 0; b < bs; ++b) {
-      for (int pass = 0; pass < 2 && b > 0; ++pass) {
-        op.bvec(R[b].data(), w.data(), L);
-        std::vector<cd> h(b);
-        for (int i = 0; i < b; ++i) h[i] = dot(V[kt + i].data(), w.data(), n2, L);
-        for (int i = 0; i < b; ++i) {
-          axpy(-h[i], V[kt + i].data(), R[b].data(), n2, L);
-          H(kt + i, kc + b) += h[i];
+      for (int b = 0; b < wd; ++b) {
+        for (int sub = 0; sub < 2 && b > 0; ++sub) {
+          op.bvec(X[b].data(), w.data(), L);
+          std::vector<cd> g(b);
+          for (int i = 0; i < b; ++i) g[i] = dot(V[kt + i].data(), w.data(), n2, L);
+          for (int i = 0; i < b; ++i) {
+            axpy(-g[i], V[kt + i].data(), X[b].data(), n2, L);
+            Rq[pass][i + static_cast<size_t>(b) * wd] += g[i];
+          }
         }
+        op.bvec(X[b].data(), w.data(), L);
+        const double beta = std::sqrt(std::max(0.0, dot(X[b].data(), w.data(), n2, L).real()));
+        Rq[pass][b + static_cast<size_t>(b) * wd] = beta;
+        for (int64_t i = 0; i < n2; ++i) V[kt + b][i] = X[b][i] / beta;
       }
-      op.bvec(R[b].data(), w.data(), L);
-      const double beta = std::sqrt(std::max(0.0, dot(R[b].data(), w.data(), n2, L).real()));
-      H(kt + b, kc + b) = beta;
-      for (int64_t i = 0; i < n2; ++i) V[kt + b][i] = R[b][i] / beta;
+      if (pass == 0)
+        for (int b = 0; b < wd; ++b) R[b] = V[kt + b];
+    }
+    for (int b = 0; b < wd; ++b) {
+      for (int i = 0; i < kt; ++i) {
+        cd v = Hp[0][i + static_cast<size_t>(b) * kt];
+        for (int t = 0; t <= b; ++t) v += Hp[1][i + static_cast<size_t>(t) * kt] * Rq[0][t + static_cast<size_t>(b) * wd];
+        H(i, kc + b) += v;
+      }
+      for (int i = 0; i <= b; ++i) {
+        cd v = 0.0;
+        for (int t = i; t <= b; ++t) v += Rq[1][i + static_cast<size_t>(t) * wd] * Rq[0][t + static_cast<size_t>(b) * wd];
+        H(kt + i, kc + b) = v;
+      }
     }
   }
 }
@@ -766,7 +807,7 @@ void arnoldi_run(Operator& op, const cd* v1, int m, std::vector<std::vector<cd>>
 // blocks: member b from splitmix64(seed + b * golden) (b = 0: the
 // single-vector start), CGS2 against everything before it.
 EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, int max_restarts,
-                       int guard_on, Ledger* L, int bs) {
+                       int guard_on, Ledger* L, int bs, int min_steps = 1) {
   const int64_t n = op.n, n2 = 2 * n;
   const double sig = op.s.real();
   const int keep_t = nev + std::min(20, m - nev - 1);
@@ -798,11 +839,11 @@ EigOut solve_quadratic(Operator& op, int nev, int m, double tol, uint64_t seed, 
   while (pass_cycles < max_restarts) {
     ++cycles;
     ++pass_cycles;
-    const int mm = k + bs * ((m - k) / bs), m0 = mm - bs;
+    const int mm = m, m0 = mm - bs;
     if (bs == 1)
       arnoldi_steps(op, V, H, k, m, r, w, L);
     else
-      arnoldi_block_steps(op, V, H, k, m, bs, R, w, L);
+      arnoldi_block_steps(op, V, H, k, m, bs, R, w, L, min_steps);
     DM T(mm), Z;
     for (int j = 0; j < mm; ++j)
       for (int i = 0; i < mm; ++i) T(i, j) = H(i, j);
@@ -1282,14 +1323,15 @@ void oracle_eig_ledger(void* h, double* out) {
 void oracle_eig_ledger_reset(void* h) { static_cast<OracleEig*>(h)->L = oracle::Ledger{}; }
 
 int oracle_eig_solve_quadratic_block(void* h, int nev, int m, double tol, uint64_t seed, int max_restarts,
-                                     int guard, int block, double* lam_c, double* res, double* vec_c,
+                                     int guard, int block, int min_steps, double* lam_c, double* res, double* vec_c,
                                      int32_t* stats, double* ledger) {
   return guarded([&] {
     auto* E = static_cast<OracleEig*>(h);
     const int bs = std::max(1, block);
     const int mk = m > 0 ? m : 2 * nev + 1;
     if (bs > 1 && (mk < nev + bs || mk + bs > 2 * E->op->n)) throw oracle::OracleError{2, "oracle: m too small for the block"};
-    const oracle::EigOut o = oracle::solve_quadratic(*E->op, nev, mk, tol, seed, max_restarts, guard, &E->L, bs);
+    const oracle::EigOut o = oracle::solve_quadratic(*E->op, nev, mk, tol, seed, max_restarts, guard, &E->L, bs,
+                                                     min_steps > 0 ? min_steps : 1);
     for (int i = 0; i < nev && i < static_cast<int>(o.lam.size()); ++i) {
       lam_c[2 * i] = o.lam[i].real() * E->varsigma;  // lambda = varsigma gamma
       lam_c[2 * i + 1] = o.lam[i].imag() * E->varsigma;
@@ -1307,7 +1349,7 @@ int oracle_eig_solve_quadratic_block(void* h, int nev, int m, double tol, uint64
 int oracle_eig_solve_quadratic(void* h, int nev, int m, double tol, uint64_t seed, int max_restarts,
                                int guard, double* lam_c, double* res, double* vec_c, int32_t* stats,
                                double* ledger) {
-  return oracle_eig_solve_quadratic_block(h, nev, m, tol, seed, max_restarts, guard, 1, lam_c, res, vec_c, stats,
+  return oracle_eig_solve_quadratic_block(h, nev, m, tol, seed, max_restarts, guard, 1, 1, lam_c, res, vec_c, stats,
                                           ledger);
 }
 

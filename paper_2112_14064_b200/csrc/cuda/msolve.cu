@@ -140,6 +140,121 @@ __device__ __forceinline__ int wait_pub(const MArgs& A, int f, int need) {
   return p;
 }
 
+// Pivot-block solution entries are published by value: the sweep resets y and
+// x to an all-ones bit pattern (a NaN no FP64 operation produces) and an item
+// polls the 64 x KR entries of the block it needs directly (relaxed loads of
+// relaxed stores, 8-byte single-copy atomic), so the chain of pivot blocks
+// has no fence + counter round trip.
+constexpr long long kUnsetBits = -1LL;
+__device__ __forceinline__ void st_rlx(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_rlx(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// warp 0: wait until the nv (<= 64 KR) entries at src are all published, copy
+// them to dst (shared memory). false if the watchdog fired.
+template <int KR>
+__device__ __forceinline__ bool poll_vals(const MArgs& A, const double* src, int nv, double* dst, int lane) {
+  constexpr int kPer = 2 * KR;  // 64 KR / 32 lanes
+  unsigned long long t0 = 0;
+  for (;;) {
+    double v[kPer];
+    bool ok = true;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int i = lane + 32 * u;
+      v[u] = i < nv ? ld_rlx(src + i) : 0.0;
+      ok = ok && (i >= nv || __double_as_longlong(v[u]) != kUnsetBits);
+    }
+    if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+      for (int u = 0; u < kPer; ++u)
+        if (lane + 32 * u < nv) dst[lane + 32 * u] = v[u];
+      return true;
+    }
+    int st = 0;
+    if (lane == 0) {
+      __nanosleep(20);
+      st = mstalled(A, t0);
+    }
+    if (__shfl_sync(0xffffffffu, st, 0)) return false;
+  }
+}
+
+// acc[j] += sum over the pivot-block columns [c_lo, c_hi) of this front of
+// A[row, c] v[c][j], consuming one 64-column block at a time in chain order
+// (ascending for the forward sweep, descending for the backward one): the
+// block's matrix columns are loaded into registers before its entries are
+// polled (the next block's while the current one is consumed), warp 0 polls
+// and stages the block's published entries, and each block's partial is added
+// to acc in block order (bitwise deterministic whatever the timing).
+template <int KR, bool kAsc>
+__device__ __forceinline__ void consume_blocks(const MArgs& A, const double* vals, const double* lp, int64_t ld,
+                                               bool rowok, int c_lo, int c_hi, double* stg, int tid, int grp,
+                                               double (&acc)[KR]) {
+  if (c_lo >= c_hi) return;
+  const int lane = tid & 31, warp = tid >> 5;
+  auto bounds = [&](int i, int& b0, int& b1) {  // i-th block in chain order
+    if (kAsc) {
+      b0 = c_lo + i * kMB;
+      b1 = min(c_hi, b0 + kMB);
+    } else {
+      const int top0 = c_lo + ((c_hi - 1 - c_lo) / kMB) * kMB;  // first (highest) block start
+      b0 = top0 - i * kMB;
+      b1 = min(c_hi, b0 + kMB);
+    }
+  };
+  const int nblk = (c_hi - c_lo + kMB - 1) / kMB;
+  constexpr int kU = kMB / 4;
+  double cur[kU], nxt[kU];
+  int b0, b1;
+  bounds(0, b0, b1);
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int c = b0 + grp + 4 * u;
+    cur[u] = (rowok && c < b1) ? lp[(int64_t)c * ld] : 0.0;
+  }
+  for (int i = 0; i < nblk; ++i) {
+    bounds(i, b0, b1);
+    if (i + 1 < nblk) {
+      int n0, n1;
+      bounds(i + 1, n0, n1);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int c = n0 + grp + 4 * u;
+        nxt[u] = (rowok && c < n1) ? lp[(int64_t)c * ld] : 0.0;
+      }
+    }
+    if (warp == 0) poll_vals<KR>(A, vals + (int64_t)b0 * KR, (b1 - b0) * KR, stg, lane);
+    __syncthreads();
+    double t[KR];
+#pragma unroll
+    for (int j = 0; j < KR; ++j) t[j] = 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int c = grp + 4 * u;
+      if (c < b1 - b0) {
+        const double2* xp = reinterpret_cast<const double2*>(stg + c * KR);
+#pragma unroll
+        for (int q = 0; q < KR / 2; ++q) {
+          const double2 x = xp[q];
+          t[2 * q] += cur[u] * x.x;
+          t[2 * q + 1] += cur[u] * x.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KR; ++j) acc[j] += t[j];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kU; ++u) cur[u] = nxt[u];
+  }
+}
+
 // acc[j] += sum over this thread's column class (c = cb + grp mod 4) of
 // A[row, c] xs[c][j]: eight column loads in flight per iteration, the staged
 // right-hand sides read as double2 broadcasts (every lane of a warp reads the
@@ -351,25 +466,9 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mfwd_sweep(MArgs A) {
       double acc[KR];
 #pragma unroll
       for (int j = 0; j < KR; ++j) acc[j] = 0.0;
-      int done = 0;
-      while (done < ncol) {
-        if (tid == 0) {
-          const int need = min(I.npb, done / kMB + 1);
-          const int p = wait_pub(A, I.front, need);
-          avail_s = p < 0 ? ncol : min(ncol, p * kMB);
-        }
-        __syncthreads();
-        const int avail = avail_s;
-        for (int base = done; base < avail; base += kMStage) {
-          const int hi = min(avail, base + kMStage);
-          for (int idx = tid; idx < (hi - base) * KR; idx += kMT)
-            S.stg[idx] = __ldcg(&A.y[(int64_t)(I.start + base) * KR + idx]);
-          __syncthreads();
-          mstream<KR>(g + I.r0 + row, ld, row < nr, S.stg - base * KR, base, hi, grp, acc);
-          __syncthreads();
-        }
-        done = avail;
-      }
+      __syncthreads();  // w and D staged
+      consume_blocks<KR, true>(A, A.y + (int64_t)I.start * KR, g + I.r0 + row, ld, row < nr, 0, ncol, S.stg, tid,
+                               grp, acc);
       put_part<KR>(S.part, grp, row, acc);
       __syncthreads();
       if (blk >= 0) {
@@ -380,7 +479,7 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mfwd_sweep(MArgs A) {
         if (row < nr)
 #pragma unroll
           for (int t = 0; t < KR / 4; ++t)
-            A.y[(int64_t)(I.start + I.r0 + row) * KR + jq * (KR / 4) + t] = out[t];
+            st_rlx(&A.y[(int64_t)(I.start + I.r0 + row) * KR + jq * (KR / 4) + t], out[t]);
       } else {
         for (int idx = tid; idx < nr * KR; idx += kMT) {
           const int r = idx / KR, j = idx % KR;
@@ -390,12 +489,8 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mfwd_sweep(MArgs A) {
         }
       }
     }
-    __syncthreads();  // every row written before thread 0 publishes
+    __syncthreads();  // every row written before thread 0 releases the parent
     if (tid == 0) {
-      if (I.blk >= 0) {
-        __threadfence();
-        red_rel(&A.pub[I.front], 1);
-      }
       if (I.parent >= 0) {
         int old;
         asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(A.deps + I.parent) : "memory");
@@ -412,7 +507,7 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mfwd_sweep(MArgs A) {
 // backward sweep
 template <int KR>
 __device__ __forceinline__ void store_xm(const MArgs& A, int gi, int j, double v) {
-  A.xnew[(int64_t)gi * KR + j] = v;
+  st_rlx(&A.xnew[(int64_t)gi * KR + j], v);
   if (j < A.nrhs) {
     const int64_t o = A.perm[gi];
     const double sv = A.scale * v;
@@ -496,39 +591,9 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
         mstream<KR>(g + r0 + row, ld, row < nr, S.stg - base * KR, base, hi, grp, acc);
         __syncthreads();
       }
-      // later pivot blocks of this front, published last first
-      int done_hi = np;
-      while (done_hi > lo) {
-        if (tid == 0) {
-          const int need = I.npb - (done_hi - 1) / kMB;  // blocks from the end down to the one holding done_hi-1
-          const int p = wait_pub(A, I.front, need);
-          avail_s = p < 0 ? lo : max(lo, (I.npb - p) * kMB);
-        }
-        __syncthreads();
-        const int avail_lo = avail_s;
-        // one partial per 64-column pivot block, added to acc from the last
-        // block down: the summation order does not depend on how publication
-        // rounds grouped the blocks (bitwise deterministic solves)
-        for (int top = done_hi; top > avail_lo;) {
-          const int bot = max(avail_lo, (max(0, top - kMStage) + kMB - 1) / kMB * kMB);
-          for (int idx = tid; idx < (top - bot) * KR; idx += kMT)
-            S.stg[idx] = __ldcg(&A.xnew[(int64_t)(I.start + bot) * KR + idx]);
-          __syncthreads();
-          for (int bh = top; bh > bot;) {
-            const int bl = max(bot, (bh - 1) / kMB * kMB);
-            double t[KR];
-#pragma unroll
-            for (int j = 0; j < KR; ++j) t[j] = 0.0;
-            mstream<KR>(g + r0 + row, ld, row < nr, S.stg - bot * KR, bl, bh, grp, t);
-#pragma unroll
-            for (int j = 0; j < KR; ++j) acc[j] += t[j];
-            bh = bl;
-          }
-          __syncthreads();
-          top = bot;
-        }
-        done_hi = avail_lo;
-      }
+      // later pivot blocks of this front, published last first, consumed by value
+      consume_blocks<KR, false>(A, A.xnew + (int64_t)I.start * KR, g + r0 + row, ld, row < nr, lo, np, S.stg, tid,
+                                grp, acc);
       put_part<KR>(S.part, grp, row, acc);
       __syncthreads();
       sub_parts<KR>(S.w, S.part, nr, tid);
@@ -540,10 +605,6 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
         for (int t = 0; t < KR / 4; ++t) store_xm<KR>(A, I.start + r0 + row, jq * (KR / 4) + t, out[t]);
     }
     __syncthreads();
-    if (tid == 0 && I.blk != kMWhole) {
-      __threadfence();
-      red_rel(&A.pub[I.front], 1);
-    }
     if (I.blk == 0 || I.blk == kMWhole) {  // the front is complete: its effective children are ready
       if (tid == 0) __threadfence();
       __syncthreads();
@@ -706,11 +767,11 @@ static void msolve_prepare(FactorEngine& fe) {
   P->d_cb.alloc(sizeof(double) * kMaxRhs * std::max<int64_t>(1, S.cbvec));
   int nsm = 148, occ = 1;
   RQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device));
-  smem_at_least(mfwd_sweep<4, 3>, msmem_bytes<4>());
-  smem_at_least(mbwd_sweep<4, 3>, msmem_bytes<4>());
+  smem_at_least(mfwd_sweep<4, 2>, msmem_bytes<4>());
+  smem_at_least(mbwd_sweep<4, 2>, msmem_bytes<4>());
   smem_at_least(mfwd_sweep<8, 2>, msmem_bytes<8>());
   smem_at_least(mbwd_sweep<8, 2>, msmem_bytes<8>());
-  RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mfwd_sweep<4, 3>, kMT, msmem_bytes<4>()));
+  RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mfwd_sweep<4, 2>, kMT, msmem_bytes<4>()));
   P->grid4 = nsm * std::max(1, occ);
   RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mfwd_sweep<8, 2>, kMT, msmem_bytes<8>()));
   P->grid8 = nsm * std::max(1, occ);
@@ -757,6 +818,11 @@ void rqb_msolve_enqueue(FactorEngine& fe, const double* b, int64_t ldb, int nrhs
   MSolvePlan& P = *fe.mplan;
   cudaStream_t st = fe.stream;
   RQB_CUDA(cudaMemcpyAsync(P.d_state.p, P.d_state0.p, P.d_state0.bytes, cudaMemcpyDeviceToDevice, st));
+  {  // published-by-value entries start unset (all-ones bit pattern)
+    const size_t kr = nrhs <= 4 ? 4 : 8;
+    RQB_CUDA(cudaMemsetAsync(P.d_y.p, 0xff, sizeof(double) * kr * fe.n, st));
+    RQB_CUDA(cudaMemsetAsync(P.d_x.p, 0xff, sizeof(double) * kr * fe.n, st));
+  }
   MArgs A{};
   A.ech = P.d_ech.as<int32_t>();
   A.gsrc = fe.d_gsrc.as<int4>();
@@ -780,7 +846,7 @@ void rqb_msolve_enqueue(FactorEngine& fe, const double* b, int64_t ldb, int nrhs
   A.nrhs = nrhs;
   A.stall = P.d_stall.as<int>();
   if (nrhs <= 4)
-    msolve_launch<4, 3>(fe, A, P.grid4);
+    msolve_launch<4, 2>(fe, A, P.grid4);
   else
     msolve_launch<8, 2>(fe, A, P.grid8);
   fe.launches_solve = 2;

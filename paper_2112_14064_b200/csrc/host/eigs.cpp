@@ -142,7 +142,9 @@ struct EigWorkspace {
   int m = -1, bs = 1;
   int64_t n2 = 0;
   DeviceBuffer dV, dV2, dBV, dBV2, dR, dW, dHa, dHb, dBeta, dQ, dX, dRes;
+  DeviceBuffer dHc, dHd, dBeta2;  // block mode: second intra-block sub-passes, R2 diagonal
   Pinned ha, hb, betas;
+  Pinned hc, hd, betas2;
   Pinned hv, hq, hy;  // staging of the host -> device copies (start vectors, restart Q, Ritz Y)
   // cycle graph per (start index, basis buffer) and the kernels it launches
   std::map<std::pair<int, const double*>, std::pair<cudaGraphExec_t, int64_t>> graphs;
@@ -150,8 +152,11 @@ struct EigWorkspace {
   // (m + bs) x (m + bs) column-major
   EigWorkspace(int m_, int64_t n2_, int bs_)
       : m(m_), bs(bs_), n2(n2_), ha(static_cast<size_t>(m_ + bs_) * (m_ + bs_)),
-        hb(static_cast<size_t>(m_ + bs_) * (m_ + bs_)), betas(m_ + bs_), hv(static_cast<size_t>(n2_)),
-        hq(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)), hy(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)) {
+        hb(static_cast<size_t>(m_ + bs_) * (m_ + bs_)), betas(m_ + bs_),
+        hc(bs_ > 1 ? static_cast<size_t>(m_ + bs_) * (m_ + bs_) : 1),
+        hd(bs_ > 1 ? static_cast<size_t>(m_ + bs_) * (m_ + bs_) : 1), betas2(m_ + bs_),
+        hv(static_cast<size_t>(n2_)), hq(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)),
+        hy(static_cast<size_t>(m_ + 1) * (2 * m_ + 2)) {
     dV.alloc(sizeof(double) * (m + bs) * n2);
     dV2.alloc(sizeof(double) * (m + bs) * n2);
     dBV.alloc(sizeof(double) * (m + bs) * n2);
@@ -161,6 +166,11 @@ struct EigWorkspace {
     dHa.alloc(sizeof(double) * (m + bs) * (m + bs));
     dHb.alloc(sizeof(double) * (m + bs) * (m + bs));
     dBeta.alloc(sizeof(double) * (m + bs));
+    if (bs > 1) {
+      dHc.alloc(sizeof(double) * (m + bs) * (m + bs));
+      dHd.alloc(sizeof(double) * (m + bs) * (m + bs));
+      dBeta2.alloc(sizeof(double) * (m + bs));
+    }
     dQ.alloc(sizeof(double) * (m + 1) * (2 * m + 2));
     dX.alloc(sizeof(double) * n2 * 2 * (m + 1));
     dRes.alloc(sizeof(double) * 4 * (m + 1));
@@ -186,6 +196,21 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   if (m < nev + bs) fail(errc::config, "block Krylov-Schur needs m >= nev + block");
   if (!(o.tol > 0)) fail(errc::config, "tolerance must be positive");
   const int LDH = m + bs;  // leading dimension of H (rows: m accounted + the frontier block)
+  // Step plan of a cycle from k accounted vectors (block mode): steps of width
+  // bs while the cycle has room for at least block_min_steps of them, else
+  // width 1 (the banded "sliding window" form of block Arnoldi: S applied to
+  // the oldest frontier vector, projected against everything incl. the rest of
+  // the frontier). Every step of width w applies S to V[j, j+w), projects
+  // against V[0, j+bs) and appends V[j+bs, j+bs+w); the cycle always ends at
+  // m accounted vectors with a frontier of bs.
+  const int min_steps = std::getenv("RQB_BLOCK_MINSTEPS") ? std::max(1, std::atoi(std::getenv("RQB_BLOCK_MINSTEPS")))
+                                                          : o.block_min_steps;
+  auto plan_steps = [&](int k0) {
+    std::vector<std::pair<int, int>> pl;
+    const int w = (bs > 1 && (m - k0) >= bs * min_steps) ? bs : 1;
+    for (int j = k0; j < m; j += w) pl.emplace_back(j, std::min(w, m - j));
+    return pl;
+  };
   const int keep_target = nev + std::min(20, m - nev - 1);
   const double sig = op.sigma;  // scaled shift
   const double vs = op.varsigma;
@@ -210,7 +235,8 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   EigWorkspace& W = *wsp;
   if (bs > 1) op.prepare_block(m + bs, bs);  // sweep plan + block workspaces before any graph capture
   DeviceBuffer &dV = W.dV, &dV2 = W.dV2, &dBV = W.dBV, &dBV2 = W.dBV2, &dR = W.dR, &dW = W.dW, &dHa = W.dHa, &dHb = W.dHb,
-               &dBeta = W.dBeta, &dQ = W.dQ, &dX = W.dX, &dRes = W.dRes;
+               &dBeta = W.dBeta, &dQ = W.dQ, &dX = W.dX, &dRes = W.dRes, &dHc = W.dHc, &dHd = W.dHd,
+               &dBeta2 = W.dBeta2;
   double* V = dV.as<double>();
   double* V2 = dV2.as<double>();
   double* BV = dBV.as<double>();
@@ -289,15 +315,17 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     // Gram-Schmidt (CGS2 against its earlier members) and B-normalisation into
     // V[kt + j]. H column kc + j: rows [0, kt + j) projections, row kt + j the
     // B-norm. The cycle ends at mm = the last kc with kc + bs > m.
+    const std::vector<std::pair<int, int>> plan = plan_steps(k);
     auto enqueue_steps = [&](bool prof, bool skip_first) {
-      for (int j = k; j + bs <= m; j += bs) {
+      for (const auto& stp : plan) {
+        const int j = stp.first, w = stp.second;
         double* vj = V + static_cast<int64_t>(j) * n2;
         if (prof) cuda_check(cudaEventRecord(e_a, st), "ev");
         if (!(skip_first && j == k)) {
-          if (bs == 1)
+          if (w == 1)
             op.apply(vj, r);
           else
-            op.apply_block(vj, bs, r);
+            op.apply_block(vj, w, r);
         }
         if (prof) {
           cuda_check(cudaEventRecord(e_b, st), "ev");
@@ -310,7 +338,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         double* hA = dHa.as<double>() + static_cast<int64_t>(j) * LDH;
         double* hB = dHb.as<double>() + static_cast<int64_t>(j) * LDH;
         const int kt = j + bs;
-        if (bs == 1) {
+        if (w == 1) {
           // CGS2 with the stored B-images: h = (BV)^T r, r -= V h (twice),
           // then ||r||_B, v_{j+1} = r / beta and B v_{j+1} from one M-product
           op.gemv_t(BV, kt, r, hA);
@@ -320,25 +348,36 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
           op.bnorm_normalize_b(r, dBeta.as<double>() + j, V + static_cast<int64_t>(kt) * n2,
                                BV + static_cast<int64_t>(kt) * n2);
         } else {
-          op.gemm_t(BV, kt, r, bs, hA, LDH);
-          op.gemm_n(V, kt, hA, LDH, r, bs);
-          op.gemm_t(BV, kt, r, bs, hB, LDH);
-          op.gemm_n(V, kt, hB, LDH, r, bs);
-          const double* BVn = BV + static_cast<int64_t>(kt) * n2;
-          const double* Vn = V + static_cast<int64_t>(kt) * n2;
-          for (int b = 0; b < bs; ++b) {
-            double* rb = r + static_cast<int64_t>(b) * n2;
-            if (b > 0) {
-              double* ha_b = hA + kt + static_cast<int64_t>(b) * LDH;
-              double* hb_b = hB + kt + static_cast<int64_t>(b) * LDH;
-              op.gemv_t(BVn, b, rb, ha_b);
-              op.gemv_n(Vn, b, ha_b, rb, nullptr);
-              op.gemv_t(BVn, b, rb, hb_b);
-              op.gemv_n(Vn, b, hb_b, rb, nullptr);
+          // BCGS2: two passes of {project the block against V[0, kt) (every
+          // basis vector read once for the w members), B-orthonormalise it
+          // member by member (CGS2 against the earlier members)}; the second
+          // pass works on the normalised first-pass block in place, so a
+          // block whose members cancelled heavily against V or each other is
+          // re-orthogonalised at full scale (S V_blk = V (H1 + H2 R1) + Q R2 R1)
+          double* BVn = BV + static_cast<int64_t>(kt) * n2;
+          double* Vn = V + static_cast<int64_t>(kt) * n2;
+          double* hC = dHc.as<double>() + static_cast<int64_t>(j) * LDH;
+          double* hD = dHd.as<double>() + static_cast<int64_t>(j) * LDH;
+          auto intra = [&](double* src, double* h1, double* h2, double* beta) {
+            for (int b = 0; b < w; ++b) {
+              double* rb = src + static_cast<int64_t>(b) * n2;
+              if (b > 0) {
+                double* h1b = h1 + kt + static_cast<int64_t>(b) * LDH;
+                double* h2b = h2 + kt + static_cast<int64_t>(b) * LDH;
+                op.gemv_t(BVn, b, rb, h1b);
+                op.gemv_n(Vn, b, h1b, rb, nullptr);
+                op.gemv_t(BVn, b, rb, h2b);
+                op.gemv_n(Vn, b, h2b, rb, nullptr);
+              }
+              op.bnorm_normalize_b(rb, beta + b, Vn + static_cast<int64_t>(b) * n2, BVn + static_cast<int64_t>(b) * n2);
             }
-            op.bnorm_normalize_b(rb, dBeta.as<double>() + j + b, V + static_cast<int64_t>(kt + b) * n2,
-                                 BV + static_cast<int64_t>(kt + b) * n2);
-          }
+          };
+          op.gemm_t(BV, kt, r, w, hA, LDH);
+          op.gemm_n(V, kt, hA, LDH, r, w);
+          intra(r, hA, hC, dBeta.as<double>() + j);
+          op.gemm_t(BV, kt, Vn, w, hB, LDH);
+          op.gemm_n(V, kt, hB, LDH, Vn, w);
+          intra(Vn, hB, hD, dBeta2.as<double>() + j);
         }
         if (prof) {
           cuda_check(cudaEventRecord(e_b, st), "ev");
@@ -373,30 +412,32 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       op.launches += it->second.second;  // the same count on every call, cached graph or not
       res.graph_launches += 1;
     }
-    const int mm = k + bs * ((m - k) / bs);  // columns of H after this cycle
-    for (int j = k; j + bs <= m; j += bs) {
-      // per step (bs = 1): apply + 2 x (B-product, j+1 dots, j+1 axpys) + B-norm;
-      // per block step: bs applies, 2 x (bs B-products, 2 kt bs dots/axpys),
-      // the block's own CGS2 (2 x (B-product, 2b dots/axpys) for member b > 0)
-      // and bs B-norms (B-product + dot) — the oracle's block mode, op for op
+    const int mm = m;  // columns of H after this cycle
+    for (const auto& stp : plan) {
+      // per step of width 1: apply + 2 x (B-product, kt dots, kt axpys) + B-norm;
+      // per block step of width w: w applies, 2 x (w B-products, 2 kt w
+      // dots/axpys), the block's own CGS2 (2 x (B-product, 2b dots/axpys) for
+      // member b > 0) and w B-norms (B-product + dot) — the oracle's block
+      // mode, op for op
+      const int j = stp.first, w = stp.second;
       const int kt = j + bs;
-      for (int b = 0; b < bs; ++b) charge_apply(L, op);
-      if (bs == 1) {
+      for (int b = 0; b < w; ++b) charge_apply(L, op);
+      if (w == 1) {
         for (int pass = 0; pass < 3; ++pass) charge_bproduct(L, op);
         charge_vv2n(L, op, 4 * kt + 1);
       } else {
-        for (int pass = 0; pass < 2; ++pass) {
-          for (int b = 0; b < bs; ++b) charge_bproduct(L, op);
-          charge_vv2n(L, op, 2 * static_cast<int64_t>(kt) * bs);
-        }
-        for (int b = 0; b < bs; ++b) {
-          if (b > 0)
-            for (int pass = 0; pass < 2; ++pass) {
-              charge_bproduct(L, op);
-              charge_vv2n(L, op, 2 * b);
-            }
-          charge_bproduct(L, op);
-          charge_vv2n(L, op, 1);
+        for (int pass = 0; pass < 2; ++pass) {  // BCGS2: projection + intra-block CGS2 + B-norms, twice
+          for (int b = 0; b < w; ++b) charge_bproduct(L, op);
+          charge_vv2n(L, op, 2 * static_cast<int64_t>(kt) * w);
+          for (int b = 0; b < w; ++b) {
+            if (b > 0)
+              for (int sub = 0; sub < 2; ++sub) {
+                charge_bproduct(L, op);
+                charge_vv2n(L, op, 2 * b);
+              }
+            charge_bproduct(L, op);
+            charge_vv2n(L, op, 1);
+          }
         }
       }
     }
@@ -404,6 +445,12 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     cuda_check(cudaMemcpyAsync(hb.data(), dHb.p, sizeof(double) * LDH * LDH, cudaMemcpyDeviceToHost, st), "D2H H");
     cuda_check(cudaMemcpyAsync(betas.data(), dBeta.p, sizeof(double) * LDH, cudaMemcpyDeviceToHost, st),
                "D2H beta");
+    if (bs > 1) {
+      cuda_check(cudaMemcpyAsync(W.hc.data(), dHc.p, sizeof(double) * LDH * LDH, cudaMemcpyDeviceToHost, st), "D2H");
+      cuda_check(cudaMemcpyAsync(W.hd.data(), dHd.p, sizeof(double) * LDH * LDH, cudaMemcpyDeviceToHost, st), "D2H");
+      cuda_check(cudaMemcpyAsync(W.betas2.data(), dBeta2.p, sizeof(double) * LDH, cudaMemcpyDeviceToHost, st),
+                 "D2H beta2");
+    }
     cuda_check(cudaEventRecord(e_h, st), "ev");
     // Speculatively apply the operator to the frontier block V[mm, mm+bs):
     // unless the cycle ends in a deflated restart (fresh vectors), it is the
@@ -421,11 +468,38 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       cuda_check(cudaEventSynchronize(e_h), "sync");
       t_sync += ms_since(ts0);  // host blocked on the cycle's Arnoldi steps
     }
-    for (int j = k; j < mm; ++j) {
-      const int jb = j - (j - k) % bs, kt = jb + bs, b = j - jb;  // block start, its kt, member
-      for (int i = 0; i < kt + b; ++i)
-        Hc(i, j) = ha[i + static_cast<size_t>(j) * LDH] + hb[i + static_cast<size_t>(j) * LDH];
-      Hc(kt + b, j) = betas[j];
+    for (const auto& stp : plan) {
+      const int j0 = stp.first, w = stp.second, kt = j0 + bs;  // step start, width, projection range
+      if (w == 1) {
+        for (int i = 0; i < kt; ++i)
+          Hc(i, j0) = ha[i + static_cast<size_t>(j0) * LDH] + hb[i + static_cast<size_t>(j0) * LDH];
+        Hc(kt, j0) = betas[j0];
+        continue;
+      }
+      // BCGS2: H[:kt, c] = H1 + H2 R1, H[kt.., c] = R2 R1 (R1, R2 upper triangular w x w)
+      auto at = [&](const Pinned& P, int i, int c) { return P.p[i + static_cast<size_t>(c) * LDH]; };
+      std::vector<double> R1(static_cast<size_t>(w) * w, 0.0), R2(R1.size(), 0.0);
+      for (int b = 0; b < w; ++b) {
+        for (int t = 0; t < b; ++t) {
+          R1[t + static_cast<size_t>(b) * w] = at(W.ha, kt + t, j0 + b) + at(W.hc, kt + t, j0 + b);
+          R2[t + static_cast<size_t>(b) * w] = at(W.hb, kt + t, j0 + b) + at(W.hd, kt + t, j0 + b);
+        }
+        R1[b + static_cast<size_t>(b) * w] = betas[j0 + b];
+        R2[b + static_cast<size_t>(b) * w] = W.betas2[j0 + b];
+      }
+      for (int b = 0; b < w; ++b) {
+        const int c = j0 + b;
+        for (int i = 0; i < kt; ++i) {
+          double v = at(W.ha, i, c);
+          for (int t = 0; t <= b; ++t) v += at(W.hb, i, j0 + t) * R1[t + static_cast<size_t>(b) * w];
+          Hc(i, c) = v;
+        }
+        for (int i = 0; i <= b; ++i) {
+          double v = 0.0;
+          for (int t = i; t <= b; ++t) v += R2[i + static_cast<size_t>(t) * w] * R1[t + static_cast<size_t>(b) * w];
+          Hc(kt + i, c) = v;
+        }
+      }
     }
     // ---- Ritz extraction (H_mm is upper Hessenberg for bs = 1, banded with
     // bs subdiagonals for a block; after a restart it is a full matrix) ----
