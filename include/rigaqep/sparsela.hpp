@@ -32,6 +32,8 @@ struct Ordering {
   std::vector<std::int32_t> perm;  // perm[new] = old (free DOFs)
   std::string method = "geometric-nested-dissection";
   std::shared_ptr<rq_symbolic_t> sym;
+  std::vector<std::int32_t> box;  // support boxes (n x 4) the ordering was built from
+  int elems = 1, leaf = 64;
   long n() const { return static_cast<long>(perm.size()); }
 };
 
@@ -44,6 +46,9 @@ inline Ordering ordering_from_boxes(std::int64_t n, const std::vector<std::int32
   o.sym.reset(s, rq_symbolic_destroy);
   o.perm.resize(n);
   o.method = method;
+  o.box = box;
+  o.elems = elems;
+  o.leaf = leaf;
   check(rq_symbolic_perm(s, o.perm.data()));
   return o;
 }
@@ -109,6 +114,7 @@ inline Ordering natural_order(long n) {
 struct Factorization {
   std::shared_ptr<rq_factor_t> f;
   long n = 0;
+  bool complex_values = false;  // factored as the real-equivalent 2n system
   std::int64_t nnz_l = 0, nnz_u = 0;
   double flops = 0;
   double fb_macs = 0;
@@ -122,12 +128,29 @@ inline std::vector<double> real_values(const SparseMatrix& a) {
 }
 
 /// lu_factorize: fa += the structural multiply-add count.
+/// A complex A (a complex shift) is factored on the GPU as its
+/// real-equivalent 2n system over the ordering's boxes repeated per (Re, Im)
+/// pair (rq_factor_create_complex); the ledger charges the complex problem's
+/// structural count of the given ordering, as the reference path would.
 inline Factorization lu_factorize(const SparseMatrix& A, const Ordering& ord, CostLedger* ledger) {
   if (A.n != ord.n()) fail(errc::dimension, "lu_factorize: matrix and ordering sizes differ");
-  const std::vector<double> v = real_values(A);
   rq_factor_t* f = nullptr;
-  b200::check(rq_factor_create(ord.sym.get(), A.n, A.rowptr.data(), A.col.data(), v.data(), &f));
+  const bool cplx = !A.is_real();
+  if (cplx) {
+    if (ord.box.size() != 4 * static_cast<std::size_t>(A.n)) fail(errc::config, "ordering without support boxes");
+    std::vector<std::int32_t> box2(8 * static_cast<std::size_t>(A.n));
+    for (long k = 0; k < A.n; ++k)
+      for (int t = 0; t < 4; ++t) box2[8 * k + t] = box2[8 * k + 4 + t] = ord.box[4 * k + t];
+    const Ordering o2 = b200::ordering_from_boxes(2 * A.n, box2, ord.elems, ord.leaf, ord.method.c_str());
+    std::vector<double> re(A.val.size()), im(A.val.size());
+    for (std::size_t k = 0; k < re.size(); ++k) re[k] = A.val[k].real(), im[k] = A.val[k].imag();
+    b200::check(rq_factor_create_complex(o2.sym.get(), A.n, A.rowptr.data(), A.col.data(), re.data(), im.data(), &f));
+  } else {
+    const std::vector<double> v = real_values(A);
+    b200::check(rq_factor_create(ord.sym.get(), A.n, A.rowptr.data(), A.col.data(), v.data(), &f));
+  }
   Factorization F;
+  F.complex_values = cplx;
   F.f.reset(f, rq_factor_destroy);
   F.n = A.n;
   rq_symbolic_stats st{};
@@ -144,6 +167,13 @@ inline Factorization lu_factorize(const SparseMatrix& A, const Ordering& ord, Co
 inline std::vector<cdouble> solve_factored(const Factorization& F, const std::vector<cdouble>& rhs,
                                            CostLedger* ledger) {
   if (static_cast<long>(rhs.size()) != F.n) fail(errc::dimension, "solve_factored dimension mismatch");
+  if (F.complex_values) {  // cdouble[n] is the interleaved real-equivalent vector
+    std::vector<cdouble> out(F.n);
+    b200::check(rq_factor_solve_complex(F.f.get(), reinterpret_cast<const double*>(rhs.data()),
+                                        reinterpret_cast<double*>(out.data()), 1));
+    if (ledger) ledger->add_fb(static_cast<std::uint64_t>(F.fb_macs));
+    return out;
+  }
   bool cplx = false;
   for (const cdouble& z : rhs) cplx = cplx || z.imag() != 0.0;
   const int nr = cplx ? 2 : 1;

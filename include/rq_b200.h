@@ -162,6 +162,20 @@ int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs);
 /* Same with an explicit sweep width: block = right-hand sides per pass over
  * the factors (1: the single-vector sweeps, 2..8: multi-RHS sweeps). */
 int rq_factor_solve_ex(rq_factor_t* f, const double* b, double* x, int nrhs, int block);
+/* Complex A = Are + i Aim on the pattern (rowptr, col) (Q(s)
+ * over complex scalars, e.g. a complex shift): factored on the
+ * GPU as its real-equivalent 2n system (unknowns 2k = Re x_k, 2k+1 = Im x_k,
+ * i.e. the cdouble layout; 2 x 2 blocks [[Re a, -Im a], [Im a, Re a]]) by the
+ * same multifrontal LU with threshold pivoting over the 2n unknowns. s2 is the
+ * ordering of the 2n unknowns (rq_nd_order over the support boxes repeated
+ * per unknown pair). Aim may be NULL (real). */
+int rq_factor_create_complex(const rq_symbolic_t* s2, int64_t n, const int64_t* rowptr, const int32_t* col,
+                             const double* are, const double* aim, rq_factor_t** out);
+int rq_factor_refactor_complex(rq_factor_t* f, const double* are, const double* aim, const int64_t* rowptr,
+                               const int32_t* col);
+/* x = A^{-1} b for a complex factorization; b, x: nrhs interleaved {re, im}
+ * vectors of n (cdouble[n] each). RQ_E_CONFIG on a real factorization. */
+int rq_factor_solve_complex(rq_factor_t* f, const double* b, double* x, int nrhs);
 /* Copy front f back: dense ld*nf column-major block holding L\U and the
  * Schur complement, ld = *ld_out; ipiv[npiv] local swap sequence. */
 int rq_factor_front_export(const rq_factor_t* f, int64_t front, double* dense, int32_t* ipiv,

@@ -135,6 +135,9 @@ _sig("rq_factor_refactor", C.c_int, vp, f64p)
 _sig("rq_factor_get_info", C.c_int, vp, C.POINTER(FactorInfo))
 _sig("rq_factor_solve", C.c_int, vp, f64p, f64p, C.c_int)
 _sig("rq_factor_solve_ex", C.c_int, vp, f64p, f64p, C.c_int, C.c_int)
+_sig("rq_factor_create_complex", C.c_int, vp, C.c_int64, i64p, i32p, f64p, vp, C.POINTER(vp))
+_sig("rq_factor_refactor_complex", C.c_int, vp, f64p, vp, i64p, i32p)
+_sig("rq_factor_solve_complex", C.c_int, vp, f64p, f64p, C.c_int)
 _sig("rq_factor_front_export", C.c_int, vp, C.c_int64, vp, vp, C.POINTER(C.c_int64))
 _sig("rq_factor_profile", C.c_int, vp, f64p, i64p, f64p)
 _sig("rq_factor_dag_profile", C.c_int, vp, f64p)
@@ -180,7 +183,8 @@ EXPORTS = [
     "rq_pencil_supports", "rq_pencil_destroy", "rq_space_dims", "rq_space_boundary_mask",
     "rq_nd_order", "rq_symbolic_stats_get", "rq_symbolic_perm", "rq_symbolic_fronts",
     "rq_symbolic_front_rows", "rq_symbolic_destroy", "rq_factor_create", "rq_factor_refactor",
-    "rq_factor_get_info", "rq_factor_solve", "rq_factor_solve_ex", "rq_factor_front_export", "rq_factor_profile", "rq_factor_dag_profile", "rq_factor_bench_updcb",
+    "rq_factor_get_info", "rq_factor_solve", "rq_factor_solve_ex", "rq_factor_create_complex",
+    "rq_factor_refactor_complex", "rq_factor_solve_complex", "rq_factor_front_export", "rq_factor_profile", "rq_factor_dag_profile", "rq_factor_bench_updcb",
     "rq_factor_destroy",
     "rq_operator_create", "rq_operator_create_pencil", "rq_mm_write", "rq_mm_write_vector", "rq_mm_read",
     "rq_mm_dims", "rq_mm_csr", "rq_mm_destroy", "rq_pencil_write_mm", "rq_eigenpairs_json", "rq_operator_varsigma", "rq_operator_apply", "rq_operator_b_inner",

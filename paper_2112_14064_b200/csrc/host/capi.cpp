@@ -34,6 +34,7 @@ struct rq_factor {
   std::unique_ptr<rqb::FactorEngine> owned;
   rqb::FactorEngine* fe = nullptr;
   rqb::DeviceBuffer d_b, d_x;
+  int64_t n_complex = -1;  // complex factorization: size of the complex system (the engine holds 2n)
 };
 struct rq_operator {
   std::unique_ptr<rqb::OperatorEngine> op;
@@ -268,6 +269,73 @@ int rq_factor_create(const rq_symbolic_t* s, int64_t n, const int64_t* rowptr, c
   });
 }
 
+namespace {
+// real-equivalent 2n x 2n system of the complex A: unknowns 2k = Re x_k,
+// 2k+1 = Im x_k (the cdouble layout), block (i, j) = [[ar, -ai], [ai, ar]]
+void complex_equivalent(int64_t n, const int64_t* rowptr, const int32_t* col, const double* are, const double* aim,
+                        std::vector<int64_t>& rp2, std::vector<int32_t>& col2, std::vector<double>& v2) {
+  const int64_t nnz = rowptr[n];
+  if (2 * n > INT32_MAX) rqb::fail(rqb::errc::dimension, "complex system too large for int32 columns");
+  rp2.assign(2 * n + 1, 0);
+  col2.resize(4 * nnz);
+  v2.resize(4 * nnz);
+  int64_t q = 0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int part = 0; part < 2; ++part) {
+      rp2[2 * i + part] = q;
+      for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+        const int32_t j = col[k];
+        const double ar = are[k], ai = aim ? aim[k] : 0.0;
+        col2[q] = 2 * j;
+        v2[q++] = part == 0 ? ar : ai;
+        col2[q] = 2 * j + 1;
+        v2[q++] = part == 0 ? -ai : ar;
+      }
+    }
+  rp2[2 * n] = q;
+}
+}  // namespace
+
+int rq_factor_create_complex(const rq_symbolic_t* s2, int64_t n, const int64_t* rowptr, const int32_t* col,
+                             const double* are, const double* aim, rq_factor_t** out) {
+  return guarded([&] {
+    need(s2, "symbolic");
+    need(rowptr, "rowptr");
+    need(col, "col");
+    need(are, "are");
+    need(out, "out");
+    if (2 * n != s2->S.n) rqb::fail(rqb::errc::dimension, "the ordering must cover the 2n real-equivalent unknowns");
+    std::vector<int64_t> rp2;
+    std::vector<int32_t> col2;
+    std::vector<double> v2;
+    complex_equivalent(n, rowptr, col, are, aim, rp2, col2, v2);
+    auto f = std::make_unique<rq_factor>();
+    f->owned = std::make_unique<rqb::FactorEngine>(s2->S, 2 * n, rp2.data(), col2.data(), v2.data());
+    f->fe = f->owned.get();
+    f->n_complex = n;
+    f->fe->factor();
+    *out = f.release();
+  });
+}
+
+int rq_factor_refactor_complex(rq_factor_t* f, const double* are, const double* aim, const int64_t* rowptr,
+                               const int32_t* col) {
+  return guarded([&] {
+    need(f, "factor");
+    need(are, "are");
+    need(rowptr, "rowptr");
+    need(col, "col");
+    if (f->n_complex < 0) rqb::fail(rqb::errc::config, "not a complex factorization");
+    std::vector<int64_t> rp2;
+    std::vector<int32_t> col2;
+    std::vector<double> v2;
+    complex_equivalent(f->n_complex, rowptr, col, are, aim, rp2, col2, v2);
+    std::lock_guard<std::mutex> lock(f->fe->mu);
+    f->fe->set_values(v2.data());
+    f->fe->factor();
+  });
+}
+
 int rq_factor_refactor(rq_factor_t* f, const double* aval) {
   return guarded([&] {
     need(f, "factor");
@@ -318,6 +386,16 @@ int rq_factor_solve_ex(rq_factor_t* f, const double* b, double* x, int nrhs, int
     fe.check_sweeps();
     rqb::rqb_msolve_check(fe);
   });
+}
+
+int rq_factor_solve_complex(rq_factor_t* f, const double* b, double* x, int nrhs) {
+  const int rc = guarded([&] {
+    need(f, "factor");
+    if (f->n_complex < 0) rqb::fail(rqb::errc::config, "not a complex factorization");
+  });
+  if (rc != 0) return rc;
+  // interleaved {re, im} vectors are exactly the real-equivalent unknowns
+  return rq_factor_solve_ex(f, b, x, nrhs, nrhs > 1 ? 8 : 1);
 }
 
 int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs) {

@@ -27,6 +27,7 @@ class Ordering:
         self._h = C.c_void_p()
         check(_lib.lib.rq_nd_order(int(n), box, int(elems), int(leaf), C.byref(self._h)))
         self.n, self.elems, self.leaf = int(n), int(elems), int(leaf)
+        self.box = box.reshape(-1, 4)
         st = SymbolicStats()
         check(_lib.lib.rq_symbolic_stats_get(self._h, C.byref(st)))
         self.stats = {k: getattr(st, k) for k, _ in SymbolicStats._fields_}
@@ -64,13 +65,16 @@ def nested_dissection_order(pencil, leaf: int = 64) -> Ordering:
 
 
 class Factorization:
-    """Device-resident multifrontal LU of A (immutable; shareable read-only)."""
+    """Device-resident multifrontal LU of A (immutable; shareable read-only).
+    A complex A (any nonzero imaginary part, e.g. Q(s) at a complex shift) is
+    factored as its real-equivalent 2n system (rq_factor_create_complex): the
+    2n unknowns (Re x_k, Im x_k) get their own nested-dissection ordering over
+    the support boxes repeated per pair; solves take and return complex vectors."""
 
     def __init__(self, ordering: Ordering, rowptr, col, values):
         values = np.asarray(values)
-        if np.iscomplexobj(values):
-            if np.any(values.imag != 0):
-                raise RqError(2, "the B200 path factors real matrices only")
+        self.is_complex = bool(np.iscomplexobj(values) and np.any(values.imag != 0))
+        if np.iscomplexobj(values) and not self.is_complex:
             values = values.real
         self.ordering = ordering
         self.n = ordering.n
@@ -79,6 +83,14 @@ class Factorization:
         if self.rowptr.size != self.n + 1:
             raise RqError(7, "rowptr size does not match the ordering")
         self._h = C.c_void_p()
+        if self.is_complex:
+            self.ordering2 = Ordering(2 * self.n, np.repeat(ordering.box, 2, axis=0), ordering.elems,
+                                      ordering.leaf)
+            check(_lib.lib.rq_factor_create_complex(self.ordering2.handle, self.n, self.rowptr, self.col,
+                                                    np.ascontiguousarray(values.real, np.float64),
+                                                    _lib.ptr(np.ascontiguousarray(values.imag, np.float64)),
+                                                    C.byref(self._h)))
+            return
         check(_lib.lib.rq_factor_create(ordering.handle, self.n, self.rowptr, self.col,
                                         np.ascontiguousarray(values, np.float64),
                                         C.byref(self._h)))
@@ -95,6 +107,17 @@ class Factorization:
         """x = A^{-1} b; b of shape (n,) or (n, nrhs). Several right-hand sides
         pass through the multi-RHS sweeps, `block` (1..8, default 8) vectors per
         pass over the factors; block=1 forces the single-vector sweeps."""
+        if self.is_complex:
+            bc = np.asarray(b, dtype=np.complex128)
+            if bc.shape[0] != self.n:
+                raise RqError(7, "solve_factored dimension mismatch")
+            bb = np.ascontiguousarray(bc.reshape(self.n, -1).T)  # nrhs x n complex = interleaved {re, im}
+            x = np.zeros_like(bb)
+            check(_lib.lib.rq_factor_solve_complex(self._h, bb.view(np.float64).reshape(-1),
+                                                   x.view(np.float64).reshape(-1), bb.shape[0]))
+            return x.T.reshape(bc.shape)
+        if np.iscomplexobj(b):  # real factorization, complex right-hand side: two real solves
+            return self.solve(np.real(b), block) + 1j * self.solve(np.imag(b), block)
         b = np.asarray(b, dtype=np.float64)
         if b.shape[0] != self.n:
             raise RqError(7, "solve_factored dimension mismatch")

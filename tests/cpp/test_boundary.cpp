@@ -155,6 +155,19 @@ int main() {
     CHECK(std::abs(Ax[0] - 1.0) <= 1e-14 && std::abs(Ax[1] - 2.0) <= 1e-14 && std::abs(Ax[2] - 3.0) <= 1e-14);
     CHECK(L3.fa_ops() == 1 && L3.fa_macs() == 4 + 1 && L3.fb_ops() == 1);  // (3-1)^2 + (3-2)^2 MACs
   }
+  {  // complex A (complex shift): Q(-0.5 + 0.3i) of the cfg1 pencil, real-equivalent GPU LU
+    const rq::cdouble sc(-0.5, 0.3);
+    rq::SparseMatrix Q = P.K;
+    for (std::size_t k = 0; k < Q.val.size(); ++k) Q.val[k] = P.K.val[k] + sc * P.C.val[k] + sc * sc * P.M.val[k];
+    const rq::Factorization Fc = rq::lu_factorize(Q, *P.ordering, nullptr);
+    std::vector<rq::cdouble> bc(n), Qx(n);
+    for (long i = 0; i < n; ++i) bc[i] = rq::cdouble(std::sin(0.3 * i), std::cos(0.7 * i));
+    const auto xc = rq::solve_factored(Fc, bc, nullptr);
+    rq::spmv(Q, xc, Qx, nullptr);
+    double rmax = 0, xmax = 0;
+    for (long i = 0; i < n; ++i) rmax = std::max(rmax, std::abs(Qx[i] - bc[i])), xmax = std::max(xmax, std::abs(xc[i]));
+    CHECK(Fc.complex_values && rmax <= 1e-10 * std::max(1.0, xmax));
+  }
   // ---- error behaviour: reference error categories through the boundary
   bool threw = false;
   try {
