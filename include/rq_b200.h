@@ -72,6 +72,14 @@ typedef struct {
 } rq_space_desc;
 
 int rq_pencil_assemble(const rq_space_desc* desc, rq_pencil_t** out);
+/* The paper's vibroacoustic pencil (assemble_acoustic, SPEC.md:225-232;
+ * PAPER.md:165-200, Fig. 8 material rho = 1, c = 340, alpha = 5e4, beta =
+ * 200): H(div) space of `degree` on the unit square (rIGA levels as above),
+ * u.n = 0 on the rigid edges, absorbing edges (bit mask: left 1, right 2,
+ * bottom 4, top 8) free; K = int rho c^2 div u div v + int_GA alpha (u.n)(v.n),
+ * C = int_GA beta (u.n)(v.n), M = int rho u.v; all real. Host assembly. */
+int rq_pencil_assemble_acoustic(int degree, int elems, int levels, double rho, double c, double alpha, double beta,
+                                int absorbing_edges, rq_pencil_t** out);
 /* The same pencil, bit for bit, assembled on the current CUDA device
  * (pattern, per-element Gauss quadrature, colour-ordered
  * gather; no atomics). resident = 1 keeps K, C, M in device memory only

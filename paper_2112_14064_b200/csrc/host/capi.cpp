@@ -110,6 +110,17 @@ int rq_pencil_assemble(const rq_space_desc* desc, rq_pencil_t** out) {
   });
 }
 
+int rq_pencil_assemble_acoustic(int degree, int elems, int levels, double rho, double c, double alpha, double beta,
+                                int absorbing_edges, rq_pencil_t** out) {
+  return guarded([&] {
+    need(out, "out");
+    const rqb::VectorSpace vs = rqb::build_space(rqb::SpaceKind::div, degree, elems, levels);
+    auto p = std::make_unique<rq_pencil>();
+    p->P = rqb::assemble_acoustic(vs, rho, c, alpha, beta, absorbing_edges);
+    *out = p.release();
+  });
+}
+
 int rq_pencil_assemble_device(const rq_space_desc* desc, int resident, rq_pencil_t** out, double* ms) {
   return guarded([&] {
     need(out, "out");

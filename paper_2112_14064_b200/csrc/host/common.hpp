@@ -84,12 +84,19 @@ struct Pencil {
   int elems = 0;
 };
 
-Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta);
+// mask: constrained full DOF ids (sorted; default boundary_mask(vs));
+// full_to_free_out: the free numbering used.
+Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta, const std::vector<int64_t>* mask = nullptr,
+                       std::vector<int64_t>* full_to_free_out = nullptr);
+// The paper's vibroacoustic pencil: rigid
+// edges constrained, absorbing edges (bit mask: left 1, right 2, bottom 4, top
+// 8) carry the impedance terms alpha / beta.
+Pencil assemble_acoustic(const VectorSpace& vs, double rho, double c, double alpha, double beta, int absorbing);
 
 // Pieces shared by the host assembler and the device one (cuda/assembly.cu).
 // Free numbering: full_to_free[g] = free id or -1 (constrained), free_to_full.
 void free_numbering(const VectorSpace& vs, std::vector<int64_t>* full_to_free,
-                    std::vector<int64_t>* free_to_full);
+                    std::vector<int64_t>* free_to_full, const std::vector<int64_t>* mask = nullptr);
 // Inclusive element support box {x0, x1, y0, y1} of every free DOF.
 std::vector<int32_t> support_boxes(const VectorSpace& vs, const std::vector<int64_t>& free_to_full);
 

@@ -256,8 +256,8 @@ void quad_tables(const VectorSpace& vs, QuadTable tab[2][2]) {
 }
 
 void free_numbering(const VectorSpace& vs, std::vector<int64_t>* full_to_free,
-                    std::vector<int64_t>* free_to_full) {
-  const std::vector<int64_t> mask = boundary_mask(vs);
+                    std::vector<int64_t>* free_to_full, const std::vector<int64_t>* mask_in) {
+  const std::vector<int64_t> mask = mask_in ? *mask_in : boundary_mask(vs);
   const int64_t N = vs.N();
   full_to_free->assign(N, -1);
   free_to_full->clear();
@@ -291,13 +291,14 @@ std::vector<int32_t> support_boxes(const VectorSpace& vs, const std::vector<int6
   return box;
 }
 
-Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta) {
+Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta, const std::vector<int64_t>* mask,
+                       std::vector<int64_t>* full_to_free_out) {
   if (vs.degree > kMaxP) fail(errc::domain, "degree too large for assembly tables");
   Pencil P;
   P.elems = vs.elems;
   P.n_full = vs.N();
   std::vector<int64_t> full_to_free;
-  free_numbering(vs, &full_to_free, &P.free_to_full);
+  free_numbering(vs, &full_to_free, &P.free_to_full, mask);
   P.n = static_cast<int64_t>(P.free_to_full.size());
   const Tensor2* comp[2] = {&vs.cx, &vs.cy};
   const int64_t base[2] = {0, vs.Nx()};
@@ -442,6 +443,88 @@ Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta) {
   }
   P.C.resize(nnz);
   for (int64_t k = 0; k < nnz; ++k) P.C[k] = alpha * P.M[k] + beta * P.K[k];
+  if (full_to_free_out) *full_to_free_out = std::move(full_to_free);
+  return P;
+}
+
+// The paper's vibroacoustic pencil (SPEC.md:225-232,
+// assemble_acoustic): u . n = 0 on the rigid edges only (the absorbing ones
+// stay free), K = int rho c^2 div u div v + int_{Gamma_A} alpha (u.n)(v.n),
+// C = int_{Gamma_A} beta (u.n)(v.n), M = int rho u.v, all real. On an edge
+// only the normal component's bases of the last (or first) index across the
+// edge are nonzero (open knot vectors: value 1 there), so the edge integral is
+// the 1-D mass matrix of the tangential univariate space, integrated with p+1
+// Gauss points per element.
+Pencil assemble_acoustic(const VectorSpace& vs, double rho, double c, double alpha, double beta, int absorbing) {
+  if (vs.kind != SpaceKind::div) fail(errc::domain, "the acoustic problem lives in H(div)");
+  if (!(rho > 0 && c > 0 && alpha > 0 && beta > 0)) fail(errc::domain, "acoustic material: rho, c, alpha, beta > 0");
+  if (absorbing < 0 || absorbing > 15) fail(errc::domain, "absorbing edges: bit mask of left 1, right 2, bottom 4, top 8");
+  // rigid edges: the normal component's boundary DOFs
+  std::vector<int64_t> mask;
+  const int64_t nx1 = vs.cx.nx(), ny1 = vs.cx.ny(), nx2 = vs.cy.nx(), ny2 = vs.cy.ny(), Nx = vs.Nx();
+  for (int64_t j = 0; j < ny1; ++j) {
+    if (!(absorbing & 1)) mask.push_back(j * nx1);
+    if (!(absorbing & 2)) mask.push_back(j * nx1 + nx1 - 1);
+  }
+  for (int64_t i = 0; i < nx2; ++i) {
+    if (!(absorbing & 4)) mask.push_back(Nx + i);
+    if (!(absorbing & 8)) mask.push_back(Nx + (ny2 - 1) * nx2 + i);
+  }
+  std::sort(mask.begin(), mask.end());
+  std::vector<int64_t> full_to_free;
+  Pencil P = assemble_pencil(vs, 0.0, 0.0, &mask, &full_to_free);
+  const int64_t nnz = P.rowptr[P.n];
+  const double rc2 = rho * c * c;
+  for (int64_t k = 0; k < nnz; ++k) {
+    P.K[k] = rc2 * (P.K[k] - P.M[k]);  // the BASELINE K carries div-div + u.v
+    P.M[k] = rho * P.M[k];
+    P.C[k] = 0.0;
+  }
+  auto add = [&](int64_t fr, int64_t fs, double v) {
+    const int32_t* cb = P.col.data() + P.rowptr[fr];
+    const int32_t* ce = P.col.data() + P.rowptr[fr + 1];
+    const int32_t* it = std::lower_bound(cb, ce, static_cast<int32_t>(fs));
+    if (it == ce || *it != fs) fail(errc::assembly, "pattern misses an edge pair");
+    const int64_t pos = it - P.col.data();
+    P.K[pos] += alpha * v;
+    P.C[pos] += beta * v;
+  };
+  const int nq = vs.degree + 1;
+  std::vector<double> gx(nq), gw(nq);
+  gauss_legendre(nq, gx.data(), gw.data());
+  for (int edge = 0; edge < 4; ++edge) {
+    if (!(absorbing & (1 << edge))) continue;
+    // vertical edges (left/right): x-component, tangential univariate cx.sy;
+    // horizontal edges (bottom/top): y-component, tangential cy.sx
+    const bool vert = edge < 2;
+    const Tensor2& T = vert ? vs.cx : vs.cy;
+    const Univariate& tu = vert ? T.sy : T.sx;
+    const int64_t nxt = T.nx();
+    const int64_t across = (edge == 0 || edge == 2) ? 0 : (vert ? T.nx() - 1 : T.ny() - 1);
+    const int64_t base = vert ? 0 : Nx;
+    auto dof = [&](int64_t t) {  // full index of the normal-component basis (t along the edge)
+      return base + (vert ? t * nxt + across : across * nxt + t);
+    };
+    const int p = tu.degree;
+    std::vector<double> val(p + 1), der(p + 1);
+    for (int e = 0; e < tu.elems; ++e) {
+      const int span = tu.elem_span[e];
+      const double u0 = tu.knots[span], u1 = tu.knots[span + 1], h = u1 - u0;
+      for (int q = 0; q < nq; ++q) {
+        const double u = u0 + 0.5 * (gx[q] + 1.0) * h, w = 0.5 * h * gw[q];
+        basis_eval(tu.knots, p, span, u, val.data(), der.data());
+        for (int a = 0; a <= p; ++a) {
+          const int64_t fa = full_to_free[dof(span - p + a)];
+          if (fa < 0) continue;
+          for (int b = 0; b <= p; ++b) {
+            const int64_t fb = full_to_free[dof(span - p + b)];
+            if (fb < 0) continue;
+            add(fa, fb, w * val[a] * val[b]);
+          }
+        }
+      }
+    }
+  }
   return P;
 }
 

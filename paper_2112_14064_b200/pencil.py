@@ -164,6 +164,39 @@ def assemble(kind: int, degree: int, elems: int, levels: int = 0, alpha: float =
                            box.reshape(-1, 4), f2f, alpha, beta)
 
 
+ACOUSTIC_EDGES = {"left": 1, "right": 2, "bottom": 4, "top": 8}
+
+
+def assemble_acoustic(degree: int, elems: int, levels: int = 0, rho: float = 1.0, c: float = 340.0,
+                      alpha: float = 5e4, beta: float = 200.0, absorbing=("top",)) -> QuadraticPencil:
+    """The paper's vibroacoustic pencil (SPEC.md:225 assemble_acoustic; PAPER.md:165-200,
+    the Fig. 8 cavity: unit square, one absorbing wall, air rho = 1, c = 340, impedance
+    alpha = 5e4, beta = 200): K = rho c^2 div-div + alpha edge term, C = beta edge term,
+    M = rho mass; rigid edges constrained, absorbing ones free. Real pencil."""
+    mask = 0
+    for e in absorbing:
+        mask |= ACOUSTIC_EDGES[e]
+    h = C.c_void_p()
+    check(_lib.lib.rq_pencil_assemble_acoustic(int(degree), int(elems), int(levels), float(rho), float(c),
+                                               float(alpha), float(beta), int(mask), C.byref(h)))
+    try:
+        nf, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        check(_lib.lib.rq_pencil_dims(h, C.byref(nf), C.byref(n), C.byref(nnz)))
+        rowptr = np.zeros(n.value + 1, np.int64)
+        col = np.zeros(nnz.value, np.int32)
+        K = np.zeros(nnz.value)
+        Cm = np.zeros(nnz.value)
+        M = np.zeros(nnz.value)
+        check(_lib.lib.rq_pencil_csr(h, rowptr, col, K, Cm, M))
+        box = np.zeros(4 * n.value, np.int32)
+        f2f = np.zeros(n.value, np.int64)
+        check(_lib.lib.rq_pencil_supports(h, box, f2f))
+    finally:
+        _lib.lib.rq_pencil_destroy(h)
+    return QuadraticPencil(DIV, degree, elems, levels, nf.value, n.value, rowptr, col, K, Cm, M,
+                           box.reshape(-1, 4), f2f, 0.0, 0.0)
+
+
 def baseline_config(name: str, device: bool = False, resident: bool = False) -> QuadraticPencil:
     """The BASELINE.json configurations by short name."""
     table = {
