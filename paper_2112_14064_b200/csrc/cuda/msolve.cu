@@ -39,6 +39,9 @@ constexpr int kMT = 256;        // threads per CTA
 constexpr int kMStage = 256;    // staged solution rows per round
 constexpr int kMWholeNf = 512;  // whole-front items: nf bound (their y / x live in shared memory)
 constexpr int kMWhole = -2;     // MItem::blk of a whole-front item
+constexpr int kMPart = -3;      // MItem::blk of a backward partial item (contribution-column chunk of a block)
+constexpr int kMCbChunk = 256;  // contribution columns per backward partial item
+constexpr int kMSlot = kMB * 8; // doubles per partial-sum slot (64 rows x up to 8 right-hand sides)
 constexpr int kDL = kMB + 1;    // leading dimension of the diagonal tile in shared memory
 
 struct MItem {
@@ -55,7 +58,11 @@ struct MArgs {
   int* deps;   // per front: unfinished predecessor items (fwd) / fronts (bwd)
   int* queue;
   int* qctl;   // {head, tail}
+  int* done;   // items finished (termination: items kept by a CTA never pass through the queue)
   int* pub;    // per front: pivot blocks published
+  int* pdone;  // backward: per front, partial items finished
+  const int32_t* npart;  // backward: per front, partial items (0: blocks stream their contribution columns)
+  double* bpart;         // backward partial sums, kMSlot doubles per (front, block, chunk)
   const int32_t* fbase;
   const int32_t* fcnt;
   const int32_t* ech;  // backward: effective children (nearest descendants with pivots)
@@ -78,6 +85,7 @@ struct MArgs {
   double* xl;  // stride ldx
   int nrhs;
   int* stall;
+  unsigned long long* trace;  // development trace (RQB_MSOLVE_TRACE): per item start, end
 };
 
 __device__ __forceinline__ unsigned long long mtime() {
@@ -108,8 +116,10 @@ __device__ __forceinline__ bool mstalled(const MArgs& A, unsigned long long& t0)
   return false;
 }
 
-__device__ __forceinline__ void mpush(const MArgs& A, int f) {
-  const int i0 = A.fbase[f], n = A.fcnt[f];
+// push the items of front f from its `from`-th on (the earlier ones are kept
+// by the calling CTA: depth-first, the data it just produced is still in L2)
+__device__ __forceinline__ void mpush(const MArgs& A, int f, int from = 0) {
+  const int i0 = A.fbase[f] + from, n = A.fcnt[f] - from;
   if (n <= 0) return;
   const int slot = atomicAdd(&A.qctl[1], n);
   for (int i = 0; i < n; ++i) atomicExch(&A.queue[slot + i], i0 + i);
@@ -121,6 +131,7 @@ __device__ __forceinline__ int mpop(const MArgs& A) {
   int t;
   unsigned long long t0 = 0;
   while ((t = ld_acq(&A.queue[h])) < 0) {
+    if (ld_acq(A.done) >= A.nitems) return -1;
     __nanosleep(32);
     if (mstalled(A, t0)) return -1;
   }
@@ -210,7 +221,11 @@ __device__ __forceinline__ void consume_blocks(const MArgs& A, const double* val
   };
   const int nblk = (c_hi - c_lo + kMB - 1) / kMB;
   constexpr int kU = kMB / 4;
-  double cur[kU], nxt[kU];
+  // KR = 8 (128 registers): the next block's columns are loaded while the
+  // current one is consumed; KR = 4 (80 registers, 3 CTAs / SM): each block's
+  // columns are issued right before its entries are polled
+  constexpr bool kNext = KR == 8;
+  double cur[kU], nxt[kNext ? kU : 1];
   int b0, b1;
   bounds(0, b0, b1);
 #pragma unroll
@@ -220,13 +235,20 @@ __device__ __forceinline__ void consume_blocks(const MArgs& A, const double* val
   }
   for (int i = 0; i < nblk; ++i) {
     bounds(i, b0, b1);
-    if (i + 1 < nblk) {
+    if (!kNext && i > 0) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int c = b0 + grp + 4 * u;
+        cur[u] = (rowok && c < b1) ? lp[(int64_t)c * ld] : 0.0;
+      }
+    }
+    if (kNext && i + 1 < nblk) {
       int n0, n1;
       bounds(i + 1, n0, n1);
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int c = n0 + grp + 4 * u;
-        nxt[u] = (rowok && c < n1) ? lp[(int64_t)c * ld] : 0.0;
+        nxt[kNext ? u : 0] = (rowok && c < n1) ? lp[(int64_t)c * ld] : 0.0;
       }
     }
     if (warp == 0) poll_vals<KR>(A, vals + (int64_t)b0 * KR, (b1 - b0) * KR, stg, lane);
@@ -250,8 +272,9 @@ __device__ __forceinline__ void consume_blocks(const MArgs& A, const double* val
 #pragma unroll
     for (int j = 0; j < KR; ++j) acc[j] += t[j];
     __syncthreads();
+    if (kNext)
 #pragma unroll
-    for (int u = 0; u < kU; ++u) cur[u] = nxt[u];
+      for (int u = 0; u < kU; ++u) cur[u] = nxt[kNext ? u : 0];
   }
 }
 
@@ -445,15 +468,20 @@ template <int KR, int kMinBlocks>
 __global__ void __launch_bounds__(kMT, kMinBlocks) mfwd_sweep(MArgs A) {
   extern __shared__ __align__(16) double msm[];
   MSmem<KR> S = carve<KR>(msm);
-  __shared__ int item_s, avail_s;
+  __shared__ int item_s, keep_s;
   const int tid = threadIdx.x, row = tid & (kMB - 1), grp = tid >> 6, jq = tid >> 6;
+  if (tid == 0) keep_s = -1;
   for (;;) {
     __syncthreads();
-    if (tid == 0) item_s = mpop(A);
+    if (tid == 0) {
+      item_s = keep_s >= 0 ? keep_s : mpop(A);
+      keep_s = -1;
+    }
     __syncthreads();
     const int it = item_s;
     if (it < 0) return;
     const MItem I = A.items[it];
+    if (A.trace && tid == 0) A.trace[2 * (size_t)it] = mtime();
     if (I.blk == kMWhole) {
       mfwd_whole<KR>(A, I, S, tid);
     } else {
@@ -490,15 +518,18 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mfwd_sweep(MArgs A) {
       }
     }
     __syncthreads();  // every row written before thread 0 releases the parent
+    if (A.trace && tid == 0) A.trace[2 * (size_t)it + 1] = mtime();
     if (tid == 0) {
       if (I.parent >= 0) {
         int old;
         asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(A.deps + I.parent) : "memory");
-        if (old == 1) {
+        if (old == 1) {  // depth first: the parent's first item runs here next
           __threadfence();
-          mpush(A, I.parent);
+          mpush(A, I.parent, 1);
+          keep_s = A.fbase[I.parent];
         }
       }
+      atomicAdd(A.done, 1);
     }
   }
 }
@@ -558,15 +589,51 @@ template <int KR, int kMinBlocks>
 __global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
   extern __shared__ __align__(16) double msm[];
   MSmem<KR> S = carve<KR>(msm);
-  __shared__ int item_s, avail_s;
+  __shared__ int item_s, keep_s;
   const int tid = threadIdx.x, row = tid & (kMB - 1), grp = tid >> 6, jq = tid >> 6;
+  if (tid == 0) keep_s = -1;
   for (;;) {
     __syncthreads();
-    if (tid == 0) item_s = mpop(A);
+    if (tid == 0) {
+      item_s = keep_s >= 0 ? keep_s : mpop(A);
+      keep_s = -1;
+    }
     __syncthreads();
     const int it = item_s;
     if (it < 0) return;
     const MItem I = A.items[it];
+    if (A.trace && tid == 0) A.trace[2 * (size_t)it] = mtime();
+    if (I.blk == kMPart) {
+      // one contribution-column chunk [np + ech_off, np + nech) of one pivot
+      // block: U[blk rows, chunk] x_chunk into its partial-sum slot, no waits
+      const double* g = A.pool + I.goff;
+      const int32_t* rw = A.rows + I.rows_off;
+      const int c0 = I.np + I.ech_off, c1 = I.np + I.nech, nr = I.nr;
+      for (int idx = tid; idx < (c1 - c0) * KR; idx += kMT) {
+        const int c = c0 + idx / KR, j = idx % KR;
+        S.stg[idx] = __ldcg(&A.xnew[(int64_t)rw[c] * KR + j]);
+      }
+      double acc[KR];
+#pragma unroll
+      for (int j = 0; j < KR; ++j) acc[j] = 0.0;
+      __syncthreads();
+      mstream<KR>(g + I.r0 + row, I.ld, row < nr, S.stg - c0 * KR, c0, c1, grp, acc);
+      put_part<KR>(S.part, grp, row, acc);
+      __syncthreads();
+      for (int idx = tid; idx < nr * KR; idx += kMT) {
+        const int r = idx / KR, j = idx % KR;
+        A.bpart[(int64_t)I.cbvec_off + idx] = (S.part[(0 * kMB + r) * KR + j] + S.part[(1 * kMB + r) * KR + j]) +
+                                              (S.part[(2 * kMB + r) * KR + j] + S.part[(3 * kMB + r) * KR + j]);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        if (A.trace) A.trace[2 * (size_t)it + 1] = mtime();
+        __threadfence();
+        atomicAdd(&A.pdone[I.front], 1);
+        atomicAdd(A.done, 1);
+      }
+      continue;
+    }
     if (I.blk == kMWhole) {
       mbwd_whole<KR>(A, I, S, tid);
     } else {
@@ -580,8 +647,9 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
       double acc[KR];
 #pragma unroll
       for (int j = 0; j < KR; ++j) acc[j] = 0.0;
-      // contribution columns: the ancestors' x (final: the front is ready)
-      for (int base = np; base < nf; base += kMStage) {
+      // contribution columns: the ancestors' x (final: the front is ready);
+      // wide fronts have them in partial items instead (I.pad chunks)
+      for (int base = I.pad > 0 ? nf : np; base < nf; base += kMStage) {
         const int hi = min(nf, base + kMStage);
         for (int idx = tid; idx < (hi - base) * KR; idx += kMT) {
           const int c = base + idx / KR, j = idx % KR;
@@ -595,8 +663,21 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
       consume_blocks<KR, false>(A, A.xnew + (int64_t)I.start * KR, g + r0 + row, ld, row < nr, lo, np, S.stg, tid,
                                 grp, acc);
       put_part<KR>(S.part, grp, row, acc);
+      if (I.pad > 0 && tid == 0) {  // the front's partial items (queued ahead of its blocks)
+        unsigned long long t0 = 0;
+        while (ld_acq(&A.pdone[I.front]) < A.npart[I.front]) {
+          __nanosleep(32);
+          if (mstalled(A, t0)) break;
+        }
+      }
       __syncthreads();
       sub_parts<KR>(S.w, S.part, nr, tid);
+      if (I.pad > 0)  // chunk partials in chunk order (deterministic)
+        for (int idx = tid; idx < nr * KR; idx += kMT) {
+          double t = 0.0;
+          for (int k = 0; k < I.pad; ++k) t += __ldcg(&A.bpart[(int64_t)I.cbvec_off + (int64_t)k * kMSlot + idx]);
+          S.w[idx] -= t;
+        }
       __syncthreads();
       double out[KR / 4];
       tile_mul<KR>(S.D, S.w, nr, row, jq, out);
@@ -605,6 +686,7 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
         for (int t = 0; t < KR / 4; ++t) store_xm<KR>(A, I.start + r0 + row, jq * (KR / 4) + t, out[t]);
     }
     __syncthreads();
+    if (A.trace && tid == 0) A.trace[2 * (size_t)it + 1] = mtime();
     if (I.blk == 0 || I.blk == kMWhole) {  // the front is complete: its effective children are ready
       if (tid == 0) __threadfence();
       __syncthreads();
@@ -612,10 +694,17 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
         const int f = A.ech[I.ech_off + x];
         if (atomicSub(&A.deps[f], 1) == 1) {
           __threadfence();
-          mpush(A, f);
+          if (x == 0) {  // the first effective child's first item runs here next
+            mpush(A, f, 1);
+            keep_s = A.fbase[f];
+          } else {
+            mpush(A, f);
+          }
         }
       }
     }
+    __syncthreads();
+    if (tid == 0) atomicAdd(A.done, 1);
   }
 }
 
@@ -626,6 +715,7 @@ struct MSolvePlan {
   int nfr = 0, n_fwd = 0, n_bwd = 0;
   DeviceBuffer d_items_f, d_items_b, d_meta, d_ech, d_state0, d_state, d_stall;
   DeviceBuffer d_y, d_x, d_cb;  // interleaved, sized for 8 right-hand sides
+  DeviceBuffer d_bpart;         // backward partial sums of wide fronts
   int64_t st_dep_f = 0, st_dep_b = 0, st_q_f = 0, st_q_b = 0, st_qctl = 0, st_pub = 0;
   int grid4 = 148, grid8 = 148;
 };
@@ -703,12 +793,37 @@ static void msolve_prepare(FactorEngine& fe) {
     }
     fcnt_f[f] = static_cast<int32_t>(fwd.size()) - fbase_f[f];
   }
+  std::vector<int32_t> npart(nfr, 0);
+  int64_t pslots = 0;
   for (int f = nfr - 1; f >= 0; --f) {
     const Front& F = S.fronts[f];
     fbase_b[f] = static_cast<int32_t>(bwd.size());
     if (npb[f] > 0) {
+      const int ncb = F.nf - F.npiv;
       if (whole[f]) {
         bwd.push_back(item(f, 0, F.npiv, kMWhole));
+      } else if (ncb > kMCbChunk) {
+        // wide front: per pivot block, one partial item per kMCbChunk
+        // contribution columns (independent, ahead of the blocks in the queue),
+        // the block items add the partials in chunk order
+        const int nck = (ncb + kMCbChunk - 1) / kMCbChunk;
+        for (int b = npb[f] - 1; b >= 0; --b)
+          for (int k = 0; k < nck; ++k) {
+            MItem it = item(f, b * kMB, std::min(F.npiv, (b + 1) * kMB), kMPart);
+            it.ech_off = k * kMCbChunk;
+            it.nech = std::min(ncb, (k + 1) * kMCbChunk);
+            it.cbvec_off = static_cast<int32_t>(pslots + (static_cast<int64_t>(b) * nck + k) * kMSlot);
+            bwd.push_back(it);
+          }
+        for (int b = npb[f] - 1; b >= 0; --b) {
+          MItem it = item(f, b * kMB, std::min(F.npiv, (b + 1) * kMB), b);
+          it.pad = nck;
+          it.cbvec_off = static_cast<int32_t>(pslots + static_cast<int64_t>(b) * nck * kMSlot);
+          bwd.push_back(it);
+        }
+        npart[f] = npb[f] * nck;
+        pslots += static_cast<int64_t>(npb[f]) * nck * kMSlot;
+        if (pslots > INT32_MAX) throw Error(errc::solver, "multi-RHS solve: partial-sum slots exceed int32");
       } else {
         for (int b = npb[f] - 1; b >= 0; --b) bwd.push_back(item(f, b * kMB, std::min(F.npiv, (b + 1) * kMB), b));
       }
@@ -743,6 +858,7 @@ static void msolve_prepare(FactorEngine& fe) {
   meta.insert(meta.end(), fcnt_f.begin(), fcnt_f.end());
   meta.insert(meta.end(), fbase_b.begin(), fbase_b.end());
   meta.insert(meta.end(), fcnt_b.begin(), fcnt_b.end());
+  meta.insert(meta.end(), npart.begin(), npart.end());
   P->d_meta.upload(meta.data(), sizeof(int32_t) * meta.size(), fe.stream);
   P->d_ech.upload(ech.data(), sizeof(int32_t) * ech.size(), fe.stream);
   std::vector<int32_t> st;
@@ -755,9 +871,9 @@ static void msolve_prepare(FactorEngine& fe) {
   P->st_q_b = static_cast<int64_t>(st.size());
   st.insert(st.end(), qb.begin(), qb.end());
   P->st_qctl = static_cast<int64_t>(st.size());
-  st.insert(st.end(), {0, nq_f, 0, nq_b});
+  st.insert(st.end(), {0, nq_f, 0, nq_b, 0, 0});  // {head, tail} fwd, bwd; items done fwd, bwd
   P->st_pub = static_cast<int64_t>(st.size());
-  st.resize(st.size() + 2 * static_cast<size_t>(nfr), 0);  // published blocks fwd, bwd
+  st.resize(st.size() + 3 * static_cast<size_t>(nfr), 0);  // published blocks fwd, bwd; bwd partials done
   P->d_state0.upload(st.data(), sizeof(int32_t) * st.size(), fe.stream);
   P->d_state.alloc(P->d_state0.bytes);
   P->d_stall.alloc(sizeof(int));
@@ -765,13 +881,14 @@ static void msolve_prepare(FactorEngine& fe) {
   P->d_y.alloc(sizeof(double) * kMaxRhs * std::max<int64_t>(1, fe.n));
   P->d_x.alloc(sizeof(double) * kMaxRhs * std::max<int64_t>(1, fe.n));
   P->d_cb.alloc(sizeof(double) * kMaxRhs * std::max<int64_t>(1, S.cbvec));
+  P->d_bpart.alloc(sizeof(double) * std::max<int64_t>(1, pslots));
   int nsm = 148, occ = 1;
   RQB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, fe.device));
-  smem_at_least(mfwd_sweep<4, 2>, msmem_bytes<4>());
-  smem_at_least(mbwd_sweep<4, 2>, msmem_bytes<4>());
+  smem_at_least(mfwd_sweep<4, 3>, msmem_bytes<4>());
+  smem_at_least(mbwd_sweep<4, 3>, msmem_bytes<4>());
   smem_at_least(mfwd_sweep<8, 2>, msmem_bytes<8>());
   smem_at_least(mbwd_sweep<8, 2>, msmem_bytes<8>());
-  RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mfwd_sweep<4, 2>, kMT, msmem_bytes<4>()));
+  RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mfwd_sweep<4, 3>, kMT, msmem_bytes<4>()));
   P->grid4 = nsm * std::max(1, occ);
   RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mfwd_sweep<8, 2>, kMT, msmem_bytes<8>()));
   P->grid8 = nsm * std::max(1, occ);
@@ -793,19 +910,25 @@ static void msolve_launch(FactorEngine& fe, MArgs A, int grid) {
   F.deps = sb + P.st_dep_f;
   F.queue = sb + P.st_q_f;
   F.qctl = sb + P.st_qctl;
+  F.done = sb + P.st_qctl + 4;
   F.pub = sb + P.st_pub;
   F.fbase = meta;
   F.fcnt = meta + nfr;
   if (P.n_fwd > 0) mfwd_sweep<KR, kMinB><<<std::min(grid, P.n_fwd), kMT, msmem_bytes<KR>(), st>>>(F);
   MArgs B = A;
+  if (A.trace) B.trace = A.trace + 2 * (size_t)P.n_fwd;
   B.items = P.d_items_b.as<MItem>();
   B.nitems = P.n_bwd;
   B.deps = sb + P.st_dep_b;
   B.queue = sb + P.st_q_b;
   B.qctl = sb + P.st_qctl + 2;
+  B.done = sb + P.st_qctl + 5;
   B.pub = sb + P.st_pub + nfr;
+  B.pdone = sb + P.st_pub + 2 * nfr;
   B.fbase = meta + 2 * nfr;
   B.fcnt = meta + 3 * nfr;
+  B.npart = meta + 4 * nfr;
+  B.bpart = P.d_bpart.as<double>();
   if (P.n_bwd > 0) mbwd_sweep<KR, kMinB><<<std::min(grid, P.n_bwd), kMT, msmem_bytes<KR>(), st>>>(B);
   RQB_CUDA(cudaGetLastError());
 }
@@ -845,11 +968,31 @@ void rqb_msolve_enqueue(FactorEngine& fe, const double* b, int64_t ldb, int nrhs
   A.xl = xl;
   A.nrhs = nrhs;
   A.stall = P.d_stall.as<int>();
+  unsigned long long* trace = nullptr;
+  {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (std::getenv("RQB_MSOLVE_TRACE") && cs == cudaStreamCaptureStatusNone)
+      RQB_CUDA(cudaMalloc(&trace, sizeof(unsigned long long) * 2 * (size_t)(P.n_fwd + P.n_bwd)));
+  }
+  A.trace = trace;
   if (nrhs <= 4)
-    msolve_launch<4, 2>(fe, A, P.grid4);
+    msolve_launch<4, 3>(fe, A, P.grid4);
   else
     msolve_launch<8, 2>(fe, A, P.grid8);
   fe.launches_solve = 2;
+  if (trace) {  // development trace: {n_fwd, n_bwd} then per item {start, end} (ns)
+    cudaStreamSynchronize(st);
+    std::vector<unsigned long long> h(2 * (size_t)(P.n_fwd + P.n_bwd));
+    cudaMemcpy(h.data(), trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+    if (FILE* fp = std::fopen(std::getenv("RQB_MSOLVE_TRACE"), "wb")) {
+      const int32_t hdr[2] = {P.n_fwd, P.n_bwd};
+      std::fwrite(hdr, sizeof(hdr), 1, fp);
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
+      std::fclose(fp);
+    }
+    cudaFree(trace);
+  }
 }
 
 void rqb_msolve_prepare(FactorEngine& fe) {
