@@ -401,7 +401,8 @@ def run_b200(args):
             "free_to_full")})
         t0 = time.perf_counter()
         op2 = rq.build_operator(PH, SIGMA, o)
-        op2.solve_quadratic(nev, eps=1e-10, seed=0, max_restarts=args.max_restarts, raise_partial=False)
+        op2.solve_quadratic(nev, eps=1e-10, seed=0, max_restarts=args.max_restarts, raise_partial=False,
+                            block=max(1, args.block))
         e2e_nev_ms = (time.perf_counter() - t0) * 1e3
         del op2
 
@@ -463,7 +464,15 @@ def run_b200(args):
                    "l2": "flushed (256 MiB scrub) before every timed step"},
         "factor_frac_fp64": round(value / ws / (FP64_PEAK_TFLOPS * 1e3), 5),
         "iga_companion": companion,
-        "time_to_nev_ms": round(rest[len(rest) // 2], 3), "time_to_nev_first_call_ms": round(first, 3),
+        # headline: the faster of the two solvers (block Krylov-Schur with
+        # multi-RHS sweeps, else the single-vector one), same tolerance and checks
+        "time_to_nev_ms": round(min(rest[len(rest) // 2], sorted(t_nev_b[1:])[len(t_nev_b[1:]) // 2])
+                                if t_nev_b else rest[len(rest) // 2], 3),
+        "time_to_nev_method": ("block Krylov-Schur, block %d" % args.block)
+                              if t_nev_b and sorted(t_nev_b[1:])[len(t_nev_b[1:]) // 2] < rest[len(rest) // 2]
+                              else "single-vector Krylov-Schur",
+        "time_to_nev_single_ms": round(rest[len(rest) // 2], 3),
+        "time_to_nev_first_call_ms": round(first, 3),
         "time_to_nev_min_ms": round(rest[0], 3), "time_to_nev_max_ms": round(rest[-1], 3),
         "time_to_nev_seeds": {str(s_): {"ms": round(t, 1), "cycles": i.get("restarts"), "n_fb": i.get("n_fb")}
                               for s_, t, i in zip(seeds[1:], t_nev[1:], infos[1:])},
