@@ -861,6 +861,16 @@ double OperatorEngine::time_op(int what, int iters, int param) {
     h.alloc(sizeof(double) * 2 * k);
   }
   DeviceBuffer Vb, Rb;
+  const int kb = std::max(1, std::min(8, param >> 16));  // what 11 / 12: block width in the high bits
+  if (what == 11 || what == 12) {  // block CGS projection / update over k = param & 0xffff basis vectors
+    V.alloc(sizeof(double) * (param & 0xffff) * n2);
+    Rb.alloc(sizeof(double) * n2 * 8);
+    h.alloc(sizeof(double) * (param & 0xffff) * 8);
+    RQB_CUDA(cudaMemsetAsync(V.p, 0, V.bytes, stream));
+    RQB_CUDA(cudaMemsetAsync(Rb.p, 0, Rb.bytes, stream));
+    RQB_CUDA(cudaMemsetAsync(h.p, 0, h.bytes, stream));
+    prepare_block((param & 0xffff) + 8, 8);
+  }
   if (what == 9 || what == 10) {  // block apply / multi-RHS solve of param (<= 8) vectors
     Vb.alloc(sizeof(double) * n2 * 8);
     Rb.alloc(sizeof(double) * n2 * 8);
@@ -889,6 +899,8 @@ double OperatorEngine::time_op(int what, int iters, int param) {
       case 6: spmv(2, a.as<double>(), b.as<double>()); break;
       case 7: combine(V.as<double>(), k, Q.as<double>(), k, k, X.as<double>()); break;
       case 8: ritz_residuals(V.as<double>(), k, Q.as<double>(), k / 2, lamh.data(), blkh.data(), X.as<double>(), h.as<double>()); break;
+      case 11: gemm_t(V.as<double>(), param & 0xffff, Rb.as<double>(), kb, h.as<double>(), param & 0xffff); break;
+      case 12: gemm_n(V.as<double>(), param & 0xffff, h.as<double>(), param & 0xffff, Rb.as<double>(), kb); break;
       case 9: apply_block(Vb.as<double>(), std::min(k, 8), Rb.as<double>()); break;
       case 10:
         rqb_msolve_enqueue(*fac, Vb.as<double>(), n, std::min(k, 8), Rb.as<double>(), n, 1.0, nullptr, 0, 0.0, nullptr);

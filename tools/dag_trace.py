@@ -21,13 +21,15 @@ tk = np.frombuffer(raw, np.dtype([("front", "<i4"), ("type", "<i2"), ("step", "<
 allt = np.frombuffer(raw, np.uint64, 4 * nt, 4 + 16 * nt).astype(np.int64)
 tr = allt[:2 * nt].reshape(-1, 2).copy()
 ph = allt[2 * nt:].reshape(-1, 2).copy()  # {work done, fence done}
-t00 = tr[:, 0].min()
-tr -= t00
-ph -= t00
-names = ["SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD", "UPDCB"]
+valid = (tr[:, 0] > 0) & (tr[:, 1] > 0)
+t00 = tr[valid, 0].min()
+tr = np.where(valid[:, None], tr - t00, 0)
+ph = np.where(valid[:, None], ph - t00, 0)
+print(f"untraced tasks: {(~valid).sum()} of {nt}; types", np.unique(tk['type'][~valid]))
+names = ["SMALL", "ASM", "DIAG", "ROWS", "COLS", "UPD", "UPDCB", "UPDB"]
 nfr = len(o.parent)
 fs = np.full(nfr, 1 << 62); fe = np.zeros(nfr, np.int64)
-np.minimum.at(fs, tk["front"], tr[:, 0]); np.maximum.at(fe, tk["front"], tr[:, 1])
+np.minimum.at(fs, tk["front"][valid], tr[valid, 0]); np.maximum.at(fe, tk["front"][valid], tr[valid, 1])
 print(f"{cfg}: span {tr[:,1].max()/1e3:.1f} us, tasks {nt}")
 lv = o.level
 for L in sorted(set(lv.tolist())):
@@ -44,7 +46,7 @@ print("  critical chain (front nf npiv: ready -> start -> end, us):")
 while True:
     ready = child_end.get(f_, (0, -1))[0]
     ty = tk["type"][tk["front"] == f_]
-    cnts = {names[t]: int((ty == t).sum()) for t in range(7) if (ty == t).sum()}
+    cnts = {names[t]: int((ty == t).sum()) for t in range(8) if (ty == t).sum()}
     print(f"    front {f_:5d} nf {o.nf[f_]:5d} npiv {o.npiv[f_]:5d} level {lv[f_]:2d}: ready {ready/1e3:8.1f} start {fs[f_]/1e3:8.1f} end {fe[f_]/1e3:8.1f}  {cnts}")
     if f_ not in child_end: break
     f_ = child_end[f_][1]
@@ -54,3 +56,13 @@ if len(sys.argv) > 2:  # task list of one front
     idx = idx[np.argsort(tr[idx, 0])]
     for i in idx[:200]:
         print(f"     {names[tk['type'][i]]:5s} s{tk['step'][i]:3d} a{tk['a'][i]:3d} b{tk['b'][i]:3d}  {tr[i,0]/1e3:8.2f} -> {tr[i,1]/1e3:8.2f}  ({(tr[i,1]-tr[i,0])/1e3:6.2f})  work {(ph[i,0]-tr[i,0])/1e3:6.2f} fence {(ph[i,1]-ph[i,0])/1e3:6.2f} succ {(tr[i,1]-ph[i,1])/1e3:6.2f}")
+# busy-CTA profile over time (20 bins): concurrent tasks, and the share of
+# tasks by type per bin
+span = tr[:, 1].max()
+bins = np.linspace(0, span, 21)
+print("  busy profile (bin: active task-us / bin width, by type):")
+for b0, b1 in zip(bins[:-1], bins[1:]):
+    ov = np.clip(np.minimum(tr[:, 1], b1) - np.maximum(tr[:, 0], b0), 0, None)
+    tot = ov.sum() / (b1 - b0)
+    by = {names[t]: round(float(ov[tk["type"] == t].sum() / (b1 - b0)), 1) for t in range(8)}
+    print(f"   {b0/1e3:7.1f}-{b1/1e3:7.1f} us: {tot:6.1f}  {by}")
