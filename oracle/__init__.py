@@ -50,6 +50,8 @@ def _bind(lib):
     s("oracle_eig_solve_quadratic_block", C.c_int, vp, C.c_int, C.c_int, C.c_double, C.c_uint64,
       C.c_int, C.c_int, C.c_int, C.c_int, f64p, f64p, vp, i32p, f64p)
     s("oracle_eig_destroy", None, vp)
+    s("oracle_gh_solve", C.c_int, C.c_int64, i64p, i32p, f64p, f64p, i32p, C.c_int, C.c_int, C.c_double,
+      C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, f64p, f64p, i32p)
     s("oracle_eig_create2", C.c_int, vp, C.c_int64, i64p, i32p, f64p, f64p, f64p, i32p, C.c_int,
       C.c_int, C.c_double, C.c_int, C.POINTER(vp))
     s("oracle_eig_varsigma", C.c_double, vp)
@@ -374,3 +376,19 @@ class RefPencil:
 
 def ref_config(name):
     return RefPencil(*CONFIGS[name])
+
+
+def solve_generalized_hermitian(rowptr, col, A, B, box, elems, s, nev, m=0, tol=1e-10, seed=0, max_restarts=100,
+                                leaf=64, kind="port"):
+    """Oracle restatement of solve_generalized_hermitian:
+    complex multifrontal LU of A - s B, Lanczos with full reorthogonalisation,
+    thick restarts. Returns (lam, res) nearest the shift first."""
+    lib = lib_for(kind)
+    n = len(rowptr) - 1
+    lam, res, st = np.zeros(nev), np.zeros(nev), np.zeros(2, np.int32)
+    _chk(lib, lib.oracle_gh_solve(n, np.ascontiguousarray(rowptr, np.int64), np.ascontiguousarray(col, np.int32),
+                                  np.ascontiguousarray(A, np.float64), np.ascontiguousarray(B, np.float64),
+                                  np.ascontiguousarray(np.asarray(box).ravel(), np.int32), int(elems), int(leaf),
+                                  float(s), int(nev), int(m), float(tol), int(seed), int(max_restarts), lam, res, st))
+    return lam, res
+

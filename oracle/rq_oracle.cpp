@@ -1058,6 +1058,159 @@ double scale_pencil(Pencil& P) {
   return s;
 }
 
+// solve_generalized_hermitian (Alg. 1, Remark 3):
+// A u = lambda B u, A Hermitian, B HPD, real shift s. The reference path's
+// restatement: the oracle's complex multifrontal LU of A - s B, S = (A - s
+// B)^{-1} B, the three-term Lanczos recurrence (alpha_j = v_j^H B S v_j,
+// beta_j = ||r||_B) with a full CGS2 reorthogonalisation pass per step whose
+// coefficients are not added to T (selective reorthogonalisation always
+// engaged), thick restart keeping the p Ritz vectors nearest the shift (T =
+// diag(theta) bordered by beta_m y_m), cyclic-Jacobi eigenvalues of the real
+// symmetric T, explicit residuals ||A u - lambda B u|| / ((||A||_1 + |lambda|
+// ||B||_1) ||u||).
+void jacobi_sym(std::vector<double> A, int n, std::vector<double>& w, std::vector<double>& Z) {
+  Z.assign(static_cast<size_t>(n) * n, 0.0);
+  for (int i = 0; i < n; ++i) Z[i + static_cast<size_t>(i) * n] = 1.0;
+  auto a = [&](int i, int j) -> double& { return A[i + static_cast<size_t>(j) * n]; };
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) tot += a(i, j) * a(i, j), off += i != j ? a(i, j) * a(i, j) : 0.0;
+    if (off <= 1e-30 * tot) break;
+    for (int p = 0; p + 1 < n; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        if (a(p, q) == 0.0) continue;
+        const double th = (a(q, q) - a(p, p)) / (2.0 * a(p, q));
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < n; ++k) {
+          const double x = a(k, p), y = a(k, q);
+          a(k, p) = c * x - sn * y, a(k, q) = sn * x + c * y;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double x = a(p, k), y = a(q, k);
+          a(p, k) = c * x - sn * y, a(q, k) = sn * x + c * y;
+        }
+        for (int k = 0; k < n; ++k) {
+          double& x = Z[k + static_cast<size_t>(p) * n];
+          double& y = Z[k + static_cast<size_t>(q) * n];
+          const double zx = x, zy = y;
+          x = c * zx - sn * zy, y = sn * zx + c * zy;
+        }
+      }
+  }
+  w.resize(n);
+  for (int i = 0; i < n; ++i) w[i] = a(i, i);
+}
+
+struct GhOut {
+  std::vector<double> lam, res;
+  int cycles = 0;
+  bool ok = false;
+};
+
+GhOut solve_generalized_hermitian(const Csr& A, const Csr& B, const Factor& F, double s, int nev, int m, double tol,
+                                  uint64_t seed, int max_restarts) {
+  const int64_t n = A.n;
+  const int keep = nev + std::min(20, m - nev - 1);
+  std::vector<std::vector<cd>> V(m + 1, std::vector<cd>(n));
+  std::vector<cd> r(n), w(n), t(n);
+  auto bvec = [&](const cd* x, cd* y) { spmv(B, x, y, nullptr); };
+  auto apply = [&](const cd* v, cd* out) {
+    bvec(v, t.data());
+    solve_factored(F, t.data(), out, nullptr);
+  };
+  const double nA = norm1(A), nB = norm1(B);
+  {
+    uint64_t st = seed;
+    for (int64_t i = 0; i < n; ++i) r[i] = uni(st);
+    bvec(r.data(), w.data());
+    const double b = std::sqrt(k_dotc(r.data(), w.data(), n).real());
+    for (int64_t i = 0; i < n; ++i) V[0][i] = r[i] / b;
+  }
+  std::vector<double> T(static_cast<size_t>(m + 1) * (m + 1), 0.0), beta(m + 1, 0.0);
+  auto Tc = [&](int i, int j) -> double& { return T[i + static_cast<size_t>(j) * (m + 1)]; };
+  int k = 0;
+  GhOut out;
+  while (out.cycles < max_restarts) {
+    ++out.cycles;
+    int mm = m;
+    for (int j = k; j < m; ++j) {
+      apply(V[j].data(), r.data());
+      double alpha = 0.0;
+      for (int pass = 0; pass < 2; ++pass) {
+        bvec(r.data(), w.data());
+        std::vector<cd> h(j + 1);
+        dots(V, j + 1, w.data(), n, h.data(), nullptr);
+        axpys(V, j + 1, h.data(), r.data(), n, -1.0, nullptr);
+        alpha += h[j].real();
+      }
+      bvec(r.data(), w.data());
+      beta[j] = std::sqrt(std::max(0.0, k_dotc(r.data(), w.data(), n).real()));
+      Tc(j, j) = alpha;
+      Tc(j + 1, j) = Tc(j, j + 1) = beta[j];
+      for (int64_t i = 0; i < n; ++i) V[j + 1][i] = r[i] / beta[j];
+      if (beta[j] <= 1e-14 * std::max(1.0, std::fabs(alpha))) {
+        mm = j + 1;
+        break;
+      }
+    }
+    std::vector<double> Tm(static_cast<size_t>(mm) * mm), th, Y;
+    for (int j = 0; j < mm; ++j)
+      for (int i = 0; i < mm; ++i) Tm[i + static_cast<size_t>(j) * mm] = Tc(i, j);
+    jacobi_sym(Tm, mm, th, Y);
+    std::vector<int> ord(mm);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](int a_, int b_) { return std::fabs(1.0 / th[a_]) < std::fabs(1.0 / th[b_]); });
+    const double bm = mm < m ? 0.0 : beta[m - 1];
+    const int nw = std::min(nev, mm);
+    bool all = true;
+    for (int c = 0; c < nw; ++c)
+      if (!(std::fabs(bm * Y[(mm - 1) + static_cast<size_t>(ord[c]) * mm]) / std::fabs(th[ord[c]]) <= 1e3 * tol))
+        all = false;
+    if (all || mm < m) {
+      out.lam.clear();
+      out.res.clear();
+      all = true;
+      for (int c = 0; c < nw; ++c) {
+        const int i = ord[c];
+        std::vector<cd> x(n, 0.0), y(mm);
+        for (int q = 0; q < mm; ++q) y[q] = Y[q + static_cast<size_t>(i) * mm];
+        axpys(V, mm, y.data(), x.data(), n, 1.0, nullptr);
+        const double lam = s + 1.0 / th[i];
+        std::vector<cd> ax(n), bx(n);
+        spmv(A, x.data(), ax.data(), nullptr);
+        spmv(B, x.data(), bx.data(), nullptr);
+        double rr = 0, xx = 0;
+        for (int64_t e = 0; e < n; ++e) rr += std::norm(ax[e] - lam * bx[e]), xx += std::norm(x[e]);
+        const double res = std::sqrt(rr) / ((nA + std::fabs(lam) * nB) * std::sqrt(xx));
+        out.lam.push_back(lam);
+        out.res.push_back(res);
+        if (!(res <= tol)) all = false;
+      }
+      if (all || mm < m) {
+        out.ok = all;
+        break;
+      }
+    }
+    // thick restart
+    const int p = std::min(keep, m - 1);
+    std::vector<std::vector<cd>> V2(p + 1, std::vector<cd>(n, 0.0));
+    for (int c = 0; c < p; ++c)
+      for (int q = 0; q < mm; ++q) k_axpy(Y[q + static_cast<size_t>(ord[c]) * mm], V[q].data(), V2[c].data(), n);
+    V2[p] = V[mm];
+    for (int c = 0; c <= p; ++c) V[c].swap(V2[c]);
+    std::fill(T.begin(), T.end(), 0.0);
+    for (int c = 0; c < p; ++c) {
+      Tc(c, c) = th[ord[c]];
+      Tc(p, c) = Tc(c, p) = bm * Y[(mm - 1) + static_cast<size_t>(ord[c]) * mm];
+    }
+    k = p;
+  }
+  return out;
+}
+
 }  // namespace oracle
 
 // ============================================================================
@@ -1354,6 +1507,27 @@ int oracle_eig_solve_quadratic(void* h, int nev, int m, double tol, uint64_t see
 }
 
 void oracle_eig_destroy(void* h) { delete static_cast<OracleEig*>(h); }
+
+// solve_generalized_hermitian: real A, B (values, not
+// interleaved) on one pattern; lam / res: double[nev] (nearest the shift first);
+// stats: {cycles, ok}.
+int oracle_gh_solve(int64_t n, const int64_t* rp, const int32_t* col, const double* a, const double* b,
+                    const int32_t* box, int elems, int leaf, double s, int nev, int m, double tol, uint64_t seed,
+                    int max_restarts, double* lam, double* res, int32_t* stats) {
+  return guarded([&] {
+    std::vector<double> ac(2 * rp[n], 0.0), bc(2 * rp[n], 0.0), qc(2 * rp[n], 0.0);
+    for (int64_t k = 0; k < rp[n]; ++k) ac[2 * k] = a[k], bc[2 * k] = b[k], qc[2 * k] = a[k] - s * b[k];
+    const oracle::Csr A = make_csr(n, rp, col, ac.data()), B = make_csr(n, rp, col, bc.data()),
+                      Q = make_csr(n, rp, col, qc.data());
+    const oracle::Symbolic S = oracle::symbolic(n, rp, col, box, elems, leaf);
+    const oracle::Factor F = oracle::lu_factorize(S, Q, nullptr);
+    const int mk = m > 0 ? m : std::max(2 * nev, nev + 20);
+    const oracle::GhOut o = oracle::solve_generalized_hermitian(A, B, F, s, nev, mk, tol, seed, max_restarts);
+    for (int i = 0; i < nev && i < static_cast<int>(o.lam.size()); ++i) lam[i] = o.lam[i], res[i] = o.res[i];
+    if (stats) stats[0] = o.cycles, stats[1] = o.ok;
+    if (!o.ok) throw oracle::OracleError{4, "oracle: generalized Hermitian solve did not converge"};
+  });
+}
 
 int oracle_eig_step_profile(void* h, int j0, int nsteps, uint64_t seed, double* out) {
   return guarded([&] { oracle::step_profile(*static_cast<OracleEig*>(h)->op, j0, nsteps, seed, out); });

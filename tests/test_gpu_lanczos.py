@@ -88,3 +88,18 @@ def test_maxwell_non_conductive_lambda_23_23():
     w = sla.eigsh(As.tocsc(), k=4, M=Ms.tocsc(), sigma=s, which="LM", return_eigenvectors=False, tol=1e-12)
     w = np.sort(w[np.argsort(np.abs(w - s))])
     np.testing.assert_allclose(np.sort(lam), w, rtol=1e-8)
+
+
+@pytest.mark.parametrize("ne,s", [(16, 200.0), (32, 1500.0)])
+def test_maxwell_vs_oracle_restatement(ne, s):
+    """GPU Lanczos against the oracle's restatement of
+    solve_generalized_hermitian (complex multifrontal LU of A - s B on the
+    reference kernels, Lanczos with full reorthogonalisation, thick restarts)
+    on the H(curl) p = 4 Maxwell pencil: eigenvalues within relative 1e-9."""
+    import oracle
+    P = rq.assemble(rq.CURL, 4, ne, 0)
+    pairs = rq.solve_generalized_hermitian(P.K - P.M, P.M, s, 6, pencil=P, eps=1e-10)
+    lam = np.sort([p.lam.real for p in pairs])
+    lo, ro = oracle.solve_generalized_hermitian(P.rowptr, P.col, P.K - P.M, P.M, P.box, P.elems, s, 6)
+    assert np.all(ro <= 1e-10)
+    np.testing.assert_allclose(lam, np.sort(lo), rtol=1e-9)

@@ -210,3 +210,23 @@ def test_scale_pencil_known_answer():
     with pytest.raises(oracle.OracleError) as e:  # zero M
         oracle.scale_pencil(n, rp, col, np.ones(n), np.ones(n), np.zeros(n))
     assert e.value.code == 6
+
+
+def test_oracle_generalized_hermitian_known_answers():
+    """The oracle's solve_generalized_hermitian: diag(1, 2, 3)
+    with B = I -> {1, 2, 3}, and the H(curl) p = 4 16^2 Maxwell
+    pencil (curl-curl = K - M, B = M) against scipy's ARPACK shift-invert; the
+    double eigenvalue pi^2 (2^2 + 4^2) = 197.39 within the discretisation error."""
+    import scipy.sparse.linalg as sla
+    rp = np.arange(0, 10, 3, dtype=np.int64)
+    col = np.tile(np.arange(3, dtype=np.int32), 3)
+    lam, res = oracle.solve_generalized_hermitian(rp, col, np.diag([1.0, 2, 3]).ravel(), np.eye(3).ravel(),
+                                                  np.zeros((3, 4), np.int32), 1, 0.0, 3, m=3)
+    np.testing.assert_allclose(np.sort(lam), [1, 2, 3], rtol=1e-13)
+    P = rq.assemble(rq.CURL, 4, 16, 0)
+    lam, res = oracle.solve_generalized_hermitian(P.rowptr, P.col, P.K - P.M, P.M, P.box, P.elems, 200.0, 4)
+    assert np.all(res <= 1e-10)
+    w = sla.eigsh((P.to_scipy("K") - P.to_scipy("M")).tocsc(), k=4, M=P.to_scipy("M").tocsc(), sigma=200.0,
+                  return_eigenvectors=False, tol=1e-12)
+    np.testing.assert_allclose(np.sort(lam), np.sort(w), rtol=1e-9)
+    assert abs(lam[0] - 20 * np.pi ** 2) <= 1e-4 * 20 * np.pi ** 2
