@@ -138,15 +138,16 @@ __global__ void reduce_parts(const double* __restrict__ part, int nb, int k, dou
   }
 }
 
-__global__ void gemv_n_k(const double* __restrict__ V, int k, int64_t n2,
+// r[e] -= sum_i V[i ldv + e] h[i], e < len
+__global__ void gemv_n_k(const double* __restrict__ V, int k, int64_t ldv, int64_t len,
                          const double* __restrict__ h, double* __restrict__ r) {
   extern __shared__ double hs[];
   for (int i = threadIdx.x; i < k; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < len;
        e += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int i = 0; i < k; ++i) s += V[(int64_t)i * n2 + e] * hs[i];
+    for (int i = 0; i < k; ++i) s += V[(int64_t)i * ldv + e] * hs[i];
     r[e] -= s;
   }
 }
@@ -351,6 +352,35 @@ __global__ void spmm_op_k(int64_t n, const int64_t* __restrict__ rowptr, const i
     double2* o = reinterpret_cast<double2*>(Ti + row * KB);
 #pragma unroll
     for (int q = 0; q < KB / 2; ++q) o[q] = make_double2(s[2 * q], s[2 * q + 1]);
+  }
+}
+
+// Y[j * ldy + row] = sum_k A[row, k] Xi[col_k * KB + j], j < w (interleaved
+// input, column-major output): one pass over the pattern for the w vectors
+template <int KB>
+__global__ void spmm_csr_k(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                           const double* __restrict__ val, const double* __restrict__ Xi, int w,
+                           double* __restrict__ Y, int64_t ldy) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) s[j] = 0.0;
+  for (int64_t k = rowptr[row] + lane; k < rowptr[row + 1]; k += 32) {
+    const double a = val[k];
+    const double2* x = reinterpret_cast<const double2*>(Xi + (int64_t)col[k] * KB);
+#pragma unroll
+    for (int q = 0; q < KB / 2; ++q) {
+      const double2 t = x[q];
+      s[2 * q] += a * t.x;
+      s[2 * q + 1] += a * t.y;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    const double t = warp_sum(s[j]);
+    if (lane == 0 && j < w) Y[j * ldy + row] = t;
   }
 }
 
@@ -686,7 +716,7 @@ void OperatorEngine::gemv_t(const double* V, int k, const double* w, double* h) 
 
 void OperatorEngine::gemv_n(const double* V, int k, const double* h, double* r, double* h_acc) {
   if (k <= 0) return;
-  gemv_n_k<<<std::min(div_up(2 * n, 256), 148 * 8), 256, sizeof(double) * k, stream>>>(V, k, 2 * n,
+  gemv_n_k<<<std::min(div_up(2 * n, 256), 148 * 8), 256, sizeof(double) * k, stream>>>(V, k, 2 * n, 2 * n,
                                                                                      h, r);
   ++launches;
   (void)h_acc;
@@ -714,6 +744,30 @@ void OperatorEngine::apply_block(const double* V, int bs, double* R) {
   // R_u = -Q(s)^{-1} T ; R_l = s R_u + V_u (fused in the backward sweep), bs vectors per pass
   rqb_msolve_enqueue(*fac, Ti, 1, bs, R, n2, -1.0, V, n2, sigma, R + n, kb);
   launches += fac->launches_solve;
+}
+
+void OperatorEngine::mspmv_block(const double* R, int w, double* Wl) {
+  if (w <= 0) return;
+  if (d_tb.bytes < sizeof(double) * n * 8 * 3) d_tb.alloc(sizeof(double) * n * 8 * 3);
+  double* Xi = d_tb.as<double>();
+  const int64_t n2 = 2 * n;
+  const int grid = std::min(div_up(n, 256), 148 * 8);
+  if (w <= 4) {
+    interleave_k<4><<<grid, 256, 0, stream>>>(R + n, n2, n, w, Xi);
+    spmm_csr_k<4><<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
+                                                           d_M.as<double>(), Xi, w, Wl, n);
+  } else {
+    interleave_k<8><<<grid, 256, 0, stream>>>(R + n, n2, n, w, Xi);
+    spmm_csr_k<8><<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
+                                                           d_M.as<double>(), Xi, w, Wl, n);
+  }
+  launches += 2;
+}
+
+void OperatorEngine::gemv_n_len(const double* V, int k, int64_t ldv, int64_t len, const double* h, double* r) {
+  if (k <= 0) return;
+  gemv_n_k<<<std::min(div_up(len, 256), 148 * 8), 256, sizeof(double) * k, stream>>>(V, k, ldv, len, h, r);
+  ++launches;
 }
 
 void OperatorEngine::prepare_block(int kmax, int bs) {
@@ -787,6 +841,14 @@ void OperatorEngine::bnorm_normalize_b(const double* r, double* beta_out, double
   spmv(2, r + n, t);  // t = M r_l
   dot_part<<<kRedBlocks, kRedThreads, 0, stream>>>(r, r + n, r, t, n, 2 * n, d_part.as<double>());
   normalize_b_k<<<std::min(div_up(2 * n, 256), 148 * 8), 256, 0, stream>>>(d_part.as<double>(), kRedBlocks, r, t,
+                                                                          n, beta_out, v_next, bv_next);
+  launches += 2;
+}
+
+void OperatorEngine::bnorm_normalize_w(const double* r, const double* wl, double* beta_out, double* v_next,
+                                       double* bv_next) {
+  dot_part<<<kRedBlocks, kRedThreads, 0, stream>>>(r, r + n, r, wl, n, 2 * n, d_part.as<double>());
+  normalize_b_k<<<std::min(div_up(2 * n, 256), 148 * 8), 256, 0, stream>>>(d_part.as<double>(), kRedBlocks, r, wl,
                                                                           n, beta_out, v_next, bv_next);
   launches += 2;
 }
@@ -1040,7 +1102,7 @@ void GhEngine::gemv_t(const double* V, int k, const double* w, double* h) {
 
 void GhEngine::gemv_n(const double* V, int k, const double* h, double* r) {
   if (k <= 0) return;
-  gemv_n_k<<<std::min(div_up(n, 256), 148 * 8), 256, sizeof(double) * k, stream>>>(V, k, n, h, r);
+  gemv_n_k<<<std::min(div_up(n, 256), 148 * 8), 256, sizeof(double) * k, stream>>>(V, k, n, n, h, r);
   ++launches;
 }
 

@@ -245,6 +245,12 @@ struct OperatorEngine {
   // Block Krylov-Schur (bs <= 8 vectors, column j at V + j 2n):
   // R[:, j] = L(s)^{-1} B V[:, j] through the multi-RHS sweeps
   void apply_block(const double* V, int bs, double* R);
+  // Wl[:, j] = M R_l[:, j] for the w block members (R: 2n columns at stride 2n; Wl: n x w, ld n)
+  void mspmv_block(const double* R, int w, double* Wl);
+  // r[e] -= sum_{i<k} V[i ldv + e] h[i] for e < len
+  void gemv_n_len(const double* V, int k, int64_t ldv, int64_t len, const double* h, double* r);
+  // beta = ||r||_B from the tracked wl = M r_l; v_next = r / beta, bv_next = [r_u; wl] / beta
+  void bnorm_normalize_w(const double* r, const double* wl, double* beta_out, double* v_next, double* bv_next);
   // allocate what apply_block / gemm_t need for bases up to kmax vectors (outside graph captures)
   void prepare_block(int kmax, int bs);
   // H[i + j ldh] = V[:, i] . R[:, j] for i < k, j < bs (deterministic two-stage reduction)

@@ -143,6 +143,7 @@ struct EigWorkspace {
   int64_t n2 = 0;
   DeviceBuffer dV, dV2, dBV, dBV2, dR, dW, dHa, dHb, dBeta, dQ, dX, dRes;
   DeviceBuffer dHc, dHd, dBeta2;  // block mode: second intra-block sub-passes, R2 diagonal
+  DeviceBuffer dWl;               // block mode: tracked M r_l of the block members (n x bs)
   Pinned ha, hb, betas;
   Pinned hc, hd, betas2;
   Pinned hv, hq, hy;  // staging of the host -> device copies (start vectors, restart Q, Ritz Y)
@@ -170,6 +171,7 @@ struct EigWorkspace {
       dHc.alloc(sizeof(double) * (m + bs) * (m + bs));
       dHd.alloc(sizeof(double) * (m + bs) * (m + bs));
       dBeta2.alloc(sizeof(double) * (m + bs));
+      dWl.alloc(sizeof(double) * (n2_ / 2) * bs);
     }
     dQ.alloc(sizeof(double) * (m + 1) * (2 * m + 2));
     dX.alloc(sizeof(double) * n2 * 2 * (m + 1));
@@ -358,18 +360,23 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
           double* Vn = V + static_cast<int64_t>(kt) * n2;
           double* hC = dHc.as<double>() + static_cast<int64_t>(j) * LDH;
           double* hD = dHd.as<double>() + static_cast<int64_t>(j) * LDH;
+          // intra-block CGS2 with the members' M r_l tracked alongside (one
+          // block SpMV per pass instead of one M-product per member: B r_b is
+          // updated with the stored B-images of the earlier members)
+          double* Wl = W.dWl.as<double>();
           auto intra = [&](double* src, double* h1, double* h2, double* beta) {
+            op.mspmv_block(src, w, Wl);
             for (int b = 0; b < w; ++b) {
               double* rb = src + static_cast<int64_t>(b) * n2;
-              if (b > 0) {
-                double* h1b = h1 + kt + static_cast<int64_t>(b) * LDH;
-                double* h2b = h2 + kt + static_cast<int64_t>(b) * LDH;
-                op.gemv_t(BVn, b, rb, h1b);
-                op.gemv_n(Vn, b, h1b, rb, nullptr);
-                op.gemv_t(BVn, b, rb, h2b);
-                op.gemv_n(Vn, b, h2b, rb, nullptr);
-              }
-              op.bnorm_normalize_b(rb, beta + b, Vn + static_cast<int64_t>(b) * n2, BVn + static_cast<int64_t>(b) * n2);
+              double* wlb = Wl + static_cast<int64_t>(b) * (n2 / 2);
+              if (b > 0)
+                for (double* hh : {h1 + kt + static_cast<int64_t>(b) * LDH, h2 + kt + static_cast<int64_t>(b) * LDH}) {
+                  op.gemv_t(BVn, b, rb, hh);
+                  op.gemv_n(Vn, b, hh, rb, nullptr);
+                  op.gemv_n_len(BVn + n2 / 2, b, n2, n2 / 2, hh, wlb);
+                }
+              op.bnorm_normalize_w(rb, wlb, beta + b, Vn + static_cast<int64_t>(b) * n2,
+                                   BVn + static_cast<int64_t>(b) * n2);
             }
           };
           op.gemm_t(BV, kt, r, w, hA, LDH);
