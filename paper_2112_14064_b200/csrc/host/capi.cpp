@@ -351,6 +351,7 @@ int rq_factor_refactor(rq_factor_t* f, const double* aval) {
   return guarded([&] {
     need(f, "factor");
     need(aval, "aval");
+    if (f->n_complex >= 0) rqb::fail(rqb::errc::config, "complex factorization: use rq_factor_refactor_complex");
     std::lock_guard<std::mutex> lock(f->fe->mu);
     f->fe->set_values(aval);
     f->fe->factor();
@@ -368,7 +369,22 @@ int rq_factor_get_info(const rq_factor_t* f, rq_factor_info* o) {
   });
 }
 
+namespace {
+int factor_solve_impl(rq_factor_t* f, const double* b, double* x, int nrhs, int block);
+}
+
 int rq_factor_solve_ex(rq_factor_t* f, const double* b, double* x, int nrhs, int block) {
+  const int rc = guarded([&] {
+    need(f, "factor");
+    if (f->n_complex >= 0)
+      rqb::fail(rqb::errc::config, "complex factorization: use rq_factor_solve_complex (interleaved vectors of n)");
+  });
+  if (rc != 0) return rc;
+  return factor_solve_impl(f, b, x, nrhs, block);
+}
+
+namespace {
+int factor_solve_impl(rq_factor_t* f, const double* b, double* x, int nrhs, int block) {
   return guarded([&] {
     need(f, "factor");
     need(b, "b");
@@ -399,6 +415,8 @@ int rq_factor_solve_ex(rq_factor_t* f, const double* b, double* x, int nrhs, int
   });
 }
 
+}  // namespace
+
 int rq_factor_solve_complex(rq_factor_t* f, const double* b, double* x, int nrhs) {
   const int rc = guarded([&] {
     need(f, "factor");
@@ -406,7 +424,7 @@ int rq_factor_solve_complex(rq_factor_t* f, const double* b, double* x, int nrhs
   });
   if (rc != 0) return rc;
   // interleaved {re, im} vectors are exactly the real-equivalent unknowns
-  return rq_factor_solve_ex(f, b, x, nrhs, nrhs > 1 ? 8 : 1);
+  return factor_solve_impl(f, b, x, nrhs, nrhs > 1 ? 8 : 1);
 }
 
 int rq_factor_solve(rq_factor_t* f, const double* b, double* x, int nrhs) {

@@ -517,6 +517,10 @@ def test_complex_shift_factor_solve_vs_oracle(name):
     of = oracle.Factor(P.n, P.rowptr, P.col, Qv, P.box, P.elems)
     xo = of.solve(b)
     assert np.max(np.abs(x - xo)) <= 1e-9 * np.max(np.abs(xo))
+    # the real entry points refuse a complex factorization (their buffers are n, not 2n)
+    with pytest.raises(rq.RqError) as e:
+        rq.sparsela._lib.check(rq.sparsela._lib.lib.rq_factor_solve_ex(f._h, np.zeros(2 * P.n), np.zeros(2 * P.n), 1, 1))
+    assert e.value.code == 2
     # several right-hand sides at once (multi-RHS sweeps over the 2n system)
     B = rng.standard_normal((P.n, 3)) + 1j * rng.standard_normal((P.n, 3))
     X = f.solve(B)
