@@ -363,6 +363,26 @@ int rq_gh_run(rq_gh_t* h, const rq_gh_opts* opts, double* lam, double* resid, do
 void rq_gh_destroy(rq_gh_t* h);
 
 /* ------------------------------------------------------------------------ */
+/* Complex pencils / complex shifts (SPEC.md:408-470 over complex scalars;  */
+/* SURVEY.md §8 f4; the conductive EM pencil has C = -i sigma M_sigma):     */
+/* K, C, M complex on one pattern (interleaved {re, im} per entry), complex */
+/* shift s. Q(s) is factored on the GPU as its real-equivalent 2n system    */
+/* (s2: ordering of the 2n unknowns, rq_nd_order over the boxes repeated    */
+/* per (Re, Im) pair); complex Krylov-Schur with conjugated CGS2            */
+/* projections on the device, complex Schur form of H_m on the host.        */
+/* ------------------------------------------------------------------------ */
+typedef struct rq_zeig rq_zeig_t;
+int rq_zeig_create(const rq_symbolic_t* s2, int64_t n, const int64_t* rowptr, const int32_t* col, const double* K_c,
+                   const double* C_c, const double* M_c, double s_re, double s_im, rq_zeig_t** out);
+/* nev pairs nearest s: lam_c (interleaved, double[2 nev]), resid (double[nev]:
+ * ||Q(lam) u|| / ((||K||_1 + |lam| ||C||_1 + |lam|^2 ||M||_1) ||u||)), vec_c (n x
+ * nev complex, interleaved, may be NULL), stats {cycles, nconv}. Non-convergence
+ * -> RQ_E_SOLVER. */
+int rq_zeig_run(rq_zeig_t* h, int nev, int m, double tol, uint64_t seed, int max_restarts, double* lam_c,
+                double* resid, double* vec_c, int32_t* stats);
+void rq_zeig_destroy(rq_zeig_t* h);
+
+/* ------------------------------------------------------------------------ */
 /* Wire formats (reference sparse.cpp:121-174,         */
 /* SPEC.md:269, 371, 503). Host only.                                       */
 /* ------------------------------------------------------------------------ */

@@ -177,6 +177,10 @@ _sig("rq_operator_krylov_schur_restart", C.c_int, vp, C.c_int, C.c_int, f64p, f6
 _sig("rq_gh_create", C.c_int, C.c_int64, i64p, i32p, f64p, f64p, vp, C.c_double, C.POINTER(vp))
 _sig("rq_gh_run", C.c_int, vp, C.POINTER(GhOpts), f64p, f64p, vp, C.POINTER(GhInfo))
 _sig("rq_gh_destroy", None, vp)
+_sig("rq_zeig_create", C.c_int, vp, C.c_int64, i64p, i32p, f64p, f64p, f64p, C.c_double, C.c_double,
+     C.POINTER(vp))
+_sig("rq_zeig_run", C.c_int, vp, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int, f64p, f64p, vp, i32p)
+_sig("rq_zeig_destroy", None, vp)
 
 # every symbol include/rq_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = [
@@ -195,7 +199,7 @@ EXPORTS = [
     "rq_operator_time",
     "rq_eigs_run", "rq_eigs_ledger_json", "rq_operator_ledger", "rq_operator_ledger_json", "rq_operator_release_workspace",
     "rq_operator_ledger_reset", "rq_scale_pencil", "rq_ritz_extract", "rq_operator_krylov_schur_restart",
-    "rq_gh_create", "rq_gh_run", "rq_gh_destroy",
+    "rq_gh_create", "rq_gh_run", "rq_gh_destroy", "rq_zeig_create", "rq_zeig_run", "rq_zeig_destroy",
 ]
 
 

@@ -18,6 +18,7 @@
 #include "io.hpp"
 #include "eigs.hpp"
 #include "lanczos.hpp"
+#include "zeigs.hpp"
 #include "dense.hpp"
 
 struct rq_pencil {
@@ -1120,3 +1121,80 @@ int rq_gh_run(rq_gh_t* h, const rq_gh_opts* opts, double* lam, double* resid, do
 }
 
 void rq_gh_destroy(rq_gh_t* h) { delete h; }
+
+// ---------------------------------------------------------------------------
+// complex pencils / complex shifts
+struct rq_zeig {
+  std::unique_ptr<rqb::ZOperatorEngine> E;
+  double norms1[3] = {0, 0, 0};
+};
+
+int rq_zeig_create(const rq_symbolic_t* s2, int64_t n, const int64_t* rowptr, const int32_t* col, const double* K_c,
+                   const double* C_c, const double* M_c, double s_re, double s_im, rq_zeig_t** out) {
+  return guarded([&] {
+    need(s2, "symbolic");
+    need(rowptr, "rowptr");
+    need(col, "col");
+    need(K_c, "K");
+    need(C_c, "C");
+    need(M_c, "M");
+    need(out, "out");
+    if (2 * n != s2->S.n) rqb::fail(rqb::errc::dimension, "the ordering must cover the 2n real-equivalent unknowns");
+    if (!std::isfinite(s_re) || !std::isfinite(s_im)) rqb::fail(rqb::errc::config, "shift must be finite");
+    const int64_t nnz = rowptr[n];
+    std::vector<double> qre(nnz), qim(nnz);
+    const std::complex<double> sc(s_re, s_im);
+    for (int64_t k = 0; k < nnz; ++k) {
+      const std::complex<double> kk(K_c[2 * k], K_c[2 * k + 1]), cc(C_c[2 * k], C_c[2 * k + 1]),
+          mm(M_c[2 * k], M_c[2 * k + 1]);
+      const std::complex<double> q = kk + sc * cc + sc * sc * mm;
+      qre[k] = q.real();
+      qim[k] = q.imag();
+    }
+    std::vector<int64_t> rp2;
+    std::vector<int32_t> col2;
+    std::vector<double> v2;
+    complex_equivalent(n, rowptr, col, qre.data(), qim.data(), rp2, col2, v2);
+    auto h = std::make_unique<rq_zeig>();
+    h->E = std::make_unique<rqb::ZOperatorEngine>(n, rowptr, col, K_c, C_c, M_c, s2->S, s_re, s_im, rp2, col2, v2);
+    const double* mats[3] = {K_c, C_c, M_c};
+    for (int w = 0; w < 3; ++w) {  // 1-norms (max column sum of |a|; sparse.cpp:38-45)
+      std::vector<double> cs(n, 0.0);
+      for (int64_t r = 0; r < n; ++r)
+        for (int64_t k = rowptr[r]; k < rowptr[r + 1]; ++k) cs[col[k]] += std::hypot(mats[w][2 * k], mats[w][2 * k + 1]);
+      h->norms1[w] = cs.empty() ? 0.0 : *std::max_element(cs.begin(), cs.end());
+    }
+    *out = h.release();
+  });
+}
+
+int rq_zeig_run(rq_zeig_t* h, int nev, int m, double tol, uint64_t seed, int max_restarts, double* lam_c,
+                double* resid, double* vec_c, int32_t* stats) {
+  return guarded([&] {
+    need(h, "handle");
+    need(lam_c, "lam");
+    need(resid, "resid");
+    std::lock_guard<std::mutex> lock(h->E->fac->mu);
+    rqb::ZEigsOptions o;
+    o.nev = nev;
+    o.m = m;
+    o.tol = tol;
+    o.seed = seed;
+    o.max_restarts = max_restarts > 0 ? max_restarts : 100;
+    o.want_vectors = vec_c ? 1 : 0;
+    const rqb::ZEigsResult r = rqb::solve_quadratic_complex(*h->E, o, h->norms1);
+    for (int i = 0; i < nev; ++i) {
+      const bool have = i < static_cast<int>(r.lambda.size());
+      lam_c[2 * i] = have ? r.lambda[i].real() : 0.0;
+      lam_c[2 * i + 1] = have ? r.lambda[i].imag() : 0.0;
+      resid[i] = have ? r.resid[i] : 1.0;
+    }
+    if (vec_c && !r.vec.empty()) std::memcpy(vec_c, r.vec.data(), sizeof(double) * r.vec.size());
+    if (stats) stats[0] = r.cycles, stats[1] = r.nconv;
+    if (!r.converged)
+      rqb::fail(rqb::errc::solver, "complex solve_quadratic: only " + std::to_string(r.nconv) +
+                                       " pairs converged within max_restarts");
+  });
+}
+
+void rq_zeig_destroy(rq_zeig_t* h) { delete h; }

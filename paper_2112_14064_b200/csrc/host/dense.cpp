@@ -4,15 +4,21 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
-
+#include <thread>
+#ifdef _OPENMP
 #include <omp.h>
+#endif
 
 #include "common.hpp"
 
 namespace rqb {
 
 int host_threads() {
+#ifdef _OPENMP
   static const int t = std::max(1, std::min(8, omp_get_num_procs() / 2));
+#else
+  static const int t = 1;
+#endif
   return t;
 }
 
@@ -305,6 +311,87 @@ bool complex_schur(const std::vector<double>& A, int n, CMat& T, CMat& Z) {
     T(k + 1, k) = 0.0;
     ++k;
   }
+  return true;
+}
+
+bool complex_schur_c(const CMat& A, CMat& T, CMat& Z) {
+  const int n = A.n;
+  T = A;
+  Z = CMat(n);
+  for (int i = 0; i < n; ++i) Z(i, i) = 1.0;
+  // Householder reduction to upper Hessenberg form: T <- H T H^H, Z <- Z H^H
+  std::vector<cplx> v(n);
+  for (int k = 0; k + 2 < n; ++k) {
+    double xn2 = 0.0;
+    for (int i = k + 1; i < n; ++i) xn2 += std::norm(T(i, k));
+    if (xn2 == 0.0) continue;
+    const double xn = std::sqrt(xn2);
+    const cplx x0 = T(k + 1, k);
+    const cplx ph = std::abs(x0) > 0.0 ? x0 / std::abs(x0) : cplx(1.0);
+    const cplx alpha = -ph * xn;
+    for (int i = k + 1; i < n; ++i) v[i] = T(i, k);
+    v[k + 1] -= alpha;
+    double vn2 = 0.0;
+    for (int i = k + 1; i < n; ++i) vn2 += std::norm(v[i]);
+    if (vn2 == 0.0) continue;
+    const double tau = 2.0 / vn2;
+    for (int j = k; j < n; ++j) {  // left: rows k+1.. of columns k..n-1
+      cplx w = 0.0;
+      for (int i = k + 1; i < n; ++i) w += std::conj(v[i]) * T(i, j);
+      w *= tau;
+      for (int i = k + 1; i < n; ++i) T(i, j) -= v[i] * w;
+    }
+    for (CMat* M : {&T, &Z}) {  // right: columns k+1.. (all rows)
+      for (int i = 0; i < n; ++i) {
+        cplx w = 0.0;
+        for (int j = k + 1; j < n; ++j) w += (*M)(i, j) * v[j];
+        w *= tau;
+        for (int j = k + 1; j < n; ++j) (*M)(i, j) -= w * std::conj(v[j]);
+      }
+    }
+    for (int i = k + 2; i < n; ++i) T(i, k) = 0.0;
+  }
+  // single-shift QR with Wilkinson shifts (complex Givens), deflation at
+  // eps (|t_{l-1,l-1}| + |t_{l,l}|), an exceptional shift every 10 iterations
+  const double eps = std::numeric_limits<double>::epsilon();
+  int hi = n - 1, its = 0, total = 0;
+  while (hi > 0) {
+    int l = hi;
+    for (; l > 0; --l)
+      if (std::abs(T(l, l - 1)) <= eps * (std::abs(T(l - 1, l - 1)) + std::abs(T(l, l)))) {
+        T(l, l - 1) = 0.0;
+        break;
+      }
+    if (l == hi) {
+      --hi;
+      its = 0;
+      continue;
+    }
+    if (++total > 30 * n) return false;
+    ++its;
+    cplx mu;
+    const cplx a = T(hi - 1, hi - 1), b = T(hi - 1, hi), c = T(hi, hi - 1), d = T(hi, hi);
+    if (its % 10 == 0) {
+      mu = d + std::abs(c);
+    } else {
+      const cplx tr2 = 0.5 * (a + d), dsc = std::sqrt(0.25 * (a - d) * (a - d) + b * c);
+      mu = std::abs(tr2 + dsc - d) < std::abs(tr2 - dsc - d) ? tr2 + dsc : tr2 - dsc;
+    }
+    for (int k = l; k < hi; ++k) {
+      double cs;
+      cplx sn;
+      if (k == l)
+        givens(T(l, l) - mu, T(l + 1, l), cs, sn);
+      else
+        givens(T(k, k - 1), T(k + 1, k - 1), cs, sn);
+      rot_rows(T, k, k == l ? l : k - 1, n, cs, sn);
+      if (k > l) T(k + 1, k - 1) = 0.0;
+      rot_cols(T, k, 0, std::min(k + 3, hi + 1), cs, sn);
+      rot_cols(Z, k, 0, n, cs, sn);
+    }
+  }
+  for (int j = 0; j < n; ++j)
+    for (int i = j + 1; i < n; ++i) T(i, j) = 0.0;
   return true;
 }
 

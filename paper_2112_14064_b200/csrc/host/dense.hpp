@@ -28,6 +28,10 @@ struct CMat {
 // within 30 n iterations per eigenvalue.
 bool complex_schur(const std::vector<double>& A, int n, CMat& T, CMat& Z);
 
+// A = Z T Z^H for a complex A (Householder Hessenberg + single-shift complex
+// QR with Wilkinson shifts). Returns false past 30 n iterations.
+bool complex_schur_c(const CMat& A, CMat& T, CMat& Z);
+
 // Move the selected diagonal entries of T to the leading positions (stable
 // order), updating Z. sel is permuted alongside.
 void schur_reorder(CMat& T, CMat& Z, std::vector<int>& sel);

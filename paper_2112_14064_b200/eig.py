@@ -309,3 +309,49 @@ def solve_generalized_hermitian(A, B, s: float, nev: int, m: int = 0, eps: float
     solve_generalized_hermitian.last_info = solver.last_info
     return pairs
 
+
+
+def solve_quadratic_complex(pencil, s: complex, nev: int, m: int = 0, eps: float = 1e-10, seed: int = 0,
+                            max_restarts: int = 100, vectors: bool = False, K=None, C=None, M=None):
+    """solve_quadratic for complex pencils and complex shifts (SURVEY.md
+    §8 f4): K, C, M (default: the pencil's; any may be complex, e.g. the conductive
+    EM damping C = -i sigma M_sigma) on the pencil's pattern, complex shift s. Q(s)
+    is factored on the GPU as its real-equivalent 2n system; complex Krylov-Schur
+    on the device. Returns EigenPair list (lam complex, residual, u complex)."""
+    n = int(pencil.n)
+    K = pencil.K if K is None else K
+    C = pencil.C if C is None else C
+    M = pencil.M if M is None else M
+
+    def inter(a):
+        a = np.asarray(a, np.complex128)
+        return np.ascontiguousarray(np.stack([a.real, a.imag], 1).reshape(-1))
+    Kc, Cc, Mc = inter(K), inter(C), inter(M)
+    nnz = int(pencil.rowptr[-1])
+    if Kc.size != 2 * nnz or Cc.size != 2 * nnz or Mc.size != 2 * nnz:
+        raise RqError(7, "K, C, M must live on the pencil's pattern")
+    o2 = Ordering(2 * n, np.repeat(np.asarray(pencil.box).reshape(-1, 4), 2, axis=0), pencil.elems)
+    import ctypes  # (C is the damping matrix in this function)
+    hh = ctypes.c_void_p()
+    s = complex(s)
+    check(_lib.lib.rq_zeig_create(o2.handle, n, np.ascontiguousarray(pencil.rowptr, np.int64),
+                                  np.ascontiguousarray(pencil.col, np.int32), Kc, Cc, Mc, s.real, s.imag,
+                                  ctypes.byref(hh)))
+    try:
+        lam = np.zeros(2 * nev)
+        res = np.ones(nev)
+        vec = np.zeros(2 * n * nev) if vectors else None
+        st = np.zeros(2, np.int32)
+        rc = _lib.lib.rq_zeig_run(hh, int(nev), int(m), float(eps), int(seed), int(max_restarts), lam, res,
+                                  _lib.ptr(vec), st)
+        solve_quadratic_complex.last_info = {"cycles": int(st[0]), "nconv": int(st[1])}
+        check(rc)
+    finally:
+        _lib.lib.rq_zeig_destroy(hh)
+    out = []
+    for i in range(nev):
+        u = None
+        if vectors:
+            u = vec[2 * n * i:2 * n * (i + 1)].view(np.complex128).copy()
+        out.append(EigenPair(complex(lam[2 * i], lam[2 * i + 1]), float(res[i]), u))
+    return out

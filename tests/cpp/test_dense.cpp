@@ -106,5 +106,28 @@ int main() {
                 inv, ok ? "ok" : "FAIL");
     fails += !ok;
   }
+    // complex input (complex_schur_c): random complex matrices
+  for (int n : {1, 2, 7, 40, 121}) {
+    CMat A(n);
+    for (auto& z : A.a) z = cplx(N(g), N(g));
+    CMat T, Z;
+    if (!complex_schur_c(A, T, Z)) { std::printf("zqr fail n=%d\n", n); return 1; }
+    double d = 0, u = 0, l = 0, an = 0;
+    for (const auto& z : A.a) an = std::max(an, std::abs(z));
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        cplx sacc = 0, zz = 0;
+        for (int a = 0; a < n; ++a) {
+          zz += std::conj(Z(a, i)) * Z(a, j);
+          for (int b2 = a; b2 < n; ++b2) sacc += Z(i, a) * T(a, b2) * std::conj(Z(j, b2));
+        }
+        d = std::max(d, std::abs(sacc - A(i, j)));
+        u = std::max(u, std::abs(zz - (i == j ? 1.0 : 0.0)));
+        if (i > j) l = std::max(l, std::abs(T(i, j)));
+      }
+    const bool ok = d <= 1e-12 * std::max(1.0, an) * n && u <= 1e-12 * n && l == 0.0;
+    std::printf("complex n=%d defect %.2e unitarity %.2e %s\n", n, d, u, ok ? "zok" : "zFAIL");
+    if (!ok) ++fails;
+  }
   return fails;
 }

@@ -16,3 +16,4 @@ def test_dense_kernels(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout
     assert r.stdout.count(" ok") == 7  # 5 random + 2 degenerate-cluster matrices
+    assert r.stdout.count("zok") == 5  # complex_schur_c on random complex matrices
