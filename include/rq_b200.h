@@ -80,6 +80,14 @@ int rq_pencil_assemble(const rq_space_desc* desc, rq_pencil_t** out);
  * C = int_GA beta (u.n)(v.n), M = int rho u.v; all real. Host assembly. */
 int rq_pencil_assemble_acoustic(int degree, int elems, int levels, double rho, double c, double alpha, double beta,
                                 int absorbing_edges, rq_pencil_t** out);
+/* The paper's conductive electromagnetic pencil (assemble_em, SPEC.md:216-224;
+ * PAPER.md §2.1): H(curl) space of `degree` on the unit square, E x n = 0; K =
+ * int curl u (-1/mu) curl v, M = int eps u.v, C = -i D with D = int u . diag(
+ * sigma_x(y), sigma_y(y)) v over nlayers horizontal layers (layers: nlayers x
+ * {y0, y1, sigma_x, sigma_y}). The handle's C slot holds D (real); D_out (nnz,
+ * nullable) receives a copy. Solve with rq_zeig_* (C = -i D is complex). */
+int rq_pencil_assemble_em(int degree, int elems, int levels, double mu, double eps, int nlayers, const double* layers,
+                          double* D_out, rq_pencil_t** out);
 /* The same pencil, bit for bit, assembled on the current CUDA device
  * (pattern, per-element Gauss quadrature, colour-ordered
  * gather; no atomics). resident = 1 keeps K, C, M in device memory only

@@ -118,6 +118,8 @@ _sig("rq_set_device", C.c_int, C.c_int)
 _sig("rq_pencil_assemble", C.c_int, C.POINTER(SpaceDesc), C.POINTER(vp))
 _sig("rq_pencil_assemble_acoustic", C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
      C.c_double, C.c_int, C.POINTER(vp))
+_sig("rq_pencil_assemble_em", C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, vp, vp,
+     C.POINTER(vp))
 _sig("rq_pencil_assemble_device", C.c_int, C.POINTER(SpaceDesc), C.c_int, C.POINTER(vp), f64p)
 _sig("rq_pencil_dims", C.c_int, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64))
 _sig("rq_pencil_csr", C.c_int, vp, i64n, i32n, f64n, f64n, f64n)
@@ -185,7 +187,7 @@ _sig("rq_zeig_destroy", None, vp)
 # every symbol include/rq_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = [
     "rq_last_error", "rq_version", "rq_set_device", "rq_pencil_assemble", "rq_pencil_assemble_device",
-    "rq_pencil_assemble_acoustic",
+    "rq_pencil_assemble_acoustic", "rq_pencil_assemble_em",
     "rq_pencil_dims", "rq_pencil_csr",
     "rq_pencil_supports", "rq_pencil_destroy", "rq_space_dims", "rq_space_boundary_mask",
     "rq_nd_order", "rq_symbolic_stats_get", "rq_symbolic_perm", "rq_symbolic_fronts",

@@ -122,6 +122,23 @@ int rq_pencil_assemble_acoustic(int degree, int elems, int levels, double rho, d
   });
 }
 
+int rq_pencil_assemble_em(int degree, int elems, int levels, double mu, double eps, int nlayers, const double* layers,
+                          double* D_out, rq_pencil_t** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (nlayers < 0 || (nlayers > 0 && !layers)) rqb::fail(rqb::errc::config, "layers");
+    std::vector<rqb::EmLayer> L;
+    for (int i = 0; i < nlayers; ++i) L.push_back({layers[4 * i], layers[4 * i + 1], layers[4 * i + 2], layers[4 * i + 3]});
+    const rqb::VectorSpace vs = rqb::build_space(rqb::SpaceKind::curl, degree, elems, levels);
+    auto p = std::make_unique<rq_pencil>();
+    std::vector<double> D;
+    p->P = rqb::assemble_em(vs, mu, eps, L, &D);
+    if (D_out) std::memcpy(D_out, D.data(), sizeof(double) * D.size());
+    p->P.C = D;  // the pencil handle carries D in its C slot (C = -i D)
+    *out = p.release();
+  });
+}
+
 int rq_pencil_assemble_device(const rq_space_desc* desc, int resident, rq_pencil_t** out, double* ms) {
   return guarded([&] {
     need(out, "out");

@@ -92,6 +92,14 @@ Pencil assemble_pencil(const VectorSpace& vs, double alpha, double beta, const s
 // edges constrained, absorbing edges (bit mask: left 1, right 2, bottom 4, top
 // 8) carry the impedance terms alpha / beta.
 Pencil assemble_acoustic(const VectorSpace& vs, double rho, double c, double alpha, double beta, int absorbing);
+// The paper's conductive electromagnetic pencil: K = -(1/mu)
+// curl-curl, M = eps mass, C = -i D with D the layer-weighted mass (sigma_x on
+// the x-component, sigma_y on the y-component); P.C = 0, D returned.
+struct EmLayer {
+  double y0, y1, sx, sy;
+};
+Pencil assemble_em(const VectorSpace& vs, double mu, double eps, const std::vector<EmLayer>& layers,
+                   std::vector<double>* D);
 
 // Pieces shared by the host assembler and the device one (cuda/assembly.cu).
 // Free numbering: full_to_free[g] = free id or -1 (constrained), free_to_full.

@@ -528,4 +528,79 @@ Pencil assemble_acoustic(const VectorSpace& vs, double rho, double c, double alp
   return P;
 }
 
+
+// The paper's conductive electromagnetic pencil (§2.1; SPEC.md:216-224,
+// assemble_em): H(curl) space with E x n = 0, K = int curl u (-1/mu) curl v,
+// M = int eps u.v, C = int u . (-i sigma) v with sigma = diag(sigma_x(y),
+// sigma_y(y)) piecewise constant over horizontal layers; returned as real K, M
+// and the real D with C = -i D (the pencil is complex through C only).
+Pencil assemble_em(const VectorSpace& vs, double mu, double eps, const std::vector<EmLayer>& layers,
+                   std::vector<double>* D_out) {
+  if (vs.kind != SpaceKind::curl) fail(errc::domain, "the electromagnetic problem lives in H(curl)");
+  if (!(mu > 0 && eps > 0)) fail(errc::domain, "mu and eps must be positive");
+  for (const EmLayer& L : layers)
+    if (!(L.y1 > L.y0) || L.sx < 0 || L.sy < 0) fail(errc::domain, "layers: y0 < y1, sigma >= 0");
+  std::vector<int64_t> full_to_free;
+  Pencil P = assemble_pencil(vs, 0.0, 0.0, nullptr, &full_to_free);
+  const int64_t nnz = P.rowptr[P.n];
+  for (int64_t k = 0; k < nnz; ++k) {
+    P.K[k] = -(P.K[k] - P.M[k]) / mu;  // the BASELINE K carries curl-curl + u.v
+    P.M[k] = eps * P.M[k];
+    P.C[k] = 0.0;
+  }
+  std::vector<double>& D = *D_out;
+  D.assign(nnz, 0.0);
+  const int nq = vs.degree + 1, ne = vs.elems;
+  QuadTable tab[2][2];
+  quad_tables(vs, tab);
+  double gx[kMaxP + 1], gw[kMaxP + 1];
+  gauss_legendre(nq, gx, gw);
+  const Tensor2* comp[2] = {&vs.cx, &vs.cy};
+  const int64_t base[2] = {0, vs.Nx()};
+  auto sigma_at = [&](double y, int c) {
+    for (const EmLayer& L : layers)
+      if (y >= L.y0 && y < L.y1) return c == 0 ? L.sx : L.sy;
+    return 0.0;
+  };
+  std::vector<int64_t> dof;
+  std::vector<double> vals;
+  for (int ey = 0; ey < ne; ++ey)
+    for (int ex = 0; ex < ne; ++ex)
+      for (int c = 0; c < 2; ++c) {
+        const QuadTable& TX = tab[c][0];
+        const QuadTable& TY = tab[c][1];
+        const int fx = comp[c]->sx.first_basis(ex), fy = comp[c]->sy.first_basis(ey);
+        dof.clear();
+        for (int b = 0; b <= TY.p; ++b)
+          for (int a = 0; a <= TX.p; ++a)
+            dof.push_back(full_to_free[base[c] + static_cast<int64_t>(fy + b) * comp[c]->nx() + fx + a]);
+        const int nl = static_cast<int>(dof.size());
+        for (int qy = 0; qy < nq; ++qy) {
+          const double y = (ey + 0.5 * (gx[qy] + 1.0)) / ne;
+          const double sg = sigma_at(y, c);
+          if (sg == 0.0) continue;
+          for (int qx = 0; qx < nq; ++qx) {
+            const double w = TX.w(ex, qx) * TY.w(ey, qy) * sg;
+            vals.assign(nl, 0.0);
+            const double* vx = TX.v(ex, qx);
+            const double* vy = TY.v(ey, qy);
+            for (int b = 0, o = 0; b <= TY.p; ++b)
+              for (int a = 0; a <= TX.p; ++a, ++o) vals[o] = vx[a] * vy[b];
+            for (int r = 0; r < nl; ++r) {
+              if (dof[r] < 0) continue;
+              const int32_t* cb = P.col.data() + P.rowptr[dof[r]];
+              const int32_t* ce = P.col.data() + P.rowptr[dof[r] + 1];
+              for (int q = 0; q < nl; ++q) {
+                if (dof[q] < 0) continue;
+                const int32_t* it = std::lower_bound(cb, ce, static_cast<int32_t>(dof[q]));
+                if (it == ce || *it != dof[q]) fail(errc::assembly, "pattern misses an element pair");
+                D[it - P.col.data()] += w * vals[r] * vals[q];
+              }
+            }
+          }
+        }
+      }
+  return P;
+}
+
 }  // namespace rqb

@@ -197,6 +197,35 @@ def assemble_acoustic(degree: int, elems: int, levels: int = 0, rho: float = 1.0
                            box.reshape(-1, 4), f2f, 0.0, 0.0)
 
 
+def assemble_em(degree: int, elems: int, levels: int = 0, mu: float = 1.0, eps: float = 1.0,
+                layers=((0.0, 1.0, 1.0, 1.0),)) -> QuadraticPencil:
+    """The paper's conductive electromagnetic pencil (SPEC.md:216-224 assemble_em;
+    PAPER.md §2.1): K = -(1/mu) curl-curl, M = eps mass, C = -i D with D the
+    conductivity-weighted mass over horizontal layers (y0, y1, sigma_x, sigma_y).
+    The returned pencil's C is complex (purely imaginary): solve it with
+    solve_quadratic_complex."""
+    lay = np.ascontiguousarray(np.asarray(layers, np.float64).reshape(-1, 4))
+    h = C.c_void_p()
+    check(_lib.lib.rq_pencil_assemble_em(int(degree), int(elems), int(levels), float(mu), float(eps), len(lay),
+                                         _lib.ptr(lay.reshape(-1)), None, C.byref(h)))
+    try:
+        nf, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        check(_lib.lib.rq_pencil_dims(h, C.byref(nf), C.byref(n), C.byref(nnz)))
+        rowptr = np.zeros(n.value + 1, np.int64)
+        col = np.zeros(nnz.value, np.int32)
+        K = np.zeros(nnz.value)
+        D = np.zeros(nnz.value)
+        M = np.zeros(nnz.value)
+        check(_lib.lib.rq_pencil_csr(h, rowptr, col, K, D, M))
+        box = np.zeros(4 * n.value, np.int32)
+        f2f = np.zeros(n.value, np.int64)
+        check(_lib.lib.rq_pencil_supports(h, box, f2f))
+    finally:
+        _lib.lib.rq_pencil_destroy(h)
+    return QuadraticPencil(CURL, degree, elems, levels, nf.value, n.value, rowptr, col, K, -1j * D, M,
+                           box.reshape(-1, 4), f2f, 0.0, 0.0)
+
+
 def baseline_config(name: str, device: bool = False, resident: bool = False) -> QuadraticPencil:
     """The BASELINE.json configurations by short name."""
     table = {

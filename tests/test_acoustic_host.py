@@ -40,3 +40,19 @@ def test_acoustic_pencil_structure():
     assert P0.n == B.n and np.array_equal(P0.col, B.col)
     np.testing.assert_allclose(P0.M, RHO * B.M, rtol=0, atol=1e-15 * np.abs(B.M).max())
     np.testing.assert_allclose(P0.K, RHO * C * C * (B.K - B.M), rtol=0, atol=1e-12 * np.abs(P0.K).max())
+
+
+def test_em_pencil_structure():
+    """assemble_em (SPEC.md:216-224): K = -(1/mu) curl-curl, M = eps mass, C = -i D;
+    uniform conductivity -> D = sigma M; layered: D only weights the layers' rows
+    (sigma 0 above 0.5 -> D smaller than the uniform one), symmetric."""
+    B = rq.assemble(rq.CURL, 4, 8, 0)
+    P = rq.assemble_em(4, 8, mu=2.0, eps=3.0, layers=((0.0, 1.0, 2.0, 2.0),))
+    assert np.iscomplexobj(P.C) and np.all(P.C.real == 0)
+    np.testing.assert_allclose(P.K, -(B.K - B.M) / 2.0, rtol=0, atol=1e-14 * np.abs(B.K).max())
+    np.testing.assert_allclose(P.M, 3.0 * B.M, rtol=0, atol=1e-15 * np.abs(B.M).max())
+    np.testing.assert_allclose(-P.C.imag, 2.0 * B.M, rtol=0, atol=1e-14 * np.abs(B.M).max())
+    L = rq.assemble_em(4, 8, layers=((0.0, 0.5, 1.0, 3.0), (0.5, 1.0, 0.0, 0.0)))
+    Dd = -np.asarray(L.to_scipy("C").toarray()).imag
+    assert np.abs(Dd - Dd.T).max() <= 1e-15 * np.abs(Dd).max()
+    assert Dd.trace() < (3.0 * B.to_scipy("M")).diagonal().sum()

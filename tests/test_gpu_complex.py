@@ -84,3 +84,28 @@ def test_conductive_maxwell_closed_form():
     for x in lam:
         assert np.min(np.abs(pred - x)) <= 1e-8 * abs(x)
         assert np.min(np.abs(pred + np.conj(x))) <= 1e-8 * abs(x)  # -conj(lam) is an eigenvalue too
+
+
+def test_layered_conductive_em_vs_dense_qz_and_symmetry():
+    """The paper's conductive EM pencil with two conductivity layers (assemble_em):
+    the complex solver's eigenvalues nearest a complex shift equal dense QZ's,
+    and the spectrum is symmetric under lam -> -conj(lam) (solving
+    at -conj(s) returns the mirrored values)."""
+    from scipy.linalg import eigvals
+    P = rq.assemble_em(4, 8, layers=((0.0, 0.5, 1.0, 3.0), (0.5, 1.0, 0.2, 0.2)))
+    s = 9.0 + 0.8j
+    pairs = rq.solve_quadratic_complex(P, s, 4, m=24, eps=1e-10, max_restarts=300)
+    lam = np.array([p.lam for p in pairs])
+    assert max(p.residual for p in pairs) <= 1e-10
+    n = P.n
+    Kd, Cd, Md = (P.to_scipy(w).toarray() for w in "KCM")
+    Z, I = np.zeros((n, n)), np.eye(n)
+    w = eigvals(np.block([[Z, I], [-Kd, -Cd]]), np.block([[I, Z], [Z, Md]]))
+    w = w[np.isfinite(w)]
+    w = w[np.argsort(np.abs(w - s))][:4]
+    for x in lam:
+        assert np.min(np.abs(w - x)) <= 1e-8 * abs(x)
+    mirror = rq.solve_quadratic_complex(P, -np.conj(s), 4, m=24, eps=1e-10, max_restarts=300)
+    lm = np.array([p.lam for p in mirror])
+    for x in lam:
+        assert np.min(np.abs(lm + np.conj(x))) <= 1e-8 * abs(x)
