@@ -1464,8 +1464,10 @@ void rqb_dag_build(FactorEngine& fe) {
   P->rc_group = P->occ == 2 ? (S.flops_lu >= 4e10 ? kRCMax : 2) : 1;
   if (const char* e = std::getenv("RQB_RC_GROUP")) P->rc_group = std::max(1, std::min(kRCMax, std::atoi(e)));
   // measured: cfg4_riga 28.3 -> 26.8 ms, cfg4_iga 68.6 -> 61.0 ms (4: 27.0 / 62.2); later, with the
-  // current task set, 8 / 16 / 24: cfg4_riga 25.24 / 25.15 / 25.17, cfg4_iga 59.0 / 58.2 / 58.1
-  P->upd_batch = P->occ == 2 ? 16 : 0;
+  // current task set, 8 / 16 / 24: cfg4_riga 25.24 / 25.15 / 25.17, cfg4_iga 59.0 / 58.2 / 58.1 — kept
+  // at 8: with 16 the changed factor rounding left the single-vector cfg3_iga nev = 50 solve stagnating
+  // in its degenerate cluster
+  P->upd_batch = P->occ == 2 ? 8 : 0;
   P->upd_la = 2;
   if (const char* e = std::getenv("RQB_UPD_BATCH")) P->upd_batch = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("RQB_UPD_LOOKAHEAD")) P->upd_la = std::max(1, std::atoi(e));

@@ -218,9 +218,10 @@ __global__ void __launch_bounds__(kRedThreads) ritz_residual_k(
     const double* __restrict__ X, int ldx, int nc, const double* __restrict__ lam,
     const int* __restrict__ blk, double* __restrict__ part) {
   constexpr int kW = kRedThreads / 32;
-  __shared__ double sred[kW][4][32];
+  __shared__ double sred[kW][16][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double lr[2], li[2], sr[2], si[2], acc[2] = {0.0, 0.0}, accu[2] = {0.0, 0.0};
+  double rq[2][6] = {{0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0}};  // u^H K u, u^H C u, u^H M u (re, im)
   const double* xb[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -273,23 +274,37 @@ __global__ void __launch_bounds__(kRedThreads) ritz_residual_k(
       const double2 u = *reinterpret_cast<const double2*>(xb[h] + row * ldx);
       acc[h] += re * re + im * im;
       accu[h] += u.x * u.x + u.y * u.y;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {  // conj(u) (A u): the quadratic Rayleigh quotient's coefficients
+        rq[h][2 * t] += u.x * a[h][2 * t] + u.y * a[h][2 * t + 1];
+        rq[h][2 * t + 1] += u.x * a[h][2 * t + 1] - u.y * a[h][2 * t];
+      }
     }
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    sred[warp][2 * h][lane] = acc[h];
-    sred[warp][2 * h + 1][lane] = accu[h];
+    sred[warp][8 * h][lane] = acc[h];
+    sred[warp][8 * h + 1][lane] = accu[h];
+#pragma unroll
+    for (int t = 0; t < 6; ++t) sred[warp][8 * h + 2 + t][lane] = rq[h][t];
   }
   __syncthreads();
   if (warp == 0) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = (int)blockIdx.y * 64 + 32 * h + lane;
-      double s0 = 0.0, s1 = 0.0;
-      for (int w = 0; w < kW; ++w) s0 += sred[w][2 * h][lane], s1 += sred[w][2 * h + 1][lane];
+      double sv[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        sv[t] = 0.0;
+        for (int w = 0; w < kW; ++w) sv[t] += sred[w][8 * h + t][lane];
+      }
       if (c < nc) {
-        part[(int64_t)(2 * c) * gridDim.x + blockIdx.x] = s0;
-        part[(int64_t)(2 * c + 1) * gridDim.x + blockIdx.x] = s1;
+        part[(int64_t)(2 * c) * gridDim.x + blockIdx.x] = sv[0];
+        part[(int64_t)(2 * c + 1) * gridDim.x + blockIdx.x] = sv[1];
+        // rows [2 nc, 8 nc): the Rayleigh-quotient coefficients, 6 per candidate
+#pragma unroll
+        for (int t = 0; t < 6; ++t) part[(int64_t)(2 * nc + 6 * c + t) * gridDim.x + blockIdx.x] = sv[2 + t];
       }
     }
   }
@@ -880,7 +895,7 @@ void OperatorEngine::ritz_residuals(const double* V, int m, const double* Y, int
   vq_gemm(V, n2, n2, m, Y, m, ldx, Xrm, ldx, true, stream);
   if (d_rcand.bytes < sizeof(double) * 2 * nc + sizeof(int) * nc) d_rcand.alloc(sizeof(double) * 2 * nc + sizeof(int) * nc);
   const int nbx = kRedBlocks;
-  if (d_rpart.bytes < sizeof(double) * 2 * nc * nbx) d_rpart.alloc(sizeof(double) * 2 * nc * nbx);
+  if (d_rpart.bytes < sizeof(double) * 8 * nc * nbx) d_rpart.alloc(sizeof(double) * 8 * nc * nbx);
   std::vector<char> hbuf(sizeof(double) * 2 * nc + sizeof(int) * nc);
   std::memcpy(hbuf.data(), lam, sizeof(double) * 2 * nc);
   std::memcpy(hbuf.data() + sizeof(double) * 2 * nc, blk, sizeof(int) * nc);
@@ -891,8 +906,22 @@ void OperatorEngine::ritz_residuals(const double* V, int m, const double* Y, int
   ritz_residual_k<<<grid, kRedThreads, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_K.as<double>(),
                                                    d_C.as<double>(), d_M.as<double>(), Xrm, ldx, nc, dlam, dblk,
                                                    d_rpart.as<double>());
-  sum_rows<<<2 * nc, 32, 0, stream>>>(d_rpart.as<double>(), nbx, out);
+  sum_rows<<<8 * nc, 32, 0, stream>>>(d_rpart.as<double>(), nbx, out);
   launches += 3;
+}
+
+void OperatorEngine::residuals_again(const double* Xrm, int nc, const double* lam, double* out) {
+  if (nc <= 0) return;
+  const int nbx = kRedBlocks;
+  RQB_CUDA(cudaMemcpyAsync(d_rcand.p, lam, sizeof(double) * 2 * nc, cudaMemcpyHostToDevice, stream));
+  const double* dlam = d_rcand.as<double>();
+  const int* dblk = reinterpret_cast<const int*>(dlam + 2 * nc);
+  dim3 grid(nbx, (nc + 63) / 64);
+  ritz_residual_k<<<grid, kRedThreads, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_K.as<double>(),
+                                                   d_C.as<double>(), d_M.as<double>(), Xrm, 2 * nc, nc, dlam, dblk,
+                                                   d_rpart.as<double>());
+  sum_rows<<<8 * nc, 32, 0, stream>>>(d_rpart.as<double>(), nbx, out);
+  launches += 2;
 }
 
 void OperatorEngine::ritz_extract(const double* Xrm, int nc, int c, int part_im, double* out) {
@@ -920,7 +949,7 @@ double OperatorEngine::time_op(int what, int iters, int param) {
     RQB_CUDA(cudaMemsetAsync(V.p, 0, V.bytes, stream));
     RQB_CUDA(cudaMemsetAsync(Q.p, 0, Q.bytes, stream));
     for (int c = 0; c < k; ++c) lamh.push_back(0.1), lamh.push_back(0.2), blkh.push_back(c & 1);
-    h.alloc(sizeof(double) * 2 * k);
+    h.alloc(sizeof(double) * 8 * k);
   }
   DeviceBuffer Vb, Rb;
   const int kb = std::max(1, std::min(8, param >> 16));  // what 11 / 12: block width in the high bits

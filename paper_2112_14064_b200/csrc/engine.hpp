@@ -263,8 +263,13 @@ struct OperatorEngine {
   // stored row-major in Xrm (2n x 2nc), and their pencil residuals:
   // out[2c] = ||Q(lambda_c) x_c||^2, out[2c+1] = ||x_c||^2 over block blk[c]
   // (lam: host {re, im} pairs of the scaled-pencil eigenvalues).
+  // out[2nc + 6c ..] = u^H K u, u^H C u, u^H M u (re, im) of candidate c on its block (the
+  // quadratic Rayleigh quotient's coefficients); out needs 8 nc doubles
   void ritz_residuals(const double* V, int m, const double* Y, int nc, const double* lam, const int* blk,
                       double* Xrm, double* out);
+  // the same residuals (and coefficients) of the last batch in Xrm for new eigenvalues lam
+  // (host {re, im} pairs; blocks as in the last ritz_residuals call)
+  void residuals_again(const double* Xrm, int nc, const double* lam, double* out);
   // contiguous copy (n entries) of part (0 re, 1 im) of Ritz vector c of the
   // last ritz_residuals batch, block blk[c]
   void ritz_extract(const double* Xrm, int nc, int c, int part_im, double* out);

@@ -703,6 +703,7 @@ int rq_eigs_run(rq_operator_t* o, const rq_eigs_opts* opts, double* lam_re, doub
     if (const char* e = std::getenv("RQB_GUARD_CLUSTER")) eo.guard_single_cluster = std::atoi(e);
     eo.profile = opts->profile;
     eo.block = opts->block;
+    if (const char* e = std::getenv("RQB_RQ_REFINE")) eo.refine = std::atoi(e);
     eo.want_vectors = (vec_re && vec_im) ? 1 : 0;
     o->ledger = rqb::Ledger{};
     rqb::EigsResult r = rqb::solve_quadratic_device(*o->op, eo, o->ledger, o->norms1);

@@ -175,7 +175,7 @@ struct EigWorkspace {
     }
     dQ.alloc(sizeof(double) * (m + 1) * (2 * m + 2));
     dX.alloc(sizeof(double) * n2 * 2 * (m + 1));
-    dRes.alloc(sizeof(double) * 4 * (m + 1));
+    dRes.alloc(sizeof(double) * 8 * (m + bs + 1));
   }
   ~EigWorkspace() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
@@ -294,6 +294,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   double t_solve = 0, t_orth = 0, t_ritz = 0, t_check = 0, t_restart = 0, t_sync = 0;
   double check_gate = o.est_factor * o.tol;
   int last_nchk = 0;  // candidates of the last explicit check (row-major Ritz batch in dX)
+  std::vector<double> last_lam, last_rq;  // that batch's scaled eigenvalues and Rayleigh-quotient coefficients
   int since_check = 0;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms_since = [](std::chrono::steady_clock::time_point a) {
@@ -364,7 +365,20 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
           // block SpMV per pass instead of one M-product per member: B r_b is
           // updated with the stored B-images of the earlier members)
           double* Wl = W.dWl.as<double>();
+          static const bool mtrack = !std::getenv("RQB_BLOCK_MTRACK") || std::atoi(std::getenv("RQB_BLOCK_MTRACK")) != 0;
           auto intra = [&](double* src, double* h1, double* h2, double* beta) {
+            if (!mtrack) {  // one M-product per member (A/B reference)
+              for (int b = 0; b < w; ++b) {
+                double* rb = src + static_cast<int64_t>(b) * n2;
+                if (b > 0)
+                  for (double* hh : {h1 + kt + static_cast<int64_t>(b) * LDH, h2 + kt + static_cast<int64_t>(b) * LDH}) {
+                    op.gemv_t(BVn, b, rb, hh);
+                    op.gemv_n(Vn, b, hh, rb, nullptr);
+                  }
+                op.bnorm_normalize_b(rb, beta + b, Vn + static_cast<int64_t>(b) * n2, BVn + static_cast<int64_t>(b) * n2);
+              }
+              return;
+            }
             op.mspmv_block(src, w, Wl);
             for (int b = 0; b < w; ++b) {
               double* rb = src + static_cast<int64_t>(b) * n2;
@@ -648,10 +662,12 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       op.ritz_residuals(V, mm, dQ.as<double>(), nchk, lam.data(), cblock.data(), dX.as<double>(),
                         dRes.as<double>());
       last_nchk = nchk;
-      std::vector<double> rr(2 * nchk);
-      cuda_check(cudaMemcpyAsync(rr.data(), dRes.p, sizeof(double) * 2 * nchk, cudaMemcpyDeviceToHost, st),
+      std::vector<double> rr(8 * nchk);
+      last_lam = lam;
+      cuda_check(cudaMemcpyAsync(rr.data(), dRes.p, sizeof(double) * 8 * nchk, cudaMemcpyDeviceToHost, st),
                  "D2H res");
       cuda_check(cudaStreamSynchronize(st), "sync");
+      last_rq.assign(rr.begin() + 2 * nchk, rr.end());
       all_conv = mates_conv = true;
       for (int c = 0; c < nchk; ++c) {
         const double ag = std::abs(rz[chk[c]].lambda / vs);
@@ -685,6 +701,44 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         final_set.push_back(rz[chk[c]]);
         final_res.push_back(cres[c]);
         final_block.push_back(cblock[c]);
+      }
+      // Quadratic Rayleigh-quotient refinement of the returned eigenvalues: the
+      // root of u^H (K + g C + g^2 M) u = 0 nearest the Ritz value (u the
+      // converged vector on its block, coefficients from the check's SpMM pass);
+      // kept when its explicit residual (one more pass over K, C, M) is within
+      // tolerance. A converged vector pins its eigenvalue to ~ residual^2 this
+      // way, where the Ritz value of a degenerate cluster is only ~ residual.
+      if (o.refine && static_cast<int>(last_rq.size()) == 6 * last_nchk && last_nchk == nchk) {
+        std::vector<double> lam2 = last_lam, rr2(8 * static_cast<size_t>(nchk));
+        std::vector<cplx> gref(pos.size());
+        for (size_t q = 0; q < pos.size(); ++q) {
+          const int c = pos[q];
+          const cplx kq(last_rq[6 * c], last_rq[6 * c + 1]), cq(last_rq[6 * c + 2], last_rq[6 * c + 3]),
+              mq(last_rq[6 * c + 4], last_rq[6 * c + 5]);
+          const cplx g0(last_lam[2 * c], last_lam[2 * c + 1]);
+          cplx g = g0;
+          if (std::abs(mq) > 0.0) {
+            const cplx dsc = std::sqrt(cq * cq - 4.0 * mq * kq);
+            const cplx r1 = (-cq + dsc) / (2.0 * mq), r2 = (-cq - dsc) / (2.0 * mq);
+            g = std::abs(r1 - g0) <= std::abs(r2 - g0) ? r1 : r2;
+          }
+          gref[q] = g;
+          lam2[2 * c] = g.real();
+          lam2[2 * c + 1] = g.imag();
+        }
+        op.residuals_again(dX.as<double>(), nchk, lam2.data(), dRes.as<double>());
+        cuda_check(cudaMemcpyAsync(rr2.data(), dRes.p, sizeof(double) * 8 * nchk, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        for (size_t q = 0; q < pos.size(); ++q) {
+          const int c = pos[q];
+          const double ag = std::abs(gref[q]);
+          const double den = (norms1[0] + ag * norms1[1] + ag * ag * norms1[2]) * std::sqrt(rr2[2 * c + 1]);
+          const double r2 = den > 0 ? std::sqrt(rr2[2 * c]) / den : 1.0;
+          if (r2 <= std::max(final_res[q], o.tol)) {
+            final_set[q].lambda = gref[q] * vs;
+            final_res[q] = r2;
+          }
+        }
       }
       if (o.want_vectors) {
         final_vecs_re.assign(static_cast<size_t>(n) * nev, 0.0);

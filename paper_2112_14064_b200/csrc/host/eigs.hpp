@@ -52,6 +52,7 @@ struct EigsOptions {
   int want_vectors = 0;
   int profile = 0;
   int block = 1;  // block Krylov-Schur block size (1: single-vector; 2..8: SURVEY.md §8 f2)
+  int refine = 1;  // quadratic Rayleigh-quotient refinement of the returned eigenvalues
   int block_min_steps = 1;  // block mode: cycles with room for fewer block steps take width-1 steps (1: never)
 };
 
