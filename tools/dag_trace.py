@@ -66,3 +66,21 @@ for b0, b1 in zip(bins[:-1], bins[1:]):
     tot = ov.sum() / (b1 - b0)
     by = {names[t]: round(float(ov[tk["type"] == t].sum() / (b1 - b0)), 1) for t in range(8)}
     print(f"   {b0/1e3:7.1f}-{b1/1e3:7.1f} us: {tot:6.1f}  {by}")
+# per-type phase split on the top fronts (levels >= 11): work / fence / successor release, us
+top = np.isin(tk["front"], np.nonzero(o.level >= 11)[0]) & valid
+print("  phase split on levels >= 11 (mean us: total, work, fence, succ):")
+for t in range(8):
+    m_ = top & (tk["type"] == t)
+    if m_.sum() == 0:
+        continue
+    tot_ = (tr[m_, 1] - tr[m_, 0]).mean() / 1e3
+    wk = (ph[m_, 0] - tr[m_, 0]).mean() / 1e3
+    fe_ = (ph[m_, 1] - ph[m_, 0]).mean() / 1e3
+    sc = (tr[m_, 1] - ph[m_, 1]).mean() / 1e3
+    print(f"   {names[t]:5s} n {m_.sum():6d}  {tot_:7.2f} {wk:7.2f} {fe_:7.2f} {sc:7.2f}")
+# gaps on the root's panel chain: DIAG(s) start - end of the latest predecessor-type task of step s-1
+root = int(np.argmax(o.level))
+d = np.nonzero((tk["front"] == root) & (tk["type"] == 2) & valid)[0]
+d = d[np.argsort(tk["step"][d])]
+print("  root DIAG starts (us) and step-to-step deltas:", [round(float(tr[i, 0]) / 1e3, 1) for i in d[:6]],
+      [round(float(tr[d[k + 1], 0] - tr[d[k], 0]) / 1e3, 1) for k in range(min(12, len(d) - 1))])
