@@ -288,10 +288,12 @@ def run_b200(args):
         del opI, PI
 
     # ---- time to nev eigenpairs (device-resident pencil; factor + Krylov-Schur).
-    # The requested pairs are copies of one hugely degenerate eigenvalue, so a
-    # single-vector Krylov-Schur collects them through rounding and its cycle
-    # count moves with the start vector and the last bits of the factors
-    # (cfg4_riga: 16-61 cycles): the line reports the median over seeds
+    # The requested pairs are copies of one hugely degenerate eigenvalue. In
+    # exact arithmetic a Krylov space holds one direction of a degenerate
+    # eigenspace per start vector; the other copies enter through rounding, so
+    # the cycle count moves with the start vector and the last bits of the
+    # factors and of the host dense work (cfg4_riga over 12 seeds: 6-17 cycles
+    # single-vector, 11-20 at block 4): the line reports the median over seeds
     # 0 .. nev_seeds-1 (one run each after the first, cold call on seed 0).
     t_nev, infos, resid_max = [], [], 0.0
     seeds = [0] + list(range(max(1, args.nev_seeds)))
@@ -526,7 +528,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg4_riga", choices=sorted(NEV))
     ap.add_argument("--nev", type=int, default=0)
-    ap.add_argument("--nev-seeds", type=int, default=5)
+    ap.add_argument("--nev-seeds", type=int, default=9)
     ap.add_argument("--block", type=int, default=4, help="block size of the block Krylov-Schur line (<= 1: off)")
     ap.add_argument("--max-restarts", type=int, default=1000)
     ap.add_argument("--cpu-samples", type=int, default=1)

@@ -273,14 +273,17 @@ bool francis_real(std::vector<double>& Hv, std::vector<double>& Zv, int n) {
 
 }  // namespace
 
-// Real Hessenberg reduction + Francis double-shift QR (real arithmetic), then
-// each remaining 2 x 2 block (a complex-conjugate pair) is triangularised by
-// one complex rotation: A = Z T Z^H with T upper triangular.
-bool complex_schur(const std::vector<double>& A, int n, CMat& T, CMat& Z) {
-  std::vector<double> H(A.begin(), A.begin() + static_cast<size_t>(n) * n), Zr(static_cast<size_t>(n) * n, 0.0);
-  for (int i = 0; i < n; ++i) Zr[i + static_cast<size_t>(i) * n] = 1.0;
-  hessenberg_real(H, Zr, n);
-  if (!francis_real(H, Zr, n)) return false;
+bool real_schur(const std::vector<double>& A, int n, std::vector<double>& T, std::vector<double>& Z) {
+  T.assign(A.begin(), A.begin() + static_cast<size_t>(n) * n);
+  Z.assign(static_cast<size_t>(n) * n, 0.0);
+  for (int i = 0; i < n; ++i) Z[i + static_cast<size_t>(i) * n] = 1.0;
+  hessenberg_real(T, Z, n);
+  return francis_real(T, Z, n);
+}
+
+// Each 2 x 2 block (a complex-conjugate pair) of the real Schur form is
+// triangularised by one complex rotation: A = Z T Z^H with T upper triangular.
+void complexify_schur(const std::vector<double>& H, const std::vector<double>& Zr, int n, CMat& T, CMat& Z) {
   T = CMat(n);
   Z = CMat(n);
   for (size_t i = 0; i < H.size(); ++i) {
@@ -311,6 +314,14 @@ bool complex_schur(const std::vector<double>& A, int n, CMat& T, CMat& Z) {
     T(k + 1, k) = 0.0;
     ++k;
   }
+}
+
+// Real Hessenberg reduction + Francis double-shift QR (real arithmetic), then
+// the 2 x 2 blocks are triangularised: A = Z T Z^H with T upper triangular.
+bool complex_schur(const std::vector<double>& A, int n, CMat& T, CMat& Z) {
+  std::vector<double> H, Zr;
+  if (!real_schur(A, n, H, Zr)) return false;
+  complexify_schur(H, Zr, n, T, Z);
   return true;
 }
 
@@ -416,6 +427,235 @@ void schur_reorder(CMat& T, CMat& Z, std::vector<int>& sel) {
     }
     ++ks;
   }
+}
+
+namespace {
+
+// 3-element Householder reflector I - tau v v^T with v[piv] = 1 that maps u
+// onto a multiple of e_piv (u is overwritten by v).
+double house3(double* u, int piv) {
+  const int a = piv == 0 ? 1 : 0, b = piv == 2 ? 1 : 2;
+  const double xn = std::hypot(u[a], u[b]);
+  if (xn == 0.0) {
+    u[a] = u[b] = 0.0;
+    u[piv] = 1.0;
+    return 0.0;
+  }
+  const double alpha = u[piv];
+  const double beta = -std::copysign(std::hypot(alpha, xn), alpha);
+  const double sc = 1.0 / (alpha - beta);
+  u[a] *= sc;
+  u[b] *= sc;
+  u[piv] = 1.0;
+  return (beta - alpha) / beta;
+}
+
+// M[r..r+2, c0..c1) <- (I - tau v v^T) M[r..r+2, c0..c1)   (column-major, ld)
+void refl3_left(double* M, int ld, int r, int c0, int c1, const double* v, double tau) {
+  if (tau == 0.0) return;
+  for (int c = c0; c < c1; ++c) {
+    double* x = M + r + static_cast<size_t>(c) * ld;
+    const double s = tau * (v[0] * x[0] + v[1] * x[1] + v[2] * x[2]);
+    x[0] -= s * v[0];
+    x[1] -= s * v[1];
+    x[2] -= s * v[2];
+  }
+}
+
+// M[r0..r1, c..c+2] <- M[r0..r1, c..c+2] (I - tau v v^T)
+void refl3_right(double* M, int ld, int c, int r0, int r1, const double* v, double tau) {
+  if (tau == 0.0) return;
+  double* x0 = M + static_cast<size_t>(c) * ld;
+  double* x1 = x0 + ld;
+  double* x2 = x1 + ld;
+  const double t0 = tau * v[0], t1 = tau * v[1], t2 = tau * v[2];
+  for (int i = r0; i < r1; ++i) {
+    const double s = v[0] * x0[i] + v[1] * x1[i] + v[2] * x2[i];
+    x0[i] -= s * t0;
+    x1[i] -= s * t1;
+    x2[i] -= s * t2;
+  }
+}
+
+// TL X - X TR = B for X (n1 x n2, n1, n2 <= 2), all column-major with the
+// given leading dimensions: the n1 n2 Kronecker system by Gaussian elimination
+// with complete pivoting, tiny pivots lifted to smin.
+void small_sylvester(const double* TL, int ldl, const double* TR, int ldr, const double* B, int ldb, int n1, int n2,
+                     double* X) {
+  const int m = n1 * n2;
+  double K[4][4] = {}, b[4];
+  double kmax = 0.0;
+  for (int j = 0; j < n2; ++j)
+    for (int i = 0; i < n1; ++i) {
+      const int row = i + j * n1;
+      b[row] = B[i + j * ldb];
+      for (int l = 0; l < n2; ++l)
+        for (int k = 0; k < n1; ++k) {
+          double v = 0.0;
+          if (j == l) v += TL[i + k * ldl];
+          if (i == k) v -= TR[l + j * ldr];
+          K[row][k + l * n1] = v;
+          kmax = std::max(kmax, std::fabs(v));
+        }
+    }
+  const double smin = std::max(8.0 * std::numeric_limits<double>::epsilon() * kmax, 1e-290);
+  int cperm[4] = {0, 1, 2, 3};
+  for (int c = 0; c < m; ++c) {
+    int pr = c, pc = c;
+    double best = -1.0;
+    for (int i = c; i < m; ++i)
+      for (int j = c; j < m; ++j)
+        if (std::fabs(K[i][j]) > best) best = std::fabs(K[i][j]), pr = i, pc = j;
+    if (pr != c) {
+      for (int j = 0; j < m; ++j) std::swap(K[pr][j], K[c][j]);
+      std::swap(b[pr], b[c]);
+    }
+    if (pc != c) {
+      for (int i = 0; i < m; ++i) std::swap(K[i][pc], K[i][c]);
+      std::swap(cperm[pc], cperm[c]);
+    }
+    if (std::fabs(K[c][c]) < smin) K[c][c] = smin;
+    for (int i = c + 1; i < m; ++i) {
+      const double f = K[i][c] / K[c][c];
+      for (int j = c; j < m; ++j) K[i][j] -= f * K[c][j];
+      b[i] -= f * b[c];
+    }
+  }
+  double x[4];
+  for (int i = m - 1; i >= 0; --i) {
+    double v = b[i];
+    for (int j = i + 1; j < m; ++j) v -= K[i][j] * x[j];
+    x[i] = v / K[i][i];
+  }
+  for (int i = 0; i < m; ++i) X[cperm[i]] = x[i];
+}
+
+// Swap the adjacent diagonal blocks T11 (n1 x n1, at j1) and T22 (n2 x n2) of
+// the real Schur form by an orthogonal similarity, updating Z (the direct
+// swapping method of Bai & Demmel, 1993: the Sylvester solution X of
+// T11 X - X T22 = T12 spans the invariant subspace [-X; I] of T22, whose
+// QR factor moves it up). Returns false (nothing changed) when the swapped
+// form would not be block triangular to working accuracy.
+bool swap_blocks(std::vector<double>& Tv, std::vector<double>& Zv, int n, int j1, int n1, int n2) {
+  double* T = Tv.data();
+  double* Z = Zv.data();
+  auto t = [&](int i, int j) -> double& { return T[i + static_cast<size_t>(j) * n]; };
+  if (n1 == 1 && n2 == 1) {
+    const int j2 = j1 + 1;
+    const double t11 = t(j1, j1), t22 = t(j2, j2);
+    const double f = t(j1, j2), g = t22 - t11;
+    const double r = std::hypot(f, g);
+    if (r == 0.0) return true;  // equal eigenvalues, t12 = 0: nothing to move
+    const double cs = f / r, sn = g / r;
+    for (int j = j2 + 1; j < n; ++j) {
+      const double x = t(j1, j), y = t(j2, j);
+      t(j1, j) = cs * x + sn * y;
+      t(j2, j) = cs * y - sn * x;
+    }
+    auto cols = [&](double* M, int rows) {
+      double* c0 = M + static_cast<size_t>(j1) * n;
+      double* c1 = c0 + n;
+      for (int i = 0; i < rows; ++i) {
+        const double x = c0[i], y = c1[i];
+        c0[i] = cs * x + sn * y;
+        c1[i] = cs * y - sn * x;
+      }
+    };
+    cols(T, j1);
+    cols(Z, n);
+    t(j1, j1) = t22;
+    t(j2, j2) = t11;
+    return true;
+  }
+  const int nd = n1 + n2;
+  double D[16];
+  double dnorm = 0.0;
+  for (int j = 0; j < nd; ++j)
+    for (int i = 0; i < nd; ++i) {
+      D[i + 4 * j] = t(j1 + i, j1 + j);
+      dnorm = std::max(dnorm, std::fabs(D[i + 4 * j]));
+    }
+  const double thresh = std::max(10.0 * std::numeric_limits<double>::epsilon() * dnorm, 1e-290);
+  double X[4];
+  small_sylvester(D, 4, D + n1 + 4 * n1, 4, D + 4 * n1, 4, n1, n2, X);
+  if (n1 == 1) {  // n2 = 2: reflector mapping (1, X11, X12) onto e_3
+    double v[3] = {1.0, X[0], X[1]};
+    const double tau = house3(v, 2);
+    const double t11 = t(j1, j1);
+    refl3_left(D, 4, 0, 0, 3, v, tau);
+    refl3_right(D, 4, 0, 0, 3, v, tau);
+    if (std::max({std::fabs(D[2]), std::fabs(D[2 + 4]), std::fabs(D[2 + 8] - t11)}) > thresh) return false;
+    refl3_left(T, n, j1, j1, n, v, tau);
+    refl3_right(T, n, j1, 0, j1 + 2, v, tau);
+    refl3_right(Z, n, j1, 0, n, v, tau);
+    t(j1 + 2, j1) = 0.0;
+    t(j1 + 2, j1 + 1) = 0.0;
+    t(j1 + 2, j1 + 2) = t11;
+    return true;
+  }
+  if (n2 == 1) {  // n1 = 2: reflector mapping (-X11, -X21, 1) onto e_1
+    double v[3] = {-X[0], -X[1], 1.0};
+    const double tau = house3(v, 0);
+    const double t33 = t(j1 + 2, j1 + 2);
+    refl3_left(D, 4, 0, 0, 3, v, tau);
+    refl3_right(D, 4, 0, 0, 3, v, tau);
+    if (std::max({std::fabs(D[1]), std::fabs(D[2]), std::fabs(D[0] - t33)}) > thresh) return false;
+    refl3_right(T, n, j1, 0, j1 + 3, v, tau);
+    refl3_left(T, n, j1, j1 + 1, n, v, tau);
+    refl3_right(Z, n, j1, 0, n, v, tau);
+    t(j1, j1) = t33;
+    t(j1 + 1, j1) = 0.0;
+    t(j1 + 2, j1) = 0.0;
+    return true;
+  }
+  // n1 = n2 = 2: two reflectors triangularise [-X; I]
+  double v1[3] = {-X[0], -X[1], 1.0};
+  const double tau1 = house3(v1, 0);
+  const double tmp = -tau1 * (X[2] + v1[1] * X[3]);
+  double v2[3] = {-tmp * v1[1] - X[3], -tmp * v1[2], 1.0};
+  const double tau2 = house3(v2, 0);
+  refl3_left(D, 4, 0, 0, 4, v1, tau1);
+  refl3_right(D, 4, 0, 0, 4, v1, tau1);
+  refl3_left(D, 4, 1, 0, 4, v2, tau2);
+  refl3_right(D, 4, 1, 0, 4, v2, tau2);
+  if (std::max({std::fabs(D[2]), std::fabs(D[2 + 4]), std::fabs(D[3]), std::fabs(D[3 + 4])}) > thresh) return false;
+  refl3_left(T, n, j1, j1, n, v1, tau1);
+  refl3_right(T, n, j1, 0, j1 + 4, v1, tau1);
+  refl3_left(T, n, j1 + 1, j1, n, v2, tau2);
+  refl3_right(T, n, j1 + 1, 0, j1 + 4, v2, tau2);
+  refl3_right(Z, n, j1, 0, n, v1, tau1);
+  refl3_right(Z, n, j1 + 1, 0, n, v2, tau2);
+  t(j1 + 2, j1) = t(j1 + 2, j1 + 1) = t(j1 + 3, j1) = t(j1 + 3, j1 + 1) = 0.0;
+  return true;
+}
+
+}  // namespace
+
+int real_schur_reorder(std::vector<double>& T, std::vector<double>& Z, int n, std::vector<int>& sel) {
+  auto sub = [&](int k) { return T[(k + 1) + static_cast<size_t>(k) * n]; };  // T(k+1, k)
+  for (int k = 0; k + 1 < n; ++k)
+    if (sub(k) != 0.0) {
+      const int s = sel[k] || sel[k + 1];
+      sel[k] = sel[k + 1] = s;
+      ++k;
+    }
+  auto bsize = [&](int k) { return k + 1 < n && sub(k) != 0.0 ? 2 : 1; };
+  int ks = 0;
+  while (true) {
+    int k = ks;
+    while (k < n && !sel[k]) k += bsize(k);
+    if (k >= n) break;
+    int nb = bsize(k), here = k;
+    while (here > ks) {
+      const int nprev = here - 2 >= ks && sub(here - 2) != 0.0 ? 2 : 1;
+      if (!swap_blocks(T, Z, n, here - nprev, nprev, nb)) return -1;
+      std::rotate(sel.begin() + here - nprev, sel.begin() + here, sel.begin() + here + nb);
+      here -= nprev;
+      nb = bsize(here);
+    }
+    ks += bsize(ks);
+  }
+  return ks;
 }
 
 CMat triangular_eigvecs(const CMat& T) {

@@ -28,6 +28,24 @@ struct CMat {
 // within 30 n iterations per eigenvalue.
 bool complex_schur(const std::vector<double>& A, int n, CMat& T, CMat& Z);
 
+// The real Schur form behind complex_schur: A = Z T Z^T, T upper
+// quasi-triangular (1 x 1 blocks and 2 x 2 blocks of complex-conjugate pairs),
+// Z orthogonal, both n x n column-major.
+bool real_schur(const std::vector<double>& A, int n, std::vector<double>& T, std::vector<double>& Z);
+
+// The complex triangular form of a real Schur form (one complex rotation per
+// 2 x 2 block; diagonal positions are kept: the pair of block k sits at k, k+1).
+void complexify_schur(const std::vector<double>& T, const std::vector<double>& Z, int n, CMat& Tc, CMat& Zc);
+
+// Move the selected blocks of the real Schur form (T, Z) to the leading
+// positions (stable order) by adjacent block swaps; a 2 x 2 block is selected
+// if either of its diagonal positions is (sel is closed over blocks and
+// permuted alongside). Returns the order p of the leading selected part
+// (T[:p, :p] quasi-triangular, Z[:, :p] an orthonormal real basis of its
+// invariant subspace), or -1 if a swap was refused as inaccurate (T, Z are
+// then partly reordered but still a valid Schur form).
+int real_schur_reorder(std::vector<double>& T, std::vector<double>& Z, int n, std::vector<int>& sel);
+
 // A = Z T Z^H for a complex A (Householder Hessenberg + single-shift complex
 // QR with Wilkinson shifts). Returns false past 30 n iterations.
 bool complex_schur_c(const CMat& A, CMat& T, CMat& Z);

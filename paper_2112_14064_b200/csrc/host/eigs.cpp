@@ -292,10 +292,12 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
   cuda_check(cudaEventCreateWithFlags(&e_h, cudaEventDisableTiming), "event");
   bool pre_applied = false;  // r already holds apply(V[k]) (speculative, see below)
   double t_solve = 0, t_orth = 0, t_ritz = 0, t_check = 0, t_restart = 0, t_sync = 0;
+  double t_reorder = 0, t_basis = 0, t_host = 0;  // trace only: restart split, host time per cycle
   double check_gate = o.est_factor * o.tol;
   int last_nchk = 0;  // candidates of the last explicit check (row-major Ritz batch in dX)
   std::vector<double> last_lam, last_rq;  // that batch's scaled eigenvalues and Rayleigh-quotient coefficients
   int since_check = 0;
+  int recheck_wait = 8;  // cycles before an ungated re-check (shorter when the last check was close)
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms_since = [](std::chrono::steady_clock::time_point a) {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
@@ -489,6 +491,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       cuda_check(cudaEventSynchronize(e_h), "sync");
       t_sync += ms_since(ts0);  // host blocked on the cycle's Arnoldi steps
     }
+    const auto th0 = now();
     for (const auto& stp : plan) {
       const int j0 = stp.first, w = stp.second, kt = j0 + bs;  // step start, width, projection range
       if (w == 1) {
@@ -528,8 +531,10 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
     for (int j = 0; j < mm; ++j)
       for (int i = 0; i < mm; ++i) Hm[i + static_cast<size_t>(j) * mm] = Hc(i, j);
     CMat T, Z;
+    std::vector<double> Tre, Zre;  // the real Schur form (kept for the restart)
     const auto tr0 = now();
-    if (!complex_schur(Hm, mm, T, Z)) fail(errc::solver, "Hessenberg QR did not converge");
+    if (!real_schur(Hm, mm, Tre, Zre)) fail(errc::solver, "Hessenberg QR did not converge");
+    complexify_schur(Tre, Zre, mm, T, Z);
     const CMat Y = triangular_eigvecs(T);
     t_ritz += ms_since(tr0);
     // residual rows: S V_mm = V_mm H_mm + V[mm, mm+bs) E, E = H[mm.., 0..mm) (nonzero
@@ -622,7 +627,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         est_worst = e[nev - 1];
       }
     }
-    const bool maybe = est_worst <= check_gate || (est_worst <= o.est_factor * o.tol && since_check >= 8);
+    const bool maybe = est_worst <= check_gate || (est_worst <= o.est_factor * o.tol && since_check >= recheck_wait);
     ++since_check;
     bool all_conv = false, mates_conv = false;
     std::vector<double> cres(nchk, 1.0);
@@ -650,6 +655,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         std::memcpy(W.hy.data(), Yr.data(), sizeof(double) * Yr.size());
         ysrc = W.hy.data();
       }
+      const double t_yr = ms_since(tc0);
       cuda_check(cudaMemcpyAsync(dQ.p, ysrc, sizeof(double) * Yr.size(), cudaMemcpyHostToDevice, st), "H2D Y");
       std::vector<double> lam(2 * nchk);
       for (int c = 0; c < nchk; ++c) {
@@ -666,7 +672,10 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       last_lam = lam;
       cuda_check(cudaMemcpyAsync(rr.data(), dRes.p, sizeof(double) * 8 * nchk, cudaMemcpyDeviceToHost, st),
                  "D2H res");
+      const double t_enq = ms_since(tc0);
       cuda_check(cudaStreamSynchronize(st), "sync");
+      if (trace_cycles)
+        std::fprintf(stderr, "[eigs] check %d: Y %.1f enqueue %.1f sync %.1f ms\n", nchk, t_yr, t_enq, ms_since(tc0));
       last_rq.assign(rr.begin() + 2 * nchk, rr.end());
       all_conv = mates_conv = true;
       for (int c = 0; c < nchk; ++c) {
@@ -681,6 +690,13 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
       t_check += ms_since(tc0);
       since_check = 0;
       check_gate = all_conv ? o.est_factor * o.tol : 0.1 * est_worst;
+      // a check that found most of the nev converged is re-run sooner (its
+      // cost, one SpMM pass over the candidates, is below a cycle's): the wait
+      // shrinks from 8 cycles in proportion to the converged fraction
+      int nc_all = 0;
+      for (int c = 0; c < nchk; ++c) nc_all += cres[c] <= o.tol;
+      const double frac = std::min(1.0, static_cast<double>(nc_all) / nev);
+      recheck_wait = frac >= 0.5 ? std::max(1, static_cast<int>(std::lround(8.0 * (1.0 - frac)))) : 8;
     }
     int nconv_now = 0;
     for (int c = 0; c < nev && maybe; ++c)
@@ -851,38 +867,69 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         }
       }
     }
-    // ---- restart: reorder Schur form, real basis of the kept directions ----
+    // ---- restart: reorder the Schur form, real basis of the kept directions ----
+    // Real Schur form: the selected 1 x 1 / 2 x 2 blocks are swapped to the
+    // top, Q_p = Z[:, :p] and T_p = T[:p, :p] come out directly (a selected
+    // member of a conjugate pair brings its mate). Fallback (a refused swap, or
+    // a closed selection larger than m - bs): reorder the complex form and take
+    // a rank-p real basis of the kept Schur vectors, T_p = Q_p^T H_m Q_p.
     const auto trs0 = now();
-    CMat Tr = T, Zr = Z;
-    std::vector<int> s2 = sel;
-    schur_reorder(Tr, Zr, s2);
-    std::vector<double> Qp;
-    const int rank = real_basis(Zr, p, Qp);
-    if (rank < p) p = rank;
-    if (p <= 0) fail(errc::solver, "Krylov-Schur restart lost its basis");
-    // T_p = Q_p^T H_m Q_p, b_p = beta_m e_m^T Q_p
-    // (column-oriented loops: every inner loop is a contiguous axpy / dot)
-    std::vector<double> HQ(static_cast<size_t>(mm) * p, 0.0), Tp(static_cast<size_t>(p) * p, 0.0);
+    std::vector<double> Qp, Tp;
+    {
+      static const bool real_restart = !std::getenv("RQB_RESTART_REAL") || std::atoi(std::getenv("RQB_RESTART_REAL")) != 0;
+      std::vector<double> Tq = Tre, Zq = Zre;
+      std::vector<int> s2 = sel;
+      const int pr = real_restart ? real_schur_reorder(Tq, Zq, mm, s2) : -1;
+      if (pr > 0 && pr <= m - bs && pr <= mm) {
+        p = pr;
+        Qp.assign(Zq.begin(), Zq.begin() + static_cast<size_t>(mm) * p);
+        Tp.resize(static_cast<size_t>(p) * p);
+        for (int c = 0; c < p; ++c)
+          std::copy(Tq.begin() + static_cast<size_t>(c) * mm, Tq.begin() + static_cast<size_t>(c) * mm + p,
+                    Tp.begin() + static_cast<size_t>(c) * p);
+      }
+    }
+    t_reorder += ms_since(trs0);
+    const auto trb0 = now();
+    // H Q_p (the invariance defect below; T_p itself in the fallback)
+    std::vector<double> HQ;
+    auto hq_product = [&]() {
+      HQ.assign(static_cast<size_t>(mm) * p, 0.0);
 #pragma omp parallel for schedule(static) num_threads(host_threads()) if (static_cast<int64_t>(mm) * mm * p > 1000000)
-    for (int c = 0; c < p; ++c) {
-      double* hq = HQ.data() + static_cast<size_t>(c) * mm;
-      for (int t = 0; t < mm; ++t) {
-        const double q = Qp[t + static_cast<size_t>(c) * mm];
-        if (q == 0.0) continue;
-        const double* ht = Hm.data() + static_cast<size_t>(t) * mm;
-        for (int i = 0; i < mm; ++i) hq[i] += ht[i] * q;
+      for (int c = 0; c < p; ++c) {
+        double* hq = HQ.data() + static_cast<size_t>(c) * mm;
+        for (int t = 0; t < mm; ++t) {
+          const double q = Qp[t + static_cast<size_t>(c) * mm];
+          if (q == 0.0) continue;
+          const double* ht = Hm.data() + static_cast<size_t>(t) * mm;
+          for (int i = 0; i < mm; ++i) hq[i] += ht[i] * q;
+        }
       }
-    }
+    };
+    if (Qp.empty()) {
+      CMat Tr = T, Zr = Z;
+      std::vector<int> s2 = sel;
+      schur_reorder(Tr, Zr, s2);
+      const int rank = real_basis(Zr, p, Qp);
+      if (rank < p) p = rank;
+      if (p <= 0) fail(errc::solver, "Krylov-Schur restart lost its basis");
+      // T_p = Q_p^T H_m Q_p (column-oriented loops: contiguous axpy / dot)
+      hq_product();
+      Tp.assign(static_cast<size_t>(p) * p, 0.0);
 #pragma omp parallel for schedule(static) num_threads(host_threads()) if (static_cast<int64_t>(mm) * p * p > 1000000)
-    for (int c = 0; c < p; ++c) {
-      const double* hq = HQ.data() + static_cast<size_t>(c) * mm;
-      for (int i = 0; i < p; ++i) {
-        const double* qi = Qp.data() + static_cast<size_t>(i) * mm;
-        double s = 0;
-        for (int t = 0; t < mm; ++t) s += qi[t] * hq[t];
-        Tp[i + static_cast<size_t>(c) * p] = s;
+      for (int c = 0; c < p; ++c) {
+        const double* hq = HQ.data() + static_cast<size_t>(c) * mm;
+        for (int i = 0; i < p; ++i) {
+          const double* qi = Qp.data() + static_cast<size_t>(i) * mm;
+          double s = 0;
+          for (int t = 0; t < mm; ++t) s += qi[t] * hq[t];
+          Tp[i + static_cast<size_t>(c) * p] = s;
+        }
       }
+    } else {
+      hq_product();
     }
+    t_basis += ms_since(trb0);
     {
       // invariance defect ||H Q_p - Q_p T_p|| / ||H|| (exact restart needs ~eps)
       double dmax = 0, hmax = 0;
@@ -892,6 +939,7 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
         std::vector<double> rc(HQ.begin() + static_cast<size_t>(c) * mm, HQ.begin() + static_cast<size_t>(c + 1) * mm);
         for (int t = 0; t < p; ++t) {
           const double tc = Tp[t + static_cast<size_t>(c) * p];
+          if (tc == 0.0) continue;
           const double* qt = Qp.data() + static_cast<size_t>(t) * mm;
           for (int i = 0; i < mm; ++i) rc[i] -= tc * qt[i];
         }
@@ -932,12 +980,14 @@ EigsResult solve_quadratic_device(OperatorEngine& op, const EigsOptions& o, Ledg
                                  sizeof(double) * n2 * bs, cudaMemcpyDeviceToDevice, st), "D2D Bv");
     }
     t_restart += ms_since(trs0);
+    t_host += ms_since(th0);
     if (trace_cycles)
       std::fprintf(stderr, "[eigs] cycle %d: steps %d..%d, checked %d (maybe %d, nconv %d), est worst %.2e best %.2e, "
-                   "groups %zu (first %zu), kept %d%s, t ritz %.1f check %.1f restart %.1f sync %.1f ms\n", cycles, k,
+                   "groups %zu (first %zu), kept %d%s, t ritz %.1f check %.1f restart %.1f (reorder %.1f basis %.1f) host %.1f "
+                   "sync %.1f ms\n", cycles, k,
                    mm, maybe ? nchk : 0, (int)maybe, nconv_now, est_worst, rz[order[0]].est, groups.size(),
                    groups.empty() ? size_t(0) : groups[0].size(), p, deflate ? " (deflated restart)" : "", t_ritz,
-                   t_check, t_restart, t_sync);
+                   t_check, t_restart, t_reorder, t_basis, t_host, t_sync);
     k = p;
   }
   op.fac->check_sweeps();  // watchdog of the triangular sweeps (syncs the stream)

@@ -105,6 +105,59 @@ int main() {
     std::printf("n=%d%s p=%d schur=%.2e reorder=%.2e rank=%d invariance=%.2e %s\n", n, cs.second ? " (degenerate)" : "", p, d0, d1, rank,
                 inv, ok ? "ok" : "FAIL");
     fails += !ok;
+    // the same selection on the real Schur form (real_schur_reorder): A Zr =
+    // Zr Tr, Zr orthogonal, Tr block upper triangular with the selected part
+    // leading (T[p.., :p] = 0) and its eigenvalues the selected ones
+    std::vector<double> Tr, Zr;
+    if (!real_schur(A, n, Tr, Zr)) { std::printf("real qr fail n=%d\n", n); return 1; }
+    CMat Tc, Zc;
+    complexify_schur(Tr, Zr, n, Tc, Zc);
+    std::vector<cplx> want_ev;
+    for (int i = 0; i < n; ++i) if (sel[i]) want_ev.push_back(Tc(i, i));
+    std::vector<int> s3 = sel;
+    const int pr = real_schur_reorder(Tr, Zr, n, s3);
+    double rd = 0, ro = 0, an = 0, low = 0;
+    for (double x : A) an = std::max(an, std::fabs(x));
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        double s = 0, o = 0;
+        for (int t = 0; t < n; ++t) {
+          s += A[i + t * n] * Zr[t + j * n] - Zr[i + t * n] * Tr[t + j * n];
+          o += Zr[t + i * n] * Zr[t + j * n];
+        }
+        rd = std::max(rd, std::fabs(s));
+        ro = std::max(ro, std::fabs(o - (i == j ? 1.0 : 0.0)));
+        if (i > j + 1 || (j < pr && i >= pr)) low = std::max(low, std::fabs(Tr[i + j * n]));
+      }
+    std::vector<cplx> got_ev;  // eigenvalues of the leading pr x pr blocks
+    for (int k = 0; k < pr; ++k) {
+      if (k + 1 < pr && Tr[(k + 1) + k * n] != 0.0) {
+        const double a = Tr[k + k * n], b = Tr[k + (k + 1) * n], c = Tr[(k + 1) + k * n], d = Tr[(k + 1) + (k + 1) * n];
+        const cplx h = 0.5 * (a + d), q = std::sqrt(cplx(0.25 * (a - d) * (a - d) + b * c));
+        got_ev.push_back(h + q);
+        got_ev.push_back(h - q);
+        ++k;
+      } else {
+        got_ev.push_back(Tr[k + k * n]);
+      }
+    }
+    // every selected eigenvalue is among the leading ones (the leading part
+    // may hold more: a selected pair member closes its 2 x 2 block)
+    double evd = 0;
+    std::vector<int> used(got_ev.size(), 0);
+    for (const cplx& w : want_ev) {
+      double bd = 1e300;
+      int bi = -1;
+      for (size_t q = 0; q < got_ev.size(); ++q)
+        if (!used[q] && std::abs(got_ev[q] - w) < bd) bd = std::abs(got_ev[q] - w), bi = static_cast<int>(q);
+      if (bi >= 0) used[bi] = 1;
+      evd = std::max(evd, bd / std::max(1.0, std::abs(w)));
+    }
+    const bool rok = pr >= p && (cs.second || pr == p) && rd < 1e-12 * n * std::max(1.0, an) && ro < 1e-12 * n &&
+                     low == 0.0 && evd < 1e-8;
+    std::printf("real reorder n=%d p=%d: defect %.2e orth %.2e below %.1e ev %.1e %s\n", n, pr, rd, ro, low, evd,
+                rok ? "rok" : "rFAIL");
+    fails += !rok;
   }
     // complex input (complex_schur_c): random complex matrices
   for (int n : {1, 2, 7, 40, 121}) {

@@ -17,3 +17,4 @@ def test_dense_kernels(tmp_path):
     assert r.returncode == 0, r.stdout
     assert r.stdout.count(" ok") == 7  # 5 random + 2 degenerate-cluster matrices
     assert r.stdout.count("zok") == 5  # complex_schur_c on random complex matrices
+    assert r.stdout.count(" rok") == 7  # real_schur_reorder on the same 7 matrices
