@@ -73,6 +73,76 @@ __global__ void spmv_op_k(int64_t n, const int64_t* __restrict__ rowptr,
   if (lane == 0) t[row] = s;
 }
 
+// Version 2 of the CSR products (RQB_SPMV=1 selects the version above): LPR
+// lanes per row (32 / LPR rows per warp, fewer idle lane slots on short
+// rows), and each lane issues the (col, value) loads of U entries (k, k + LPR,
+// ..., k + LPR (U - 1)) before any gather, so U entries per lane are in
+// flight instead of one; the pattern and values are read once per product,
+// so they are loaded with the streaming hint (evict-first) and the gathered
+// vector keeps its L2 lines.
+template <int U, int LPR>
+__global__ void __launch_bounds__(256) spmv_csr_k2(int64_t n, const int64_t* __restrict__ rowptr,
+                                                  const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                  const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
+  const int sl = threadIdx.x & (LPR - 1);
+  double s = 0.0;
+  if (row < n) {
+    const int64_t e = __ldg(&rowptr[row + 1]);
+    for (int64_t k0 = __ldg(&rowptr[row]) + sl; k0 < e; k0 += LPR * U) {
+      int c[U];
+      double a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + LPR * u;
+        c[u] = k < e ? __ldcs(&col[k]) : -1;
+        a[u] = k < e ? __ldcs(&val[k]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c[u] >= 0) s += a[u] * __ldg(&x[c[u]]);
+    }
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (row < n && sl == 0) y[row] = s;
+}
+
+template <int U, int LPR>
+__global__ void __launch_bounds__(256) spmv_op_k2(int64_t n, const int64_t* __restrict__ rowptr,
+                                                 const int32_t* __restrict__ col, const double* __restrict__ Cv,
+                                                 const double* __restrict__ Mv, double sigma,
+                                                 const double* __restrict__ vu, const double* __restrict__ vl,
+                                                 double* __restrict__ t) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
+  const int sl = threadIdx.x & (LPR - 1);
+  double s = 0.0;
+  if (row < n) {
+    const int64_t e = __ldg(&rowptr[row + 1]);
+    for (int64_t k0 = __ldg(&rowptr[row]) + sl; k0 < e; k0 += LPR * U) {
+      int c[U];
+      double cv[U], mv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + LPR * u;
+        const bool ok = k < e;
+        c[u] = ok ? __ldcs(&col[k]) : -1;
+        cv[u] = ok ? __ldcs(&Cv[k]) : 0.0;
+        mv[u] = ok ? __ldcs(&Mv[k]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c[u] >= 0) {
+          const double xu = __ldg(&vu[c[u]]);
+          s += cv[u] * xu + mv[u] * (sigma * xu + __ldg(&vl[c[u]]));
+        }
+    }
+  }
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (row < n && sl == 0) t[row] = s;
+}
+
 // part[b * k + i] = sum over block b's slice of V[i] . w  (w given as two halves)
 // part[b*k + i] = V[i][chunk b] . w[chunk b]: the block stages its chunk of
 // w in shared memory once; each warp then owns basis vectors i = warp (mod 8),
@@ -399,6 +469,155 @@ __global__ void spmm_csr_k(int64_t n, const int64_t* __restrict__ rowptr, const 
   }
 }
 
+// 32-byte read-only gather (one LDG.E.256: a whole 4-wide row of an
+// interleaved block in one sector access instead of two 16-byte loads)
+__device__ __forceinline__ void ldg4(const double* p, double* v) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+
+// Version 2 of the two block products (see spmv_op_k2): U entries per lane
+// in flight, streaming loads of the pattern and values, 32-byte gathers of
+// the interleaved rows.
+template <int KB, int U, int LPR>
+__global__ void __launch_bounds__(256) spmm_op_k2(int64_t n, const int64_t* __restrict__ rowptr,
+                                                 const int32_t* __restrict__ col, const double* __restrict__ Cv,
+                                                 const double* __restrict__ Mv, double sigma,
+                                                 const double* __restrict__ Xi, double* __restrict__ Ti) {
+  // LPR lanes per row (32 / LPR rows per warp): fewer idle lane slots on
+  // short rows; every lane reaches the shuffles (no early exit)
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
+  const int sl = threadIdx.x & (LPR - 1);
+  double s[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) s[j] = 0.0;
+  if (row < n) {
+    const int64_t e = __ldg(&rowptr[row + 1]);
+    for (int64_t k0 = __ldg(&rowptr[row]) + sl; k0 < e; k0 += LPR * U) {
+      int c[U];
+      double cv[U], mv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + LPR * u;
+        const bool ok = k < e;
+        c[u] = ok ? __ldcs(&col[k]) : -1;
+        cv[u] = ok ? __ldcs(&Cv[k]) : 0.0;
+        mv[u] = ok ? __ldcs(&Mv[k]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c[u] >= 0) {
+          double a[KB], l[KB];
+#pragma unroll
+          for (int q = 0; q < KB / 4; ++q) {
+            ldg4(Xi + (int64_t)c[u] * KB + 4 * q, a + 4 * q);
+            ldg4(Xi + (n + c[u]) * KB + 4 * q, l + 4 * q);
+          }
+#pragma unroll
+          for (int j = 0; j < KB; ++j) s[j] += cv[u] * a[j] + mv[u] * (sigma * a[j] + l[j]);
+        }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KB; ++j)
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) s[j] += __shfl_xor_sync(0xffffffffu, s[j], o);
+  if (row < n && sl == 0) {
+    double2* o = reinterpret_cast<double2*>(Ti + row * KB);
+#pragma unroll
+    for (int q = 0; q < KB / 2; ++q) o[q] = make_double2(s[2 * q], s[2 * q + 1]);
+  }
+}
+
+template <int KB, int U, int LPR>
+__global__ void __launch_bounds__(256) spmm_csr_k2(int64_t n, const int64_t* __restrict__ rowptr,
+                                                  const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                  const double* __restrict__ Xi, int w, double* __restrict__ Y,
+                                                  int64_t ldy) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR;
+  const int sl = threadIdx.x & (LPR - 1);
+  double s[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) s[j] = 0.0;
+  if (row < n) {
+    const int64_t e = __ldg(&rowptr[row + 1]);
+    for (int64_t k0 = __ldg(&rowptr[row]) + sl; k0 < e; k0 += LPR * U) {
+      int c[U];
+      double a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + LPR * u;
+        c[u] = k < e ? __ldcs(&col[k]) : -1;
+        a[u] = k < e ? __ldcs(&val[k]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c[u] >= 0) {
+          double x[KB];
+#pragma unroll
+          for (int q = 0; q < KB / 4; ++q) ldg4(Xi + (int64_t)c[u] * KB + 4 * q, x + 4 * q);
+#pragma unroll
+          for (int j = 0; j < KB; ++j) s[j] += a[u] * x[j];
+        }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) s[j] += __shfl_xor_sync(0xffffffffu, s[j], o);
+    if (row < n && sl == 0 && j < w) Y[j * ldy + row] = s[j];
+  }
+}
+
+namespace {
+
+int spmv_version() {
+  static const int v = std::getenv("RQB_SPMV") ? std::atoi(std::getenv("RQB_SPMV")) : 2;
+  return v;
+}
+
+// Version 2 launch shapes (measured at cfg4_riga, ~68 nonzeros per row): 8
+// lanes per row with 5 entries in flight per lane for the single-vector and
+// width-4 products, 4 lanes per row for width 8 (32 lanes x 3: 0.205 / 0.416 /
+// 0.842 ms; 16 x 5: 0.174 / 0.298 / 0.629; 8 x 5: 0.172 / 0.263 / 0.590;
+// 4 x 5: - / 0.269 / 0.513 for the operator SpMV / width-4 / width-8 SpMM)
+void launch_spmv_csr(int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x, double* y,
+                     cudaStream_t st) {
+  if (spmv_version() == 1)
+    spmv_csr_k<<<div_up(n * 32, 256), 256, 0, st>>>(n, rp, col, val, x, y);
+  else
+    spmv_csr_k2<5, 8><<<div_up(n * 8, 256), 256, 0, st>>>(n, rp, col, val, x, y);
+}
+
+void launch_spmv_op(int64_t n, const int64_t* rp, const int32_t* col, const double* Cv, const double* Mv,
+                    double sigma, const double* vu, const double* vl, double* t, cudaStream_t st) {
+  if (spmv_version() == 1)
+    spmv_op_k<<<div_up(n * 32, 256), 256, 0, st>>>(n, rp, col, Cv, Mv, sigma, vu, vl, t);
+  else
+    spmv_op_k2<5, 8><<<div_up(n * 8, 256), 256, 0, st>>>(n, rp, col, Cv, Mv, sigma, vu, vl, t);
+}
+
+template <int KB>
+void launch_spmm_op(int64_t n, const int64_t* rp, const int32_t* col, const double* Cv, const double* Mv,
+                    double sigma, const double* Xi, double* Ti, cudaStream_t st) {
+  constexpr int kL = KB <= 4 ? 8 : 4;
+  if (spmv_version() == 1)
+    spmm_op_k<KB><<<div_up(n * 32, 256), 256, 0, st>>>(n, rp, col, Cv, Mv, sigma, Xi, Ti);
+  else
+    spmm_op_k2<KB, 5, kL><<<div_up(n * kL, 256), 256, 0, st>>>(n, rp, col, Cv, Mv, sigma, Xi, Ti);
+}
+
+template <int KB>
+void launch_spmm_csr(int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* Xi, int w,
+                     double* Y, int64_t ldy, cudaStream_t st) {
+  constexpr int kL = KB <= 4 ? 8 : 4;
+  if (spmv_version() == 1)
+    spmm_csr_k<KB><<<div_up(n * 32, 256), 256, 0, st>>>(n, rp, col, val, Xi, w, Y, ldy);
+  else
+    spmm_csr_k2<KB, 5, kL><<<div_up(n * kL, 256), 256, 0, st>>>(n, rp, col, val, Xi, w, Y, ldy);
+}
+
+}  // namespace
+
 // part[(b * k + i) * bs + j] = V[i][chunk b] . R[j][chunk b]: the block stages
 // its chunk of the bs vectors of R in shared memory ([j][t], conflict-free),
 // each warp owns basis vectors i = warp (mod 8), four at a time; every basis
@@ -699,16 +918,14 @@ void OperatorEngine::spmv(int which, const double* x, double* y) {
                       : which == 1 ? d_C.as<double>()
                       : which == 2 ? d_M.as<double>()
                                    : d_Q.as<double>();
-  spmv_csr_k<<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
-                                                      val, x, y);
+  launch_spmv_csr(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), val, x, y, stream);
   ++launches;
 }
 
 void OperatorEngine::apply(const double* v, double* r) {
   double* t = d_t.as<double>();
-  spmv_op_k<<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
-                                                     d_C.as<double>(), d_M.as<double>(), sigma, v,
-                                                     v + n, t);
+  launch_spmv_op(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_C.as<double>(), d_M.as<double>(), sigma, v, v + n,
+                 t, stream);
   ++launches;
   // r_u = -Q(s)^{-1} t ; r_l = s r_u + v_u (fused in the backward sweep)
   rqb_solve_enqueue(*fac, t, r, -1.0, v, sigma, r + n);
@@ -748,12 +965,12 @@ void OperatorEngine::apply_block(const double* V, int bs, double* R) {
   const int kb = bs <= 4 ? 4 : 8;
   if (kb == 4) {
     interleave_k<4><<<grid, 256, 0, stream>>>(V, n2, n2, bs, Xi);
-    spmm_op_k<4><<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
-                                                          d_C.as<double>(), d_M.as<double>(), sigma, Xi, Ti);
+    launch_spmm_op<4>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_C.as<double>(), d_M.as<double>(), sigma, Xi,
+                        Ti, stream);
   } else {
     interleave_k<8><<<grid, 256, 0, stream>>>(V, n2, n2, bs, Xi);
-    spmm_op_k<8><<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
-                                                          d_C.as<double>(), d_M.as<double>(), sigma, Xi, Ti);
+    launch_spmm_op<8>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_C.as<double>(), d_M.as<double>(), sigma, Xi,
+                        Ti, stream);
   }
   launches += 2;
   // R_u = -Q(s)^{-1} T ; R_l = s R_u + V_u (fused in the backward sweep), bs vectors per pass
@@ -769,12 +986,10 @@ void OperatorEngine::mspmv_block(const double* R, int w, double* Wl) {
   const int grid = std::min(div_up(n, 256), 148 * 8);
   if (w <= 4) {
     interleave_k<4><<<grid, 256, 0, stream>>>(R + n, n2, n, w, Xi);
-    spmm_csr_k<4><<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
-                                                           d_M.as<double>(), Xi, w, Wl, n);
+    launch_spmm_csr<4>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_M.as<double>(), Xi, w, Wl, n, stream);
   } else {
     interleave_k<8><<<grid, 256, 0, stream>>>(R + n, n2, n, w, Xi);
-    spmm_csr_k<8><<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
-                                                           d_M.as<double>(), Xi, w, Wl, n);
+    launch_spmm_csr<8>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_M.as<double>(), Xi, w, Wl, n, stream);
   }
   launches += 2;
 }
@@ -962,7 +1177,7 @@ double OperatorEngine::time_op(int what, int iters, int param) {
     RQB_CUDA(cudaMemsetAsync(h.p, 0, h.bytes, stream));
     prepare_block((param & 0xffff) + 8, 8);
   }
-  if (what == 9 || what == 10) {  // block apply / multi-RHS solve of param (<= 8) vectors
+  if (what == 9 || what == 10 || what == 13 || what == 14) {  // block apply / multi-RHS solve / block SpMMs
     Vb.alloc(sizeof(double) * n2 * 8);
     Rb.alloc(sizeof(double) * n2 * 8);
     RQB_CUDA(cudaMemsetAsync(Vb.p, 0, Vb.bytes, stream));
@@ -980,9 +1195,24 @@ double OperatorEngine::time_op(int what, int iters, int param) {
       case 0: apply(a.as<double>(), b.as<double>()); break;
       case 1: fac->solve_device(a.as<double>(), b.as<double>(), 1.0); break;
       case 2:
-        spmv_op_k<<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
-                                                           d_C.as<double>(), d_M.as<double>(), sigma,
-                                                           a.as<double>(), a.as<double>() + n, b.as<double>());
+        launch_spmv_op(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_C.as<double>(), d_M.as<double>(), sigma,
+                       a.as<double>(), a.as<double>() + n, b.as<double>(), stream);
+        break;
+      case 13:  // block SpMM of the operator (C, M) on an interleaved block of k (4 or 8) vectors
+        if (k <= 4)
+          launch_spmm_op<4>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_C.as<double>(), d_M.as<double>(), sigma,
+                            Vb.as<double>(), Rb.as<double>(), stream);
+        else
+          launch_spmm_op<8>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_C.as<double>(), d_M.as<double>(), sigma,
+                            Vb.as<double>(), Rb.as<double>(), stream);
+        break;
+      case 14:  // block M-SpMM (intra-block CGS tracking) on an interleaved block of k vectors
+        if (k <= 4)
+          launch_spmm_csr<4>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_M.as<double>(), Vb.as<double>(), k,
+                             Rb.as<double>(), n, stream);
+        else
+          launch_spmm_csr<8>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), d_M.as<double>(), Vb.as<double>(), k,
+                             Rb.as<double>(), n, stream);
         break;
       case 3: gemv_t(V.as<double>(), k, a.as<double>(), h.as<double>()); break;
       case 4: gemv_n(V.as<double>(), k, h.as<double>(), a.as<double>(), nullptr); break;
@@ -1109,8 +1339,8 @@ GhEngine::GhEngine(int64_t n_, const int64_t* rowptr, const int32_t* col, const 
 }
 
 void GhEngine::spmv(int which, const double* x, double* y) {
-  spmv_csr_k<<<div_up(n * 32, 256), 256, 0, stream>>>(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(),
-                                                      which == 0 ? d_A.as<double>() : d_B.as<double>(), x, y);
+  launch_spmv_csr(n, d_rowptr.as<int64_t>(), d_col.as<int32_t>(), which == 0 ? d_A.as<double>() : d_B.as<double>(),
+                  x, y, stream);
   ++launches;
 }
 
