@@ -678,6 +678,99 @@ __global__ void __launch_bounds__(kRedThreads) gemm_t_part(const double* __restr
   }
 }
 
+// Persistent form of gemm_t_part: block g takes chunks g, g + G, ... (G =
+// gridDim.x), keeps its k x bs sums in shared memory (entry (i, j) is owned
+// by warp i mod 8, so no races) and writes them once: G partial rows instead
+// of one per chunk, so the final reduction reads G (a few hundred) rows with
+// coalesced loads. 16 loads in flight per lane (4 vectors x 4 entries).
+template <int KB>
+__global__ void __launch_bounds__(kRedThreads) gemm_t_pers(const double* __restrict__ V, int k, int64_t n2,
+                                                         const double* __restrict__ R, int bs, int chunk, int nchunks,
+                                                         double* __restrict__ part) {
+  extern __shared__ double smem[];
+  double* rs = smem;                    // [j][chunk]
+  double* hsum = smem + KB * chunk;     // [i][bs]
+  for (int x = threadIdx.x; x < k * bs; x += kRedThreads) hsum[x] = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kW = kRedThreads / 32, kV = 4;
+  for (int b = blockIdx.x; b < nchunks; b += gridDim.x) {
+    const int64_t e0 = (int64_t)b * chunk;
+    const int len = static_cast<int>(min((int64_t)chunk, n2 - e0));
+    __syncthreads();  // the previous chunk is done with rs
+    for (int j = 0; j < bs; ++j)
+      for (int t = threadIdx.x; t < len; t += kRedThreads) rs[j * chunk + t] = R[j * n2 + e0 + t];
+    __syncthreads();
+    for (int i = warp; i < k; i += kV * kW) {
+      const double* vp[kV];
+#pragma unroll
+      for (int q = 0; q < kV; ++q) vp[q] = V + (int64_t)(i + q * kW < k ? i + q * kW : i) * n2 + e0;
+      double acc[kV][KB];
+#pragma unroll
+      for (int q = 0; q < kV; ++q)
+#pragma unroll
+        for (int j = 0; j < KB; ++j) acc[q][j] = 0.0;
+      int t = lane;
+      for (; t + 96 < len; t += 128) {
+        double a[kV][4];
+#pragma unroll
+        for (int q = 0; q < kV; ++q)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a[q][u] = vp[q][t + 32 * u];
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (j < bs) {
+            const double* xr = rs + j * chunk + t;
+            const double x0 = xr[0], x1 = xr[32], x2 = xr[64], x3 = xr[96];
+#pragma unroll
+            for (int q = 0; q < kV; ++q) acc[q][j] += (a[q][0] * x0 + a[q][1] * x1) + (a[q][2] * x2 + a[q][3] * x3);
+          }
+      }
+      for (; t < len; t += 32) {
+        double a[kV];
+#pragma unroll
+        for (int q = 0; q < kV; ++q) a[q] = vp[q][t];
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (j < bs) {
+            const double x0 = rs[j * chunk + t];
+#pragma unroll
+            for (int q = 0; q < kV; ++q) acc[q][j] += a[q] * x0;
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < kV; ++q)
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+          const double sq = warp_sum(acc[q][j]);
+          if (lane == 0 && j < bs && i + q * kW < k) hsum[(i + q * kW) * bs + j] += sq;
+        }
+    }
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < k * bs; x += kRedThreads) part[(int64_t)blockIdx.x * k * bs + x] = hsum[x];
+}
+
+// H[i + j ldh] = sum_g part[g * k bs + i bs + j]: 32 consecutive entries per
+// block, its 8 warps take every 8th partial row (coalesced 256-byte loads),
+// combined in warp order (deterministic)
+__global__ void __launch_bounds__(256) reduce_rows_k(const double* __restrict__ part, int g, int kb, int bs,
+                                                     double* __restrict__ H, int ldh) {
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (x < kb)
+    for (int r = warp; r < g; r += 8) s += part[(int64_t)r * kb + x];
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && x < kb) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    H[x / bs + (int64_t)(x % bs) * ldh] = t;
+  }
+}
+
 // H[i + j ldh] = sum_b part[(b * k + i) * bs + j] (fixed order), one warp per entry
 __global__ void reduce_parts_blk(const double* __restrict__ part, int nb, int k, int bs, double* __restrict__ H,
                                  int ldh) {
@@ -704,12 +797,12 @@ __global__ void gemm_n_k(const double* __restrict__ V, int k, int64_t n2, const 
 #pragma unroll
     for (int j = 0; j < KB; ++j) s[j] = 0.0;
     int i = 0;
-    for (; i + 3 < k; i += 4) {
-      double a[4];
+    for (; i + 7 < k; i += 8) {  // 8 loads in flight per thread
+      double a[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = V[(int64_t)(i + u) * n2 + e];
+      for (int u = 0; u < 8; ++u) a[u] = V[(int64_t)(i + u) * n2 + e];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int j = 0; j < KB; ++j) s[j] += a[u] * hs[(i + u) * KB + j];
     }
@@ -1015,6 +1108,23 @@ void OperatorEngine::gemm_t(const double* V, int k, const double* R, int bs, dou
   const int nb = static_cast<int>((n2 + kChunk - 1) / kChunk);
   const size_t need = sizeof(double) * static_cast<size_t>(nb) * k * bs;
   if (d_bpart.bytes < need) d_bpart.alloc(need);
+  // (width 8 keeps the per-chunk form: its persistent variant needs 140
+  // registers, one block per SM, and measured slower: 0.61 -> 0.72 ms at k = 160)
+  static const bool pers = !std::getenv("RQB_GEMMT") || std::atoi(std::getenv("RQB_GEMMT")) != 1;
+  if (pers && bs <= 4) {
+    // persistent: one wave of resident blocks (smem: the R chunk + the k x bs sums)
+    const size_t sm = sizeof(double) * (static_cast<size_t>(kChunk) * 4 + static_cast<size_t>(k) * bs);
+    auto kern = gemm_t_pers<4>;
+    smem_at_least(kern, sm);
+    int occ = 1;
+    RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRedThreads, sm));
+    const int g = std::min(nb, 148 * std::max(1, occ));
+    kern<<<g, kRedThreads, sm, stream>>>(V, k, n2, R, bs, static_cast<int>(kChunk), nb, d_bpart.as<double>());
+    reduce_rows_k<<<div_up(static_cast<int64_t>(k) * bs, 32), 256, 0, stream>>>(d_bpart.as<double>(), g, k * bs, bs,
+                                                                                H, ldh);
+    launches += 2;
+    return;
+  }
   const size_t sm = sizeof(double) * kChunk * bs;
   if (bs <= 4)
     gemm_t_part<4><<<nb, kRedThreads, sm, stream>>>(V, k, n2, R, bs, kChunk, d_bpart.as<double>());
