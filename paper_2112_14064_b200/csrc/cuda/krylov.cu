@@ -827,45 +827,35 @@ __global__ void sum_rows(const double* __restrict__ part, int nb, double* __rest
 
 
 // ---------------------------------------------------------------------------
-OperatorEngine::OperatorEngine(int64_t n_, const int64_t* rowptr, const int32_t* col,
-                               const double* K, const double* C, const double* M,
-                               const Symbolic& s, double sigma_, bool scaling)
-    : n(n_) {
-  nnz = rowptr[n];
-  varsigma = 1.0;
-  if (scaling) {
-    // scale_pencil: varsigma = sqrt(maxabs K / maxabs M)
-    double mk = 0, mm = 0;
-    for (int64_t k = 0; k < nnz; ++k) mk = std::max(mk, std::fabs(K[k])), mm = std::max(mm, std::fabs(M[k]));
-    if (!(mm > 0)) fail(errc::domain, "scale_pencil: zero M norm");
-    varsigma = std::sqrt(mk / mm);
-  }
-  sigma = sigma_ / varsigma;
+// From host arrays: the pattern and K, C, M are uploaded once (pageable
+// copies) into a temporary device pencil and the device constructor forms
+// varsigma, the scaled C / M, Q(s) and the 1-norms there (the same rounding as
+// the host formulas: the resident-pencil test checks the two paths bitwise).
+std::unique_ptr<DevicePencil> OperatorEngine::upload_pencil(int64_t n, const int64_t* rowptr, const int32_t* col,
+                                                            const double* K, const double* C, const double* M) {
   SetupTrace tr("OperatorEngine(host)");
-  std::vector<double> Cs(nnz), Ms(nnz), Q(nnz);
-  const double v = varsigma, v2 = varsigma * varsigma;
-  for (int64_t k = 0; k < nnz; ++k) {
-    Cs[k] = scaling ? v * C[k] : C[k];
-    Ms[k] = scaling ? v2 * M[k] : M[k];
-  }
-  // Q(s) on the shared pattern, formed on the host once: K + s C + s^2 M
-  for (int64_t k = 0; k < nnz; ++k) Q[k] = K[k] + sigma_ * C[k] + sigma_ * sigma_ * M[k];
-  tr.mark("scale+Q");
-  d_rowptr.alloc(sizeof(int64_t) * (n + 1));
-  d_col.alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
-  RQB_CUDA(cudaMemcpy(d_rowptr.p, rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
-  RQB_CUDA(cudaMemcpy(d_col.p, col, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
-  fac = std::make_unique<FactorEngine>(s, n, rowptr, col, Q.data(), d_rowptr.as<int64_t>(),
-                                       d_col.as<int32_t>());
-  tr.mark("FactorEngine");
-  stream = fac->stream;
-  d_K.upload(K, sizeof(double) * nnz, stream);
-  d_C.upload(Cs.data(), sizeof(double) * nnz, stream);
-  d_M.upload(Ms.data(), sizeof(double) * nnz, stream);
-  d_Q.upload(Q.data(), sizeof(double) * nnz, stream);
+  auto dp = std::make_unique<DevicePencil>();
+  dp->n = n;
+  dp->nnz = rowptr[n];
+  RQB_CUDA(cudaGetDevice(&dp->device));
+  const int64_t nnz = dp->nnz;
+  dp->d_rowptr.alloc(sizeof(int64_t) * (n + 1));
+  dp->d_col.alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  dp->d_val.alloc(sizeof(double) * std::max<int64_t>(3 * nnz, 1));
+  RQB_CUDA(cudaMemcpy(dp->d_rowptr.p, rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+  RQB_CUDA(cudaMemcpy(dp->d_col.p, col, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+  double* v = dp->d_val.as<double>();
+  RQB_CUDA(cudaMemcpy(v, K, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  RQB_CUDA(cudaMemcpy(v + nnz, C, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  RQB_CUDA(cudaMemcpy(v + 2 * nnz, M, sizeof(double) * nnz, cudaMemcpyHostToDevice));
   tr.mark("uploads");
-  init_workspaces();
+  return dp;
 }
+
+OperatorEngine::OperatorEngine(int64_t n_, const int64_t* rowptr, const int32_t* col, const double* K,
+                               const double* C, const double* M, const Symbolic& s, double sigma_, bool scaling,
+                               double* norms1)
+    : OperatorEngine(*upload_pencil(n_, rowptr, col, K, C, M), rowptr, col, s, sigma_, scaling, norms1) {}
 
 namespace {
 

@@ -220,15 +220,19 @@ struct OperatorEngine {
   int64_t gemv_t_chunk = 256;  // CGS projection: entries per block, blocks
   int gemv_t_blocks = 1;
 
+  // From host arrays (uploaded once; varsigma, C / M scaling, Q(s) and the
+  // 1-norms, when norms1 is given, formed on the device as below).
   OperatorEngine(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
                  const double* C, const double* M, const Symbolic& s, double sigma,
-                 bool scaling);
+                 bool scaling, double* norms1 = nullptr);
   // From a device-resident pencil (host copy of the pattern for the symbolic
   // scatter maps): scaling, C/M scaling, Q(s) and the 1-norms of K, vC, v^2 M
   // (norms1) are formed on the device with the host constructor's rounding.
   OperatorEngine(const DevicePencil& dp, const int64_t* rowptr_h, const int32_t* col_h,
                  const Symbolic& s, double sigma, bool scaling, double* norms1);
   ~OperatorEngine();
+  static std::unique_ptr<DevicePencil> upload_pencil(int64_t n, const int64_t* rowptr, const int32_t* col,
+                                                     const double* K, const double* C, const double* M);
   // Device vector ops (2n vectors: upper; lower), all enqueued on `stream`.
   void spmv(int which, const double* x, double* y);          // y = A x
   void apply(const double* v, double* r);                    // r = L(s)^{-1} B v

@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <array>
+#include <future>
 #include <mutex>
 #include <string>
 
@@ -79,6 +81,28 @@ rqb::VectorSpace space_of(const rq_space_desc* d) {
   if (d->kind != RQ_SPACE_CURL && d->kind != RQ_SPACE_DIV) rqb::fail(rqb::errc::config, "unknown space kind");
   return rqb::build_space(d->kind == RQ_SPACE_CURL ? rqb::SpaceKind::curl : rqb::SpaceKind::div, d->degree,
                           d->elems, d->levels);
+}
+
+// 1-norms (max column sum of |a|) of K, v C and v^2 M in one pass, columns
+// accumulated in row order (the sequence norm1 below adds)
+std::array<double, 3> norms1_3(int64_t n, const int64_t* rowptr, const int32_t* col, const double* K,
+                               const double* C, const double* M, double v) {
+  std::vector<double> c0(n, 0.0), c1(n, 0.0), c2(n, 0.0);
+  const double vv = v * v;
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t k = rowptr[r]; k < rowptr[r + 1]; ++k) {
+      const int32_t c = col[k];
+      c0[c] += std::fabs(K[k]);
+      c1[c] += std::fabs(v * C[k]);
+      c2[c] += std::fabs(vv * M[k]);
+    }
+  std::array<double, 3> out{0.0, 0.0, 0.0};
+  for (int64_t j = 0; j < n; ++j) {
+    out[0] = std::max(out[0], c0[j]);
+    out[1] = std::max(out[1], c1[j]);
+    out[2] = std::max(out[2], c2[j]);
+  }
+  return out;
 }
 
 double norm1(int64_t n, const int64_t* rowptr, const int32_t* col, const std::vector<double>& v) {
@@ -522,16 +546,27 @@ int rq_operator_create(int64_t n, const int64_t* rowptr, const int32_t* col, con
     need(out, "out");
     if (!std::isfinite(opts->sigma)) rqb::fail(rqb::errc::config, "shift must be finite and real");
     auto o = std::make_unique<rq_operator>();
-    o->op = std::make_unique<rqb::OperatorEngine>(n, rowptr, col, K, C, M, s->S, opts->sigma,
-                                                  opts->scaling != 0);
-    const int64_t nnz = rowptr[n];
-    const double v = o->op->varsigma;
-    std::vector<double> tmp(K, K + nnz);
-    o->norms1[0] = norm1(n, rowptr, col, tmp);
-    for (int64_t k = 0; k < nnz; ++k) tmp[k] = v * C[k];
-    o->norms1[1] = norm1(n, rowptr, col, tmp);
-    for (int64_t k = 0; k < nnz; ++k) tmp[k] = v * v * M[k];
-    o->norms1[2] = norm1(n, rowptr, col, tmp);
+    // the residual 1-norms of K, varsigma C, varsigma^2 M (true column sums: the
+    // host pencil need not be symmetric) on a host thread while the engine
+    // uploads the pencil and factors Q(s)
+    const bool scaling = opts->scaling != 0;
+    auto norms = std::async(std::launch::async, [&] {
+      double v = 1.0;
+      if (scaling) {
+        double mk = 0, mm = 0;
+        for (int64_t k = 0; k < rowptr[n]; ++k) mk = std::max(mk, std::fabs(K[k])), mm = std::max(mm, std::fabs(M[k]));
+        if (mm > 0) v = std::sqrt(mk / mm);
+      }
+      return norms1_3(n, rowptr, col, K, C, M, v);
+    });
+    try {
+      o->op = std::make_unique<rqb::OperatorEngine>(n, rowptr, col, K, C, M, s->S, opts->sigma, scaling);
+    } catch (...) {
+      norms.wait();
+      throw;
+    }
+    const std::array<double, 3> nr = norms.get();
+    for (int i = 0; i < 3; ++i) o->norms1[i] = nr[i];
     finish_operator(o.get());
     *out = o.release();
   });
