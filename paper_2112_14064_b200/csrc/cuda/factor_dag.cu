@@ -372,6 +372,15 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
+  // development profile (RQB_DAG_TRACE-free): sub-phase SM cycles in prof[24..29]
+  long long tph = A.prof ? clock64() : 0;
+  auto phase = [&](int k) {
+    if (A.prof && threadIdx.x == 0) {
+      const long long t = clock64();
+      atomicAdd(&A.prof[24 + k], (unsigned long long)(t - tph));
+      tph = t;
+    }
+  };
   double* Cb = sm;                             // (r, c < np)   -> Cb[r + c * ldc]
   double* Rb = sm + (int64_t)ldc * np;         // (r < np, c >= np) -> Rb[r + (c - np) * ldr]
   if (F.nchild > 0) {
@@ -380,6 +389,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
     if (F.nchild > 1) hi[1] = A.fronts[F.child1].nf - A.fronts[F.child1].npiv;
     extend_add(A, F, lo, hi, lo, hi, g, ld, true);  // ends with a barrier
   }
+  phase(1);
   // the cross in flight at once (one latency); the lines were never read
   // through L1 in this launch (extend_add reads with ld.cg)
   for (int c = warp; c < nf; c += kDT / 32) {
@@ -389,6 +399,7 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  phase(2);
   __shared__ double red_s[kDT / 32];
   __shared__ double urow_s[2][kPB];
   __shared__ int any_swap_s;
@@ -530,13 +541,17 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
     if (t0 < np && np < nf) cross_update<false>(Cb, ldc, Rb, ldr, np, Rb, ldr, np, t0, np, np, nf, k0, pw);
     __syncthreads();
   }
+  phase(3);
   for (int c = warp; c < nf; c += kDT / 32) {
     const int rows = c < np ? nf : np;
     const double* src = c < np ? Cb + (int64_t)c * ldc : Rb + (int64_t)(c - np) * ldr;
     for (int r = lane; r < rows; r += 32) g[r + (int64_t)c * ld] = src[r];
   }
+  phase(4);
   // contribution block: one K = npiv pass, operands from the cross
   if (np < nf) cross_update<true>(Cb, ldc, Rb, ldr, np, g, ld, 0, np, nf, np, nf, 0, np);
+  if (A.prof) __syncthreads();
+  phase(5);
 }
 
 // DIAG: 32x32 diagonal block of panel s, unpivoted (speculative), in the
@@ -1209,9 +1224,12 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     }
     // ---- work (every predecessor has completed: no waits)
     switch (T.type) {
-      case T_SMALL:
+      case T_SMALL: {
+        const long long ta = A.prof ? clock64() : 0;
         if (A.lazy) assemble_region(A, F, t, 0, F.ld, 0, F.nf);
+        if (A.prof && tid == 0) atomicAdd(&A.prof[24], (unsigned long long)(clock64() - ta));
         small_front(A, F, sm, piv_sh);
+      }
         break;
       case T_ASM: {  // parent column block b, parent row block a (kAsmRowTiles tiles)
         if (A.lazy)
@@ -1858,6 +1876,10 @@ void rqb_dag_profile(FactorEngine& fe, double* out) {
   out[21] = h[21] / (clk_khz * 1.0);  // UPDCB busy ms (UPD in slot 5 holds the per-step updates only)
   out[22] = 0;
   out[23] = static_cast<double>(h[23]);
+  if (std::getenv("RQB_DAG_PROF_SMALL"))  // SMALL sub-phases, CTA-ms
+    std::fprintf(stderr, "[dag] SMALL phases ms: assemble %.1f extend_add %.1f load %.1f panels %.1f writeback %.1f cb_update %.1f\n",
+                 h[24] / (clk_khz * 1.0), h[25] / (clk_khz * 1.0), h[26] / (clk_khz * 1.0), h[27] / (clk_khz * 1.0),
+                 h[28] / (clk_khz * 1.0), h[29] / (clk_khz * 1.0));
   if (const char* path = std::getenv("RQB_DAG_TRACE")) {  // development trace: tasks + timestamps
     DagPlan& P = *fe.dag;
     std::vector<unsigned long long> tr(4 * static_cast<size_t>(P.ntasks));

@@ -84,6 +84,11 @@ struct MArgs {
   double sigma;
   double* xl;  // stride ldx
   int nrhs;
+  int warp_items;        // warp items batched (RQB_MWARP=0: every item CTA-wide)
+  int* blist;            // batch lists: warp items in the order they became ready (-1 unset)
+  int* pcnt;             // per level: warp items that became ready
+  const int32_t* bbase;  // per level: first blist entry
+  const int32_t* bcnt;   // per level: warp items that become ready during the sweep (this KR)
   int* stall;
   unsigned long long* trace;  // development trace (RQB_MSOLVE_TRACE): per item start, end
 };
@@ -130,7 +135,7 @@ __device__ __forceinline__ int mpop(const MArgs& A) {
   if (h >= A.nitems) return -1;
   int t;
   unsigned long long t0 = 0;
-  while ((t = ld_acq(&A.queue[h])) < 0) {
+  while ((t = ld_acq(&A.queue[h])) == -1) {
     if (ld_acq(A.done) >= A.nitems) return -1;
     __nanosleep(32);
     if (mstalled(A, t0)) return -1;
@@ -412,6 +417,171 @@ constexpr size_t msmem_bytes() {
   return sizeof(double) * (kMB * kDL + 4 * kMB * KR + kMB * KR + (kMStage > kMWholeNf ? kMStage : kMWholeNf) * KR);
 }
 
+// Warp items: whole-front items of the bottom levels with one pivot block
+// (npiv <= 64) and nf <= mwarp_nf<KR>() (MItem::pad == 1) are taken up to 8
+// at a time by one CTA, one front per warp, each warp in its own slice of the
+// CTA's shared memory with no CTA barrier: the bottom of the tree is a
+// throughput phase of thousands of independent 25-100 KB fronts whose
+// CTA-wide items were bound by their chain of dependent round trips (one item
+// in flight per CTA); eight per CTA keep eight chains in flight.
+template <int KR>
+constexpr int mwarp_doubles() {
+  return static_cast<int>(msmem_bytes<KR>() / sizeof(double) / (kMT / 32)) & ~1;
+}
+template <int KR>
+constexpr int mwarp_nf() {
+  return mwarp_doubles<KR>() / KR;
+}
+template <int KR>
+__device__ __forceinline__ bool mwarp_ok(const MItem& I) {  // MItem::pad: bit 0 fits KR <= 8, bit 1 KR = 4; level << 8
+  return I.blk == kMWhole && (I.pad & (KR == 4 ? 2 : 1)) != 0;
+}
+
+// A queue entry v <= -2 is a batch of warp items: blist[b0 .. b0 + cnt),
+// v = -2 - (8 b0 + cnt - 1). Batches are formed on the push side: a warp item
+// that becomes ready takes the next entry of its level's batch list; whoever
+// takes the 8th (or the level's last) entry pushes the batch once the earlier
+// entries are written (their writers already hold them), so a popped batch is
+// all ready items and never waits.
+__device__ __forceinline__ int mbatch_entry(int b0, int cnt) { return -2 - (8 * b0 + cnt - 1); }
+
+template <int KR>
+__device__ __forceinline__ void mpush_warp(const MArgs& A, int it, int level) {
+  const int base = A.bbase[level], total = A.bcnt[level];
+  const int i = atomicAdd(&A.pcnt[level], 1);
+  __threadfence();
+  atomicExch(&A.blist[base + i], it);
+  if ((i & 7) == 7 || i + 1 == total) {
+    const int s0 = i & ~7;
+    unsigned long long t0 = 0;
+    for (int j = s0; j < i; ++j)
+      while (ld_acq(&A.blist[base + j]) == -1)
+        if (mstalled(A, t0)) return;
+    __threadfence();
+    const int slot = atomicAdd(&A.qctl[1], 1);
+    atomicExch(&A.queue[slot], mbatch_entry(base + s0, i - s0 + 1));
+  }
+}
+
+// push front f's items, or f's warp item into its level's batch list
+template <int KR>
+__device__ __forceinline__ void mpush_any(const MArgs& A, int f, int from = 0) {
+  const int it = A.fbase[f];
+  if (A.warp_items && A.fcnt[f] == 1) {
+    const MItem& I = A.items[it];
+    if (mwarp_ok<KR>(I)) {
+      mpush_warp<KR>(A, it, I.pad >> 8);
+      return;
+    }
+  }
+  mpush(A, f, from);
+}
+
+// thread 0: decode a popped queue entry into batch_s (count) or -1 (single item)
+__device__ __forceinline__ int mdecode(const MArgs& A, int v, int* batch) {
+  if (v > -2) return 0;
+  const int code = -2 - v, b0 = code >> 3, cnt = (code & 7) + 1;
+  for (int w = 0; w < cnt; ++w) batch[w] = __ldcg(&A.blist[b0 + w]);
+  return cnt;
+}
+
+// forward warp item: w = b + children's contribution rows (wy, nf x KR);
+// y = inv(L11) w over the np <= 64 pivot rows (rows lane, lane + 32); the
+// contribution rows w - L21 y (two 32-row chunks at a time) -> the front's
+// contribution rows for the parent; then the parent's dependency count.
+template <int KR>
+__device__ void mfwd_warp(const MArgs& A, const MItem& I, double* wy, int lane) {
+  const int np = I.np, nf = I.nf;
+  const double* g = A.pool + I.goff;
+  const int64_t ld = I.ld;
+  for (int r = lane; r < nf; r += 32) {
+    const int4 src = __ldg(&A.gsrc[I.rows_off + r]);
+    double v[KR];
+#pragma unroll
+    for (int j = 0; j < KR; ++j) v[j] = (src.x >= 0 && j < A.nrhs) ? A.b[src.x * A.bsr + j * A.ldb] : 0.0;
+    if (src.y >= 0)
+#pragma unroll
+      for (int j = 0; j < KR; ++j) v[j] += __ldcg(&A.cbvec[(int64_t)src.y * KR + j]);
+    if (src.z >= 0)
+#pragma unroll
+      for (int j = 0; j < KR; ++j) v[j] += __ldcg(&A.cbvec[(int64_t)src.z * KR + j]);
+#pragma unroll
+    for (int j = 0; j < KR; ++j) wy[r * KR + j] = v[j];
+  }
+  __syncwarp();
+  const double* D = A.dinv + I.doff;  // np x np: strictly lower inv(L11), unit diagonal
+  const int r0 = lane, r1 = lane + 32;
+  double o0[KR], o1[KR];
+#pragma unroll
+  for (int j = 0; j < KR; ++j) o0[j] = o1[j] = 0.0;
+#pragma unroll 8
+  for (int c = 0; c < np; ++c) {
+    const double d0 = (r0 < np && c < r0) ? __ldg(&D[r0 + c * np]) : (c == r0 ? 1.0 : 0.0);
+    const double d1 = (r1 < np && c < r1) ? __ldg(&D[r1 + c * np]) : (c == r1 ? 1.0 : 0.0);
+    const double2* wp = reinterpret_cast<const double2*>(wy + c * KR);
+#pragma unroll
+    for (int q = 0; q < KR / 2; ++q) {
+      const double2 x = wp[q];
+      o0[2 * q] += d0 * x.x;
+      o0[2 * q + 1] += d0 * x.y;
+      o1[2 * q] += d1 * x.x;
+      o1[2 * q + 1] += d1 * x.y;
+    }
+  }
+  __syncwarp();  // every lane read w's pivot rows before they become y
+#pragma unroll
+  for (int j = 0; j < KR; ++j) {
+    if (r0 < np) {
+      wy[r0 * KR + j] = o0[j];
+      A.y[(int64_t)(I.start + r0) * KR + j] = o0[j];
+    }
+    if (r1 < np) {
+      wy[r1 * KR + j] = o1[j];
+      A.y[(int64_t)(I.start + r1) * KR + j] = o1[j];
+    }
+  }
+  __syncwarp();
+  for (int rb = np; rb < nf; rb += 64) {
+    const int ra = rb + lane, rc = rb + 32 + lane;
+    const bool oka = ra < nf, okc = rc < nf;
+    double a0[KR], a1[KR];
+#pragma unroll
+    for (int j = 0; j < KR; ++j) a0[j] = a1[j] = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < np; ++c) {
+      const double la = oka ? g[ra + (int64_t)c * ld] : 0.0;
+      const double lc = okc ? g[rc + (int64_t)c * ld] : 0.0;
+      const double2* yp = reinterpret_cast<const double2*>(wy + c * KR);
+#pragma unroll
+      for (int q = 0; q < KR / 2; ++q) {
+        const double2 x = yp[q];
+        a0[2 * q] += la * x.x;
+        a0[2 * q + 1] += la * x.y;
+        a1[2 * q] += lc * x.x;
+        a1[2 * q + 1] += lc * x.y;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KR; ++j) {
+      if (oka) A.cbvec[(int64_t)(I.cbvec_off + ra - np) * KR + j] = wy[ra * KR + j] - a0[j];
+      if (okc) A.cbvec[(int64_t)(I.cbvec_off + rc - np) * KR + j] = wy[rc * KR + j] - a1[j];
+    }
+  }
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) {
+    if (I.parent >= 0) {
+      int old;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(A.deps + I.parent) : "memory");
+      if (old == 1) {
+        __threadfence();
+        mpush_any<KR>(A, I.parent);
+      }
+    }
+    atomicAdd(A.done, 1);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // forward sweep
 template <int KR>
@@ -468,7 +638,8 @@ template <int KR, int kMinBlocks>
 __global__ void __launch_bounds__(kMT, kMinBlocks) mfwd_sweep(MArgs A) {
   extern __shared__ __align__(16) double msm[];
   MSmem<KR> S = carve<KR>(msm);
-  __shared__ int item_s, keep_s;
+  __shared__ int item_s, keep_s, nb_s;
+  __shared__ int batch_s[kMT / 32];
   const int tid = threadIdx.x, row = tid & (kMB - 1), grp = tid >> 6, jq = tid >> 6;
   if (tid == 0) keep_s = -1;
   for (;;) {
@@ -476,10 +647,21 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mfwd_sweep(MArgs A) {
     if (tid == 0) {
       item_s = keep_s >= 0 ? keep_s : mpop(A);
       keep_s = -1;
+      nb_s = mdecode(A, item_s, batch_s);
     }
     __syncthreads();
     const int it = item_s;
-    if (it < 0) return;
+    if (it == -1) return;
+    if (nb_s > 0) {  // one warp item per warp
+      const int w = tid >> 5, lane = tid & 31;
+      if (w < nb_s) {
+        const int wi = batch_s[w];
+        if (A.trace && lane == 0) A.trace[2 * (size_t)wi] = mtime();
+        mfwd_warp<KR>(A, A.items[wi], msm + w * mwarp_doubles<KR>(), lane);
+        if (A.trace && lane == 0) A.trace[2 * (size_t)wi + 1] = mtime();
+      }
+      continue;
+    }
     const MItem I = A.items[it];
     if (A.trace && tid == 0) A.trace[2 * (size_t)it] = mtime();
     if (I.blk == kMWhole) {
@@ -525,8 +707,12 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mfwd_sweep(MArgs A) {
         asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(A.deps + I.parent) : "memory");
         if (old == 1) {  // depth first: the parent's first item runs here next
           __threadfence();
-          mpush(A, I.parent, 1);
-          keep_s = A.fbase[I.parent];
+          if (A.warp_items && A.fcnt[I.parent] == 1 && mwarp_ok<KR>(A.items[A.fbase[I.parent]])) {
+            mpush_any<KR>(A, I.parent);
+          } else {
+            mpush(A, I.parent, 1);
+            keep_s = A.fbase[I.parent];
+          }
         }
       }
       atomicAdd(A.done, 1);
@@ -585,11 +771,87 @@ __device__ void mbwd_whole(const MArgs& A, const MItem& I, MSmem<KR>& S, int tid
   }
 }
 
+// backward warp item (see mfwd_warp): xs[c] = the ancestors' x of the
+// contribution columns c >= np; w = y - U12 x_cb over the pivot rows (rows
+// lane, lane + 32, kept in xs[0, np)); x = inv(U11) w; then the effective
+// children's dependency counts.
+template <int KR>
+__device__ void mbwd_warp(const MArgs& A, const MItem& I, double* xs, int lane) {
+  const int np = I.np, nf = I.nf;
+  const double* g = A.pool + I.goff;
+  const int64_t ld = I.ld;
+  const int32_t* rw = A.rows + I.rows_off;
+  for (int idx = lane; idx < (nf - np) * KR; idx += 32) {
+    const int c = np + idx / KR, j = idx % KR;
+    xs[c * KR + j] = __ldcg(&A.xnew[(int64_t)rw[c] * KR + j]);
+  }
+  __syncwarp();
+  const int r0 = lane, r1 = lane + 32;
+  const bool ok0 = r0 < np, ok1 = r1 < np;
+  double a0[KR], a1[KR];
+#pragma unroll
+  for (int j = 0; j < KR; ++j) a0[j] = a1[j] = 0.0;
+#pragma unroll 8
+  for (int c = np; c < nf; ++c) {
+    const double u0 = ok0 ? g[r0 + (int64_t)c * ld] : 0.0;
+    const double u1 = ok1 ? g[r1 + (int64_t)c * ld] : 0.0;
+    const double2* xp = reinterpret_cast<const double2*>(xs + c * KR);
+#pragma unroll
+    for (int q = 0; q < KR / 2; ++q) {
+      const double2 x = xp[q];
+      a0[2 * q] += u0 * x.x;
+      a0[2 * q + 1] += u0 * x.y;
+      a1[2 * q] += u1 * x.x;
+      a1[2 * q + 1] += u1 * x.y;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KR; ++j) {
+    if (ok0) xs[r0 * KR + j] = A.y[(int64_t)(I.start + r0) * KR + j] - a0[j];
+    if (ok1) xs[r1 * KR + j] = A.y[(int64_t)(I.start + r1) * KR + j] - a1[j];
+  }
+  __syncwarp();
+  const double* D = A.dinv + I.doff;  // np x np: upper inv(U11) (r <= c)
+  double o0[KR], o1[KR];
+#pragma unroll
+  for (int j = 0; j < KR; ++j) o0[j] = o1[j] = 0.0;
+#pragma unroll 8
+  for (int c = 0; c < np; ++c) {
+    const double d0 = (ok0 && r0 <= c) ? __ldg(&D[r0 + c * np]) : 0.0;
+    const double d1 = (ok1 && r1 <= c) ? __ldg(&D[r1 + c * np]) : 0.0;
+    const double2* wp = reinterpret_cast<const double2*>(xs + c * KR);
+#pragma unroll
+    for (int q = 0; q < KR / 2; ++q) {
+      const double2 x = wp[q];
+      o0[2 * q] += d0 * x.x;
+      o0[2 * q + 1] += d0 * x.y;
+      o1[2 * q] += d1 * x.x;
+      o1[2 * q + 1] += d1 * x.y;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KR; ++j) {
+    if (ok0) store_xm<KR>(A, I.start + r0, j, o0[j]);
+    if (ok1) store_xm<KR>(A, I.start + r1, j, o1[j]);
+  }
+  __threadfence();
+  __syncwarp();
+  for (int x = lane; x < I.nech; x += 32) {
+    const int f = A.ech[I.ech_off + x];
+    if (atomicSub(&A.deps[f], 1) == 1) {
+      __threadfence();
+      mpush_any<KR>(A, f);
+    }
+  }
+  if (lane == 0) atomicAdd(A.done, 1);
+}
+
 template <int KR, int kMinBlocks>
 __global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
   extern __shared__ __align__(16) double msm[];
   MSmem<KR> S = carve<KR>(msm);
-  __shared__ int item_s, keep_s;
+  __shared__ int item_s, keep_s, nb_s;
+  __shared__ int batch_s[kMT / 32];
   const int tid = threadIdx.x, row = tid & (kMB - 1), grp = tid >> 6, jq = tid >> 6;
   if (tid == 0) keep_s = -1;
   for (;;) {
@@ -597,10 +859,21 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
     if (tid == 0) {
       item_s = keep_s >= 0 ? keep_s : mpop(A);
       keep_s = -1;
+      nb_s = mdecode(A, item_s, batch_s);
     }
     __syncthreads();
     const int it = item_s;
-    if (it < 0) return;
+    if (it == -1) return;
+    if (nb_s > 0) {  // one warp item per warp
+      const int w = tid >> 5, lane = tid & 31;
+      if (w < nb_s) {
+        const int wi = batch_s[w];
+        if (A.trace && lane == 0) A.trace[2 * (size_t)wi] = mtime();
+        mbwd_warp<KR>(A, A.items[wi], msm + w * mwarp_doubles<KR>(), lane);
+        if (A.trace && lane == 0) A.trace[2 * (size_t)wi + 1] = mtime();
+      }
+      continue;
+    }
     const MItem I = A.items[it];
     if (A.trace && tid == 0) A.trace[2 * (size_t)it] = mtime();
     if (I.blk == kMPart) {
@@ -694,7 +967,9 @@ __global__ void __launch_bounds__(kMT, kMinBlocks) mbwd_sweep(MArgs A) {
         const int f = A.ech[I.ech_off + x];
         if (atomicSub(&A.deps[f], 1) == 1) {
           __threadfence();
-          if (x == 0) {  // the first effective child's first item runs here next
+          if (A.warp_items && A.fcnt[f] == 1 && mwarp_ok<KR>(A.items[A.fbase[f]])) {
+            mpush_any<KR>(A, f);
+          } else if (x == 0) {  // the first effective child's first item runs here next
             mpush(A, f, 1);
             keep_s = A.fbase[f];
           } else {
@@ -717,6 +992,9 @@ struct MSolvePlan {
   DeviceBuffer d_y, d_x, d_cb;  // interleaved, sized for 8 right-hand sides
   DeviceBuffer d_bpart;         // backward partial sums of wide fronts
   int64_t st_dep_f = 0, st_dep_b = 0, st_q_f = 0, st_q_b = 0, st_qctl = 0, st_pub = 0;
+  int64_t st_bl_f = 0, st_bl_b = 0, st_pc = 0;  // batch lists, per-level counters
+  int64_t mt_bb_f = 0, mt_bb_b = 0, mt_cf4 = 0, mt_cf8 = 0, mt_cb4 = 0, mt_cb8 = 0;
+  int nlev = 1;
   int grid4 = 148, grid8 = 148;
 };
 
@@ -781,12 +1059,22 @@ static void msolve_prepare(FactorEngine& fe) {
   };
   std::vector<MItem> fwd, bwd;
   std::vector<char> whole(nfr);
+  // warp items (mwarp_ok): whole items with one pivot block whose nf x KR
+  // staging fits a warp's slice; bit 0: KR <= 8, bit 1: KR = 4; level << 8
+  static const bool warp_items = !std::getenv("RQB_MWARP") || std::atoi(std::getenv("RQB_MWARP")) != 0;
+  auto wflags = [&](int f) {
+    const Front& F = S.fronts[f];
+    if (!warp_items || npb[f] != 1) return 0;
+    const int b = (F.nf <= mwarp_nf<8>() ? 1 : 0) | (F.nf <= mwarp_nf<4>() ? 2 : 0);
+    return b ? (b | (F.level << 8)) : 0;
+  };
   for (int f = 0; f < nfr; ++f) {
     const Front& F = S.fronts[f];
     whole[f] = npb[f] <= 2 && F.nf <= kMWholeNf && lvl_count[F.level] >= whole_min;
     fbase_f[f] = static_cast<int32_t>(fwd.size());
     if (whole[f]) {
       fwd.push_back(item(f, 0, F.nf, kMWhole));
+      fwd.back().pad = wflags(f);
     } else {
       for (int b = 0; b < npb[f]; ++b) fwd.push_back(item(f, b * kMB, std::min(F.npiv, (b + 1) * kMB), b));
       for (int r = F.npiv; r < F.nf; r += kMB) fwd.push_back(item(f, r, std::min(F.nf, r + kMB), -1));
@@ -802,6 +1090,7 @@ static void msolve_prepare(FactorEngine& fe) {
       const int ncb = F.nf - F.npiv;
       if (whole[f]) {
         bwd.push_back(item(f, 0, F.npiv, kMWhole));
+        bwd.back().pad = wflags(f);
       } else if (ncb > kMCbChunk) {
         // wide front: per pivot block, one partial item per kMCbChunk
         // contribution columns (independent, ahead of the blocks in the queue),
@@ -840,12 +1129,49 @@ static void msolve_prepare(FactorEngine& fe) {
   }
   std::vector<int32_t> qf(std::max<size_t>(1, fwd.size()), -1), qb(std::max<size_t>(1, bwd.size()), -1);
   int nq_f = 0, nq_b = 0;
+  // batch lists: forward = initial batches (ready leaves eligible for both
+  // KR, grouped by 8 here) + per-level regions; backward = per-level regions
+  int nlev = 1;
+  for (const Front& F : S.fronts) nlev = std::max(nlev, F.level + 1);
+  std::vector<int32_t> blf, bbase_f(nlev, 0), bbase_b(nlev, 0), cf4(nlev, 0), cf8(nlev, 0), cb4(nlev, 0), cb8(nlev, 0);
+  auto wpad = [](const std::vector<MItem>& v, int i) { return v[i].blk == kMWhole ? v[i].pad : 0; };
   for (int f = 0; f < nfr; ++f) {
-    if (dfwd[f] == 0)
-      for (int i = 0; i < fcnt_f[f]; ++i) qf[nq_f++] = fbase_f[f] + i;
-    if (dbwd[f] == 0)
+    if (dfwd[f] == 0) {
+      for (int i = 0; i < fcnt_f[f]; ++i) {
+        const int it = fbase_f[f] + i;
+        if (fcnt_f[f] == 1 && (wpad(fwd, it) & 1)) {
+          blf.push_back(it);
+          if (blf.size() % 8 == 0) qf[nq_f++] = -2 - (8 * static_cast<int>(blf.size() - 8) + 7);
+        } else {
+          qf[nq_f++] = it;
+        }
+      }
+    } else if (fcnt_f[f] == 1) {
+      const int pd = wpad(fwd, fbase_f[f]);
+      if (pd & 1) ++cf8[pd >> 8];
+      if (pd & 2) ++cf4[pd >> 8];
+    }
+    if (dbwd[f] == 0) {
       for (int i = 0; i < fcnt_b[f]; ++i) qb[nq_b++] = fbase_b[f] + i;
+    } else if (fcnt_b[f] == 1) {
+      const int pd = wpad(bwd, fbase_b[f]);
+      if (pd & 1) ++cb8[pd >> 8];
+      if (pd & 2) ++cb4[pd >> 8];
+    }
   }
+  if (blf.size() % 8) {
+    const int r = static_cast<int>(blf.size() % 8);
+    qf[nq_f++] = -2 - (8 * static_cast<int>(blf.size() - r) + r - 1);
+  }
+  int nbf = static_cast<int>(blf.size()), nbb = 0;
+  for (int L = 0; L < nlev; ++L) {
+    bbase_f[L] = nbf;
+    nbf += cf4[L];  // KR = 4 counts bound KR = 8 (bit 0 implies bit 1)
+    bbase_b[L] = nbb;
+    nbb += cb4[L];
+  }
+  blf.resize(std::max(1, nbf), -1);
+  std::vector<int32_t> blb(std::max(1, nbb), -1);
   P->n_fwd = static_cast<int>(fwd.size());
   P->n_bwd = static_cast<int>(bwd.size());
   if (fwd.empty()) fwd.push_back(MItem{});
@@ -859,6 +1185,19 @@ static void msolve_prepare(FactorEngine& fe) {
   meta.insert(meta.end(), fbase_b.begin(), fbase_b.end());
   meta.insert(meta.end(), fcnt_b.begin(), fcnt_b.end());
   meta.insert(meta.end(), npart.begin(), npart.end());
+  P->nlev = nlev;
+  P->mt_bb_f = static_cast<int64_t>(meta.size());
+  meta.insert(meta.end(), bbase_f.begin(), bbase_f.end());
+  P->mt_bb_b = static_cast<int64_t>(meta.size());
+  meta.insert(meta.end(), bbase_b.begin(), bbase_b.end());
+  P->mt_cf4 = static_cast<int64_t>(meta.size());
+  meta.insert(meta.end(), cf4.begin(), cf4.end());
+  P->mt_cf8 = static_cast<int64_t>(meta.size());
+  meta.insert(meta.end(), cf8.begin(), cf8.end());
+  P->mt_cb4 = static_cast<int64_t>(meta.size());
+  meta.insert(meta.end(), cb4.begin(), cb4.end());
+  P->mt_cb8 = static_cast<int64_t>(meta.size());
+  meta.insert(meta.end(), cb8.begin(), cb8.end());
   P->d_meta.upload(meta.data(), sizeof(int32_t) * meta.size(), fe.stream);
   P->d_ech.upload(ech.data(), sizeof(int32_t) * ech.size(), fe.stream);
   std::vector<int32_t> st;
@@ -874,6 +1213,12 @@ static void msolve_prepare(FactorEngine& fe) {
   st.insert(st.end(), {0, nq_f, 0, nq_b, 0, 0});  // {head, tail} fwd, bwd; items done fwd, bwd
   P->st_pub = static_cast<int64_t>(st.size());
   st.resize(st.size() + 3 * static_cast<size_t>(nfr), 0);  // published blocks fwd, bwd; bwd partials done
+  P->st_bl_f = static_cast<int64_t>(st.size());
+  st.insert(st.end(), blf.begin(), blf.end());
+  P->st_bl_b = static_cast<int64_t>(st.size());
+  st.insert(st.end(), blb.begin(), blb.end());
+  P->st_pc = static_cast<int64_t>(st.size());
+  st.resize(st.size() + 2 * static_cast<size_t>(nlev), 0);  // batch-list counters fwd, bwd
   P->d_state0.upload(st.data(), sizeof(int32_t) * st.size(), fe.stream);
   P->d_state.alloc(P->d_state0.bytes);
   P->d_stall.alloc(sizeof(int));
@@ -914,6 +1259,10 @@ static void msolve_launch(FactorEngine& fe, MArgs A, int grid) {
   F.pub = sb + P.st_pub;
   F.fbase = meta;
   F.fcnt = meta + nfr;
+  F.blist = sb + P.st_bl_f;
+  F.pcnt = sb + P.st_pc;
+  F.bbase = meta + P.mt_bb_f;
+  F.bcnt = meta + (KR == 4 ? P.mt_cf4 : P.mt_cf8);
   if (P.n_fwd > 0) mfwd_sweep<KR, kMinB><<<std::min(grid, P.n_fwd), kMT, msmem_bytes<KR>(), st>>>(F);
   MArgs B = A;
   if (A.trace) B.trace = A.trace + 2 * (size_t)P.n_fwd;
@@ -928,6 +1277,10 @@ static void msolve_launch(FactorEngine& fe, MArgs A, int grid) {
   B.fbase = meta + 2 * nfr;
   B.fcnt = meta + 3 * nfr;
   B.npart = meta + 4 * nfr;
+  B.blist = sb + P.st_bl_b;
+  B.pcnt = sb + P.st_pc + P.nlev;
+  B.bbase = meta + P.mt_bb_b;
+  B.bcnt = meta + (KR == 4 ? P.mt_cb4 : P.mt_cb8);
   B.bpart = P.d_bpart.as<double>();
   if (P.n_bwd > 0) mbwd_sweep<KR, kMinB><<<std::min(grid, P.n_bwd), kMT, msmem_bytes<KR>(), st>>>(B);
   RQB_CUDA(cudaGetLastError());
@@ -967,6 +1320,7 @@ void rqb_msolve_enqueue(FactorEngine& fe, const double* b, int64_t ldb, int nrhs
   A.sigma = sigma;
   A.xl = xl;
   A.nrhs = nrhs;
+  A.warp_items = !std::getenv("RQB_MWARP") || std::atoi(std::getenv("RQB_MWARP")) != 0;
   A.stall = P.d_stall.as<int>();
   unsigned long long* trace = nullptr;
   {
