@@ -659,6 +659,7 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
   d_ipiv.alloc(sizeof(int32_t) * n);
   d_scratch.alloc(sizeof(double) * std::max<int64_t>(1, nscratch) * 2 * kNB * kNB);
   d_flags.alloc(sizeof(int) * 4);
+  d_arrived.alloc(sizeof(int));
   d_y.alloc(sizeof(double) * n);
   d_xnew.alloc(sizeof(double) * n);
   d_cbvec.alloc(sizeof(double) * std::max<int64_t>(1, sym.cbvec));
@@ -714,6 +715,9 @@ FactorEngine::FactorEngine(const Symbolic& s, int64_t n_, const int64_t* rowptr,
 FactorEngine::~FactorEngine() {
   if (graph_factor_exec) cudaGraphExecDestroy(graph_factor_exec);
   if (graph_factor) cudaGraphDestroy(graph_factor);
+  if (stream_up) cudaStreamDestroy(stream_up);
+  if (ev_up) cudaEventDestroy(ev_up);
+  if (h_marks) cudaFreeHost(h_marks);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (stream) cudaStreamDestroy(stream);
@@ -830,16 +834,87 @@ void FactorEngine::enqueue_factor(KernelTimer* kt) {
   launches_factor = launches;
 }
 
+void FactorEngine::factor_streamed(const double* aval) {
+  static const bool off = std::getenv("RQB_STREAM_UPLOAD") && std::atoi(std::getenv("RQB_STREAM_UPLOAD")) == 0;
+  if (!(use_dag && dag_lazy) || off || nnz < (1 << 20)) {
+    set_values(aval);
+    factor();
+    return;
+  }
+  const int64_t kChunk = std::getenv("RQB_STREAM_CHUNK") ? std::atoll(std::getenv("RQB_STREAM_CHUNK")) : (1 << 21);  // values per chunk (16 MiB)
+  const int nch = static_cast<int>((nnz + kChunk - 1) / kChunk);
+  if (!stream_up) {
+    RQB_CUDA(cudaStreamCreateWithFlags(&stream_up, cudaStreamNonBlocking));
+    RQB_CUDA(cudaEventCreateWithFlags(&ev_up, cudaEventDisableTiming));
+  }
+  if (n_marks != nch) {
+    if (h_marks) cudaFreeHost(h_marks);
+    RQB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_marks), sizeof(int) * nch));
+    for (int c = 0; c < nch; ++c) h_marks[c] = static_cast<int>(std::min<int64_t>(nnz, (c + 1) * kChunk));
+    n_marks = nch;
+  }
+  if (!graph_factor_exec) {  // first use: capture with the values resident
+    set_values(aval);
+    factor();
+    return;
+  }
+  streaming = true;
+  try {
+    // everything enqueued so far (earlier solves read the factors, an earlier
+    // factorization reads d_aval) precedes the first chunk
+    RQB_CUDA(cudaMemsetAsync(d_arrived.p, 0, sizeof(int), stream));
+    RQB_CUDA(cudaEventRecord(ev0, stream));  // last_ms: upload + factorization
+    RQB_CUDA(cudaEventRecord(ev_up, stream));
+    RQB_CUDA(cudaStreamWaitEvent(stream_up, ev_up, 0));
+    // the graph first: its state-reset copies must not queue behind the chunks on a copy engine
+    launch_factor_graph();
+    for (int c = 0; c < nch; ++c) {
+      const int64_t o = c * kChunk, len = h_marks[c] - o;
+      RQB_CUDA(cudaMemcpyAsync(d_aval.as<double>() + o, aval + o, sizeof(double) * len, cudaMemcpyHostToDevice,
+                               stream_up));
+      RQB_CUDA(cudaMemcpyAsync(d_arrived.p, h_marks + c, sizeof(int), cudaMemcpyHostToDevice, stream_up));
+    }
+    static const bool dbg = std::getenv("RQB_STREAM_DEBUG") != nullptr;
+    if (dbg) {
+      cudaEvent_t e;
+      RQB_CUDA(cudaEventCreate(&e));
+      RQB_CUDA(cudaEventRecord(e, stream_up));
+      RQB_CUDA(cudaEventSynchronize(e));
+      float ms = 0;
+      RQB_CUDA(cudaEventElapsedTime(&ms, ev0, e));
+      std::fprintf(stderr, "[stream] upload of %d chunks done %.3f ms after the reset\n", nch, ms);
+      cudaEventDestroy(e);
+    }
+    RQB_CUDA(cudaStreamSynchronize(stream_up));
+  } catch (...) {
+    streaming = false;
+    cudaStreamSynchronize(stream_up);
+    cudaStreamSynchronize(stream);
+    throw;
+  }
+  streaming = false;
+  finish_factor();
+}
+
 void FactorEngine::factor() {
+  RQB_CUDA(cudaMemsetAsync(d_arrived.p, 0x7f, sizeof(int), stream));  // values resident
+  launch_factor_graph();
+  finish_factor();
+}
+
+void FactorEngine::launch_factor_graph() {
   if (!graph_factor_exec) {
     RQB_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     enqueue_factor();
     RQB_CUDA(cudaStreamEndCapture(stream, &graph_factor));
     RQB_CUDA(cudaGraphInstantiate(&graph_factor_exec, graph_factor, 0));
   }
-  RQB_CUDA(cudaEventRecord(ev0, stream));
+  if (!streaming) RQB_CUDA(cudaEventRecord(ev0, stream));
   RQB_CUDA(cudaGraphLaunch(graph_factor_exec, stream));
   RQB_CUDA(cudaEventRecord(ev1, stream));
+}
+
+void FactorEngine::finish_factor() {
   int flags[4];
   RQB_CUDA(cudaMemcpyAsync(flags, d_flags.p, sizeof(flags), cudaMemcpyDeviceToHost, stream));
   RQB_CUDA(cudaStreamSynchronize(stream));

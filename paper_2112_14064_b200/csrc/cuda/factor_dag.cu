@@ -137,8 +137,10 @@ struct DagArgs {
   // lazy assembly: the SMALL / ASM task that owns a pool region zeroes it and
   // writes the original entries that land there (no pool memset, no separate
   // scatter launch): entries ent_beg[t] .. ent_end[t] - 1 of task t
+  int keep_small;            // a SMALL parent runs in the CTA that completed its last child
   int lazy;
   const double* aval;        // Q(sigma) values (CSR order)
+  const int* arrived;        // leading CSR values present in aval (streamed upload; see scatter_entries)
   const int32_t* ent_src;    // CSR entry of each sorted position
   const int64_t* ent_dst;    // its pool offset
   const int32_t* ent_beg;
@@ -288,7 +290,7 @@ __device__ __forceinline__ void cp_async16z(double* smem, const double* gmem, in
 template <bool kGlobal>
 __device__ __forceinline__ void cross_update(const double* Lb, int ldl, const double* Ub, int ldu, int uoff,
                                              double* D, int64_t ldd, int doff, int r0, int r1, int c0,
-                                             int c1, int k0, int kw) {
+                                             int c1, int k0, int kw, bool rd = true) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   const int mt = (r1 - r0 + 15) / 16, nt = (c1 - c0 + 31) / 32;
@@ -305,7 +307,7 @@ __device__ __forceinline__ void cross_update(const double* Lb, int ldl, const do
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int r = rr + gid + (e >> 1) * 8, c = cc + y * 8 + 2 * tig + (e & 1);
-          cv[y][e] = (r < r1 && c < c1) ? __ldcg(&D[r + (int64_t)(c - doff) * ldd]) : 0.0;
+          cv[y][e] = (rd && r < r1 && c < c1) ? __ldcg(&D[r + (int64_t)(c - doff) * ldd]) : 0.0;
         }
     const int ra = rr + gid, rb = rr + gid + 8;
 #pragma unroll 4
@@ -336,7 +338,7 @@ __device__ __forceinline__ void cross_update(const double* Lb, int ldl, const do
 
 // Zero rows [r0, r1) x columns [c0, c1) of front F and write the original
 // entries task t owns (lazy assembly, see DagArgs::lazy). Ends with a barrier.
-__device__ void assemble_region(const DagArgs& A, const FrontDev& F, int t, int r0, int r1, int c0, int c1) {
+__device__ void zero_region(const DagArgs& A, const FrontDev& F, int r0, int r1, int c0, int c1) {
   double* g = A.pool + F.off;
   const int64_t ld = F.ld;
   const int nr = r1 - r0, nc = c1 - c0;
@@ -352,10 +354,42 @@ __device__ void assemble_region(const DagArgs& A, const FrontDev& F, int t, int 
       g[(r0 + r) + (int64_t)(c0 + c) * ld] = 0.0;
     }
   }
+}
+
+// Original entries of task t. When the values stream in from the host while
+// the kernel runs (FactorEngine::factor_streamed) thread 0 first waits until
+// the task's last CSR position has arrived: the entries of a task are sorted
+// by CSR position (stable sort by task), `arrived` counts the leading CSR
+// values uploaded so far (0x7f7f7f7f when the values are resident). The
+// values are read through L2 (the copy engine writes there; a line may also
+// hold a neighbour task's values that arrive later).
+__device__ void scatter_entries(const DagArgs& A, int t) {
+  const int e0 = A.ent_beg[t], e1 = A.ent_end[t];
+  if (threadIdx.x == 0 && e1 > e0) {
+    const int need = __ldg(&A.ent_src[e1 - 1]) + 1;
+    int got;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(got) : "l"(A.arrived) : "memory");
+    if (got < need) {
+      const unsigned long long t0 = gtimer();
+      for (;;) {
+        __nanosleep(256);
+        asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(got) : "l"(A.arrived) : "memory");
+        if (got >= need) break;
+        if (gtimer() - t0 > kStallNs || *((volatile int*)&A.flags[2])) {
+          atomicCAS(&A.flags[2], 0, 2);
+          break;
+        }
+      }
+    }
+  }
   __syncthreads();
-  const int e1 = A.ent_end[t];
-  for (int i = A.ent_beg[t] + threadIdx.x; i < e1; i += kDT) A.pool[__ldg(&A.ent_dst[i])] = __ldg(&A.aval[__ldg(&A.ent_src[i])]);
+  for (int i = e0 + threadIdx.x; i < e1; i += kDT) A.pool[__ldg(&A.ent_dst[i])] = __ldcg(&A.aval[__ldg(&A.ent_src[i])]);
   __syncthreads();
+}
+
+__device__ void assemble_region(const DagArgs& A, const FrontDev& F, int t, int r0, int r1, int c0, int c1) {
+  zero_region(A, F, r0, r1, c0, c1);
+  scatter_entries(A, t);
 }
 
 // SMALL front (nf <= 256 = one thread per row): the pivot "cross" lives in
@@ -549,7 +583,9 @@ __device__ void small_front(const DagArgs& A, const FrontDev& F, double* sm, int
   }
   phase(4);
   // contribution block: one K = npiv pass, operands from the cross
-  if (np < nf) cross_update<true>(Cb, ldc, Rb, ldr, np, g, ld, 0, np, nf, np, nf, 0, np);
+  // (a leaf's contribution block holds no original entries and was not
+  // zeroed, DagArgs::lazy == 2: written as -L21 U12 without the read)
+  if (np < nf) cross_update<true>(Cb, ldc, Rb, ldr, np, g, ld, 0, np, nf, np, nf, 0, np, !(A.lazy == 2 && F.nchild == 0));
   if (A.prof) __syncthreads();
   phase(5);
 }
@@ -1170,6 +1206,7 @@ __device__ __forceinline__ void release_tile(const DagArgs& A, const FrontDag& D
   }
 }
 
+constexpr int kNopTask = 0x7fffffff;
 __device__ int pop_task(const DagArgs& A) {
   const int h = atomicAdd(&A.qctl[0], 1);
   if (h >= A.nqueued) return -1;
@@ -1211,6 +1248,7 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     __syncthreads();
     const int t = task_s;
     if (t < 0) return;
+    if (t == kNopTask) continue;  // slot of a task its predecessor's CTA kept
     const Task T = A.tasks[t];
     const int f = T.front;
     const FrontDev F = A.fronts[f];
@@ -1226,7 +1264,13 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     switch (T.type) {
       case T_SMALL: {
         const long long ta = A.prof ? clock64() : 0;
-        if (A.lazy) assemble_region(A, F, t, 0, F.ld, 0, F.nf);
+        if (A.lazy == 2 && F.nchild == 0 && F.npiv < F.nf) {  // leaf: only the pivot cross is zeroed
+          zero_region(A, F, 0, F.ld, 0, F.npiv);
+          zero_region(A, F, 0, F.npiv, F.npiv, F.nf);
+          scatter_entries(A, t);
+        } else if (A.lazy) {
+          assemble_region(A, F, t, 0, F.ld, 0, F.nf);
+        }
         if (A.prof && tid == 0) atomicAdd(&A.prof[24], (unsigned long long)(clock64() - ta));
         small_front(A, F, sm, piv_sh);
       }
@@ -1372,7 +1416,23 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     if (done_s && D.parent >= 0) {
       const FrontDag PD = A.dag[D.parent];
       if (PD.tiles == 0) {
-        if (tid == 0) notify(A, PD.task_base);
+        // depth-first: the CTA that completes a SMALL parent's last child runs
+        // the parent next (one child's Schur block is still hot in L2, and
+        // when the values stream in the parents do not queue up behind leaves
+        // whose entries have not arrived). The parent's queue slot is filled
+        // with a no-op so the queue accounting (nqueued) stays exact.
+        if (tid == 0) {
+          if (A.keep_small) {
+            if (atomicSub(&A.deps[PD.task_base], 1) == 1) {
+              __threadfence();
+              const int slot = atomicAdd(&A.qctl[1], 1);
+              atomicExch(&A.queue[slot], kNopTask);
+              next_s = PD.task_base;
+            }
+          } else {
+            notify(A, PD.task_base);
+          }
+        }
       } else {
         for (int x = tid; x < PD.nasm; x += kDT) notify(A, PD.task_base + x);
       }
@@ -1422,6 +1482,14 @@ __global__ void ent_bounds_k(int64_t n, const int32_t* __restrict__ key, int32_t
     if (i == 0 || key[i - 1] != k) beg[k] = static_cast<int32_t>(i);
     if (i == n - 1 || key[i + 1] != k) end[k] = static_cast<int32_t>(i + 1);
   }
+}
+
+// per task: CSR values that must have arrived before its entries can be read
+// (its last entry's CSR position + 1; 0 without entries)
+__global__ void ent_need_k(int ntasks, const int32_t* __restrict__ beg, const int32_t* __restrict__ end,
+                           const int32_t* __restrict__ src, int32_t* __restrict__ need) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ntasks) need[t] = end[t] > beg[t] ? src[end[t] - 1] + 1 : 0;
 }
 
 __global__ void gather_i64_k(int64_t n, const int32_t* __restrict__ idx, const int64_t* __restrict__ src,
@@ -1679,7 +1747,7 @@ void rqb_dag_build(FactorEngine& fe) {
   // measured: cfg4_riga 26.8 -> 25.5 ms, cfg4_iga 61.3 -> 60.0 ms; the latency
   // variant keeps the pool memset + scatter (cfg2_riga 0.78 vs 0.81 ms lazy:
   // the zeroing sits on its critical path)
-  P->lazy = P->occ == 2 ? 1 : 0;
+  P->lazy = P->occ == 2 ? 2 : 0;  // 2: leaf SMALL fronts zero only their pivot cross (1: whole fronts)
   if (const char* e = std::getenv("RQB_LAZY_ZERO")) P->lazy = std::atoi(e);
   if (P->lazy && fe.nnz > 0) {
     const int64_t nnz = fe.nnz;
@@ -1722,6 +1790,25 @@ void rqb_dag_build(FactorEngine& fe) {
     gather_i64_k<<<blocks, 256, 0, fe.stream>>>(nnz, P->d_ent_src.as<int32_t>(), fe.d_qdst.as<int64_t>(),
                                                  P->d_ent_dst.as<int64_t>());
     RQB_CUDA(cudaGetLastError());
+    // initial ready tasks (the leaves' SMALL / ASM tasks) in the order their
+    // entries arrive when the values stream in from the host in CSR order
+    // (FactorEngine::factor_streamed): a CTA waiting for its task's entries
+    // then never holds back a task whose entries are already there
+    static const bool by_need = !(std::getenv("RQB_QUEUE_BY_NEED") && std::atoi(std::getenv("RQB_QUEUE_BY_NEED")) == 0);
+    if (by_need && P->nready > 1) {
+      DeviceBuffer d_need;
+      d_need.alloc(sizeof(int32_t) * P->ntasks);
+      ent_need_k<<<(P->ntasks + 255) / 256, 256, 0, fe.stream>>>(P->ntasks, P->d_ent_beg.as<int32_t>(),
+                                                                 P->d_ent_end.as<int32_t>(),
+                                                                 P->d_ent_src.as<int32_t>(), d_need.as<int32_t>());
+      RQB_CUDA(cudaGetLastError());
+      std::vector<int32_t> need(P->ntasks), q(P->nready);
+      RQB_CUDA(cudaMemcpyAsync(need.data(), d_need.p, sizeof(int32_t) * P->ntasks, cudaMemcpyDeviceToHost, fe.stream));
+      RQB_CUDA(cudaMemcpyAsync(q.data(), P->d_queue0.p, sizeof(int32_t) * P->nready, cudaMemcpyDeviceToHost, fe.stream));
+      RQB_CUDA(cudaStreamSynchronize(fe.stream));
+      std::stable_sort(q.begin(), q.end(), [&](int32_t a, int32_t b) { return need[a] < need[b]; });
+      RQB_CUDA(cudaMemcpyAsync(P->d_queue0.p, q.data(), sizeof(int32_t) * P->nready, cudaMemcpyHostToDevice, fe.stream));
+    }
     RQB_CUDA(cudaStreamSynchronize(fe.stream));  // the temporaries are freed on return
   }
   fe.dag_lazy = P->lazy != 0;
@@ -1806,7 +1893,9 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   A.upd_la = P.upd_la;
   A.ubase = P.d_ubase.as<int32_t>();
   A.lazy = P.lazy;
+  A.keep_small = std::getenv("RQB_KEEP_SMALL") ? std::atoi(std::getenv("RQB_KEEP_SMALL")) : 1;
   A.aval = fe.d_aval.as<double>();
+  A.arrived = fe.d_arrived.as<int>();
   A.ent_src = P.d_ent_src.as<int32_t>();
   A.ent_dst = P.d_ent_dst.as<int64_t>();
   A.ent_beg = P.d_ent_beg.as<int32_t>();

@@ -110,6 +110,11 @@ struct FactorEngine {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t stream_up = nullptr;  // streamed upload of the values (factor_streamed)
+  cudaEvent_t ev_up = nullptr;
+  DeviceBuffer d_arrived;            // int: leading CSR values present in d_aval
+  int* h_marks = nullptr;            // pinned: chunk end positions
+  int n_marks = 0;
   DeviceBuffer d_pool, d_aval, d_qdst, d_rows, d_fronts, d_inv, d_ipiv, d_lists, d_scratch, d_rel;
   std::vector<int32_t> rel_h;  // concatenated child -> parent row maps
   DeviceBuffer d_flags;   // [0] singular, [1] swaps
@@ -150,6 +155,14 @@ struct FactorEngine {
   // last_ms). Returns the singular flag.
   void factor();
   void set_values(const double* aval_host);
+  // set_values + factor with the upload overlapped: the values go up in CSR
+  // order in chunks on a second stream while the task-DAG kernel runs; a task
+  // waits until its own entries have arrived (lazy assembly only; otherwise
+  // upload, then factor)
+  void factor_streamed(const double* aval_host);
+  void launch_factor_graph();
+  void finish_factor();
+  bool streaming = false;
   void set_values_device(const double* aval_dev);
   // x = A^{-1} b on device vectors (original ordering), enqueued on `stream`.
   void solve_device(const double* b, double* x, double scale_out = 1.0);

@@ -395,8 +395,7 @@ int rq_factor_refactor(rq_factor_t* f, const double* aval) {
     need(aval, "aval");
     if (f->n_complex >= 0) rqb::fail(rqb::errc::config, "complex factorization: use rq_factor_refactor_complex");
     std::lock_guard<std::mutex> lock(f->fe->mu);
-    f->fe->set_values(aval);
-    f->fe->factor();
+    f->fe->factor_streamed(aval);  // the upload overlaps the factorization (chunks in CSR order)
   });
 }
 

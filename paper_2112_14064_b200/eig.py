@@ -171,7 +171,7 @@ class ShiftInvertOperator:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None and _lib.lib is not None:  # (interpreter shutdown)
             _lib.lib.rq_operator_destroy(h)
             self._h = None
 
@@ -283,7 +283,7 @@ class GeneralizedHermitianSolver:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None and _lib.lib is not None:  # (interpreter shutdown)
             _lib.lib.rq_gh_destroy(h)
             self._h = None
 

@@ -86,7 +86,7 @@ class DevicePencil(QuadraticPencil):
 
     def __del__(self):
         h = getattr(self, "_handle", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None and _lib.lib is not None:  # (interpreter shutdown)
             _lib.lib.rq_pencil_destroy(h)
             self._handle = None
 

@@ -54,7 +54,7 @@ class Ordering:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None and _lib.lib is not None:  # (interpreter shutdown)
             _lib.lib.rq_symbolic_destroy(h)
             self._h = None
 
@@ -141,7 +141,7 @@ class Factorization:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None and _lib.lib is not None:  # (interpreter shutdown)
             _lib.lib.rq_factor_destroy(h)
             self._h = None
 
