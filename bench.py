@@ -499,7 +499,7 @@ def run_b200(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(ws * flu / (e2e_ms * 1e6), 3), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * P.nnz, "d2h_bytes_per_step": 16,
-                "note": "rq_factor_refactor from pinned host Q(sigma) values: H2D + factor + D2H of flags",
+                "note": "rq_factor_refactor from pinned host Q(sigma) values: H2D (chunks streamed while the task-DAG kernel runs) + factor + D2H of flags",
                 "time_to_nev_ms_from_host": None if e2e_nev_ms is None else round(e2e_nev_ms, 3)},
         "gpu_launches": int(launches * args.steps),
         "clocks": clk.summary(),

@@ -841,8 +841,13 @@ void FactorEngine::factor_streamed(const double* aval) {
     factor();
     return;
   }
-  const int64_t kChunk = std::getenv("RQB_STREAM_CHUNK") ? std::atoll(std::getenv("RQB_STREAM_CHUNK")) : (1 << 21);  // values per chunk (16 MiB)
-  const int nch = static_cast<int>((nnz + kChunk - 1) / kChunk);
+  const int64_t kChunk = stream_chunk;
+  const int nch = static_cast<int>(chunk_order.size());
+  if (nch == 0) {
+    set_values(aval);
+    factor();
+    return;
+  }
   if (!stream_up) {
     RQB_CUDA(cudaStreamCreateWithFlags(&stream_up, cudaStreamNonBlocking));
     RQB_CUDA(cudaEventCreateWithFlags(&ev_up, cudaEventDisableTiming));
@@ -850,7 +855,7 @@ void FactorEngine::factor_streamed(const double* aval) {
   if (n_marks != nch) {
     if (h_marks) cudaFreeHost(h_marks);
     RQB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_marks), sizeof(int) * nch));
-    for (int c = 0; c < nch; ++c) h_marks[c] = static_cast<int>(std::min<int64_t>(nnz, (c + 1) * kChunk));
+    for (int c = 0; c < nch; ++c) h_marks[c] = c + 1;
     n_marks = nch;
   }
   if (!graph_factor_exec) {  // first use: capture with the values resident
@@ -869,7 +874,7 @@ void FactorEngine::factor_streamed(const double* aval) {
     // the graph first: its state-reset copies must not queue behind the chunks on a copy engine
     launch_factor_graph();
     for (int c = 0; c < nch; ++c) {
-      const int64_t o = c * kChunk, len = h_marks[c] - o;
+      const int64_t o = chunk_order[c] * kChunk, len = std::min<int64_t>(nnz, o + kChunk) - o;
       RQB_CUDA(cudaMemcpyAsync(d_aval.as<double>() + o, aval + o, sizeof(double) * len, cudaMemcpyHostToDevice,
                                stream_up));
       RQB_CUDA(cudaMemcpyAsync(d_arrived.p, h_marks + c, sizeof(int), cudaMemcpyHostToDevice, stream_up));

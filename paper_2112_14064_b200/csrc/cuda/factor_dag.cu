@@ -42,6 +42,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
 #include <string>
 
 #include <cub/cub.cuh>
@@ -140,7 +141,8 @@ struct DagArgs {
   int keep_small;            // a SMALL parent runs in the CTA that completed its last child
   int lazy;
   const double* aval;        // Q(sigma) values (CSR order)
-  const int* arrived;        // leading CSR values present in aval (streamed upload; see scatter_entries)
+  const int* arrived;        // chunks of the upload sequence present in aval (streamed upload; see scatter_entries)
+  const int32_t* ent_need;   // per task: chunks that must have arrived
   const int32_t* ent_src;    // CSR entry of each sorted position
   const int64_t* ent_dst;    // its pool offset
   const int32_t* ent_beg;
@@ -358,15 +360,15 @@ __device__ void zero_region(const DagArgs& A, const FrontDev& F, int r0, int r1,
 
 // Original entries of task t. When the values stream in from the host while
 // the kernel runs (FactorEngine::factor_streamed) thread 0 first waits until
-// the task's last CSR position has arrived: the entries of a task are sorted
-// by CSR position (stable sort by task), `arrived` counts the leading CSR
-// values uploaded so far (0x7f7f7f7f when the values are resident). The
+// the chunks holding the task's entries have arrived: ent_need[t] chunks of
+// the upload sequence, `arrived` counts the chunks uploaded so far
+// (0x7f7f7f7f when the values are resident). The
 // values are read through L2 (the copy engine writes there; a line may also
 // hold a neighbour task's values that arrive later).
 __device__ void scatter_entries(const DagArgs& A, int t) {
   const int e0 = A.ent_beg[t], e1 = A.ent_end[t];
   if (threadIdx.x == 0 && e1 > e0) {
-    const int need = __ldg(&A.ent_src[e1 - 1]) + 1;
+    const int need = __ldg(&A.ent_need[t]);
     int got;
     asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(got) : "l"(A.arrived) : "memory");
     if (got < need) {
@@ -1484,12 +1486,27 @@ __global__ void ent_bounds_k(int64_t n, const int32_t* __restrict__ key, int32_t
   }
 }
 
-// per task: CSR values that must have arrived before its entries can be read
-// (its last entry's CSR position + 1; 0 without entries)
-__global__ void ent_need_k(int ntasks, const int32_t* __restrict__ beg, const int32_t* __restrict__ end,
-                           const int32_t* __restrict__ src, int32_t* __restrict__ need) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < ntasks) need[t] = end[t] > beg[t] ? src[end[t] - 1] + 1 : 0;
+// Streamed upload plan (FactorEngine::factor_streamed). The CSR values go up
+// in chunks of `chunk` values; chunk_first_k: per chunk, the earliest position
+// in the initial ready queue among the tasks owning one of its entries (the
+// host sends the chunks in that order); ent_need_k: per task, how many chunks
+// of that sequence must have arrived before its entries can be read.
+__global__ void chunk_first_k(int64_t n, const int32_t* __restrict__ key, const int32_t* __restrict__ src,
+                              const int32_t* __restrict__ rank, int64_t chunk, int32_t* __restrict__ first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rank[key[i]];
+    const int c = static_cast<int>(src[i] / chunk);
+    if (r < first[c]) atomicMin(&first[c], r);
+  }
+}
+
+__global__ void ent_need_k(int64_t n, const int32_t* __restrict__ key, const int32_t* __restrict__ src,
+                           const int32_t* __restrict__ seq, int64_t chunk, int32_t* __restrict__ need) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = seq[src[i] / chunk] + 1;
+    int* p = &need[key[i]];
+    if (v > *p) atomicMax(p, v);
+  }
 }
 
 __global__ void gather_i64_k(int64_t n, const int32_t* __restrict__ idx, const int64_t* __restrict__ src,
@@ -1509,7 +1526,7 @@ struct DagPlan {
   int rc_group = 1;               // tiles per ROWS / COLS task
   DeviceBuffer d_ubase;
   int lazy = 0;                   // lazy assembly (DagArgs::lazy)
-  DeviceBuffer d_ent_src, d_ent_dst, d_ent_beg, d_ent_end;
+  DeviceBuffer d_ent_src, d_ent_dst, d_ent_beg, d_ent_end, d_ent_need;
   std::vector<FrontDag> dag_h;   // host copy of the per-front plan (tile counts, acb)
   size_t smem = 0;
   double flops_upd = 0;
@@ -1790,24 +1807,49 @@ void rqb_dag_build(FactorEngine& fe) {
     gather_i64_k<<<blocks, 256, 0, fe.stream>>>(nnz, P->d_ent_src.as<int32_t>(), fe.d_qdst.as<int64_t>(),
                                                  P->d_ent_dst.as<int64_t>());
     RQB_CUDA(cudaGetLastError());
+    // ---- streamed upload plan: chunk sequence, per-task needs, and the
     // initial ready tasks (the leaves' SMALL / ASM tasks) in the order their
-    // entries arrive when the values stream in from the host in CSR order
-    // (FactorEngine::factor_streamed): a CTA waiting for its task's entries
-    // then never holds back a task whose entries are already there
-    static const bool by_need = !(std::getenv("RQB_QUEUE_BY_NEED") && std::atoi(std::getenv("RQB_QUEUE_BY_NEED")) == 0);
-    if (by_need && P->nready > 1) {
-      DeviceBuffer d_need;
-      d_need.alloc(sizeof(int32_t) * P->ntasks);
-      ent_need_k<<<(P->ntasks + 255) / 256, 256, 0, fe.stream>>>(P->ntasks, P->d_ent_beg.as<int32_t>(),
-                                                                 P->d_ent_end.as<int32_t>(),
-                                                                 P->d_ent_src.as<int32_t>(), d_need.as<int32_t>());
-      RQB_CUDA(cudaGetLastError());
-      std::vector<int32_t> need(P->ntasks), q(P->nready);
-      RQB_CUDA(cudaMemcpyAsync(need.data(), d_need.p, sizeof(int32_t) * P->ntasks, cudaMemcpyDeviceToHost, fe.stream));
+    // entries arrive, so a CTA waiting for its task's entries never holds
+    // back a task whose entries are already there
+    {
+      if (const char* e = std::getenv("RQB_STREAM_CHUNK")) fe.stream_chunk = std::max<int64_t>(1 << 16, std::atoll(e));
+      const int64_t chunk = fe.stream_chunk;
+      const int nch = static_cast<int>((nnz + chunk - 1) / chunk);
+      std::vector<int32_t> q(P->nready), rank(P->ntasks, 0x7fffffff);
       RQB_CUDA(cudaMemcpyAsync(q.data(), P->d_queue0.p, sizeof(int32_t) * P->nready, cudaMemcpyDeviceToHost, fe.stream));
       RQB_CUDA(cudaStreamSynchronize(fe.stream));
-      std::stable_sort(q.begin(), q.end(), [&](int32_t a, int32_t b) { return need[a] < need[b]; });
-      RQB_CUDA(cudaMemcpyAsync(P->d_queue0.p, q.data(), sizeof(int32_t) * P->nready, cudaMemcpyHostToDevice, fe.stream));
+      for (int i = 0; i < P->nready; ++i) rank[q[i]] = i;
+      DeviceBuffer d_rank, d_first, d_seq;
+      d_rank.upload(rank.data(), sizeof(int32_t) * rank.size(), fe.stream);
+      d_first.alloc(sizeof(int32_t) * nch);
+      RQB_CUDA(cudaMemsetAsync(d_first.p, 0x7f, sizeof(int32_t) * nch, fe.stream));
+      chunk_first_k<<<blocks, 256, 0, fe.stream>>>(nnz, k1.as<int32_t>(), P->d_ent_src.as<int32_t>(),
+                                                    d_rank.as<int32_t>(), chunk, d_first.as<int32_t>());
+      RQB_CUDA(cudaGetLastError());
+      std::vector<int32_t> first(nch), seq(nch);
+      RQB_CUDA(cudaMemcpyAsync(first.data(), d_first.p, sizeof(int32_t) * nch, cudaMemcpyDeviceToHost, fe.stream));
+      RQB_CUDA(cudaStreamSynchronize(fe.stream));
+      fe.chunk_order.resize(nch);
+      std::iota(fe.chunk_order.begin(), fe.chunk_order.end(), 0);
+      static const bool csr_order = std::getenv("RQB_STREAM_ORDER") && std::atoi(std::getenv("RQB_STREAM_ORDER")) == 0;
+      if (!csr_order)
+        std::stable_sort(fe.chunk_order.begin(), fe.chunk_order.end(),
+                         [&](int32_t a, int32_t b) { return first[a] < first[b]; });
+      for (int i = 0; i < nch; ++i) seq[fe.chunk_order[i]] = i;
+      d_seq.upload(seq.data(), sizeof(int32_t) * nch, fe.stream);
+      P->d_ent_need.alloc(sizeof(int32_t) * P->ntasks);
+      RQB_CUDA(cudaMemsetAsync(P->d_ent_need.p, 0, sizeof(int32_t) * P->ntasks, fe.stream));
+      ent_need_k<<<blocks, 256, 0, fe.stream>>>(nnz, k1.as<int32_t>(), P->d_ent_src.as<int32_t>(),
+                                                 d_seq.as<int32_t>(), chunk, P->d_ent_need.as<int32_t>());
+      RQB_CUDA(cudaGetLastError());
+      std::vector<int32_t> need(P->ntasks);
+      RQB_CUDA(cudaMemcpyAsync(need.data(), P->d_ent_need.p, sizeof(int32_t) * P->ntasks, cudaMemcpyDeviceToHost, fe.stream));
+      RQB_CUDA(cudaStreamSynchronize(fe.stream));
+      if (P->nready > 1) {
+        std::stable_sort(q.begin(), q.end(), [&](int32_t a, int32_t b) { return need[a] < need[b]; });
+        RQB_CUDA(cudaMemcpyAsync(P->d_queue0.p, q.data(), sizeof(int32_t) * P->nready, cudaMemcpyHostToDevice, fe.stream));
+        RQB_CUDA(cudaStreamSynchronize(fe.stream));
+      }
     }
     RQB_CUDA(cudaStreamSynchronize(fe.stream));  // the temporaries are freed on return
   }
@@ -1896,6 +1938,7 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   A.keep_small = std::getenv("RQB_KEEP_SMALL") ? std::atoi(std::getenv("RQB_KEEP_SMALL")) : 1;
   A.aval = fe.d_aval.as<double>();
   A.arrived = fe.d_arrived.as<int>();
+  A.ent_need = P.d_ent_need.as<int32_t>();
   A.ent_src = P.d_ent_src.as<int32_t>();
   A.ent_dst = P.d_ent_dst.as<int64_t>();
   A.ent_beg = P.d_ent_beg.as<int32_t>();

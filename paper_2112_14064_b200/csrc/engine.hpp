@@ -112,9 +112,11 @@ struct FactorEngine {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t stream_up = nullptr;  // streamed upload of the values (factor_streamed)
   cudaEvent_t ev_up = nullptr;
-  DeviceBuffer d_arrived;            // int: leading CSR values present in d_aval
-  int* h_marks = nullptr;            // pinned: chunk end positions
+  DeviceBuffer d_arrived;            // int: chunks of the upload sequence present in d_aval
+  int* h_marks = nullptr;            // pinned: 1, 2, ... (the arrival counter's values)
   int n_marks = 0;
+  int64_t stream_chunk = 1 << 21;    // values per chunk (16 MiB)
+  std::vector<int32_t> chunk_order;  // upload sequence (rqb_dag_build: by the first task needing each chunk)
   DeviceBuffer d_pool, d_aval, d_qdst, d_rows, d_fronts, d_inv, d_ipiv, d_lists, d_scratch, d_rel;
   std::vector<int32_t> rel_h;  // concatenated child -> parent row maps
   DeviceBuffer d_flags;   // [0] singular, [1] swaps

@@ -275,3 +275,30 @@ def test_nondegenerate_spectrum_cfg2_riga_vs_oracle():
     lo, ro = E.solve_quadratic(20, tol=1e-10, max_restarts=400)
     assert np.max(ro) <= 1e-10
     assert np.max(np.abs(lam - sorted_lams(lo)) / np.abs(lo)) <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["cfg3_riga", "cfg3_iga"])
+def test_streamed_refactor_matches_resident_factor(name):
+    """rq_factor_refactor uploads the values in chunks while the task-DAG kernel
+    runs (tasks wait for their own entries; FactorEngine::factor_streamed): the
+    factors must be those of a factorization with the values resident (the
+    first factorization of a handle, and lu_factorize on the new values)."""
+    P = rq.baseline_config(name)
+    assert P.nnz >= 1 << 20  # below that the refactor uploads first
+    o = rq.nested_dissection_order(P)
+    Q = P.q_values(-0.5)
+    b = np.random.default_rng(7).uniform(-1.0, 1.0, P.n)
+    f = rq.lu_factorize((P.rowptr, P.col, Q), o)  # values resident
+    x0 = f.solve(b)
+    for _ in range(3):
+        f.refactor(Q)  # streamed
+        assert np.array_equal(f.solve(b), x0)
+    Q2 = P.q_values(-0.7)
+    f.refactor(Q2)  # streamed, new values
+    x2 = f.solve(b)
+    g = rq.lu_factorize((P.rowptr, P.col, Q2), o)
+    assert np.array_equal(g.solve(b), x2)
+    import scipy.sparse as sp
+    A = sp.csr_matrix((Q2, P.col, P.rowptr), shape=(P.n, P.n))
+    nA = abs(A).sum(0).max()
+    assert np.linalg.norm(A @ x2 - b, 1) / (nA * np.linalg.norm(x2, 1) + np.linalg.norm(b, 1)) <= 1e-14
