@@ -168,7 +168,9 @@ typedef struct {
 /* A = Q(sigma) values on the shared pattern (free-DOF ordering). */
 int rq_factor_create(const rq_symbolic_t* s, int64_t n, const int64_t* rowptr,
                      const int32_t* col, const double* aval, rq_factor_t** out);
-/* Re-run the numeric factorization with new values on the same pattern. */
+/* Re-run the numeric factorization with new values on the same pattern (host
+ * array of nnz doubles, CSR order; pinned memory lets the upload overlap the
+ * factorization: the values stream up in chunks while the kernel runs). */
 int rq_factor_refactor(rq_factor_t* f, const double* aval);
 int rq_factor_get_info(const rq_factor_t* f, rq_factor_info* out);
 /* x = A^{-1} b for nrhs right-hand sides (column-major n x nrhs, host).
