@@ -397,16 +397,23 @@ def run_b200(args):
     del fac
     # time to nev from host arrays: operator creation (H2D of K, C, M, Q, factor) + eigensolve
     e2e_nev_ms = None
+    e2e_nev_all = None
     if single:
-        PH = rq.QuadraticPencil(**{k: getattr(P, k) for k in (
-            "kind", "degree", "elems", "levels", "n_full", "n", "rowptr", "col", "K", "C", "M", "box",
-            "free_to_full")})
-        t0 = time.perf_counter()
-        op2 = rq.build_operator(PH, SIGMA, o)
-        op2.solve_quadratic(nev, eps=1e-10, seed=0, max_restarts=args.max_restarts, raise_partial=False,
-                            block=max(1, args.block))
-        e2e_nev_ms = (time.perf_counter() - t0) * 1e3
-        del op2
+        # a fresh operator from host arrays every repetition (upload of K, C, M and the
+        # pattern, scaling, Q(sigma), factorization, workspace + graphs, eigensolve); the
+        # repetitions differ by host noise only (cold allocations), the minimum is reported
+        e2e_nev_all = []
+        for _ in range(3):
+            PH = rq.QuadraticPencil(**{k: getattr(P, k) for k in (
+                "kind", "degree", "elems", "levels", "n_full", "n", "rowptr", "col", "K", "C", "M", "box",
+                "free_to_full")})
+            t0 = time.perf_counter()
+            op2 = rq.build_operator(PH, SIGMA, o)
+            op2.solve_quadratic(nev, eps=1e-10, seed=0, max_restarts=args.max_restarts, raise_partial=False,
+                                block=max(1, args.block))
+            e2e_nev_all.append(round((time.perf_counter() - t0) * 1e3, 3))
+            del op2
+        e2e_nev_ms = min(e2e_nev_all)
 
     # ---- CPU baseline (rank 0, N = 1 only): the oracle on the host cores
     cpu = None
@@ -500,7 +507,11 @@ def run_b200(args):
         "e2e": {"value": round(ws * flu / (e2e_ms * 1e6), 3), "unit": "GFLOP/s",
                 "h2d_bytes_per_step": 8 * P.nnz, "d2h_bytes_per_step": 16,
                 "note": "rq_factor_refactor from pinned host Q(sigma) values: H2D (chunks streamed while the task-DAG kernel runs) + factor + D2H of flags",
-                "time_to_nev_ms_from_host": None if e2e_nev_ms is None else round(e2e_nev_ms, 3)},
+                "time_to_nev_ms_from_host": None if e2e_nev_ms is None else round(e2e_nev_ms, 3),
+                "time_to_nev_ms_from_host_all": e2e_nev_all,
+                "time_to_nev_from_host_note": "fresh operator from pageable host arrays (K, C, M, pattern staged up "
+                                              "through pinned buffers), factor, workspace + graphs, block "
+                                              "Krylov-Schur seed 0; minimum of the repetitions listed"},
         "gpu_launches": int(launches * args.steps),
         "clocks": clk.summary(),
     }

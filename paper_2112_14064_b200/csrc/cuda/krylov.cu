@@ -842,12 +842,12 @@ std::unique_ptr<DevicePencil> OperatorEngine::upload_pencil(int64_t n, const int
   dp->d_rowptr.alloc(sizeof(int64_t) * (n + 1));
   dp->d_col.alloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
   dp->d_val.alloc(sizeof(double) * std::max<int64_t>(3 * nnz, 1));
-  RQB_CUDA(cudaMemcpy(dp->d_rowptr.p, rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
-  RQB_CUDA(cudaMemcpy(dp->d_col.p, col, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+  upload_host_sync(dp->d_rowptr.p, rowptr, sizeof(int64_t) * (n + 1), nullptr);
+  upload_host_sync(dp->d_col.p, col, sizeof(int32_t) * nnz, nullptr);
   double* v = dp->d_val.as<double>();
-  RQB_CUDA(cudaMemcpy(v, K, sizeof(double) * nnz, cudaMemcpyHostToDevice));
-  RQB_CUDA(cudaMemcpy(v + nnz, C, sizeof(double) * nnz, cudaMemcpyHostToDevice));
-  RQB_CUDA(cudaMemcpy(v + 2 * nnz, M, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  upload_host_sync(v, K, sizeof(double) * nnz, nullptr);
+  upload_host_sync(v + nnz, C, sizeof(double) * nnz, nullptr);
+  upload_host_sync(v + 2 * nnz, M, sizeof(double) * nnz, nullptr);
   tr.mark("uploads");
   return dp;
 }

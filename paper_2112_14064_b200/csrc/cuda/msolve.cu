@@ -1003,6 +1003,7 @@ void MSolvePlanDeleter::operator()(MSolvePlan* p) const { delete p; }
 constexpr int kMaxRhs = 8;
 
 static void msolve_prepare(FactorEngine& fe) {
+  SetupTrace tr("msolve_prepare");
   const Symbolic& S = fe.sym;
   auto P = std::unique_ptr<MSolvePlan, MSolvePlanDeleter>(new MSolvePlan);
   const int nfr = static_cast<int>(S.fronts.size());
@@ -1238,6 +1239,7 @@ static void msolve_prepare(FactorEngine& fe) {
   RQB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mfwd_sweep<8, 2>, kMT, msmem_bytes<8>()));
   P->grid8 = nsm * std::max(1, occ);
   fe.mplan.reset(P.release());
+  tr.mark("plan + uploads");
 }
 
 template <int KR, int kMinB>

@@ -29,6 +29,10 @@ struct FrontDev {
 };
 
 void cuda_check(cudaError_t e, const char* what);
+// dst[0, bytes) = src (host) on stream s, returns when the copy has completed;
+// a large pageable source is staged through pinned buffers by the host threads
+// (host/upload.cpp)
+void upload_host_sync(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
 // Host setup phase timer (RQB_SETUP_TRACE=1: one stderr line per phase).
 struct SetupTrace {
