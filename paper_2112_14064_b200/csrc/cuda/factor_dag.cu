@@ -143,6 +143,8 @@ struct DagArgs {
   const double* aval;        // Q(sigma) values (CSR order)
   const int* arrived;        // chunks of the upload sequence present in aval (streamed upload; see scatter_entries)
   const int32_t* ent_need;   // per task: chunks that must have arrived
+  const int32_t* init_list;  // fed initial tasks (see the feeder in factor_dag_kernel); nullptr: all queued at the start
+  int ninit;
   const int32_t* ent_src;    // CSR entry of each sorted position
   const int64_t* ent_dst;    // its pool offset
   const int32_t* ent_beg;
@@ -1256,6 +1258,17 @@ __global__ void __launch_bounds__(kDT, kMinBlocks) factor_dag_kernel(DagArgs A) 
     const FrontDev F = A.fronts[f];
     const FrontDag D = A.dag[f];
     int* cnt = A.cnt + kCnt * f;
+    // feeder: only the first kInitWindow initial tasks (the leaves' SMALL / ASM
+    // tasks) start in the ready queue; every one popped pushes the next of the
+    // list, so tasks released during the run never queue up behind thousands
+    // of leaves (whose entries may not have arrived yet when the values stream in)
+    if (tid == 0 && A.init_list && (T.type == T_SMALL || T.type == T_ASM) && F.nchild == 0) {
+      const int i = atomicAdd(&A.qctl[2], 1);
+      if (i < A.ninit) {
+        const int slot = atomicAdd(&A.qctl[1], 1);
+        atomicExch(&A.queue[slot], __ldg(&A.init_list[i]));
+      }
+    }
     const long long t_work = A.prof ? clock64() : 0;
     if (A.trace && tid == 0) {
       unsigned long long gt;
@@ -1526,7 +1539,8 @@ struct DagPlan {
   int rc_group = 1;               // tiles per ROWS / COLS task
   DeviceBuffer d_ubase;
   int lazy = 0;                   // lazy assembly (DagArgs::lazy)
-  DeviceBuffer d_ent_src, d_ent_dst, d_ent_beg, d_ent_end, d_ent_need;
+  DeviceBuffer d_ent_src, d_ent_dst, d_ent_beg, d_ent_end, d_ent_need, d_init;
+  int ninit = 0;  // initial tasks fed during the run (0: all in the queue at the start)
   std::vector<FrontDag> dag_h;   // host copy of the per-front plan (tile counts, acb)
   size_t smem = 0;
   double flops_upd = 0;
@@ -1847,7 +1861,22 @@ void rqb_dag_build(FactorEngine& fe) {
       RQB_CUDA(cudaStreamSynchronize(fe.stream));
       if (P->nready > 1) {
         std::stable_sort(q.begin(), q.end(), [&](int32_t a, int32_t b) { return need[a] < need[b]; });
-        RQB_CUDA(cudaMemcpyAsync(P->d_queue0.p, q.data(), sizeof(int32_t) * P->nready, cudaMemcpyHostToDevice, fe.stream));
+        // feeder (see factor_dag_kernel): the initial tasks must be exactly the SMALL / ASM tasks of
+        // the childless fronts, which is how the kernel recognises them
+        const int kInitWindow = std::getenv("RQB_FEED_WINDOW") ? std::max(64, std::atoi(std::getenv("RQB_FEED_WINDOW"))) : 320;  // measured (e2e refactor, ms): 320 / 600 / 1024 / 2048 / 4096: cfg4_riga 26.6 / 26.7 / 26.9 / 27.3 / 27.3, cfg4_iga 60.7 / 61.0 / 61.4 / 62.7 / 63.7
+        static const bool feed = !(std::getenv("RQB_FEED_INIT") && std::atoi(std::getenv("RQB_FEED_INIT")) == 0);
+        int nleaf_tasks = 0;
+        for (size_t t = 0; t < tasks.size(); ++t)
+          nleaf_tasks += (tasks[t].type == T_SMALL || tasks[t].type == T_ASM) && S.fronts[tasks[t].front].children.empty();
+        std::vector<int32_t> q0v(q);
+        if (feed && P->nready > kInitWindow && nleaf_tasks == P->nready) {
+          P->ninit = P->nready;
+          P->d_init.upload(q.data(), sizeof(int32_t) * P->nready, fe.stream);
+          std::fill(q0v.begin() + kInitWindow, q0v.end(), -1);
+          const int qc[4] = {0, kInitWindow, kInitWindow, 0};
+          RQB_CUDA(cudaMemcpyAsync(P->d_qctl0.p, qc, sizeof(qc), cudaMemcpyHostToDevice, fe.stream));
+        }
+        RQB_CUDA(cudaMemcpyAsync(P->d_queue0.p, q0v.data(), sizeof(int32_t) * P->nready, cudaMemcpyHostToDevice, fe.stream));
         RQB_CUDA(cudaStreamSynchronize(fe.stream));
       }
     }
@@ -1939,6 +1968,8 @@ void rqb_dag_enqueue(FactorEngine& fe) {
   A.aval = fe.d_aval.as<double>();
   A.arrived = fe.d_arrived.as<int>();
   A.ent_need = P.d_ent_need.as<int32_t>();
+  A.init_list = P.ninit > 0 ? P.d_init.as<int32_t>() : nullptr;
+  A.ninit = P.ninit;
   A.ent_src = P.d_ent_src.as<int32_t>();
   A.ent_dst = P.d_ent_dst.as<int64_t>();
   A.ent_beg = P.d_ent_beg.as<int32_t>();
