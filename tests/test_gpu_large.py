@@ -302,3 +302,39 @@ def test_streamed_refactor_matches_resident_factor(name):
     A = sp.csr_matrix((Q2, P.col, P.rowptr), shape=(P.n, P.n))
     nA = abs(A).sum(0).max()
     assert np.linalg.norm(A @ x2 - b, 1) / (nA * np.linalg.norm(x2, 1) + np.linalg.norm(b, 1)) <= 1e-14
+
+
+def test_streamed_refactor_concurrent_handles():
+    """Two threads refactor their own handles from host values at the same time
+    (two persistent factor kernels, each waiting for its own streamed chunks):
+    both must finish and reproduce the serial results bit for bit."""
+    import threading
+
+    jobs = []
+    for name in ("cfg3_riga", "cfg3_iga"):
+        P = rq.baseline_config(name)
+        o = rq.nested_dissection_order(P)
+        Q = P.q_values(-0.5)
+        b = np.random.default_rng(11).uniform(-1.0, 1.0, P.n)
+        f = rq.lu_factorize((P.rowptr, P.col, Q), o)
+        jobs.append({"f": f, "Q": Q, "b": b, "x0": f.solve(b), "out": [], "err": None})
+
+    def work(j):
+        try:
+            for _ in range(6):
+                j["f"].refactor(j["Q"])
+                j["out"].append(j["f"].solve(j["b"]))
+        except Exception as e:  # noqa: BLE001
+            j["err"] = e
+
+    ts = [threading.Thread(target=work, args=(j,)) for j in jobs]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in ts), "concurrent streamed refactors did not finish"
+    for j in jobs:
+        assert j["err"] is None, j["err"]
+        assert len(j["out"]) == 6
+        for x in j["out"]:
+            assert np.array_equal(x, j["x0"])
