@@ -398,10 +398,17 @@ def run_b200(args):
     # time to nev from host arrays: operator creation (H2D of K, C, M, Q, factor) + eigensolve
     e2e_nev_ms = None
     e2e_nev_all = None
+    e2e_seed = None
     if single:
         # a fresh operator from host arrays every repetition (upload of K, C, M and the
         # pattern, scaling, Q(sigma), factorization, workspace + graphs, eigensolve); the
         # repetitions differ by host noise only (cold allocations), the minimum is reported
+        # start vector: the seed whose device-resident block solve above is the median one (the
+        # headline time_to_nev_ms), so the from-host number differs from it by the host path only
+        e2e_seed = 0
+        if t_nev_b:
+            order_b = sorted(range(1, len(seeds)), key=lambda i: t_nev_b[i])
+            e2e_seed = seeds[order_b[len(order_b) // 2]]
         e2e_nev_all = []
         for _ in range(3):
             PH = rq.QuadraticPencil(**{k: getattr(P, k) for k in (
@@ -409,7 +416,7 @@ def run_b200(args):
                 "free_to_full")})
             t0 = time.perf_counter()
             op2 = rq.build_operator(PH, SIGMA, o)
-            op2.solve_quadratic(nev, eps=1e-10, seed=0, max_restarts=args.max_restarts, raise_partial=False,
+            op2.solve_quadratic(nev, eps=1e-10, seed=e2e_seed, max_restarts=args.max_restarts, raise_partial=False,
                                 block=max(1, args.block))
             e2e_nev_all.append(round((time.perf_counter() - t0) * 1e3, 3))
             del op2
@@ -511,7 +518,9 @@ def run_b200(args):
                 "time_to_nev_ms_from_host_all": e2e_nev_all,
                 "time_to_nev_from_host_note": "fresh operator from pageable host arrays (K, C, M, pattern staged up "
                                               "through pinned buffers), factor, workspace + graphs, block "
-                                              "Krylov-Schur seed 0; minimum of the repetitions listed"},
+                                              "Krylov-Schur from the median seed of time_to_nev_block "
+                                              f"(seed {e2e_seed}); minimum of the "
+                                              "repetitions listed"},
         "gpu_launches": int(launches * args.steps),
         "clocks": clk.summary(),
     }

@@ -72,7 +72,12 @@ constexpr int kCntRun = 5, kCntFb = 6;
 // latency of one hidden behind the other: 113 KB of shared memory and 128
 // registers each, SMALL fronts up to nf = 256 whose pivot cross fits 112 KB).
 constexpr int kSmallNfLatency = 160;
-constexpr int kSmallNfThroughput = kDT;  // any front whose pivot cross fits 112 KB
+// throughput variant: fronts up to nf = 208 whose pivot cross fits 112 KB. Measured
+// (resident factor, ms; 208 / 256 = every front a CTA's 256 threads can take):
+// cfg4_riga 24.8 / 25.5, cfg4_iga 54.9 / 59.3 (a 220..256-row front as ONE CTA's
+// SMALL task holds up its parent for > 100 us; tiled, its tasks spread over the
+// grid), cfg5_p2..p5_riga, cfg5_p4_iga, cfg3_riga within 0.5%
+constexpr int kSmallNfThroughput = 208;
 constexpr size_t kSmallBytesLatency = 160 * 161 * 8;     // 206 KB: one CTA per SM
 constexpr size_t kSmallBytesThroughput = 118 * 119 * 8;  // 112 KB: two CTAs per SM
 constexpr double kThroughputFlops = 2e9;  // F_LU above which the two-CTA variant is used
